@@ -1,0 +1,175 @@
+/*
+ * rbicg.h -- C ABI of the B200-native recycling BiCG (RBiCG) hot path.
+ *
+ * Method: Ahuja, de Sturler, Gugercin, Chang, "Recycling BiCG" (arXiv
+ * 1010.0762); citations "P:n" are lines of that paper's PAPER.md.
+ *
+ *   * Problem: a sequence of dual systems A x = b, A^* x~ = b~.
+ *   * Iteration: Algorithm 2 with the augmented bi-Lanczos
+ *     relations and the oblique projections against C, C~.
+ *   * Recycle space: harmonic Ritz vectors, first-system cases
+ *     (P:614-684), bi-orthogonal C, C~ by SVD.
+ *   * Bilinear form u^*A^{-1}w.
+ *
+ * Conventions shared by every entry point
+ *   - Scalars: RBICG_F64 = IEEE double; RBICG_C128 = interleaved (re, im)
+ *     doubles.  Inner product (u, v) = u^* v (reading Q1).
+ *   - Vectors are contiguous arrays of n scalars.  n x k blocks (U, Ũ) are
+ *     COLUMN-major with leading dimension n in this ABI (the library keeps its
+ *     own row-major device copies).
+ *   - Pointers are host or device memory according to the `on_device` flag of
+ *     the call (device pointers must be from the ctx's device).  The caller
+ *     owns every array it passes; the library reads/writes them on the ctx
+ *     stream and every call returns only once its outputs are host-visible
+ *     (the call synchronises the ctx stream before returning).
+ *   - Handles (ctx, mat, rec) are owned by the library until the matching
+ *     *_free / rbicg_finalize.  One ctx per host thread.
+ *   - Errors: no exception crosses the ABI.  Return value 0 = success,
+ *     > 0 = numerical outcome with valid outputs, < 0 = error (outputs
+ *     undefined, recycle state unchanged where possible).  rbicg_strerror()
+ *     gives a static message.
+ *   - Every step of the solve runs in this library's sm_100a kernels; the only
+ *     host arithmetic is the small dense cycle-end control work (the
+ *     generalised eigenproblem of order k+s and the k x k SVD, LAPACK via
+ *     dlopen of the OpenBLAS shipped with scipy; path from $RBICG_LAPACK).
+ */
+#ifndef RBICG_H
+#define RBICG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  RBICG_OK = 0,
+  RBICG_MAXITER = 1,            /* max_itn reached; outputs = last iterate   */
+  RBICG_BREAKDOWN_SERIOUS = 2,  /* (r~_i, r_i) = 0                    */
+  RBICG_BREAKDOWN_SECOND = 3,   /* (p~_i, q_i) = 0                */
+  RBICG_RECYCLE_EMPTY = 4,      /* p = 0 after truncation (P:702 footnote);  */
+                                /* solve valid, returned basis has k = 0     */
+  RBICG_EINVAL = -1,
+  RBICG_ENOMEM = -2,
+  RBICG_ECUDA = -3,
+  RBICG_ENCCL = -4,
+  RBICG_ELAPACK = -5,
+  RBICG_ESTATE = -6
+};
+
+typedef enum { RBICG_F64 = 0, RBICG_C128 = 1 } rbicg_dtype;
+
+typedef struct rbicg_ctx rbicg_ctx;
+typedef struct rbicg_mat rbicg_mat;
+typedef struct rbicg_rec rbicg_rec;
+
+/* Multi-GPU row partition (one process per GPU).  NULL = single GPU.
+ * Round 1: only nranks == 1 is accepted (RBICG_EINVAL otherwise). */
+typedef struct {
+  int32_t rank, nranks;
+  uint8_t nccl_id[128];
+  int64_t row_begin, row_end;
+} rbicg_dist;
+
+typedef struct {
+  int32_t k;              /* recycle width (0 = plain BiCG, Algorithm 1)      */
+  int32_t s;              /* cycle length, >= 2                        */
+  int32_t max_itn;        /* iteration cap                             */
+  double tol;             /* relative: ||r|| <= tol ||b|| and ||r~|| <= tol ||b~|| (Q2) */
+  double trunc_tol;       /* keep sigma_i >= trunc_tol of the column-normalised
+                             Gram C~^*C (reading Q13)                   */
+  uint64_t seed;          /* unused by the library (random draws are inputs)  */
+  int32_t update_recycle; /* build U_j, Ũ_j at cycle ends (§4)                 */
+  int32_t record_history; /* fill `hist` when non-NULL                         */
+  int32_t force_iters;    /* > 0: run exactly this many iterations, stop test
+                             off (parity protocol Q27); 0 = normal            */
+  int32_t reserved;
+} rbicg_opts;
+
+typedef struct {
+  int32_t status, iterations, cycles, k_in, k_out;
+  double relres_rec, relres_dual_rec;    /* recursive ||r||/||b||, ||r~||/||b~|| */
+  double relres_true, relres_dual_true;  /* after step 7            */
+  double t_loop_ms, t_cycle_dev_ms, t_host_eig_ms, t_refresh_ms, t_total_ms;
+  double alg_bytes;                       /* algorithmic HBM bytes of the loop */
+  int32_t kernel_launches;                /* kernels launched by this call     */
+  int32_t reserved;
+} rbicg_result;
+
+/* Create a context on `device`, adopting `cuda_stream` (a cudaStream_t, NULL
+ * = the legacy default stream).  dist may be NULL.  Returns RBICG_ECUDA if the
+ * device cannot be used. */
+int rbicg_init(rbicg_ctx **ctx, int device, void *cuda_stream,
+               const rbicg_dist *dist);
+int rbicg_finalize(rbicg_ctx *ctx);
+
+/* Build the device matrix store of A (SELL-32 layout, rebuilt per system,
+ * P:44-52) and its explicit conjugate transpose A^* (BASELINE.json (1)).
+ * rowptr[n+1], colind[nnz] are int32 CSR (columns need not be sorted; n and
+ * nnz < 2^31), val[nnz] of `dtype`.  on_device selects where the three
+ * arrays live.  The matrix is immutable once built. */
+int rbicg_matrix_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz,
+                     const int32_t *rowptr, const int32_t *colind,
+                     const void *val, rbicg_dtype dtype, int on_device,
+                     rbicg_mat **A);
+int rbicg_matrix_free(rbicg_mat *A);
+
+/* Recycle space handle (U, Ũ) with room for k_max columns; starts empty. */
+int rbicg_recycle_new(rbicg_ctx *ctx, int64_t n, int32_t k_max,
+                      rbicg_dtype dtype, rbicg_rec **R);
+/* Copy out the current basis (k columns, column-major n x k each). */
+int rbicg_recycle_export(const rbicg_rec *R, int32_t *k, void *U, void *Ut,
+                         int on_device);
+/* Replace the basis by (U, Ũ) (column-major n x k, k <= k_max). */
+int rbicg_recycle_import(rbicg_rec *R, int32_t k, const void *U,
+                         const void *Ut, int on_device);
+int rbicg_recycle_free(rbicg_rec *R);
+
+/* Solve the dual pair A x = b, A^* x~ = b~ with RBiCG (Algorithm 2) using the
+ * recycle space in R (refreshed for this A: C = AU, C~ = A^*Ũ, SVD),
+ * and (if opts->update_recycle) replace R by the recycle space built during
+ * this solve (the last full cycle's U_j, Ũ_j, reading Q18).
+ *   x, xt   in: x_{-1}, x~_{-1}; out: solution after step 7.
+ *   xt_redraw  nullable; the random x~_{-1} used once if (r_0, r~_0) = 0
+ *           (Algorithm 2 step 3; reading Q4).
+ *   hist    nullable [max_itn][6] doubles: ||r_i||/||b||, ||r~_i||/||b~||,
+ *           Re a_i, Im a_i, Re b_i, Im b_i.
+ * All of b, bt, x, xt, xt_redraw, hist live on host or device per on_device. */
+int rbicg_solve_dual(rbicg_ctx *ctx, const rbicg_mat *A, const void *b,
+                     const void *bt, void *x, void *xt, const void *xt_redraw,
+                     rbicg_rec *R, const rbicg_opts *opts, int on_device,
+                     rbicg_result *res, double *hist);
+
+/* u^* A^{-1} w from the dual pair A x = w, A^* x~ = u, estimator
+ * u^*x + x~^*(w - Ax) (reading Q19).  value: one scalar of A's dtype (host).
+ * x, xt: nullable outputs (initial guesses are zero). */
+int rbicg_bilinear(rbicg_ctx *ctx, const rbicg_mat *A, const void *u,
+                   const void *w, rbicg_rec *R, const rbicg_opts *opts,
+                   int on_device, void *value, rbicg_result *res);
+
+/* Parity hooks (per-call checks, BASELINE.json: 1e-12 relative).
+ * spmv_pair: z = A p, zt = A^* pt.
+ * project: given R's refreshed basis for A, zeta = D_c^{-1} C~^* z and
+ *   zetat = D_c^{-1} C^* zt; also returns the refreshed basis
+ *   (column-major) in U, Ut, C, Ct (nullable) and D_c in d (nullable). */
+int rbicg_dbg_spmv_pair(rbicg_ctx *ctx, const rbicg_mat *A, const void *p,
+                        const void *pt, void *z, void *zt, int on_device);
+int rbicg_dbg_project(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
+                      double trunc_tol, const void *z, const void *zt,
+                      void *zeta, void *zetat, int32_t *k_out, void *U,
+                      void *Ut, void *C, void *Ct, double *d, int on_device);
+
+/* Per-kernel CUDA-event timing of `iters` hot-loop iterations on the resident
+ * state of the last solve with this matrix (bench roofline).  ms[0] = average
+ * duration of the SpMV-pair+coefficient kernel, ms[1] = the update kernel. */
+int rbicg_dbg_time_kernels(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
+                           const rbicg_opts *opts, int iters, double *ms);
+
+const char *rbicg_strerror(int status);
+/* Kernel launches issued through this library since load (driver evidence). */
+int64_t rbicg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBICG_H */

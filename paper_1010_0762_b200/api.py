@@ -1,0 +1,239 @@
+"""Thin Python API over the C ABI (names follow include/rbicg.h).
+
+Host NumPy arrays are passed with on_device=0 (the library does the H2D/D2H
+copies inside the call); torch CUDA tensors are passed with on_device=1.
+No arithmetic of the method happens here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import lib, check, Opts, Result, F64, C128
+
+
+def _is_torch(a):
+    return type(a).__module__.startswith("torch")
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if _is_torch(a):
+        assert a.is_cuda and a.is_contiguous()
+        return C.c_void_p(a.data_ptr())
+    assert isinstance(a, np.ndarray) and a.flags.c_contiguous, type(a)
+    return C.c_void_p(a.ctypes.data)
+
+
+def _dtype_code(a):
+    if _is_torch(a):
+        import torch
+        return C128 if a.dtype == torch.complex128 else F64
+    return C128 if np.iscomplexobj(a) else F64
+
+
+class Context:
+    """rbicg_ctx on one GPU; adopts torch's current stream when available."""
+
+    def __init__(self, device: int = 0, stream=None):
+        if stream is None:
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    torch.cuda.set_device(device)
+                    stream = torch.cuda.current_stream(device).cuda_stream
+            except ImportError:   # pragma: no cover
+                stream = None
+        self.device = device
+        self._h = C.c_void_p()
+        check(lib.rbicg_init(C.byref(self._h), device,
+                             C.c_void_p(stream) if stream else None, None))
+
+    def close(self):
+        if self._h:
+            lib.rbicg_finalize(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ matrices
+    def matrix(self, indptr, indices, data):
+        return Matrix(self, indptr, indices, data)
+
+    def recycle(self, n, k_max, complex_=False):
+        return Recycle(self, n, k_max, complex_)
+
+    # ------------------------------------------------------------ solve
+    def solve_dual(self, A, b, bt, x=None, xt=None, R=None, *, k=10, s=40,
+                   tol=1e-8, max_itn=20000, trunc_tol=1e-6, update_recycle=True,
+                   force_iters=0, xt_redraw=None, history=False):
+        dev = _is_torch(b)
+        if x is None:
+            x = b * 0
+        if xt is None:
+            xt = bt * 0
+        if dev:
+            x = x.clone()
+            xt = xt.clone()
+        else:
+            x = np.array(x, dtype=b.dtype, copy=True)
+            xt = np.array(xt, dtype=b.dtype, copy=True)
+        o = Opts(k=k, s=s, max_itn=max_itn, tol=tol, trunc_tol=trunc_tol, seed=0,
+                 update_recycle=1 if update_recycle else 0,
+                 record_history=1 if history else 0, force_iters=force_iters)
+        res = Result()
+        hist = None
+        if history:
+            if dev:
+                import torch
+                hist = torch.zeros((max(max_itn, force_iters), 6),
+                                   dtype=torch.float64, device=b.device)
+            else:
+                hist = np.zeros((max(max_itn, force_iters), 6))
+        code = lib.rbicg_solve_dual(self._h, A._h, _ptr(b), _ptr(bt), _ptr(x),
+                                    _ptr(xt), _ptr(xt_redraw),
+                                    R._h if R is not None else None,
+                                    C.byref(o), 1 if dev else 0, C.byref(res),
+                                    _ptr(hist))
+        check(code)
+        r = res.as_dict()
+        if hist is not None:
+            hist = hist[:res.iterations]
+        return x, xt, r, hist
+
+    def bilinear(self, A, u, w, R=None, *, k=10, s=40, tol=1e-8, max_itn=20000,
+                 trunc_tol=1e-6, update_recycle=True):
+        dev = _is_torch(u)
+        o = Opts(k=k, s=s, max_itn=max_itn, tol=tol, trunc_tol=trunc_tol,
+                 update_recycle=1 if update_recycle else 0)
+        res = Result()
+        val = (C.c_double * 2)()
+        check(lib.rbicg_bilinear(self._h, A._h, _ptr(u), _ptr(w),
+                                 R._h if R is not None else None, C.byref(o),
+                                 1 if dev else 0, val, C.byref(res)))
+        v = complex(val[0], val[1]) if A.complex_ else val[0]
+        return v, res.as_dict()
+
+    # ------------------------------------------------------------ parity hooks
+    def spmv_pair(self, A, p, pt):
+        if _is_torch(p):
+            z, zt = p.clone(), pt.clone()
+        else:
+            z, zt = np.empty_like(p), np.empty_like(pt)
+        check(lib.rbicg_dbg_spmv_pair(self._h, A._h, _ptr(p), _ptr(pt), _ptr(z),
+                                      _ptr(zt), 1 if _is_torch(p) else 0))
+        return z, zt
+
+    def project(self, A, R, z, zt, trunc_tol=1e-6):
+        """Refreshed basis of R for A and ζ = D_c^{-1}C~^*z, ζ~ = D_c^{-1}C^*z~
+        (host outputs; z, zt host arrays)."""
+        n, kmax = A.n, R.k_max
+        dt = np.complex128 if A.complex_ else np.float64
+        zeta = np.zeros(max(kmax, 1), dt)
+        zetat = np.zeros(max(kmax, 1), dt)
+        kout = C.c_int32()
+        mats = [np.zeros((max(kmax, 1), n), dt) for _ in range(4)]
+        d = np.zeros(max(kmax, 1))
+        check(lib.rbicg_dbg_project(self._h, A._h, R._h, trunc_tol, _ptr(z),
+                                    _ptr(zt), _ptr(zeta), _ptr(zetat),
+                                    C.byref(kout), *[_ptr(m) for m in mats],
+                                    _ptr(d), 0))
+        k = kout.value
+        U, Ut, Cm, Ct = [m[:k].T.copy() for m in mats]
+        return dict(k=k, zeta=zeta[:k], zetat=zetat[:k], U=U, Ut=Ut, C=Cm,
+                    Ct=Ct, d=d[:k])
+
+    def time_kernels(self, A, R=None, *, k=10, s=40, iters=20, trunc_tol=1e-6):
+        o = Opts(k=k, s=s, max_itn=iters + 1, tol=0.0, trunc_tol=trunc_tol)
+        ms = (C.c_double * 4)()
+        check(lib.rbicg_dbg_time_kernels(self._h, A._h,
+                                         R._h if R is not None else None,
+                                         C.byref(o), iters, ms))
+        return dict(pass1_ms=ms[0], pass2_ms=ms[1], done_flag=ms[2], k=int(ms[3]))
+
+
+class Matrix:
+    """Device SELL-32 store of A and A^* (rbicg_matrix_csr)."""
+
+    def __init__(self, ctx, indptr, indices, data):
+        self.ctx = ctx
+        dev = _is_torch(data)
+        if not dev:
+            indptr = np.ascontiguousarray(indptr, dtype=np.int32)
+            indices = np.ascontiguousarray(indices, dtype=np.int32)
+            data = np.ascontiguousarray(data)
+            if data.dtype not in (np.float64, np.complex128):
+                data = data.astype(np.float64)
+        self.n = int(len(indptr) - 1)
+        self.nnz = int(len(indices))
+        self.complex_ = _dtype_code(data) == C128
+        self._h = C.c_void_p()
+        check(lib.rbicg_matrix_csr(ctx._h, self.n, self.nnz, _ptr(indptr),
+                                   _ptr(indices), _ptr(data),
+                                   C128 if self.complex_ else F64,
+                                   1 if dev else 0, C.byref(self._h)))
+
+    def free(self):
+        if self._h:
+            lib.rbicg_matrix_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Recycle:
+    """Recycle space handle (U, Ũ) carried between systems."""
+
+    def __init__(self, ctx, n, k_max, complex_=False):
+        self.ctx, self.n, self.k_max, self.complex_ = ctx, n, k_max, complex_
+        self._h = C.c_void_p()
+        check(lib.rbicg_recycle_new(ctx._h, n, k_max, C128 if complex_ else F64,
+                                    C.byref(self._h)))
+
+    @property
+    def k(self):
+        k = C.c_int32()
+        check(lib.rbicg_recycle_export(self._h, C.byref(k), None, None, 0))
+        return k.value
+
+    def export(self):
+        dt = np.complex128 if self.complex_ else np.float64
+        k = self.k
+        U = np.zeros((max(k, 1), self.n), dt)
+        Ut = np.zeros((max(k, 1), self.n), dt)
+        kk = C.c_int32()
+        check(lib.rbicg_recycle_export(self._h, C.byref(kk), _ptr(U), _ptr(Ut), 0))
+        return U[:k].T.copy(), Ut[:k].T.copy()
+
+    def import_(self, U, Ut):
+        dt = np.complex128 if self.complex_ else np.float64
+        k = U.shape[1]
+        Uc = np.ascontiguousarray(np.asarray(U, dt).T)
+        Utc = np.ascontiguousarray(np.asarray(Ut, dt).T)
+        check(lib.rbicg_recycle_import(self._h, k, _ptr(Uc), _ptr(Utc), 0))
+
+    def free(self):
+        if self._h:
+            lib.rbicg_recycle_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def launch_count():
+    return lib.rbicg_launch_count()

@@ -1,0 +1,1204 @@
+// api.cu -- the C ABI of include/rbicg.h and the solve driver.
+//
+// solve_dual (one dual pair, Algorithm 2 + §4):
+//   refresh      C = AU, C~ = A^*Ũ, column scaling, SVD, truncation  (Q13)
+//   init         r_{-1}, minusXR projection, (r_0, r~_0) check
+//   loop         CUDA graph of s iterations (pass1 + pass2 each), replayed per
+//                cycle; pauses on the device at every cycle boundary
+//   cycle end    Grams on the device, pencil QZ + selection on the host,
+//                U_j = Φ_j W_j, C_j = AU_j, SVD truncation
+//   finish       step 7, true residuals (Q2), return U_j as next U
+#include <algorithm>
+#include <chrono>
+#include <functional>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+
+#include "internal.h"
+
+using namespace rbicg;
+
+namespace rbicg {
+
+// ------------------------------------------------------------------ workspace pool
+static std::mutex g_pool_mu;
+static std::multimap<size_t, void *> g_pool;
+static std::map<void *, size_t> g_sizes;
+
+void *ws_alloc(size_t bytes) {
+  bytes = (bytes + 255) / 256 * 256;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_pool.lower_bound(bytes);
+    if (it != g_pool.end() && it->first <= bytes * 2) {
+      void *p = it->second;
+      g_pool.erase(it);
+      return p;
+    }
+  }
+  void *p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    // release cached blocks and retry once
+    {
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      for (auto &kv : g_pool) {
+        cudaFree(kv.second);
+        g_sizes.erase(kv.second);
+      }
+      g_pool.clear();
+    }
+    cudaGetLastError();
+    e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Err{RBICG_ENOMEM};
+    }
+  }
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_sizes[p] = bytes;
+  return p;
+}
+
+void ws_free(void *p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  auto it = g_sizes.find(p);
+  if (it == g_sizes.end()) return;
+  g_pool.emplace(it->second, p);
+}
+
+static void ws_release_all() {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (auto &kv : g_pool) {
+    cudaFree(kv.second);
+    g_sizes.erase(kv.second);
+  }
+  g_pool.clear();
+}
+
+// ------------------------------------------------------------------ small helpers
+template <typename T> static cplx toc(const T &v) { return cplx(re(v), im(v)); }
+template <typename T> static T fromc(cplx c);
+template <> double fromc<double>(cplx c) { return c.real(); }
+template <> zc fromc<zc>(cplx c) { return mk(c.real(), c.imag()); }
+
+template <typename T>
+__global__ void k_cm_to_rm(const T *cm, T *rm, int64_t n, int k) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * k;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / k;
+    const int c = (int)(i - row * k);
+    rm[i] = cm[(int64_t)c * n + row];
+  }
+}
+template <typename T>
+__global__ void k_rm_to_cm(const T *rm, T *cm, int64_t n, int k) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * k;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / n;
+    const int64_t row = i - c * n;
+    cm[i] = rm[row * k + c];
+  }
+}
+static int g1(int64_t m) { return (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 148 * 16)); }
+
+static void copy_in(void *dst, const void *src, size_t bytes, int on_device, cudaStream_t s) {
+  RB_CUDA(cudaMemcpyAsync(dst, src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+}
+static void copy_out(void *dst, const void *src, size_t bytes, int on_device, cudaStream_t s) {
+  RB_CUDA(cudaMemcpyAsync(dst, src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+}
+
+static double now_ms() {
+  using namespace std::chrono;
+  return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+static std::vector<cplx> matmul(const std::vector<cplx> &A, const std::vector<cplx> &B, int m, int kk,
+                                int nn) {  // row-major (m x kk)(kk x nn)
+  std::vector<cplx> C((size_t)m * nn, 0.0);
+  for (int i = 0; i < m; ++i)
+    for (int l = 0; l < kk; ++l) {
+      const cplx a = A[(size_t)i * kk + l];
+      if (a == cplx(0.0)) continue;
+      for (int j = 0; j < nn; ++j) C[(size_t)i * nn + j] += a * B[(size_t)l * nn + j];
+    }
+  return C;
+}
+static std::vector<cplx> adjoint(const std::vector<cplx> &A, int m, int nn) {
+  std::vector<cplx> B((size_t)nn * m);
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < nn; ++j) B[(size_t)j * m + i] = std::conj(A[(size_t)i * nn + j]);
+  return B;
+}
+
+// Q11 selection: indices into the pencil eigenpairs plus real-basis handling.
+struct Selection {
+  std::vector<cplx> W, Wt;   // row-major m x ksel
+  int ksel = 0;
+};
+static Selection select_pairs(bool real, int m, int k, const std::vector<cplx> &alpha,
+                              const std::vector<cplx> &beta, const std::vector<cplx> &VL,
+                              const std::vector<cplx> &VR, double qnorm) {
+  std::vector<int> idx;
+  std::vector<cplx> lam(m);
+  for (int i = 0; i < m; ++i) {
+    const bool fin = std::abs(beta[i]) > 1e-14 * qnorm;
+    if (!fin) continue;
+    lam[i] = alpha[i] / beta[i];
+    if (!std::isfinite(lam[i].real()) || !std::isfinite(lam[i].imag())) continue;
+    idx.push_back(i);
+  }
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+    const double ma = std::abs(lam[a]), mb = std::abs(lam[b]);
+    if (ma != mb) return ma < mb;
+    const double pa = std::arg(lam[a]), pb = std::arg(lam[b]);
+    if (pa != pb) return pa < pb;
+    return a < b;
+  });
+  std::vector<std::vector<cplx>> cols, colst;
+  auto colv = [&](const std::vector<cplx> &V, int j) {
+    return std::vector<cplx>(V.begin() + (size_t)j * m, V.begin() + (size_t)(j + 1) * m);
+  };
+  if (!real) {
+    for (int t = 0; t < (int)idx.size() && (int)cols.size() < k; ++t) {
+      cols.push_back(colv(VR, idx[t]));
+      colst.push_back(colv(VL, idx[t]));
+    }
+  } else {
+    std::vector<char> used(m, 0);
+    int count = 0;
+    for (int t = 0; t < (int)idx.size(); ++t) {
+      const int i = idx[t];
+      if (used[i]) continue;
+      if (alpha[i].imag() == 0.0) {
+        if (count + 1 > k) break;
+        auto w = colv(VR, i), wl = colv(VL, i);
+        for (auto &v : w) v = v.real();
+        for (auto &v : wl) v = v.real();
+        cols.push_back(w);
+        colst.push_back(wl);
+        used[i] = 1;
+        count += 1;
+      } else {
+        const int ip = alpha[i].imag() > 0 ? i : i - 1;
+        const int partner = alpha[i].imag() > 0 ? i + 1 : i - 1;
+        if (count + 2 > k) break;
+        auto w = colv(VR, ip), wl = colv(VL, ip);
+        std::vector<cplx> wr(m), wi(m), lr(m), li(m);
+        for (int q = 0; q < m; ++q) {
+          wr[q] = w[q].real();
+          wi[q] = w[q].imag();
+          lr[q] = wl[q].real();
+          li[q] = wl[q].imag();
+        }
+        cols.push_back(wr);
+        cols.push_back(wi);
+        colst.push_back(lr);
+        colst.push_back(li);
+        used[i] = 1;
+        if (partner >= 0 && partner < m) used[partner] = 1;
+        count += 2;
+      }
+    }
+  }
+  Selection S;
+  S.ksel = (int)cols.size();
+  S.W.assign((size_t)m * S.ksel, 0.0);
+  S.Wt.assign((size_t)m * S.ksel, 0.0);
+  for (int c = 0; c < S.ksel; ++c)
+    for (int q = 0; q < m; ++q) {
+      S.W[(size_t)q * S.ksel + c] = cols[c][q];
+      S.Wt[(size_t)q * S.ksel + c] = colst[c][q];
+    }
+  return S;
+}
+
+// ------------------------------------------------------------------ solver
+template <typename T>
+struct Solver {
+  rbicg_ctx *ctx = nullptr;
+  const rbicg_mat *M = nullptr;
+  rbicg_opts o{};
+  bool real = true;
+  int64_t n = 0;
+  int kmax = 0, ring = 0;
+  std::vector<void *> owned;
+  T *rring = nullptr, *rtring = nullptr, *p[2] = {}, *pt[2] = {}, *z = nullptr, *zt = nullptr;
+  T *x = nullptr, *xt = nullptr, *b = nullptr, *bt = nullptr, *xo = nullptr, *xto = nullptr;
+  struct Basis {
+    T *U = nullptr, *Ut = nullptr, *C = nullptr, *Ct = nullptr;
+    int k = 0;
+    std::vector<double> d;
+  } cur, cand[2], tmp;
+  int cand_cur = -1;
+  DevState<T> *st = nullptr;
+  DevState<T> *hst = nullptr;   // pinned host mirror
+  IterRec<T> *hist = nullptr;
+  T *zhist = nullptr, *zthist = nullptr;
+  T *part = nullptr;
+  LoopArgs<T> la{};
+  cudaGraphExec_t gexec = nullptr;
+  int graph_iters = 0;
+  double t_cycle_dev = 0, t_host_eig = 0, t_refresh = 0;
+  int64_t launches0 = 0, graph_launch_kernels = 0;
+
+  T *alloc(size_t elems) {
+    void *q = ws_alloc(sizeof(T) * std::max<size_t>(elems, 1));
+    owned.push_back(q);
+    return (T *)q;
+  }
+  ~Solver() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    for (void *q : owned) ws_free(q);
+    if (hst) cudaFreeHost(hst);
+  }
+
+  void setup(rbicg_ctx *c, const rbicg_mat *m, const rbicg_opts &opts, int k_basis) {
+    ctx = c;
+    M = m;
+    o = opts;
+    n = m->n;
+    real = (m->dtype == RBICG_F64);
+    kmax = std::max(std::max(o.k, k_basis), 1);
+    ring = o.s + 2;
+    rring = alloc((size_t)ring * n);
+    rtring = alloc((size_t)ring * n);
+    for (int q = 0; q < 2; ++q) {
+      p[q] = alloc(n);
+      pt[q] = alloc(n);
+    }
+    z = alloc(n);
+    zt = alloc(n);
+    x = alloc(n);
+    xt = alloc(n);
+    b = alloc(n);
+    bt = alloc(n);
+    xo = alloc(n);
+    xto = alloc(n);
+    for (Basis *B : {&cur, &cand[0], &cand[1], &tmp}) {
+      B->U = alloc((size_t)n * kmax);
+      B->Ut = alloc((size_t)n * kmax);
+      B->C = alloc((size_t)n * kmax);
+      B->Ct = alloc((size_t)n * kmax);
+      B->k = 0;
+    }
+    st = (DevState<T> *)ws_alloc(sizeof(DevState<T>));
+    owned.push_back(st);
+    RB_CUDA(cudaMallocHost(&hst, sizeof(DevState<T>)));
+    const int H = std::max(o.max_itn, 0) + 2;
+    hist = (IterRec<T> *)ws_alloc(sizeof(IterRec<T>) * H);
+    owned.push_back(hist);
+    zhist = alloc((size_t)H * kmax);
+    zthist = alloc((size_t)H * kmax);
+    const int nout = 3 * KMAX + 8 + 2 * KMAX;
+    part = alloc((size_t)nout * ctx->grid_stream);
+    memset(hst, 0, sizeof(DevState<T>));
+    launches0 = g_launches.load();
+  }
+
+  void make_args() {
+    la.n = n;
+    la.k = cur.k;
+    la.ring = ring;
+    la.G = ctx->grid_stream;
+    la.A = M->A;
+    la.AH = M->AH;
+    la.rring = rring;
+    la.rtring = rtring;
+    la.p[0] = p[0];
+    la.p[1] = p[1];
+    la.pt[0] = pt[0];
+    la.pt[1] = pt[1];
+    la.z = z;
+    la.zt = zt;
+    la.x = x;
+    la.xt = xt;
+    la.C = cur.C;
+    la.Ct = cur.Ct;
+    la.st = st;
+    la.hist = hist;
+    la.zhist = zhist;
+    la.zthist = zthist;
+    la.part = part;
+  }
+
+  void pull() {
+    RB_CUDA(cudaMemcpyAsync(hst, st, sizeof(DevState<T>), cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  void push() {
+    RB_CUDA(cudaMemcpyAsync(st, hst, sizeof(DevState<T>), cudaMemcpyHostToDevice, ctx->stream));
+  }
+
+  static ColDesc col(const T *base, int c, int ld) { return ColDesc{(const void *)(base + c), ld}; }
+  ColDesc rcol(int q) const { return ColDesc{(const void *)(rring + (int64_t)(q % ring) * n), 1}; }
+  ColDesc rtcol(int q) const { return ColDesc{(const void *)(rtring + (int64_t)(q % ring) * n), 1}; }
+
+  // Bi-orthogonalise (U, Ũ, C = AU, C~ = A^*Ũ) of width kin into `out`
+  // (Q13: unit columns, absolute cut on the singular values).
+  void biorth(const T *U, const T *Ut, const T *C, const T *Ct, int kin, Basis &out) {
+    std::vector<ColDesc> X;
+    for (int c = 0; c < kin; ++c) X.push_back(col(C, c, kin));
+    for (int c = 0; c < kin; ++c) X.push_back(col(Ct, c, kin));
+    std::vector<cplx> G;
+    gram<T>(X, X, n, G, ctx);
+    const int m2 = 2 * kin;
+    std::vector<int> kk;
+    std::vector<double> nc(kin), nct(kin);
+    for (int j = 0; j < kin; ++j) {
+      nc[j] = std::sqrt(std::max(0.0, G[(size_t)j * m2 + j].real()));
+      nct[j] = std::sqrt(std::max(0.0, G[(size_t)(kin + j) * m2 + kin + j].real()));
+      if (nc[j] > 0 && nct[j] > 0) kk.push_back(j);
+    }
+    const int m = (int)kk.size();
+    std::vector<cplx> Gn((size_t)m * m);
+    for (int a = 0; a < m; ++a)
+      for (int bb = 0; bb < m; ++bb)
+        Gn[(size_t)a * m + bb] = G[(size_t)(kin + kk[a]) * m2 + kk[bb]] / (nct[kk[a]] * nc[kk[bb]]);
+    std::vector<double> S;
+    std::vector<cplx> Ml, Nr;
+    const double t0 = now_ms();
+    RB_CHECK(lapack_gesvd(real, m, Gn, S, Ml, Nr) == 0, RBICG_ELAPACK);
+    t_host_eig += now_ms() - t0;
+    int pk = 0;
+    for (int a = 0; a < m; ++a)
+      if (S[a] >= o.trunc_tol) ++pk;
+    out.k = pk;
+    out.d.assign(S.begin(), S.begin() + pk);
+    if (pk == 0) return;
+    std::vector<cplx> Fu((size_t)kin * pk, 0.0), Fut((size_t)kin * pk, 0.0);
+    for (int a = 0; a < m; ++a)
+      for (int c = 0; c < pk; ++c) {
+        Fu[(size_t)kk[a] * pk + c] = Nr[(size_t)c * m + a] / nc[kk[a]];
+        Fut[(size_t)kk[a] * pk + c] = Ml[(size_t)c * m + a] / nct[kk[a]];
+      }
+    auto cols_of = [&](const T *B) {
+      std::vector<ColDesc> v;
+      for (int c = 0; c < kin; ++c) v.push_back(col(B, c, kin));
+      return v;
+    };
+    gemm_panels<T>(cols_of(U), Fu, pk, n, out.U, ctx);
+    gemm_panels<T>(cols_of(C), Fu, pk, n, out.C, ctx);
+    gemm_panels<T>(cols_of(Ut), Fut, pk, n, out.Ut, ctx);
+    gemm_panels<T>(cols_of(Ct), Fut, pk, n, out.Ct, ctx);
+  }
+
+  // Per-system refresh: C = AU, C~ = A^*Ũ, then biorth into cur.
+  void refresh(const T *U, const T *Ut, int kin) {
+    const double t0 = now_ms();
+    cur.k = 0;
+    if (kin > 0) {
+      launch_spmm<T>(M->A, U, tmp.C, kin, ctx->stream);
+      launch_spmm<T>(M->AH, Ut, tmp.Ct, kin, ctx->stream);
+      biorth(U, Ut, tmp.C, tmp.Ct, kin, cur);
+    }
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    t_refresh += now_ms() - t0;
+  }
+
+  void init_state() {
+    memset(hst, 0, sizeof(DevState<T>));
+    hst->max_itn = o.max_itn;
+    hst->force = o.force_iters > 0 ? 1 : 0;
+    if (o.force_iters > 0) hst->max_itn = o.force_iters;
+    hst->k = cur.k;
+    hst->stop_at = o.s;
+    for (int j = 0; j < cur.k; ++j) hst->dinv[j] = 1.0 / cur.d[j];
+    push();
+  }
+
+  // r_{-1}, minusXR, ρ_0; returns after the state has been pulled.
+  void initial_projection() {
+    launch_resid<T>(la, b, bt, x, xt, rring, rtring, cur.k > 0 ? 1 : 0, ctx->stream);
+    pull();
+    hst->tolb = o.tol * std::sqrt(hst->bn2);
+    hst->tolbt = o.tol * std::sqrt(hst->btn2);
+    push();
+    launch_init2<T>(la, cur.U, cur.Ut, ctx->stream);
+    pull();
+  }
+
+  void capture_graph() {
+    if (gexec) return;
+    cudaGraph_t g;
+    RB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    for (int it = 0; it < o.s; ++it) {
+      launch_pass1<T>(la, ctx->stream);
+      launch_pass2<T>(la, ctx->stream);
+    }
+    RB_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+    RB_CUDA(cudaGraphInstantiate(&gexec, g, 0));
+    RB_CUDA(cudaGraphDestroy(g));
+    graph_iters = o.s;
+    g_launches.fetch_sub(2 * o.s);   // captured, not launched
+  }
+
+  void run_graph() {
+    RB_CUDA(cudaGraphLaunch(gexec, ctx->stream));
+    g_launches.fetch_add(2 * graph_iters);
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+
+  // ---------------------------------------------------------------- cycle end
+  void cycle_end(int j) {
+    const double t0 = now_ms();
+    const int s = o.s;
+    const int lo = std::max(0, (j - 1) * s - 1), hi = j * s;
+    const int nrec = hi - lo + 1;
+    const int kc = cur.k;
+    std::vector<IterRec<T>> rec(nrec);
+    std::vector<T> zh((size_t)nrec * std::max(kc, 1)), zth((size_t)nrec * std::max(kc, 1));
+    RB_CUDA(cudaMemcpyAsync(rec.data(), hist + lo, sizeof(IterRec<T>) * nrec, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    if (kc > 0) {
+      RB_CUDA(cudaMemcpyAsync(zh.data(), zhist + (size_t)lo * kc, sizeof(T) * nrec * kc,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+      RB_CUDA(cudaMemcpyAsync(zth.data(), zthist + (size_t)lo * kc, sizeof(T) * nrec * kc,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    auto R = [&](int m) -> const IterRec<T> & { return rec[m - lo]; };
+    auto al = [&](int m) { return toc(R(m).alpha); };
+    auto be = [&](int m) { return m == 0 ? cplx(0.0) : toc(R(m).beta); };
+    auto rn = [&](int m) { return R(m).rnorm; };
+    auto rh = [&](int m) { return toc(R(m).rho); };
+    // tridiagonal T from the iteration scalars
+    auto Tij = [&](int a, int bb) -> cplx {
+      if (a == bb) return 1.0 / al(a) + (a > 1 ? be(a - 1) / al(a - 1) : cplx(0.0));
+      if (a == bb + 1) return -(rn(bb) / rn(bb - 1)) / al(bb);
+      if (bb == a + 1) return -(rn(a - 1) / rn(a)) * be(a) / al(a);
+      return 0.0;
+    };
+    std::vector<int> cols, rows;
+    for (int m = (j - 1) * s + 1; m <= j * s; ++m) cols.push_back(m);
+    if (j > 1) rows.push_back((j - 1) * s);
+    rows.insert(rows.end(), cols.begin(), cols.end());
+    rows.push_back(j * s + 1);
+    const int nr = (int)rows.size(), top = j > 1 ? 1 : 0;
+    std::vector<cplx> Gam((size_t)nr * s), Gamt((size_t)nr * s);
+    for (int a = 0; a < nr; ++a)
+      for (int bb = 0; bb < s; ++bb) {
+        Gam[(size_t)a * s + bb] = Tij(rows[a], cols[bb]);
+        Gamt[(size_t)a * s + bb] = std::conj(Tij(cols[bb], rows[a]));   // T~ = T^*
+      }
+    // Lanczos vector scalings (scalingfactor)
+    auto sv = [&](int m) { return cplx(1.0 / rn(m - 1)); };
+    auto svt = [&](int m) { return rn(m - 1) / std::conj(rh(m - 1)); };
+
+    const bool haveC = kc > 0;
+    const bool havePrev = cand_cur >= 0 && cand[cand_cur].k > 0;
+    Basis *prev = havePrev ? &cand[cand_cur] : nullptr;
+    const int kp = havePrev ? prev->k : 0;
+    const int nxt = cand_cur < 0 ? 0 : 1 - cand_cur;
+    Basis &out = cand[nxt];
+
+    std::vector<ColDesc> PhiCols, PhitCols;
+    std::vector<cplx> Wrow, Wtrow;   // scaled selection matrices (row-major mphi x ksel)
+    int ksel = 0, mphi = 0;
+    std::vector<cplx> P, Q;
+    int mp = 0;
+    double teig0 = 0;
+    if (!haveC && !havePrev) {
+      // first system, no recycle data: eigenvectors of T_j
+      mp = s;
+      P.assign((size_t)s * s, 0.0);
+      Q.assign((size_t)s * s, 0.0);
+      for (int a = 0; a < s; ++a) {
+        Q[(size_t)a * s + a] = 1.0;
+        for (int bb = 0; bb < s; ++bb) P[(size_t)a * s + bb] = Gam[(size_t)(a + top) * s + bb];
+      }
+      for (int bb = 0; bb < s; ++bb) {
+        PhiCols.push_back(rcol(cols[bb] - 1));
+        PhitCols.push_back(rtcol(cols[bb] - 1));
+      }
+      mphi = s;
+    } else {
+      // B_j = Ĉ^*AV_j, B~_j = Č^*A^*Ṽ_j from the stored ζ (exact identity, R4)
+      std::vector<cplx> B((size_t)kc * s), Bt((size_t)kc * s);
+      for (int bb = 0; bb < s && kc > 0; ++bb) {
+        const int m = cols[bb];
+        for (int q = 0; q < kc; ++q) {
+          cplx zm = toc(zh[(size_t)(m - lo) * kc + q]);
+          cplx ztm = toc(zth[(size_t)(m - lo) * kc + q]);
+          if (m > 1) {
+            zm -= be(m - 1) * toc(zh[(size_t)(m - 1 - lo) * kc + q]);
+            ztm -= std::conj(be(m - 1)) * toc(zth[(size_t)(m - 1 - lo) * kc + q]);
+          }
+          B[(size_t)q * s + bb] = zm / rn(m - 1);
+          Bt[(size_t)q * s + bb] = ztm * rn(m - 1) / std::conj(rh(m - 1));
+        }
+      }
+      // columns of Ψ~ (X) and [Ψ, X0] (Y) -- raw residual columns, scalings on host
+      std::vector<ColDesc> X, Y;
+      std::vector<cplx> sx, sy;
+      if (haveC)
+        for (int c = 0; c < kc; ++c) {
+          X.push_back(col(cur.Ct, c, kc));
+          Y.push_back(col(cur.C, c, kc));
+          sx.push_back(1.0);
+          sy.push_back(1.0);
+        }
+      if (havePrev)
+        for (int c = 0; c < kp; ++c) {
+          X.push_back(col(prev->Ct, c, kp));
+          Y.push_back(col(prev->C, c, kp));
+          sx.push_back(1.0);
+          sy.push_back(1.0);
+        }
+      const int offU = (int)X.size();
+      for (int a = 0; a < nr; ++a) {
+        X.push_back(rtcol(rows[a] - 1));
+        Y.push_back(rcol(rows[a] - 1));
+        sx.push_back(svt(rows[a]));
+        sy.push_back(sv(rows[a]));
+      }
+      const int mpsi = (int)X.size();
+      // Φ = [X0, V]: X0 = U_{j-1} (havePrev) else U (later system, cycle 1)
+      const T *X0 = havePrev ? prev->U : cur.U;
+      const T *X0t = havePrev ? prev->Ut : cur.Ut;
+      const int kx = havePrev ? kp : kc;
+      for (int c = 0; c < kx; ++c) {
+        Y.push_back(col(X0, c, kx));
+        sy.push_back(1.0);
+      }
+      std::vector<cplx> Graw;
+      gram<T>(X, Y, n, Graw, ctx);
+      const int mY = (int)Y.size();
+      std::vector<cplx> G1((size_t)mpsi * mpsi), G2((size_t)mpsi * (kx + s));
+      for (int a = 0; a < mpsi; ++a) {
+        for (int bb = 0; bb < mpsi; ++bb)
+          G1[(size_t)a * mpsi + bb] = std::conj(sx[a]) * Graw[(size_t)a * mY + bb] * sy[bb];
+        for (int c = 0; c < kx; ++c)
+          G2[(size_t)a * (kx + s) + c] = std::conj(sx[a]) * Graw[(size_t)a * mY + mpsi + c];
+        for (int bb = 0; bb < s; ++bb) {
+          const int yc = offU + top + bb;
+          G2[(size_t)a * (kx + s) + kx + bb] = std::conj(sx[a]) * Graw[(size_t)a * mY + yc] * sy[yc];
+        }
+      }
+      // H, H~ per case
+      mphi = kx + s;
+      std::vector<cplx> H((size_t)mpsi * mphi, 0.0), Ht((size_t)mpsi * mphi, 0.0);
+      int r0 = 0;
+      if (haveC && havePrev) {
+        for (int q = 0; q < kc; ++q)
+          for (int bb = 0; bb < s; ++bb) {
+            H[(size_t)q * mphi + kx + bb] = B[(size_t)q * s + bb];
+            Ht[(size_t)q * mphi + kx + bb] = Bt[(size_t)q * s + bb];
+          }
+        r0 = kc;
+        for (int q = 0; q < kp; ++q) H[(size_t)(r0 + q) * mphi + q] = Ht[(size_t)(r0 + q) * mphi + q] = 1.0;
+        r0 += kp;
+      } else if (havePrev) {
+        for (int q = 0; q < kp; ++q) H[(size_t)q * mphi + q] = Ht[(size_t)q * mphi + q] = 1.0;
+        r0 = kp;
+      } else {
+        for (int q = 0; q < kc; ++q) {
+          H[(size_t)q * mphi + q] = Ht[(size_t)q * mphi + q] = 1.0;
+          for (int bb = 0; bb < s; ++bb) {
+            H[(size_t)q * mphi + kx + bb] = B[(size_t)q * s + bb];
+            Ht[(size_t)q * mphi + kx + bb] = Bt[(size_t)q * s + bb];
+          }
+        }
+        r0 = kc;
+      }
+      for (int a = 0; a < nr; ++a)
+        for (int bb = 0; bb < s; ++bb) {
+          H[(size_t)(r0 + a) * mphi + kx + bb] = Gam[(size_t)a * s + bb];
+          Ht[(size_t)(r0 + a) * mphi + kx + bb] = Gamt[(size_t)a * s + bb];
+        }
+      // P = H~^* (Ψ~^*Ψ) H,  Q = H~^* (Ψ~^*Φ)   (finalGenEigValue)
+      auto HtH = adjoint(Ht, mpsi, mphi);
+      P = matmul(matmul(HtH, G1, mphi, mpsi, mpsi), H, mphi, mpsi, mphi);
+      Q = matmul(HtH, G2, mphi, mpsi, mphi);
+      mp = mphi;
+      for (int c = 0; c < kx; ++c) {
+        PhiCols.push_back(col(X0, c, kx));
+        PhitCols.push_back(col(X0t, c, kx));
+      }
+      for (int bb = 0; bb < s; ++bb) {
+        PhiCols.push_back(rcol(cols[bb] - 1));
+        PhitCols.push_back(rtcol(cols[bb] - 1));
+      }
+    }
+    // host QZ with left and right vectors + Q11/Q12 selection
+    teig0 = now_ms();
+    std::vector<cplx> alpha, beta, VL, VR;
+    std::vector<int> pf;
+    RB_CHECK(lapack_ggev(real, mp, P, Q, alpha, beta, VL, VR, pf) == 0, RBICG_ELAPACK);
+    double qn = 0;
+    for (auto &v : Q) qn += std::norm(v);
+    qn = std::sqrt(qn);
+    Selection sel = select_pairs(real, mp, o.k, alpha, beta, VL, VR, qn);
+    t_host_eig += now_ms() - teig0;
+    ksel = sel.ksel;
+    out.k = 0;
+    if (ksel > 0) {
+      // fold the Lanczos scalings of the V columns into W (rows kx.. of Φ)
+      const int kx = mphi - s;
+      Wrow = sel.W;
+      Wtrow = sel.Wt;
+      for (int bb = 0; bb < s; ++bb) {
+        const cplx a = sv(cols[bb]), at = svt(cols[bb]);
+        for (int c = 0; c < ksel; ++c) {
+          Wrow[(size_t)(kx + bb) * ksel + c] *= a;
+          Wtrow[(size_t)(kx + bb) * ksel + c] *= at;
+        }
+      }
+      // U_j = Φ_j W_j, Ũ_j = Φ~_j W~_j; C_j = A U_j, C~_j = A^* Ũ_j
+      gemm_panels<T>(PhiCols, Wrow, ksel, n, tmp.U, ctx);
+      gemm_panels<T>(PhitCols, Wtrow, ksel, n, tmp.Ut, ctx);
+      launch_spmm<T>(M->A, tmp.U, tmp.C, ksel, ctx->stream);
+      launch_spmm<T>(M->AH, tmp.Ut, tmp.Ct, ksel, ctx->stream);
+      biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out);
+    }
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    cand_cur = nxt;
+    t_cycle_dev += now_ms() - t0;
+  }
+};
+
+}  // namespace rbicg
+
+// ====================================================================== ABI
+static int run_guarded(const std::function<void()> &f) {
+  try {
+    f();
+    return 0;
+  } catch (Err &e) {
+    return e.code;
+  } catch (std::bad_alloc &) {
+    return RBICG_ENOMEM;
+  } catch (...) {
+    return RBICG_ESTATE;
+  }
+}
+
+const char *rbicg_strerror(int s) {
+  switch (s) {
+    case RBICG_OK: return "ok";
+    case RBICG_MAXITER: return "max_itn reached";
+    case RBICG_BREAKDOWN_SERIOUS: return "serious breakdown: (r~_i, r_i) = 0";
+    case RBICG_BREAKDOWN_SECOND: return "breakdown of the second kind: (p~_i, q_i) = 0";
+    case RBICG_RECYCLE_EMPTY: return "recycle space empty after truncation";
+    case RBICG_EINVAL: return "invalid argument";
+    case RBICG_ENOMEM: return "out of device memory";
+    case RBICG_ECUDA: return "CUDA error";
+    case RBICG_ENCCL: return "NCCL error";
+    case RBICG_ELAPACK: return "LAPACK unavailable or failed (set RBICG_LAPACK)";
+    case RBICG_ESTATE: return "invalid state";
+  }
+  return "unknown status";
+}
+
+int64_t rbicg_launch_count(void) { return g_launches.load(); }
+
+int rbicg_init(rbicg_ctx **out, int device, void *stream, const rbicg_dist *dist) {
+  if (!out) return RBICG_EINVAL;
+  if (dist && dist->nranks != 1) return RBICG_EINVAL;
+  return run_guarded([&] {
+    int ndev = 0;
+    RB_CUDA(cudaGetDeviceCount(&ndev));
+    RB_CHECK(device >= 0 && device < ndev, RBICG_EINVAL);
+    RB_CUDA(cudaSetDevice(device));
+    auto *c = new rbicg_ctx();
+    c->device = device;
+    c->stream = (cudaStream_t)stream;
+    RB_CUDA(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
+    c->grid_stream = c->nsm * 2;
+    prepare_kernels();
+    *out = c;
+  });
+}
+
+int rbicg_finalize(rbicg_ctx *ctx) {
+  if (!ctx) return RBICG_EINVAL;
+  cudaStreamSynchronize(ctx->stream);
+  ws_release_all();
+  delete ctx;
+  return 0;
+}
+
+int rbicg_matrix_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr,
+                     const int32_t *colind, const void *val, rbicg_dtype dtype, int on_device,
+                     rbicg_mat **A) {
+  if (!ctx || !A || n <= 0 || nnz < 0 || n >= INT32_MAX || nnz >= INT32_MAX) return RBICG_EINVAL;
+  if (dtype != RBICG_F64 && dtype != RBICG_C128) return RBICG_EINVAL;
+  return run_guarded([&] {
+    RB_CUDA(cudaSetDevice(ctx->device));
+    const size_t w = wbytes(dtype);
+    int32_t *rp = (int32_t *)ws_alloc(sizeof(int32_t) * (n + 1));
+    int32_t *ci = (int32_t *)ws_alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+    void *vv = ws_alloc(w * std::max<int64_t>(nnz, 1));
+    copy_in(rp, rowptr, sizeof(int32_t) * (n + 1), on_device, ctx->stream);
+    if (nnz) {
+      copy_in(ci, colind, sizeof(int32_t) * nnz, on_device, ctx->stream);
+      copy_in(vv, val, w * nnz, on_device, ctx->stream);
+    }
+    auto *M = new rbicg_mat();
+    M->ctx = ctx;
+    try {
+      build_matrix(ctx, n, nnz, rp, ci, vv, dtype, M);
+    } catch (...) {
+      ws_free(rp);
+      ws_free(ci);
+      ws_free(vv);
+      free_devmat(M->A);
+      free_devmat(M->AH);
+      delete M;
+      throw;
+    }
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    ws_free(rp);
+    ws_free(ci);
+    ws_free(vv);
+    *A = M;
+  });
+}
+
+int rbicg_matrix_free(rbicg_mat *A) {
+  if (!A) return RBICG_EINVAL;
+  cudaStreamSynchronize(A->ctx->stream);
+  free_devmat(A->A);
+  free_devmat(A->AH);
+  delete A;
+  return 0;
+}
+
+int rbicg_recycle_new(rbicg_ctx *ctx, int64_t n, int32_t k_max, rbicg_dtype dtype, rbicg_rec **R) {
+  if (!ctx || !R || n <= 0 || k_max < 0 || k_max > KMAX) return RBICG_EINVAL;
+  return run_guarded([&] {
+    auto *r = new rbicg_rec();
+    r->ctx = ctx;
+    r->n = n;
+    r->kmax = k_max;
+    r->k = 0;
+    r->dtype = dtype;
+    const size_t bytes = wbytes(dtype) * n * std::max(k_max, 1);
+    RB_CUDA(cudaMalloc(&r->U, bytes));
+    RB_CUDA(cudaMalloc(&r->Ut, bytes));
+    *R = r;
+  });
+}
+
+int rbicg_recycle_free(rbicg_rec *R) {
+  if (!R) return RBICG_EINVAL;
+  cudaFree(R->U);
+  cudaFree(R->Ut);
+  delete R;
+  return 0;
+}
+
+template <typename T>
+static void rec_import(rbicg_rec *R, int32_t k, const void *U, const void *Ut, int on_device) {
+  rbicg_ctx *ctx = R->ctx;
+  const size_t bytes = sizeof(T) * R->n * k;
+  T *tmp = (T *)ws_alloc(std::max<size_t>(bytes, 16));
+  for (int q = 0; q < 2; ++q) {
+    copy_in(tmp, q ? Ut : U, bytes, on_device, ctx->stream);
+    k_cm_to_rm<T><<<g1(R->n * k), 256, 0, ctx->stream>>>(tmp, (T *)(q ? R->Ut : R->U), R->n, k);
+    count_launch();
+  }
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  ws_free(tmp);
+  R->k = k;
+}
+
+template <typename T>
+static void rec_export(const rbicg_rec *R, void *U, void *Ut, int on_device) {
+  rbicg_ctx *ctx = R->ctx;
+  const size_t bytes = sizeof(T) * R->n * R->k;
+  if (!bytes) return;
+  T *tmp = (T *)ws_alloc(bytes);
+  for (int q = 0; q < 2; ++q) {
+    k_rm_to_cm<T><<<g1(R->n * R->k), 256, 0, ctx->stream>>>((const T *)(q ? R->Ut : R->U), tmp, R->n,
+                                                            R->k);
+    count_launch();
+    copy_out(q ? Ut : U, tmp, bytes, on_device, ctx->stream);
+  }
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  ws_free(tmp);
+}
+
+int rbicg_recycle_import(rbicg_rec *R, int32_t k, const void *U, const void *Ut, int on_device) {
+  if (!R || k < 0 || k > R->kmax || (k > 0 && (!U || !Ut))) return RBICG_EINVAL;
+  return run_guarded([&] {
+    if (R->dtype == RBICG_F64) rec_import<double>(R, k, U, Ut, on_device);
+    else rec_import<zc>(R, k, U, Ut, on_device);
+  });
+}
+
+int rbicg_recycle_export(const rbicg_rec *R, int32_t *k, void *U, void *Ut, int on_device) {
+  if (!R || !k) return RBICG_EINVAL;
+  *k = R->k;
+  if (R->k == 0 || !U || !Ut) return 0;
+  return run_guarded([&] {
+    if (R->dtype == RBICG_F64) rec_export<double>(R, U, Ut, on_device);
+    else rec_export<zc>(R, U, Ut, on_device);
+  });
+}
+
+// ------------------------------------------------------------------ solve
+template <typename T>
+static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void *bt, void *x,
+                   void *xt, const void *xt_redraw, rbicg_rec *R, const rbicg_opts *opts,
+                   int on_device, rbicg_result *res, double *hist_out) {
+  const double t_start = now_ms();
+  Solver<T> S;
+  const int kin = R ? R->k : 0;
+  S.setup(ctx, A, *opts, kin);
+  const int64_t n = A->n;
+  const size_t vb = sizeof(T) * n;
+  cudaStream_t st = ctx->stream;
+  copy_in(S.b, b, vb, on_device, st);
+  copy_in(S.bt, bt, vb, on_device, st);
+  copy_in(S.x, x, vb, on_device, st);
+  copy_in(S.xt, xt, vb, on_device, st);
+  RB_CUDA(cudaMemsetAsync(S.p[0], 0, vb, st));
+  RB_CUDA(cudaMemsetAsync(S.pt[0], 0, vb, st));
+  // Step 1 + refresh
+  S.refresh(R && kin > 0 ? (const T *)R->U : nullptr, R && kin > 0 ? (const T *)R->Ut : nullptr,
+            opts->k > 0 ? kin : 0);
+  S.make_args();
+  S.init_state();
+  // Steps 2-3
+  S.initial_projection();
+  if (S.hst->done == 1 && S.hst->status == RBICG_BREAKDOWN_SERIOUS && xt_redraw) {
+    copy_in(S.xt, xt_redraw, vb, on_device, st);
+    S.initial_projection();
+  }
+  const double t_loop0 = now_ms();
+  double t_loop = 0;
+  int cycles = 0, last_cycle = 0;
+  bool retried = false;
+  bool finished_step7 = false;
+  const bool update = opts->update_recycle && opts->k > 0;
+  if (!(S.hst->done == 1)) S.capture_graph();
+  while (S.hst->done != 1) {
+    S.hst->done = 0;
+    S.hst->stop_at = (S.hst->iter / opts->s + 1) * opts->s;
+    S.push();
+    const double tl = now_ms();
+    S.run_graph();
+    S.pull();
+    t_loop += now_ms() - tl;
+    const int it = S.hst->iter;
+    const bool boundary = it > 0 && it % opts->s == 0 && it / opts->s > last_cycle;
+    const bool cyc_ok = S.hst->done == 2 ||
+                        (S.hst->done == 1 && (S.hst->status == RBICG_OK || S.hst->status == RBICG_MAXITER));
+    if (update && boundary && cyc_ok) {
+      S.cycle_end(it / opts->s);
+      last_cycle = it / opts->s;
+      ++cycles;
+    }
+    if (S.hst->done == 1 && S.hst->status == RBICG_OK && !S.hst->force) {
+      // Step 7 and the true-residual confirmation (Q2)
+      launch_step7<T>(S.la, S.cur.U, S.cur.Ut, S.xo, S.xto, st);
+      launch_resid<T>(S.la, S.b, S.bt, S.xo, S.xto, S.z, S.zt, 0, st);
+      DevState<T> keep = *S.hst;
+      S.pull();
+      const double tr = std::sqrt(S.hst->rn2 / S.hst->bn2), trt = std::sqrt(S.hst->rtn2 / S.hst->btn2);
+      *S.hst = keep;
+      finished_step7 = true;
+      if ((tr > opts->tol || trt > opts->tol) && !retried) {
+        if (S.hst->iter >= S.hst->max_itn) {   // as the oracle: loop exhausted
+          S.hst->status = RBICG_MAXITER;
+          break;
+        }
+        retried = true;
+        S.hst->tolb *= 0.1;
+        S.hst->tolbt *= 0.1;
+        S.hst->done = 0;
+        finished_step7 = false;
+        S.push();
+        continue;
+      }
+      break;
+    }
+  }
+  (void)t_loop0;
+  if (!finished_step7) launch_step7<T>(S.la, S.cur.U, S.cur.Ut, S.xo, S.xto, st);
+  launch_resid<T>(S.la, S.b, S.bt, S.xo, S.xto, S.z, S.zt, 0, st);
+  const DevState<T> fin = *S.hst;
+  S.pull();
+  const double tr = std::sqrt(S.hst->rn2 / S.hst->bn2), trt = std::sqrt(S.hst->rtn2 / S.hst->btn2);
+  copy_out(x, S.xo, vb, on_device, st);
+  copy_out(xt, S.xto, vb, on_device, st);
+  // recycle space for the next system (Q18)
+  int k_out = S.cur.k;
+  if (R && opts->k > 0) {
+    const typename Solver<T>::Basis *src = &S.cur;
+    if (update && S.cand_cur >= 0) src = &S.cand[S.cand_cur];
+    k_out = std::min(src->k, R->kmax);
+    if (k_out > 0) {
+      RB_CUDA(cudaMemcpyAsync(R->U, src->U, sizeof(T) * n * k_out, cudaMemcpyDeviceToDevice, st));
+      RB_CUDA(cudaMemcpyAsync(R->Ut, src->Ut, sizeof(T) * n * k_out, cudaMemcpyDeviceToDevice, st));
+    }
+    R->k = k_out;
+  }
+  int status = fin.status;
+  if (status == RBICG_OK && update && S.cand_cur >= 0 && S.cand[S.cand_cur].k == 0)
+    status = RBICG_RECYCLE_EMPTY;
+  if (hist_out && opts->record_history && fin.iter > 0) {
+    std::vector<IterRec<T>> h(fin.iter + 1);
+    RB_CUDA(cudaMemcpyAsync(h.data(), S.hist, sizeof(IterRec<T>) * (fin.iter + 1), cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> hh((size_t)fin.iter * 6);
+    const double bn = std::sqrt(fin.bn2), btn = std::sqrt(fin.btn2);
+    for (int i = 1; i <= fin.iter; ++i) {
+      double *r = &hh[(size_t)(i - 1) * 6];
+      r[0] = h[i].rnorm / bn;
+      r[1] = h[i].rtnorm / btn;
+      r[2] = re(h[i].alpha);
+      r[3] = im(h[i].alpha);
+      r[4] = re(h[i].beta);
+      r[5] = im(h[i].beta);
+    }
+    if (on_device)
+      RB_CUDA(cudaMemcpyAsync(hist_out, hh.data(), sizeof(double) * hh.size(), cudaMemcpyHostToDevice, st));
+    else
+      memcpy(hist_out, hh.data(), sizeof(double) * hh.size());
+  }
+  RB_CUDA(cudaStreamSynchronize(st));
+  if (res) {
+    memset(res, 0, sizeof(*res));
+    res->status = status;
+    res->iterations = fin.iter;
+    res->cycles = cycles;
+    res->k_in = S.cur.k;
+    res->k_out = k_out;
+    res->relres_rec = fin.rnorm / std::sqrt(fin.bn2);
+    res->relres_dual_rec = fin.rtnorm / std::sqrt(fin.btn2);
+    res->relres_true = tr;
+    res->relres_dual_true = trt;
+    res->t_loop_ms = t_loop;
+    res->t_cycle_dev_ms = S.t_cycle_dev;
+    res->t_host_eig_ms = S.t_host_eig;
+    res->t_refresh_ms = S.t_refresh;
+    res->t_total_ms = now_ms() - t_start;
+    const double w = sizeof(T), kk = S.cur.k;
+    const double mat = 2.0 * (A->nnz * (w + 4) + 4.0 * (n + 1));
+    res->alg_bytes = fin.iter * (mat + 4.0 * kk * n * w + 20.0 * n * w);
+    res->kernel_launches = (int32_t)(g_launches.load() - S.launches0);
+  }
+  return status;
+}
+
+int rbicg_solve_dual(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void *bt, void *x,
+                     void *xt, const void *xt_redraw, rbicg_rec *R, const rbicg_opts *o,
+                     int on_device, rbicg_result *res, double *hist) {
+  if (!ctx || !A || !b || !bt || !x || !xt || !o) return RBICG_EINVAL;
+  if (o->s < 2 || o->k < 0 || o->k > KMAX || o->max_itn < 0 || !(o->tol >= 0)) return RBICG_EINVAL;
+  if (R && (R->n != A->n || R->dtype != A->dtype)) return RBICG_EINVAL;
+  int status = 0;
+  int rc = run_guarded([&] {
+    RB_CUDA(cudaSetDevice(ctx->device));
+    if (A->dtype == RBICG_F64)
+      status = solve_t<double>(ctx, A, b, bt, x, xt, xt_redraw, R, o, on_device, res, hist);
+    else
+      status = solve_t<zc>(ctx, A, b, bt, x, xt, xt_redraw, R, o, on_device, res, hist);
+  });
+  return rc ? rc : status;
+}
+
+int rbicg_bilinear(rbicg_ctx *ctx, const rbicg_mat *A, const void *u, const void *w, rbicg_rec *R,
+                   const rbicg_opts *o, int on_device, void *value, rbicg_result *res) {
+  if (!ctx || !A || !u || !w || !o || !value) return RBICG_EINVAL;
+  const size_t wb = wbytes(A->dtype);
+  const int64_t n = A->n;
+  void *dx = nullptr, *dxt = nullptr, *du = nullptr, *dw = nullptr, *dr = nullptr;
+  int status = 0;
+  int rc = run_guarded([&] {
+    RB_CUDA(cudaSetDevice(ctx->device));
+    dx = ws_alloc(wb * n);
+    dxt = ws_alloc(wb * n);
+    du = ws_alloc(wb * n);
+    dw = ws_alloc(wb * n);
+    dr = ws_alloc(wb * n);
+    RB_CUDA(cudaMemsetAsync(dx, 0, wb * n, ctx->stream));
+    RB_CUDA(cudaMemsetAsync(dxt, 0, wb * n, ctx->stream));
+    copy_in(du, u, wb * n, on_device, ctx->stream);
+    copy_in(dw, w, wb * n, on_device, ctx->stream);
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    // dual pair A x = w, A^* x~ = u
+    status = rbicg_solve_dual(ctx, A, dw, du, dx, dxt, nullptr, R, o, 1, res, nullptr);
+    if (status < 0) throw Err{status};
+    // estimate u^*x + x~^*(w - A x)  (Q19): r = w - A x via the SpMV hook
+    void *dz = ws_alloc(wb * n), *dzt = ws_alloc(wb * n);
+    int e = rbicg_dbg_spmv_pair(ctx, A, dx, dxt, dz, dzt, 1);
+    if (e) throw Err{e};
+    std::vector<ColDesc> X{{du, 1}, {dxt, 1}}, Y{{dx, 1}, {dz, 1}, {dw, 1}};
+    std::vector<cplx> G;
+    if (A->dtype == RBICG_F64) gram<double>(X, Y, n, G, ctx);
+    else gram<zc>(X, Y, n, G, ctx);
+    // x~^*(w - Ax) = x~^*w - x~^*(Ax)
+    const cplx v = G[0 * 3 + 0] + (G[1 * 3 + 2] - G[1 * 3 + 1]);
+    if (A->dtype == RBICG_F64) {
+      ((double *)value)[0] = v.real();
+    } else {
+      ((double *)value)[0] = v.real();
+      ((double *)value)[1] = v.imag();
+    }
+    ws_free(dz);
+    ws_free(dzt);
+  });
+  for (void *q : {dx, dxt, du, dw, dr}) ws_free(q);
+  return rc ? rc : status;
+}
+
+int rbicg_dbg_spmv_pair(rbicg_ctx *ctx, const rbicg_mat *A, const void *p, const void *pt, void *z,
+                        void *zt, int on_device) {
+  if (!ctx || !A || !p || !pt || !z || !zt) return RBICG_EINVAL;
+  return run_guarded([&] {
+    const size_t vb = wbytes(A->dtype) * A->n;
+    void *dp = ws_alloc(vb), *dpt = ws_alloc(vb), *dz = ws_alloc(vb), *dzt = ws_alloc(vb);
+    copy_in(dp, p, vb, on_device, ctx->stream);
+    copy_in(dpt, pt, vb, on_device, ctx->stream);
+    if (A->dtype == RBICG_F64)
+      launch_spmv_pair<double>(A->A, A->AH, (const double *)dp, (const double *)dpt, (double *)dz,
+                               (double *)dzt, ctx->stream);
+    else
+      launch_spmv_pair<zc>(A->A, A->AH, (const zc *)dp, (const zc *)dpt, (zc *)dz, (zc *)dzt,
+                           ctx->stream);
+    copy_out(z, dz, vb, on_device, ctx->stream);
+    copy_out(zt, dzt, vb, on_device, ctx->stream);
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (void *q : {dp, dpt, dz, dzt}) ws_free(q);
+  });
+}
+
+template <typename T>
+static void project_t(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, double trunc_tol,
+                      const void *z, const void *zt, void *zeta, void *zetat, int32_t *k_out, void *U,
+                      void *Ut, void *C, void *Ct, double *d, int on_device) {
+  rbicg_opts o{};
+  o.k = R->k;
+  o.s = 2;
+  o.max_itn = 1;
+  o.trunc_tol = trunc_tol;
+  Solver<T> S;
+  S.setup(ctx, A, o, R->k);
+  S.refresh((const T *)R->U, (const T *)R->Ut, R->k);
+  const int k = S.cur.k;
+  *k_out = k;
+  const int64_t n = A->n;
+  const size_t vb = sizeof(T) * n;
+  copy_in(S.z, z, vb, on_device, ctx->stream);
+  copy_in(S.zt, zt, vb, on_device, ctx->stream);
+  std::vector<ColDesc> X, Y{{S.z, 1}, {S.zt, 1}};
+  for (int c = 0; c < k; ++c) X.push_back(Solver<T>::col(S.cur.Ct, c, k));
+  for (int c = 0; c < k; ++c) X.push_back(Solver<T>::col(S.cur.C, c, k));
+  std::vector<cplx> G;
+  gram<T>(X, Y, n, G, ctx);
+  std::vector<T> hz(k), hzt(k);
+  for (int j = 0; j < k; ++j) {
+    hz[j] = fromc<T>(G[(size_t)j * 2 + 0] / S.cur.d[j]);
+    hzt[j] = fromc<T>(G[(size_t)(k + j) * 2 + 1] / S.cur.d[j]);
+  }
+  if (k) {
+    memcpy(zeta, hz.data(), sizeof(T) * k);
+    memcpy(zetat, hzt.data(), sizeof(T) * k);
+  }
+  if (d)
+    for (int j = 0; j < k; ++j) d[j] = S.cur.d[j];
+  T *tmp = S.z;   // reuse as scratch for column-major export of one block at a time
+  (void)tmp;
+  const T *src[4] = {S.cur.U, S.cur.Ut, S.cur.C, S.cur.Ct};
+  void *dst[4] = {U, Ut, C, Ct};
+  if (k) {
+    T *cm = (T *)ws_alloc(sizeof(T) * n * k);
+    for (int q = 0; q < 4; ++q) {
+      if (!dst[q]) continue;
+      k_rm_to_cm<T><<<g1(n * k), 256, 0, ctx->stream>>>(src[q], cm, n, k);
+      count_launch();
+      copy_out(dst[q], cm, sizeof(T) * n * k, on_device, ctx->stream);
+    }
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    ws_free(cm);
+  }
+}
+
+int rbicg_dbg_project(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, double trunc_tol,
+                      const void *z, const void *zt, void *zeta, void *zetat, int32_t *k_out, void *U,
+                      void *Ut, void *C, void *Ct, double *d, int on_device) {
+  if (!ctx || !A || !R || !z || !zt || !zeta || !zetat || !k_out) return RBICG_EINVAL;
+  return run_guarded([&] {
+    if (A->dtype == RBICG_F64)
+      project_t<double>(ctx, A, R, trunc_tol, z, zt, zeta, zetat, k_out, U, Ut, C, Ct, d, on_device);
+    else
+      project_t<zc>(ctx, A, R, trunc_tol, z, zt, zeta, zetat, k_out, U, Ut, C, Ct, d, on_device);
+  });
+}
+
+template <typename T>
+__global__ void k_fill_probe(T *v, int64_t n, double phase) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    T t = zero<T>();
+    reinterpret_cast<double *>(&t)[0] = sin(0.37 * (double)i + phase);
+    v[i] = t;
+  }
+}
+
+template <typename T>
+static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbicg_opts *opts, int iters,
+                    double *ms) {
+  rbicg_opts o = *opts;
+  o.force_iters = iters + 1;
+  o.max_itn = iters + 1;
+  Solver<T> S;
+  const int kin = R ? R->k : 0;
+  S.setup(ctx, A, o, kin);
+  const int64_t n = A->n;
+  k_fill_probe<T><<<g1(n), 256, 0, ctx->stream>>>(S.b, n, 0.1);
+  k_fill_probe<T><<<g1(n), 256, 0, ctx->stream>>>(S.bt, n, 0.7);
+  count_launch(2);
+  RB_CUDA(cudaMemsetAsync(S.x, 0, sizeof(T) * n, ctx->stream));
+  RB_CUDA(cudaMemsetAsync(S.xt, 0, sizeof(T) * n, ctx->stream));
+  RB_CUDA(cudaMemsetAsync(S.p[0], 0, sizeof(T) * n, ctx->stream));
+  RB_CUDA(cudaMemsetAsync(S.pt[0], 0, sizeof(T) * n, ctx->stream));
+  S.refresh(kin ? (const T *)R->U : nullptr, kin ? (const T *)R->Ut : nullptr, opts->k > 0 ? kin : 0);
+  S.make_args();
+  S.init_state();
+  S.hst->stop_at = 1 << 30;
+  S.push();
+  S.initial_projection();
+  S.hst->stop_at = 1 << 30;
+  S.hst->done = 0;
+  S.push();
+  cudaEvent_t ev[3];
+  for (auto &e : ev) RB_CUDA(cudaEventCreate(&e));
+  double t1 = 0, t2 = 0;
+  for (int i = 0; i < iters; ++i) {
+    RB_CUDA(cudaEventRecord(ev[0], ctx->stream));
+    launch_pass1<T>(S.la, ctx->stream);
+    RB_CUDA(cudaEventRecord(ev[1], ctx->stream));
+    launch_pass2<T>(S.la, ctx->stream);
+    RB_CUDA(cudaEventRecord(ev[2], ctx->stream));
+    RB_CUDA(cudaEventSynchronize(ev[2]));
+    float a = 0, b = 0;
+    RB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    RB_CUDA(cudaEventElapsedTime(&b, ev[1], ev[2]));
+    t1 += a;
+    t2 += b;
+  }
+  S.pull();
+  for (auto &e : ev) cudaEventDestroy(e);
+  ms[0] = t1 / std::max(iters, 1);
+  ms[1] = t2 / std::max(iters, 1);
+  ms[2] = S.hst->done;   // 0 means every timed kernel did full work
+  ms[3] = S.cur.k;
+}
+
+int rbicg_dbg_time_kernels(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbicg_opts *opts,
+                           int iters, double *ms) {
+  if (!ctx || !A || !opts || !ms || iters <= 0) return RBICG_EINVAL;
+  return run_guarded([&] {
+    if (A->dtype == RBICG_F64) time_t_<double>(ctx, A, R, opts, iters, ms);
+    else time_t_<zc>(ctx, A, R, opts, iters, ms);
+  });
+}
+

@@ -1,0 +1,214 @@
+// blocks.cu -- cycle-end / per-system block kernels.
+//
+//   spmm         C = A U, C~ = A^* Ũ (k columns, row-major n x k)
+//   gram         G = X^H Y for column lists X, Y (the pencil Grams
+//                Ψ~^*Ψ, Ψ~^*Φ of finalGenEigValue, and C~^*C)
+//   gemm_panels  out = [columns] M (U_j = Φ_j W_j N_j etc.)
+//
+// The Gram is a two-stage deterministic reduction: blocks own a 32 x 32
+// output tile and a chunk of rows; the per-chunk partials are summed in chunk
+// order by a second kernel.
+#include "internal.h"
+
+namespace rbicg {
+
+template <typename T> __device__ __forceinline__ T ldp(const void *p, int64_t i) {
+  return reinterpret_cast<const T *>(p)[i];
+}
+
+// ------------------------------------------------------------------ SpMM
+template <typename T>
+__global__ void __launch_bounds__(256) k_spmm(DevMat A, const T *__restrict__ X, T *__restrict__ Y,
+                                              int k) {
+  const int64_t total = A.n * k;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx / k;
+    const int j = (int)(idx - row * k);
+    const int64_t sl = row >> 5;
+    const int lane = (int)(row & 31);
+    const int64_t off = A.sptr[sl];
+    const int w = (int)((A.sptr[sl + 1] - off) >> 5);
+    T acc = zero<T>();
+    for (int jj = 0; jj < w; ++jj) {
+      const int c = A.cols[off + jj * 32 + lane];
+      const T v = reinterpret_cast<const T *>(A.vals)[off + jj * 32 + lane];
+      acc = mad(v, X[(int64_t)c * k + j], acc);
+    }
+    Y[idx] = acc;
+  }
+}
+
+template <typename T> void launch_spmm(const DevMat &A, const T *X, T *Y, int k, cudaStream_t s) {
+  if (k <= 0) return;
+  const int64_t total = A.n * k;
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_spmm<T><<<grid, 256, 0, s>>>(A, X, Y, k);
+  count_launch();
+}
+
+// ------------------------------------------------------------------ Gram
+constexpr int GT = 32;   // output tile edge
+constexpr int GR = 32;   // rows per smem sub-tile
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_gram(const ColDesc *__restrict__ X, int mX,
+                                              const ColDesc *__restrict__ Y, int mY, int64_t n,
+                                              int64_t chunk, T *__restrict__ part) {
+  __shared__ T sx[GR][GT + 1];
+  __shared__ T sy[GR][GT + 1];
+  const int tilesY = (mY + GT - 1) / GT;
+  const int tx0 = (blockIdx.x / tilesY) * GT, ty0 = (blockIdx.x % tilesY) * GT;
+  const int64_t r0 = (int64_t)blockIdx.y * chunk;
+  const int64_t r1 = min(n, r0 + chunk);
+  const int tid = threadIdx.x;
+  // each thread: 2 x 2 outputs (a = ta + 16*u, b = tb + 16*v)
+  const int ta = tid / 16, tb = tid % 16;
+  T acc[2][2] = {{zero<T>(), zero<T>()}, {zero<T>(), zero<T>()}};
+  for (int64_t rb = r0; rb < r1; rb += GR) {
+    // load: rr fastest (coalesced for vector columns)
+    for (int e = tid; e < GR * GT; e += 256) {
+      const int rr = e % GR, cc = e / GR;
+      const int64_t row = rb + rr;
+      T vx = zero<T>(), vy = zero<T>();
+      if (row < r1) {
+        if (tx0 + cc < mX) vx = conj(ldp<T>(X[tx0 + cc].p, row * X[tx0 + cc].stride));
+        if (ty0 + cc < mY) vy = ldp<T>(Y[ty0 + cc].p, row * Y[ty0 + cc].stride);
+      }
+      sx[rr][cc] = vx;
+      sy[rr][cc] = vy;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < GR; ++rr) {
+      const T x0 = sx[rr][ta], x1 = sx[rr][ta + 16];
+      const T y0 = sy[rr][tb], y1 = sy[rr][tb + 16];
+      acc[0][0] = mad(x0, y0, acc[0][0]);
+      acc[0][1] = mad(x0, y1, acc[0][1]);
+      acc[1][0] = mad(x1, y0, acc[1][0]);
+      acc[1][1] = mad(x1, y1, acc[1][1]);
+    }
+    __syncthreads();
+  }
+  for (int u = 0; u < 2; ++u)
+    for (int v = 0; v < 2; ++v) {
+      const int a = tx0 + ta + 16 * u, b = ty0 + tb + 16 * v;
+      if (a < mX && b < mY) part[((int64_t)blockIdx.y * mX + a) * mY + b] = acc[u][v];
+    }
+}
+
+template <typename T>
+__global__ void k_gram_reduce(const T *__restrict__ part, int nchunks, int mXY, T *__restrict__ G) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= mXY) return;
+  T s = zero<T>();
+  for (int c = 0; c < nchunks; ++c) s = add(s, part[(int64_t)c * mXY + i]);
+  G[i] = s;
+}
+
+template <typename T>
+void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
+          std::vector<cplx> &G, rbicg_ctx *ctx) {
+  const int mX = (int)X.size(), mY = (int)Y.size();
+  G.assign((size_t)mX * mY, cplx(0, 0));
+  if (mX == 0 || mY == 0) return;
+  const int tiles = ((mX + GT - 1) / GT) * ((mY + GT - 1) / GT);
+  int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096,
+                                                            (2 * ctx->nsm + tiles - 1) / tiles * 2));
+  const int64_t chunk = ((n + nchunks - 1) / nchunks + GR - 1) / GR * GR;
+  nchunks = (int)((n + chunk - 1) / chunk);
+  const size_t desc_bytes = sizeof(ColDesc) * (mX + mY);
+  const size_t part_bytes = sizeof(T) * (size_t)nchunks * mX * mY;
+  const size_t g_bytes = sizeof(T) * (size_t)mX * mY;
+  char *buf = (char *)ws_alloc(desc_bytes + part_bytes + g_bytes + 64);
+  ColDesc *dX = (ColDesc *)buf;
+  T *dpart = (T *)(buf + ((desc_bytes + 15) / 16) * 16);
+  T *dG = dpart + (size_t)nchunks * mX * mY;
+  std::vector<ColDesc> both(X);
+  both.insert(both.end(), Y.begin(), Y.end());
+  RB_CUDA(cudaMemcpyAsync(dX, both.data(), desc_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  dim3 grid(tiles, nchunks);
+  k_gram<T><<<grid, 256, 0, ctx->stream>>>(dX, mX, dX + mX, mY, n, chunk, dpart);
+  k_gram_reduce<T><<<(mX * mY + 255) / 256, 256, 0, ctx->stream>>>(dpart, nchunks, mX * mY, dG);
+  count_launch(2);
+  std::vector<T> h((size_t)mX * mY);
+  RB_CUDA(cudaMemcpyAsync(h.data(), dG, g_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  ws_free(buf);
+  for (size_t i = 0; i < h.size(); ++i) G[i] = cplx(re(h[i]), im(h[i]));
+}
+
+// ------------------------------------------------------------------ panels x M
+// out[row, c] = Σ_a X_a[row] M[a, c]; one thread per row keeps the whole output
+// row in registers, so out may alias an input panel with the same layout.
+template <typename T>
+__global__ void __launch_bounds__(128) k_gemm_panels(const ColDesc *__restrict__ X, int mX,
+                                                     const T *__restrict__ M, int p, int64_t n,
+                                                     T *out) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  T *sM = reinterpret_cast<T *>(sm_raw);
+  for (int e = threadIdx.x; e < mX * p; e += blockDim.x) sM[e] = M[e];
+  __syncthreads();
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    T acc[KMAX];
+#pragma unroll
+    for (int c = 0; c < KMAX; ++c) acc[c] = zero<T>();
+    for (int a = 0; a < mX; ++a) {
+      const T xv = ldp<T>(X[a].p, row * X[a].stride);
+#pragma unroll
+      for (int c = 0; c < KMAX; ++c)
+        if (c < p) acc[c] = mad(xv, sM[a * p + c], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < KMAX; ++c)
+      if (c < p) out[row * p + c] = acc[c];
+  }
+}
+
+template <typename T>
+void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int p, int64_t n,
+                 T *out, rbicg_ctx *ctx) {
+  const int mX = (int)X.size();
+  if (p <= 0) return;
+  RB_CHECK(p <= KMAX, RBICG_EINVAL);
+  std::vector<T> hM((size_t)mX * p);
+  for (size_t i = 0; i < hM.size(); ++i) {
+    T v = zero<T>();
+    reinterpret_cast<double *>(&v)[0] = M[i].real();
+    if (sizeof(T) == 16) reinterpret_cast<double *>(&v)[1] = M[i].imag();
+    hM[i] = v;
+  }
+  const size_t desc_bytes = sizeof(ColDesc) * std::max(mX, 1);
+  const size_t m_bytes = sizeof(T) * std::max<size_t>(hM.size(), 1);
+  char *buf = (char *)ws_alloc(desc_bytes + m_bytes + 32);
+  ColDesc *dX = (ColDesc *)buf;
+  T *dM = (T *)(buf + ((desc_bytes + 15) / 16) * 16);
+  if (mX) {
+    RB_CUDA(cudaMemcpyAsync(dX, X.data(), sizeof(ColDesc) * mX, cudaMemcpyHostToDevice, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(dM, hM.data(), sizeof(T) * hM.size(), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  const size_t sm = sizeof(T) * (size_t)mX * p;
+  RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
+  const int grid = (int)std::min<int64_t>((n + 127) / 128, (int64_t)ctx->nsm * 8);
+  k_gemm_panels<T><<<grid, 128, sm, ctx->stream>>>(dX, mX, dM, p, n, out);
+  count_launch();
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  ws_free(buf);
+}
+
+void prepare_block_kernels() {
+  RB_CUDA(cudaFuncSetAttribute(k_gemm_panels<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_gemm_panels<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+}
+
+#define RB_BINST(T)                                                                        \
+  template void launch_spmm<T>(const DevMat &, const T *, T *, int, cudaStream_t);         \
+  template void gram<T>(const std::vector<ColDesc> &, const std::vector<ColDesc> &, int64_t, \
+                        std::vector<cplx> &, rbicg_ctx *);                                 \
+  template void gemm_panels<T>(const std::vector<ColDesc> &, const std::vector<cplx> &, int, \
+                               int64_t, T *, rbicg_ctx *);
+RB_BINST(double)
+RB_BINST(zc)
+
+}  // namespace rbicg

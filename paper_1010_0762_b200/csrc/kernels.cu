@@ -1,0 +1,615 @@
+// kernels.cu -- the RBiCG hot loop on sm_100a (Algorithm 2).
+//
+// One iteration = two persistent streaming kernels, each ending in a
+// deterministic grid reduction done by the last block to finish:
+//
+//   pass 1  p_i = r_{i-1} + β_{i-1} p_{i-1},  p~_i = r~_{i-1} + β̄ p~_{i-1}
+//           z_i = A p_i,  z~_i = A^* p~_i          (SELL-32 SpMV pair, the
+//           direction update fused into the gather)
+//           partial sums of C~^*z, C^*z~, C^*p~, p~^*z  (oblique-projection
+//           coefficients; σ_i via reading Q23)
+//           last block: ζ = D_c^{-1}C~^*z, ζ~ = D_c^{-1}C^*z~,
+//                       σ = p~^*z - (C^*p~)^*ζ, α = ρ/σ, ζ_c += αζ, ...
+//   pass 2  q = z - Cζ, q~ = z~ - C~ζ~; x += αp; x~ += ᾱp~;
+//           r_i = r_{i-1} - αq (written straight into the Lanczos ring
+//           column i), r~_i likewise; partial ρ_i, ||r||², ||r~||²
+//           last block: β_i = ρ_i/ρ_{i-1}, stop test (Q2), breakdown (Q3),
+//           iteration record for the cycle-end control.
+//
+// Kernels read the iteration index from the device state, so one captured
+// CUDA graph of s iterations is replayed for every cycle; once the state says
+// done/paused every kernel is a no-op (exact iteration counts, no host poll).
+#include "internal.h"
+
+namespace rbicg {
+
+std::atomic<int64_t> g_launches{0};
+
+template <typename T> __device__ __forceinline__ T ldg(const T *p);
+template <> __device__ __forceinline__ double ldg<double>(const double *p) { return __ldg(p); }
+template <> __device__ __forceinline__ zc ldg<zc>(const zc *p) {
+  double2 v = __ldg(reinterpret_cast<const double2 *>(p));
+  return mk(v.x, v.y);
+}
+// streaming (evict-first) loads for data touched once per pass
+template <typename T> __device__ __forceinline__ T ldcs(const T *p);
+template <> __device__ __forceinline__ double ldcs<double>(const double *p) { return __ldcs(p); }
+template <> __device__ __forceinline__ zc ldcs<zc>(const zc *p) {
+  double2 v = __ldcs(reinterpret_cast<const double2 *>(p));
+  return mk(v.x, v.y);
+}
+
+// y_row = Σ_j a_{row,j} (r_j + β p_j)   (FUSE)   or   Σ_j a_{row,j} p_j
+template <typename T, bool FUSE>
+__device__ __forceinline__ T sell_row(const DevMat &M, int64_t row, const T *__restrict__ r,
+                                      const T *__restrict__ p, T beta) {
+  const int64_t sl = row >> 5;
+  const int lane = (int)(row & 31);
+  const int64_t off = M.sptr[sl];
+  const int w = (int)((M.sptr[sl + 1] - off) >> 5);
+  const int32_t *__restrict__ cols = M.cols + off + lane;
+  const T *__restrict__ vals = reinterpret_cast<const T *>(M.vals) + off + lane;
+  T acc = zero<T>();
+#pragma unroll 4
+  for (int jj = 0; jj < w; ++jj) {
+    const int c = __ldcs(cols + jj * 32);
+    const T v = ldcs(vals + jj * 32);
+    T pj;
+    if (FUSE) pj = mad(beta, ldg(p + c), ldg(r + c));
+    else pj = ldg(p + c);
+    acc = mad(v, pj, acc);
+  }
+  return acc;
+}
+
+// Deterministic block sum (fixed shuffle tree + fixed warp order). Valid in
+// thread 0.  sbuf needs BS/32 entries.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T *sbuf) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sbuf[w] = v;
+  __syncthreads();
+  T r = zero<T>();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < BS / 32; ++i) r = add(r, sbuf[i]);
+  return r;
+}
+
+// Last-block election; returns true in every thread of the last block.
+__device__ __forceinline__ bool last_block(unsigned *cnt, int *s_flag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned v = atomicAdd(cnt, 1u);
+    *s_flag = (v == gridDim.x - 1);
+  }
+  __syncthreads();
+  return *s_flag != 0;
+}
+
+// Final fixed-order reduction of `nout` outputs stored as part[o*G + b].
+template <typename T>
+__device__ __forceinline__ void final_reduce(const T *part, int nout, int G, T *s_fin) {
+  __threadfence();
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int o = w; o < nout; o += BS / 32) {
+    T acc = zero<T>();
+    for (int b = l; b < G; b += 32) acc = add(acc, ldcg(part + (int64_t)o * G + b));
+    acc = warp_sum(acc);
+    if (l == 0) s_fin[o] = acc;
+  }
+  __syncthreads();
+}
+
+// ============================================================== pass 1
+template <typename T>
+__global__ void __launch_bounds__(BS) k_pass1(LoopArgs<T> a) {
+  __shared__ T s_z[BS], s_zt[BS], s_pt[BS];
+  __shared__ T s_red[3 * BS];
+  __shared__ T s_fin[3 * KMAX + 1];
+  __shared__ T s_w[BS / 32];
+  __shared__ int s_last;
+  DevState<T> *st = a.st;
+  if (st->done) return;
+  const int tid = threadIdx.x;
+  const int it = st->iter;
+  const T beta = st->beta;
+  const T cb = conj(beta);
+  const int64_t n = a.n;
+  const T *__restrict__ r = a.rring + (int64_t)(it % a.ring) * n;
+  const T *__restrict__ rt = a.rtring + (int64_t)(it % a.ring) * n;
+  const T *__restrict__ pold = a.p[it & 1];
+  const T *__restrict__ ptold = a.pt[it & 1];
+  T *__restrict__ pnew = a.p[(it + 1) & 1];
+  T *__restrict__ ptnew = a.pt[(it + 1) & 1];
+  const int k = a.k;
+  const int rstep = k > 0 ? BS / k : 0;
+  const int kt = rstep * k;
+  T a1 = zero<T>(), a2 = zero<T>(), a3 = zero<T>(), aptz = zero<T>();
+  const int64_t ntiles = (n + BS - 1) / BS;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * BS;
+    const int rows = (int)min((int64_t)BS, n - row0);
+    if (tid < rows) {
+      const int64_t row = row0 + tid;
+      const T z = sell_row<T, true>(a.A, row, r, pold, beta);
+      const T zt = sell_row<T, true>(a.AH, row, rt, ptold, cb);
+      const T pn = mad(beta, ldg(pold + row), ldg(r + row));
+      const T ptn = mad(cb, ldg(ptold + row), ldg(rt + row));
+      pnew[row] = pn;
+      ptnew[row] = ptn;
+      a.z[row] = z;
+      a.zt[row] = zt;
+      aptz = cmad(ptn, z, aptz);
+      s_z[tid] = z;
+      s_zt[tid] = zt;
+      s_pt[tid] = ptn;
+    }
+    if (k > 0) {
+      __syncthreads();
+      if (tid < kt) {
+        // thread tid always meets column tid % k because kt is a multiple of k
+        const int nel = rows * k;
+        const T *__restrict__ Ct = a.Ct + row0 * k;
+        const T *__restrict__ C = a.C + row0 * k;
+        int lr = tid / k;
+        for (int e = tid; e < nel; e += kt, lr += rstep) {
+          const T ct = ldcs(Ct + e), c = ldcs(C + e);
+          a1 = cmad(ct, s_z[lr], a1);   // conj(c~_{row,j}) z_row
+          a2 = cmad(c, s_zt[lr], a2);   // conj(c_{row,j}) z~_row
+          a3 = cmad(c, s_pt[lr], a3);   // conj(c_{row,j}) p~_row
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---- block reduction, fixed order
+  const int G = gridDim.x;
+  const int nout = 3 * k + 1;
+  if (k > 0) {
+    s_red[tid] = tid < kt ? a1 : zero<T>();
+    s_red[BS + tid] = tid < kt ? a2 : zero<T>();
+    s_red[2 * BS + tid] = tid < kt ? a3 : zero<T>();
+  }
+  const T bptz = block_sum(aptz, s_w);   // contains __syncthreads
+  if (tid < 3 * k) {
+    const int ty = tid / k, j = tid % k;
+    T s = zero<T>();
+    for (int m = 0; m < rstep; ++m) s = add(s, s_red[ty * BS + j + m * k]);
+    a.part[(int64_t)tid * G + blockIdx.x] = s;
+  }
+  if (tid == 0) a.part[(int64_t)(3 * k) * G + blockIdx.x] = bptz;
+  if (!last_block(&st->cnt[0], &s_last)) return;
+  final_reduce(a.part, nout, G, s_fin);
+  if (tid == 0) {
+    st->cnt[0] = 0;
+    const int i = it + 1;
+    T sigma = s_fin[3 * k];
+    T zeta[KMAX], zetat[KMAX];
+    for (int j = 0; j < k; ++j) {
+      zeta[j] = scal(st->dinv[j], s_fin[j]);          // ζ_i = D_c^{-1} C~^* z_i
+      zetat[j] = scal(st->dinv[j], s_fin[k + j]);     // ζ~_i = D_c^{-1} C^* z~_i
+      sigma = sub(sigma, cmul(s_fin[2 * k + j], zeta[j]));  // (p~, z - Cζ)
+    }
+    const T alpha = divd(st->rho, sigma);
+    if (iszero(sigma) || !finite(alpha)) {   // breakdown of the second kind
+      st->status = RBICG_BREAKDOWN_SECOND;
+      st->done = 1;
+      return;
+    }
+    st->alpha = alpha;
+    st->sigma = sigma;
+    const T ca = conj(alpha);
+    for (int j = 0; j < k; ++j) {
+      st->zeta[j] = zeta[j];
+      st->zetat[j] = zetat[j];
+      st->zc[j] = mad(alpha, zeta[j], st->zc[j]);
+      st->ztc[j] = mad(ca, zetat[j], st->ztc[j]);
+      a.zhist[(int64_t)i * k + j] = zeta[j];
+      a.zthist[(int64_t)i * k + j] = zetat[j];
+    }
+  }
+}
+
+// ============================================================== pass 2
+template <typename T>
+__global__ void __launch_bounds__(BS) k_pass2(LoopArgs<T> a, int staged) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ T s_zeta[KMAX], s_zetat[KMAX];
+  __shared__ T s_w[BS / 32];
+  __shared__ T s_fin[3];
+  __shared__ int s_last;
+  DevState<T> *st = a.st;
+  if (st->done) return;
+  const int tid = threadIdx.x;
+  const int it = st->iter;
+  const int k = a.k;
+  const T alpha = st->alpha;
+  const T ca = conj(alpha);
+  if (tid < k) {
+    s_zeta[tid] = st->zeta[tid];
+    s_zetat[tid] = st->zetat[tid];
+  }
+  __syncthreads();
+  const int64_t n = a.n;
+  const T *__restrict__ rold = a.rring + (int64_t)(it % a.ring) * n;
+  const T *__restrict__ rtold = a.rtring + (int64_t)(it % a.ring) * n;
+  T *__restrict__ rnew = a.rring + (int64_t)((it + 1) % a.ring) * n;
+  T *__restrict__ rtnew = a.rtring + (int64_t)((it + 1) % a.ring) * n;
+  const T *__restrict__ pn = a.p[(it + 1) & 1];
+  const T *__restrict__ ptn = a.pt[(it + 1) & 1];
+  T *sC = reinterpret_cast<T *>(smem_raw);
+  T *sCt = sC + BS * k;
+  T arho = zero<T>();
+  double an = 0.0, ant = 0.0;
+  const int64_t ntiles = (n + BS - 1) / BS;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * BS;
+    const int rows = (int)min((int64_t)BS, n - row0);
+    if (k > 0 && staged) {
+      const T *__restrict__ C = a.C + row0 * k;
+      const T *__restrict__ Ct = a.Ct + row0 * k;
+      const int nel = rows * k;
+      for (int e = tid; e < nel; e += BS) {
+        sC[e] = ldcs(C + e);
+        sCt[e] = ldcs(Ct + e);
+      }
+      __syncthreads();
+    }
+    if (tid < rows) {
+      const int64_t row = row0 + tid;
+      T q = ldcs(a.z + row), qt = ldcs(a.zt + row);
+      if (k > 0) {
+        const T *cr = staged ? sC + tid * k : a.C + row * k;
+        const T *ctr = staged ? sCt + tid * k : a.Ct + row * k;
+        T d = zero<T>(), dt = zero<T>();
+        for (int j = 0; j < k; ++j) {
+          d = mad(cr[j], s_zeta[j], d);
+          dt = mad(ctr[j], s_zetat[j], dt);
+        }
+        q = sub(q, d);     // q_i = z_i - C ζ_i
+        qt = sub(qt, dt);  // q~_i = z~_i - C~ ζ~_i
+      }
+      a.x[row] = mad(alpha, ldg(pn + row), a.x[row]);
+      a.xt[row] = mad(ca, ldg(ptn + row), a.xt[row]);
+      const T rn = sub(ldcs(rold + row), mul(alpha, q));
+      const T rtn = sub(ldcs(rtold + row), mul(ca, qt));
+      rnew[row] = rn;
+      rtnew[row] = rtn;
+      arho = cmad(rtn, rn, arho);
+      an += abs2(rn);
+      ant += abs2(rtn);
+    }
+    if (k > 0 && staged) __syncthreads();
+  }
+  const int G = gridDim.x;
+  const T b0 = block_sum(arho, s_w);
+  double b1 = block_sum(an, reinterpret_cast<double *>(s_w));
+  double b2 = block_sum(ant, reinterpret_cast<double *>(s_w));
+  if (tid == 0) {
+    a.part[blockIdx.x] = b0;
+    T t1 = zero<T>(), t2 = zero<T>();
+    reinterpret_cast<double *>(&t1)[0] = b1;
+    reinterpret_cast<double *>(&t2)[0] = b2;
+    a.part[G + blockIdx.x] = t1;
+    a.part[2 * G + blockIdx.x] = t2;
+  }
+  if (!last_block(&st->cnt[1], &s_last)) return;
+  final_reduce(a.part, 3, G, s_fin);
+  if (tid == 0) {
+    st->cnt[1] = 0;
+    const int i = it + 1;
+    const T rho = s_fin[0];
+    const double rn = sqrt(re(s_fin[1])), rtn = sqrt(re(s_fin[2]));
+    const T beta = divd(rho, st->rho);   // β_i = ρ_i / ρ_{i-1}
+    IterRec<T> rec;
+    rec.alpha = alpha;
+    rec.beta = beta;
+    rec.rho = rho;
+    rec.sigma = st->sigma;
+    rec.rnorm = rn;
+    rec.rtnorm = rtn;
+    a.hist[i] = rec;
+    st->iter = i;
+    st->rnorm = rn;
+    st->rtnorm = rtn;
+    const bool conv = !st->force && rn <= st->tolb && rtn <= st->tolbt;
+    if (conv) {
+      st->done = 1;
+      st->status = RBICG_OK;
+    } else if (iszero(rho) || !finite(beta)) {
+      st->done = 1;
+      st->status = RBICG_BREAKDOWN_SERIOUS;
+    } else if (i >= st->max_itn) {
+      st->done = 1;
+      st->status = st->force ? RBICG_OK : RBICG_MAXITER;
+    } else if (i == st->stop_at) {
+      st->done = 2;   // paused at a cycle boundary for the recycle update
+    }
+    st->rho = rho;
+    st->beta = beta;
+  }
+}
+
+// ============================================================== init / finish
+// r = b - A x, r~ = b~ - A^* x~; partial ||b||², ||b~||², ||r||², ||r~||² and,
+// with coef, C~^*r and C^*r~ (minusXR).
+template <typename T>
+__global__ void __launch_bounds__(BS) k_resid(LoopArgs<T> a, const T *b, const T *bt, const T *x,
+                                              const T *xt, T *r, T *rt, int coef) {
+  __shared__ T s_r[BS], s_rt[BS];
+  __shared__ T s_red[2 * BS];
+  __shared__ T s_w[BS / 32];
+  __shared__ T s_fin[4 + 2 * KMAX];
+  __shared__ int s_last;
+  DevState<T> *st = a.st;
+  const int tid = threadIdx.x;
+  const int64_t n = a.n;
+  const int k = coef ? a.k : 0;
+  const int rstep = k > 0 ? BS / k : 0;
+  const int kt = rstep * k;
+  double nb = 0, nbt = 0, nr = 0, nrt = 0;
+  T a1 = zero<T>(), a2 = zero<T>();
+  const int64_t ntiles = (n + BS - 1) / BS;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * BS;
+    const int rows = (int)min((int64_t)BS, n - row0);
+    if (tid < rows) {
+      const int64_t row = row0 + tid;
+      const T bv = b[row], btv = bt[row];
+      const T rv = sub(bv, sell_row<T, false>(a.A, row, nullptr, x, zero<T>()));
+      const T rtv = sub(btv, sell_row<T, false>(a.AH, row, nullptr, xt, zero<T>()));
+      r[row] = rv;
+      rt[row] = rtv;
+      nb += abs2(bv);
+      nbt += abs2(btv);
+      nr += abs2(rv);
+      nrt += abs2(rtv);
+      s_r[tid] = rv;
+      s_rt[tid] = rtv;
+    }
+    if (k > 0) {
+      __syncthreads();
+      if (tid < kt) {
+        const int nel = rows * k;
+        const T *Ct = a.Ct + row0 * k;
+        const T *C = a.C + row0 * k;
+        int lr = tid / k;
+        for (int e = tid; e < nel; e += kt, lr += rstep) {
+          a1 = cmad(Ct[e], s_r[lr], a1);
+          a2 = cmad(C[e], s_rt[lr], a2);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const int G = gridDim.x;
+  if (k > 0) {
+    s_red[tid] = tid < kt ? a1 : zero<T>();
+    s_red[BS + tid] = tid < kt ? a2 : zero<T>();
+  }
+  double sums[4] = {nb, nbt, nr, nrt};
+  for (int q = 0; q < 4; ++q) {
+    double v = block_sum(sums[q], reinterpret_cast<double *>(s_w));
+    if (tid == 0) {
+      T t = zero<T>();
+      reinterpret_cast<double *>(&t)[0] = v;
+      a.part[(int64_t)q * G + blockIdx.x] = t;
+    }
+  }
+  if (tid < 2 * k) {
+    const int ty = tid / k, j = tid % k;
+    T s = zero<T>();
+    for (int m = 0; m < rstep; ++m) s = add(s, s_red[ty * BS + j + m * k]);
+    a.part[(int64_t)(4 + tid) * G + blockIdx.x] = s;
+  }
+  if (!last_block(&st->cnt[2], &s_last)) return;
+  final_reduce(a.part, 4 + 2 * k, G, s_fin);
+  if (tid == 0) {
+    st->cnt[2] = 0;
+    st->bn2 = re(s_fin[0]);
+    st->btn2 = re(s_fin[1]);
+    st->rn2 = re(s_fin[2]);
+    st->rtn2 = re(s_fin[3]);
+    for (int j = 0; j < k; ++j) {
+      st->g[j] = scal(st->dinv[j], s_fin[4 + j]);       // Ĉ^* r_{-1}
+      st->gt[j] = scal(st->dinv[j], s_fin[4 + k + j]);  // Č^* r~_{-1}
+    }
+  }
+}
+
+// x_0 = x_{-1} + U g, r_0 = r_{-1} - C g (and duals); ρ_0, norms; state reset.
+template <typename T>
+__global__ void __launch_bounds__(BS) k_init2(LoopArgs<T> a, const T *U, const T *Ut) {
+  __shared__ T s_g[KMAX], s_gt[KMAX];
+  __shared__ T s_w[BS / 32];
+  __shared__ T s_fin[3];
+  __shared__ int s_last;
+  DevState<T> *st = a.st;
+  const int tid = threadIdx.x;
+  const int k = a.k;
+  if (tid < k) {
+    s_g[tid] = st->g[tid];
+    s_gt[tid] = st->gt[tid];
+  }
+  __syncthreads();
+  const int64_t n = a.n;
+  T *r = a.rring;   // ring column 0 holds r_{-1} -> r_0
+  T *rt = a.rtring;
+  T arho = zero<T>();
+  double an = 0, ant = 0;
+  for (int64_t row = (int64_t)blockIdx.x * BS + tid; row < n; row += (int64_t)gridDim.x * BS) {
+    T rv = r[row], rtv = rt[row], xv = a.x[row], xtv = a.xt[row];
+    if (k > 0) {
+      T du = zero<T>(), dc = zero<T>(), dut = zero<T>(), dct = zero<T>();
+      for (int j = 0; j < k; ++j) {
+        du = mad(U[row * k + j], s_g[j], du);
+        dc = mad(a.C[row * k + j], s_g[j], dc);
+        dut = mad(Ut[row * k + j], s_gt[j], dut);
+        dct = mad(a.Ct[row * k + j], s_gt[j], dct);
+      }
+      xv = add(xv, du);
+      rv = sub(rv, dc);
+      xtv = add(xtv, dut);
+      rtv = sub(rtv, dct);
+      a.x[row] = xv;
+      a.xt[row] = xtv;
+      r[row] = rv;
+      rt[row] = rtv;
+    }
+    arho = cmad(rtv, rv, arho);
+    an += abs2(rv);
+    ant += abs2(rtv);
+  }
+  const int G = gridDim.x;
+  const T b0 = block_sum(arho, s_w);
+  double b1 = block_sum(an, reinterpret_cast<double *>(s_w));
+  double b2 = block_sum(ant, reinterpret_cast<double *>(s_w));
+  if (tid == 0) {
+    a.part[blockIdx.x] = b0;
+    T t1 = zero<T>(), t2 = zero<T>();
+    reinterpret_cast<double *>(&t1)[0] = b1;
+    reinterpret_cast<double *>(&t2)[0] = b2;
+    a.part[G + blockIdx.x] = t1;
+    a.part[2 * G + blockIdx.x] = t2;
+  }
+  if (!last_block(&st->cnt[3], &s_last)) return;
+  final_reduce(a.part, 3, G, s_fin);
+  if (tid == 0) {
+    st->cnt[3] = 0;
+    const T rho = s_fin[0];
+    const double rn = sqrt(re(s_fin[1])), rtn = sqrt(re(s_fin[2]));
+    st->rho = rho;
+    st->beta = zero<T>();
+    st->alpha = zero<T>();
+    st->sigma = zero<T>();
+    st->iter = 0;
+    st->rnorm = rn;
+    st->rtnorm = rtn;
+    for (int j = 0; j < KMAX; ++j) {
+      st->zc[j] = zero<T>();
+      st->ztc[j] = zero<T>();
+    }
+    IterRec<T> rec;
+    rec.alpha = zero<T>();
+    rec.beta = zero<T>();
+    rec.rho = rho;
+    rec.sigma = zero<T>();
+    rec.rnorm = rn;
+    rec.rtnorm = rtn;
+    a.hist[0] = rec;
+    st->status = RBICG_OK;
+    st->done = 0;
+    if (!st->force && rn <= st->tolb && rtn <= st->tolbt) {
+      st->done = 1;
+    } else if (iszero(rho) || !finite(rho)) {
+      st->done = 1;
+      st->status = RBICG_BREAKDOWN_SERIOUS;
+    } else if (st->max_itn <= 0) {
+      st->done = 1;
+      st->status = RBICG_MAXITER;
+    }
+  }
+}
+
+// Step 7: x = x_i - U ζ_c, x~ = x~_i - Ũ ζ~_c.
+template <typename T>
+__global__ void __launch_bounds__(BS) k_step7(LoopArgs<T> a, const T *U, const T *Ut, T *xo, T *xto) {
+  __shared__ T s_c[KMAX], s_ct[KMAX];
+  const DevState<T> *st = a.st;
+  const int k = a.k;
+  if (threadIdx.x < k) {
+    s_c[threadIdx.x] = st->zc[threadIdx.x];
+    s_ct[threadIdx.x] = st->ztc[threadIdx.x];
+  }
+  __syncthreads();
+  for (int64_t row = (int64_t)blockIdx.x * BS + threadIdx.x; row < a.n;
+       row += (int64_t)gridDim.x * BS) {
+    T du = zero<T>(), dut = zero<T>();
+    for (int j = 0; j < k; ++j) {
+      du = mad(U[row * k + j], s_c[j], du);
+      dut = mad(Ut[row * k + j], s_ct[j], dut);
+    }
+    xo[row] = sub(a.x[row], du);
+    xto[row] = sub(a.xt[row], dut);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(BS) k_spmv_pair(DevMat A, DevMat AH, const T *p, const T *pt, T *z,
+                                                  T *zt) {
+  for (int64_t row = (int64_t)blockIdx.x * BS + threadIdx.x; row < A.n;
+       row += (int64_t)gridDim.x * BS) {
+    z[row] = sell_row<T, false>(A, row, nullptr, p, zero<T>());
+    zt[row] = sell_row<T, false>(AH, row, nullptr, pt, zero<T>());
+  }
+}
+
+// ============================================================== launchers
+static int grid_for(int64_t n, int G) {
+  const int64_t tiles = (n + BS - 1) / BS;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, G));
+}
+
+template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s) {
+  k_pass1<T><<<grid_for(a.n, a.G), BS, 0, s>>>(a);
+  count_launch();
+}
+
+template <typename T> size_t pass2_smem(int k) { return (size_t)2 * BS * k * sizeof(T); }
+
+template <typename T> void launch_pass2(const LoopArgs<T> &a, cudaStream_t s) {
+  size_t sm = pass2_smem<T>(a.k);
+  int staged = (a.k > 0 && sm <= 160 * 1024) ? 1 : 0;
+  if (!staged) sm = 0;
+  k_pass2<T><<<grid_for(a.n, a.G), BS, sm, s>>>(a, staged);
+  count_launch();
+}
+
+template <typename T>
+void launch_resid(const LoopArgs<T> &a, const T *b, const T *bt, const T *x, const T *xt, T *r,
+                  T *rt, int with_coef, cudaStream_t s) {
+  k_resid<T><<<grid_for(a.n, a.G), BS, 0, s>>>(a, b, bt, x, xt, r, rt, with_coef);
+  count_launch();
+}
+
+template <typename T> void launch_init2(const LoopArgs<T> &a, const T *U, const T *Ut, cudaStream_t s) {
+  k_init2<T><<<grid_for(a.n, a.G), BS, 0, s>>>(a, U, Ut);
+  count_launch();
+}
+
+template <typename T>
+void launch_step7(const LoopArgs<T> &a, const T *U, const T *Ut, T *xo, T *xto, cudaStream_t s) {
+  k_step7<T><<<grid_for(a.n, a.G), BS, 0, s>>>(a, U, Ut, xo, xto);
+  count_launch();
+}
+
+template <typename T>
+void launch_spmv_pair(const DevMat &A, const DevMat &AH, const T *p, const T *pt, T *z, T *zt,
+                      cudaStream_t s) {
+  k_spmv_pair<T><<<grid_for(A.n, 1184), BS, 0, s>>>(A, AH, p, pt, z, zt);
+  count_launch();
+}
+
+void prepare_kernels() {
+  RB_CUDA(cudaFuncSetAttribute(k_pass2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_pass2<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  prepare_block_kernels();
+}
+
+#define RB_INST(T)                                                                          \
+  template void launch_pass1<T>(const LoopArgs<T> &, cudaStream_t);                          \
+  template void launch_pass2<T>(const LoopArgs<T> &, cudaStream_t);                          \
+  template void launch_resid<T>(const LoopArgs<T> &, const T *, const T *, const T *,        \
+                                const T *, T *, T *, int, cudaStream_t);                     \
+  template void launch_init2<T>(const LoopArgs<T> &, const T *, const T *, cudaStream_t);    \
+  template void launch_step7<T>(const LoopArgs<T> &, const T *, const T *, T *, T *,         \
+                                cudaStream_t);                                               \
+  template void launch_spmv_pair<T>(const DevMat &, const DevMat &, const T *, const T *, T *, \
+                                    T *, cudaStream_t);
+RB_INST(double)
+RB_INST(zc)
+
+}  // namespace rbicg

@@ -1,0 +1,165 @@
+// matrix.cu -- device matrix store: CSR -> SELL-32 for A and for the explicit
+// conjugate transpose A^* (BASELINE.json north star (1); the operator pair of
+// Algorithm 2 lines z = A p, z~ = A^* p~).
+//
+// The transpose is a stable counting sort by column (CUB radix sort of the
+// column keys, a library sort primitive), so each row of A^* lists its
+// entries in ascending column order, like scipy's A.conj().T.tocsr().
+#include <cub/cub.cuh>
+
+#include "internal.h"
+
+namespace rbicg {
+
+__global__ void k_row_index(const int32_t *rowptr, int64_t n, int32_t *rowidx) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    for (int32_t e = rowptr[r]; e < rowptr[r + 1]; ++e) rowidx[e] = (int32_t)r;
+}
+
+__global__ void k_iota(int32_t *v, int64_t m) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = (int32_t)i;
+}
+
+__global__ void k_count_cols(const int32_t *col, int64_t nnz, int32_t *counts) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(counts + col[e], 1);
+}
+
+template <typename T>
+__global__ void k_gather_t(const int32_t *perm, const int32_t *rowidx, const T *val, int64_t nnz,
+                           int32_t *colT, T *valT) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nnz;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t e = perm[t];
+    colT[t] = rowidx[e];
+    valT[t] = conj(val[e]);
+  }
+}
+
+__global__ void k_slice_width(const int32_t *rowptr, int64_t n, int64_t nslices, int64_t *w32) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nslices;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int32_t w = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int64_t r = s * 32 + l;
+      if (r < n) w = max(w, rowptr[r + 1] - rowptr[r]);
+    }
+    w32[s] = (int64_t)w * 32;
+  }
+}
+
+template <typename T>
+__global__ void k_sell_fill(const int32_t *rowptr, const int32_t *col, const T *val, int64_t n,
+                            int64_t nslices, const int64_t *sptr, int32_t *scol, T *sval) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < nslices * 32;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = g >> 5;
+    const int lane = (int)(g & 31);
+    const int64_t off = sptr[s];
+    const int w = (int)((sptr[s + 1] - off) >> 5);
+    const int64_t r = g;   // row = slice*32 + lane
+    int32_t b = 0, len = 0;
+    if (r < n) {
+      b = rowptr[r];
+      len = rowptr[r + 1] - b;
+    }
+    for (int jj = 0; jj < w; ++jj) {
+      const int64_t idx = off + (int64_t)jj * 32 + lane;
+      if (jj < len) {
+        scol[idx] = col[b + jj];
+        sval[idx] = val[b + jj];
+      } else {
+        scol[idx] = r < n ? (int32_t)r : 0;   // padding: a valid address, zero value
+        sval[idx] = zero<T>();
+      }
+    }
+  }
+}
+
+static int grid1d(int64_t m) { return (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 148 * 32)); }
+
+template <typename T>
+static void csr_to_sell(rbicg_ctx *ctx, int64_t n, const int32_t *rowptr, const int32_t *col,
+                        const T *val, DevMat &out) {
+  cudaStream_t st = ctx->stream;
+  out.n = n;
+  out.nslices = (n + 31) / 32;
+  int64_t *w32 = (int64_t *)ws_alloc(sizeof(int64_t) * (out.nslices + 1));
+  RB_CUDA(cudaMalloc(&out.sptr, sizeof(int64_t) * (out.nslices + 1)));
+  k_slice_width<<<grid1d(out.nslices), 256, 0, st>>>(rowptr, n, out.nslices, w32);
+  RB_CUDA(cudaMemsetAsync(w32 + out.nslices, 0, sizeof(int64_t), st));
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, w32, out.sptr, out.nslices + 1, st);
+  void *dtmp = ws_alloc(tmp + 16);
+  cub::DeviceScan::ExclusiveSum(dtmp, tmp, w32, out.sptr, out.nslices + 1, st);
+  RB_CUDA(cudaMemcpyAsync(&out.padded, out.sptr + out.nslices, sizeof(int64_t),
+                          cudaMemcpyDeviceToHost, st));
+  RB_CUDA(cudaStreamSynchronize(st));
+  ws_free(dtmp);
+  ws_free(w32);
+  RB_CUDA(cudaMalloc(&out.cols, sizeof(int32_t) * std::max<int64_t>(out.padded, 1)));
+  RB_CUDA(cudaMalloc(&out.vals, sizeof(T) * std::max<int64_t>(out.padded, 1)));
+  k_sell_fill<T><<<grid1d(out.nslices * 32), 256, 0, st>>>(rowptr, col, val, n, out.nslices, out.sptr,
+                                                           out.cols, (T *)out.vals);
+  count_launch(2);
+}
+
+template <typename T>
+static void build_t(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr,
+                    const int32_t *col, const T *val, rbicg_mat *M) {
+  cudaStream_t st = ctx->stream;
+  csr_to_sell<T>(ctx, n, rowptr, col, val, M->A);
+  // ---- conjugate transpose
+  int32_t *rowidx = (int32_t *)ws_alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+  int32_t *iota = (int32_t *)ws_alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+  int32_t *keys_out = (int32_t *)ws_alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+  int32_t *perm = (int32_t *)ws_alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+  int32_t *cnt = (int32_t *)ws_alloc(sizeof(int32_t) * (n + 1));
+  int32_t *rowptrT = (int32_t *)ws_alloc(sizeof(int32_t) * (n + 1));
+  int32_t *colT = (int32_t *)ws_alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+  T *valT = (T *)ws_alloc(sizeof(T) * std::max<int64_t>(nnz, 1));
+  k_row_index<<<grid1d(n), 256, 0, st>>>(rowptr, n, rowidx);
+  k_iota<<<grid1d(nnz), 256, 0, st>>>(iota, nnz);
+  RB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n + 1), st));
+  k_count_cols<<<grid1d(nnz), 256, 0, st>>>(col, nnz, cnt);
+  count_launch(3);
+  int bits = 1;
+  while (bits < 31 && ((int64_t)1 << bits) < n) ++bits;
+  size_t t1 = 0, t2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t1, col, keys_out, iota, perm, (int)nnz, 0, bits, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, t2, cnt, rowptrT, (int)(n + 1), st);
+  void *tmp = ws_alloc(std::max(t1, t2) + 16);
+  cub::DeviceRadixSort::SortPairs(tmp, t1, col, keys_out, iota, perm, (int)nnz, 0, bits, st);
+  cub::DeviceScan::ExclusiveSum(tmp, t2, cnt, rowptrT, (int)(n + 1), st);
+  k_gather_t<T><<<grid1d(nnz), 256, 0, st>>>(perm, rowidx, val, nnz, colT, valT);
+  count_launch(3);
+  csr_to_sell<T>(ctx, n, rowptrT, colT, valT, M->AH);
+  RB_CUDA(cudaStreamSynchronize(st));
+  for (void *p : {(void *)rowidx, (void *)iota, (void *)keys_out, (void *)perm, (void *)cnt,
+                  (void *)rowptrT, (void *)colT, (void *)valT, tmp})
+    ws_free(p);
+}
+
+void build_matrix(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr_d,
+                  const int32_t *col_d, const void *val_d, rbicg_dtype dt, rbicg_mat *M) {
+  M->n = n;
+  M->nnz = nnz;
+  M->dtype = dt;
+  if (dt == RBICG_F64)
+    build_t<double>(ctx, n, nnz, rowptr_d, col_d, (const double *)val_d, M);
+  else
+    build_t<zc>(ctx, n, nnz, rowptr_d, col_d, (const zc *)val_d, M);
+}
+
+void free_devmat(DevMat &m) {
+  if (m.sptr) cudaFree(m.sptr);
+  if (m.cols) cudaFree(m.cols);
+  if (m.vals) cudaFree(m.vals);
+  m = DevMat();
+}
+
+}  // namespace rbicg

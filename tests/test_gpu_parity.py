@@ -1,0 +1,286 @@
+"""CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Tolerances are BASELINE.json's: per-call SpMV / projection 1e-12 relative
+(norm-wise, reading Q25), iterations within max(2, 3%), solutions 1e-7
+relative at matched iteration counts (Q27), true residuals <= tol, bilinear
+1e-8 relative.
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from synth import CONFIGS, system_sequence
+from synth.small import random_sparse, deflation_matrix, vec, dense_to_csr
+
+pytestmark = pytest.mark.gpu
+
+
+def _csr(t):
+    indptr, indices, data = t[:3]
+    n = len(indptr) - 1
+    return sp.csr_matrix((data, indices, indptr), shape=(n, n))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1010_0762_b200 import api
+    c = api.Context(0)
+    yield c
+    c.close()
+
+
+def iters_close(a, b):
+    return abs(a - b) <= max(2, 0.03 * max(a, b))
+
+
+# ------------------------------------------------------------------ per call
+@pytest.mark.parametrize("cplx,n", [(False, 1000), (True, 777), (False, 33),
+                                    (True, 1)])
+def test_spmv_pair_parity(ctx, cplx, n):
+    t = random_sparse(n, min(1.0, 8.0 / n), seed=n, complex_=cplx)
+    A = _csr(t)
+    M = ctx.matrix(*t)
+    p, pt = vec(n, 1, cplx), vec(n, 2, cplx)
+    z, zt = ctx.spmv_pair(M, p, pt)
+    zr, ztr = A @ p, A.conj().T @ pt
+    assert np.linalg.norm(z - zr) <= 1e-12 * np.linalg.norm(zr)
+    assert np.linalg.norm(zt - ztr) <= 1e-12 * np.linalg.norm(ztr)
+
+
+def test_spmv_pair_unsorted_and_empty_rows(ctx):
+    n = 300
+    rng = np.random.default_rng(5)
+    D = np.zeros((n, n))
+    for i in range(n):
+        if i % 7 == 3:
+            continue                      # empty row
+        cols = rng.choice(n, size=rng.integers(1, 40), replace=False)
+        D[i, cols] = rng.standard_normal(len(cols))
+    indptr, indices, data = dense_to_csr(D)
+    # shuffle column order inside each row
+    for i in range(n):
+        a, b = indptr[i], indptr[i + 1]
+        perm = rng.permutation(b - a)
+        indices[a:b] = indices[a:b][perm]
+        data[a:b] = data[a:b][perm]
+    M = ctx.matrix(indptr, indices, data)
+    p, pt = vec(n, 3), vec(n, 4)
+    z, zt = ctx.spmv_pair(M, p, pt)
+    assert np.linalg.norm(z - D @ p) <= 1e-12 * np.linalg.norm(D @ p)
+    assert np.linalg.norm(zt - D.T @ pt) <= 1e-12 * np.linalg.norm(D.T @ pt)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_projection_parity(ctx, cplx):
+    from oracle import rbicg as R
+    n, k = 500, 6
+    t = random_sparse(n, 0.02, seed=11, complex_=cplx)
+    A = _csr(t)
+    AH = A.conj().T.tocsr()
+    U = vec(n * k, 12, cplx).reshape(n, k)
+    Ut = vec(n * k, 13, cplx).reshape(n, k)
+    B = R.biorthogonalize(A, AH, U, Ut, 1e-6)
+    M = ctx.matrix(*t)
+    rec = ctx.recycle(n, k, cplx)
+    rec.import_(U, Ut)
+    z, zt = vec(n, 14, cplx), vec(n, 15, cplx)
+    out = ctx.project(M, rec, z, zt, 1e-6)
+    assert out["k"] == B.k
+    np.testing.assert_allclose(out["d"], B.d, rtol=1e-12)
+    # gauge-invariant: C ζ = C D^{-1} C~^* z (Q25 / SURVEY "never column by column")
+    ref = B.C @ ((B.Ct / B.d).conj().T @ z)
+    got = out["C"] @ out["zeta"]
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(z) * \
+        np.linalg.norm(B.C) / B.d.min()
+    reft = B.Ct @ ((B.C / B.d).conj().T @ zt)
+    gott = out["Ct"] @ out["zetat"]
+    assert np.linalg.norm(gott - reft) <= 1e-12 * np.linalg.norm(zt) * \
+        np.linalg.norm(B.Ct) / B.d.min()
+    # bi-orthogonality of the device basis
+    G = out["Ct"].conj().T @ out["C"]
+    np.testing.assert_allclose(G, np.diag(out["d"]), atol=1e-10 * out["d"].max())
+
+
+# ------------------------------------------------------------------ solves
+def _solve_both(ctx, A, Ad, b, bt, U=None, Ut=None, **kw):
+    from oracle import rbicg as R
+    ref = R.solve_dual(Ad, b, bt, U=U, Ut=Ut, **kw)
+    n = Ad.shape[0]
+    cplx = np.iscomplexobj(b)
+    rec = ctx.recycle(n, max(kw.get("k", 0), 1), cplx)
+    if U is not None and U.shape[1]:
+        rec.import_(U, Ut)
+    x, xt, res, _ = ctx.solve_dual(A, b, bt, R=rec, **kw)
+    return ref, (x, xt, res), rec
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_bicg_k0_parity(ctx, cplx):
+    n = 400
+    t = random_sparse(n, 0.02, seed=21, complex_=cplx)
+    Ad = _csr(t)
+    M = ctx.matrix(*t)
+    b, bt = vec(n, 22, cplx), vec(n, 23, cplx)
+    ref, (x, xt, res), _ = _solve_both(ctx, M, Ad, b, bt, k=0, s=10, tol=1e-10,
+                                       max_itn=2000)
+    assert res["status"] == ref.status == 0
+    assert res["iterations"] == ref.iterations
+    np.testing.assert_allclose(x, ref.x, rtol=0, atol=1e-9 * np.linalg.norm(ref.x))
+    assert res["relres_true"] <= 1e-10 and res["relres_dual_true"] <= 1e-10
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_rbicg_repeated_solves(ctx, cplx):
+    """P5-type repeated solves: the recycle space is built on the GPU and fed
+    back; iterations, solutions and final residuals track the oracle."""
+    from oracle import rbicg as R
+    n, k = 300, 4
+    A, lam, S = deflation_matrix(n, k, seed=31, complex_=cplx)
+    Ad = sp.csr_matrix(A)
+    t = dense_to_csr(A)
+    M = ctx.matrix(*t)
+    b, bt = vec(n, 32, cplx), vec(n, 33, cplx)
+    rec = ctx.recycle(n, k, cplx)
+    U = Ut = None
+    its_g, its_o = [], []
+    for run in range(4):
+        ref = R.solve_dual(Ad, b, bt, U=U, Ut=Ut, k=k, s=15, tol=1e-10,
+                           max_itn=1000, trunc_tol=1e-6)
+        x, xt, res, _ = ctx.solve_dual(M, b, bt, R=rec, k=k, s=15, tol=1e-10,
+                                       max_itn=1000, trunc_tol=1e-6)
+        U, Ut = ref.basis_out.U, ref.basis_out.Ut
+        its_g.append(res["iterations"])
+        its_o.append(ref.iterations)
+        assert iters_close(res["iterations"], ref.iterations), (its_g, its_o)
+        assert res["relres_true"] <= 1e-10 and res["relres_dual_true"] <= 1e-10
+        assert np.linalg.norm(x - ref.x) <= 1e-7 * np.linalg.norm(ref.x)
+        assert res["k_out"] == ref.basis_out.k
+    assert its_g[-1] < its_g[0]
+
+
+def test_rbicg_matched_iterations(ctx):
+    """Q27 protocol: run both sides for exactly m iterations (stop test off)
+    from the same recycle input and compare iterates."""
+    from oracle import rbicg as R
+    n, k = 250, 4
+    A, lam, S = deflation_matrix(n, k, seed=41)
+    Ad = sp.csr_matrix(A)
+    M = ctx.matrix(*dense_to_csr(A))
+    b, bt = vec(n, 42), vec(n, 43)
+    first = R.solve_dual(Ad, b, bt, k=k, s=10, tol=1e-10, max_itn=1000,
+                         trunc_tol=1e-6)
+    U, Ut = first.basis_out.U, first.basis_out.Ut
+    b2, bt2 = vec(n, 44), vec(n, 45)
+    for m in (1, 7, 10, 23):
+        ref = R.solve_dual(Ad, b2, bt2, U=U, Ut=Ut, k=k, s=10, tol=1e-10,
+                           max_itn=1000, trunc_tol=1e-6, force_iters=m)
+        rec = ctx.recycle(n, k)
+        rec.import_(U, Ut)
+        x, xt, res, h = ctx.solve_dual(M, b2, bt2, R=rec, k=k, s=10, tol=1e-10,
+                                       max_itn=1000, trunc_tol=1e-6,
+                                       force_iters=m, history=True)
+        assert res["iterations"] == m
+        assert np.linalg.norm(x - ref.x) <= 1e-9 * np.linalg.norm(ref.x)
+        assert np.linalg.norm(xt - ref.xt) <= 1e-9 * np.linalg.norm(ref.xt)
+        np.testing.assert_allclose(h[:, 2], np.real(ref.hist["alpha"]), rtol=1e-8)
+
+
+def test_c1_sequence_parity(ctx):
+    from oracle.sequence import run_sequence
+    cfg = CONFIGS["C1"]
+    items = list(system_sequence(cfg))
+    ref = run_sequence(cfg, items)
+    rec = ctx.recycle(cfg.n, cfg.k)
+    from synth import redraw_vector
+    for item, r in zip(items, ref):
+        M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+        x, xt, res, _ = ctx.solve_dual(M, item["b"], item["bt"], R=rec, k=cfg.k,
+                                       s=cfg.s, tol=cfg.tol, max_itn=cfg.max_itn,
+                                       trunc_tol=cfg.trunc_tol,
+                                       xt_redraw=redraw_vector(cfg, item["j"]))
+        assert res["status"] == r.status, (res, r.status)
+        assert iters_close(res["iterations"], r.iterations)
+        assert res["relres_true"] <= cfg.tol
+        assert res["relres_dual_true"] <= cfg.tol
+        if res["iterations"] == r.iterations:
+            assert np.linalg.norm(x - r.x) <= 1e-7 * np.linalg.norm(r.x)
+        assert res["k_out"] == r.basis_out.k
+
+
+def test_c4_small_complex_sequence(ctx):
+    from oracle.sequence import run_sequence
+    cfg = CONFIGS["C4"].scaled(12, systems=8, s=20)
+    items = list(system_sequence(cfg, lam_r=0.0))
+    ref = run_sequence(cfg, items)
+    rec = ctx.recycle(cfg.n, cfg.k, True)
+    prev = {}
+    for item, r in zip(items, ref):
+        M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+        x0, xt0 = prev.get(item["slot"], (None, None))
+        x, xt, res, _ = ctx.solve_dual(M, item["b"], item["bt"], x0, xt0, R=rec,
+                                       k=cfg.k, s=cfg.s, tol=cfg.tol,
+                                       max_itn=cfg.max_itn,
+                                       trunc_tol=cfg.trunc_tol)
+        prev[item["slot"]] = (x, xt)
+        assert iters_close(res["iterations"], r.iterations), \
+            (res["iterations"], r.iterations)
+        assert res["relres_true"] <= cfg.tol and res["relres_dual_true"] <= cfg.tol
+        assert np.linalg.norm(x - r.x) <= 1e-7 * np.linalg.norm(r.x) or \
+            res["iterations"] != r.iterations
+
+
+def test_bilinear_parity(ctx):
+    from oracle import rbicg as R
+    n = 300
+    t = random_sparse(n, 0.02, seed=51, complex_=True)
+    Ad = _csr(t)
+    M = ctx.matrix(*t)
+    u, w = vec(n, 52, True), vec(n, 53, True)
+    val_o, _ = R.bilinear(Ad, u, w, k=4, s=10, tol=1e-10, max_itn=1000)
+    val_g, res = ctx.bilinear(M, u, w, k=4, s=10, tol=1e-10, max_itn=1000)
+    assert abs(val_g - val_o) <= 1e-8 * abs(val_o)
+    exact = np.vdot(u, np.linalg.solve(Ad.toarray(), w))
+    assert abs(val_g - exact) <= 1e-8 * abs(exact)
+
+
+def test_deterministic(ctx):
+    n = 2000
+    t = random_sparse(n, 0.003, seed=61)
+    M = ctx.matrix(*t)
+    b, bt = vec(n, 62), vec(n, 63)
+    outs = []
+    for _ in range(2):
+        rec = ctx.recycle(n, 4)
+        x, xt, res, _ = ctx.solve_dual(M, b, bt, R=rec, k=4, s=10, tol=1e-10,
+                                       max_itn=3000)
+        x2, _, res2, _ = ctx.solve_dual(M, b, bt, R=rec, k=4, s=10, tol=1e-10,
+                                        max_itn=3000)
+        outs.append((x.copy(), x2.copy(), res["iterations"], res2["iterations"]))
+    assert outs[0][2:] == outs[1][2:]
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_edge_cases(ctx):
+    # identity: one iteration
+    n = 64
+    t = dense_to_csr(np.eye(n))
+    M = ctx.matrix(*t)
+    b = np.ones(n)
+    x, xt, res, _ = ctx.solve_dual(M, b, b, k=0, s=4, tol=1e-12, max_itn=10)
+    assert res["iterations"] == 1 and np.allclose(x, 1.0, rtol=1e-15)
+    # max_itn = 0 and an exact initial guess
+    x, xt, res, _ = ctx.solve_dual(M, b, b, b.copy(), b.copy(), k=0, s=4,
+                                   tol=1e-12, max_itn=0)
+    assert res["iterations"] == 0 and res["status"] == 0
+    # orthogonal initial residuals -> step-3 redraw
+    e1, e2 = np.zeros(n), np.zeros(n)
+    e1[0], e2[1] = 1.0, 1.0
+    x, xt, res, _ = ctx.solve_dual(M, e1, e2, k=0, s=4, tol=1e-12, max_itn=10)
+    assert res["status"] == 2
+    x, xt, res, _ = ctx.solve_dual(M, e1, e2, k=0, s=4, tol=1e-12, max_itn=10,
+                                   xt_redraw=vec(n, 7))
+    assert res["status"] == 0
