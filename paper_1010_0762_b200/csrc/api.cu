@@ -103,6 +103,10 @@ __global__ void k_rm_to_cm(const T *rm, T *cm, int64_t n, int k) {
     cm[i] = rm[row * k + c];
   }
 }
+static void order_after_user(rbicg_ctx *ctx) {
+  RB_CUDA(cudaEventRecord(ctx->order_ev, ctx->user_stream));
+  RB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->order_ev, 0));
+}
 static int g1(int64_t m) { return (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 148 * 16)); }
 
 static void copy_in(void *dst, const void *src, size_t bytes, int on_device, cudaStream_t s) {
@@ -706,7 +710,12 @@ int rbicg_init(rbicg_ctx **out, int device, void *stream, const rbicg_dist *dist
     RB_CUDA(cudaSetDevice(device));
     auto *c = new rbicg_ctx();
     c->device = device;
-    c->stream = (cudaStream_t)stream;
+    // the library works on its own non-blocking stream (graph capture is not
+    // allowed on the legacy default stream); calls are ordered after the
+    // caller's stream by an event and return synchronised.
+    c->user_stream = (cudaStream_t)stream;
+    RB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    RB_CUDA(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
     RB_CUDA(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
     c->grid_stream = c->nsm * 2;
     prepare_kernels();
@@ -718,6 +727,8 @@ int rbicg_finalize(rbicg_ctx *ctx) {
   if (!ctx) return RBICG_EINVAL;
   cudaStreamSynchronize(ctx->stream);
   ws_release_all();
+  cudaEventDestroy(ctx->order_ev);
+  cudaStreamDestroy(ctx->stream);
   delete ctx;
   return 0;
 }
@@ -729,6 +740,7 @@ int rbicg_matrix_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowp
   if (dtype != RBICG_F64 && dtype != RBICG_C128) return RBICG_EINVAL;
   return run_guarded([&] {
     RB_CUDA(cudaSetDevice(ctx->device));
+    order_after_user(ctx);
     const size_t w = wbytes(dtype);
     int32_t *rp = (int32_t *)ws_alloc(sizeof(int32_t) * (n + 1));
     int32_t *ci = (int32_t *)ws_alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
@@ -996,6 +1008,7 @@ int rbicg_solve_dual(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const vo
   int status = 0;
   int rc = run_guarded([&] {
     RB_CUDA(cudaSetDevice(ctx->device));
+    order_after_user(ctx);
     if (A->dtype == RBICG_F64)
       status = solve_t<double>(ctx, A, b, bt, x, xt, xt_redraw, R, o, on_device, res, hist);
     else
@@ -1053,6 +1066,7 @@ int rbicg_dbg_spmv_pair(rbicg_ctx *ctx, const rbicg_mat *A, const void *p, const
                         void *zt, int on_device) {
   if (!ctx || !A || !p || !pt || !z || !zt) return RBICG_EINVAL;
   return run_guarded([&] {
+    order_after_user(ctx);
     const size_t vb = wbytes(A->dtype) * A->n;
     void *dp = ws_alloc(vb), *dpt = ws_alloc(vb), *dz = ws_alloc(vb), *dzt = ws_alloc(vb);
     copy_in(dp, p, vb, on_device, ctx->stream);

@@ -78,7 +78,9 @@ using cplx = std::complex<double>;
 
 struct rbicg_ctx {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;       // library stream (non-blocking)
+  cudaStream_t user_stream = nullptr;  // caller's stream (may be legacy NULL)
+  cudaEvent_t order_ev = nullptr;
   int nsm = 148;
   int grid_stream = 296;  // persistent grid of the streaming kernels
   // reusable device workspace
