@@ -384,7 +384,7 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
         hist["rho"].append(rho_new)
         serious = breakdown(rho_new, rn, rtn, breakdown_tol)
         # cycle end (full cycles only, Q14)
-        if update_recycle and i % s == 0 and (converged or not serious):
+        if update_recycle and k > 0 and i % s == 0 and (converged or not serious):
             j = i // s
             cand = _cycle_end(A, AH, L, j, s, basis, cand, k, trunc_tol, dt,
                               real, pencils if keep_pencils else None)
@@ -424,7 +424,7 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
         out = cand
     else:
         out = basis  # Q18: refreshed input when no full cycle completed
-    if status == OK and update_recycle and cand is not None and cand.k == 0:
+    if status == OK and update_recycle and k > 0 and cand is not None and cand.k == 0:
         status = RECYCLE_EMPTY  # p = 0 after truncation (PAPER.md:702 footnote)
     return SolveResult(x=x, xt=xt, status=status, iterations=it, cycles=cycles,
                        basis_out=out, basis_in=basis,
