@@ -7,6 +7,7 @@ No arithmetic of the method happens here.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 
 import numpy as np
 
@@ -48,12 +49,18 @@ class Context:
             except ImportError:   # pragma: no cover
                 stream = None
         self.device = device
+        self._children = []          # weakrefs to matrices / recycle handles
         self._h = C.c_void_p()
         check(lib.rbicg_init(C.byref(self._h), device,
                              C.c_void_p(stream) if stream else None, None))
 
     def close(self):
         if self._h:
+            for ref in self._children:
+                obj = ref()
+                if obj is not None:
+                    obj.free()
+            self._children = []
             lib.rbicg_finalize(self._h)
             self._h = C.c_void_p()
 
@@ -175,6 +182,7 @@ class Matrix:
         self.nnz = int(len(indices))
         self.complex_ = _dtype_code(data) == C128
         self._h = C.c_void_p()
+        ctx._children.append(weakref.ref(self))
         check(lib.rbicg_matrix_csr(ctx._h, self.n, self.nnz, _ptr(indptr),
                                    _ptr(indices), _ptr(data),
                                    C128 if self.complex_ else F64,
@@ -198,6 +206,7 @@ class Recycle:
     def __init__(self, ctx, n, k_max, complex_=False):
         self.ctx, self.n, self.k_max, self.complex_ = ctx, n, k_max, complex_
         self._h = C.c_void_p()
+        ctx._children.append(weakref.ref(self))
         check(lib.rbicg_recycle_new(ctx._h, n, k_max, C128 if complex_ else F64,
                                     C.byref(self._h)))
 

@@ -773,7 +773,7 @@ int rbicg_matrix_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowp
 
 int rbicg_matrix_free(rbicg_mat *A) {
   if (!A) return RBICG_EINVAL;
-  cudaStreamSynchronize(A->ctx->stream);
+  // no ctx dereference: the ctx may already be finalized (cudaFree syncs)
   free_devmat(A->A);
   free_devmat(A->AH);
   delete A;
