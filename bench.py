@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""RBiCG iterations/s on B200 (BASELINE.json metric) -- one JSON line.
+
+Workload (N=1): BASELINE.json configs[1] = C2, the 2-D upwind conv-diff
+sequence on a 1024^2 grid (n = 1,048,576, fp64, k = 10, s = 40, tol 1e-8,
+10 dual pairs; synthetic, seeded per SURVEY.md §8(d)).
+
+A *step* is one dual-pair solve of the sequence through the C ABI
+(rbicg_matrix_csr from device CSR -> SELL-32 + conj-transpose build,
+rbicg_solve_dual: refresh, init, the graph-replayed hot loop, cycle-end
+recycle updates, step 7, true residuals), carrying the recycle space from
+system to system.  value = iterations / device time of the K timed steps.
+
+Timing: W warm-up steps, then K steps bracketed by barrier + synchronize and
+CUDA events; max over ranks.  Per-iteration traffic (637 MB at C2) is larger
+than the 126 MB L2, so no explicit flush is needed ("inputs larger than L2").
+
+--impl reference runs the CPU oracle (the only other allowed use of oracle/)
+on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax = float(r[1])
+                for nm, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_systems(cfg, idx):
+    from synth import system_sequence
+    want = sorted(set(j % cfg.systems for j in idx))
+    got = {it["j"]: it for it in system_sequence(cfg, systems=want)}
+    return [got[j % cfg.systems] for j in idx]
+
+
+def alg_bytes(cfg_n, nnz, k, w=8):
+    """Algorithmic HBM bytes per launch of the two hot kernels:
+    pass 1 streams A and A^* (CSR-equivalent: values + int32 column indices +
+    row pointers), C and C~ once, reads r, p, r~, p~ and writes p, p~, z, z~;
+    pass 2 reads C, C~, z, z~, r, r~, x, x~, p, p~ and writes r, r~, x, x~."""
+    mat = 2 * (nnz * (w + 4) + 4 * (cfg_n + 1))
+    p1 = mat + 2 * k * cfg_n * w + 8 * cfg_n * w
+    p2 = 2 * k * cfg_n * w + 12 * cfg_n * w
+    return p1, p2
+
+
+def run_gpu(args, rank, world):
+    import torch
+    from paper_1010_0762_b200 import api
+    from synth import CONFIGS
+    cfg = CONFIGS[args.config]
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    ctx = api.Context(dev)
+    steps = args.warmup + args.steps
+    systems = build_systems(cfg, list(range(steps)))
+    # inputs resident in HBM before the timed region
+    dsys = []
+    for it in systems:
+        dsys.append({k: torch.from_numpy(np.ascontiguousarray(it[k])).to(f"cuda:{dev}")
+                     for k in ("indptr", "indices", "data", "b", "bt")})
+    torch.cuda.synchronize()
+    R = ctx.recycle(cfg.n, cfg.k, cfg.complex)
+    stream = torch.cuda.current_stream()
+    res_all, times = [], []
+
+    def one(i, timed):
+        d = dsys[i]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        A = ctx.matrix(d["indptr"], d["indices"], d["data"])
+        x, xt, res, _ = ctx.solve_dual(A, d["b"], d["bt"], R=R, k=cfg.k, s=cfg.s,
+                                       tol=cfg.tol, max_itn=cfg.max_itn,
+                                       trunc_tol=cfg.trunc_tol)
+        A.free()
+        e1.record(stream)
+        e1.synchronize()
+        return res, e0.elapsed_time(e1)
+
+    for i in range(args.warmup):
+        one(i, False)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(dev)
+    clk.start()
+    l0 = api.launch_count()
+    for i in range(args.warmup, steps):
+        r, ms = one(i, True)
+        res_all.append(r)
+        times.append(ms)
+    torch.cuda.synchronize()
+    launches = api.launch_count() - l0
+    clocks = clk.stop()
+    if world > 1:
+        torch.distributed.barrier()
+    total_ms = float(sum(times))
+    iters = int(sum(r["iterations"] for r in res_all))
+    t = torch.tensor([total_ms, iters], dtype=torch.float64, device=f"cuda:{dev}")
+    if world > 1:
+        tmax = t.clone()
+        torch.distributed.all_reduce(tmax[:1], op=torch.distributed.ReduceOp.MAX)
+        tsum = t.clone()
+        torch.distributed.all_reduce(tsum[1:], op=torch.distributed.ReduceOp.SUM)
+        total_ms, iters = float(tmax[0]), int(tsum[1])
+
+    # ---- roofline of the dominant kernel: per-kernel CUDA events on the
+    # library stream, resident state of the last system, its recycle space
+    last = dsys[-1]
+    A = ctx.matrix(last["indptr"], last["indices"], last["data"])
+    kt = ctx.time_kernels(A, R, k=cfg.k, s=cfg.s, iters=args.kernel_iters,
+                          trunc_tol=cfg.trunc_tol)
+    A.free()
+    w = 16 if cfg.complex else 8
+    p1, p2 = alg_bytes(cfg.n, cfg.nnz, kt["k"], w)
+    peak, peak_kind = hbm_peak()
+    dom_bytes, dom_ms, dom = (p1, kt["pass1_ms"], "pass1") \
+        if kt["pass1_ms"] >= kt["pass2_ms"] else (p2, kt["pass2_ms"], "pass2")
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+
+    # ---- e2e through the public API with HOST buffers (H2D/D2H in the call)
+    e2e = None
+    if not args.no_e2e:
+        R2 = ctx.recycle(cfg.n, cfg.k, cfg.complex)
+        h_sys = systems[args.warmup:steps]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ei, h2d, d2h = 0, 0, 0
+        for it in h_sys:
+            A = ctx.matrix(it["indptr"], it["indices"], it["data"])
+            x, xt, res, _ = ctx.solve_dual(A, it["b"], it["bt"], R=R2, k=cfg.k,
+                                           s=cfg.s, tol=cfg.tol,
+                                           max_itn=cfg.max_itn,
+                                           trunc_tol=cfg.trunc_tol)
+            A.free()
+            ei += res["iterations"]
+            h2d += it["indptr"].nbytes + it["indices"].nbytes + it["data"].nbytes \
+                + it["b"].nbytes + it["bt"].nbytes + 2 * it["b"].nbytes
+            d2h += x.nbytes + xt.nbytes
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        e2e = {"value": ei / el, "unit": "iterations/s",
+               "h2d_bytes_per_step": h2d // max(1, len(h_sys)),
+               "d2h_bytes_per_step": d2h // max(1, len(h_sys))}
+
+    out = {
+        "metric": "RBiCG iterations/sec (dual pair) and achieved HBM GB/s",
+        "value": iters / (total_ms * 1e-3),
+        "unit": "iterations/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / max(1, args.steps),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128" if cfg.complex else "f64",
+        "data": "synthetic (seeded conv-diff sequence, SURVEY §8(d))",
+        "config": {"workload": f"{cfg.name}: 2-D upwind conv-diff 1024^2, n={cfg.n}, "
+                               f"nnz={cfg.nnz}, k={cfg.k}, s={cfg.s}, tol={cfg.tol}, "
+                               f"trunc_tol={cfg.trunc_tol}",
+                   "systems_timed": [int(j % cfg.systems) for j in range(args.warmup, steps)],
+                   "iterations_per_system": [r["iterations"] for r in res_all],
+                   "status_per_system": [r["status_name"] for r in res_all],
+                   "k_in_per_system": [r["k_in"] for r in res_all],
+                   "host_eig_ms": sum(r["t_host_eig_ms"] for r in res_all),
+                   "cycle_end_ms": sum(r["t_cycle_dev_ms"] for r in res_all),
+                   "loop_ms": sum(r["t_loop_ms"] for r in res_all),
+                   "l2": "per-iteration traffic > 126 MB L2 (no flush needed)",
+                   "parallelism": "replicas" if world > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "alg_bytes_per_launch": dom_bytes,
+                     "pass1_ms": kt["pass1_ms"], "pass2_ms": kt["pass2_ms"],
+                     "k_active": kt["k"],
+                     "iter_GBps": (p1 + p2) / ((kt["pass1_ms"] + kt["pass2_ms"]) * 1e-3) / 1e9},
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    return out
+
+
+def cpu_baseline(args, cfg, sample_iters):
+    """The oracle as it stands, on a bounded sample: the first `sample_iters`
+    iterations of system 0 (stop test off, Q27 force_iters), host cores."""
+    import scipy.sparse as sp
+    from oracle import rbicg as R
+    from synth import system_sequence
+    try:
+        from threadpoolctl import threadpool_info
+        blas_threads = max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
+    except Exception:
+        blas_threads = 1
+    it = next(system_sequence(cfg, systems=[0]))
+    A = sp.csr_matrix((it["data"], it["indices"], it["indptr"]), shape=(cfg.n, cfg.n))
+    t0 = time.perf_counter()
+    res = R.solve_dual(A, it["b"], it["bt"], k=cfg.k, s=cfg.s, tol=cfg.tol,
+                       max_itn=sample_iters, trunc_tol=cfg.trunc_tol,
+                       force_iters=sample_iters)
+    el = time.perf_counter() - t0
+    return {"value": res.iterations / el, "unit": "iterations/s",
+            "cores": int(blas_threads), "kind": "oracle",
+            "host_cores_available": len(os.sched_getaffinity(0)),
+            "sample": f"{cfg.name} system 0, first {sample_iters} iterations "
+                      f"(force_iters, incl. {sample_iters // cfg.s} cycle ends), "
+                      f"{el:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the same config/metric, each step a
+    bounded sample (one cycle of s iterations of system j)."""
+    import scipy.sparse as sp
+    from oracle import rbicg as R
+    from synth import CONFIGS, system_sequence
+    cfg = CONFIGS[args.config]
+    steps = args.warmup + args.steps
+    items = build_systems(cfg, list(range(steps)))
+    tot_it, tot_t = 0, 0.0
+    U = Ut = None
+    for i, it in enumerate(items):
+        A = sp.csr_matrix((it["data"], it["indices"], it["indptr"]), shape=(cfg.n, cfg.n))
+        t0 = time.perf_counter()
+        res = R.solve_dual(A, it["b"], it["bt"], U=U, Ut=Ut, k=cfg.k, s=cfg.s,
+                           tol=cfg.tol, max_itn=cfg.s, trunc_tol=cfg.trunc_tol,
+                           force_iters=cfg.s)
+        el = time.perf_counter() - t0
+        U, Ut = res.basis_out.U, res.basis_out.Ut
+        if i >= args.warmup:
+            tot_it += res.iterations
+            tot_t += el
+    try:
+        from threadpoolctl import threadpool_info
+        blas_threads = max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
+    except Exception:
+        blas_threads = 1
+    v = tot_it / tot_t
+    sample = f"{cfg.name}: per step one cycle ({cfg.s} iterations, stop test off) of system j"
+    return {"impl": "reference", "metric": "RBiCG iterations/sec (dual pair) and achieved HBM GB/s",
+            "value": v, "unit": "iterations/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / max(1, args.steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name} (bounded sample)"},
+            "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": int(blas_threads),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--kernel-iters", type=int, default=20)
+    ap.add_argument("--cpu-sample-iters", type=int, default=80)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    out = run_gpu(args, rank, world)
+    if rank == 0:
+        if not args.no_cpu and world == 1:
+            from synth import CONFIGS
+            out["cpu_baseline"] = cpu_baseline(args, CONFIGS[args.config],
+                                               args.cpu_sample_iters)
+        elif not args.no_cpu:
+            out["cpu_baseline"] = None
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
