@@ -717,8 +717,12 @@ int rbicg_init(rbicg_ctx **out, int device, void *stream, const rbicg_dist *dist
     RB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     RB_CUDA(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
     RB_CUDA(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
-    c->grid_stream = c->nsm * 2;
     prepare_kernels();
+    {
+      int mult = stream_blocks_per_sm();
+      if (const char *e = getenv("RBICG_BLOCKS_PER_SM")) mult = std::max(1, atoi(e));
+      c->grid_stream = c->nsm * mult;
+    }
     *out = c;
   });
 }

@@ -116,6 +116,7 @@ void free_devmat(DevMat &m);
 // ---- kernels.cu (launch wrappers; all on ctx->stream)
 void prepare_kernels();        // one-time function attributes (not capturable)
 void prepare_block_kernels();
+int stream_blocks_per_sm();    // occupancy of the streaming kernels
 template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_pass2(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T>

@@ -105,7 +105,7 @@ __device__ __forceinline__ void final_reduce(const T *part, int nout, int G, T *
 
 // ============================================================== pass 1
 template <typename T>
-__global__ void __launch_bounds__(BS) k_pass1(LoopArgs<T> a) {
+__global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
   __shared__ T s_z[BS], s_zt[BS], s_pt[BS];
   __shared__ T s_red[3 * BS];
   __shared__ T s_fin[3 * KMAX + 1];
@@ -187,11 +187,11 @@ __global__ void __launch_bounds__(BS) k_pass1(LoopArgs<T> a) {
     st->cnt[0] = 0;
     const int i = it + 1;
     T sigma = s_fin[3 * k];
-    T zeta[KMAX], zetat[KMAX];
     for (int j = 0; j < k; ++j) {
-      zeta[j] = scal(st->dinv[j], s_fin[j]);          // ζ_i = D_c^{-1} C~^* z_i
-      zetat[j] = scal(st->dinv[j], s_fin[k + j]);     // ζ~_i = D_c^{-1} C^* z~_i
-      sigma = sub(sigma, cmul(s_fin[2 * k + j], zeta[j]));  // (p~, z - Cζ)
+      const T zj = scal(st->dinv[j], s_fin[j]);   // ζ_i = D_c^{-1} C~^* z_i
+      s_fin[j] = zj;
+      s_fin[k + j] = scal(st->dinv[j], s_fin[k + j]);   // ζ~_i = D_c^{-1} C^* z~_i
+      sigma = sub(sigma, cmul(s_fin[2 * k + j], zj));   // (p~, z - Cζ)  (Q23)
     }
     const T alpha = divd(st->rho, sigma);
     if (iszero(sigma) || !finite(alpha)) {   // breakdown of the second kind
@@ -203,19 +203,20 @@ __global__ void __launch_bounds__(BS) k_pass1(LoopArgs<T> a) {
     st->sigma = sigma;
     const T ca = conj(alpha);
     for (int j = 0; j < k; ++j) {
-      st->zeta[j] = zeta[j];
-      st->zetat[j] = zetat[j];
-      st->zc[j] = mad(alpha, zeta[j], st->zc[j]);
-      st->ztc[j] = mad(ca, zetat[j], st->ztc[j]);
-      a.zhist[(int64_t)i * k + j] = zeta[j];
-      a.zthist[(int64_t)i * k + j] = zetat[j];
+      const T zj = s_fin[j], ztj = s_fin[k + j];
+      st->zeta[j] = zj;
+      st->zetat[j] = ztj;
+      st->zc[j] = mad(alpha, zj, st->zc[j]);
+      st->ztc[j] = mad(ca, ztj, st->ztc[j]);
+      a.zhist[(int64_t)i * k + j] = zj;
+      a.zthist[(int64_t)i * k + j] = ztj;
     }
   }
 }
 
 // ============================================================== pass 2
 template <typename T>
-__global__ void __launch_bounds__(BS) k_pass2(LoopArgs<T> a, int staged) {
+__global__ void __launch_bounds__(BS, 4) k_pass2(LoopArgs<T> a, int staged) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ T s_zeta[KMAX], s_zetat[KMAX];
   __shared__ T s_w[BS / 32];
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(BS) k_pass2(LoopArgs<T> a, int staged) {
 // r = b - A x, r~ = b~ - A^* x~; partial ||b||², ||b~||², ||r||², ||r~||² and,
 // with coef, C~^*r and C^*r~ (minusXR).
 template <typename T>
-__global__ void __launch_bounds__(BS) k_resid(LoopArgs<T> a, const T *b, const T *bt, const T *x,
+__global__ void __launch_bounds__(BS, 4) k_resid(LoopArgs<T> a, const T *b, const T *bt, const T *x,
                                               const T *xt, T *r, T *rt, int coef) {
   __shared__ T s_r[BS], s_rt[BS];
   __shared__ T s_red[2 * BS];
@@ -422,7 +423,7 @@ __global__ void __launch_bounds__(BS) k_resid(LoopArgs<T> a, const T *b, const T
 
 // x_0 = x_{-1} + U g, r_0 = r_{-1} - C g (and duals); ρ_0, norms; state reset.
 template <typename T>
-__global__ void __launch_bounds__(BS) k_init2(LoopArgs<T> a, const T *U, const T *Ut) {
+__global__ void __launch_bounds__(BS, 4) k_init2(LoopArgs<T> a, const T *U, const T *Ut) {
   __shared__ T s_g[KMAX], s_gt[KMAX];
   __shared__ T s_w[BS / 32];
   __shared__ T s_fin[3];
@@ -591,6 +592,13 @@ void launch_spmv_pair(const DevMat &A, const DevMat &AH, const T *p, const T *pt
                       cudaStream_t s) {
   k_spmv_pair<T><<<grid_for(A.n, 1184), BS, 0, s>>>(A, AH, p, pt, z, zt);
   count_launch();
+}
+
+int stream_blocks_per_sm() {
+  int b1 = 0, b2 = 0;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_pass1<double>, BS, 0));
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_pass1<zc>, BS, 0));
+  return std::max(1, std::min(b1, b2));
 }
 
 void prepare_kernels() {
