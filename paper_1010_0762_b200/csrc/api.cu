@@ -311,6 +311,8 @@ struct Solver {
     la.G = ctx->grid_stream;
     la.A = M->A;
     la.AH = M->AH;
+    la.tile_max = std::max(M->A.tile_max, M->AH.tile_max);
+    la.staged = (2.0 * la.tile_max * (4 + sizeof(T)) <= 96 * 1024 && !getenv("RBICG_NO_TMA")) ? 1 : 0;
     la.rring = rring;
     la.rtring = rtring;
     la.p[0] = p[0];

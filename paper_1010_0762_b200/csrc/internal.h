@@ -18,6 +18,7 @@ constexpr int BS = 256;    // threads per block of the streaming kernels
 // vectors keep their natural order).
 struct DevMat {
   int64_t n = 0, nslices = 0, padded = 0;
+  int tile_max = 0;         // max elements in one 256-row tile (8 slices)
   int64_t *sptr = nullptr;  // nslices + 1 element offsets (multiples of 32)
   int32_t *cols = nullptr;
   void *vals = nullptr;
@@ -55,6 +56,7 @@ template <typename T>
 struct LoopArgs {
   int64_t n;
   int k, ring, G;
+  int staged, tile_max;    // pass 1 stages SELL tiles in smem via TMA
   DevMat A, AH;
   T *rring, *rtring;       // ring of residual columns (r_m in column m % ring)
   T *p[2], *pt[2];         // ping-pong search directions

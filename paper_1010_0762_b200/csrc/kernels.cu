@@ -39,6 +39,39 @@ template <> __device__ __forceinline__ zc ldcs<zc>(const zc *p) {
   return mk(v.x, v.y);
 }
 
+
+// ---------------------------------------------------------------- TMA / mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion via mbarrier tx count
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra "
+      "WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 // y_row = Σ_j a_{row,j} (r_j + β p_j)   (FUSE)   or   Σ_j a_{row,j} p_j
 template <typename T, bool FUSE>
 __device__ __forceinline__ T sell_row(const DevMat &M, int64_t row, const T *__restrict__ r,
@@ -60,6 +93,47 @@ __device__ __forceinline__ T sell_row(const DevMat &M, int64_t row, const T *__r
     acc = mad(v, pj, acc);
   }
   return acc;
+}
+
+
+// One row of the SpMV pair from TMA-staged SELL tiles (column-major slices in
+// shared memory).  Both matrices' gathers are issued together in chunks of 4
+// so up to 16 independent loads per thread are in flight.
+template <typename T>
+__device__ __forceinline__ void sell_pair_smem(const int32_t *__restrict__ cA, const T *__restrict__ vA,
+                                               int wA, const int32_t *__restrict__ cH,
+                                               const T *__restrict__ vH, int wH,
+                                               const T *__restrict__ r, const T *__restrict__ p,
+                                               const T *__restrict__ rt, const T *__restrict__ pt,
+                                               T beta, T cb, T &z, T &zt) {
+  z = zero<T>();
+  zt = zero<T>();
+  const int wm = max(wA, wH);
+  for (int j0 = 0; j0 < wm; j0 += 4) {
+    int ca[4], ch[4];
+    T va[4], vh[4], ra[4], pa[4], rh[4], ph[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int jj = j0 + q;
+      const bool ia = jj < wA, ih = jj < wH;
+      ca[q] = ia ? cA[jj * 32] : 0;
+      va[q] = ia ? vA[jj * 32] : zero<T>();
+      ch[q] = ih ? cH[jj * 32] : 0;
+      vh[q] = ih ? vH[jj * 32] : zero<T>();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ra[q] = ldg(r + ca[q]);
+      pa[q] = ldg(p + ca[q]);
+      rh[q] = ldg(rt + ch[q]);
+      ph[q] = ldg(pt + ch[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      z = mad(va[q], mad(beta, pa[q], ra[q]), z);
+      zt = mad(vh[q], mad(cb, ph[q], rh[q]), zt);
+    }
+  }
 }
 
 // Deterministic block sum (fixed shuffle tree + fixed warp order). Valid in
@@ -129,10 +203,72 @@ __global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
   const int kt = rstep * k;
   T a1 = zero<T>(), a2 = zero<T>(), a3 = zero<T>(), aptz = zero<T>();
   const int64_t ntiles = (n + BS - 1) / BS;
+  // TMA staging of the SELL tiles of A and A^* (one tile = 8 slices = BS rows)
+  extern __shared__ __align__(128) unsigned char p1_smem[];
+  __shared__ uint64_t bar;
+  const int TM = a.tile_max;   // elements per tile per matrix (multiple of 32)
+  int32_t *scA = reinterpret_cast<int32_t *>(p1_smem);
+  int32_t *scH = scA + TM;
+  T *svA = reinterpret_cast<T *>(scH + TM);
+  T *svH = svA + TM;
+  const int64_t ns = a.A.nslices;
+  auto issue = [&](int64_t t) {
+    const int64_t s0 = t * (BS / 32), s1 = min(s0 + BS / 32, ns);
+    const int64_t oA = a.A.sptr[s0], eA = a.A.sptr[s1];
+    const int64_t oH = a.AH.sptr[s0], eH = a.AH.sptr[s1];
+    const uint32_t nA = (uint32_t)(eA - oA), nH = (uint32_t)(eH - oH);
+    mbar_expect_tx(&bar, (nA + nH) * (4u + (uint32_t)sizeof(T)));
+    if (nA) {
+      tma_load_1d(scA, a.A.cols + oA, nA * 4u, &bar);
+      tma_load_1d(svA, reinterpret_cast<const T *>(a.A.vals) + oA, nA * (uint32_t)sizeof(T), &bar);
+    }
+    if (nH) {
+      tma_load_1d(scH, a.AH.cols + oH, nH * 4u, &bar);
+      tma_load_1d(svH, reinterpret_cast<const T *>(a.AH.vals) + oH, nH * (uint32_t)sizeof(T), &bar);
+    }
+  };
+  if (a.staged) {
+    if (tid == 0) {
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0 && (int64_t)blockIdx.x < ntiles) issue(blockIdx.x);
+  }
+  uint32_t phase = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row0 = tile * BS;
     const int rows = (int)min((int64_t)BS, n - row0);
-    if (tid < rows) {
+    if (a.staged) {
+      // slice geometry (global loads overlap the bulk copy)
+      const int64_t sl = (row0 >> 5) + (tid >> 5);
+      const int64_t slc = min(sl, ns - 1);
+      const int64_t bA = a.A.sptr[tile * (BS / 32)], bH = a.AH.sptr[tile * (BS / 32)];
+      const int64_t oA = a.A.sptr[slc], oH = a.AH.sptr[slc];
+      const int wA = (int)((a.A.sptr[slc + 1] - oA) >> 5), wH = (int)((a.AH.sptr[slc + 1] - oH) >> 5);
+      const int lane = tid & 31;
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+      if (tid < rows) {
+        const int64_t row = row0 + tid;
+        T z, zt;
+        sell_pair_smem<T>(scA + (oA - bA) + lane, svA + (oA - bA) + lane, wA,
+                          scH + (oH - bH) + lane, svH + (oH - bH) + lane, wH, r, pold, rt, ptold,
+                          beta, cb, z, zt);
+        const T pn = mad(beta, ldg(pold + row), ldg(r + row));
+        const T ptn = mad(cb, ldg(ptold + row), ldg(rt + row));
+        pnew[row] = pn;
+        ptnew[row] = ptn;
+        a.z[row] = z;
+        a.zt[row] = zt;
+        aptz = cmad(ptn, z, aptz);
+        s_z[tid] = z;
+        s_zt[tid] = zt;
+        s_pt[tid] = ptn;
+      }
+      __syncthreads();   // staged tile consumed -> refill
+      if (tid == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x);
+    } else if (tid < rows) {
       const int64_t row = row0 + tid;
       const T z = sell_row<T, true>(a.A, row, r, pold, beta);
       const T zt = sell_row<T, true>(a.AH, row, rt, ptold, cb);
@@ -261,7 +397,11 @@ __global__ void __launch_bounds__(BS, 4) k_pass2(LoopArgs<T> a, int staged) {
     }
     if (tid < rows) {
       const int64_t row = row0 + tid;
+      // all independent loads first (no aliasing stalls behind the stores)
       T q = ldcs(a.z + row), qt = ldcs(a.zt + row);
+      const T ro = ldcs(rold + row), rto = ldcs(rtold + row);
+      const T pv = ldg(pn + row), ptv = ldg(ptn + row);
+      const T xv = ldcs(a.x + row), xtv = ldcs(a.xt + row);
       if (k > 0) {
         const T *cr = staged ? sC + tid * k : a.C + row * k;
         const T *ctr = staged ? sCt + tid * k : a.Ct + row * k;
@@ -273,10 +413,10 @@ __global__ void __launch_bounds__(BS, 4) k_pass2(LoopArgs<T> a, int staged) {
         q = sub(q, d);     // q_i = z_i - C ζ_i
         qt = sub(qt, dt);  // q~_i = z~_i - C~ ζ~_i
       }
-      a.x[row] = mad(alpha, ldg(pn + row), a.x[row]);
-      a.xt[row] = mad(ca, ldg(ptn + row), a.xt[row]);
-      const T rn = sub(ldcs(rold + row), mul(alpha, q));
-      const T rtn = sub(ldcs(rtold + row), mul(ca, qt));
+      const T rn = sub(ro, mul(alpha, q));
+      const T rtn = sub(rto, mul(ca, qt));
+      a.x[row] = mad(alpha, pv, xv);
+      a.xt[row] = mad(ca, ptv, xtv);
       rnew[row] = rn;
       rtnew[row] = rtn;
       arho = cmad(rtn, rn, arho);
@@ -554,8 +694,12 @@ static int grid_for(int64_t n, int G) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, G));
 }
 
+template <typename T> size_t pass1_smem(int tile_max) {
+  return (size_t)2 * tile_max * (4 + sizeof(T));
+}
 template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s) {
-  k_pass1<T><<<grid_for(a.n, a.G), BS, 0, s>>>(a);
+  const size_t sm = a.staged ? pass1_smem<T>(a.tile_max) : 0;
+  k_pass1<T><<<grid_for(a.n, a.G), BS, sm, s>>>(a);
   count_launch();
 }
 
@@ -602,6 +746,8 @@ int stream_blocks_per_sm() {
 }
 
 void prepare_kernels() {
+  RB_CUDA(cudaFuncSetAttribute(k_pass1<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_pass1<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_pass2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_pass2<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   prepare_block_kernels();

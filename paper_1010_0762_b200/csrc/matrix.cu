@@ -96,9 +96,15 @@ static void csr_to_sell(rbicg_ctx *ctx, int64_t n, const int32_t *rowptr, const 
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, w32, out.sptr, out.nslices + 1, st);
   void *dtmp = ws_alloc(tmp + 16);
   cub::DeviceScan::ExclusiveSum(dtmp, tmp, w32, out.sptr, out.nslices + 1, st);
-  RB_CUDA(cudaMemcpyAsync(&out.padded, out.sptr + out.nslices, sizeof(int64_t),
+  std::vector<int64_t> hs(out.nslices + 1);
+  RB_CUDA(cudaMemcpyAsync(hs.data(), out.sptr, sizeof(int64_t) * (out.nslices + 1),
                           cudaMemcpyDeviceToHost, st));
   RB_CUDA(cudaStreamSynchronize(st));
+  out.padded = hs[out.nslices];
+  int64_t tm = 0;
+  for (int64_t s0 = 0; s0 < out.nslices; s0 += BS / 32)
+    tm = std::max(tm, hs[std::min(s0 + BS / 32, out.nslices)] - hs[s0]);
+  out.tile_max = (int)std::min<int64_t>(tm, INT32_MAX);
   ws_free(dtmp);
   ws_free(w32);
   RB_CUDA(cudaMalloc(&out.cols, sizeof(int32_t) * std::max<int64_t>(out.padded, 1)));
