@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <string>
 #include <mutex>
 
 #include "internal.h"
@@ -77,6 +78,43 @@ static void ws_release_all() {
     g_sizes.erase(kv.second);
   }
   g_pool.clear();
+}
+
+// ------------------------------------------------------------------ tracing
+// RBICG_TRACE=1: synchronise around each phase and print per-phase totals.
+static bool trace_on() {
+  static int on = getenv("RBICG_TRACE") ? 1 : 0;
+  return on;
+}
+static std::map<std::string, std::pair<double, int>> g_trace;
+struct Phase {
+  const char *nm;
+  cudaStream_t s;
+  double t0;
+  Phase(const char *n, cudaStream_t st) : nm(n), s(st), t0(0) {
+    if (trace_on()) {
+      cudaStreamSynchronize(s);
+      t0 = std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch()).count();
+    }
+  }
+  ~Phase() {
+    if (trace_on()) {
+      cudaStreamSynchronize(s);
+      const double t1 = std::chrono::duration<double, std::milli>(
+                            std::chrono::steady_clock::now().time_since_epoch()).count();
+      auto &e = g_trace[nm];
+      e.first += t1 - t0;
+      e.second += 1;
+    }
+  }
+};
+static void trace_dump() {
+  if (!trace_on()) return;
+  for (auto &kv : g_trace)
+    fprintf(stderr, "rbicg trace %-24s %10.3f ms  (%d)\n", kv.first.c_str(), kv.second.first,
+            kv.second.second);
+  g_trace.clear();
 }
 
 // ------------------------------------------------------------------ small helpers
@@ -351,7 +389,10 @@ struct Solver {
     for (int c = 0; c < kin; ++c) X.push_back(col(C, c, kin));
     for (int c = 0; c < kin; ++c) X.push_back(col(Ct, c, kin));
     std::vector<cplx> G;
-    gram<T>(X, X, n, G, ctx);
+    {
+      Phase ph("biorth.gram", ctx->stream);
+      gram<T>(X, X, n, G, ctx);
+    }
     const int m2 = 2 * kin;
     std::vector<int> kk;
     std::vector<double> nc(kin), nct(kin);
@@ -387,6 +428,7 @@ struct Solver {
       for (int c = 0; c < kin; ++c) v.push_back(col(B, c, kin));
       return v;
     };
+    Phase ph("biorth.gemm4", ctx->stream);
     gemm_panels<T>(cols_of(U), Fu, pk, n, out.U, ctx);
     gemm_panels<T>(cols_of(C), Fu, pk, n, out.C, ctx);
     gemm_panels<T>(cols_of(Ut), Fut, pk, n, out.Ut, ctx);
@@ -456,6 +498,7 @@ struct Solver {
     const int lo = std::max(0, (j - 1) * s - 1), hi = j * s;
     const int nrec = hi - lo + 1;
     const int kc = cur.k;
+    Phase ph_all("cycle.total", ctx->stream);
     std::vector<IterRec<T>> rec(nrec);
     std::vector<T> zh((size_t)nrec * std::max(kc, 1)), zth((size_t)nrec * std::max(kc, 1));
     RB_CUDA(cudaMemcpyAsync(rec.data(), hist + lo, sizeof(IterRec<T>) * nrec, cudaMemcpyDeviceToHost,
@@ -572,7 +615,10 @@ struct Solver {
         sy.push_back(1.0);
       }
       std::vector<cplx> Graw;
-      gram<T>(X, Y, n, Graw, ctx);
+      {
+        Phase ph("cycle.gram", ctx->stream);
+        gram<T>(X, Y, n, Graw, ctx);
+      }
       const int mY = (int)Y.size();
       std::vector<cplx> G1((size_t)mpsi * mpsi), G2((size_t)mpsi * (kx + s));
       for (int a = 0; a < mpsi; ++a) {
@@ -632,6 +678,7 @@ struct Solver {
     }
     // host QZ with left and right vectors + Q11/Q12 selection
     teig0 = now_ms();
+    Phase phe("cycle.host_eig", ctx->stream);
     std::vector<cplx> alpha, beta, VL, VR;
     std::vector<int> pf;
     RB_CHECK(lapack_ggev(real, mp, P, Q, alpha, beta, VL, VR, pf) == 0, RBICG_ELAPACK);
@@ -655,10 +702,16 @@ struct Solver {
         }
       }
       // U_j = Φ_j W_j, Ũ_j = Φ~_j W~_j; C_j = A U_j, C~_j = A^* Ũ_j
-      gemm_panels<T>(PhiCols, Wrow, ksel, n, tmp.U, ctx);
-      gemm_panels<T>(PhitCols, Wtrow, ksel, n, tmp.Ut, ctx);
-      launch_spmm<T>(M->A, tmp.U, tmp.C, ksel, ctx->stream);
-      launch_spmm<T>(M->AH, tmp.Ut, tmp.Ct, ksel, ctx->stream);
+      {
+        Phase ph("cycle.gemm_UW", ctx->stream);
+        gemm_panels<T>(PhiCols, Wrow, ksel, n, tmp.U, ctx);
+        gemm_panels<T>(PhitCols, Wtrow, ksel, n, tmp.Ut, ctx);
+      }
+      {
+        Phase ph("cycle.spmm", ctx->stream);
+        launch_spmm<T>(M->A, tmp.U, tmp.C, ksel, ctx->stream);
+        launch_spmm<T>(M->AH, tmp.Ut, tmp.Ct, ksel, ctx->stream);
+      }
       biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out);
     }
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -900,8 +953,11 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
     S.hst->stop_at = (S.hst->iter / opts->s + 1) * opts->s;
     S.push();
     const double tl = now_ms();
-    S.run_graph();
-    S.pull();
+    {
+      Phase ph("loop.graph", st);
+      S.run_graph();
+      S.pull();
+    }
     t_loop += now_ms() - tl;
     const int it = S.hst->iter;
     const bool boundary = it > 0 && it % opts->s == 0 && it / opts->s > last_cycle;
@@ -981,6 +1037,7 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
       memcpy(hist_out, hh.data(), sizeof(double) * hh.size());
   }
   RB_CUDA(cudaStreamSynchronize(st));
+  trace_dump();
   if (res) {
     memset(res, 0, sizeof(*res));
     res->status = status;
