@@ -16,6 +16,7 @@
 #include <map>
 #include <string>
 #include <mutex>
+#include <thread>
 
 #include "internal.h"
 
@@ -285,6 +286,8 @@ struct Solver {
   LoopArgs<T> la{};
   cudaGraphExec_t gexec = nullptr;
   int graph_iters = 0;
+  bool async_cycle = false;
+  cudaStream_t side = nullptr;
   double t_cycle_dev = 0, t_host_eig = 0, t_refresh = 0;
   int64_t launches0 = 0, graph_launch_kernels = 0;
 
@@ -294,6 +297,8 @@ struct Solver {
     return (T *)q;
   }
   ~Solver() {
+    if (worker.joinable()) worker.join();
+    if (side) cudaStreamDestroy(side);
     if (gexec) cudaGraphExecDestroy(gexec);
     for (void *q : owned) ws_free(q);
     if (hst) cudaFreeHost(hst);
@@ -307,6 +312,17 @@ struct Solver {
     real = (m->dtype == RBICG_F64);
     kmax = std::max(std::max(o.k, k_basis), 1);
     ring = o.s + 2;
+    if (o.k > 0 && o.update_recycle && !getenv("RBICG_SYNC_CYCLE")) {
+      size_t fr = 0, tot = 0;
+      RB_CUDA(cudaMemGetInfo(&fr, &tot));
+      const size_t extra = (size_t)2 * ring * n * sizeof(T);
+      const size_t need = extra + (size_t)(16 * kmax + 2 * ring + 16) * n * sizeof(T);
+      if (fr > need + ((size_t)2 << 30)) {
+        ring *= 2;
+        async_cycle = true;
+        RB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      }
+    }
     rring = alloc((size_t)ring * n);
     rtring = alloc((size_t)ring * n);
     for (int q = 0; q < 2; ++q) {
@@ -384,14 +400,15 @@ struct Solver {
 
   // Bi-orthogonalise (U, Ũ, C = AU, C~ = A^*Ũ) of width kin into `out`
   // (Q13: unit columns, absolute cut on the singular values).
-  void biorth(const T *U, const T *Ut, const T *C, const T *Ct, int kin, Basis &out) {
+  void biorth(const T *U, const T *Ut, const T *C, const T *Ct, int kin, Basis &out,
+              cudaStream_t bs) {
     std::vector<ColDesc> X;
     for (int c = 0; c < kin; ++c) X.push_back(col(C, c, kin));
     for (int c = 0; c < kin; ++c) X.push_back(col(Ct, c, kin));
     std::vector<cplx> G;
     {
-      Phase ph("biorth.gram", ctx->stream);
-      gram<T>(X, X, n, G, ctx);
+      Phase ph("biorth.gram", bs);
+      gram<T>(X, X, n, G, ctx, bs);
     }
     const int m2 = 2 * kin;
     std::vector<int> kk;
@@ -428,11 +445,11 @@ struct Solver {
       for (int c = 0; c < kin; ++c) v.push_back(col(B, c, kin));
       return v;
     };
-    Phase ph("biorth.gemm4", ctx->stream);
-    gemm_panels<T>(cols_of(U), Fu, pk, n, out.U, ctx);
-    gemm_panels<T>(cols_of(C), Fu, pk, n, out.C, ctx);
-    gemm_panels<T>(cols_of(Ut), Fut, pk, n, out.Ut, ctx);
-    gemm_panels<T>(cols_of(Ct), Fut, pk, n, out.Ct, ctx);
+    Phase ph("biorth.gemm4", bs);
+    gemm_panels<T>(cols_of(U), Fu, pk, n, out.U, ctx, bs);
+    gemm_panels<T>(cols_of(C), Fu, pk, n, out.C, ctx, bs);
+    gemm_panels<T>(cols_of(Ut), Fut, pk, n, out.Ut, ctx, bs);
+    gemm_panels<T>(cols_of(Ct), Fut, pk, n, out.Ct, ctx, bs);
   }
 
   // Per-system refresh: C = AU, C~ = A^*Ũ, then biorth into cur.
@@ -442,7 +459,7 @@ struct Solver {
     if (kin > 0) {
       launch_spmm<T>(M->A, U, tmp.C, kin, ctx->stream);
       launch_spmm<T>(M->AH, Ut, tmp.Ct, kin, ctx->stream);
-      biorth(U, Ut, tmp.C, tmp.Ct, kin, cur);
+      biorth(U, Ut, tmp.C, tmp.Ct, kin, cur, ctx->stream);
     }
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
     t_refresh += now_ms() - t0;
@@ -493,23 +510,24 @@ struct Solver {
 
   // ---------------------------------------------------------------- cycle end
   void cycle_end(int j) {
+    const cudaStream_t cs = async_cycle ? side : ctx->stream;
     const double t0 = now_ms();
     const int s = o.s;
     const int lo = std::max(0, (j - 1) * s - 1), hi = j * s;
     const int nrec = hi - lo + 1;
     const int kc = cur.k;
-    Phase ph_all("cycle.total", ctx->stream);
+    Phase ph_all("cycle.total", cs);
     std::vector<IterRec<T>> rec(nrec);
     std::vector<T> zh((size_t)nrec * std::max(kc, 1)), zth((size_t)nrec * std::max(kc, 1));
     RB_CUDA(cudaMemcpyAsync(rec.data(), hist + lo, sizeof(IterRec<T>) * nrec, cudaMemcpyDeviceToHost,
-                            ctx->stream));
+                            cs));
     if (kc > 0) {
       RB_CUDA(cudaMemcpyAsync(zh.data(), zhist + (size_t)lo * kc, sizeof(T) * nrec * kc,
-                              cudaMemcpyDeviceToHost, ctx->stream));
+                              cudaMemcpyDeviceToHost, cs));
       RB_CUDA(cudaMemcpyAsync(zth.data(), zthist + (size_t)lo * kc, sizeof(T) * nrec * kc,
-                              cudaMemcpyDeviceToHost, ctx->stream));
+                              cudaMemcpyDeviceToHost, cs));
     }
-    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    RB_CUDA(cudaStreamSynchronize(cs));
     auto R = [&](int m) -> const IterRec<T> & { return rec[m - lo]; };
     auto al = [&](int m) { return toc(R(m).alpha); };
     auto be = [&](int m) { return m == 0 ? cplx(0.0) : toc(R(m).beta); };
@@ -616,8 +634,8 @@ struct Solver {
       }
       std::vector<cplx> Graw;
       {
-        Phase ph("cycle.gram", ctx->stream);
-        gram<T>(X, Y, n, Graw, ctx);
+        Phase ph("cycle.gram", cs);
+        gram<T>(X, Y, n, Graw, ctx, cs);
       }
       const int mY = (int)Y.size();
       std::vector<cplx> G1((size_t)mpsi * mpsi), G2((size_t)mpsi * (kx + s));
@@ -678,7 +696,7 @@ struct Solver {
     }
     // host QZ with left and right vectors + Q11/Q12 selection
     teig0 = now_ms();
-    Phase phe("cycle.host_eig", ctx->stream);
+    Phase phe("cycle.host_eig", cs);
     std::vector<cplx> alpha, beta, VL, VR;
     std::vector<int> pf;
     RB_CHECK(lapack_ggev(real, mp, P, Q, alpha, beta, VL, VR, pf) == 0, RBICG_ELAPACK);
@@ -703,20 +721,51 @@ struct Solver {
       }
       // U_j = Φ_j W_j, Ũ_j = Φ~_j W~_j; C_j = A U_j, C~_j = A^* Ũ_j
       {
-        Phase ph("cycle.gemm_UW", ctx->stream);
-        gemm_panels<T>(PhiCols, Wrow, ksel, n, tmp.U, ctx);
-        gemm_panels<T>(PhitCols, Wtrow, ksel, n, tmp.Ut, ctx);
+        Phase ph("cycle.gemm_UW", cs);
+        gemm_panels<T>(PhiCols, Wrow, ksel, n, tmp.U, ctx, cs);
+        gemm_panels<T>(PhitCols, Wtrow, ksel, n, tmp.Ut, ctx, cs);
       }
       {
-        Phase ph("cycle.spmm", ctx->stream);
-        launch_spmm<T>(M->A, tmp.U, tmp.C, ksel, ctx->stream);
-        launch_spmm<T>(M->AH, tmp.Ut, tmp.Ct, ksel, ctx->stream);
+        Phase ph("cycle.spmm", cs);
+        launch_spmm<T>(M->A, tmp.U, tmp.C, ksel, cs);
+        launch_spmm<T>(M->AH, tmp.Ut, tmp.Ct, ksel, cs);
       }
-      biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out);
+      biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs);
     }
-    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    RB_CUDA(cudaStreamSynchronize(cs));
     cand_cur = nxt;
     t_cycle_dev += now_ms() - t0;
+  }
+
+  // Cycle ends overlap the next cycle's iterations: U_j is only used by the
+  // next system, and the doubled ring keeps cycle j's Lanczos
+  // columns intact while cycle j+1 runs.
+  std::thread worker;
+  int worker_err = 0;
+  void cycle_end_async(int j) {
+    join_cycle();
+    if (!async_cycle) {
+      cycle_end(j);
+      return;
+    }
+    worker = std::thread([this, j] {
+      try {
+        cudaSetDevice(ctx->device);
+        cycle_end(j);
+      } catch (Err &e) {
+        worker_err = e.code;
+      } catch (...) {
+        worker_err = RBICG_ESTATE;
+      }
+    });
+  }
+  void join_cycle() {
+    if (worker.joinable()) worker.join();
+    if (worker_err) {
+      const int e = worker_err;
+      worker_err = 0;
+      throw Err{e};
+    }
   }
 };
 
@@ -964,7 +1013,7 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
     const bool cyc_ok = S.hst->done == 2 ||
                         (S.hst->done == 1 && (S.hst->status == RBICG_OK || S.hst->status == RBICG_MAXITER));
     if (update && boundary && cyc_ok) {
-      S.cycle_end(it / opts->s);
+      S.cycle_end_async(it / opts->s);
       last_cycle = it / opts->s;
       ++cycles;
     }
@@ -994,6 +1043,7 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
     }
   }
   (void)t_loop0;
+  S.join_cycle();
   if (!finished_step7) launch_step7<T>(S.la, S.cur.U, S.cur.Ut, S.xo, S.xto, st);
   launch_resid<T>(S.la, S.b, S.bt, S.xo, S.xto, S.z, S.zt, 0, st);
   const DevState<T> fin = *S.hst;
@@ -1108,8 +1158,8 @@ int rbicg_bilinear(rbicg_ctx *ctx, const rbicg_mat *A, const void *u, const void
     if (e) throw Err{e};
     std::vector<ColDesc> X{{du, 1}, {dxt, 1}}, Y{{dx, 1}, {dz, 1}, {dw, 1}};
     std::vector<cplx> G;
-    if (A->dtype == RBICG_F64) gram<double>(X, Y, n, G, ctx);
-    else gram<zc>(X, Y, n, G, ctx);
+    if (A->dtype == RBICG_F64) gram<double>(X, Y, n, G, ctx, ctx->stream);
+    else gram<zc>(X, Y, n, G, ctx, ctx->stream);
     // x~^*(w - Ax) = x~^*w - x~^*(Ax)
     const cplx v = G[0 * 3 + 0] + (G[1 * 3 + 2] - G[1 * 3 + 1]);
     if (A->dtype == RBICG_F64) {
@@ -1169,7 +1219,7 @@ static void project_t(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, double t
   for (int c = 0; c < k; ++c) X.push_back(Solver<T>::col(S.cur.Ct, c, k));
   for (int c = 0; c < k; ++c) X.push_back(Solver<T>::col(S.cur.C, c, k));
   std::vector<cplx> G;
-  gram<T>(X, Y, n, G, ctx);
+  gram<T>(X, Y, n, G, ctx, ctx->stream);
   std::vector<T> hz(k), hzt(k);
   for (int j = 0; j < k; ++j) {
     hz[j] = fromc<T>(G[(size_t)j * 2 + 0] / S.cur.d[j]);

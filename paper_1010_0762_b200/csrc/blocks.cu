@@ -108,7 +108,7 @@ __global__ void k_gram_reduce(const T *__restrict__ part, int nchunks, int mXY, 
 
 template <typename T>
 void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
-          std::vector<cplx> &G, rbicg_ctx *ctx) {
+          std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t strm) {
   const int mX = (int)X.size(), mY = (int)Y.size();
   G.assign((size_t)mX * mY, cplx(0, 0));
   if (mX == 0 || mY == 0) return;
@@ -126,14 +126,14 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   T *dG = dpart + (size_t)nchunks * mX * mY;
   std::vector<ColDesc> both(X);
   both.insert(both.end(), Y.begin(), Y.end());
-  RB_CUDA(cudaMemcpyAsync(dX, both.data(), desc_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(dX, both.data(), desc_bytes, cudaMemcpyHostToDevice, strm));
   dim3 grid(tiles, nchunks);
-  k_gram<T><<<grid, 256, 0, ctx->stream>>>(dX, mX, dX + mX, mY, n, chunk, dpart);
-  k_gram_reduce<T><<<(mX * mY + 255) / 256, 256, 0, ctx->stream>>>(dpart, nchunks, mX * mY, dG);
+  k_gram<T><<<grid, 256, 0, strm>>>(dX, mX, dX + mX, mY, n, chunk, dpart);
+  k_gram_reduce<T><<<(mX * mY + 255) / 256, 256, 0, strm>>>(dpart, nchunks, mX * mY, dG);
   count_launch(2);
   std::vector<T> h((size_t)mX * mY);
-  RB_CUDA(cudaMemcpyAsync(h.data(), dG, g_bytes, cudaMemcpyDeviceToHost, ctx->stream));
-  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(h.data(), dG, g_bytes, cudaMemcpyDeviceToHost, strm));
+  RB_CUDA(cudaStreamSynchronize(strm));
   ws_free(buf);
   for (size_t i = 0; i < h.size(); ++i) G[i] = cplx(re(h[i]), im(h[i]));
 }
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(128) k_gemm_panels(const ColDesc *__restrict__
 
 template <typename T>
 void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int p, int64_t n,
-                 T *out, rbicg_ctx *ctx) {
+                 T *out, rbicg_ctx *ctx, cudaStream_t strm) {
   const int mX = (int)X.size();
   if (p <= 0) return;
   RB_CHECK(p <= KMAX, RBICG_EINVAL);
@@ -185,15 +185,15 @@ void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int 
   ColDesc *dX = (ColDesc *)buf;
   T *dM = (T *)(buf + ((desc_bytes + 15) / 16) * 16);
   if (mX) {
-    RB_CUDA(cudaMemcpyAsync(dX, X.data(), sizeof(ColDesc) * mX, cudaMemcpyHostToDevice, ctx->stream));
-    RB_CUDA(cudaMemcpyAsync(dM, hM.data(), sizeof(T) * hM.size(), cudaMemcpyHostToDevice, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(dX, X.data(), sizeof(ColDesc) * mX, cudaMemcpyHostToDevice, strm));
+    RB_CUDA(cudaMemcpyAsync(dM, hM.data(), sizeof(T) * hM.size(), cudaMemcpyHostToDevice, strm));
   }
   const size_t sm = sizeof(T) * (size_t)mX * p;
   RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
   const int grid = (int)std::min<int64_t>((n + 127) / 128, (int64_t)ctx->nsm * 8);
-  k_gemm_panels<T><<<grid, 128, sm, ctx->stream>>>(dX, mX, dM, p, n, out);
+  k_gemm_panels<T><<<grid, 128, sm, strm>>>(dX, mX, dM, p, n, out);
   count_launch();
-  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  RB_CUDA(cudaStreamSynchronize(strm));
   ws_free(buf);
 }
 
@@ -205,9 +205,9 @@ void prepare_block_kernels() {
 #define RB_BINST(T)                                                                        \
   template void launch_spmm<T>(const DevMat &, const T *, T *, int, cudaStream_t);         \
   template void gram<T>(const std::vector<ColDesc> &, const std::vector<ColDesc> &, int64_t, \
-                        std::vector<cplx> &, rbicg_ctx *);                                 \
+                        std::vector<cplx> &, rbicg_ctx *, cudaStream_t);                   \
   template void gemm_panels<T>(const std::vector<ColDesc> &, const std::vector<cplx> &, int, \
-                               int64_t, T *, rbicg_ctx *);
+                               int64_t, T *, rbicg_ctx *, cudaStream_t);
 RB_BINST(double)
 RB_BINST(zc)
 

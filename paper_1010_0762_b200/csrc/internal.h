@@ -137,10 +137,10 @@ template <typename T>
 void launch_spmm(const DevMat &A, const T *X, T *Y, int k, cudaStream_t s);
 template <typename T>
 void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
-          std::vector<cplx> &G, rbicg_ctx *ctx);   // G = X^H Y (row-major mX x mY)
+          std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t s);   // G = X^H Y (row-major mX x mY)
 template <typename T>
 void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int p, int64_t n,
-                 T *out, rbicg_ctx *ctx);          // out (row-major n x p) = X M
+                 T *out, rbicg_ctx *ctx, cudaStream_t s);   // out (row-major n x p) = X M
 
 // ---- workspace helpers (api.cu)
 void *ws_alloc(size_t bytes);
