@@ -84,7 +84,7 @@ static void ws_release_all() {
 // ------------------------------------------------------------------ tracing
 // RBICG_TRACE=1: synchronise around each phase and print per-phase totals.
 static bool trace_on() {
-  static int on = getenv("RBICG_TRACE") ? 1 : 0;
+  static int on = (getenv("RBICG_TRACE") && atoi(getenv("RBICG_TRACE")) > 0) ? 1 : 0;
   return on;
 }
 static std::map<std::string, std::pair<double, int>> g_trace;
