@@ -49,12 +49,13 @@ template <typename T> void launch_spmm(const DevMat &A, const T *X, T *Y, int k,
 
 // ------------------------------------------------------------------ Gram
 constexpr int GT = 32;   // output tile edge
-constexpr int GR = 32;   // rows per smem sub-tile
+template <typename T> struct GramRows { static constexpr int v = sizeof(T) == 8 ? 64 : 32; };
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_gram(const ColDesc *__restrict__ X, int mX,
                                               const ColDesc *__restrict__ Y, int mY, int64_t n,
                                               int64_t chunk, T *__restrict__ part) {
+  constexpr int GR = GramRows<T>::v;   // rows per smem sub-tile
   __shared__ T sx[GR][GT + 1];
   __shared__ T sy[GR][GT + 1];
   const int tilesY = (mY + GT - 1) / GT;
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(256) k_gram(const ColDesc *__restrict__ X, int
       sy[rr][cc] = vy;
     }
     __syncthreads();
-#pragma unroll 8
+#pragma unroll 16
     for (int rr = 0; rr < GR; ++rr) {
       const T x0 = sx[rr][ta], x1 = sx[rr][ta + 16];
       const T y0 = sy[rr][tb], y1 = sy[rr][tb + 16];
@@ -113,8 +114,9 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   G.assign((size_t)mX * mY, cplx(0, 0));
   if (mX == 0 || mY == 0) return;
   const int tiles = ((mX + GT - 1) / GT) * ((mY + GT - 1) / GT);
-  int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096,
-                                                            (2 * ctx->nsm + tiles - 1) / tiles * 2));
+  int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 2047) / 2048,
+                                                            (8 * ctx->nsm + tiles - 1) / tiles));
+  constexpr int GR = GramRows<T>::v;
   const int64_t chunk = ((n + nchunks - 1) / nchunks + GR - 1) / GR * GR;
   nchunks = (int)((n + chunk - 1) / chunk);
   const size_t desc_bytes = sizeof(ColDesc) * (mX + mY);
@@ -140,30 +142,47 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
 
 // ------------------------------------------------------------------ panels x M
 // out[row, c] = Σ_a X_a[row] M[a, c]; one thread per row keeps the whole output
-// row in registers, so out may alias an input panel with the same layout.
-template <typename T>
-__global__ void __launch_bounds__(128) k_gemm_panels(const ColDesc *__restrict__ X, int mX,
+// row in registers (PB >= p accumulators), so out may alias an input panel
+// with the same layout.  Column loads are coalesced across the warp for
+// vector columns; M lives in shared memory.
+template <typename T, int PB>
+__global__ void __launch_bounds__(256) k_gemm_panels(const ColDesc *__restrict__ X, int mX,
                                                      const T *__restrict__ M, int p, int64_t n,
                                                      T *out) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
-  T *sM = reinterpret_cast<T *>(sm_raw);
-  for (int e = threadIdx.x; e < mX * p; e += blockDim.x) sM[e] = M[e];
+  T *sM = reinterpret_cast<T *>(sm_raw);                 // [mX][PB], zero padded
+  ColDesc *sX = reinterpret_cast<ColDesc *>(sM + (size_t)mX * PB);
+  for (int e = threadIdx.x; e < mX * PB; e += blockDim.x) {
+    const int a = e / PB, c = e % PB;
+    sM[e] = c < p ? M[a * p + c] : zero<T>();
+  }
+  for (int e = threadIdx.x; e < mX; e += blockDim.x) sX[e] = X[e];
   __syncthreads();
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
        row += (int64_t)gridDim.x * blockDim.x) {
-    T acc[KMAX];
+    T acc[PB];
 #pragma unroll
-    for (int c = 0; c < KMAX; ++c) acc[c] = zero<T>();
+    for (int c = 0; c < PB; ++c) acc[c] = zero<T>();
+#pragma unroll 4
     for (int a = 0; a < mX; ++a) {
-      const T xv = ldp<T>(X[a].p, row * X[a].stride);
+      const T xv = ldp<T>(sX[a].p, row * sX[a].stride);
 #pragma unroll
-      for (int c = 0; c < KMAX; ++c)
-        if (c < p) acc[c] = mad(xv, sM[a * p + c], acc[c]);
+      for (int c = 0; c < PB; ++c) acc[c] = mad(xv, sM[a * PB + c], acc[c]);
     }
 #pragma unroll
-    for (int c = 0; c < KMAX; ++c)
+    for (int c = 0; c < PB; ++c)
       if (c < p) out[row * p + c] = acc[c];
   }
+}
+
+template <typename T, int PB>
+static void gemm_launch(const ColDesc *dX, int mX, const T *dM, int p, int64_t n, T *out,
+                        rbicg_ctx *ctx, cudaStream_t strm) {
+  const size_t sm = sizeof(T) * (size_t)mX * PB + sizeof(ColDesc) * mX;
+  RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 8);
+  k_gemm_panels<T, PB><<<grid, 256, sm, strm>>>(dX, mX, dM, p, n, out);
+  count_launch();
 }
 
 template <typename T>
@@ -188,18 +207,25 @@ void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int 
     RB_CUDA(cudaMemcpyAsync(dX, X.data(), sizeof(ColDesc) * mX, cudaMemcpyHostToDevice, strm));
     RB_CUDA(cudaMemcpyAsync(dM, hM.data(), sizeof(T) * hM.size(), cudaMemcpyHostToDevice, strm));
   }
-  const size_t sm = sizeof(T) * (size_t)mX * p;
-  RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
-  const int grid = (int)std::min<int64_t>((n + 127) / 128, (int64_t)ctx->nsm * 8);
-  k_gemm_panels<T><<<grid, 128, sm, strm>>>(dX, mX, dM, p, n, out);
-  count_launch();
+  if (p <= 4) gemm_launch<T, 4>(dX, mX, dM, p, n, out, ctx, strm);
+  else if (p <= 8) gemm_launch<T, 8>(dX, mX, dM, p, n, out, ctx, strm);
+  else if (p <= 12) gemm_launch<T, 12>(dX, mX, dM, p, n, out, ctx, strm);
+  else if (p <= 16) gemm_launch<T, 16>(dX, mX, dM, p, n, out, ctx, strm);
+  else if (p <= 24) gemm_launch<T, 24>(dX, mX, dM, p, n, out, ctx, strm);
+  else gemm_launch<T, 32>(dX, mX, dM, p, n, out, ctx, strm);
   RB_CUDA(cudaStreamSynchronize(strm));
   ws_free(buf);
 }
 
 void prepare_block_kernels() {
-  RB_CUDA(cudaFuncSetAttribute(k_gemm_panels<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  RB_CUDA(cudaFuncSetAttribute(k_gemm_panels<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+#define RB_GATTR(T, PB)                                                                      \
+  RB_CUDA(cudaFuncSetAttribute(k_gemm_panels<T, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                               200 * 1024));
+  RB_GATTR(double, 4) RB_GATTR(double, 8) RB_GATTR(double, 12) RB_GATTR(double, 16)
+  RB_GATTR(double, 24) RB_GATTR(double, 32)
+  RB_GATTR(zc, 4) RB_GATTR(zc, 8) RB_GATTR(zc, 12) RB_GATTR(zc, 16) RB_GATTR(zc, 24)
+  RB_GATTR(zc, 32)
+#undef RB_GATTR
 }
 
 #define RB_BINST(T)                                                                        \
