@@ -54,30 +54,36 @@ template <typename T> struct GramRows { static constexpr int v = sizeof(T) == 8 
 template <typename T>
 __global__ void __launch_bounds__(256) k_gram(const ColDesc *__restrict__ X, int mX,
                                               const ColDesc *__restrict__ Y, int mY, int64_t n,
-                                              int64_t chunk, T *__restrict__ part) {
+                                              int64_t chunk, unsigned xrow_fast, unsigned yrow_fast,
+                                              T *__restrict__ part) {
   constexpr int GR = GramRows<T>::v;   // rows per smem sub-tile
   __shared__ T sx[GR][GT + 1];
   __shared__ T sy[GR][GT + 1];
   const int tilesY = (mY + GT - 1) / GT;
-  const int tx0 = (blockIdx.x / tilesY) * GT, ty0 = (blockIdx.x % tilesY) * GT;
+  const int txi = blockIdx.x / tilesY, tyi = blockIdx.x % tilesY;
+  const int tx0 = txi * GT, ty0 = tyi * GT;
+  // per 32-column group: rows fastest (vector columns, coalesced down a
+  // column) or columns fastest (row-major panels, coalesced along a row)
+  const bool xr = (xrow_fast >> txi) & 1u, yr = (yrow_fast >> tyi) & 1u;
   const int64_t r0 = (int64_t)blockIdx.y * chunk;
   const int64_t r1 = min(n, r0 + chunk);
   const int tid = threadIdx.x;
-  // each thread: 2 x 2 outputs (a = ta + 16*u, b = tb + 16*v)
   const int ta = tid / 16, tb = tid % 16;
   T acc[2][2] = {{zero<T>(), zero<T>()}, {zero<T>(), zero<T>()}};
   for (int64_t rb = r0; rb < r1; rb += GR) {
-    // load: rr fastest (coalesced for vector columns)
     for (int e = tid; e < GR * GT; e += 256) {
-      const int rr = e % GR, cc = e / GR;
+      const int rr = xr ? e % GR : e / GT, cc = xr ? e / GR : e % GT;
       const int64_t row = rb + rr;
-      T vx = zero<T>(), vy = zero<T>();
-      if (row < r1) {
-        if (tx0 + cc < mX) vx = conj(ldp<T>(X[tx0 + cc].p, row * X[tx0 + cc].stride));
-        if (ty0 + cc < mY) vy = ldp<T>(Y[ty0 + cc].p, row * Y[ty0 + cc].stride);
-      }
-      sx[rr][cc] = vx;
-      sy[rr][cc] = vy;
+      T v = zero<T>();
+      if (row < r1 && tx0 + cc < mX) v = conj(ldp<T>(X[tx0 + cc].p, row * X[tx0 + cc].stride));
+      sx[rr][cc] = v;
+    }
+    for (int e = tid; e < GR * GT; e += 256) {
+      const int rr = yr ? e % GR : e / GT, cc = yr ? e / GR : e % GT;
+      const int64_t row = rb + rr;
+      T v = zero<T>();
+      if (row < r1 && ty0 + cc < mY) v = ldp<T>(Y[ty0 + cc].p, row * Y[ty0 + cc].stride);
+      sy[rr][cc] = v;
     }
     __syncthreads();
 #pragma unroll 16
@@ -98,13 +104,15 @@ __global__ void __launch_bounds__(256) k_gram(const ColDesc *__restrict__ X, int
     }
 }
 
+// one warp per output entry: lanes sum chunks strided by 32, fixed shuffle tree
 template <typename T>
 __global__ void k_gram_reduce(const T *__restrict__ part, int nchunks, int mXY, T *__restrict__ G) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= mXY) return;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, l = threadIdx.x & 31;
+  if (w >= mXY) return;
   T s = zero<T>();
-  for (int c = 0; c < nchunks; ++c) s = add(s, part[(int64_t)c * mXY + i]);
-  G[i] = s;
+  for (int c = l; c < nchunks; c += 32) s = add(s, part[(int64_t)c * mXY + w]);
+  s = warp_sum(s);
+  if (l == 0) G[w] = s;
 }
 
 template <typename T>
@@ -129,9 +137,18 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   std::vector<ColDesc> both(X);
   both.insert(both.end(), Y.begin(), Y.end());
   RB_CUDA(cudaMemcpyAsync(dX, both.data(), desc_bytes, cudaMemcpyHostToDevice, strm));
+  auto flags = [](const std::vector<ColDesc> &V) {
+    unsigned f = 0;
+    for (size_t g = 0; g * GT < V.size() && g < 32; ++g) {
+      bool vec = true;
+      for (size_t c = g * GT; c < std::min(V.size(), (g + 1) * GT); ++c) vec &= V[c].stride == 1;
+      if (vec) f |= 1u << g;
+    }
+    return f;
+  };
   dim3 grid(tiles, nchunks);
-  k_gram<T><<<grid, 256, 0, strm>>>(dX, mX, dX + mX, mY, n, chunk, dpart);
-  k_gram_reduce<T><<<(mX * mY + 255) / 256, 256, 0, strm>>>(dpart, nchunks, mX * mY, dG);
+  k_gram<T><<<grid, 256, 0, strm>>>(dX, mX, dX + mX, mY, n, chunk, flags(X), flags(Y), dpart);
+  k_gram_reduce<T><<<(mX * mY * 32 + 255) / 256, 256, 0, strm>>>(dpart, nchunks, mX * mY, dG);
   count_launch(2);
   std::vector<T> h((size_t)mX * mY);
   RB_CUDA(cudaMemcpyAsync(h.data(), dG, g_bytes, cudaMemcpyDeviceToHost, strm));
