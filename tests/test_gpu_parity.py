@@ -324,3 +324,53 @@ def test_edge_cases(ctx):
     x, xt, res, _ = ctx.solve_dual(M, e1, e2, k=0, s=4, tol=1e-12, max_itn=10,
                                    xt_redraw=vec(n, 7))
     assert res["status"] == 0
+
+
+# ------------------------------------------------------------------ full size
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_full_size_spmv_pair(ctx, name):
+    """BASELINE sizes (C2: n = 1,048,576; C3: n = 7,077,888): the SpMV pair
+    of the device SELL store vs scipy, 1e-12 norm-wise."""
+    cfg = CONFIGS[name]
+    it = next(system_sequence(cfg, systems=[0]))
+    A = _csr((it["indptr"], it["indices"], it["data"]))
+    M = ctx.matrix(it["indptr"], it["indices"], it["data"])
+    p, pt = it["b"], it["bt"]
+    z, zt = ctx.spmv_pair(M, p, pt)
+    zr, ztr = A @ p, A.T @ pt
+    assert np.linalg.norm(z - zr) <= 1e-12 * np.linalg.norm(zr)
+    assert np.linalg.norm(zt - ztr) <= 1e-12 * np.linalg.norm(ztr)
+    M.free()
+
+
+def test_full_size_c2_matched_iterations(ctx):
+    """C2 system 0 at full size in the bench configuration: both sides run
+    exactly 2s + 3 iterations (two cycle ends, Q27 force_iters), then
+    compare iterates, the recycle space they build, and the recursive vs
+    true residual relation; then the next system from that space."""
+    from oracle import rbicg as R
+    cfg = CONFIGS["C2"]
+    items = list(system_sequence(cfg, systems=[0, 1]))
+    m = 2 * cfg.s + 3
+    rec = ctx.recycle(cfg.n, cfg.k)
+    U = Ut = None
+    for item in items:
+        A = _csr((item["indptr"], item["indices"], item["data"]))
+        ref = R.solve_dual(A, item["b"], item["bt"], U=U, Ut=Ut, k=cfg.k, s=cfg.s,
+                           tol=cfg.tol, max_itn=m, trunc_tol=cfg.trunc_tol,
+                           force_iters=m)
+        if U is not None and U.shape[1]:
+            rec.import_(U, Ut)
+        M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+        x, xt, res, h = ctx.solve_dual(M, item["b"], item["bt"], R=rec, k=cfg.k,
+                                       s=cfg.s, tol=cfg.tol, max_itn=m,
+                                       trunc_tol=cfg.trunc_tol, force_iters=m,
+                                       history=True)
+        assert res["iterations"] == m and res["cycles"] == ref.cycles == 2
+        assert np.linalg.norm(x - ref.x) <= 1e-7 * np.linalg.norm(ref.x)
+        assert np.linalg.norm(xt - ref.xt) <= 1e-7 * np.linalg.norm(ref.xt)
+        np.testing.assert_allclose(h[:, 0], np.array(ref.hist["rnorm"][1:]) /
+                                   np.linalg.norm(item["b"]), rtol=1e-6)
+        assert res["k_out"] == ref.basis_out.k
+        U, Ut = ref.basis_out.U, ref.basis_out.Ut
+        M.free()
