@@ -367,6 +367,8 @@ struct Solver {
     la.AH = M->AH;
     la.tile_max = std::max(M->A.tile_max, M->AH.tile_max);
     la.staged = (2.0 * la.tile_max * (4 + sizeof(T)) <= 96 * 1024 && !getenv("RBICG_NO_TMA")) ? 1 : 0;
+    la.pass2_tma = getenv("RBICG_NO_TMA2") ? 0 : 1;
+    la.nsm = ctx->nsm;
     la.rring = rring;
     la.rtring = rtring;
     la.p[0] = p[0];

@@ -57,6 +57,8 @@ struct LoopArgs {
   int64_t n;
   int k, ring, G;
   int staged, tile_max;    // pass 1 stages SELL tiles in smem via TMA
+  int pass2_tma;           // pass 2 streams its tiles through smem via TMA
+  int nsm;
   DevMat A, AH;
   T *rring, *rtring;       // ring of residual columns (r_m in column m % ring)
   T *p[2], *pt[2];         // ping-pong search directions

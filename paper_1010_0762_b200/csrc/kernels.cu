@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
 
 // ============================================================== pass 2
 template <typename T>
-__global__ void __launch_bounds__(BS, 4) k_pass2(LoopArgs<T> a, int staged) {
+__global__ void __launch_bounds__(BS, 3) k_pass2(LoopArgs<T> a, int staged) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ T s_zeta[KMAX], s_zetat[KMAX];
   __shared__ T s_w[BS / 32];
@@ -377,53 +377,100 @@ __global__ void __launch_bounds__(BS, 4) k_pass2(LoopArgs<T> a, int staged) {
   T *__restrict__ rtnew = a.rtring + (int64_t)((it + 1) % a.ring) * n;
   const T *__restrict__ pn = a.p[(it + 1) & 1];
   const T *__restrict__ ptn = a.pt[(it + 1) & 1];
-  T *sC = reinterpret_cast<T *>(smem_raw);
-  T *sCt = sC + BS * k;
   T arho = zero<T>();
   double an = 0.0, ant = 0.0;
   const int64_t ntiles = (n + BS - 1) / BS;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t row0 = tile * BS;
-    const int rows = (int)min((int64_t)BS, n - row0);
-    if (k > 0 && staged) {
-      const T *__restrict__ C = a.C + row0 * k;
-      const T *__restrict__ Ct = a.Ct + row0 * k;
-      const int nel = rows * k;
-      for (int e = tid; e < nel; e += BS) {
-        sC[e] = ldcs(C + e);
-        sCt[e] = ldcs(Ct + e);
+  const int64_t nfull = n / BS;
+  // row update shared by the staged and the direct path
+  auto update_row = [&](int64_t row, T q, T qt, T ro, T rto, T pv, T ptv, T xv, T xtv,
+                        const T *cr, const T *ctr) {
+    if (k > 0) {
+      T d = zero<T>(), dt = zero<T>();
+      for (int j = 0; j < k; ++j) {
+        d = mad(cr[j], s_zeta[j], d);
+        dt = mad(ctr[j], s_zetat[j], dt);
       }
-      __syncthreads();
+      q = sub(q, d);     // q_i = z_i - C ζ_i
+      qt = sub(qt, dt);  // q~_i = z~_i - C~ ζ~_i
     }
-    if (tid < rows) {
-      const int64_t row = row0 + tid;
-      // all independent loads first (no aliasing stalls behind the stores)
-      T q = ldcs(a.z + row), qt = ldcs(a.zt + row);
-      const T ro = ldcs(rold + row), rto = ldcs(rtold + row);
-      const T pv = ldg(pn + row), ptv = ldg(ptn + row);
-      const T xv = ldcs(a.x + row), xtv = ldcs(a.xt + row);
+    const T rn = sub(ro, mul(alpha, q));
+    const T rtn = sub(rto, mul(ca, qt));
+    a.x[row] = mad(alpha, pv, xv);
+    a.xt[row] = mad(ca, ptv, xtv);
+    rnew[row] = rn;
+    rtnew[row] = rtn;
+    arho = cmad(rtn, rn, arho);
+    an += abs2(rn);
+    ant += abs2(rtn);
+  };
+  if (staged) {
+    // TMA double buffering: each full 256-row tile of the ten input streams
+    // (z, z~, r, r~, p, p~, x, x~ and the C, C~ tiles) is bulk-copied into
+    // shared memory while the previous tile is being processed.
+    __shared__ uint64_t bars[2];
+    const int64_t stage = (int64_t)8 * BS + (int64_t)2 * BS * k;
+    T *sb = reinterpret_cast<T *>(smem_raw);
+    auto issue = [&](int64_t t, int si) {
+      T *b = sb + si * stage;
+      const int64_t r0 = t * BS;
+      const uint32_t vb = BS * (uint32_t)sizeof(T);
+      const uint32_t cb = (uint32_t)(BS * k * sizeof(T));
+      mbar_expect_tx(&bars[si], 8u * vb + 2u * cb);
+      tma_load_1d(b + 0 * BS, a.z + r0, vb, &bars[si]);
+      tma_load_1d(b + 1 * BS, a.zt + r0, vb, &bars[si]);
+      tma_load_1d(b + 2 * BS, rold + r0, vb, &bars[si]);
+      tma_load_1d(b + 3 * BS, rtold + r0, vb, &bars[si]);
+      tma_load_1d(b + 4 * BS, pn + r0, vb, &bars[si]);
+      tma_load_1d(b + 5 * BS, ptn + r0, vb, &bars[si]);
+      tma_load_1d(b + 6 * BS, a.x + r0, vb, &bars[si]);
+      tma_load_1d(b + 7 * BS, a.xt + r0, vb, &bars[si]);
       if (k > 0) {
-        const T *cr = staged ? sC + tid * k : a.C + row * k;
-        const T *ctr = staged ? sCt + tid * k : a.Ct + row * k;
-        T d = zero<T>(), dt = zero<T>();
-        for (int j = 0; j < k; ++j) {
-          d = mad(cr[j], s_zeta[j], d);
-          dt = mad(ctr[j], s_zetat[j], dt);
-        }
-        q = sub(q, d);     // q_i = z_i - C ζ_i
-        qt = sub(qt, dt);  // q~_i = z~_i - C~ ζ~_i
+        tma_load_1d(b + 8 * BS, a.C + r0 * k, cb, &bars[si]);
+        tma_load_1d(b + 8 * BS + BS * k, a.Ct + r0 * k, cb, &bars[si]);
       }
-      const T rn = sub(ro, mul(alpha, q));
-      const T rtn = sub(rto, mul(ca, qt));
-      a.x[row] = mad(alpha, pv, xv);
-      a.xt[row] = mad(ca, ptv, xtv);
-      rnew[row] = rn;
-      rtnew[row] = rtn;
-      arho = cmad(rtn, rn, arho);
-      an += abs2(rn);
-      ant += abs2(rtn);
+    };
+    if (tid == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      fence_mbar_init();
     }
-    if (k > 0 && staged) __syncthreads();
+    __syncthreads();
+    if (tid == 0 && (int64_t)blockIdx.x < nfull) issue(blockIdx.x, 0);
+    uint32_t ph[2] = {0u, 0u};
+    int i = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+      const int si = i & 1;
+      const int64_t nxt = tile + gridDim.x;
+      if (tid == 0 && nxt < nfull) issue(nxt, si ^ 1);
+      const int64_t row0 = tile * BS;
+      if (tile < nfull) {
+        mbar_wait(&bars[si], ph[si]);
+        ph[si] ^= 1u;
+        const T *b = sb + si * stage;
+        update_row(row0 + tid, b[tid], b[BS + tid], b[2 * BS + tid], b[3 * BS + tid],
+                   b[4 * BS + tid], b[5 * BS + tid], b[6 * BS + tid], b[7 * BS + tid],
+                   b + 8 * BS + tid * k, b + 8 * BS + BS * k + tid * k);
+      } else if (tid < (int)(n - row0)) {
+        const int64_t row = row0 + tid;
+        update_row(row, a.z[row], a.zt[row], rold[row], rtold[row], pn[row], ptn[row], a.x[row],
+                   a.xt[row], a.C + row * k, a.Ct + row * k);
+      }
+      __syncthreads();   // stage si consumed before it is refilled
+    }
+  } else {
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t row0 = tile * BS;
+      const int rows = (int)min((int64_t)BS, n - row0);
+      if (tid < rows) {
+        const int64_t row = row0 + tid;
+        // all independent loads first (no aliasing stalls behind the stores)
+        const T q = ldcs(a.z + row), qt = ldcs(a.zt + row);
+        const T ro = ldcs(rold + row), rto = ldcs(rtold + row);
+        const T pv = ldg(pn + row), ptv = ldg(ptn + row);
+        const T xv = ldcs(a.x + row), xtv = ldcs(a.xt + row);
+        update_row(row, q, qt, ro, rto, pv, ptv, xv, xtv, a.C + row * k, a.Ct + row * k);
+      }
+    }
   }
   const int G = gridDim.x;
   const T b0 = block_sum(arho, s_w);
@@ -703,13 +750,19 @@ template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s) {
   count_launch();
 }
 
-template <typename T> size_t pass2_smem(int k) { return (size_t)2 * BS * k * sizeof(T); }
+// two stages of (8 vector tiles + C, C~ tiles)
+template <typename T> size_t pass2_smem(int k) {
+  return (size_t)2 * (8 * BS + 2 * BS * k) * sizeof(T);
+}
 
 template <typename T> void launch_pass2(const LoopArgs<T> &a, cudaStream_t s) {
   size_t sm = pass2_smem<T>(a.k);
-  int staged = (a.k > 0 && sm <= 160 * 1024) ? 1 : 0;
+  const int staged = (sm <= 200 * 1024 && a.pass2_tma) ? 1 : 0;
   if (!staged) sm = 0;
-  k_pass2<T><<<grid_for(a.n, a.G), BS, sm, s>>>(a, staged);
+  int per_sm = 1;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass2<T>, BS, sm));
+  const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
+  k_pass2<T><<<grid_for(a.n, G), BS, sm, s>>>(a, staged);
   count_launch();
 }
 
@@ -748,8 +801,8 @@ int stream_blocks_per_sm() {
 void prepare_kernels() {
   RB_CUDA(cudaFuncSetAttribute(k_pass1<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_pass1<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-  RB_CUDA(cudaFuncSetAttribute(k_pass2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-  RB_CUDA(cudaFuncSetAttribute(k_pass2<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_pass2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_pass2<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   prepare_block_kernels();
 }
 
