@@ -20,10 +20,12 @@
 // CUDA graph of s iterations is replayed for every cycle; once the state says
 // done/paused every kernel is a no-op (exact iteration counts, no host poll).
 #include "internal.h"
+#include <cstdlib>
 
 namespace rbicg {
 
 std::atomic<int64_t> g_launches{0};
+static const bool g_pdl = getenv("RBICG_NO_PDL") == nullptr;
 
 template <typename T> __device__ __forceinline__ T ldg(const T *p);
 template <> __device__ __forceinline__ double ldg<double>(const double *p) { return __ldg(p); }
@@ -39,6 +41,15 @@ template <> __device__ __forceinline__ zc ldcs<zc>(const zc *p) {
   return mk(v.x, v.y);
 }
 
+
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: the next kernel of the loop is launched while
+// this one drains; it may run its independent prologue (TMA of matrix tiles)
+// and then waits here for the full completion of its predecessor.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // ---------------------------------------------------------------- TMA / mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -186,22 +197,8 @@ __global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
   __shared__ T s_w[BS / 32];
   __shared__ int s_last;
   DevState<T> *st = a.st;
-  if (st->done) return;
   const int tid = threadIdx.x;
-  const int it = st->iter;
-  const T beta = st->beta;
-  const T cb = conj(beta);
   const int64_t n = a.n;
-  const T *__restrict__ r = a.rring + (int64_t)(it % a.ring) * n;
-  const T *__restrict__ rt = a.rtring + (int64_t)(it % a.ring) * n;
-  const T *__restrict__ pold = a.p[it & 1];
-  const T *__restrict__ ptold = a.pt[it & 1];
-  T *__restrict__ pnew = a.p[(it + 1) & 1];
-  T *__restrict__ ptnew = a.pt[(it + 1) & 1];
-  const int k = a.k;
-  const int rstep = k > 0 ? BS / k : 0;
-  const int kt = rstep * k;
-  T a1 = zero<T>(), a2 = zero<T>(), a3 = zero<T>(), aptz = zero<T>();
   const int64_t ntiles = (n + BS - 1) / BS;
   // TMA staging of the SELL tiles of A and A^* (one tile = 8 slices = BS rows)
   extern __shared__ __align__(128) unsigned char p1_smem[];
@@ -227,6 +224,7 @@ __global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
       tma_load_1d(svH, reinterpret_cast<const T *>(a.AH.vals) + oH, nH * (uint32_t)sizeof(T), &bar);
     }
   };
+  // prologue independent of the previous kernel: first matrix tile
   if (a.staged) {
     if (tid == 0) {
       mbar_init(&bar, 1);
@@ -235,6 +233,24 @@ __global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
     __syncthreads();
     if (tid == 0 && (int64_t)blockIdx.x < ntiles) issue(blockIdx.x);
   }
+  pdl_wait();
+  if (st->done) {
+    if (a.staged && (int64_t)blockIdx.x < ntiles) mbar_wait(&bar, 0);   // drain the copy
+    return;
+  }
+  const int it = st->iter;
+  const T beta = st->beta;
+  const T cb = conj(beta);
+  const T *__restrict__ r = a.rring + (int64_t)(it % a.ring) * n;
+  const T *__restrict__ rt = a.rtring + (int64_t)(it % a.ring) * n;
+  const T *__restrict__ pold = a.p[it & 1];
+  const T *__restrict__ ptold = a.pt[it & 1];
+  T *__restrict__ pnew = a.p[(it + 1) & 1];
+  T *__restrict__ ptnew = a.pt[(it + 1) & 1];
+  const int k = a.k;
+  const int rstep = k > 0 ? BS / k : 0;
+  const int kt = rstep * k;
+  T a1 = zero<T>(), a2 = zero<T>(), a3 = zero<T>(), aptz = zero<T>();
   uint32_t phase = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row0 = tile * BS;
@@ -301,6 +317,7 @@ __global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
       __syncthreads();
     }
   }
+  pdl_trigger();
   // ---- block reduction, fixed order
   const int G = gridDim.x;
   const int nout = 3 * k + 1;
@@ -359,6 +376,7 @@ __global__ void __launch_bounds__(BS, 3) k_pass2(LoopArgs<T> a, int staged) {
   __shared__ T s_fin[3];
   __shared__ int s_last;
   DevState<T> *st = a.st;
+  pdl_wait();
   if (st->done) return;
   const int tid = threadIdx.x;
   const int it = st->iter;
@@ -472,6 +490,7 @@ __global__ void __launch_bounds__(BS, 3) k_pass2(LoopArgs<T> a, int staged) {
       }
     }
   }
+  pdl_trigger();
   const int G = gridDim.x;
   const T b0 = block_sum(arho, s_w);
   double b1 = block_sum(an, reinterpret_cast<double *>(s_w));
@@ -744,9 +763,24 @@ static int grid_for(int64_t n, int G) {
 template <typename T> size_t pass1_smem(int tile_max) {
   return (size_t)2 * tile_max * (4 + sizeof(T));
 }
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), int grid, size_t sm, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(BS);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RB_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s) {
   const size_t sm = a.staged ? pass1_smem<T>(a.tile_max) : 0;
-  k_pass1<T><<<grid_for(a.n, a.G), BS, sm, s>>>(a);
+  launch_pdl(k_pass1<T>, grid_for(a.n, a.G), sm, s, a);
   count_launch();
 }
 
@@ -762,7 +796,7 @@ template <typename T> void launch_pass2(const LoopArgs<T> &a, cudaStream_t s) {
   int per_sm = 1;
   RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass2<T>, BS, sm));
   const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
-  k_pass2<T><<<grid_for(a.n, G), BS, sm, s>>>(a, staged);
+  launch_pdl(k_pass2<T>, grid_for(a.n, G), sm, s, a, staged);
   count_launch();
 }
 
