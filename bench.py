@@ -105,14 +105,15 @@ def build_systems(cfg, idx):
     return [got[j % cfg.systems] for j in idx]
 
 
-def alg_bytes(cfg_n, nnz, k, w=8):
+def alg_bytes(cfg_n, nnz, k, w=8, lazy_x=True):
     """Algorithmic HBM bytes per launch of the two hot kernels:
     pass 1 streams A and A^* (CSR-equivalent: values + int32 column indices +
     row pointers), C and C~ once, reads r, p, r~, p~ and writes p, p~, z, z~;
-    pass 2 reads C, C~, z, z~, r, r~, x, x~, p, p~ and writes r, r~, x, x~."""
+    pass 2 reads C, C~, z, z~, r, r~ and writes r, r~ (with lazy x; eager x
+    adds reads of x, x~, p, p~ and writes of x, x~)."""
     mat = 2 * (nnz * (w + 4) + 4 * (cfg_n + 1))
     p1 = mat + 2 * k * cfg_n * w + 8 * cfg_n * w
-    p2 = 2 * k * cfg_n * w + 12 * cfg_n * w
+    p2 = 2 * k * cfg_n * w + (6 if lazy_x else 12) * cfg_n * w
     return p1, p2
 
 
@@ -184,7 +185,7 @@ def run_gpu(args, rank, world):
                           trunc_tol=cfg.trunc_tol)
     A.free()
     w = 16 if cfg.complex else 8
-    p1, p2 = alg_bytes(cfg.n, cfg.nnz, kt["k"], w)
+    p1, p2 = alg_bytes(cfg.n, cfg.nnz, kt["k"], w, kt["lazy_x"])
     peak, peak_kind = hbm_peak()
     dom_bytes, dom_ms, dom = (p1, kt["pass1_ms"], "pass1") \
         if kt["pass1_ms"] >= kt["pass2_ms"] else (p2, kt["pass2_ms"], "pass2")
@@ -243,7 +244,8 @@ def run_gpu(args, rank, world):
                      "frac": achieved / peak, "traffic": None,
                      "alg_bytes_per_launch": dom_bytes,
                      "pass1_ms": kt["pass1_ms"], "pass2_ms": kt["pass2_ms"],
-                     "k_active": kt["k"],
+                     "k_active": kt["k"], "lazy_x": kt["lazy_x"],
+                     "tma_pass1": kt["tma_pass1"],
                      "iter_GBps": (p1 + p2) / ((kt["pass1_ms"] + kt["pass2_ms"]) * 1e-3) / 1e9},
         "e2e": e2e,
         "gpu_launches": int(launches),

@@ -159,9 +159,12 @@ int rbicg_dbg_project(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
                       void *zeta, void *zetat, int32_t *k_out, void *U,
                       void *Ut, void *C, void *Ct, double *d, int on_device);
 
-/* Per-kernel CUDA-event timing of `iters` hot-loop iterations on the resident
- * state of the last solve with this matrix (bench roofline).  ms[0] = average
- * duration of the SpMV-pair+coefficient kernel, ms[1] = the update kernel. */
+/* Per-kernel CUDA-event timing of `iters` hot-loop iterations (stop test off)
+ * on a fresh state for this matrix and R's recycle space (bench roofline).
+ * ms[6] out: [0] average duration (ms) of the SpMV-pair + coefficient kernel,
+ * [1] of the update kernel, [2] 0 if every timed launch did full work,
+ * [3] active recycle width k, [4] 1 if x is rebuilt lazily (the update kernel
+ * does not touch x, p), [5] 1 if pass 1 stages matrix tiles via TMA. */
 int rbicg_dbg_time_kernels(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
                            const rbicg_opts *opts, int iters, double *ms);
 

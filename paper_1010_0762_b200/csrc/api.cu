@@ -272,6 +272,8 @@ struct Solver {
   std::vector<void *> owned;
   T *rring = nullptr, *rtring = nullptr, *p[2] = {}, *pt[2] = {}, *z = nullptr, *zt = nullptr;
   T *x = nullptr, *xt = nullptr, *b = nullptr, *bt = nullptr, *xo = nullptr, *xto = nullptr;
+  T *pseg = nullptr, *ptseg = nullptr;
+  bool lazy_x = true;
   struct Basis {
     T *U = nullptr, *Ut = nullptr, *C = nullptr, *Ct = nullptr;
     int k = 0;
@@ -337,6 +339,9 @@ struct Solver {
     bt = alloc(n);
     xo = alloc(n);
     xto = alloc(n);
+    lazy_x = getenv("RBICG_EAGER_X") == nullptr;
+    pseg = alloc(n);
+    ptseg = alloc(n);
     for (Basis *B : {&cur, &cand[0], &cand[1], &tmp}) {
       B->U = alloc((size_t)n * kmax);
       B->Ut = alloc((size_t)n * kmax);
@@ -368,6 +373,9 @@ struct Solver {
     la.tile_max = std::max(M->A.tile_max, M->AH.tile_max);
     la.staged = (2.0 * la.tile_max * (4 + sizeof(T)) <= 96 * 1024 && !getenv("RBICG_NO_TMA")) ? 1 : 0;
     la.pass2_tma = getenv("RBICG_NO_TMA2") ? 0 : 1;
+    la.lazy_x = lazy_x ? 1 : 0;
+    la.pseg = pseg;
+    la.ptseg = ptseg;
     la.nsm = ctx->nsm;
     la.rring = rring;
     la.rtring = rtring;
@@ -474,6 +482,7 @@ struct Solver {
     if (o.force_iters > 0) hst->max_itn = o.force_iters;
     hst->k = cur.k;
     hst->stop_at = o.s;
+    hst->seg_start = 0;
     for (int j = 0; j < cur.k; ++j) hst->dinv[j] = 1.0 / cur.d[j];
     push();
   }
@@ -487,6 +496,53 @@ struct Solver {
     push();
     launch_init2<T>(la, cur.U, cur.Ut, ctx->stream);
     pull();
+  }
+
+  // Lazy x: over the open segment (a, b] the iterate update
+  // x_b = x_a + Σ_i α_i p_i is rebuilt from the Lanczos ring and p_a:
+  // x_b = x_a + c_p p_a + Σ_{l=a}^{b-1} c_l r_l with c_{b} = 0,
+  // c_l = α_{l+1} + β_{l+1} c_{l+1}, c_p = β_a c_a; the dual uses conj(c).
+  void flush_x(int bidx) {
+    const int a0 = hst->seg_start;
+    if (!lazy_x || bidx <= a0) {
+      hst->seg_start = bidx;
+      return;
+    }
+    const int m = bidx - a0;
+    std::vector<IterRec<T>> rec(m + 1);
+    RB_CUDA(cudaMemcpyAsync(rec.data(), hist + a0, sizeof(IterRec<T>) * (m + 1),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::vector<cplx> c(m + 1, 0.0);   // c[l - a0], l = a0..b-1 ; c[m] = c_p
+    cplx nxt = 0.0;
+    for (int l = bidx - 1; l >= a0; --l) {
+      const cplx al = toc(rec[l + 1 - a0].alpha);
+      const cplx be = (l + 1 < bidx) ? toc(rec[l + 1 - a0].beta) : cplx(0.0);
+      nxt = al + be * nxt;
+      c[l - a0] = nxt;
+    }
+    const cplx beta_a = a0 == 0 ? cplx(0.0) : toc(rec[0].beta);
+    const std::vector<cplx> cr = [&] {
+      std::vector<cplx> v(m + 2);
+      for (int l = 0; l < m; ++l) v[l] = c[l];
+      v[m] = beta_a * c[0];
+      v[m + 1] = 1.0;
+      return v;
+    }();
+    std::vector<cplx> cd(cr);
+    for (auto &v : cd) v = std::conj(v);
+    std::vector<ColDesc> X, Xt;
+    for (int l = a0; l < bidx; ++l) {
+      X.push_back(rcol(l));
+      Xt.push_back(rtcol(l));
+    }
+    X.push_back(ColDesc{pseg, 1});
+    Xt.push_back(ColDesc{ptseg, 1});
+    X.push_back(ColDesc{x, 1});
+    Xt.push_back(ColDesc{xt, 1});
+    gemm_panels<T>(X, cr, 1, n, x, ctx, ctx->stream);
+    gemm_panels<T>(Xt, cd, 1, n, xt, ctx, ctx->stream);
+    hst->seg_start = bidx;
   }
 
   void capture_graph() {
@@ -1010,6 +1066,7 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
       S.pull();
     }
     t_loop += now_ms() - tl;
+    S.flush_x(S.hst->iter);   // lazy x: close the segment at every pause/stop
     const int it = S.hst->iter;
     const bool boundary = it > 0 && it % opts->s == 0 && it / opts->s > last_cycle;
     const bool cyc_ok = S.hst->done == 2 ||
@@ -1320,6 +1377,8 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
   ms[1] = t2 / std::max(iters, 1);
   ms[2] = S.hst->done;   // 0 means every timed kernel did full work
   ms[3] = S.cur.k;
+  ms[4] = S.lazy_x ? 1.0 : 0.0;
+  ms[5] = S.la.staged;
 }
 
 int rbicg_dbg_time_kernels(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbicg_opts *opts,

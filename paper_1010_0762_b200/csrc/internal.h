@@ -34,7 +34,7 @@ struct DevState {
   int force;     // stop test disabled (Q27 protocol)
   int stop_at;   // pause after this iteration (cycle boundary)
   int k;
-  int pad0;
+  int seg_start;   // lazy x: first iteration index of the open segment
   unsigned cnt[4];
   T rho, beta, alpha, sigma;   // ρ_{i}, β_{i}, α_i, σ_i
   double rnorm, rtnorm;        // ||r_i||, ||r~_i||
@@ -58,6 +58,8 @@ struct LoopArgs {
   int k, ring, G;
   int staged, tile_max;    // pass 1 stages SELL tiles in smem via TMA
   int pass2_tma;           // pass 2 streams its tiles through smem via TMA
+  int lazy_x;              // x, x~ rebuilt per segment from the Lanczos ring
+  T *pseg, *ptseg;         // p_a, p~_a at the start of the open segment
   int nsm;
   DevMat A, AH;
   T *rring, *rtring;       // ring of residual columns (r_m in column m % ring)

@@ -25,7 +25,7 @@
 namespace rbicg {
 
 std::atomic<int64_t> g_launches{0};
-static const bool g_pdl = getenv("RBICG_NO_PDL") == nullptr;
+static const bool g_pdl = getenv("RBICG_PDL") != nullptr;   // measured: no gain
 
 template <typename T> __device__ __forceinline__ T ldg(const T *p);
 template <> __device__ __forceinline__ double ldg<double>(const double *p) { return __ldg(p); }
@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
     return;
   }
   const int it = st->iter;
+  const bool segcopy = a.lazy_x && it == st->seg_start;
   const T beta = st->beta;
   const T cb = conj(beta);
   const T *__restrict__ r = a.rring + (int64_t)(it % a.ring) * n;
@@ -271,8 +272,13 @@ __global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
         sell_pair_smem<T>(scA + (oA - bA) + lane, svA + (oA - bA) + lane, wA,
                           scH + (oH - bH) + lane, svH + (oH - bH) + lane, wH, r, pold, rt, ptold,
                           beta, cb, z, zt);
-        const T pn = mad(beta, ldg(pold + row), ldg(r + row));
-        const T ptn = mad(cb, ldg(ptold + row), ldg(rt + row));
+        const T po = ldg(pold + row), pto = ldg(ptold + row);
+        const T pn = mad(beta, po, ldg(r + row));
+        const T ptn = mad(cb, pto, ldg(rt + row));
+        if (segcopy) {   // lazy x: keep p_a, p~_a of the new segment
+          a.pseg[row] = po;
+          a.ptseg[row] = pto;
+        }
         pnew[row] = pn;
         ptnew[row] = ptn;
         a.z[row] = z;
@@ -288,8 +294,13 @@ __global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
       const int64_t row = row0 + tid;
       const T z = sell_row<T, true>(a.A, row, r, pold, beta);
       const T zt = sell_row<T, true>(a.AH, row, rt, ptold, cb);
-      const T pn = mad(beta, ldg(pold + row), ldg(r + row));
-      const T ptn = mad(cb, ldg(ptold + row), ldg(rt + row));
+      const T po = ldg(pold + row), pto = ldg(ptold + row);
+      const T pn = mad(beta, po, ldg(r + row));
+      const T ptn = mad(cb, pto, ldg(rt + row));
+      if (segcopy) {
+        a.pseg[row] = po;
+        a.ptseg[row] = pto;
+      }
       pnew[row] = pn;
       ptnew[row] = ptn;
       a.z[row] = z;
@@ -399,6 +410,7 @@ __global__ void __launch_bounds__(BS, 3) k_pass2(LoopArgs<T> a, int staged) {
   double an = 0.0, ant = 0.0;
   const int64_t ntiles = (n + BS - 1) / BS;
   const int64_t nfull = n / BS;
+  const bool lazy = a.lazy_x != 0;
   // row update shared by the staged and the direct path
   auto update_row = [&](int64_t row, T q, T qt, T ro, T rto, T pv, T ptv, T xv, T xtv,
                         const T *cr, const T *ctr) {
@@ -413,8 +425,10 @@ __global__ void __launch_bounds__(BS, 3) k_pass2(LoopArgs<T> a, int staged) {
     }
     const T rn = sub(ro, mul(alpha, q));
     const T rtn = sub(rto, mul(ca, qt));
-    a.x[row] = mad(alpha, pv, xv);
-    a.xt[row] = mad(ca, ptv, xtv);
+    if (!lazy) {
+      a.x[row] = mad(alpha, pv, xv);
+      a.xt[row] = mad(ca, ptv, xtv);
+    }
     rnew[row] = rn;
     rtnew[row] = rtn;
     arho = cmad(rtn, rn, arho);
@@ -433,15 +447,17 @@ __global__ void __launch_bounds__(BS, 3) k_pass2(LoopArgs<T> a, int staged) {
       const int64_t r0 = t * BS;
       const uint32_t vb = BS * (uint32_t)sizeof(T);
       const uint32_t cb = (uint32_t)(BS * k * sizeof(T));
-      mbar_expect_tx(&bars[si], 8u * vb + 2u * cb);
+      mbar_expect_tx(&bars[si], (lazy ? 4u : 8u) * vb + 2u * cb);
       tma_load_1d(b + 0 * BS, a.z + r0, vb, &bars[si]);
       tma_load_1d(b + 1 * BS, a.zt + r0, vb, &bars[si]);
       tma_load_1d(b + 2 * BS, rold + r0, vb, &bars[si]);
       tma_load_1d(b + 3 * BS, rtold + r0, vb, &bars[si]);
-      tma_load_1d(b + 4 * BS, pn + r0, vb, &bars[si]);
-      tma_load_1d(b + 5 * BS, ptn + r0, vb, &bars[si]);
-      tma_load_1d(b + 6 * BS, a.x + r0, vb, &bars[si]);
-      tma_load_1d(b + 7 * BS, a.xt + r0, vb, &bars[si]);
+      if (!lazy) {
+        tma_load_1d(b + 4 * BS, pn + r0, vb, &bars[si]);
+        tma_load_1d(b + 5 * BS, ptn + r0, vb, &bars[si]);
+        tma_load_1d(b + 6 * BS, a.x + r0, vb, &bars[si]);
+        tma_load_1d(b + 7 * BS, a.xt + r0, vb, &bars[si]);
+      }
       if (k > 0) {
         tma_load_1d(b + 8 * BS, a.C + r0 * k, cb, &bars[si]);
         tma_load_1d(b + 8 * BS + BS * k, a.Ct + r0 * k, cb, &bars[si]);
@@ -470,8 +486,10 @@ __global__ void __launch_bounds__(BS, 3) k_pass2(LoopArgs<T> a, int staged) {
                    b + 8 * BS + tid * k, b + 8 * BS + BS * k + tid * k);
       } else if (tid < (int)(n - row0)) {
         const int64_t row = row0 + tid;
-        update_row(row, a.z[row], a.zt[row], rold[row], rtold[row], pn[row], ptn[row], a.x[row],
-                   a.xt[row], a.C + row * k, a.Ct + row * k);
+        update_row(row, a.z[row], a.zt[row], rold[row], rtold[row],
+                   lazy ? zero<T>() : pn[row], lazy ? zero<T>() : ptn[row],
+                   lazy ? zero<T>() : a.x[row], lazy ? zero<T>() : a.xt[row], a.C + row * k,
+                   a.Ct + row * k);
       }
       __syncthreads();   // stage si consumed before it is refilled
     }
@@ -484,8 +502,13 @@ __global__ void __launch_bounds__(BS, 3) k_pass2(LoopArgs<T> a, int staged) {
         // all independent loads first (no aliasing stalls behind the stores)
         const T q = ldcs(a.z + row), qt = ldcs(a.zt + row);
         const T ro = ldcs(rold + row), rto = ldcs(rtold + row);
-        const T pv = ldg(pn + row), ptv = ldg(ptn + row);
-        const T xv = ldcs(a.x + row), xtv = ldcs(a.xt + row);
+        T pv = zero<T>(), ptv = zero<T>(), xv = zero<T>(), xtv = zero<T>();
+        if (!lazy) {
+          pv = ldg(pn + row);
+          ptv = ldg(ptn + row);
+          xv = ldcs(a.x + row);
+          xtv = ldcs(a.xt + row);
+        }
         update_row(row, q, qt, ro, rto, pv, ptv, xv, xtv, a.C + row * k, a.Ct + row * k);
       }
     }

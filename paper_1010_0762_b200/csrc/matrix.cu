@@ -89,7 +89,7 @@ static void csr_to_sell(rbicg_ctx *ctx, int64_t n, const int32_t *rowptr, const 
   out.n = n;
   out.nslices = (n + 31) / 32;
   int64_t *w32 = (int64_t *)ws_alloc(sizeof(int64_t) * (out.nslices + 1));
-  RB_CUDA(cudaMalloc(&out.sptr, sizeof(int64_t) * (out.nslices + 1)));
+  out.sptr = (int64_t *)ws_alloc(sizeof(int64_t) * (out.nslices + 1));
   k_slice_width<<<grid1d(out.nslices), 256, 0, st>>>(rowptr, n, out.nslices, w32);
   RB_CUDA(cudaMemsetAsync(w32 + out.nslices, 0, sizeof(int64_t), st));
   size_t tmp = 0;
@@ -107,8 +107,8 @@ static void csr_to_sell(rbicg_ctx *ctx, int64_t n, const int32_t *rowptr, const 
   out.tile_max = (int)std::min<int64_t>(tm, INT32_MAX);
   ws_free(dtmp);
   ws_free(w32);
-  RB_CUDA(cudaMalloc(&out.cols, sizeof(int32_t) * std::max<int64_t>(out.padded, 1)));
-  RB_CUDA(cudaMalloc(&out.vals, sizeof(T) * std::max<int64_t>(out.padded, 1)));
+  out.cols = (int32_t *)ws_alloc(sizeof(int32_t) * std::max<int64_t>(out.padded, 1));
+  out.vals = ws_alloc(sizeof(T) * std::max<int64_t>(out.padded, 1));
   k_sell_fill<T><<<grid1d(out.nslices * 32), 256, 0, st>>>(rowptr, col, val, n, out.nslices, out.sptr,
                                                            out.cols, (T *)out.vals);
   count_launch(2);
@@ -162,9 +162,10 @@ void build_matrix(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr_
 }
 
 void free_devmat(DevMat &m) {
-  if (m.sptr) cudaFree(m.sptr);
-  if (m.cols) cudaFree(m.cols);
-  if (m.vals) cudaFree(m.vals);
+  // pooled device memory (reused by the next system's store); no device sync
+  ws_free(m.sptr);
+  ws_free(m.cols);
+  ws_free(m.vals);
   m = DevMat();
 }
 

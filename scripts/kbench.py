@@ -25,7 +25,7 @@ for k in (0, cfg.k):
     mat = 2 * (nnz * (w + 4) + 4 * (n + 1))
     kk = t["k"]
     b1 = mat + 2 * kk * n * w + 8 * n * w
-    b2 = 2 * kk * n * w + 12 * n * w
+    b2 = 2 * kk * n * w + (6 if t["lazy_x"] else 12) * n * w
     print(json.dumps(dict(config=cfg.name, k=kk, pass1_ms=t["pass1_ms"], pass2_ms=t["pass2_ms"],
                           pass1_GBps=b1 / t["pass1_ms"] / 1e6, pass2_GBps=b2 / t["pass2_ms"] / 1e6,
                           iter_GBps=(b1 + b2) / (t["pass1_ms"] + t["pass2_ms"]) / 1e6, done=t["done_flag"])))
