@@ -1025,9 +1025,15 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
                    void *xt, const void *xt_redraw, rbicg_rec *R, const rbicg_opts *opts,
                    int on_device, rbicg_result *res, double *hist_out) {
   const double t_start = now_ms();
+  static const bool timing = getenv("RBICG_TIMING") != nullptr;
+  std::vector<std::pair<const char *, double>> marks;
+  auto mark = [&](const char *nm) {
+    if (timing) marks.emplace_back(nm, now_ms());
+  };
   Solver<T> S;
   const int kin = R ? R->k : 0;
   S.setup(ctx, A, *opts, kin);
+  mark("setup");
   const int64_t n = A->n;
   const size_t vb = sizeof(T) * n;
   cudaStream_t st = ctx->stream;
@@ -1040,10 +1046,12 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
   // Step 1 + refresh
   S.refresh(R && kin > 0 ? (const T *)R->U : nullptr, R && kin > 0 ? (const T *)R->Ut : nullptr,
             opts->k > 0 ? kin : 0);
+  mark("refresh");
   S.make_args();
   S.init_state();
   // Steps 2-3
   S.initial_projection();
+  mark("init");
   if (S.hst->done == 1 && S.hst->status == RBICG_BREAKDOWN_SERIOUS && xt_redraw) {
     copy_in(S.xt, xt_redraw, vb, on_device, st);
     S.initial_projection();
@@ -1055,6 +1063,8 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
   bool finished_step7 = false;
   const bool update = opts->update_recycle && opts->k > 0;
   if (!(S.hst->done == 1)) S.capture_graph();
+  mark("capture");
+  double t_flush = 0, t_cyc_launch = 0;
   while (S.hst->done != 1) {
     S.hst->done = 0;
     S.hst->stop_at = (S.hst->iter / opts->s + 1) * opts->s;
@@ -1066,13 +1076,17 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
       S.pull();
     }
     t_loop += now_ms() - tl;
+    const double tf0 = now_ms();
     S.flush_x(S.hst->iter);   // lazy x: close the segment at every pause/stop
+    t_flush += now_ms() - tf0;
     const int it = S.hst->iter;
     const bool boundary = it > 0 && it % opts->s == 0 && it / opts->s > last_cycle;
     const bool cyc_ok = S.hst->done == 2 ||
                         (S.hst->done == 1 && (S.hst->status == RBICG_OK || S.hst->status == RBICG_MAXITER));
     if (update && boundary && cyc_ok) {
+      const double tc0 = now_ms();
       S.cycle_end_async(it / opts->s);
+      t_cyc_launch += now_ms() - tc0;
       last_cycle = it / opts->s;
       ++cycles;
     }
@@ -1102,7 +1116,9 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
     }
   }
   (void)t_loop0;
+  mark("loop");
   S.join_cycle();
+  mark("join");
   if (!finished_step7) launch_step7<T>(S.la, S.cur.U, S.cur.Ut, S.xo, S.xto, st);
   launch_resid<T>(S.la, S.b, S.bt, S.xo, S.xto, S.z, S.zt, 0, st);
   const DevState<T> fin = *S.hst;
@@ -1147,6 +1163,17 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
   }
   RB_CUDA(cudaStreamSynchronize(st));
   trace_dump();
+  mark("finish");
+  if (timing) {
+    fprintf(stderr, "rbicg timing: iters %d loop(graph) %.2f flush %.2f cycle_launch+wait %.2f |", S.hst->iter,
+            t_loop, t_flush, t_cyc_launch);
+    double prev = t_start;
+    for (auto &m : marks) {
+      fprintf(stderr, " %s %.2f", m.first, m.second - prev);
+      prev = m.second;
+    }
+    fprintf(stderr, " total %.2f\n", now_ms() - t_start);
+  }
   if (res) {
     memset(res, 0, sizeof(*res));
     res->status = status;
