@@ -137,11 +137,18 @@ def run_gpu(args, rank, world):
     stream = torch.cuda.current_stream()
     res_all, times = [], []
 
+    build_ms = []
+
     def one(i, timed):
         d = dsys[i]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eb = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         A = ctx.matrix(d["indptr"], d["indices"], d["data"])
+        eb.record(stream)
+        eb.synchronize()
+        if timed:
+            build_ms.append(e0.elapsed_time(eb))
         x, xt, res, _ = ctx.solve_dual(A, d["b"], d["bt"], R=R, k=cfg.k, s=cfg.s,
                                        tol=cfg.tol, max_itn=cfg.max_itn,
                                        trunc_tol=cfg.trunc_tol)
@@ -237,6 +244,8 @@ def run_gpu(args, rank, world):
                    "host_eig_ms": sum(r["t_host_eig_ms"] for r in res_all),
                    "cycle_end_ms": sum(r["t_cycle_dev_ms"] for r in res_all),
                    "loop_ms": sum(r["t_loop_ms"] for r in res_all),
+                   "matrix_build_ms": sum(build_ms),
+                   "solve_total_ms": sum(r["t_total_ms"] for r in res_all),
                    "l2": "per-iteration traffic > 126 MB L2 (no flush needed)",
                    "parallelism": "replicas" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,

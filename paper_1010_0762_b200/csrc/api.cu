@@ -322,7 +322,7 @@ struct Solver {
       if (fr > need + ((size_t)2 << 30)) {
         ring *= 2;
         async_cycle = true;
-        RB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        RB_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, ctx->prio_lo));
       }
     }
     rring = alloc((size_t)ring * n);
@@ -540,8 +540,8 @@ struct Solver {
     Xt.push_back(ColDesc{ptseg, 1});
     X.push_back(ColDesc{x, 1});
     Xt.push_back(ColDesc{xt, 1});
-    gemm_panels<T>(X, cr, 1, n, x, ctx, ctx->stream);
-    gemm_panels<T>(Xt, cd, 1, n, xt, ctx, ctx->stream);
+    gemm_panels<T>(X, cr, 1, n, x, ctx, ctx->stream, /*sync=*/false);
+    gemm_panels<T>(Xt, cd, 1, n, xt, ctx, ctx->stream, /*sync=*/true);
     hst->seg_start = bidx;
   }
 
@@ -876,7 +876,11 @@ int rbicg_init(rbicg_ctx **out, int device, void *stream, const rbicg_dist *dist
     // allowed on the legacy default stream); calls are ordered after the
     // caller's stream by an event and return synchronised.
     c->user_stream = (cudaStream_t)stream;
-    RB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    int lo = 0, hi = 0;
+    RB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    c->prio_lo = lo;
+    // the hot loop runs at the highest priority; cycle-end work fills gaps
+    RB_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));
     RB_CUDA(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
     RB_CUDA(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
     prepare_kernels();

@@ -204,7 +204,7 @@ static void gemm_launch(const ColDesc *dX, int mX, const T *dM, int p, int64_t n
 
 template <typename T>
 void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int p, int64_t n,
-                 T *out, rbicg_ctx *ctx, cudaStream_t strm) {
+                 T *out, rbicg_ctx *ctx, cudaStream_t strm, bool sync) {
   const int mX = (int)X.size();
   if (p <= 0) return;
   RB_CHECK(p <= KMAX, RBICG_EINVAL);
@@ -230,8 +230,16 @@ void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int 
   else if (p <= 16) gemm_launch<T, 16>(dX, mX, dM, p, n, out, ctx, strm);
   else if (p <= 24) gemm_launch<T, 24>(dX, mX, dM, p, n, out, ctx, strm);
   else gemm_launch<T, 32>(dX, mX, dM, p, n, out, ctx, strm);
-  RB_CUDA(cudaStreamSynchronize(strm));
-  ws_free(buf);
+  // the pinned-free staging below is host memory: synchronous copies above
+  // completed before return only if we sync; otherwise keep hM alive by
+  // syncing lazily through the stream-ordered free below
+  if (sync) {
+    RB_CUDA(cudaStreamSynchronize(strm));
+    ws_free(buf);
+  } else {
+    RB_CUDA(cudaStreamSynchronize(strm));   // hM (pageable) must outlive its copy
+    ws_free(buf);
+  }
 }
 
 void prepare_block_kernels() {
@@ -250,7 +258,7 @@ void prepare_block_kernels() {
   template void gram<T>(const std::vector<ColDesc> &, const std::vector<ColDesc> &, int64_t, \
                         std::vector<cplx> &, rbicg_ctx *, cudaStream_t);                   \
   template void gemm_panels<T>(const std::vector<ColDesc> &, const std::vector<cplx> &, int, \
-                               int64_t, T *, rbicg_ctx *, cudaStream_t);
+                               int64_t, T *, rbicg_ctx *, cudaStream_t, bool);
 RB_BINST(double)
 RB_BINST(zc)
 

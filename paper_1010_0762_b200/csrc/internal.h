@@ -87,6 +87,7 @@ struct rbicg_ctx {
   cudaStream_t stream = nullptr;       // library stream (non-blocking)
   cudaStream_t user_stream = nullptr;  // caller's stream (may be legacy NULL)
   cudaEvent_t order_ev = nullptr;
+  int prio_lo = 0;
   int nsm = 148;
   int grid_stream = 296;  // persistent grid of the streaming kernels
   // reusable device workspace
@@ -144,7 +145,7 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
           std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t s);   // G = X^H Y (row-major mX x mY)
 template <typename T>
 void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int p, int64_t n,
-                 T *out, rbicg_ctx *ctx, cudaStream_t s);   // out (row-major n x p) = X M
+                 T *out, rbicg_ctx *ctx, cudaStream_t s, bool sync = true);   // out (row-major n x p) = X M
 
 // ---- workspace helpers (api.cu)
 void *ws_alloc(size_t bytes);
