@@ -17,9 +17,36 @@ template <typename T> __device__ __forceinline__ T ldp(const void *p, int64_t i)
 }
 
 // ------------------------------------------------------------------ SpMM
+// One block per SELL slice (32 rows) x k columns: the slice's column indices
+// and values are loaded once, coalesced, into shared memory; thread
+// (row lr, column j), j fastest, then gathers X rows (k contiguous values).
 template <typename T>
-__global__ void __launch_bounds__(256) k_spmm(DevMat A, const T *__restrict__ X, T *__restrict__ Y,
-                                              int k) {
+__global__ void __launch_bounds__(1024) k_spmm(DevMat A, const T *__restrict__ X, T *__restrict__ Y,
+                                               int k) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  const int64_t sl = blockIdx.x;
+  const int64_t off = A.sptr[sl];
+  const int w = (int)((A.sptr[sl + 1] - off) >> 5);
+  T *sv = reinterpret_cast<T *>(sm_raw);
+  int32_t *sc = reinterpret_cast<int32_t *>(sv + 32 * w);
+  for (int e = threadIdx.x; e < 32 * w; e += blockDim.x) {
+    sc[e] = A.cols[off + e];
+    sv[e] = reinterpret_cast<const T *>(A.vals)[off + e];
+  }
+  __syncthreads();
+  const int lr = threadIdx.x / k, j = threadIdx.x - lr * k;
+  const int64_t row = sl * 32 + lr;
+  if (lr >= 32 || row >= A.n) return;
+  T acc = zero<T>();
+#pragma unroll 4
+  for (int jj = 0; jj < w; ++jj) acc = mad(sv[jj * 32 + lr], X[(int64_t)sc[jj * 32 + lr] * k + j], acc);
+  Y[row * k + j] = acc;
+}
+
+// generic fallback for very wide slices: thread per (row, column)
+template <typename T>
+__global__ void __launch_bounds__(256) k_spmm_wide(DevMat A, const T *__restrict__ X,
+                                                   T *__restrict__ Y, int k) {
   const int64_t total = A.n * k;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -30,20 +57,23 @@ __global__ void __launch_bounds__(256) k_spmm(DevMat A, const T *__restrict__ X,
     const int64_t off = A.sptr[sl];
     const int w = (int)((A.sptr[sl + 1] - off) >> 5);
     T acc = zero<T>();
-    for (int jj = 0; jj < w; ++jj) {
-      const int c = A.cols[off + jj * 32 + lane];
-      const T v = reinterpret_cast<const T *>(A.vals)[off + jj * 32 + lane];
-      acc = mad(v, X[(int64_t)c * k + j], acc);
-    }
+    for (int jj = 0; jj < w; ++jj)
+      acc = mad(reinterpret_cast<const T *>(A.vals)[off + jj * 32 + lane],
+                X[(int64_t)A.cols[off + jj * 32 + lane] * k + j], acc);
     Y[idx] = acc;
   }
 }
 
 template <typename T> void launch_spmm(const DevMat &A, const T *X, T *Y, int k, cudaStream_t s) {
   if (k <= 0) return;
-  const int64_t total = A.n * k;
-  const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  k_spmm<T><<<grid, 256, 0, s>>>(A, X, Y, k);
+  RB_CHECK(k <= KMAX, RBICG_EINVAL);
+  const size_t sm = (size_t)32 * std::max(1, A.max_w) * (sizeof(T) + 4);
+  if (sm <= 48 * 1024) {
+    k_spmm<T><<<(int)A.nslices, 32 * k, sm, s>>>(A, X, Y, k);
+  } else {
+    const int grid = (int)std::min<int64_t>((A.n * k + 255) / 256, 148 * 16);
+    k_spmm_wide<T><<<grid, 256, 0, s>>>(A, X, Y, k);
+  }
   count_launch();
 }
 
@@ -180,7 +210,7 @@ __global__ void __launch_bounds__(256) k_gemm_panels(const ColDesc *__restrict__
     T acc[PB];
 #pragma unroll
     for (int c = 0; c < PB; ++c) acc[c] = zero<T>();
-#pragma unroll 4
+#pragma unroll 8
     for (int a = 0; a < mX; ++a) {
       const T xv = ldp<T>(sX[a].p, row * sX[a].stride);
 #pragma unroll
@@ -243,6 +273,8 @@ void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int 
 }
 
 void prepare_block_kernels() {
+  RB_CUDA(cudaFuncSetAttribute(k_spmm<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_spmm<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 #define RB_GATTR(T, PB)                                                                      \
   RB_CUDA(cudaFuncSetAttribute(k_gemm_panels<T, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                200 * 1024));

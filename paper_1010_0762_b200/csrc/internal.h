@@ -19,6 +19,7 @@ constexpr int BS = 256;    // threads per block of the streaming kernels
 struct DevMat {
   int64_t n = 0, nslices = 0, padded = 0;
   int tile_max = 0;         // max elements in one 256-row tile (8 slices)
+  int max_w = 0;            // widest slice (padded row length)
   int64_t *sptr = nullptr;  // nslices + 1 element offsets (multiples of 32)
   int32_t *cols = nullptr;
   void *vals = nullptr;

@@ -105,6 +105,9 @@ static void csr_to_sell(rbicg_ctx *ctx, int64_t n, const int32_t *rowptr, const 
   for (int64_t s0 = 0; s0 < out.nslices; s0 += BS / 32)
     tm = std::max(tm, hs[std::min(s0 + BS / 32, out.nslices)] - hs[s0]);
   out.tile_max = (int)std::min<int64_t>(tm, INT32_MAX);
+  int64_t mw = 0;
+  for (int64_t s0 = 0; s0 < out.nslices; ++s0) mw = std::max(mw, (hs[s0 + 1] - hs[s0]) / 32);
+  out.max_w = (int)std::min<int64_t>(mw, INT32_MAX);
   ws_free(dtmp);
   ws_free(w32);
   out.cols = (int32_t *)ws_alloc(sizeof(int32_t) * std::max<int64_t>(out.padded, 1));
