@@ -100,20 +100,38 @@ __global__ void __launch_bounds__(256) k_gram(const ColDesc *__restrict__ X, int
   const int tid = threadIdx.x;
   const int ta = tid / 16, tb = tid % 16;
   T acc[2][2] = {{zero<T>(), zero<T>()}, {zero<T>(), zero<T>()}};
+  // element e = tid + 256 q of a GR x GT sub-tile; the column (and its
+  // descriptor) each thread touches is fixed for the whole chunk -> hoisted
+  constexpr int NQ = GR * GT / 256;
+  const T *xp[NQ];
+  int64_t xs[NQ];
+  int xrr[NQ], xcc[NQ];
+  const T *yp[NQ];
+  int64_t ys[NQ];
+  int yrr[NQ], ycc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int e = tid + 256 * q;
+    xrr[q] = xr ? e % GR : e / GT;
+    xcc[q] = xr ? e / GR : e % GT;
+    yrr[q] = yr ? e % GR : e / GT;
+    ycc[q] = yr ? e / GR : e % GT;
+    const bool xv = tx0 + xcc[q] < mX, yv = ty0 + ycc[q] < mY;
+    xp[q] = xv ? reinterpret_cast<const T *>(X[tx0 + xcc[q]].p) : nullptr;
+    xs[q] = xv ? X[tx0 + xcc[q]].stride : 0;
+    yp[q] = yv ? reinterpret_cast<const T *>(Y[ty0 + ycc[q]].p) : nullptr;
+    ys[q] = yv ? Y[ty0 + ycc[q]].stride : 0;
+  }
   for (int64_t rb = r0; rb < r1; rb += GR) {
-    for (int e = tid; e < GR * GT; e += 256) {
-      const int rr = xr ? e % GR : e / GT, cc = xr ? e / GR : e % GT;
-      const int64_t row = rb + rr;
-      T v = zero<T>();
-      if (row < r1 && tx0 + cc < mX) v = conj(ldp<T>(X[tx0 + cc].p, row * X[tx0 + cc].stride));
-      sx[rr][cc] = v;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int64_t row = rb + xrr[q];
+      sx[xrr[q]][xcc[q]] = (xp[q] && row < r1) ? conj(xp[q][row * xs[q]]) : zero<T>();
     }
-    for (int e = tid; e < GR * GT; e += 256) {
-      const int rr = yr ? e % GR : e / GT, cc = yr ? e / GR : e % GT;
-      const int64_t row = rb + rr;
-      T v = zero<T>();
-      if (row < r1 && ty0 + cc < mY) v = ldp<T>(Y[ty0 + cc].p, row * Y[ty0 + cc].stride);
-      sy[rr][cc] = v;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int64_t row = rb + yrr[q];
+      sy[yrr[q]][ycc[q]] = (yp[q] && row < r1) ? yp[q][row * ys[q]] : zero<T>();
     }
     __syncthreads();
 #pragma unroll 16
@@ -210,7 +228,7 @@ __global__ void __launch_bounds__(256) k_gemm_panels(const ColDesc *__restrict__
     T acc[PB];
 #pragma unroll
     for (int c = 0; c < PB; ++c) acc[c] = zero<T>();
-#pragma unroll 8
+#pragma unroll 4
     for (int a = 0; a < mX; ++a) {
       const T xv = ldp<T>(sX[a].p, row * sX[a].stride);
 #pragma unroll
