@@ -87,68 +87,71 @@ __global__ void __launch_bounds__(256) k_gram(const ColDesc *__restrict__ X, int
                                               int64_t chunk, unsigned xrow_fast, unsigned yrow_fast,
                                               T *__restrict__ part) {
   constexpr int GR = GramRows<T>::v;   // rows per smem sub-tile
-  __shared__ T sx[GR][GT + 1];
-  __shared__ T sy[GR][GT + 1];
+  constexpr int LD = GT + 2;           // padded row (keeps 16-byte alignment)
+  __shared__ __align__(16) T sx[GR][LD];
+  __shared__ __align__(16) T sy[GR][LD];
   const int tilesY = (mY + GT - 1) / GT;
   const int txi = blockIdx.x / tilesY, tyi = blockIdx.x % tilesY;
   const int tx0 = txi * GT, ty0 = tyi * GT;
-  // per 32-column group: rows fastest (vector columns, coalesced down a
-  // column) or columns fastest (row-major panels, coalesced along a row)
   const bool xr = (xrow_fast >> txi) & 1u, yr = (yrow_fast >> tyi) & 1u;
   const int64_t r0 = (int64_t)blockIdx.y * chunk;
   const int64_t r1 = min(n, r0 + chunk);
   const int tid = threadIdx.x;
-  const int ta = tid / 16, tb = tid % 16;
-  T acc[2][2] = {{zero<T>(), zero<T>()}, {zero<T>(), zero<T>()}};
-  // element e = tid + 256 q of a GR x GT sub-tile; the column (and its
-  // descriptor) each thread touches is fixed for the whole chunk -> hoisted
-  constexpr int NQ = GR * GT / 256;
-  const T *xp[NQ];
-  int64_t xs[NQ];
-  int xrr[NQ], xcc[NQ];
-  const T *yp[NQ];
-  int64_t ys[NQ];
-  int yrr[NQ], ycc[NQ];
+  // 4 row groups x (8 x 8) threads, each thread a 4 x 4 register micro-tile
+  const int g = tid >> 6, t = tid & 63, ta = t >> 3, tb = t & 7;
+  T acc[4][4];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    const int e = tid + 256 * q;
-    xrr[q] = xr ? e % GR : e / GT;
-    xcc[q] = xr ? e / GR : e % GT;
-    yrr[q] = yr ? e % GR : e / GT;
-    ycc[q] = yr ? e / GR : e % GT;
-    const bool xv = tx0 + xcc[q] < mX, yv = ty0 + ycc[q] < mY;
-    xp[q] = xv ? reinterpret_cast<const T *>(X[tx0 + xcc[q]].p) : nullptr;
-    xs[q] = xv ? X[tx0 + xcc[q]].stride : 0;
-    yp[q] = yv ? reinterpret_cast<const T *>(Y[ty0 + ycc[q]].p) : nullptr;
-    ys[q] = yv ? Y[ty0 + ycc[q]].stride : 0;
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = zero<T>();
+  constexpr int NQ = GR * GT / 256;
+  __shared__ ColDesc sdx[GT], sdy[GT];
+  if (tid < GT) {
+    sdx[tid] = tx0 + tid < mX ? X[tx0 + tid] : ColDesc{nullptr, 0};
+    sdy[tid] = ty0 + tid < mY ? Y[ty0 + tid] : ColDesc{nullptr, 0};
   }
+  __syncthreads();
   for (int64_t rb = r0; rb < r1; rb += GR) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      const int64_t row = rb + xrr[q];
-      sx[xrr[q]][xcc[q]] = (xp[q] && row < r1) ? conj(xp[q][row * xs[q]]) : zero<T>();
+      const int e = tid + 256 * q;
+      const int rr = xr ? e % GR : e / GT, cc = xr ? e / GR : e % GT;
+      const int64_t row = rb + rr;
+      const ColDesc d = sdx[cc];
+      sx[rr][cc] = (d.p && row < r1) ? conj(ldp<T>(d.p, row * d.stride)) : zero<T>();
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      const int64_t row = rb + yrr[q];
-      sy[yrr[q]][ycc[q]] = (yp[q] && row < r1) ? yp[q][row * ys[q]] : zero<T>();
+      const int e = tid + 256 * q;
+      const int rr = yr ? e % GR : e / GT, cc = yr ? e / GR : e % GT;
+      const int64_t row = rb + rr;
+      const ColDesc d = sdy[cc];
+      sy[rr][cc] = (d.p && row < r1) ? ldp<T>(d.p, row * d.stride) : zero<T>();
     }
     __syncthreads();
-#pragma unroll 16
-    for (int rr = 0; rr < GR; ++rr) {
-      const T x0 = sx[rr][ta], x1 = sx[rr][ta + 16];
-      const T y0 = sy[rr][tb], y1 = sy[rr][tb + 16];
-      acc[0][0] = mad(x0, y0, acc[0][0]);
-      acc[0][1] = mad(x0, y1, acc[0][1]);
-      acc[1][0] = mad(x1, y0, acc[1][0]);
-      acc[1][1] = mad(x1, y1, acc[1][1]);
+#pragma unroll 4
+    for (int rr = g; rr < GR; rr += 4) {
+      T xv[4], yv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        xv[u] = sx[rr][ta * 4 + u];
+        yv[u] = sy[rr][tb * 4 + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = mad(xv[u], yv[v], acc[u][v]);
     }
     __syncthreads();
   }
-  for (int u = 0; u < 2; ++u)
-    for (int v = 0; v < 2; ++v) {
-      const int a = tx0 + ta + 16 * u, b = ty0 + tb + 16 * v;
-      if (a < mX && b < mY) part[((int64_t)blockIdx.y * mX + a) * mY + b] = acc[u][v];
+  // partial chunk index = 4 * chunk + group (fixed order in the reduction)
+  const int64_t pc = (int64_t)blockIdx.y * 4 + g;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int a = tx0 + ta * 4 + u, bb = ty0 + tb * 4 + v;
+      if (a < mX && bb < mY) part[(pc * mX + a) * mY + bb] = acc[u][v];
     }
 }
 
@@ -176,12 +179,12 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   const int64_t chunk = ((n + nchunks - 1) / nchunks + GR - 1) / GR * GR;
   nchunks = (int)((n + chunk - 1) / chunk);
   const size_t desc_bytes = sizeof(ColDesc) * (mX + mY);
-  const size_t part_bytes = sizeof(T) * (size_t)nchunks * mX * mY;
+  const size_t part_bytes = sizeof(T) * (size_t)nchunks * 4 * mX * mY;
   const size_t g_bytes = sizeof(T) * (size_t)mX * mY;
   char *buf = (char *)ws_alloc(desc_bytes + part_bytes + g_bytes + 64);
   ColDesc *dX = (ColDesc *)buf;
   T *dpart = (T *)(buf + ((desc_bytes + 15) / 16) * 16);
-  T *dG = dpart + (size_t)nchunks * mX * mY;
+  T *dG = dpart + (size_t)nchunks * 4 * mX * mY;
   std::vector<ColDesc> both(X);
   both.insert(both.end(), Y.begin(), Y.end());
   RB_CUDA(cudaMemcpyAsync(dX, both.data(), desc_bytes, cudaMemcpyHostToDevice, strm));
@@ -196,7 +199,7 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   };
   dim3 grid(tiles, nchunks);
   k_gram<T><<<grid, 256, 0, strm>>>(dX, mX, dX + mX, mY, n, chunk, flags(X), flags(Y), dpart);
-  k_gram_reduce<T><<<(mX * mY * 32 + 255) / 256, 256, 0, strm>>>(dpart, nchunks, mX * mY, dG);
+  k_gram_reduce<T><<<(mX * mY * 32 + 255) / 256, 256, 0, strm>>>(dpart, 4 * nchunks, mX * mY, dG);
   count_launch(2);
   std::vector<T> h((size_t)mX * mY);
   RB_CUDA(cudaMemcpyAsync(h.data(), dG, g_bytes, cudaMemcpyDeviceToHost, strm));
