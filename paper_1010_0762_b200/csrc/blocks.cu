@@ -82,7 +82,7 @@ constexpr int GT = 32;   // output tile edge
 template <typename T> struct GramRows { static constexpr int v = sizeof(T) == 8 ? 64 : 32; };
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_gram(const ColDesc *__restrict__ X, int mX,
+__global__ void __launch_bounds__(256, 3) k_gram(const ColDesc *__restrict__ X, int mX,
                                               const ColDesc *__restrict__ Y, int mY, int64_t n,
                                               int64_t chunk, unsigned xrow_fast, unsigned yrow_fast,
                                               T *__restrict__ part) {
@@ -173,8 +173,11 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   G.assign((size_t)mX * mY, cplx(0, 0));
   if (mX == 0 || mY == 0) return;
   const int tiles = ((mX + GT - 1) / GT) * ((mY + GT - 1) / GT);
-  int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 2047) / 2048,
-                                                            (8 * ctx->nsm + tiles - 1) / tiles));
+  // whole waves: tiles * nchunks a multiple of 3 resident blocks per SM
+  const int64_t slots = (int64_t)3 * ctx->nsm;
+  int64_t want = std::max<int64_t>(1, (n + 1023) / 1024);          // >= 1024 rows per chunk
+  int64_t waves = std::max<int64_t>(1, std::min<int64_t>(4, (want * tiles + slots - 1) / slots));
+  int nchunks = (int)std::max<int64_t>(1, (waves * slots) / tiles);
   constexpr int GR = GramRows<T>::v;
   const int64_t chunk = ((n + nchunks - 1) / nchunks + GR - 1) / GR * GR;
   nchunks = (int)((n + chunk - 1) / chunk);
