@@ -885,7 +885,7 @@ int rbicg_init(rbicg_ctx **out, int device, void *stream, const rbicg_dist *dist
     RB_CUDA(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
     prepare_kernels();
     {
-      int mult = stream_blocks_per_sm();
+      int mult = std::max(stream_blocks_per_sm(), 8);
       if (const char *e = getenv("RBICG_BLOCKS_PER_SM")) mult = std::max(1, atoi(e));
       c->grid_stream = c->nsm * mult;
     }

@@ -190,7 +190,7 @@ __device__ __forceinline__ void final_reduce(const T *part, int nout, int G, T *
 
 // ============================================================== pass 1
 template <typename T>
-__global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
+__global__ void __launch_bounds__(BS, 6) k_pass1(LoopArgs<T> a) {
   __shared__ T s_z[BS], s_zt[BS], s_pt[BS];
   __shared__ T s_red[3 * BS];
   __shared__ T s_fin[3 * KMAX + 1];
@@ -803,7 +803,10 @@ static void launch_pdl(void (*kern)(KArgs...), int grid, size_t sm, cudaStream_t
 
 template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s) {
   const size_t sm = a.staged ? pass1_smem<T>(a.tile_max) : 0;
-  launch_pdl(k_pass1<T>, grid_for(a.n, a.G), sm, s, a);
+  int per_sm = 1;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass1<T>, BS, sm));
+  const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
+  launch_pdl(k_pass1<T>, grid_for(a.n, G), sm, s, a);
   count_launch();
 }
 
