@@ -190,7 +190,7 @@ __device__ __forceinline__ void final_reduce(const T *part, int nout, int G, T *
 
 // ============================================================== pass 1
 template <typename T>
-__global__ void __launch_bounds__(BS, 6) k_pass1(LoopArgs<T> a) {
+__global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
   __shared__ T s_z[BS], s_zt[BS], s_pt[BS];
   __shared__ T s_red[3 * BS];
   __shared__ T s_fin[3 * KMAX + 1];
