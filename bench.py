@@ -345,7 +345,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
-        if rank == 0:
+        if rank == 0:   # the other ranks exit without work
             print(json.dumps(run_reference(args)), flush=True)
         return
     if world > 1:

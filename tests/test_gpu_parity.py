@@ -374,3 +374,52 @@ def test_full_size_c2_matched_iterations(ctx):
         assert res["k_out"] == ref.basis_out.k
         U, Ut = ref.basis_out.U, ref.basis_out.Ut
         M.free()
+
+
+def test_full_size_c3_matched_iterations(ctx):
+    """C3 system 0 (n = 7,077,888, 3-D) at full size: s + 3 iterations with
+    one cycle end, iterates and residual histories vs the oracle."""
+    from oracle import rbicg as R
+    cfg = CONFIGS["C3"]
+    item = next(system_sequence(cfg, systems=[0]))
+    m = cfg.s + 3
+    A = _csr((item["indptr"], item["indices"], item["data"]))
+    ref = R.solve_dual(A, item["b"], item["bt"], k=cfg.k, s=cfg.s, tol=cfg.tol,
+                       max_itn=m, trunc_tol=cfg.trunc_tol, force_iters=m)
+    rec = ctx.recycle(cfg.n, cfg.k)
+    M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+    x, xt, res, h = ctx.solve_dual(M, item["b"], item["bt"], R=rec, k=cfg.k,
+                                   s=cfg.s, tol=cfg.tol, max_itn=m,
+                                   trunc_tol=cfg.trunc_tol, force_iters=m,
+                                   history=True)
+    assert res["iterations"] == m and res["cycles"] == ref.cycles == 1
+    assert np.linalg.norm(x - ref.x) <= 1e-7 * np.linalg.norm(ref.x)
+    assert np.linalg.norm(xt - ref.xt) <= 1e-7 * np.linalg.norm(ref.xt)
+    np.testing.assert_allclose(h[:, 0], np.array(ref.hist["rnorm"][1:]) /
+                               np.linalg.norm(item["b"]), rtol=1e-6)
+    assert res["k_out"] == ref.basis_out.k
+    M.free()
+
+
+def test_full_size_c4_bilinear_conjugate_pair(ctx):
+    """C4 operator at 100^3 (complex128, n = 1,000,000), the first conjugate
+    shift pair (slots 0, 1; λ_R taken as 0 -- the shifts stay right of the
+    spectrum): converged solves to tol, G(σ) = c^*A^{-1}b within
+    1e-8 of the oracle, and G(σ̄) = conj G(σ) (P11)."""
+    from oracle import rbicg as R
+    cfg = CONFIGS["C4"]
+    items = list(system_sequence(cfg, systems=[0, 1], lam_r=0.0))
+    vals = []
+    for item in items:
+        A = _csr((item["indptr"], item["indices"], item["data"]))
+        val_o, ref = R.bilinear(A, item["bt"], item["b"], k=0, s=cfg.s,
+                                tol=cfg.tol, max_itn=cfg.max_itn)
+        M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+        val_g, res = ctx.bilinear(M, item["bt"], item["b"], k=0, s=cfg.s,
+                                  tol=cfg.tol, max_itn=cfg.max_itn)
+        assert res["status"] == 0
+        assert iters_close(res["iterations"], ref.iterations)
+        assert abs(val_g - val_o) <= 1e-8 * abs(val_o)
+        vals.append(val_g)
+        M.free()
+    assert abs(vals[1] - np.conj(vals[0])) <= 1e-8 * abs(vals[0])
