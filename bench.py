@@ -197,6 +197,12 @@ def run_gpu(args, rank, world):
     dom_bytes, dom_ms, dom = (p1, kt["pass1_ms"], "pass1") \
         if kt["pass1_ms"] >= kt["pass2_ms"] else (p2, kt["pass2_ms"], "pass2")
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        pass
 
     # ---- e2e through the public API with HOST buffers (H2D/D2H in the call)
     e2e = None
@@ -250,7 +256,7 @@ def run_gpu(args, rank, world):
                    "parallelism": "replicas" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": dom_bytes,
                      "pass1_ms": kt["pass1_ms"], "pass2_ms": kt["pass2_ms"],
                      "k_active": kt["k"], "lazy_x": kt["lazy_x"],

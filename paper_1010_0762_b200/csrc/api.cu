@@ -885,8 +885,8 @@ int rbicg_init(rbicg_ctx **out, int device, void *stream, const rbicg_dist *dist
     RB_CUDA(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
     prepare_kernels();
     {
-      int mult = std::max(stream_blocks_per_sm(), 8);
-      if (const char *e = getenv("RBICG_BLOCKS_PER_SM")) mult = std::max(1, atoi(e));
+      int mult = std::min(std::max(stream_blocks_per_sm(), 8), 8);   // G <= 40*32 (final_reduce)
+      if (const char *e = getenv("RBICG_BLOCKS_PER_SM")) mult = std::min(8, std::max(1, atoi(e)));
       c->grid_stream = c->nsm * mult;
     }
     *out = c;

@@ -175,13 +175,24 @@ __device__ __forceinline__ bool last_block(unsigned *cnt, int *s_flag) {
 }
 
 // Final fixed-order reduction of `nout` outputs stored as part[o*G + b].
+// All partial loads of a lane are issued before any add (they are L2 hits;
+// a dependent chain of G/32 loads would cost microseconds at the kernel tail).
+constexpr int RED_PER_LANE = 40;   // supports G <= 1280 blocks
 template <typename T>
 __device__ __forceinline__ void final_reduce(const T *part, int nout, int G, T *s_fin) {
   __threadfence();
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   for (int o = w; o < nout; o += BS / 32) {
+    const T *src = part + (int64_t)o * G;
+    T v[RED_PER_LANE];
+#pragma unroll
+    for (int q = 0; q < RED_PER_LANE; ++q) {
+      const int b = l + 32 * q;
+      v[q] = b < G ? ldcg(src + b) : zero<T>();
+    }
     T acc = zero<T>();
-    for (int b = l; b < G; b += 32) acc = add(acc, ldcg(part + (int64_t)o * G + b));
+#pragma unroll
+    for (int q = 0; q < RED_PER_LANE; ++q) acc = add(acc, v[q]);
     acc = warp_sum(acc);
     if (l == 0) s_fin[o] = acc;
   }
