@@ -412,13 +412,27 @@ struct Solver {
   // (Q13: unit columns, absolute cut on the singular values).
   void biorth(const T *U, const T *Ut, const T *C, const T *Ct, int kin, Basis &out,
               cudaStream_t bs) {
+    // only ||c_j||^2, ||c~_j||^2 and C~^*C are needed (Q13 scaling + SVD)
     std::vector<ColDesc> X;
     for (int c = 0; c < kin; ++c) X.push_back(col(C, c, kin));
     for (int c = 0; c < kin; ++c) X.push_back(col(Ct, c, kin));
-    std::vector<cplx> G;
+    std::vector<std::pair<int, int>> pairs;
+    for (int j = 0; j < kin; ++j) pairs.emplace_back(j, j);
+    for (int j = 0; j < kin; ++j) pairs.emplace_back(kin + j, kin + j);
+    for (int a2 = 0; a2 < kin; ++a2)
+      for (int b2 = 0; b2 < kin; ++b2) pairs.emplace_back(kin + a2, b2);
+    std::vector<cplx> G((size_t)4 * kin * kin, 0.0), gv;
     {
       Phase ph("biorth.gram", bs);
-      gram<T>(X, X, n, G, ctx, bs);
+      gram_pairs<T>(X, X, pairs, n, gv, ctx, bs);
+    }
+    {
+      const int mm = 2 * kin;
+      size_t q = 0;
+      for (int j = 0; j < kin; ++j) G[(size_t)j * mm + j] = gv[q++];
+      for (int j = 0; j < kin; ++j) G[(size_t)(kin + j) * mm + kin + j] = gv[q++];
+      for (int a2 = 0; a2 < kin; ++a2)
+        for (int b2 = 0; b2 < kin; ++b2) G[(size_t)(kin + a2) * mm + b2] = gv[q++];
     }
     const int m2 = 2 * kin;
     std::vector<int> kk;

@@ -211,6 +211,98 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   for (size_t i = 0; i < h.size(); ++i) G[i] = cplx(re(h[i]), im(h[i]));
 }
 
+// ------------------------------------------------------------------ sparse Gram
+// Selected entries G[a][b] = x_a^H y_b (pairs list).  Used where only a few
+// entries of a Gram are needed (column norms and C~^*C of the SVD step):
+// the whole row sub-tile of the used columns is staged in shared memory and
+// each thread accumulates up to PPT pairs in registers.
+constexpr int PPT = 6;
+template <typename T>
+__global__ void __launch_bounds__(256) k_gram_pairs(const ColDesc *__restrict__ X, int mX,
+                                                    const ColDesc *__restrict__ Y, int mY,
+                                                    const int2 *__restrict__ pairs, int npairs,
+                                                    int64_t n, int64_t chunk, T *__restrict__ part) {
+  constexpr int GR = 32;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  T *sx = reinterpret_cast<T *>(sm_raw);         // [GR][mX]
+  T *sy = sx + GR * mX;                           // [GR][mY]
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(n, r0 + chunk);
+  T acc[PPT];
+  int pa[PPT], pb[PPT];
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    acc[q] = zero<T>();
+    const int pi = tid + 256 * q;
+    pa[q] = pi < npairs ? pairs[pi].x : -1;
+    pb[q] = pi < npairs ? pairs[pi].y : 0;
+  }
+  for (int64_t rb = r0; rb < r1; rb += GR) {
+    // columns fastest: row-major panels are read along their rows
+    for (int e = tid; e < GR * mX; e += 256) {
+      const int rr = e / mX, cc = e - rr * mX;
+      const int64_t row = rb + rr;
+      sx[e] = row < r1 ? conj(ldp<T>(X[cc].p, row * X[cc].stride)) : zero<T>();
+    }
+    for (int e = tid; e < GR * mY; e += 256) {
+      const int rr = e / mY, cc = e - rr * mY;
+      const int64_t row = rb + rr;
+      sy[e] = row < r1 ? ldp<T>(Y[cc].p, row * Y[cc].stride) : zero<T>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      if (pa[q] < 0) continue;
+      T s = acc[q];
+#pragma unroll 8
+      for (int rr = 0; rr < GR; ++rr) s = mad(sx[rr * mX + pa[q]], sy[rr * mY + pb[q]], s);
+      acc[q] = s;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int pi = tid + 256 * q;
+    if (pi < npairs) part[(int64_t)blockIdx.x * npairs + pi] = acc[q];
+  }
+}
+
+template <typename T>
+void gram_pairs(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y,
+                const std::vector<std::pair<int, int>> &pairs, int64_t n, std::vector<cplx> &out,
+                rbicg_ctx *ctx, cudaStream_t strm) {
+  const int mX = (int)X.size(), mY = (int)Y.size(), np = (int)pairs.size();
+  out.assign(np, cplx(0, 0));
+  if (!np) return;
+  RB_CHECK(np <= 256 * PPT, RBICG_EINVAL);
+  const size_t sm = sizeof(T) * 32 * (size_t)(mX + mY);
+  RB_CHECK(sm <= 160 * 1024, RBICG_EINVAL);
+  const int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, 4 * ctx->nsm));
+  const int64_t chunk = ((n + nchunks - 1) / nchunks + 31) / 32 * 32;
+  const int nb = (int)((n + chunk - 1) / chunk);
+  std::vector<int2> hp(np);
+  for (int i = 0; i < np; ++i) hp[i] = make_int2(pairs[i].first, pairs[i].second);
+  const size_t db = sizeof(ColDesc) * (mX + mY), pb = sizeof(int2) * np;
+  const size_t off1 = (db + 15) / 16 * 16, off2 = off1 + (pb + 15) / 16 * 16;
+  char *buf = (char *)ws_alloc(off2 + sizeof(T) * ((size_t)nb * np + np) + 64);
+  ColDesc *dX = (ColDesc *)buf;
+  int2 *dp = (int2 *)(buf + off1);
+  T *dpart = (T *)(buf + off2);
+  T *dG = dpart + (size_t)nb * np;
+  std::vector<ColDesc> both(X);
+  both.insert(both.end(), Y.begin(), Y.end());
+  RB_CUDA(cudaMemcpyAsync(dX, both.data(), db, cudaMemcpyHostToDevice, strm));
+  RB_CUDA(cudaMemcpyAsync(dp, hp.data(), pb, cudaMemcpyHostToDevice, strm));
+  k_gram_pairs<T><<<nb, 256, sm, strm>>>(dX, mX, dX + mX, mY, dp, np, n, chunk, dpart);
+  k_gram_reduce<T><<<(np * 32 + 255) / 256, 256, 0, strm>>>(dpart, nb, np, dG);
+  count_launch(2);
+  std::vector<T> h(np);
+  RB_CUDA(cudaMemcpyAsync(h.data(), dG, sizeof(T) * np, cudaMemcpyDeviceToHost, strm));
+  RB_CUDA(cudaStreamSynchronize(strm));
+  ws_free(buf);
+  for (int i = 0; i < np; ++i) out[i] = cplx(re(h[i]), im(h[i]));
+}
+
 // ------------------------------------------------------------------ panels x M
 // out[row, c] = Σ_a X_a[row] M[a, c]; one thread per row keeps the whole output
 // row in registers (PB >= p accumulators), so out may alias an input panel
@@ -297,6 +389,8 @@ void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int 
 }
 
 void prepare_block_kernels() {
+  RB_CUDA(cudaFuncSetAttribute(k_gram_pairs<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_gram_pairs<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_spmm<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_spmm<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 #define RB_GATTR(T, PB)                                                                      \
@@ -310,6 +404,9 @@ void prepare_block_kernels() {
 }
 
 #define RB_BINST(T)                                                                        \
+  template void gram_pairs<T>(const std::vector<ColDesc> &, const std::vector<ColDesc> &,     \
+                              const std::vector<std::pair<int, int>> &, int64_t,              \
+                              std::vector<cplx> &, rbicg_ctx *, cudaStream_t);               \
   template void launch_spmm<T>(const DevMat &, const T *, T *, int, cudaStream_t);         \
   template void gram<T>(const std::vector<ColDesc> &, const std::vector<ColDesc> &, int64_t, \
                         std::vector<cplx> &, rbicg_ctx *, cudaStream_t);                   \
