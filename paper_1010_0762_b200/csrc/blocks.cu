@@ -16,6 +16,29 @@ template <typename T> __device__ __forceinline__ T ldp(const void *p, int64_t i)
   return reinterpret_cast<const T *>(p)[i];
 }
 
+// cp.async (LDGSTS) element copies with zero fill, for software pipelining of
+// the row sub-tiles of the Gram kernels (the columns are arbitrary strided
+// descriptors, so per-element async copies rather than bulk tensor copies).
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+template <typename T>
+__device__ __forceinline__ void cp_async_el(T *dst, const T *src, bool pred) {
+  const int sz = pred ? (int)sizeof(T) : 0;
+  if (sizeof(T) == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "r"(sz)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "r"(sz)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ------------------------------------------------------------------ SpMM
 // One block per SELL slice (32 rows) x k columns: the slice's column indices
 // and values are loaded once, coalesced, into shared memory; thread
@@ -83,13 +106,15 @@ template <typename T> struct GramRows { static constexpr int v = sizeof(T) == 8 
 
 template <typename T>
 __global__ void __launch_bounds__(256, 3) k_gram(const ColDesc *__restrict__ X, int mX,
-                                              const ColDesc *__restrict__ Y, int mY, int64_t n,
-                                              int64_t chunk, unsigned xrow_fast, unsigned yrow_fast,
-                                              T *__restrict__ part) {
+                                                 const ColDesc *__restrict__ Y, int mY, int64_t n,
+                                                 int64_t chunk, unsigned xrow_fast,
+                                                 unsigned yrow_fast, T *__restrict__ part) {
   constexpr int GR = GramRows<T>::v;   // rows per smem sub-tile
   constexpr int LD = GT + 2;           // padded row (keeps 16-byte alignment)
-  __shared__ __align__(16) T sx[GR][LD];
-  __shared__ __align__(16) T sy[GR][LD];
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  T *sbase = reinterpret_cast<T *>(sm_raw);   // 2 stages x (sx[GR][LD], sy[GR][LD])
+  constexpr int STAGE = 2 * GR * LD;
+  __shared__ ColDesc sdx[GT], sdy[GT];
   const int tilesY = (mY + GT - 1) / GT;
   const int txi = blockIdx.x / tilesY, tyi = blockIdx.x % tilesY;
   const int tx0 = txi * GT, ty0 = tyi * GT;
@@ -105,20 +130,22 @@ __global__ void __launch_bounds__(256, 3) k_gram(const ColDesc *__restrict__ X, 
 #pragma unroll
     for (int v = 0; v < 4; ++v) acc[u][v] = zero<T>();
   constexpr int NQ = GR * GT / 256;
-  __shared__ ColDesc sdx[GT], sdy[GT];
   if (tid < GT) {
     sdx[tid] = tx0 + tid < mX ? X[tx0 + tid] : ColDesc{nullptr, 0};
     sdy[tid] = ty0 + tid < mY ? Y[ty0 + tid] : ColDesc{nullptr, 0};
   }
   __syncthreads();
-  for (int64_t rb = r0; rb < r1; rb += GR) {
+  auto load = [&](int64_t rb, int buf) {
+    T *sx = sbase + buf * STAGE, *sy = sx + GR * LD;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int e = tid + 256 * q;
       const int rr = xr ? e % GR : e / GT, cc = xr ? e / GR : e % GT;
       const int64_t row = rb + rr;
       const ColDesc d = sdx[cc];
-      sx[rr][cc] = (d.p && row < r1) ? conj(ldp<T>(d.p, row * d.stride)) : zero<T>();
+      const bool ok = d.p && row < r1;
+      const T *src = reinterpret_cast<const T *>(d.p ? d.p : (const void *)part);
+      cp_async_el(sx + rr * LD + cc, ok ? src + row * d.stride : src, ok);
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -126,16 +153,27 @@ __global__ void __launch_bounds__(256, 3) k_gram(const ColDesc *__restrict__ X, 
       const int rr = yr ? e % GR : e / GT, cc = yr ? e / GR : e % GT;
       const int64_t row = rb + rr;
       const ColDesc d = sdy[cc];
-      sy[rr][cc] = (d.p && row < r1) ? ldp<T>(d.p, row * d.stride) : zero<T>();
+      const bool ok = d.p && row < r1;
+      const T *src = reinterpret_cast<const T *>(d.p ? d.p : (const void *)part);
+      cp_async_el(sy + rr * LD + cc, ok ? src + row * d.stride : src, ok);
     }
+    cp_async_commit();
+  };
+  if (r0 < r1) load(r0, 0);
+  int buf = 0;
+  for (int64_t rb = r0; rb < r1; rb += GR, buf ^= 1) {
+    if (rb + GR < r1) load(rb + GR, buf ^ 1);
+    else cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
+    const T *sx = sbase + buf * STAGE, *sy = sx + GR * LD;
 #pragma unroll 4
     for (int rr = g; rr < GR; rr += 4) {
       T xv[4], yv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        xv[u] = sx[rr][ta * 4 + u];
-        yv[u] = sy[rr][tb * 4 + u];
+        xv[u] = conj(sx[rr * LD + ta * 4 + u]);
+        yv[u] = sy[rr * LD + tb * 4 + u];
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -201,7 +239,8 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
     return f;
   };
   dim3 grid(tiles, nchunks);
-  k_gram<T><<<grid, 256, 0, strm>>>(dX, mX, dX + mX, mY, n, chunk, flags(X), flags(Y), dpart);
+  const size_t gsm = sizeof(T) * 2 * 2 * GramRows<T>::v * (GT + 2);
+  k_gram<T><<<grid, 256, gsm, strm>>>(dX, mX, dX + mX, mY, n, chunk, flags(X), flags(Y), dpart);
   k_gram_reduce<T><<<(mX * mY * 32 + 255) / 256, 256, 0, strm>>>(dpart, 4 * nchunks, mX * mY, dG);
   count_launch(2);
   std::vector<T> h((size_t)mX * mY);
@@ -224,8 +263,8 @@ __global__ void __launch_bounds__(256) k_gram_pairs(const ColDesc *__restrict__ 
                                                     int64_t n, int64_t chunk, T *__restrict__ part) {
   constexpr int GR = 32;
   extern __shared__ __align__(16) unsigned char sm_raw[];
-  T *sx = reinterpret_cast<T *>(sm_raw);         // [GR][mX]
-  T *sy = sx + GR * mX;                           // [GR][mY]
+  T *sbase = reinterpret_cast<T *>(sm_raw);   // 2 stages of [GR][mX] + [GR][mY]
+  const int stage = GR * (mX + mY);
   const int tid = threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(n, r0 + chunk);
   T acc[PPT];
@@ -237,25 +276,36 @@ __global__ void __launch_bounds__(256) k_gram_pairs(const ColDesc *__restrict__ 
     pa[q] = pi < npairs ? pairs[pi].x : -1;
     pb[q] = pi < npairs ? pairs[pi].y : 0;
   }
-  for (int64_t rb = r0; rb < r1; rb += GR) {
-    // columns fastest: row-major panels are read along their rows
+  auto load = [&](int64_t rb, int buf) {
+    T *sx = sbase + buf * stage, *sy = sx + GR * mX;
     for (int e = tid; e < GR * mX; e += 256) {
       const int rr = e / mX, cc = e - rr * mX;
       const int64_t row = rb + rr;
-      sx[e] = row < r1 ? conj(ldp<T>(X[cc].p, row * X[cc].stride)) : zero<T>();
+      const T *src = reinterpret_cast<const T *>(X[cc].p);
+      cp_async_el(sx + e, row < r1 ? src + row * X[cc].stride : src, row < r1);
     }
     for (int e = tid; e < GR * mY; e += 256) {
       const int rr = e / mY, cc = e - rr * mY;
       const int64_t row = rb + rr;
-      sy[e] = row < r1 ? ldp<T>(Y[cc].p, row * Y[cc].stride) : zero<T>();
+      const T *src = reinterpret_cast<const T *>(Y[cc].p);
+      cp_async_el(sy + e, row < r1 ? src + row * Y[cc].stride : src, row < r1);
     }
+    cp_async_commit();
+  };
+  if (r0 < r1) load(r0, 0);
+  int buf = 0;
+  for (int64_t rb = r0; rb < r1; rb += GR, buf ^= 1) {
+    if (rb + GR < r1) load(rb + GR, buf ^ 1);
+    else cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
+    const T *sx = sbase + buf * stage, *sy = sx + GR * mX;
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
       if (pa[q] < 0) continue;
       T s = acc[q];
 #pragma unroll 8
-      for (int rr = 0; rr < GR; ++rr) s = mad(sx[rr * mX + pa[q]], sy[rr * mY + pb[q]], s);
+      for (int rr = 0; rr < GR; ++rr) s = mad(conj(sx[rr * mX + pa[q]]), sy[rr * mY + pb[q]], s);
       acc[q] = s;
     }
     __syncthreads();
@@ -275,7 +325,7 @@ void gram_pairs(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y,
   out.assign(np, cplx(0, 0));
   if (!np) return;
   RB_CHECK(np <= 256 * PPT, RBICG_EINVAL);
-  const size_t sm = sizeof(T) * 32 * (size_t)(mX + mY);
+  const size_t sm = 2 * sizeof(T) * 32 * (size_t)(mX + mY);
   RB_CHECK(sm <= 160 * 1024, RBICG_EINVAL);
   const int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, 4 * ctx->nsm));
   const int64_t chunk = ((n + nchunks - 1) / nchunks + 31) / 32 * 32;
@@ -389,6 +439,8 @@ void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int 
 }
 
 void prepare_block_kernels() {
+  RB_CUDA(cudaFuncSetAttribute(k_gram<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_gram<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_gram_pairs<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_gram_pairs<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_spmm<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
