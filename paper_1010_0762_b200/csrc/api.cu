@@ -424,7 +424,7 @@ struct Solver {
     std::vector<cplx> G((size_t)4 * kin * kin, 0.0), gv;
     {
       Phase ph("biorth.gram", bs);
-      gram_pairs<T>(X, X, pairs, n, gv, ctx, bs);
+      gram_pairs<T>({C, Ct}, {kin, kin}, pairs, n, gv, ctx, bs);
     }
     {
       const int mm = 2 * kin;

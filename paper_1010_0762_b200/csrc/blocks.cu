@@ -251,44 +251,61 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
 }
 
 // ------------------------------------------------------------------ sparse Gram
-// Selected entries G[a][b] = x_a^H y_b (pairs list).  Used where only a few
-// entries of a Gram are needed (column norms and C~^*C of the SVD step):
-// the whole row sub-tile of the used columns is staged in shared memory and
-// each thread accumulates up to PPT pairs in registers.
+// Selected entries G[a][b] = x_a^H x_b of the column concatenation of a few
+// compact row-major panels (column norms and C~^*C of the SVD step).  A row
+// sub-tile of every panel is one contiguous block: it is copied with 16-byte
+// cp.async (double-buffered) and each thread accumulates up to PPT pairs.
 constexpr int PPT = 6;
+constexpr int MAXP = 4;
+struct PanelSet {
+  const void *p[MAXP];
+  int nc[MAXP];     // columns (= leading dimension, compact panels)
+  int off[MAXP];    // smem offset (elements) of the panel's sub-tile in a stage
+  int np, width;    // panels, total columns
+};
 template <typename T>
-__global__ void __launch_bounds__(256) k_gram_pairs(const ColDesc *__restrict__ X, int mX,
-                                                    const ColDesc *__restrict__ Y, int mY,
-                                                    const int2 *__restrict__ pairs, int npairs,
-                                                    int64_t n, int64_t chunk, T *__restrict__ part) {
+__global__ void __launch_bounds__(256) k_gram_pairs(PanelSet P, const int2 *__restrict__ pairs,
+                                                    int npairs, int64_t n, int64_t chunk,
+                                                    T *__restrict__ part) {
   constexpr int GR = 32;
   extern __shared__ __align__(16) unsigned char sm_raw[];
-  T *sbase = reinterpret_cast<T *>(sm_raw);   // 2 stages of [GR][mX] + [GR][mY]
-  const int stage = GR * (mX + mY);
+  T *sbase = reinterpret_cast<T *>(sm_raw);
+  const int stage = GR * P.width;
   const int tid = threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(n, r0 + chunk);
   T acc[PPT];
-  int pa[PPT], pb[PPT];
+  int pa[PPT], pb[PPT], sa[PPT], sb[PPT];
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
     acc[q] = zero<T>();
     const int pi = tid + 256 * q;
-    pa[q] = pi < npairs ? pairs[pi].x : -1;
-    pb[q] = pi < npairs ? pairs[pi].y : 0;
+    int a = pi < npairs ? pairs[pi].x : -1, b = pi < npairs ? pairs[pi].y : 0;
+    // map concatenated column -> (smem offset, row stride)
+    int oa = 0, ob = 0, wa = 1, wb = 1;
+    for (int p = 0, c0 = 0; p < P.np; c0 += P.nc[p], ++p) {
+      if (a >= c0 && a < c0 + P.nc[p]) { oa = P.off[p] + (a - c0); wa = P.nc[p]; }
+      if (b >= c0 && b < c0 + P.nc[p]) { ob = P.off[p] + (b - c0); wb = P.nc[p]; }
+    }
+    pa[q] = a < 0 ? -1 : oa;
+    pb[q] = ob;
+    sa[q] = wa;
+    sb[q] = wb;
   }
   auto load = [&](int64_t rb, int buf) {
-    T *sx = sbase + buf * stage, *sy = sx + GR * mX;
-    for (int e = tid; e < GR * mX; e += 256) {
-      const int rr = e / mX, cc = e - rr * mX;
-      const int64_t row = rb + rr;
-      const T *src = reinterpret_cast<const T *>(X[cc].p);
-      cp_async_el(sx + e, row < r1 ? src + row * X[cc].stride : src, row < r1);
-    }
-    for (int e = tid; e < GR * mY; e += 256) {
-      const int rr = e / mY, cc = e - rr * mY;
-      const int64_t row = rb + rr;
-      const T *src = reinterpret_cast<const T *>(Y[cc].p);
-      cp_async_el(sy + e, row < r1 ? src + row * Y[cc].stride : src, row < r1);
+    T *s = sbase + buf * stage;
+    const int rows = (int)min((int64_t)GR, r1 - rb);
+    for (int p = 0; p < P.np; ++p) {
+      const T *src = reinterpret_cast<const T *>(P.p[p]) + rb * P.nc[p];
+      T *dst = s + P.off[p];
+      const int ne = GR * P.nc[p], nv = rows * P.nc[p];
+      constexpr int PER = 16 / sizeof(T);   // elements per 16-byte copy
+      for (int e = tid * PER; e < ne; e += 256 * PER) {
+        // bytes actually read (the rest of the 16-byte chunk is zero filled)
+        const int valid = max(0, min(PER, nv - e)) * (int)sizeof(T);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst + e)),
+                     "l"(valid ? src + e : src), "r"(valid)
+                     : "memory");
+      }
     }
     cp_async_commit();
   };
@@ -299,14 +316,15 @@ __global__ void __launch_bounds__(256) k_gram_pairs(const ColDesc *__restrict__ 
     else cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    const T *sx = sbase + buf * stage, *sy = sx + GR * mX;
+    const T *s = sbase + buf * stage;
+    const int rows = (int)min((int64_t)GR, r1 - rb);
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
       if (pa[q] < 0) continue;
-      T s = acc[q];
-#pragma unroll 8
-      for (int rr = 0; rr < GR; ++rr) s = mad(conj(sx[rr * mX + pa[q]]), sy[rr * mY + pb[q]], s);
-      acc[q] = s;
+      T acc_q = acc[q];
+      for (int rr = 0; rr < rows; ++rr)
+        acc_q = mad(conj(s[pa[q] + rr * sa[q]]), s[pb[q] + rr * sb[q]], acc_q);
+      acc[q] = acc_q;
     }
     __syncthreads();
   }
@@ -318,32 +336,37 @@ __global__ void __launch_bounds__(256) k_gram_pairs(const ColDesc *__restrict__ 
 }
 
 template <typename T>
-void gram_pairs(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y,
+void gram_pairs(const std::vector<const T *> &panels, const std::vector<int> &ncols,
                 const std::vector<std::pair<int, int>> &pairs, int64_t n, std::vector<cplx> &out,
                 rbicg_ctx *ctx, cudaStream_t strm) {
-  const int mX = (int)X.size(), mY = (int)Y.size(), np = (int)pairs.size();
+  const int np = (int)pairs.size();
   out.assign(np, cplx(0, 0));
   if (!np) return;
-  RB_CHECK(np <= 256 * PPT, RBICG_EINVAL);
-  const size_t sm = 2 * sizeof(T) * 32 * (size_t)(mX + mY);
+  RB_CHECK(np <= 256 * PPT && panels.size() <= (size_t)MAXP, RBICG_EINVAL);
+  PanelSet P{};
+  P.np = (int)panels.size();
+  int w = 0;
+  for (int p = 0; p < P.np; ++p) {
+    P.p[p] = panels[p];
+    P.nc[p] = ncols[p];
+    P.off[p] = 32 * w;
+    w += ncols[p];
+  }
+  P.width = w;
+  const size_t sm = 2 * sizeof(T) * 32 * (size_t)w;
   RB_CHECK(sm <= 160 * 1024, RBICG_EINVAL);
   const int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, 4 * ctx->nsm));
   const int64_t chunk = ((n + nchunks - 1) / nchunks + 31) / 32 * 32;
   const int nb = (int)((n + chunk - 1) / chunk);
   std::vector<int2> hp(np);
   for (int i = 0; i < np; ++i) hp[i] = make_int2(pairs[i].first, pairs[i].second);
-  const size_t db = sizeof(ColDesc) * (mX + mY), pb = sizeof(int2) * np;
-  const size_t off1 = (db + 15) / 16 * 16, off2 = off1 + (pb + 15) / 16 * 16;
+  const size_t pb = sizeof(int2) * np, off2 = (pb + 15) / 16 * 16;
   char *buf = (char *)ws_alloc(off2 + sizeof(T) * ((size_t)nb * np + np) + 64);
-  ColDesc *dX = (ColDesc *)buf;
-  int2 *dp = (int2 *)(buf + off1);
+  int2 *dp = (int2 *)buf;
   T *dpart = (T *)(buf + off2);
   T *dG = dpart + (size_t)nb * np;
-  std::vector<ColDesc> both(X);
-  both.insert(both.end(), Y.begin(), Y.end());
-  RB_CUDA(cudaMemcpyAsync(dX, both.data(), db, cudaMemcpyHostToDevice, strm));
   RB_CUDA(cudaMemcpyAsync(dp, hp.data(), pb, cudaMemcpyHostToDevice, strm));
-  k_gram_pairs<T><<<nb, 256, sm, strm>>>(dX, mX, dX + mX, mY, dp, np, n, chunk, dpart);
+  k_gram_pairs<T><<<nb, 256, sm, strm>>>(P, dp, np, n, chunk, dpart);
   k_gram_reduce<T><<<(np * 32 + 255) / 256, 256, 0, strm>>>(dpart, nb, np, dG);
   count_launch(2);
   std::vector<T> h(np);
@@ -456,7 +479,7 @@ void prepare_block_kernels() {
 }
 
 #define RB_BINST(T)                                                                        \
-  template void gram_pairs<T>(const std::vector<ColDesc> &, const std::vector<ColDesc> &,     \
+  template void gram_pairs<T>(const std::vector<const T *> &, const std::vector<int> &,        \
                               const std::vector<std::pair<int, int>> &, int64_t,              \
                               std::vector<cplx> &, rbicg_ctx *, cudaStream_t);               \
   template void launch_spmm<T>(const DevMat &, const T *, T *, int, cudaStream_t);         \
