@@ -63,12 +63,20 @@ typedef struct rbicg_ctx rbicg_ctx;
 typedef struct rbicg_mat rbicg_mat;
 typedef struct rbicg_rec rbicg_rec;
 
-/* Multi-GPU row partition (one process per GPU).  NULL = single GPU.
- * Round 1: only nranks == 1 is accepted (RBICG_EINVAL otherwise). */
+/* Multi-GPU row partition.  NULL = single GPU.
+ *   mode 0: one process per GPU, NCCL communicator from nccl_id (an
+ *           ncclUniqueId broadcast by the caller), this process is `rank`.
+ *   mode 1: "virtual ranks" -- nranks row blocks held by this one context on
+ *           one device, halo and reductions done in-process in rank order
+ *           (exercises the partition/halo/reduction logic on one GPU).
+ * Rows are split evenly: rank q owns [floor(q n/P), floor((q+1) n/P)).
+ * row_begin/row_end are outputs filled by rbicg_matrix_csr (informative). */
 typedef struct {
   int32_t rank, nranks;
   uint8_t nccl_id[128];
   int64_t row_begin, row_end;
+  int32_t mode;
+  int32_t reserved;
 } rbicg_dist;
 
 typedef struct {
@@ -167,6 +175,19 @@ int rbicg_dbg_project(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
  * does not touch x, p), [5] 1 if pass 1 stages matrix tiles via TMA. */
 int rbicg_dbg_time_kernels(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
                            const rbicg_opts *opts, int iters, double *ms);
+
+/* Host-only partition plan (no GPU needed): for `rank` of `nranks` even row
+ * blocks of the n x n CSR (global column indices), the ghost columns of the
+ * SpMV pair (columns of local rows of A and A^* owned elsewhere, sorted), the
+ * owners they are received from and the own rows sent to each neighbour.
+ * Two-call pattern: counts[6] = {row_begin, row_end, nghost, nrecv_nbr,
+ * nsend_nbr, nsend_idx}; array outputs may be NULL.  send_idx holds local
+ * row indices, concatenated per send neighbour in that neighbour's ghost
+ * order. */
+int rbicg_plan_partition(int64_t n, const int32_t *rowptr, const int32_t *colind,
+                         int32_t nranks, int32_t rank, int64_t *counts, int64_t *ghost,
+                         int32_t *recv_nbr, int64_t *recv_cnt, int32_t *send_nbr,
+                         int64_t *send_cnt, int32_t *send_idx);
 
 const char *rbicg_strerror(int status);
 /* Kernel launches issued through this library since load (driver evidence). */

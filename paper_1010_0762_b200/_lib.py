@@ -46,7 +46,8 @@ STATUS = {0: "ok", 1: "maxiter", 2: "breakdown_serious", 3: "breakdown_second",
 class Dist(C.Structure):
     _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32),
                 ("nccl_id", C.c_uint8 * 128), ("row_begin", C.c_int64),
-                ("row_end", C.c_int64)]
+                ("row_end", C.c_int64), ("mode", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class Opts(C.Structure):
@@ -96,6 +97,8 @@ _sig = {
                                     C.c_int]),
     "rbicg_dbg_time_kernels": (C.c_int, [vp, vp, vp, C.POINTER(Opts), C.c_int,
                                          vp]),
+    "rbicg_plan_partition": (C.c_int, [C.c_int64, vp, vp, C.c_int32, C.c_int32,
+                                       vp, vp, vp, vp, vp, vp, vp]),
     "rbicg_strerror": (C.c_char_p, [C.c_int]),
     "rbicg_launch_count": (C.c_int64, []),
 }

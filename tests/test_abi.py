@@ -37,4 +37,4 @@ def test_struct_layouts_match_header():
     from paper_1010_0762_b200 import _lib
     assert C.sizeof(_lib.Opts) == 4 * 3 + 4 + 8 * 2 + 8 + 4 * 4
     assert C.sizeof(_lib.Result) == 5 * 4 + 4 + 8 * 10 + 8
-    assert C.sizeof(_lib.Dist) == 4 + 4 + 128 + 8 + 8
+    assert C.sizeof(_lib.Dist) == 4 + 4 + 128 + 8 + 8 + 4 + 4
