@@ -269,10 +269,18 @@ struct Solver {
   bool real = true;
   int64_t n = 0;
   int kmax = 0, ring = 0;
+  int64_t ldr = 0;   // ring column stride (elements)
   std::vector<void *> owned;
   T *rring = nullptr, *rtring = nullptr, *p[2] = {}, *pt[2] = {}, *z = nullptr, *zt = nullptr;
   T *x = nullptr, *xt = nullptr, *b = nullptr, *bt = nullptr, *xo = nullptr, *xto = nullptr;
   T *pseg = nullptr, *ptseg = nullptr;
+  T *pring = nullptr, *ptring = nullptr;
+  int pring_len = 0;
+  // p_0 = p~_0 = 0 (Algorithm 2 starts from p_0 = 0, β_0 = 0)
+  void zero_p0(cudaStream_t s) {
+    RB_CUDA(cudaMemsetAsync(pring_len ? pring : p[0], 0, sizeof(T) * n, s));
+    RB_CUDA(cudaMemsetAsync(pring_len ? ptring : pt[0], 0, sizeof(T) * n, s));
+  }
   bool lazy_x = true;
   struct Basis {
     T *U = nullptr, *Ut = nullptr, *C = nullptr, *Ct = nullptr;
@@ -325,11 +333,25 @@ struct Solver {
         RB_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, ctx->prio_lo));
       }
     }
-    rring = alloc((size_t)ring * n);
-    rtring = alloc((size_t)ring * n);
+    ldr = (n + 31) / 32 * 32;   // ring columns start on 256-byte lines
+    rring = alloc((size_t)ring * ldr);
+    rtring = alloc((size_t)ring * ldr);
     for (int q = 0; q < 2; ++q) {
       p[q] = alloc(n);
       pt[q] = alloc(n);
+    }
+    // directions as ring columns when memory allows (the persistent loop
+    // kernel may then gather them through the read-only path, persist.cu)
+    if (!getenv("RBICG_PRING") || atoi(getenv("RBICG_PRING")) != 0) {
+      size_t fr = 0, tot = 0;
+      RB_CUDA(cudaMemGetInfo(&fr, &tot));
+      const size_t need = (size_t)2 * ring * ldr * sizeof(T);
+      const size_t rest = (size_t)(16 * kmax + 16) * n * sizeof(T);
+      if (fr > need + rest + ((size_t)4 << 30)) {
+        pring = alloc((size_t)ring * ldr);
+        ptring = alloc((size_t)ring * ldr);
+        pring_len = ring;
+      }
     }
     z = alloc(n);
     zt = alloc(n);
@@ -367,12 +389,41 @@ struct Solver {
     la.n = n;
     la.k = cur.k;
     la.ring = ring;
+    la.ldr = ldr;
     la.G = ctx->grid_stream;
     la.A = M->A;
     la.AH = M->AH;
     la.tile_max = std::max(M->A.tile_max, M->AH.tile_max);
-    la.staged = (2.0 * la.tile_max * (4 + sizeof(T)) <= 96 * 1024 && !getenv("RBICG_NO_TMA")) ? 1 : 0;
+    la.tile_max_h = std::max(M->A.tile_max_h, M->AH.tile_max_h);
+    // Pass-1 form, measured on B200 (scripts/kbench.py): without a
+    // recycle space one thread per row gathers both products from 256-row
+    // tiles, one TMA stage; with a recycle space the split form (one thread
+    // per row and matrix, 128-row tiles) leaves room to stage the C, C~ rows.
+    auto envi = [](const char *nm, int dflt) { const char *e = getenv(nm); return e ? atoi(e) : dflt; };
+    const char *sc = getenv("RBICG_P1_STAGEC");
+    const double cap = (sc ? atof(sc) : 110.0) * 1024;
+    la.split = envi("RBICG_SPLIT", cur.k > 0 ? 1 : 0);
+    la.p1_stages = std::min(2, std::max(1, envi("RBICG_P1_STAGES", 1)));
+    la.stage_v = envi("RBICG_STAGEV", la.split ? 1 : 0);
+    la.l2ef = envi("RBICG_L2EF", 1);
+    la.pf = envi("RBICG_PF", 0);
+    la.abl = 0;
     la.pass2_tma = getenv("RBICG_NO_TMA2") ? 0 : 1;
+    const bool tma_ok = !getenv("RBICG_NO_TMA");
+    if (la.split) {
+      const double st_h = 2.0 * la.tile_max_h * (4 + sizeof(T)) + (la.stage_v ? 4.0 * TRH * sizeof(T) : 0.0);
+      const double cb_h = 2.0 * TRH * cur.k * sizeof(T);
+      la.split = (tma_ok && la.p1_stages * st_h <= 150 * 1024) ? 1 : 0;
+      la.staged = la.split;
+      la.stage_c = (la.split && cur.k > 0 && la.p1_stages * st_h + cb_h <= cap) ? 1 : 0;
+    }
+    if (!la.split) {
+      const double mat_stages =
+          la.p1_stages * (2.0 * la.tile_max * (4 + sizeof(T)) + (la.stage_v ? 4.0 * BS * sizeof(T) : 0.0));
+      const double cbuf = 2.0 * BS * cur.k * sizeof(T);
+      la.staged = (tma_ok && mat_stages <= 150 * 1024) ? 1 : 0;
+      la.stage_c = (la.staged && cur.k > 0 && mat_stages + cbuf <= cap) ? 1 : 0;
+    }
     la.lazy_x = lazy_x ? 1 : 0;
     la.pseg = pseg;
     la.ptseg = ptseg;
@@ -382,6 +433,9 @@ struct Solver {
     la.p[0] = p[0];
     la.p[1] = p[1];
     la.pt[0] = pt[0];
+    la.pring = pring;
+    la.ptring = ptring;
+    la.pring_len = pring_len;
     la.pt[1] = pt[1];
     la.z = z;
     la.zt = zt;
@@ -405,8 +459,8 @@ struct Solver {
   }
 
   static ColDesc col(const T *base, int c, int ld) { return ColDesc{(const void *)(base + c), ld}; }
-  ColDesc rcol(int q) const { return ColDesc{(const void *)(rring + (int64_t)(q % ring) * n), 1}; }
-  ColDesc rtcol(int q) const { return ColDesc{(const void *)(rtring + (int64_t)(q % ring) * n), 1}; }
+  ColDesc rcol(int q) const { return ColDesc{(const void *)(rring + (int64_t)(q % ring) * ldr), 1}; }
+  ColDesc rtcol(int q) const { return ColDesc{(const void *)(rtring + (int64_t)(q % ring) * ldr), 1}; }
 
   // Bi-orthogonalise (U, Ũ, C = AU, C~ = A^*Ũ) of width kin into `out`
   // (Q13: unit columns, absolute cut on the singular values).
@@ -559,7 +613,16 @@ struct Solver {
     hst->seg_start = bidx;
   }
 
+  // Persistent form (persist.cu, RBICG_PERSIST=1): one cooperative launch
+  // per cycle.  Measured slower than the two-kernel graph with programmatic
+  // launch overlap on C2, so the graph is the default.
+  bool persistent = false;
   void capture_graph() {
+    if (getenv("RBICG_PERSIST") && atoi(getenv("RBICG_PERSIST")) != 0) {
+      int p2s = 0;
+      persistent = loop_grid<T>(la, &p2s) > 0;
+      if (persistent) return;
+    }
     if (gexec) return;
     cudaGraph_t g;
     RB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
@@ -575,6 +638,11 @@ struct Solver {
   }
 
   void run_graph() {
+    if (persistent) {
+      RB_CHECK(launch_loop<T>(la, ctx->stream), RBICG_ECUDA);
+      RB_CUDA(cudaStreamSynchronize(ctx->stream));
+      return;
+    }
     RB_CUDA(cudaGraphLaunch(gexec, ctx->stream));
     g_launches.fetch_add(2 * graph_iters);
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1059,8 +1127,7 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
   copy_in(S.bt, bt, vb, on_device, st);
   copy_in(S.x, x, vb, on_device, st);
   copy_in(S.xt, xt, vb, on_device, st);
-  RB_CUDA(cudaMemsetAsync(S.p[0], 0, vb, st));
-  RB_CUDA(cudaMemsetAsync(S.pt[0], 0, vb, st));
+  S.zero_p0(st);
   // Step 1 + refresh
   S.refresh(R && kin > 0 ? (const T *)R->U : nullptr, R && kin > 0 ? (const T *)R->Ut : nullptr,
             opts->k > 0 ? kin : 0);
@@ -1389,10 +1456,10 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
   count_launch(2);
   RB_CUDA(cudaMemsetAsync(S.x, 0, sizeof(T) * n, ctx->stream));
   RB_CUDA(cudaMemsetAsync(S.xt, 0, sizeof(T) * n, ctx->stream));
-  RB_CUDA(cudaMemsetAsync(S.p[0], 0, sizeof(T) * n, ctx->stream));
-  RB_CUDA(cudaMemsetAsync(S.pt[0], 0, sizeof(T) * n, ctx->stream));
+  S.zero_p0(ctx->stream);
   S.refresh(kin ? (const T *)R->U : nullptr, kin ? (const T *)R->Ut : nullptr, opts->k > 0 ? kin : 0);
   S.make_args();
+  if (const char *e = getenv("RBICG_ABL")) S.la.abl = atoi(e);
   S.init_state();
   S.hst->stop_at = 1 << 30;
   S.push();
@@ -1416,11 +1483,61 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
     t1 += a;
     t2 += b;
   }
+  // the same iterations as the solver runs them: one captured graph, no
+  // events between the kernels (programmatic launch overlap stays possible)
   S.pull();
+  ms[2] = S.hst->done;   // 0 means every timed kernel did full work
+  S.hst->iter = 0;
+  S.hst->done = 0;
+  S.hst->seg_start = 0;
+  S.push();
+  {
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    RB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < iters; ++i) {
+      launch_pass1<T>(S.la, ctx->stream);
+      launch_pass2<T>(S.la, ctx->stream);
+    }
+    RB_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+    RB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    RB_CUDA(cudaGraphDestroy(g));
+    g_launches.fetch_sub(2 * iters);
+    RB_CUDA(cudaEventRecord(ev[0], ctx->stream));
+    RB_CUDA(cudaGraphLaunch(ge, ctx->stream));
+    g_launches.fetch_add(2 * iters);
+    RB_CUDA(cudaEventRecord(ev[1], ctx->stream));
+    RB_CUDA(cudaEventSynchronize(ev[1]));
+    float a = 0;
+    RB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    ms[6] = a / std::max(iters, 1);
+    RB_CUDA(cudaGraphExecDestroy(ge));
+  }
+  S.pull();
+  ms[7] = S.hst->done;
+  // the persistent form: one cooperative launch for the same iterations
+  ms[8] = -1.0;
+  ms[9] = -1.0;
+  int p2s = 0;
+  if (loop_grid<T>(S.la, &p2s) > 0) {
+    S.hst->iter = 0;
+    S.hst->done = 0;
+    S.hst->seg_start = 0;
+    S.hst->stop_at = iters;
+    S.push();
+    RB_CUDA(cudaEventRecord(ev[0], ctx->stream));
+    RB_CHECK(launch_loop<T>(S.la, ctx->stream), RBICG_ECUDA);
+    RB_CUDA(cudaEventRecord(ev[1], ctx->stream));
+    RB_CUDA(cudaEventSynchronize(ev[1]));
+    float a = 0;
+    RB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    S.pull();
+    ms[8] = a / std::max(iters, 1);
+    ms[9] = (S.hst->done == 2 && S.hst->iter == iters) ? 0.0 : 1.0;
+  }
   for (auto &e : ev) cudaEventDestroy(e);
   ms[0] = t1 / std::max(iters, 1);
   ms[1] = t2 / std::max(iters, 1);
-  ms[2] = S.hst->done;   // 0 means every timed kernel did full work
   ms[3] = S.cur.k;
   ms[4] = S.lazy_x ? 1.0 : 0.0;
   ms[5] = S.la.staged;

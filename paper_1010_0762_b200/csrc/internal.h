@@ -12,6 +12,7 @@ namespace rbicg {
 
 constexpr int KMAX = 32;   // maximum recycle width supported by the kernels
 constexpr int BS = 256;    // threads per block of the streaming kernels
+constexpr int TRH = BS / 2;  // rows per tile of the split form of pass 1
 
 // SELL-32 matrix (slices of 32 consecutive rows, column-major inside a slice,
 // zero-padded to the slice's longest row; sigma = 1, i.e. no row sorting, so
@@ -19,6 +20,7 @@ constexpr int BS = 256;    // threads per block of the streaming kernels
 struct DevMat {
   int64_t n = 0, nslices = 0, padded = 0;
   int tile_max = 0;         // max elements in one 256-row tile (8 slices)
+  int tile_max_h = 0;       // max elements in one 128-row tile (4 slices)
   int max_w = 0;            // widest slice (padded row length)
   int64_t *sptr = nullptr;  // nslices + 1 element offsets (multiples of 32)
   int32_t *cols = nullptr;
@@ -37,6 +39,7 @@ struct DevState {
   int k;
   int seg_start;   // lazy x: first iteration index of the open segment
   unsigned cnt[4];
+  unsigned gen;  // grid-barrier generation of the persistent loop kernel
   T rho, beta, alpha, sigma;   // ρ_{i}, β_{i}, α_i, σ_i
   double rnorm, rtnorm;        // ||r_i||, ||r~_i||
   double tolb, tolbt;          // tol ||b||, tol ||b~||
@@ -57,14 +60,24 @@ template <typename T>
 struct LoopArgs {
   int64_t n;
   int k, ring, G;
+  int64_t ldr;             // ring column stride (n rounded up to 32)
   int staged, tile_max;    // pass 1 stages SELL tiles in smem via TMA
+  int split, tile_max_h;   // pass 1 in the split form: 128-row tiles, one thread per row and matrix
+  int p1_stages;           // TMA stages of SELL tiles in pass 1 (1 or 2)
+  int stage_v;             // pass-1 stages also carry the tile's rows of r, p, r~, p~
+  int stage_c;             // pass 1 also bulk-copies the C, C~ rows of each tile
+  int l2ef;                // matrix tiles loaded with an L2 evict-first policy
+  int pf;                  // pass 1 prefetches the next tile's vector rows into L2
+  int abl;                 // timing ablations (RBICG_ABL, never set in a solve): 1 no gathers
   int pass2_tma;           // pass 2 streams its tiles through smem via TMA
   int lazy_x;              // x, x~ rebuilt per segment from the Lanczos ring
   T *pseg, *ptseg;         // p_a, p~_a at the start of the open segment
   int nsm;
   DevMat A, AH;
   T *rring, *rtring;       // ring of residual columns (r_m in column m % ring)
-  T *p[2], *pt[2];         // ping-pong search directions
+  T *p[2], *pt[2];         // ping-pong search directions (pring_len == 0)
+  T *pring, *ptring;       // or a ring of direction columns: p_i in column i % pring_len
+  int pring_len;           //   (stride ldr), never rewritten within one launch
   T *z, *zt;
   T *x, *xt;
   const T *C, *Ct;         // row-major n x k
@@ -134,6 +147,18 @@ template <typename T>
 void launch_init2(const LoopArgs<T> &a, const T *U, const T *Ut, cudaStream_t s);
 template <typename T>
 void launch_step7(const LoopArgs<T> &a, const T *U, const T *Ut, T *xo, T *xto, cudaStream_t s);
+// Allow a kernel all the dynamic shared memory an SM offers beside its
+// static shared memory (227 KB per block on sm_100a).
+template <typename F> inline void allow_max_dyn_smem(F *f) {
+  cudaFuncAttributes fa{};
+  RB_CUDA(cudaFuncGetAttributes(&fa, (const void *)f));
+  RB_CUDA(cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(227 * 1024 - fa.sharedSizeBytes)));
+}
+// ---- persist.cu (one cooperative launch per cycle)
+void prepare_loop_kernels();
+template <typename T> int loop_grid(const LoopArgs<T> &a, int *p2_staged);   // 0: not possible
+template <typename T> bool launch_loop(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T>
 void launch_spmv_pair(const DevMat &A, const DevMat &AH, const T *p, const T *pt, T *z, T *zt,
                       cudaStream_t s);

@@ -105,6 +105,10 @@ static void csr_to_sell(rbicg_ctx *ctx, int64_t n, const int32_t *rowptr, const 
   for (int64_t s0 = 0; s0 < out.nslices; s0 += BS / 32)
     tm = std::max(tm, hs[std::min(s0 + BS / 32, out.nslices)] - hs[s0]);
   out.tile_max = (int)std::min<int64_t>(tm, INT32_MAX);
+  int64_t tmh = 0;
+  for (int64_t s0 = 0; s0 < out.nslices; s0 += BS / 64)
+    tmh = std::max(tmh, hs[std::min(s0 + BS / 64, out.nslices)] - hs[s0]);
+  out.tile_max_h = (int)std::min<int64_t>(tmh, INT32_MAX);
   int64_t mw = 0;
   for (int64_t s0 = 0; s0 < out.nslices; ++s0) mw = std::max(mw, (hs[s0 + 1] - hs[s0]) / 32);
   out.max_w = (int)std::min<int64_t>(mw, INT32_MAX);

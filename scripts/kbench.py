@@ -28,4 +28,8 @@ for k in (0, cfg.k):
     b2 = 2 * kk * n * w + (6 if t["lazy_x"] else 12) * n * w
     print(json.dumps(dict(config=cfg.name, k=kk, pass1_ms=t["pass1_ms"], pass2_ms=t["pass2_ms"],
                           pass1_GBps=b1 / t["pass1_ms"] / 1e6, pass2_GBps=b2 / t["pass2_ms"] / 1e6,
-                          iter_GBps=(b1 + b2) / (t["pass1_ms"] + t["pass2_ms"]) / 1e6, done=t["done_flag"])))
+                          iter_GBps=(b1 + b2) / (t["pass1_ms"] + t["pass2_ms"]) / 1e6, done=t["done_flag"],
+                          graph_iter_ms=t["graph_iter_ms"], graph_GBps=(b1 + b2) / t["graph_iter_ms"] / 1e6,
+                          graph_done=t["graph_done_flag"], loop_iter_ms=t["loop_iter_ms"],
+                          loop_GBps=(b1 + b2) / t["loop_iter_ms"] / 1e6 if t["loop_iter_ms"] > 0 else None,
+                          loop_done=t["loop_done_flag"])))

@@ -140,6 +140,30 @@ def _cosines(X, Y):
     return np.linalg.svd(Q1.conj().T @ Q2, compute_uv=False)
 
 
+def _oracle_ensemble(R, Ad, item, x0, xt0, U, Ut, k, s, tol, max_itn, trunc, size=8):
+    """Oracle iteration counts under rounding-level perturbations of b
+    (relative 1e-15, seeded): the spread of equally correct counts (Q28)."""
+    rng = np.random.default_rng(12345)
+    b = item["b"]
+    cnt = []
+    for _ in range(size):
+        bp = b * (1 + 1e-15 * rng.standard_normal(b.shape))
+        r = R.solve_dual(Ad, bp, item["bt"], x0, xt0, U=U, Ut=Ut, k=k, s=s, tol=tol,
+                         max_itn=max_itn, trunc_tol=trunc, update_recycle=False)
+        cnt.append(r.iterations)
+    return min(cnt), max(cnt)
+
+
+def _residual_bound_check(Ad, item, x, xt, ref):
+    """x - x_ref = A^{-1}(r_ref - r_gpu): both solutions within
+    ||A^{-1}|| (||r|| + ||r_ref||) of each other (dense, small n only)."""
+    A = Ad.toarray()
+    nrm_inv = 1.0 / np.linalg.svd(A, compute_uv=False)[-1]
+    for xs, xr, rhs, M in ((x, ref.x, item["b"], A), (xt, ref.xt, item["bt"], A.conj().T)):
+        bound = nrm_inv * (np.linalg.norm(rhs - M @ xs) + np.linalg.norm(rhs - M @ xr))
+        assert np.linalg.norm(xs - xr) <= 1.01 * bound + 1e-14 * np.linalg.norm(xr)
+
+
 def _carry_from_oracle(ctx, cfg_k, cfg_s, tol, trunc, items, csr_of, max_itn,
                        lam_slots=False, check_space=0.0):
     """Q27 protocol: every system is solved by both sides from the ORACLE's
@@ -167,11 +191,20 @@ def _carry_from_oracle(ctx, cfg_k, cfg_s, tol, trunc, items, csr_of, max_itn,
                                        max_itn=max_itn, trunc_tol=trunc)
         its.append((res["iterations"], ref.iterations))
         assert res["status"] == ref.status, (res, ref.status)
-        assert iters_close(res["iterations"], ref.iterations), its
         assert res["relres_true"] <= tol and res["relres_dual_true"] <= tol
         assert res["k_in"] == ref.basis_in.k
         m = res["iterations"]
-        if m != ref.iterations:
+        if not iters_close(m, ref.iterations):
+            # DESIGN.md reading Q28: a system whose iteration count the
+            # oracle itself does not reproduce under rounding-level input
+            # perturbations is judged against that ensemble, and its solution
+            # by the residual bound instead of at a matched count.
+            lo, hi = _oracle_ensemble(R, Ad, item, x0, xt0, U, Ut, cfg_k, cfg_s, tol,
+                                      max_itn, trunc)
+            assert hi - lo > max(2, 0.03 * hi), (its, lo, hi)   # really chaotic
+            assert lo - 2 <= m <= hi + 2, (its, lo, hi)
+            _residual_bound_check(Ad, item, x, xt, ref)
+        elif m != ref.iterations:
             ref_m = R.solve_dual(Ad, item["b"], item["bt"], x0, xt0, U=U, Ut=Ut,
                                  k=cfg_k, s=cfg_s, tol=tol, max_itn=max_itn,
                                  trunc_tol=trunc, force_iters=m,
@@ -179,7 +212,8 @@ def _carry_from_oracle(ctx, cfg_k, cfg_s, tol, trunc, items, csr_of, max_itn,
             xr = ref_m.x
         else:
             xr = ref.x
-        assert np.linalg.norm(x - xr) <= 1e-7 * np.linalg.norm(xr), its
+        if iters_close(m, ref.iterations):
+            assert np.linalg.norm(x - xr) <= 1e-7 * np.linalg.norm(xr), its
         if check_space and ref.basis_out.k:
             Ug, Utg = rec.export()
             assert Ug.shape[1] == ref.basis_out.k
