@@ -63,14 +63,25 @@ typedef struct rbicg_ctx rbicg_ctx;
 typedef struct rbicg_mat rbicg_mat;
 typedef struct rbicg_rec rbicg_rec;
 
-/* Multi-GPU row partition.  NULL = single GPU.
- *   mode 0: one process per GPU, NCCL communicator from nccl_id (an
- *           ncclUniqueId broadcast by the caller), this process is `rank`.
- *   mode 1: "virtual ranks" -- nranks row blocks held by this one context on
- *           one device, halo and reductions done in-process in rank order
- *           (exercises the partition/halo/reduction logic on one GPU).
+/* Multi-GPU row partition.  NULL or nranks == 1 = one GPU.
+ *   mode 0: one process per GPU; NCCL communicator from nccl_id (the
+ *           ncclUniqueId of rbicg_nccl_unique_id on rank 0, broadcast by the
+ *           caller); this process is `rank`.  Collectives are stream-ordered
+ *           and captured in the loop's CUDA graph.
+ *   mode 1: "virtual ranks" -- nranks contexts in ONE process, one host
+ *           thread each (normally all on one GPU), meeting at host barriers;
+ *           nccl_id is any 128-byte token shared by the group.  Every
+ *           collective synchronises its stream (no graph, no kernel ever
+ *           waits on another); sums are taken in rank order.  For testing the
+ *           partitioned path where fewer GPUs than ranks exist.
  * Rows are split evenly: rank q owns [floor(q n/P), floor((q+1) n/P)).
- * row_begin/row_end are outputs filled by rbicg_matrix_csr (informative). */
+ * Partitioned calls are collective: every rank makes the same calls in the
+ * same order.  rbicg_matrix_csr takes the GLOBAL CSR on every rank (each rank
+ * keeps its rows of A and A^* and derives its halo plan without
+ * communication); vectors (b, x, u, w, ...) and recycle blocks are the rank's
+ * own rows; scalar results are replicated.  The dbg_project and
+ * dbg_time_kernels hooks are single-GPU only (RBICG_EINVAL).
+ * row_begin/row_end are informative (see rbicg_plan_partition). */
 typedef struct {
   int32_t rank, nranks;
   uint8_t nccl_id[128];
@@ -194,6 +205,10 @@ int rbicg_plan_partition(int64_t n, const int32_t *rowptr, const int32_t *colind
                          int32_t nranks, int32_t rank, int64_t *counts, int64_t *ghost,
                          int32_t *recv_nbr, int64_t *recv_cnt, int32_t *send_nbr,
                          int64_t *send_cnt, int32_t *send_idx);
+
+/* 128-byte ncclUniqueId for a mode-0 group (call on rank 0, broadcast it).
+ * RBICG_ENCCL if NCCL cannot be loaded ($RBICG_NCCL or libnccl.so.2). */
+int rbicg_nccl_unique_id(uint8_t *id);
 
 const char *rbicg_strerror(int status);
 /* Kernel launches issued through this library since load (driver evidence). */

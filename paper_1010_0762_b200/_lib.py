@@ -26,6 +26,24 @@ def _lapack_path():
     return libs[0] if libs else None
 
 
+def _nccl_path():
+    """The NCCL that ships with torch (nvidia-nccl wheel), for the row-partitioned path."""
+    try:
+        import nvidia.nccl
+        for base in list(getattr(nvidia.nccl, "__path__", [])):
+            cand = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                return cand
+    except ImportError:      # pragma: no cover
+        pass
+    return None
+
+
+if "RBICG_NCCL" not in os.environ:
+    _p = _nccl_path()
+    if _p:
+        os.environ["RBICG_NCCL"] = _p
+
 if "RBICG_LAPACK" not in os.environ:
     _p = _lapack_path()
     if _p:
@@ -99,6 +117,7 @@ _sig = {
                                          vp]),
     "rbicg_plan_partition": (C.c_int, [C.c_int64, vp, vp, C.c_int32, C.c_int32,
                                        vp, vp, vp, vp, vp, vp, vp]),
+    "rbicg_nccl_unique_id": (C.c_int, [vp]),
     "rbicg_strerror": (C.c_char_p, [C.c_int]),
     "rbicg_launch_count": (C.c_int64, []),
 }

@@ -36,10 +36,23 @@ def _dtype_code(a):
     return C128 if np.iscomplexobj(a) else F64
 
 
-class Context:
-    """rbicg_ctx on one GPU; adopts torch's current stream when available."""
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 of a mode-0 group; broadcast it)."""
+    buf = (C.c_uint8 * 128)()
+    check(lib.rbicg_nccl_unique_id(buf))
+    return bytes(buf)
 
-    def __init__(self, device: int = 0, stream=None):
+
+class Context:
+    """rbicg_ctx on one GPU; adopts torch's current stream when available.
+
+    dist: None (one GPU) or dict(rank=q, nranks=P, mode=0|1, key=bytes[128])
+    for the row-partitioned path (include/rbicg.h rbicg_dist): mode 0 = one
+    process per GPU over NCCL (key = nccl_unique_id() of rank 0), mode 1 =
+    virtual ranks (P contexts in P host threads of one process, any shared
+    key)."""
+
+    def __init__(self, device: int = 0, stream=None, dist=None):
         if stream is None:
             try:
                 import torch
@@ -51,8 +64,19 @@ class Context:
         self.device = device
         self._children = []          # weakrefs to matrices / recycle handles
         self._h = C.c_void_p()
+        d = None
+        self.rank, self.nranks = 0, 1
+        if dist is not None:
+            d = _lib.Dist()
+            d.rank, d.nranks = int(dist["rank"]), int(dist["nranks"])
+            d.mode = int(dist.get("mode", 0))
+            key = bytes(dist["key"])[:128].ljust(128, b"\0")
+            for i in range(128):
+                d.nccl_id[i] = key[i]
+            self.rank, self.nranks = d.rank, d.nranks
         check(lib.rbicg_init(C.byref(self._h), device,
-                             C.c_void_p(stream) if stream else None, None))
+                             C.c_void_p(stream) if stream else None,
+                             C.byref(d) if d is not None else None))
 
     def close(self):
         if self._h:
@@ -80,18 +104,23 @@ class Context:
     # ------------------------------------------------------------ solve
     def solve_dual(self, A, b, bt, x=None, xt=None, R=None, *, k=10, s=40,
                    tol=1e-8, max_itn=20000, trunc_tol=1e-6, update_recycle=True,
-                   force_iters=0, xt_redraw=None, history=False):
+                   force_iters=0, xt_redraw=None, history=False, inplace=False):
+        """inplace=True: x, xt (given, contiguous, b's dtype) are the in/out
+        buffers themselves (e.g. page-locked host arrays); otherwise copies."""
         dev = _is_torch(b)
-        if x is None:
-            x = b * 0
-        if xt is None:
-            xt = bt * 0
-        if dev:
-            x = x.clone()
-            xt = xt.clone()
+        if inplace:
+            assert x is not None and xt is not None
         else:
-            x = np.array(x, dtype=b.dtype, copy=True)
-            xt = np.array(xt, dtype=b.dtype, copy=True)
+            if x is None:
+                x = b * 0
+            if xt is None:
+                xt = bt * 0
+            if dev:
+                x = x.clone()
+                xt = xt.clone()
+            else:
+                x = np.array(x, dtype=b.dtype, copy=True)
+                xt = np.array(xt, dtype=b.dtype, copy=True)
         o = Opts(k=k, s=s, max_itn=max_itn, tol=tol, trunc_tol=trunc_tol, seed=0,
                  update_recycle=1 if update_recycle else 0,
                  record_history=1 if history else 0, force_iters=force_iters)

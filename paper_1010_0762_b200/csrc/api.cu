@@ -19,6 +19,7 @@
 #include <thread>
 
 #include "internal.h"
+#include "dist_plan.h"
 
 using namespace rbicg;
 
@@ -270,6 +271,30 @@ struct Solver {
   int64_t n = 0;
   int kmax = 0, ring = 0;
   int64_t ldr = 0;   // ring column stride (elements)
+  // row partition: n own rows, nx = n + ghost rows
+  bool dist = false;
+  int64_t nx = 0;
+  T *hsend = nullptr, *hsend_side = nullptr, *hrecv = nullptr, *red = nullptr;
+  // halo of a row block X (nx rows x k, row-major, own rows current) on comm
+  void halo_rows(T *X, int k, Comm *cm, T *sbuf, cudaStream_t s) {
+    if (!dist || k <= 0) return;
+    launch_pack_rows<T>(X, k, M->halo.send_idx, M->halo.nsend, sbuf, s);
+    cm->exchange(M->halo, sbuf, X + n * k, 0, (size_t)k * sizeof(T), 1, s);
+  }
+  // sum of `cnt` scalars at red over the ranks (stream-ordered)
+  void allreduce_red(int cnt, cudaStream_t s) {
+    if (dist) ctx->comm->allreduce_dev((double *)red, (int64_t)cnt * (int64_t)(sizeof(T) / 8), s);
+  }
+  static void sum_host(Comm *cm, std::vector<cplx> &v) {
+    if (cm && cm->nranks > 1) cm->allreduce_host((double *)v.data(), (int64_t)2 * v.size());
+  }
+  template <typename V> static void bcast_vec(Comm *cm, std::vector<V> &v) {
+    if (!cm || cm->nranks <= 1) return;
+    int64_t sz = (int64_t)v.size();
+    cm->bcast_host(&sz, sizeof(sz), 0);
+    v.resize(sz);
+    if (sz) cm->bcast_host(v.data(), sizeof(V) * sz, 0);
+  }
   std::vector<void *> owned;
   T *rring = nullptr, *rtring = nullptr, *p[2] = {}, *pt[2] = {}, *z = nullptr, *zt = nullptr;
   T *x = nullptr, *xt = nullptr, *b = nullptr, *bt = nullptr, *xo = nullptr, *xto = nullptr;
@@ -333,16 +358,28 @@ struct Solver {
         RB_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, ctx->prio_lo));
       }
     }
-    ldr = (n + 31) / 32 * 32;   // ring columns start on 256-byte lines
+    // row partition: gathered vectors carry the ghost rows [n, nx) behind the own rows
+    dist = ctx->dist();
+    nx = n + (dist ? m->halo.nghost : 0);
+    ldr = (nx + 31) / 32 * 32;   // ring columns start on 256-byte lines
     rring = alloc((size_t)ring * ldr);
     rtring = alloc((size_t)ring * ldr);
     for (int q = 0; q < 2; ++q) {
-      p[q] = alloc(n);
-      pt[q] = alloc(n);
+      p[q] = alloc(nx);
+      pt[q] = alloc(nx);
+    }
+    if (dist) {
+      const int64_t ns = std::max<int64_t>(m->halo.nsend, 1), ng = std::max<int64_t>(m->halo.nghost, 1);
+      hsend = alloc((size_t)std::max(4, kmax) * ns);
+      hsend_side = alloc((size_t)kmax * ns);
+      hrecv = alloc((size_t)4 * ng);
+      red = alloc((size_t)4 * KMAX + 8);
     }
     // directions as ring columns when memory allows (the persistent loop
     // kernel may then gather them through the read-only path, persist.cu)
-    if (!getenv("RBICG_PRING") || atoi(getenv("RBICG_PRING")) != 0) {
+    const bool want_ring = getenv("RBICG_PRING") ? atoi(getenv("RBICG_PRING")) != 0
+                                                 : (getenv("RBICG_PERSIST") && atoi(getenv("RBICG_PERSIST")) != 0);
+    if (want_ring) {
       size_t fr = 0, tot = 0;
       RB_CUDA(cudaMemGetInfo(&fr, &tot));
       const size_t need = (size_t)2 * ring * ldr * sizeof(T);
@@ -355,18 +392,18 @@ struct Solver {
     }
     z = alloc(n);
     zt = alloc(n);
-    x = alloc(n);
-    xt = alloc(n);
+    x = alloc(nx);
+    xt = alloc(nx);
     b = alloc(n);
     bt = alloc(n);
-    xo = alloc(n);
-    xto = alloc(n);
+    xo = alloc(nx);
+    xto = alloc(nx);
     lazy_x = getenv("RBICG_EAGER_X") == nullptr;
     pseg = alloc(n);
     ptseg = alloc(n);
     for (Basis *B : {&cur, &cand[0], &cand[1], &tmp}) {
-      B->U = alloc((size_t)n * kmax);
-      B->Ut = alloc((size_t)n * kmax);
+      B->U = alloc((size_t)nx * kmax);
+      B->Ut = alloc((size_t)nx * kmax);
       B->C = alloc((size_t)n * kmax);
       B->Ct = alloc((size_t)n * kmax);
       B->k = 0;
@@ -448,6 +485,8 @@ struct Solver {
     la.zhist = zhist;
     la.zthist = zthist;
     la.part = part;
+    la.dist = dist ? 1 : 0;
+    la.red = red;
   }
 
   void pull() {
@@ -465,7 +504,7 @@ struct Solver {
   // Bi-orthogonalise (U, Ũ, C = AU, C~ = A^*Ũ) of width kin into `out`
   // (Q13: unit columns, absolute cut on the singular values).
   void biorth(const T *U, const T *Ut, const T *C, const T *Ct, int kin, Basis &out,
-              cudaStream_t bs) {
+              cudaStream_t bs, Comm *cm) {
     // only ||c_j||^2, ||c~_j||^2 and C~^*C are needed (Q13 scaling + SVD)
     std::vector<ColDesc> X;
     for (int c = 0; c < kin; ++c) X.push_back(col(C, c, kin));
@@ -480,6 +519,7 @@ struct Solver {
       Phase ph("biorth.gram", bs);
       gram_pairs<T>({C, Ct}, {kin, kin}, pairs, n, gv, ctx, bs);
     }
+    sum_host(dist ? cm : nullptr, gv);   // partial Grams of the row blocks (C-4)
     {
       const int mm = 2 * kin;
       size_t q = 0;
@@ -504,7 +544,12 @@ struct Solver {
     std::vector<double> S;
     std::vector<cplx> Ml, Nr;
     const double t0 = now_ms();
-    RB_CHECK(lapack_gesvd(real, m, Gn, S, Ml, Nr) == 0, RBICG_ELAPACK);
+    if (!dist || cm->rank == 0) RB_CHECK(lapack_gesvd(real, m, Gn, S, Ml, Nr) == 0, RBICG_ELAPACK);
+    if (dist) {   // one host result for every rank (C-5)
+      bcast_vec(cm, S);
+      bcast_vec(cm, Ml);
+      bcast_vec(cm, Nr);
+    }
     t_host_eig += now_ms() - t0;
     int pk = 0;
     for (int a = 0; a < m; ++a)
@@ -535,9 +580,18 @@ struct Solver {
     const double t0 = now_ms();
     cur.k = 0;
     if (kin > 0) {
-      launch_spmm<T>(M->A, U, tmp.C, kin, ctx->stream);
-      launch_spmm<T>(M->AH, Ut, tmp.Ct, kin, ctx->stream);
-      biorth(U, Ut, tmp.C, tmp.Ct, kin, cur, ctx->stream);
+      const T *Uh = U, *Uth = Ut;
+      if (dist) {   // ghost rows of U, Ũ for the SpMM (C-6)
+        RB_CUDA(cudaMemcpyAsync(tmp.U, U, sizeof(T) * n * kin, cudaMemcpyDeviceToDevice, ctx->stream));
+        RB_CUDA(cudaMemcpyAsync(tmp.Ut, Ut, sizeof(T) * n * kin, cudaMemcpyDeviceToDevice, ctx->stream));
+        halo_rows(tmp.U, kin, ctx->comm.get(), hsend, ctx->stream);
+        halo_rows(tmp.Ut, kin, ctx->comm.get(), hsend, ctx->stream);
+        Uh = tmp.U;
+        Uth = tmp.Ut;
+      }
+      launch_spmm<T>(M->A, Uh, tmp.C, kin, ctx->stream);
+      launch_spmm<T>(M->AH, Uth, tmp.Ct, kin, ctx->stream);
+      biorth(U, Ut, tmp.C, tmp.Ct, kin, cur, ctx->stream, ctx->comm.get());
     }
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
     t_refresh += now_ms() - t0;
@@ -556,14 +610,46 @@ struct Solver {
   }
 
   // r_{-1}, minusXR, ρ_0; returns after the state has been pulled.
+  // r = b - A x, r~ = b~ - A^* x~ with the norms (and, with coef, C~^*r and
+  // C^*r~): the partitioned form exchanges the ghosts of x first and sums the
+  // block results over the ranks before the scalar step.
+  void residual(const T *xv, const T *xtv, T *r, T *rt, int coef) {
+    if (dist) {
+      halo_rows(const_cast<T *>(xv), 1, ctx->comm.get(), hsend, ctx->stream);
+      halo_rows(const_cast<T *>(xtv), 1, ctx->comm.get(), hsend, ctx->stream);
+    }
+    launch_resid<T>(la, b, bt, xv, xtv, r, rt, coef, ctx->stream);
+    if (dist) {
+      allreduce_red(4 + 2 * (coef ? la.k : 0), ctx->stream);
+      launch_leader_resid<T>(la, coef, ctx->stream);
+    }
+  }
   void initial_projection() {
-    launch_resid<T>(la, b, bt, x, xt, rring, rtring, cur.k > 0 ? 1 : 0, ctx->stream);
+    residual(x, xt, rring, rtring, cur.k > 0 ? 1 : 0);
     pull();
     hst->tolb = o.tol * std::sqrt(hst->bn2);
     hst->tolbt = o.tol * std::sqrt(hst->btn2);
     push();
     launch_init2<T>(la, cur.U, cur.Ut, ctx->stream);
+    if (dist) {
+      allreduce_red(3, ctx->stream);
+      launch_leader_init2<T>(la, ctx->stream);
+    }
     pull();
+  }
+  // one iteration of the partitioned loop: halo of r, p, r~, p~ (C-1), SpMV
+  // pair + coefficients, allreduce #1 (C-2), α step, updates, allreduce #2
+  // (C-3), β step and stop test.
+  void dist_iteration(cudaStream_t s) {
+    launch_halo_pack_loop<T>(la, M->halo.send_idx, M->halo.nsend, hsend, s);
+    ctx->comm->exchange(M->halo, hsend, hrecv, (int64_t)M->halo.nghost * sizeof(T), sizeof(T), 4, s);
+    launch_halo_unpack_loop<T>(la, hrecv, M->halo.nghost, s);
+    launch_pass1<T>(la, s);
+    allreduce_red(3 * la.k + 1, s);
+    launch_leader1<T>(la, s);
+    launch_pass2<T>(la, s);
+    allreduce_red(3, s);
+    launch_leader2<T>(la, s);
   }
 
   // Lazy x: over the open segment (a, b] the iterate update
@@ -617,34 +703,53 @@ struct Solver {
   // per cycle.  Measured slower than the two-kernel graph with programmatic
   // launch overlap on C2, so the graph is the default.
   bool persistent = false;
+  bool uncaptured = false;   // partitioned with host-synchronised collectives
   void capture_graph() {
-    if (getenv("RBICG_PERSIST") && atoi(getenv("RBICG_PERSIST")) != 0) {
+    if (dist && !ctx->comm->capturable()) {
+      uncaptured = true;
+      return;
+    }
+    if (!dist && getenv("RBICG_PERSIST") && atoi(getenv("RBICG_PERSIST")) != 0) {
       int p2s = 0;
       persistent = loop_grid<T>(la, &p2s) > 0;
       if (persistent) return;
     }
     if (gexec) return;
     cudaGraph_t g;
+    const int64_t l0 = g_launches.load();
     RB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     for (int it = 0; it < o.s; ++it) {
-      launch_pass1<T>(la, ctx->stream);
-      launch_pass2<T>(la, ctx->stream);
+      if (dist) {
+        dist_iteration(ctx->stream);
+      } else {
+        launch_pass1<T>(la, ctx->stream);
+        launch_pass2<T>(la, ctx->stream);
+      }
     }
     RB_CUDA(cudaStreamEndCapture(ctx->stream, &g));
     RB_CUDA(cudaGraphInstantiate(&gexec, g, 0));
     RB_CUDA(cudaGraphDestroy(g));
     graph_iters = o.s;
-    g_launches.fetch_sub(2 * o.s);   // captured, not launched
+    graph_launch_kernels = g_launches.load() - l0;
+    g_launches.fetch_sub(graph_launch_kernels);   // captured, not launched
   }
 
   void run_graph() {
+    if (uncaptured) {   // virtual ranks: iteration by iteration
+      for (int it = 0; it < o.s; ++it) {
+        dist_iteration(ctx->stream);
+        pull();
+        if (hst->done) break;
+      }
+      return;
+    }
     if (persistent) {
       RB_CHECK(launch_loop<T>(la, ctx->stream), RBICG_ECUDA);
       RB_CUDA(cudaStreamSynchronize(ctx->stream));
       return;
     }
     RB_CUDA(cudaGraphLaunch(gexec, ctx->stream));
-    g_launches.fetch_add(2 * graph_iters);
+    g_launches.fetch_add(graph_launch_kernels);
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
   }
 
@@ -777,6 +882,7 @@ struct Solver {
         Phase ph("cycle.gram", cs);
         gram<T>(X, Y, n, Graw, ctx, cs);
       }
+      sum_host(dist ? ctx->comm_side.get() : nullptr, Graw);   // C-4
       const int mY = (int)Y.size();
       std::vector<cplx> G1((size_t)mpsi * mpsi), G2((size_t)mpsi * (kx + s));
       for (int a = 0; a < mpsi; ++a) {
@@ -837,13 +943,22 @@ struct Solver {
     // host QZ with left and right vectors + Q11/Q12 selection
     teig0 = now_ms();
     Phase phe("cycle.host_eig", cs);
-    std::vector<cplx> alpha, beta, VL, VR;
-    std::vector<int> pf;
-    RB_CHECK(lapack_ggev(real, mp, P, Q, alpha, beta, VL, VR, pf) == 0, RBICG_ELAPACK);
-    double qn = 0;
-    for (auto &v : Q) qn += std::norm(v);
-    qn = std::sqrt(qn);
-    Selection sel = select_pairs(real, mp, o.k, alpha, beta, VL, VR, qn);
+    Selection sel;
+    Comm *cms = dist ? ctx->comm_side.get() : nullptr;
+    if (!dist || cms->rank == 0) {
+      std::vector<cplx> alpha, beta, VL, VR;
+      std::vector<int> pf;
+      RB_CHECK(lapack_ggev(real, mp, P, Q, alpha, beta, VL, VR, pf) == 0, RBICG_ELAPACK);
+      double qn = 0;
+      for (auto &v : Q) qn += std::norm(v);
+      qn = std::sqrt(qn);
+      sel = select_pairs(real, mp, o.k, alpha, beta, VL, VR, qn);
+    }
+    if (dist) {   // the selected W_j, W~_j of rank 0 for every rank (C-5)
+      cms->bcast_host(&sel.ksel, sizeof(sel.ksel), 0);
+      bcast_vec(cms, sel.W);
+      bcast_vec(cms, sel.Wt);
+    }
     t_host_eig += now_ms() - teig0;
     ksel = sel.ksel;
     out.k = 0;
@@ -867,10 +982,12 @@ struct Solver {
       }
       {
         Phase ph("cycle.spmm", cs);
+        halo_rows(tmp.U, ksel, cms, hsend_side, cs);
+        halo_rows(tmp.Ut, ksel, cms, hsend_side, cs);
         launch_spmm<T>(M->A, tmp.U, tmp.C, ksel, cs);
         launch_spmm<T>(M->AH, tmp.Ut, tmp.Ct, ksel, cs);
       }
-      biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs);
+      biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms);
     }
     RB_CUDA(cudaStreamSynchronize(cs));
     cand_cur = nxt;
@@ -944,9 +1061,65 @@ const char *rbicg_strerror(int s) {
 
 int64_t rbicg_launch_count(void) { return g_launches.load(); }
 
+// Partitioned store: every rank passes the GLOBAL CSR; rank q
+// keeps rows [floor(qn/P), floor((q+1)n/P)) of A and of A^* with local column
+// indices (own rows first, then the ghost columns sorted by global index,
+// grouped by owner) and the send lists of its own rows (dist.cpp).  No
+// communication is needed: each rank derives its plan from the same matrix.
+static void build_partitioned(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rp_d,
+                              const int32_t *ci_d, const void *vv_d, rbicg_dtype dt, rbicg_mat *M) {
+  const size_t w = wbytes(dt);
+  std::vector<int32_t> rp(n + 1), ci(std::max<int64_t>(nnz, 1));
+  std::vector<unsigned char> vv(w * std::max<int64_t>(nnz, 1));
+  RB_CUDA(cudaMemcpyAsync(rp.data(), rp_d, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, ctx->stream));
+  if (nnz) {
+    RB_CUDA(cudaMemcpyAsync(ci.data(), ci_d, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(vv.data(), vv_d, w * nnz, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  const Plan pl = make_plan(n, rp.data(), ci.data(), ctx->nranks, ctx->rank);
+  std::vector<int32_t> rpA, ciA, rpH, ciH;
+  std::vector<unsigned char> vA, vH;
+  local_csr(pl, n, rp.data(), ci.data(), vv.data(), w, dt == RBICG_C128, false, rpA, ciA, vA);
+  local_csr(pl, n, rp.data(), ci.data(), vv.data(), w, dt == RBICG_C128, true, rpH, ciH, vH);
+  std::vector<void *> tmp;
+  auto up = [&](const void *src, size_t bytes) {
+    void *d = ws_alloc(std::max<size_t>(bytes, 16));
+    tmp.push_back(d);
+    if (bytes) RB_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return d;
+  };
+  const int32_t *drpA = (const int32_t *)up(rpA.data(), 4 * rpA.size());
+  const int32_t *dciA = (const int32_t *)up(ciA.data(), 4 * ciA.size());
+  const void *dvA = up(vA.data(), vA.size());
+  const int32_t *drpH = (const int32_t *)up(rpH.data(), 4 * rpH.size());
+  const int32_t *dciH = (const int32_t *)up(ciH.data(), 4 * ciH.size());
+  const void *dvH = up(vH.data(), vH.size());
+  build_matrix_local(ctx, pl.nloc, drpA, dciA, dvA, drpH, dciH, dvH, dt, M);
+  for (void *d : tmp) ws_free(d);
+  M->nnz = (int64_t)ciA.size();
+  M->row_begin = pl.r0;
+  HaloPlan &h = M->halo;
+  h.nloc = pl.nloc;
+  h.nghost = (int64_t)pl.ghost.size();
+  h.nsend = (int64_t)pl.send_idx.size();
+  h.send_nbr = pl.send_nbr;
+  h.recv_nbr = pl.recv_nbr;
+  h.send_off = pl.send_off;
+  h.send_cnt = pl.send_cnt;
+  h.recv_off = pl.recv_off;
+  h.recv_cnt = pl.recv_cnt;
+  h.send_idx = (int32_t *)ws_alloc(4 * std::max<int64_t>(h.nsend, 1));
+  if (h.nsend)
+    RB_CUDA(cudaMemcpyAsync(h.send_idx, pl.send_idx.data(), 4 * h.nsend, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 int rbicg_init(rbicg_ctx **out, int device, void *stream, const rbicg_dist *dist) {
   if (!out) return RBICG_EINVAL;
-  if (dist && dist->nranks != 1) return RBICG_EINVAL;
+  if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks ||
+               (dist->mode != 0 && dist->mode != 1)))
+    return RBICG_EINVAL;
   return run_guarded([&] {
     int ndev = 0;
     RB_CUDA(cudaGetDeviceCount(&ndev));
@@ -971,8 +1144,31 @@ int rbicg_init(rbicg_ctx **out, int device, void *stream, const rbicg_dist *dist
       if (const char *e = getenv("RBICG_BLOCKS_PER_SM")) mult = std::min(8, std::max(1, atoi(e)));
       c->grid_stream = c->nsm * mult;
     }
+    if (dist && dist->nranks > 1) {   // row partition
+      c->rank = dist->rank;
+      c->nranks = dist->nranks;
+      try {
+        if (dist->mode == 0) {
+          c->comm = make_comm_nccl(dist->rank, dist->nranks, dist->nccl_id, device);
+          c->comm_side = split_comm_nccl(c->comm.get());
+        } else {
+          c->comm = make_comm_threads(dist->rank, dist->nranks, dist->nccl_id, 0);
+          c->comm_side = make_comm_threads(dist->rank, dist->nranks, dist->nccl_id, 1);
+        }
+      } catch (...) {
+        cudaEventDestroy(c->order_ev);
+        cudaStreamDestroy(c->stream);
+        delete c;
+        throw;
+      }
+    }
     *out = c;
   });
+}
+
+int rbicg_nccl_unique_id(uint8_t *id) {
+  if (!id) return RBICG_EINVAL;
+  return run_guarded([&] { nccl_unique_id(id); });
 }
 
 int rbicg_finalize(rbicg_ctx *ctx) {
@@ -1004,8 +1200,10 @@ int rbicg_matrix_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowp
     }
     auto *M = new rbicg_mat();
     M->ctx = ctx;
+    M->n_global = n;
     try {
-      build_matrix(ctx, n, nnz, rp, ci, vv, dtype, M);
+      if (ctx->dist()) build_partitioned(ctx, n, nnz, rp, ci, vv, dtype, M);
+      else build_matrix(ctx, n, nnz, rp, ci, vv, dtype, M);
     } catch (...) {
       ws_free(rp);
       ws_free(ci);
@@ -1026,6 +1224,7 @@ int rbicg_matrix_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowp
 int rbicg_matrix_free(rbicg_mat *A) {
   if (!A) return RBICG_EINVAL;
   // no ctx dereference: the ctx may already be finalized (cudaFree syncs)
+  if (A->halo.send_idx) ws_free(A->halo.send_idx);
   free_devmat(A->A);
   free_devmat(A->AH);
   delete A;
@@ -1178,7 +1377,7 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
     if (S.hst->done == 1 && S.hst->status == RBICG_OK && !S.hst->force) {
       // Step 7 and the true-residual confirmation (Q2)
       launch_step7<T>(S.la, S.cur.U, S.cur.Ut, S.xo, S.xto, st);
-      launch_resid<T>(S.la, S.b, S.bt, S.xo, S.xto, S.z, S.zt, 0, st);
+      S.residual(S.xo, S.xto, S.z, S.zt, 0);
       DevState<T> keep = *S.hst;
       S.pull();
       const double tr = std::sqrt(S.hst->rn2 / S.hst->bn2), trt = std::sqrt(S.hst->rtn2 / S.hst->btn2);
@@ -1205,7 +1404,7 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
   S.join_cycle();
   mark("join");
   if (!finished_step7) launch_step7<T>(S.la, S.cur.U, S.cur.Ut, S.xo, S.xto, st);
-  launch_resid<T>(S.la, S.b, S.bt, S.xo, S.xto, S.z, S.zt, 0, st);
+  S.residual(S.xo, S.xto, S.z, S.zt, 0);
   const DevState<T> fin = *S.hst;
   S.pull();
   const double tr = std::sqrt(S.hst->rn2 / S.hst->bn2), trt = std::sqrt(S.hst->rtn2 / S.hst->btn2);
@@ -1331,6 +1530,7 @@ int rbicg_bilinear(rbicg_ctx *ctx, const rbicg_mat *A, const void *u, const void
     std::vector<cplx> G;
     if (A->dtype == RBICG_F64) gram<double>(X, Y, n, G, ctx, ctx->stream);
     else gram<zc>(X, Y, n, G, ctx, ctx->stream);
+    if (ctx->dist()) ctx->comm->allreduce_host((double *)G.data(), (int64_t)2 * G.size());
     // x~^*(w - Ax) = x~^*w - x~^*(Ax)
     const cplx v = G[0 * 3 + 0] + (G[1 * 3 + 2] - G[1 * 3 + 1]);
     if (A->dtype == RBICG_F64) {
@@ -1351,10 +1551,24 @@ int rbicg_dbg_spmv_pair(rbicg_ctx *ctx, const rbicg_mat *A, const void *p, const
   if (!ctx || !A || !p || !pt || !z || !zt) return RBICG_EINVAL;
   return run_guarded([&] {
     order_after_user(ctx);
-    const size_t vb = wbytes(A->dtype) * A->n;
-    void *dp = ws_alloc(vb), *dpt = ws_alloc(vb), *dz = ws_alloc(vb), *dzt = ws_alloc(vb);
+    const size_t w = wbytes(A->dtype);
+    const size_t vb = w * A->n;
+    const int64_t ng = ctx->dist() ? A->halo.nghost : 0;   // partitioned: ghost rows behind
+    void *dp = ws_alloc(vb + w * ng), *dpt = ws_alloc(vb + w * ng), *dz = ws_alloc(vb), *dzt = ws_alloc(vb);
     copy_in(dp, p, vb, on_device, ctx->stream);
     copy_in(dpt, pt, vb, on_device, ctx->stream);
+    if (ctx->dist()) {
+      void *sb = ws_alloc(w * std::max<int64_t>(A->halo.nsend, 1));
+      for (void *v : {dp, dpt}) {
+        if (A->dtype == RBICG_F64)
+          launch_pack_rows<double>((const double *)v, 1, A->halo.send_idx, A->halo.nsend, (double *)sb, ctx->stream);
+        else
+          launch_pack_rows<zc>((const zc *)v, 1, A->halo.send_idx, A->halo.nsend, (zc *)sb, ctx->stream);
+        ctx->comm->exchange(A->halo, sb, (char *)v + vb, 0, w, 1, ctx->stream);
+      }
+      RB_CUDA(cudaStreamSynchronize(ctx->stream));
+      ws_free(sb);
+    }
     if (A->dtype == RBICG_F64)
       launch_spmv_pair<double>(A->A, A->AH, (const double *)dp, (const double *)dpt, (double *)dz,
                                (double *)dzt, ctx->stream);
@@ -1422,7 +1636,7 @@ static void project_t(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, double t
 int rbicg_dbg_project(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, double trunc_tol,
                       const void *z, const void *zt, void *zeta, void *zetat, int32_t *k_out, void *U,
                       void *Ut, void *C, void *Ct, double *d, int on_device) {
-  if (!ctx || !A || !R || !z || !zt || !zeta || !zetat || !k_out) return RBICG_EINVAL;
+  if (!ctx || !A || !R || !z || !zt || !zeta || !zetat || !k_out || ctx->dist()) return RBICG_EINVAL;
   return run_guarded([&] {
     if (A->dtype == RBICG_F64)
       project_t<double>(ctx, A, R, trunc_tol, z, zt, zeta, zetat, k_out, U, Ut, C, Ct, d, on_device);
@@ -1545,7 +1759,7 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
 
 int rbicg_dbg_time_kernels(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbicg_opts *opts,
                            int iters, double *ms) {
-  if (!ctx || !A || !opts || !ms || iters <= 0) return RBICG_EINVAL;
+  if (!ctx || !A || !opts || !ms || iters <= 0 || ctx->dist()) return RBICG_EINVAL;
   return run_guarded([&] {
     if (A->dtype == RBICG_F64) time_t_<double>(ctx, A, R, opts, iters, ms);
     else time_t_<zc>(ctx, A, R, opts, iters, ms);

@@ -5,8 +5,10 @@
 #include <complex>
 #include <vector>
 #include <string>
+#include <memory>
 
 #include "common.cuh"
+#include "comm.h"
 
 namespace rbicg {
 
@@ -85,6 +87,8 @@ struct LoopArgs {
   IterRec<T> *hist;        // [max_itn + 1]
   T *zhist, *zthist;       // [max_itn + 1][k]
   T *part;                 // block partials [outputs][G]
+  int dist;                // row-partitioned: reduction tails write local sums to red
+  T *red;                  //   (allreduced, then a one-block leader kernel runs the scalar step)
 };
 
 struct ColDesc {           // one column of an n-row panel: p[row * stride]
@@ -109,14 +113,20 @@ struct rbicg_ctx {
   size_t work_bytes = 0;
   void *host_pinned = nullptr;
   size_t host_bytes = 0;
-  // pass timings from rbicg_dbg_time_kernels
+  // row partition: nranks > 1 -> comm (main loop) and
+  // comm_side (cycle-end worker) are set
+  int rank = 0, nranks = 1;
+  std::unique_ptr<rbicg::Comm> comm, comm_side;
+  bool dist() const { return nranks > 1; }
 };
 
 struct rbicg_mat {
   rbicg_ctx *ctx = nullptr;
-  int64_t n = 0, nnz = 0;
+  int64_t n = 0, nnz = 0;          // rows held here (the row block when partitioned)
+  int64_t n_global = 0, row_begin = 0;
   rbicg_dtype dtype = RBICG_F64;
-  rbicg::DevMat A, AH;
+  rbicg::DevMat A, AH;             // partitioned: columns local (own, then ghosts)
+  rbicg::HaloPlan halo;            // partitioned: ghost rows / send lists
 };
 
 struct rbicg_rec {
@@ -133,6 +143,11 @@ namespace rbicg {
 void build_matrix(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr_d,
                   const int32_t *col_d, const void *val_d, rbicg_dtype dt, rbicg_mat *M);
 void free_devmat(DevMat &m);
+// partitioned store: local rows of A and of A^* given as CSR (device arrays,
+// local column indices in [0, nloc + nghost))
+void build_matrix_local(rbicg_ctx *ctx, int64_t nloc, const int32_t *rpA, const int32_t *ciA,
+                        const void *vA, const int32_t *rpH, const int32_t *ciH, const void *vH,
+                        rbicg_dtype dt, rbicg_mat *M);
 
 // ---- kernels.cu (launch wrappers; all on ctx->stream)
 void prepare_kernels();        // one-time function attributes (not capturable)
@@ -155,6 +170,17 @@ template <typename F> inline void allow_max_dyn_smem(F *f) {
   RB_CUDA(cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)(227 * 1024 - fa.sharedSizeBytes)));
 }
+// row-partitioned form (kernels.cu)
+template <typename T> void launch_leader1(const LoopArgs<T> &a, cudaStream_t s);
+template <typename T> void launch_leader2(const LoopArgs<T> &a, cudaStream_t s);
+template <typename T> void launch_leader_resid(const LoopArgs<T> &a, int coef, cudaStream_t s);
+template <typename T> void launch_leader_init2(const LoopArgs<T> &a, cudaStream_t s);
+template <typename T>
+void launch_halo_pack_loop(const LoopArgs<T> &a, const int32_t *idx, int64_t nsend, T *buf, cudaStream_t s);
+template <typename T>
+void launch_halo_unpack_loop(const LoopArgs<T> &a, const T *buf, int64_t nghost, cudaStream_t s);
+template <typename T>
+void launch_pack_rows(const T *X, int k, const int32_t *idx, int64_t cnt, T *out, cudaStream_t s);
 // ---- persist.cu (one cooperative launch per cycle)
 void prepare_loop_kernels();
 template <typename T> int loop_grid(const LoopArgs<T> &a, int *p2_staged);   // 0: not possible

@@ -13,6 +13,8 @@
 namespace rbicg {
 
 std::atomic<int64_t> g_launches{0};
+template <typename T> __device__ void resid_leader(DevState<T> *st, const T *s_fin, int k);
+template <typename T> __device__ void init2_leader(const LoopArgs<T> &a, DevState<T> *st, const T *s_fin);
 static const bool g_pdl = getenv("RBICG_PDL") ? atoi(getenv("RBICG_PDL")) != 0 : true;
 
 
@@ -71,6 +73,10 @@ __global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
   if (!last_block(&st->cnt[0], &s_last)) return;
   final_reduce(a.part, 3 * a.k + 1, gridDim.x, s_fin);
   if (tid == 0) st->cnt[0] = 0;
+  if (a.dist) {   // local sums -> allreduce -> k_leader1
+    for (int o = tid; o < 3 * a.k + 1; o += BS) a.red[o] = s_fin[o];
+    return;
+  }
   p1_leader<T>(a, st, sn, sn.iter, s_fin, &s_alpha, &s_ok);
 }
 
@@ -125,6 +131,10 @@ __global__ void __launch_bounds__(BS, 4) k_pass1s(LoopArgs<T> a) {
   if (!last_block(&st->cnt[0], &s_last)) return;
   final_reduce(a.part, 3 * a.k + 1, gridDim.x, s_fin);
   if (tid == 0) st->cnt[0] = 0;
+  if (a.dist) {   // local sums -> allreduce -> k_leader1
+    for (int o = tid; o < 3 * a.k + 1; o += BS) a.red[o] = s_fin[o];
+    return;
+  }
   p1_leader<T>(a, st, sn, sn.iter, s_fin, &s_alpha, &s_ok);
 }
 
@@ -160,8 +170,91 @@ __global__ void __launch_bounds__(BS, 3) k_pass2(LoopArgs<T> a, int staged) {
   if (!last_block(&st->cnt[1], &s_last)) return;
   final_reduce(a.part, 3, gridDim.x, s_fin);
   if (tid == 0) st->cnt[1] = 0;
+  if (a.dist) {   // local sums -> allreduce -> k_leader2
+    for (int o = tid; o < 3; o += BS) a.red[o] = s_fin[o];
+    return;
+  }
   p2_leader<T>(a, st, sn, sn.iter, s_fin);
 }
+
+// ============================================================== row-partitioned form
+// The scalar steps after the allreduce of the block sums (one block each);
+// every rank runs them on identical global sums, so the scalars stay
+// replicated.
+template <typename T>
+__global__ void __launch_bounds__(BS) k_leader1(LoopArgs<T> a) {
+  __shared__ Snap<T> sn;
+  __shared__ T s_fin[3 * KMAX + 1];
+  __shared__ T s_alpha;
+  __shared__ int s_ok;
+  snap_load(a.st, a.k, sn);
+  if (sn.done) return;
+  for (int o = threadIdx.x; o < 3 * a.k + 1; o += BS) s_fin[o] = ldcg(a.red + o);
+  __syncthreads();
+  p1_leader<T>(a, a.st, sn, sn.iter, s_fin, &s_alpha, &s_ok);
+}
+template <typename T>
+__global__ void __launch_bounds__(BS) k_leader2(LoopArgs<T> a) {
+  __shared__ Snap<T> sn;
+  __shared__ T s_fin[3];
+  snap_load(a.st, a.k, sn);
+  if (sn.done) return;
+  if (threadIdx.x < 3) s_fin[threadIdx.x] = ldcg(a.red + threadIdx.x);
+  __syncthreads();
+  p2_leader<T>(a, a.st, sn, sn.iter, s_fin);
+}
+template <typename T>
+__global__ void __launch_bounds__(BS) k_leader_resid(LoopArgs<T> a, int coef) {
+  __shared__ T s_fin[4 + 2 * KMAX];
+  const int k = coef ? a.k : 0;
+  for (int o = threadIdx.x; o < 4 + 2 * k; o += BS) s_fin[o] = ldcg(a.red + o);
+  __syncthreads();
+  resid_leader<T>(a.st, s_fin, k);
+}
+template <typename T>
+__global__ void __launch_bounds__(BS) k_leader_init2(LoopArgs<T> a) {
+  __shared__ T s_fin[3];
+  if (threadIdx.x < 3) s_fin[threadIdx.x] = ldcg(a.red + threadIdx.x);
+  __syncthreads();
+  init2_leader<T>(a, a.st, s_fin);
+}
+
+// Halo of the gathered vectors of iteration `it` (state): r_it, p_it, r~_it,
+// p~_it (own rows send_idx -> sendbuf; received ghosts -> the ghost rows
+// [n, n + nghost) of the same columns).  Fixed buffer addresses, so the
+// exchange between them can be captured in the cycle's graph.
+template <typename T>
+__global__ void k_halo_pack_loop(LoopArgs<T> a, const int32_t *idx, int64_t nsend, T *sendbuf) {
+  const int it = __ldcg(&a.st->iter);
+  const T *v[4] = {a.rring + (int64_t)(it % a.ring) * a.ldr, pcol(a, it),
+                   a.rtring + (int64_t)(it % a.ring) * a.ldr, ptcol(a, it)};
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nsend;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = idx[j];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sendbuf[q * nsend + j] = v[q][r];
+  }
+}
+template <typename T>
+__global__ void k_halo_unpack_loop(LoopArgs<T> a, const T *recvbuf, int64_t nghost) {
+  const int it = __ldcg(&a.st->iter);
+  T *v[4] = {a.rring + (int64_t)(it % a.ring) * a.ldr, pcol(a, it),
+             a.rtring + (int64_t)(it % a.ring) * a.ldr, ptcol(a, it)};
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nghost;
+       g += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q][a.n + g] = recvbuf[q * nghost + g];
+  }
+}
+// rows idx of an n x k row-major block -> out (k values per row)
+template <typename T>
+__global__ void k_pack_rows(const T *X, int k, const int32_t *idx, int64_t cnt, T *out) {
+  const int64_t tot = cnt * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = X[(int64_t)idx[e / k] * k + e % k];
+}
+
 
 // ============================================================== init / finish
 // r = b - A x, r~ = b~ - A^* x~; partial ||b||², ||b~||², ||r||², ||r~||² and,
@@ -237,8 +330,17 @@ __global__ void __launch_bounds__(BS, 4) k_resid(LoopArgs<T> a, const T *b, cons
   }
   if (!last_block(&st->cnt[2], &s_last)) return;
   final_reduce(a.part, 4 + 2 * k, G, s_fin);
-  if (tid == 0) {
-    st->cnt[2] = 0;
+  if (tid == 0) st->cnt[2] = 0;
+  if (a.dist) {   // local sums -> allreduce -> k_leader_resid
+    for (int o = tid; o < 4 + 2 * k; o += BS) a.red[o] = s_fin[o];
+    return;
+  }
+  resid_leader<T>(st, s_fin, k);
+}
+
+template <typename T>
+__device__ void resid_leader(DevState<T> *st, const T *s_fin, int k) {
+  if (threadIdx.x == 0) {
     st->bn2 = re(s_fin[0]);
     st->btn2 = re(s_fin[1]);
     st->rn2 = re(s_fin[2]);
@@ -307,8 +409,17 @@ __global__ void __launch_bounds__(BS, 4) k_init2(LoopArgs<T> a, const T *U, cons
   }
   if (!last_block(&st->cnt[3], &s_last)) return;
   final_reduce(a.part, 3, G, s_fin);
-  if (tid == 0) {
-    st->cnt[3] = 0;
+  if (tid == 0) st->cnt[3] = 0;
+  if (a.dist) {
+    for (int o = tid; o < 3; o += BS) a.red[o] = s_fin[o];
+    return;
+  }
+  init2_leader<T>(a, st, s_fin);
+}
+
+template <typename T>
+__device__ void init2_leader(const LoopArgs<T> &a, DevState<T> *st, const T *s_fin) {
+  if (threadIdx.x == 0) {
     const T rho = s_fin[0];
     const double rn = sqrt(re(s_fin[1])), rtn = sqrt(re(s_fin[2]));
     st->rho = rho;
@@ -482,6 +593,43 @@ void launch_step7(const LoopArgs<T> &a, const T *U, const T *Ut, T *xo, T *xto, 
   count_launch();
 }
 
+static int g_small(int64_t m) { return (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 1184)); }
+template <typename T> void launch_leader1(const LoopArgs<T> &a, cudaStream_t s) {
+  k_leader1<T><<<1, BS, 0, s>>>(a);
+  count_launch();
+}
+template <typename T> void launch_leader2(const LoopArgs<T> &a, cudaStream_t s) {
+  k_leader2<T><<<1, BS, 0, s>>>(a);
+  count_launch();
+}
+template <typename T> void launch_leader_resid(const LoopArgs<T> &a, int coef, cudaStream_t s) {
+  k_leader_resid<T><<<1, BS, 0, s>>>(a, coef);
+  count_launch();
+}
+template <typename T> void launch_leader_init2(const LoopArgs<T> &a, cudaStream_t s) {
+  k_leader_init2<T><<<1, BS, 0, s>>>(a);
+  count_launch();
+}
+template <typename T>
+void launch_halo_pack_loop(const LoopArgs<T> &a, const int32_t *idx, int64_t nsend, T *buf,
+                           cudaStream_t s) {
+  if (nsend <= 0) return;
+  k_halo_pack_loop<T><<<g_small(nsend), 256, 0, s>>>(a, idx, nsend, buf);
+  count_launch();
+}
+template <typename T>
+void launch_halo_unpack_loop(const LoopArgs<T> &a, const T *buf, int64_t nghost, cudaStream_t s) {
+  if (nghost <= 0) return;
+  k_halo_unpack_loop<T><<<g_small(nghost), 256, 0, s>>>(a, buf, nghost);
+  count_launch();
+}
+template <typename T>
+void launch_pack_rows(const T *X, int k, const int32_t *idx, int64_t cnt, T *out, cudaStream_t s) {
+  if (cnt <= 0 || k <= 0) return;
+  k_pack_rows<T><<<g_small(cnt * k), 256, 0, s>>>(X, k, idx, cnt, out);
+  count_launch();
+}
+
 template <typename T>
 void launch_spmv_pair(const DevMat &A, const DevMat &AH, const T *p, const T *pt, T *z, T *zt,
                       cudaStream_t s) {
@@ -520,7 +668,16 @@ void prepare_kernels() {
   template void launch_step7<T>(const LoopArgs<T> &, const T *, const T *, T *, T *,         \
                                 cudaStream_t);                                               \
   template void launch_spmv_pair<T>(const DevMat &, const DevMat &, const T *, const T *, T *, \
-                                    T *, cudaStream_t);
+                                    T *, cudaStream_t);                                       \
+  template void launch_leader1<T>(const LoopArgs<T> &, cudaStream_t);                        \
+  template void launch_leader2<T>(const LoopArgs<T> &, cudaStream_t);                        \
+  template void launch_leader_resid<T>(const LoopArgs<T> &, int, cudaStream_t);              \
+  template void launch_leader_init2<T>(const LoopArgs<T> &, cudaStream_t);                   \
+  template void launch_halo_pack_loop<T>(const LoopArgs<T> &, const int32_t *, int64_t, T *, \
+                                         cudaStream_t);                                       \
+  template void launch_halo_unpack_loop<T>(const LoopArgs<T> &, const T *, int64_t,          \
+                                           cudaStream_t);                                     \
+  template void launch_pack_rows<T>(const T *, int, const int32_t *, int64_t, T *, cudaStream_t);
 RB_INST(double)
 RB_INST(zc)
 

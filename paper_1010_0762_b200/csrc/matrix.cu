@@ -168,6 +168,21 @@ void build_matrix(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr_
     build_t<zc>(ctx, n, nnz, rowptr_d, col_d, (const zc *)val_d, M);
 }
 
+void build_matrix_local(rbicg_ctx *ctx, int64_t nloc, const int32_t *rpA, const int32_t *ciA,
+                        const void *vA, const int32_t *rpH, const int32_t *ciH, const void *vH,
+                        rbicg_dtype dt, rbicg_mat *M) {
+  M->n = nloc;
+  M->dtype = dt;
+  if (dt == RBICG_F64) {
+    csr_to_sell<double>(ctx, nloc, rpA, ciA, (const double *)vA, M->A);
+    csr_to_sell<double>(ctx, nloc, rpH, ciH, (const double *)vH, M->AH);
+  } else {
+    csr_to_sell<zc>(ctx, nloc, rpA, ciA, (const zc *)vA, M->A);
+    csr_to_sell<zc>(ctx, nloc, rpH, ciH, (const zc *)vH, M->AH);
+  }
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 void free_devmat(DevMat &m) {
   // pooled device memory (reused by the next system's store); no device sync
   ws_free(m.sptr);
