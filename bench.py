@@ -124,16 +124,32 @@ def run_gpu(args, rank, world):
     cfg = CONFIGS[args.config]
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
-    ctx = api.Context(dev)
+    # N > 1: the row-partitioned path -- every rank holds a row
+    # block, halo exchange + scalar allreduces over NCCL; --replicas runs N
+    # independent copies instead.
+    part = world > 1 and not args.replicas
+    r0, r1 = 0, cfg.n
+    if part:
+        import torch.distributed as tdist
+        obj = [api.nccl_unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(obj, src=0)
+        ctx = api.Context(dev, dist=dict(rank=rank, nranks=world, mode=0, key=obj[0]))
+        r0, r1 = (cfg.n * rank) // world, (cfg.n * (rank + 1)) // world
+    else:
+        ctx = api.Context(dev)
     steps = args.warmup + args.steps
     systems = build_systems(cfg, list(range(steps)))
-    # inputs resident in HBM before the timed region
+    # inputs resident in HBM before the timed region (the matrix is passed
+    # whole; vectors are this rank's rows)
     dsys = []
     for it in systems:
-        dsys.append({k: torch.from_numpy(np.ascontiguousarray(it[k])).to(f"cuda:{dev}")
-                     for k in ("indptr", "indices", "data", "b", "bt")})
+        d = {k: torch.from_numpy(np.ascontiguousarray(it[k])).to(f"cuda:{dev}")
+             for k in ("indptr", "indices", "data")}
+        for k in ("b", "bt"):
+            d[k] = torch.from_numpy(np.ascontiguousarray(it[k][r0:r1])).to(f"cuda:{dev}")
+        dsys.append(d)
     torch.cuda.synchronize()
-    R = ctx.recycle(cfg.n, cfg.k, cfg.complex)
+    R = ctx.recycle(r1 - r0, cfg.k, cfg.complex)
     stream = torch.cuda.current_stream()
     res_all, times = [], []
 
@@ -182,14 +198,20 @@ def run_gpu(args, rank, world):
         torch.distributed.all_reduce(tmax[:1], op=torch.distributed.ReduceOp.MAX)
         tsum = t.clone()
         torch.distributed.all_reduce(tsum[1:], op=torch.distributed.ReduceOp.SUM)
-        total_ms, iters = float(tmax[0]), int(tsum[1])
+        # partitioned: every rank did the same (replicated) iterations
+        total_ms = float(tmax[0])
+        iters = int(tsum[1]) // world if part else int(tsum[1])
 
     # ---- roofline of the dominant kernel: per-kernel CUDA events on the
     # library stream, resident state of the last system, its recycle space
     last = dsys[-1]
-    A = ctx.matrix(last["indptr"], last["indices"], last["data"])
-    kt = ctx.time_kernels(A, R, k=cfg.k, s=cfg.s, iters=args.kernel_iters,
-                          trunc_tol=cfg.trunc_tol)
+    kctx, kR = ctx, R
+    if part:   # the partitioned context has no timing hook: the kernels on one GPU
+        kctx = api.Context(dev)
+        kR = kctx.recycle(cfg.n, cfg.k, cfg.complex)
+    A = kctx.matrix(last["indptr"], last["indices"], last["data"])
+    kt = kctx.time_kernels(A, kR, k=cfg.k, s=cfg.s, iters=args.kernel_iters,
+                           trunc_tol=cfg.trunc_tol)
     A.free()
     w = 16 if cfg.complex else 8
     p1, p2 = alg_bytes(cfg.n, cfg.nnz, kt["k"], w, kt["lazy_x"])
@@ -207,7 +229,7 @@ def run_gpu(args, rank, world):
     # ---- e2e through the public API with HOST buffers (H2D/D2H in the call)
     e2e = None
     if not args.no_e2e:
-        R2 = ctx.recycle(cfg.n, cfg.k, cfg.complex)
+        R2 = ctx.recycle(r1 - r0, cfg.k, cfg.complex)
 
         def pinned(a):   # NumPy view of page-locked host memory holding a copy of a
             t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
@@ -216,9 +238,11 @@ def run_gpu(args, rank, world):
             return out
         h_sys = []
         for it in systems[args.warmup:steps]:
-            hs = {k: pinned(np.ascontiguousarray(it[k])) for k in ("indptr", "indices", "data", "b", "bt")}
-            hs["x"] = pinned(np.zeros_like(it["b"]))
-            hs["xt"] = pinned(np.zeros_like(it["bt"]))
+            hs = {k: pinned(np.ascontiguousarray(it[k])) for k in ("indptr", "indices", "data")}
+            for k in ("b", "bt"):
+                hs[k] = pinned(np.ascontiguousarray(it[k][r0:r1]))
+            hs["x"] = pinned(np.zeros_like(hs["b"]))
+            hs["xt"] = pinned(np.zeros_like(hs["bt"]))
             h_sys.append(hs)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -239,6 +263,12 @@ def run_gpu(args, rank, world):
             per.append(round(1e3 * (time.perf_counter() - ts), 2))
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
+        if world > 1:   # whole job: slowest rank; iterations replicated (partition) or summed
+            tt = torch.tensor([el, ei], dtype=torch.float64, device=f"cuda:{dev}")
+            tm = tt.clone()
+            torch.distributed.all_reduce(tm[:1], op=torch.distributed.ReduceOp.MAX)
+            torch.distributed.all_reduce(tt[1:], op=torch.distributed.ReduceOp.SUM)
+            el, ei = float(tm[0]), float(tt[1]) / (world if part else 1)
         e2e = {"value": ei / el, "unit": "iterations/s",
                "h2d_bytes_per_step": h2d // max(1, len(h_sys)),
                "d2h_bytes_per_step": d2h // max(1, len(h_sys)),
@@ -251,7 +281,7 @@ def run_gpu(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / max(1, args.steps),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if part else "weak",
         "vs_baseline": None,
         "dtype": "c128" if cfg.complex else "f64",
         "data": "synthetic (seeded conv-diff sequence, SURVEY §8(d))",
@@ -268,7 +298,8 @@ def run_gpu(args, rank, world):
                    "matrix_build_ms": sum(build_ms),
                    "solve_total_ms": sum(r["t_total_ms"] for r in res_all),
                    "l2": "per-iteration traffic > 126 MB L2 (no flush needed)",
-                   "parallelism": "replicas" if world > 1 else "single GPU"},
+                   "parallelism": (f"row partition x{world} (NCCL halo + allreduce)" if part
+                                   else ("replicas" if world > 1 else "single GPU"))},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -362,6 +393,8 @@ def main():
     ap.add_argument("--cpu-sample-iters", type=int, default=80)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent copies instead of the row partition")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

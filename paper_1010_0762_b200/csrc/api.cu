@@ -17,6 +17,7 @@
 #include <string>
 #include <mutex>
 #include <thread>
+#include <tuple>
 
 #include "internal.h"
 #include "dist_plan.h"
@@ -355,7 +356,9 @@ struct Solver {
       if (fr > need + ((size_t)2 << 30)) {
         ring *= 2;
         async_cycle = true;
-        RB_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, ctx->prio_lo));
+        // RBICG_SIDE_PRIO=hi runs the cycle-end kernels at the loop's priority
+        const bool side_hi = getenv("RBICG_SIDE_PRIO") && getenv("RBICG_SIDE_PRIO")[0] == 'h';
+        RB_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, side_hi ? ctx->prio_hi : ctx->prio_lo));
       }
     }
     // row partition: gathered vectors carry the ghost rows [n, nx) behind the own rows
@@ -1077,7 +1080,23 @@ static void build_partitioned(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int3
     RB_CUDA(cudaMemcpyAsync(vv.data(), vv_d, w * nnz, cudaMemcpyDeviceToHost, ctx->stream));
   }
   RB_CUDA(cudaStreamSynchronize(ctx->stream));
-  const Plan pl = make_plan(n, rp.data(), ci.data(), ctx->nranks, ctx->rank);
+  // the plan depends only on the pattern, which a sequence keeps:
+  // reuse the last one when the pattern is unchanged
+  static std::mutex mu;
+  static std::map<const rbicg_ctx *, std::tuple<std::vector<int32_t>, std::vector<int32_t>, Plan>> cache;
+  Plan pl;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(ctx);
+    if (it != cache.end() && std::get<2>(it->second).P == ctx->nranks &&
+        std::get<2>(it->second).q == ctx->rank && std::get<0>(it->second) == rp &&
+        std::get<1>(it->second) == ci) {
+      pl = std::get<2>(it->second);
+    } else {
+      pl = make_plan(n, rp.data(), ci.data(), ctx->nranks, ctx->rank);
+      cache[ctx] = std::make_tuple(rp, ci, pl);
+    }
+  }
   std::vector<int32_t> rpA, ciA, rpH, ciH;
   std::vector<unsigned char> vA, vH;
   local_csr(pl, n, rp.data(), ci.data(), vv.data(), w, dt == RBICG_C128, false, rpA, ciA, vA);
@@ -1134,6 +1153,7 @@ int rbicg_init(rbicg_ctx **out, int device, void *stream, const rbicg_dist *dist
     int lo = 0, hi = 0;
     RB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     c->prio_lo = lo;
+    c->prio_hi = hi;
     // the hot loop runs at the highest priority; cycle-end work fills gaps
     RB_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));
     RB_CUDA(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));

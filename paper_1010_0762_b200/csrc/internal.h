@@ -105,7 +105,7 @@ struct rbicg_ctx {
   cudaStream_t stream = nullptr;       // library stream (non-blocking)
   cudaStream_t user_stream = nullptr;  // caller's stream (may be legacy NULL)
   cudaEvent_t order_ev = nullptr;
-  int prio_lo = 0;
+  int prio_lo = 0, prio_hi = 0;
   int nsm = 148;
   int grid_stream = 296;  // persistent grid of the streaming kernels
   // reusable device workspace
