@@ -154,6 +154,7 @@ def run_gpu(args, rank, world):
     res_all, times = [], []
 
     build_ms = []
+    host_ms = []   # (solve_dual call, free) wall ms per timed step
 
     def one(i, timed):
         d = dsys[i]
@@ -165,12 +166,16 @@ def run_gpu(args, rank, world):
         eb.synchronize()
         if timed:
             build_ms.append(e0.elapsed_time(eb))
+        t0 = time.perf_counter()
         x, xt, res, _ = ctx.solve_dual(A, d["b"], d["bt"], R=R, k=cfg.k, s=cfg.s,
                                        tol=cfg.tol, max_itn=cfg.max_itn,
                                        trunc_tol=cfg.trunc_tol)
+        t1 = time.perf_counter()
         A.free()
         e1.record(stream)
         e1.synchronize()
+        if timed:
+            host_ms.append((round(1e3 * (t1 - t0), 2), round(1e3 * (time.perf_counter() - t1), 2)))
         return res, e0.elapsed_time(e1)
 
     for i in range(args.warmup):
@@ -296,6 +301,9 @@ def run_gpu(args, rank, world):
                    "cycle_end_ms": sum(r["t_cycle_dev_ms"] for r in res_all),
                    "loop_ms": sum(r["t_loop_ms"] for r in res_all),
                    "matrix_build_ms": sum(build_ms),
+                   "solve_call_ms": [h[0] for h in host_ms],
+                   "free_ms": [h[1] for h in host_ms],
+                   "step_ms": [round(t, 2) for t in times],
                    "solve_total_ms": sum(r["t_total_ms"] for r in res_all),
                    "l2": "per-iteration traffic > 126 MB L2 (no flush needed)",
                    "parallelism": (f"row partition x{world} (NCCL halo + allreduce)" if part

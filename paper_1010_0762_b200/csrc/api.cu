@@ -35,8 +35,14 @@ void *ws_alloc(size_t bytes) {
   bytes = (bytes + 255) / 256 * 256;
   {
     std::lock_guard<std::mutex> lk(g_pool_mu);
-    auto it = g_pool.lower_bound(bytes);
-    if (it != g_pool.end() && it->first <= bytes * 2) {
+    // an exact size first (the per-system buffers repeat), then at most
+    // 1.25x, so small requests do not take the blocks larger ones reuse
+    auto it = g_pool.find(bytes);
+    if (it == g_pool.end()) {
+      it = g_pool.lower_bound(bytes);
+      if (it != g_pool.end() && it->first > bytes + bytes / 4) it = g_pool.end();
+    }
+    if (it != g_pool.end()) {
       void *p = it->second;
       g_pool.erase(it);
       return p;
@@ -72,6 +78,30 @@ void ws_free(void *p) {
   auto it = g_sizes.find(p);
   if (it == g_sizes.end()) return;
   g_pool.emplace(it->second, p);
+}
+
+// page-locked host staging (the device-state mirror), cached: cudaMallocHost
+// per solve measured up to 100+ ms on the bench box
+static std::mutex g_pin_mu;
+static std::multimap<size_t, void *> g_pin_pool;
+static void *pinned_alloc(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_pool.find(bytes);
+    if (it != g_pin_pool.end()) {
+      void *p = it->second;
+      g_pin_pool.erase(it);
+      return p;
+    }
+  }
+  void *p = nullptr;
+  RB_CUDA(cudaMallocHost(&p, bytes));
+  return p;
+}
+static void pinned_free(void *p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_pool.emplace(bytes, p);
 }
 
 static void ws_release_all() {
@@ -299,7 +329,7 @@ struct Solver {
   std::vector<void *> owned;
   T *rring = nullptr, *rtring = nullptr, *p[2] = {}, *pt[2] = {}, *z = nullptr, *zt = nullptr;
   T *x = nullptr, *xt = nullptr, *b = nullptr, *bt = nullptr, *xo = nullptr, *xto = nullptr;
-  T *pseg = nullptr, *ptseg = nullptr;
+  T *psegs[2] = {}, *ptsegs[2] = {};
   T *pring = nullptr, *ptring = nullptr;
   int pring_len = 0;
   // p_0 = p~_0 = 0 (Algorithm 2 starts from p_0 = 0, β_0 = 0)
@@ -333,11 +363,19 @@ struct Solver {
     return (T *)q;
   }
   ~Solver() {
+    static const bool tm = getenv("RBICG_TIMING") != nullptr;
+    const double t0 = tm ? now_ms() : 0;
     if (worker.joinable()) worker.join();
+    const double t1 = tm ? now_ms() : 0;
     if (side) cudaStreamDestroy(side);
+    const double t2 = tm ? now_ms() : 0;
     if (gexec) cudaGraphExecDestroy(gexec);
+    const double t3 = tm ? now_ms() : 0;
     for (void *q : owned) ws_free(q);
-    if (hst) cudaFreeHost(hst);
+    pinned_free(hst, sizeof(DevState<T>));
+    if (tm)
+      fprintf(stderr, "rbicg ~Solver join %.2f stream %.2f graph %.2f free %.2f ms\n", t1 - t0, t2 - t1,
+              t3 - t2, now_ms() - t3);
   }
 
   void setup(rbicg_ctx *c, const rbicg_mat *m, const rbicg_opts &opts, int k_basis) {
@@ -402,8 +440,10 @@ struct Solver {
     xo = alloc(nx);
     xto = alloc(nx);
     lazy_x = getenv("RBICG_EAGER_X") == nullptr;
-    pseg = alloc(n);
-    ptseg = alloc(n);
+    for (int q = 0; q < 2; ++q) {   // by segment parity: a deferred flush may still read it
+      psegs[q] = alloc(n);
+      ptsegs[q] = alloc(n);
+    }
     for (Basis *B : {&cur, &cand[0], &cand[1], &tmp}) {
       B->U = alloc((size_t)nx * kmax);
       B->Ut = alloc((size_t)nx * kmax);
@@ -413,7 +453,7 @@ struct Solver {
     }
     st = (DevState<T> *)ws_alloc(sizeof(DevState<T>));
     owned.push_back(st);
-    RB_CUDA(cudaMallocHost(&hst, sizeof(DevState<T>)));
+    hst = (DevState<T> *)pinned_alloc(sizeof(DevState<T>));
     const int H = std::max(o.max_itn, 0) + 2;
     hist = (IterRec<T> *)ws_alloc(sizeof(IterRec<T>) * H);
     owned.push_back(hist);
@@ -465,8 +505,11 @@ struct Solver {
       la.stage_c = (la.staged && cur.k > 0 && mat_stages + cbuf <= cap) ? 1 : 0;
     }
     la.lazy_x = lazy_x ? 1 : 0;
-    la.pseg = pseg;
-    la.ptseg = ptseg;
+    la.pseg[0] = psegs[0];
+    la.pseg[1] = psegs[1];
+    la.ptseg[0] = ptsegs[0];
+    la.ptseg[1] = ptsegs[1];
+    la.cyc = o.s;
     la.nsm = ctx->nsm;
     la.rring = rring;
     la.rtring = rtring;
@@ -659,6 +702,24 @@ struct Solver {
   // x_b = x_a + Σ_i α_i p_i is rebuilt from the Lanczos ring and p_a:
   // x_b = x_a + c_p p_a + Σ_{l=a}^{b-1} c_l r_l with c_{b} = 0,
   // c_l = α_{l+1} + β_{l+1} c_{l+1}, c_p = β_a c_a; the dual uses conj(c).
+  // rec[i] = record a + i, i = 0..b-a.  Returns [c_a..c_{b-1}, c_p, 1].
+  static std::vector<cplx> flush_coeffs(int a0, int bidx, const IterRec<T> *rec) {
+    const int m = bidx - a0;
+    std::vector<cplx> c(m + 2, 0.0);
+    cplx nxt = 0.0;
+    for (int l = bidx - 1; l >= a0; --l) {
+      const cplx al = toc(rec[l + 1 - a0].alpha);
+      const cplx be = (l + 1 < bidx) ? toc(rec[l + 1 - a0].beta) : cplx(0.0);
+      nxt = al + be * nxt;
+      c[l - a0] = nxt;
+    }
+    const cplx beta_a = a0 == 0 ? cplx(0.0) : toc(rec[0].beta);
+    c[m] = beta_a * c[0];
+    c[m + 1] = 1.0;
+    return c;
+  }
+  T *pseg_of(int a0) const { return psegs[(a0 / o.s) & 1]; }
+  T *ptseg_of(int a0) const { return ptsegs[(a0 / o.s) & 1]; }
   void flush_x(int bidx) {
     const int a0 = hst->seg_start;
     if (!lazy_x || bidx <= a0) {
@@ -670,22 +731,7 @@ struct Solver {
     RB_CUDA(cudaMemcpyAsync(rec.data(), hist + a0, sizeof(IterRec<T>) * (m + 1),
                             cudaMemcpyDeviceToHost, ctx->stream));
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::vector<cplx> c(m + 1, 0.0);   // c[l - a0], l = a0..b-1 ; c[m] = c_p
-    cplx nxt = 0.0;
-    for (int l = bidx - 1; l >= a0; --l) {
-      const cplx al = toc(rec[l + 1 - a0].alpha);
-      const cplx be = (l + 1 < bidx) ? toc(rec[l + 1 - a0].beta) : cplx(0.0);
-      nxt = al + be * nxt;
-      c[l - a0] = nxt;
-    }
-    const cplx beta_a = a0 == 0 ? cplx(0.0) : toc(rec[0].beta);
-    const std::vector<cplx> cr = [&] {
-      std::vector<cplx> v(m + 2);
-      for (int l = 0; l < m; ++l) v[l] = c[l];
-      v[m] = beta_a * c[0];
-      v[m + 1] = 1.0;
-      return v;
-    }();
+    const std::vector<cplx> cr = flush_coeffs(a0, bidx, rec.data());
     std::vector<cplx> cd(cr);
     for (auto &v : cd) v = std::conj(v);
     std::vector<ColDesc> X, Xt;
@@ -693,8 +739,8 @@ struct Solver {
       X.push_back(rcol(l));
       Xt.push_back(rtcol(l));
     }
-    X.push_back(ColDesc{pseg, 1});
-    Xt.push_back(ColDesc{ptseg, 1});
+    X.push_back(ColDesc{pseg_of(a0), 1});
+    Xt.push_back(ColDesc{ptseg_of(a0), 1});
     X.push_back(ColDesc{x, 1});
     Xt.push_back(ColDesc{xt, 1});
     gemm_panels<T>(X, cr, 1, n, x, ctx, ctx->stream, /*sync=*/false);
@@ -757,7 +803,54 @@ struct Solver {
   }
 
   // ---------------------------------------------------------------- cycle end
-  void cycle_end(int j) {
+  // [U_j | x] = [Φ_j | p_a | x] [[W_j, c_Φ], [0, c_p], [0, 1]] and the dual:
+  // one pass over the ring columns for the recycle-space GEMM and the lazy-x
+  // flush (c_Φ = 0 on the U_{j-1} columns, the flush coefficients on V_j).
+  void fused_flush_gemm(const std::vector<ColDesc> &Phi, const std::vector<ColDesc> &Phit,
+                        const std::vector<cplx> &W, const std::vector<cplx> &Wt, int ksel, int kx,
+                        int fa, int fb, int lo, const std::vector<IterRec<T>> &rec, cudaStream_t cs) {
+    const int m = fb - fa;
+    const std::vector<cplx> cr = flush_coeffs(fa, fb, rec.data() + (fa - lo));
+    std::vector<ColDesc> X, Xt;
+    if (ksel > 0) {
+      RB_CHECK((int)Phi.size() == kx + m, RBICG_ESTATE);
+      X = Phi;
+      Xt = Phit;
+    } else {
+      for (int l = fa; l < fb; ++l) {
+        X.push_back(rcol(l));
+        Xt.push_back(rtcol(l));
+      }
+      kx = 0;
+    }
+    X.push_back(ColDesc{pseg_of(fa), 1});
+    Xt.push_back(ColDesc{ptseg_of(fa), 1});
+    X.push_back(ColDesc{x, 1});
+    Xt.push_back(ColDesc{xt, 1});
+    const int mX = (int)X.size(), p = ksel + 1;
+    std::vector<cplx> M((size_t)mX * p, 0.0), Mt((size_t)mX * p, 0.0);
+    for (int a = 0; a < kx + m; ++a) {
+      for (int c = 0; c < ksel; ++c) {
+        M[(size_t)a * p + c] = W[(size_t)a * ksel + c];
+        Mt[(size_t)a * p + c] = Wt[(size_t)a * ksel + c];
+      }
+      if (a >= kx) {
+        M[(size_t)a * p + ksel] = cr[a - kx];
+        Mt[(size_t)a * p + ksel] = std::conj(cr[a - kx]);
+      }
+    }
+    M[(size_t)(kx + m) * p + ksel] = cr[m];
+    Mt[(size_t)(kx + m) * p + ksel] = std::conj(cr[m]);
+    M[(size_t)(kx + m + 1) * p + ksel] = 1.0;
+    Mt[(size_t)(kx + m + 1) * p + ksel] = 1.0;
+    gemm_panels<T>(X, M, ksel, n, tmp.U, ctx, cs, true, x);
+    gemm_panels<T>(Xt, Mt, ksel, n, tmp.Ut, ctx, cs, true, xt);
+  }
+
+  // fa < fb: also the deferred lazy-x flush of segment (fa, fb] = this
+  // cycle's iterations, fused into the U_j GEMM (both read the same ring
+  // columns r_fa .. r_{fb-1})
+  void cycle_end(int j, int fa = 0, int fb = 0) {
     const cudaStream_t cs = async_cycle ? side : ctx->stream;
     const double t0 = now_ms();
     const int s = o.s;
@@ -951,7 +1044,10 @@ struct Solver {
     if (!dist || cms->rank == 0) {
       std::vector<cplx> alpha, beta, VL, VR;
       std::vector<int> pf;
-      RB_CHECK(lapack_ggev(real, mp, P, Q, alpha, beta, VL, VR, pf) == 0, RBICG_ELAPACK);
+      if (!haveC && !havePrev)   // Q = I: eigenvectors of T_j
+        RB_CHECK(lapack_geev(real, mp, P, alpha, beta, VL, VR) == 0, RBICG_ELAPACK);
+      else
+        RB_CHECK(lapack_ggev(real, mp, P, Q, alpha, beta, VL, VR, pf) == 0, RBICG_ELAPACK);
       double qn = 0;
       for (auto &v : Q) qn += std::norm(v);
       qn = std::sqrt(qn);
@@ -980,8 +1076,13 @@ struct Solver {
       // U_j = Φ_j W_j, Ũ_j = Φ~_j W~_j; C_j = A U_j, C~_j = A^* Ũ_j
       {
         Phase ph("cycle.gemm_UW", cs);
-        gemm_panels<T>(PhiCols, Wrow, ksel, n, tmp.U, ctx, cs);
-        gemm_panels<T>(PhitCols, Wtrow, ksel, n, tmp.Ut, ctx, cs);
+        if (fb > fa) {
+          fused_flush_gemm(PhiCols, PhitCols, Wrow, Wtrow, ksel, mphi - s, fa, fb, lo, rec, cs);
+        } else {
+          gemm_panels<T>(PhiCols, Wrow, ksel, n, tmp.U, ctx, cs);
+          gemm_panels<T>(PhitCols, Wtrow, ksel, n, tmp.Ut, ctx, cs);
+        }
+        fa = fb = 0;   // done
       }
       {
         Phase ph("cycle.spmm", cs);
@@ -992,6 +1093,8 @@ struct Solver {
       }
       biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms);
     }
+    if (fb > fa)   // no selection: the deferred flush alone
+      fused_flush_gemm({}, {}, {}, {}, 0, 0, fa, fb, lo, rec, cs);
     RB_CUDA(cudaStreamSynchronize(cs));
     cand_cur = nxt;
     t_cycle_dev += now_ms() - t0;
@@ -1002,16 +1105,16 @@ struct Solver {
   // columns intact while cycle j+1 runs.
   std::thread worker;
   int worker_err = 0;
-  void cycle_end_async(int j) {
+  void cycle_end_async(int j, int fa = 0, int fb = 0) {
     join_cycle();
     if (!async_cycle) {
-      cycle_end(j);
+      cycle_end(j, fa, fb);
       return;
     }
-    worker = std::thread([this, j] {
+    worker = std::thread([this, j, fa, fb] {
       try {
         cudaSetDevice(ctx->device);
-        cycle_end(j);
+        cycle_end(j, fa, fb);
       } catch (Err &e) {
         worker_err = e.code;
       } catch (...) {
@@ -1380,16 +1483,29 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
       S.pull();
     }
     t_loop += now_ms() - tl;
-    const double tf0 = now_ms();
-    S.flush_x(S.hst->iter);   // lazy x: close the segment at every pause/stop
-    t_flush += now_ms() - tf0;
     const int it = S.hst->iter;
     const bool boundary = it > 0 && it % opts->s == 0 && it / opts->s > last_cycle;
     const bool cyc_ok = S.hst->done == 2 ||
                         (S.hst->done == 1 && (S.hst->status == RBICG_OK || S.hst->status == RBICG_MAXITER));
-    if (update && boundary && cyc_ok) {
+    const bool will_cycle = update && boundary && cyc_ok;
+    // lazy x: close the segment at every pause/stop -- at a cycle boundary of a
+    // running solve the flush rides along with the cycle end on the side
+    // stream (same ring columns as the U_j GEMM); otherwise it runs here,
+    // after any flush still in flight
+    const int seg_a = S.hst->seg_start;
+    const bool defer = S.lazy_x && S.async_cycle && will_cycle && S.hst->done == 2 &&
+                       seg_a == it - opts->s;
+    const double tf0 = now_ms();
+    if (defer) {
+      S.hst->seg_start = it;
+    } else {
+      if (S.async_cycle && S.lazy_x) S.join_cycle();
+      S.flush_x(it);
+    }
+    t_flush += now_ms() - tf0;
+    if (will_cycle) {
       const double tc0 = now_ms();
-      S.cycle_end_async(it / opts->s);
+      S.cycle_end_async(it / opts->s, defer ? seg_a : 0, defer ? it : 0);
       t_cyc_launch += now_ms() - tc0;
       last_cycle = it / opts->s;
       ++cycles;

@@ -9,6 +9,7 @@
 // output tile and a chunk of rows; the per-chunk partials are summed in chunk
 // order by a second kernel.
 #include "internal.h"
+#include <cstdlib>
 
 namespace rbicg {
 
@@ -87,9 +88,63 @@ __global__ void __launch_bounds__(256) k_spmm_wide(DevMat A, const T *__restrict
   }
 }
 
+// One thread per row computing all k outputs (KB >= k accumulators): the
+// row's SELL entries are read once (coalesced across the warp) and each
+// nonzero gathers one contiguous k-row of X; the output row is k contiguous
+// values.  A persistent grid of whole waves.
+template <typename T, int KB>
+__global__ void __launch_bounds__(256) k_spmm_rows(DevMat A, const T *__restrict__ X,
+                                                   T *__restrict__ Y, int k) {
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < A.n;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sl = row >> 5;
+    const int lane = (int)(row & 31);
+    const int64_t off = A.sptr[sl];
+    const int w = (int)((A.sptr[sl + 1] - off) >> 5);
+    T acc[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) acc[j] = zero<T>();
+    for (int jj = 0; jj < w; ++jj) {
+      const int c = __ldcs(A.cols + off + jj * 32 + lane);
+      const T v = reinterpret_cast<const T *>(A.vals)[off + jj * 32 + lane];
+      const T *xr = X + (int64_t)c * k;
+#pragma unroll
+      for (int j = 0; j < KB; ++j)
+        if (j < k) acc[j] = mad(v, xr[j], acc[j]);
+    }
+    T *yr = Y + row * k;
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < k) yr[j] = acc[j];
+  }
+}
+
+template <typename T, int KB>
+static void spmm_rows_launch(const DevMat &A, const T *X, T *Y, int k, cudaStream_t s, int nsm) {
+  int per = 1;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_spmm_rows<T, KB>, 256, 0));
+  const int64_t blocks = (A.n + 255) / 256;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)std::max(1, per) * nsm));
+  k_spmm_rows<T, KB><<<grid, 256, 0, s>>>(A, X, Y, k);
+}
+
 template <typename T> void launch_spmm(const DevMat &A, const T *X, T *Y, int k, cudaStream_t s) {
   if (k <= 0) return;
   RB_CHECK(k <= KMAX, RBICG_EINVAL);
+  static const bool rows_form = !getenv("RBICG_SPMM_SLICE");
+  if (rows_form && A.max_w <= 64) {
+    int dev = 0, nsm = 148;
+    RB_CUDA(cudaGetDevice(&dev));
+    RB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (k <= 4) spmm_rows_launch<T, 4>(A, X, Y, k, s, nsm);
+    else if (k <= 8) spmm_rows_launch<T, 8>(A, X, Y, k, s, nsm);
+    else if (k <= 12) spmm_rows_launch<T, 12>(A, X, Y, k, s, nsm);
+    else if (k <= 16) spmm_rows_launch<T, 16>(A, X, Y, k, s, nsm);
+    else if (k <= 24) spmm_rows_launch<T, 24>(A, X, Y, k, s, nsm);
+    else spmm_rows_launch<T, 32>(A, X, Y, k, s, nsm);
+    count_launch();
+    return;
+  }
   const size_t sm = (size_t)32 * std::max(1, A.max_w) * (sizeof(T) + 4);
   if (sm <= 48 * 1024) {
     k_spmm<T><<<(int)A.nslices, 32 * k, sm, s>>>(A, X, Y, k);
@@ -257,6 +312,7 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
 // cp.async (double-buffered) and each thread accumulates up to PPT pairs.
 constexpr int PPT = 6;
 constexpr int MAXP = 4;
+constexpr int GPR = 64;   // rows per double-buffered sub-tile of k_gram_pairs
 struct PanelSet {
   const void *p[MAXP];
   int nc[MAXP];     // columns (= leading dimension, compact panels)
@@ -267,7 +323,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_gram_pairs(PanelSet P, const int2 *__restrict__ pairs,
                                                     int npairs, int64_t n, int64_t chunk,
                                                     T *__restrict__ part) {
-  constexpr int GR = 32;
+  constexpr int GR = GPR;
   extern __shared__ __align__(16) unsigned char sm_raw[];
   T *sbase = reinterpret_cast<T *>(sm_raw);
   const int stage = GR * P.width;
@@ -349,14 +405,14 @@ void gram_pairs(const std::vector<const T *> &panels, const std::vector<int> &nc
   for (int p = 0; p < P.np; ++p) {
     P.p[p] = panels[p];
     P.nc[p] = ncols[p];
-    P.off[p] = 32 * w;
+    P.off[p] = GPR * w;
     w += ncols[p];
   }
   P.width = w;
-  const size_t sm = 2 * sizeof(T) * 32 * (size_t)w;
+  const size_t sm = 2 * sizeof(T) * GPR * (size_t)w;
   RB_CHECK(sm <= 160 * 1024, RBICG_EINVAL);
   const int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, 4 * ctx->nsm));
-  const int64_t chunk = ((n + nchunks - 1) / nchunks + 31) / 32 * 32;
+  const int64_t chunk = ((n + nchunks - 1) / nchunks + GPR - 1) / GPR * GPR;
   const int nb = (int)((n + chunk - 1) / chunk);
   std::vector<int2> hp(np);
   for (int i = 0; i < np; ++i) hp[i] = make_int2(pairs[i].first, pairs[i].second);
@@ -384,7 +440,7 @@ void gram_pairs(const std::vector<const T *> &panels, const std::vector<int> &nc
 template <typename T, int PB>
 __global__ void __launch_bounds__(256) k_gemm_panels(const ColDesc *__restrict__ X, int mX,
                                                      const T *__restrict__ M, int p, int64_t n,
-                                                     T *out) {
+                                                     T *out, T *out_last) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   T *sM = reinterpret_cast<T *>(sm_raw);                 // [mX][PB], zero padded
   ColDesc *sX = reinterpret_cast<ColDesc *>(sM + (size_t)mX * PB);
@@ -405,26 +461,31 @@ __global__ void __launch_bounds__(256) k_gemm_panels(const ColDesc *__restrict__
 #pragma unroll
       for (int c = 0; c < PB; ++c) acc[c] = mad(xv, sM[a * PB + c], acc[c]);
     }
+    // with out_last the last of the p columns goes to its own vector
+    const int po = out_last ? p - 1 : p;
 #pragma unroll
-    for (int c = 0; c < PB; ++c)
-      if (c < p) out[row * p + c] = acc[c];
+    for (int c = 0; c < PB; ++c) {
+      if (c < po) out[row * po + c] = acc[c];
+      else if (c == po && out_last) out_last[row] = acc[c];
+    }
   }
 }
 
 template <typename T, int PB>
 static void gemm_launch(const ColDesc *dX, int mX, const T *dM, int p, int64_t n, T *out,
-                        rbicg_ctx *ctx, cudaStream_t strm) {
+                        T *out_last, rbicg_ctx *ctx, cudaStream_t strm) {
   const size_t sm = sizeof(T) * (size_t)mX * PB + sizeof(ColDesc) * mX;
   RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 8);
-  k_gemm_panels<T, PB><<<grid, 256, sm, strm>>>(dX, mX, dM, p, n, out);
+  k_gemm_panels<T, PB><<<grid, 256, sm, strm>>>(dX, mX, dM, p, n, out, out_last);
   count_launch();
 }
 
 template <typename T>
-void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int p, int64_t n,
-                 T *out, rbicg_ctx *ctx, cudaStream_t strm, bool sync) {
+void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int pin, int64_t n,
+                 T *out, rbicg_ctx *ctx, cudaStream_t strm, bool sync, T *out_last) {
   const int mX = (int)X.size();
+  const int p = pin + (out_last ? 1 : 0);   // columns of M
   if (p <= 0) return;
   RB_CHECK(p <= KMAX, RBICG_EINVAL);
   std::vector<T> hM((size_t)mX * p);
@@ -443,12 +504,12 @@ void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int 
     RB_CUDA(cudaMemcpyAsync(dX, X.data(), sizeof(ColDesc) * mX, cudaMemcpyHostToDevice, strm));
     RB_CUDA(cudaMemcpyAsync(dM, hM.data(), sizeof(T) * hM.size(), cudaMemcpyHostToDevice, strm));
   }
-  if (p <= 4) gemm_launch<T, 4>(dX, mX, dM, p, n, out, ctx, strm);
-  else if (p <= 8) gemm_launch<T, 8>(dX, mX, dM, p, n, out, ctx, strm);
-  else if (p <= 12) gemm_launch<T, 12>(dX, mX, dM, p, n, out, ctx, strm);
-  else if (p <= 16) gemm_launch<T, 16>(dX, mX, dM, p, n, out, ctx, strm);
-  else if (p <= 24) gemm_launch<T, 24>(dX, mX, dM, p, n, out, ctx, strm);
-  else gemm_launch<T, 32>(dX, mX, dM, p, n, out, ctx, strm);
+  if (p <= 4) gemm_launch<T, 4>(dX, mX, dM, p, n, out, out_last, ctx, strm);
+  else if (p <= 8) gemm_launch<T, 8>(dX, mX, dM, p, n, out, out_last, ctx, strm);
+  else if (p <= 12) gemm_launch<T, 12>(dX, mX, dM, p, n, out, out_last, ctx, strm);
+  else if (p <= 16) gemm_launch<T, 16>(dX, mX, dM, p, n, out, out_last, ctx, strm);
+  else if (p <= 24) gemm_launch<T, 24>(dX, mX, dM, p, n, out, out_last, ctx, strm);
+  else gemm_launch<T, 32>(dX, mX, dM, p, n, out, out_last, ctx, strm);
   // the pinned-free staging below is host memory: synchronous copies above
   // completed before return only if we sync; otherwise keep hM alive by
   // syncing lazily through the stream-ordered free below
@@ -486,7 +547,7 @@ void prepare_block_kernels() {
   template void gram<T>(const std::vector<ColDesc> &, const std::vector<ColDesc> &, int64_t, \
                         std::vector<cplx> &, rbicg_ctx *, cudaStream_t);                   \
   template void gemm_panels<T>(const std::vector<ColDesc> &, const std::vector<cplx> &, int, \
-                               int64_t, T *, rbicg_ctx *, cudaStream_t, bool);
+                               int64_t, T *, rbicg_ctx *, cudaStream_t, bool, T *);
 RB_BINST(double)
 RB_BINST(zc)
 

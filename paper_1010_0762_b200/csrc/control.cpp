@@ -30,9 +30,18 @@ typedef void (*zgesvd_t)(const char *, const char *, const int *, const int *, c
                          double *, cplx *, const int *, cplx *, const int *, cplx *, const int *,
                          double *, int *, size_t, size_t);
 
+typedef void (*dgeev_t)(const char *, const char *, const int *, double *, const int *, double *,
+                        double *, double *, const int *, double *, const int *, double *,
+                        const int *, int *, size_t, size_t);
+typedef void (*zgeev_t)(const char *, const char *, const int *, cplx *, const int *, cplx *,
+                        cplx *, const int *, cplx *, const int *, cplx *, const int *, double *,
+                        int *, size_t, size_t);
+
 static struct {
   std::once_flag once;
   void *h = nullptr;
+  dgeev_t dgeev = nullptr;
+  zgeev_t zgeev = nullptr;
   dggev_t dggev = nullptr;
   zggev_t zggev = nullptr;
   dgesvd_t dgesvd = nullptr;
@@ -53,12 +62,78 @@ static void load() {
     if (!L.h) L.h = dlopen("liblapack.so.3", RTLD_NOW | RTLD_LOCAL);
     if (!L.h) L.h = dlopen("libopenblas.so.0", RTLD_NOW | RTLD_LOCAL);
     if (!L.h) return;
+    L.dgeev = (dgeev_t)sym("dgeev_");
+    L.zgeev = (zgeev_t)sym("zgeev_");
     L.dggev = (dggev_t)sym("dggev_");
     L.zggev = (zggev_t)sym("zggev_");
     L.dgesvd = (dgesvd_t)sym("dgesvd_");
     L.zgesvd = (zgesvd_t)sym("zgesvd_");
   });
-  RB_CHECK(L.dggev && L.zggev && L.dgesvd && L.zgesvd, RBICG_ELAPACK);
+  RB_CHECK(L.dggev && L.zggev && L.dgesvd && L.zgesvd && L.dgeev && L.zgeev, RBICG_ELAPACK);
+}
+
+// Standard eigenproblem P w = λ w with left and right vectors (the Q = I
+// pencil of the first cycle of the first system, eigenvectors of T_1,
+// P:614-628): the QR algorithm instead of QZ, same outputs as lapack_ggev
+// with beta = 1.
+int lapack_geev(bool real, int m, const std::vector<cplx> &P, std::vector<cplx> &alpha,
+                std::vector<cplx> &beta, std::vector<cplx> &VL, std::vector<cplx> &VR) {
+  load();
+  alpha.assign(m, 0.0);
+  beta.assign(m, 1.0);
+  VL.assign((size_t)m * m, 0.0);
+  VR.assign((size_t)m * m, 0.0);
+  if (m == 0) return 0;
+  int info = 0;
+  const char V = 'V';
+  if (real) {
+    std::vector<double> a((size_t)m * m), vl((size_t)m * m), vr((size_t)m * m), wr(m), wi(m);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) a[(size_t)j * m + i] = P[(size_t)i * m + j].real();
+    int lwork = -1;
+    double wq = 0;
+    L.dgeev(&V, &V, &m, a.data(), &m, wr.data(), wi.data(), vl.data(), &m, vr.data(), &m, &wq, &lwork,
+            &info, 1, 1);
+    lwork = std::max(1, (int)wq);
+    std::vector<double> work(lwork);
+    L.dgeev(&V, &V, &m, a.data(), &m, wr.data(), wi.data(), vl.data(), &m, vr.data(), &m,
+            work.data(), &lwork, &info, 1, 1);
+    if (info != 0) return RBICG_ELAPACK;
+    for (int j = 0; j < m; ++j) alpha[j] = cplx(wr[j], wi[j]);
+    for (int j = 0; j < m; ++j) {
+      if (wi[j] == 0.0) {
+        for (int i = 0; i < m; ++i) {
+          VR[(size_t)j * m + i] = vr[(size_t)j * m + i];
+          VL[(size_t)j * m + i] = vl[(size_t)j * m + i];
+        }
+      } else if (wi[j] > 0.0 && j + 1 < m) {   // conjugate pair in adjacent columns
+        for (int i = 0; i < m; ++i) {
+          const cplx cr(vr[(size_t)j * m + i], vr[(size_t)(j + 1) * m + i]);
+          const cplx cl(vl[(size_t)j * m + i], vl[(size_t)(j + 1) * m + i]);
+          VR[(size_t)j * m + i] = cr;
+          VR[(size_t)(j + 1) * m + i] = std::conj(cr);
+          VL[(size_t)j * m + i] = cl;
+          VL[(size_t)(j + 1) * m + i] = std::conj(cl);
+        }
+        ++j;
+      }
+    }
+  } else {
+    std::vector<cplx> a((size_t)m * m);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) a[(size_t)j * m + i] = P[(size_t)i * m + j];
+    int lwork = -1;
+    cplx wq;
+    std::vector<double> rwork(2 * m);
+    L.zgeev(&V, &V, &m, a.data(), &m, alpha.data(), VL.data(), &m, VR.data(), &m, &wq, &lwork,
+            rwork.data(), &info, 1, 1);
+    lwork = std::max(1, (int)wq.real());
+    std::vector<cplx> work(lwork);
+    L.zgeev(&V, &V, &m, a.data(), &m, alpha.data(), VL.data(), &m, VR.data(), &m, work.data(),
+            &lwork, rwork.data(), &info, 1, 1);
+    if (info != 0) return RBICG_ELAPACK;
+  }
+  return 0;
 }
 
 // P, Q row-major m x m.  Outputs: alpha, beta (complex), VL, VR column-major

@@ -507,8 +507,8 @@ __device__ __forceinline__ void p1_tiles(const LoopArgs<T> &a, unsigned char *ds
       const T pn = mad(beta, po, rr);
       const T ptn = mad(cb, pto, rtr);
       if (segcopy) {   // lazy x: keep p_a, p~_a of the new segment
-        a.pseg[row] = po;
-        a.ptseg[row] = pto;
+        a.pseg[(it / a.cyc) & 1][row] = po;
+        a.ptseg[(it / a.cyc) & 1][row] = pto;
       }
       if (!(a.abl & 2)) {   // (timing ablation 2: no stores)
         pnew[row] = pn;
@@ -719,7 +719,7 @@ __device__ __forceinline__ void p1_tiles_split(const LoopArgs<T> &a, unsigned ch
   const T *__restrict__ pold = side ? ptcol(a, it) : pcol(a, it);
   T *__restrict__ pnew = side ? ptcol(a, it + 1) : pcol(a, it + 1);
   T *__restrict__ zout = side ? a.zt : a.z;
-  T *__restrict__ pseg = side ? a.ptseg : a.pseg;
+  T *__restrict__ pseg = side ? a.ptseg[(it / a.cyc) & 1] : a.pseg[(it / a.cyc) & 1];
   T *s_z = sc.s_z(), *s_zt = s_z + TRH, *s_pt2 = s_z + 2 * TRH;   // s_pt double-buffered
   const int rstep = k > 0 ? BS / k : 0;
   const int kt = rstep * k;

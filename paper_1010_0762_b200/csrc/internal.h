@@ -73,7 +73,8 @@ struct LoopArgs {
   int abl;                 // timing ablations (RBICG_ABL, never set in a solve): 1 no gathers
   int pass2_tma;           // pass 2 streams its tiles through smem via TMA
   int lazy_x;              // x, x~ rebuilt per segment from the Lanczos ring
-  T *pseg, *ptseg;         // p_a, p~_a at the start of the open segment
+  T *pseg[2], *ptseg[2];   // p_a, p~_a at the start of the open segment, by segment parity
+  int cyc;                 // cycle length s (segment parity = (seg_start / s) & 1)
   int nsm;
   DevMat A, AH;
   T *rring, *rtring;       // ring of residual columns (r_m in column m % ring)
@@ -201,7 +202,9 @@ void gram_pairs(const std::vector<const T *> &panels, const std::vector<int> &nc
                 rbicg_ctx *ctx, cudaStream_t s);   // out[i] = x_{a_i}^H x_{b_i}, compact panels
 template <typename T>
 void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int p, int64_t n,
-                 T *out, rbicg_ctx *ctx, cudaStream_t s, bool sync = true);   // out (row-major n x p) = X M
+                 T *out, rbicg_ctx *ctx, cudaStream_t s, bool sync = true,
+                 T *out_last = nullptr);   // out (row-major n x p) = X M; with out_last, M has
+                                           // p + 1 columns and the last one goes to out_last[n]
 
 // ---- workspace helpers (api.cu)
 void *ws_alloc(size_t bytes);
@@ -211,6 +214,8 @@ void ws_free(void *p);
 int lapack_ggev(bool real, int m, std::vector<cplx> P, std::vector<cplx> Q,
                 std::vector<cplx> &alpha, std::vector<cplx> &beta, std::vector<cplx> &VL,
                 std::vector<cplx> &VR, std::vector<int> &pair_first);
+int lapack_geev(bool real, int m, const std::vector<cplx> &P, std::vector<cplx> &alpha,
+                std::vector<cplx> &beta, std::vector<cplx> &VL, std::vector<cplx> &VR);
 int lapack_gesvd(bool real, int m, std::vector<cplx> G, std::vector<double> &S,
                  std::vector<cplx> &Mleft, std::vector<cplx> &Nright);
 
