@@ -19,8 +19,8 @@ static const bool g_pdl = getenv("RBICG_PDL") ? atoi(getenv("RBICG_PDL")) != 0 :
 
 
 // ============================================================== pass 1
-template <typename T>
-__global__ void __launch_bounds__(BS, 4) k_pass1(LoopArgs<T> a) {
+template <typename T, int MINB = 4>
+__global__ void __launch_bounds__(BS, MINB) k_pass1(LoopArgs<T> a) {
   __shared__ P1Scratch<T> sc;
   __shared__ Snap<T> sn;
   __shared__ T s_fin[3 * KMAX + 1];
@@ -553,9 +553,12 @@ template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s) {
   }
   const size_t sm = a.staged ? pass1_smem<T>(a) : 0;
   int per_sm = 1;
-  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass1<T>, BS, sm));
+  // register bound of the k = 0 form: RBICG_P1_MINB (4 = 64 regs, 5, 6)
+  static const int minb = getenv("RBICG_P1_MINB") ? atoi(getenv("RBICG_P1_MINB")) : 4;
+  auto fn = minb >= 6 ? k_pass1<T, 6> : (minb == 5 ? k_pass1<T, 5> : k_pass1<T, 4>);
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BS, sm));
   const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
-  launch_pdl(k_pass1<T>, grid_for(a.n, G), sm, s, a);
+  launch_pdl(fn, grid_for(a.n, G), sm, s, a);
   count_launch();
 }
 
@@ -651,8 +654,12 @@ void prepare_kernels() {
   allow_max_dyn_smem(k_pass1s<zc, 4>);
   allow_max_dyn_smem(k_pass1s<zc, 6>);
   allow_max_dyn_smem(k_pass1s<zc, 8>);
-  allow_max_dyn_smem(k_pass1<double>);
-  allow_max_dyn_smem(k_pass1<zc>);
+  allow_max_dyn_smem(k_pass1<double, 4>);
+  allow_max_dyn_smem(k_pass1<double, 5>);
+  allow_max_dyn_smem(k_pass1<double, 6>);
+  allow_max_dyn_smem(k_pass1<zc, 4>);
+  allow_max_dyn_smem(k_pass1<zc, 5>);
+  allow_max_dyn_smem(k_pass1<zc, 6>);
   allow_max_dyn_smem(k_pass2<double>);
   allow_max_dyn_smem(k_pass2<zc>);
   prepare_block_kernels();
