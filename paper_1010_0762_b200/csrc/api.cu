@@ -357,21 +357,45 @@ struct Solver {
   double t_cycle_dev = 0, t_host_eig = 0, t_refresh = 0;
   int64_t launches0 = 0, graph_launch_kernels = 0;
 
-  T *alloc(size_t elems) {
-    void *q = ws_alloc(sizeof(T) * std::max<size_t>(elems, 1));
+  // Device buffers of a solve.  The previous solve's buffers of this context
+  // (ctx->arena, in allocation order) are taken back when the sizes repeat --
+  // a sequence keeps n, k, s -- so the per-system setup makes no allocations.
+  size_t arena_pos = 0;
+  std::vector<size_t> owned_bytes;
+  void *alloc_bytes(size_t bytes) {
+    bytes = std::max<size_t>(bytes, 1);
+    void *q = nullptr;
+    if (ctx)
+      for (size_t i = arena_pos; i < ctx->arena.size(); ++i)   // same size, first free one
+        if (ctx->arena[i].second && ctx->arena[i].first == bytes) {
+          q = ctx->arena[i].second;
+          ctx->arena[i].second = nullptr;
+          if (i == arena_pos) ++arena_pos;
+          break;
+        }
+    if (!q) q = ws_alloc(bytes);
     owned.push_back(q);
-    return (T *)q;
+    owned_bytes.push_back(bytes);
+    return q;
   }
+  T *alloc(size_t elems) { return (T *)alloc_bytes(sizeof(T) * elems); }
   ~Solver() {
     static const bool tm = getenv("RBICG_TIMING") != nullptr;
     const double t0 = tm ? now_ms() : 0;
     if (worker.joinable()) worker.join();
     const double t1 = tm ? now_ms() : 0;
-    if (side) cudaStreamDestroy(side);
+    // the side stream belongs to the ctx (reused by the next solve)
     const double t2 = tm ? now_ms() : 0;
     if (gexec) cudaGraphExecDestroy(gexec);
     const double t3 = tm ? now_ms() : 0;
-    for (void *q : owned) ws_free(q);
+    if (ctx) {   // keep this solve's buffers for the next solve on the ctx
+      for (auto &kv : ctx->arena)
+        if (kv.second) ws_free(kv.second);
+      ctx->arena.clear();
+      for (size_t i = 0; i < owned.size(); ++i) ctx->arena.emplace_back(owned_bytes[i], owned[i]);
+    } else {
+      for (void *q : owned) ws_free(q);
+    }
     pinned_free(hst, sizeof(DevState<T>));
     if (tm)
       fprintf(stderr, "rbicg ~Solver join %.2f stream %.2f graph %.2f free %.2f ms\n", t1 - t0, t2 - t1,
@@ -379,6 +403,22 @@ struct Solver {
   }
 
   void setup(rbicg_ctx *c, const rbicg_mat *m, const rbicg_opts &opts, int k_basis) {
+    static const bool tm = getenv("RBICG_TIMING") != nullptr;
+    std::vector<std::pair<const char *, double>> tmk;
+    auto tmark = [&](const char *nm) {
+      if (tm) tmk.emplace_back(nm, now_ms());
+    };
+    tmark("start");
+    struct Dump {
+      std::vector<std::pair<const char *, double>> &v;
+      ~Dump() {
+        if (v.size() > 1 && v.back().second - v.front().second > 5.0) {
+          fprintf(stderr, "rbicg setup:");
+          for (size_t i = 1; i < v.size(); ++i) fprintf(stderr, " %s %.2f", v[i].first, v[i].second - v[i - 1].second);
+          fprintf(stderr, "\n");
+        }
+      }
+    } dump{tmk};
     ctx = c;
     M = m;
     o = opts;
@@ -387,18 +427,33 @@ struct Solver {
     kmax = std::max(std::max(o.k, k_basis), 1);
     ring = o.s + 2;
     if (o.k > 0 && o.update_recycle && !getenv("RBICG_SYNC_CYCLE")) {
-      size_t fr = 0, tot = 0;
-      RB_CUDA(cudaMemGetInfo(&fr, &tot));
+      // doubled ring for the overlapped cycle end when memory allows; the
+      // decision is kept per (ctx, n, k, s) so a sequence does not query the
+      // allocator every system (cudaMemGetInfo measured up to 20 ms)
       const size_t extra = (size_t)2 * ring * n * sizeof(T);
       const size_t need = extra + (size_t)(16 * kmax + 2 * ring + 16) * n * sizeof(T);
-      if (fr > need + ((size_t)2 << 30)) {
+      const uint64_t key = ((uint64_t)n << 20) ^ ((uint64_t)kmax << 10) ^ (uint64_t)o.s ^ (sizeof(T) << 60);
+      if (ctx->async_key != key) {
+        size_t fr = 0, tot = 0;
+        RB_CUDA(cudaMemGetInfo(&fr, &tot));
+        // the previous solve's buffers (arena) count as available
+        size_t held = 0;
+        for (auto &kv : ctx->arena) held += kv.first;
+        ctx->async_key = key;
+        ctx->async_ok = fr + held > need + ((size_t)2 << 30);
+      }
+      if (ctx->async_ok) {
         ring *= 2;
         async_cycle = true;
-        // RBICG_SIDE_PRIO=hi runs the cycle-end kernels at the loop's priority
-        const bool side_hi = getenv("RBICG_SIDE_PRIO") && getenv("RBICG_SIDE_PRIO")[0] == 'h';
-        RB_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, side_hi ? ctx->prio_hi : ctx->prio_lo));
+        if (!ctx->side) {   // RBICG_SIDE_PRIO=hi runs the cycle-end kernels at the loop's priority
+          const bool side_hi = getenv("RBICG_SIDE_PRIO") && getenv("RBICG_SIDE_PRIO")[0] == 'h';
+          RB_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking,
+                                               side_hi ? ctx->prio_hi : ctx->prio_lo));
+        }
+        side = ctx->side;
       }
     }
+    tmark("meminfo+stream");
     // row partition: gathered vectors carry the ghost rows [n, nx) behind the own rows
     dist = ctx->dist();
     nx = n + (dist ? m->halo.nghost : 0);
@@ -431,6 +486,7 @@ struct Solver {
         pring_len = ring;
       }
     }
+    tmark("ring+p");
     z = alloc(n);
     zt = alloc(n);
     x = alloc(nx);
@@ -451,18 +507,18 @@ struct Solver {
       B->Ct = alloc((size_t)n * kmax);
       B->k = 0;
     }
-    st = (DevState<T> *)ws_alloc(sizeof(DevState<T>));
-    owned.push_back(st);
+    tmark("vectors+bases");
+    st = (DevState<T> *)alloc_bytes(sizeof(DevState<T>));
     hst = (DevState<T> *)pinned_alloc(sizeof(DevState<T>));
     const int H = std::max(o.max_itn, 0) + 2;
-    hist = (IterRec<T> *)ws_alloc(sizeof(IterRec<T>) * H);
-    owned.push_back(hist);
+    hist = (IterRec<T> *)alloc_bytes(sizeof(IterRec<T>) * H);
     zhist = alloc((size_t)H * kmax);
     zthist = alloc((size_t)H * kmax);
     const int nout = 3 * KMAX + 8 + 2 * KMAX;
     part = alloc((size_t)nout * ctx->grid_stream);
     memset(hst, 0, sizeof(DevState<T>));
     launches0 = g_launches.load();
+    tmark("state+hist");
   }
 
   void make_args() {
@@ -847,6 +903,70 @@ struct Solver {
     gemm_panels<T>(Xt, Mt, ksel, n, tmp.Ut, ctx, cs, true, xt);
   }
 
+  // [U_j | C_j | x] = [Υ_j | p_a | x] M for the T_j pencil: the U block is
+  // W_j on the V_j rows (Lanczos scalings folded, Wrow), the C block
+  // diag(sv) Γ_j W_j over all Υ_j rows, the x block the lazy-x flush (when
+  // fa < fb).  The dual likewise with Ῡ_j, Γ~_j, W~_j, svt and conj(c).
+  template <typename SV, typename SVT>
+  void relation_gemm(const std::vector<int> &rows, const std::vector<int> &cols, int top,
+                     const std::vector<cplx> &Gam, const std::vector<cplx> &Gamt,
+                     const std::vector<cplx> &Wun, const std::vector<cplx> &Wtun,
+                     const std::vector<cplx> &Wrow, const std::vector<cplx> &Wtrow, int ksel,
+                     SV sv, SVT svt, int fa, int fb, int lo, const std::vector<IterRec<T>> &rec,
+                     cudaStream_t cs) {
+    const int s = (int)cols.size(), nr = (int)rows.size();
+    const bool fl = fb > fa;
+    std::vector<cplx> cr;
+    if (fl) {
+      RB_CHECK(fb - fa == s && fa == cols[0] - 1, RBICG_ESTATE);
+      cr = flush_coeffs(fa, fb, rec.data() + (fa - lo));
+    }
+    std::vector<ColDesc> X, Xt;
+    for (int a = 0; a < nr; ++a) {
+      X.push_back(rcol(rows[a] - 1));
+      Xt.push_back(rtcol(rows[a] - 1));
+    }
+    if (fl) {
+      X.push_back(ColDesc{pseg_of(fa), 1});
+      Xt.push_back(ColDesc{ptseg_of(fa), 1});
+      X.push_back(ColDesc{x, 1});
+      Xt.push_back(ColDesc{xt, 1});
+    }
+    const int mX = (int)X.size(), p = 2 * ksel + (fl ? 1 : 0);
+    std::vector<cplx> M((size_t)mX * p, 0.0), Mt((size_t)mX * p, 0.0);
+    for (int a = 0; a < nr; ++a) {
+      const bool vrow = a >= top && a < top + s;
+      for (int c = 0; c < ksel; ++c) {
+        if (vrow) {
+          M[(size_t)a * p + c] = Wrow[(size_t)(a - top) * ksel + c];
+          Mt[(size_t)a * p + c] = Wtrow[(size_t)(a - top) * ksel + c];
+        }
+        cplx g = 0.0, gt = 0.0;
+        for (int bb = 0; bb < s; ++bb) {
+          g += Gam[(size_t)a * s + bb] * Wun[(size_t)bb * ksel + c];
+          gt += Gamt[(size_t)a * s + bb] * Wtun[(size_t)bb * ksel + c];
+        }
+        M[(size_t)a * p + ksel + c] = sv(rows[a]) * g;
+        Mt[(size_t)a * p + ksel + c] = svt(rows[a]) * gt;
+      }
+      if (fl && vrow) {
+        M[(size_t)a * p + 2 * ksel] = cr[a - top];
+        Mt[(size_t)a * p + 2 * ksel] = std::conj(cr[a - top]);
+      }
+    }
+    std::vector<std::pair<T *, int>> outs{{tmp.U, ksel}, {tmp.C, ksel}}, outst{{tmp.Ut, ksel}, {tmp.Ct, ksel}};
+    if (fl) {
+      M[(size_t)nr * p + 2 * ksel] = cr[s];
+      Mt[(size_t)nr * p + 2 * ksel] = std::conj(cr[s]);
+      M[(size_t)(nr + 1) * p + 2 * ksel] = 1.0;
+      Mt[(size_t)(nr + 1) * p + 2 * ksel] = 1.0;
+      outs.push_back({x, 1});
+      outst.push_back({xt, 1});
+    }
+    gemm_multi<T>(X, M, outs, n, ctx, cs);
+    gemm_multi<T>(Xt, Mt, outst, n, ctx, cs);
+  }
+
   // fa < fb: also the deferred lazy-x flush of segment (fa, fb] = this
   // cycle's iterations, fused into the U_j GEMM (both read the same ring
   // columns r_fa .. r_{fb-1})
@@ -1074,6 +1194,35 @@ struct Solver {
         }
       }
       // U_j = Φ_j W_j, Ũ_j = Φ~_j W~_j; C_j = A U_j, C~_j = A^* Ũ_j
+      static const bool crel = !getenv("RBICG_C_SPMM");
+      if (!haveC && !havePrev && crel) {
+        // T_j pencil (no recycle data): A V_j = Υ_j Γ_j, the bi-Lanczos relation
+        // (P:527-550), so C_j = Υ_j (Γ_j W_j) and C~_j = Ῡ_j (Γ~_j W~_j): U_j, C_j
+        // and the deferred lazy-x flush come out of ONE pass over the Υ_j ring
+        // columns -- no SpMM, no halo.  DESIGN §6 (reading Q15).
+        Phase ph("cycle.gemm_UCx", cs);
+        relation_gemm(rows, cols, top, Gam, Gamt, sel.W, sel.Wt, Wrow, Wtrow, ksel, sv, svt, fa, fb,
+                      lo, rec, cs);
+        fa = fb = 0;
+        if (getenv("RBICG_C_CHECK") && !dist) {   // debug: relation vs explicit SpMM
+          RB_CUDA(cudaStreamSynchronize(cs));
+          std::vector<T> c1((size_t)n * ksel), c2((size_t)n * ksel);
+          T *chk = (T *)ws_alloc(sizeof(T) * n * ksel);
+          launch_spmm<T>(M->A, tmp.U, chk, ksel, cs);
+          RB_CUDA(cudaMemcpyAsync(c1.data(), tmp.C, sizeof(T) * n * ksel, cudaMemcpyDeviceToHost, cs));
+          RB_CUDA(cudaMemcpyAsync(c2.data(), chk, sizeof(T) * n * ksel, cudaMemcpyDeviceToHost, cs));
+          RB_CUDA(cudaStreamSynchronize(cs));
+          ws_free(chk);
+          double dn = 0, nn = 0;
+          for (size_t i = 0; i < c1.size(); ++i) {
+            dn += abs2(sub(c1[i], c2[i]));
+            nn += abs2(c2[i]);
+          }
+          fprintf(stderr, "rbicg C_j relation vs SpMM: cycle %d ksel %d rel diff %.3e\n", j, ksel,
+                  std::sqrt(dn / std::max(nn, 1e-300)));
+        }
+        biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms);
+      } else {
       {
         Phase ph("cycle.gemm_UW", cs);
         if (fb > fa) {
@@ -1092,6 +1241,7 @@ struct Solver {
         launch_spmm<T>(M->AH, tmp.Ut, tmp.Ct, ksel, cs);
       }
       biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms);
+      }
     }
     if (fb > fa)   // no selection: the deferred flush alone
       fused_flush_gemm({}, {}, {}, {}, 0, 0, fa, fb, lo, rec, cs);
@@ -1297,6 +1447,10 @@ int rbicg_nccl_unique_id(uint8_t *id) {
 int rbicg_finalize(rbicg_ctx *ctx) {
   if (!ctx) return RBICG_EINVAL;
   cudaStreamSynchronize(ctx->stream);
+  for (auto &kv : ctx->arena)
+    if (kv.second) ws_free(kv.second);
+  ctx->arena.clear();
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   ws_release_all();
   cudaEventDestroy(ctx->order_ev);
   cudaStreamDestroy(ctx->stream);

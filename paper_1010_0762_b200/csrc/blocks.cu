@@ -522,6 +522,93 @@ void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int 
   }
 }
 
+// Several outputs from one pass over the panel columns: output segment q takes
+// columns [c0_q, c0_q + nc_q) of X M into its own row-major n x nc_q array
+// (U_j, C_j and the lazy-x flush of a cycle end, api.cu).
+struct OutSegs {
+  void *p[4];
+  int nc[4];
+  int ns;
+};
+template <typename T, int PB>
+__global__ void __launch_bounds__(256) k_gemm_multi(const ColDesc *__restrict__ X, int mX,
+                                                    const T *__restrict__ M, int p, int64_t n,
+                                                    OutSegs O) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  T *sM = reinterpret_cast<T *>(sm_raw);   // [mX][PB], zero padded
+  ColDesc *sX = reinterpret_cast<ColDesc *>(sM + (size_t)mX * PB);
+  for (int e = threadIdx.x; e < mX * PB; e += blockDim.x) {
+    const int a = e / PB, c = e % PB;
+    sM[e] = c < p ? M[a * p + c] : zero<T>();
+  }
+  for (int e = threadIdx.x; e < mX; e += blockDim.x) sX[e] = X[e];
+  __syncthreads();
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    T acc[PB];
+#pragma unroll
+    for (int c = 0; c < PB; ++c) acc[c] = zero<T>();
+#pragma unroll 4
+    for (int a = 0; a < mX; ++a) {
+      const T xv = ldp<T>(sX[a].p, row * sX[a].stride);
+#pragma unroll
+      for (int c = 0; c < PB; ++c) acc[c] = mad(xv, sM[a * PB + c], acc[c]);
+    }
+    int c0 = 0;
+    for (int q = 0; q < O.ns; ++q) {
+      T *out = reinterpret_cast<T *>(O.p[q]);
+      const int nc = O.nc[q];
+#pragma unroll
+      for (int c = 0; c < PB; ++c)
+        if (c >= c0 && c < c0 + nc) out[row * nc + (c - c0)] = acc[c];
+      c0 += nc;
+    }
+  }
+}
+
+template <typename T>
+void gemm_multi(const std::vector<ColDesc> &X, const std::vector<cplx> &M,
+                const std::vector<std::pair<T *, int>> &outs, int64_t n, rbicg_ctx *ctx,
+                cudaStream_t strm) {
+  const int mX = (int)X.size();
+  int p = 0;
+  OutSegs O{};
+  RB_CHECK(outs.size() <= 4, RBICG_EINVAL);
+  for (size_t q = 0; q < outs.size(); ++q) {
+    O.p[q] = outs[q].first;
+    O.nc[q] = outs[q].second;
+    p += outs[q].second;
+  }
+  O.ns = (int)outs.size();
+  if (p <= 0 || mX == 0) return;
+  RB_CHECK(p <= 32 && (int)M.size() == mX * p, RBICG_EINVAL);
+  std::vector<T> hM((size_t)mX * p);
+  for (size_t i = 0; i < hM.size(); ++i) {
+    T v = zero<T>();
+    reinterpret_cast<double *>(&v)[0] = M[i].real();
+    if (sizeof(T) == 16) reinterpret_cast<double *>(&v)[1] = M[i].imag();
+    hM[i] = v;
+  }
+  const size_t desc_bytes = sizeof(ColDesc) * mX;
+  char *buf = (char *)ws_alloc(desc_bytes + sizeof(T) * hM.size() + 32);
+  ColDesc *dX = (ColDesc *)buf;
+  T *dM = (T *)(buf + ((desc_bytes + 15) / 16) * 16);
+  RB_CUDA(cudaMemcpyAsync(dX, X.data(), desc_bytes, cudaMemcpyHostToDevice, strm));
+  RB_CUDA(cudaMemcpyAsync(dM, hM.data(), sizeof(T) * hM.size(), cudaMemcpyHostToDevice, strm));
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 8);
+  auto go = [&](auto kern, int PB) {
+    const size_t sm = sizeof(T) * (size_t)mX * PB + sizeof(ColDesc) * mX;
+    RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
+    kern<<<grid, 256, sm, strm>>>(dX, mX, dM, p, n, O);
+  };
+  if (p <= 12) go(k_gemm_multi<T, 12>, 12);
+  else if (p <= 24) go(k_gemm_multi<T, 24>, 24);
+  else go(k_gemm_multi<T, 32>, 32);
+  count_launch();
+  RB_CUDA(cudaStreamSynchronize(strm));   // hM (pageable) must outlive its copy
+  ws_free(buf);
+}
+
 void prepare_block_kernels() {
   RB_CUDA(cudaFuncSetAttribute(k_gram<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_gram<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
@@ -537,6 +624,10 @@ void prepare_block_kernels() {
   RB_GATTR(zc, 4) RB_GATTR(zc, 8) RB_GATTR(zc, 12) RB_GATTR(zc, 16) RB_GATTR(zc, 24)
   RB_GATTR(zc, 32)
 #undef RB_GATTR
+  for (auto f : {(const void *)k_gemm_multi<double, 12>, (const void *)k_gemm_multi<double, 24>,
+                 (const void *)k_gemm_multi<double, 32>, (const void *)k_gemm_multi<zc, 12>,
+                 (const void *)k_gemm_multi<zc, 24>, (const void *)k_gemm_multi<zc, 32>})
+    RB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 }
 
 #define RB_BINST(T)                                                                        \
@@ -547,7 +638,10 @@ void prepare_block_kernels() {
   template void gram<T>(const std::vector<ColDesc> &, const std::vector<ColDesc> &, int64_t, \
                         std::vector<cplx> &, rbicg_ctx *, cudaStream_t);                   \
   template void gemm_panels<T>(const std::vector<ColDesc> &, const std::vector<cplx> &, int, \
-                               int64_t, T *, rbicg_ctx *, cudaStream_t, bool, T *);
+                               int64_t, T *, rbicg_ctx *, cudaStream_t, bool, T *);       \
+  template void gemm_multi<T>(const std::vector<ColDesc> &, const std::vector<cplx> &,       \
+                              const std::vector<std::pair<T *, int>> &, int64_t, rbicg_ctx *, \
+                              cudaStream_t);
 RB_BINST(double)
 RB_BINST(zc)
 

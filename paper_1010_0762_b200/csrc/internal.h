@@ -119,6 +119,11 @@ struct rbicg_ctx {
   int rank = 0, nranks = 1;
   std::unique_ptr<rbicg::Comm> comm, comm_side;
   bool dist() const { return nranks > 1; }
+  // device buffers of the last solve (bytes, pointer), reused by the next
+  std::vector<std::pair<size_t, void *>> arena;
+  cudaStream_t side = nullptr;   // cycle-end stream (low priority), kept across solves
+  uint64_t async_key = 0;        // (n, k, s, dtype) of the last doubled-ring decision
+  bool async_ok = false;
 };
 
 struct rbicg_mat {
@@ -205,6 +210,11 @@ void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int 
                  T *out, rbicg_ctx *ctx, cudaStream_t s, bool sync = true,
                  T *out_last = nullptr);   // out (row-major n x p) = X M; with out_last, M has
                                            // p + 1 columns and the last one goes to out_last[n]
+
+template <typename T>
+void gemm_multi(const std::vector<ColDesc> &X, const std::vector<cplx> &M,
+                const std::vector<std::pair<T *, int>> &outs, int64_t n, rbicg_ctx *ctx,
+                cudaStream_t s);   // [out_0 | out_1 | ...] = X M (M row-major mX x Σ widths)
 
 // ---- workspace helpers (api.cu)
 void *ws_alloc(size_t bytes);
