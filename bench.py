@@ -183,7 +183,8 @@ def run_gpu(args, rank, world):
         x0, xt0 = prev.get(slot, (None, None))
         x, xt, res, _ = ctx.solve_dual(A, d["b"], d["bt"], x0, xt0, R=R, k=cfg.k, s=cfg.s,
                                        tol=cfg.tol, max_itn=cfg.max_itn,
-                                       trunc_tol=cfg.trunc_tol)
+                                       trunc_tol=cfg.trunc_tol,
+                                       update_recycle=not args.no_update)
         if slot is not None:
             prev[slot] = (x, xt)
         t1 = time.perf_counter()
@@ -417,6 +418,8 @@ def main():
     ap.add_argument("--cpu-sample-iters", type=int, default=80)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-update", action="store_true",
+                    help="diagnostic only: no recycle-space updates (not the method's workload)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent copies instead of the row partition")
     args = ap.parse_args()

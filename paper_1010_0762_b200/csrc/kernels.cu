@@ -139,8 +139,8 @@ __global__ void __launch_bounds__(BS, 4) k_pass1s(LoopArgs<T> a) {
 }
 
 // ============================================================== pass 2
-template <typename T>
-__global__ void __launch_bounds__(BS, 3) k_pass2(LoopArgs<T> a, int staged) {
+template <typename T, int MINB = 3>
+__global__ void __launch_bounds__(BS, MINB) k_pass2(LoopArgs<T> a, int staged) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ Snap<T> sn;
   __shared__ T s_w[BS / 32];
@@ -572,9 +572,12 @@ template <typename T> void launch_pass2(const LoopArgs<T> &a, cudaStream_t s) {
   const int staged = (sm <= 200 * 1024 && a.pass2_tma) ? 1 : 0;
   if (!staged) sm = 0;
   int per_sm = 1;
-  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass2<T>, BS, sm));
+  // register bound: RBICG_P2_MINB (4 = 64 regs, measured C3 pass 2 63.4 -> 58.5 us; 3 = 80)
+  static const int minb = getenv("RBICG_P2_MINB") ? atoi(getenv("RBICG_P2_MINB")) : 4;
+  auto fn = minb >= 4 ? k_pass2<T, 4> : k_pass2<T, 3>;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BS, sm));
   const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
-  launch_pdl(k_pass2<T>, grid_for(a.n, G), sm, s, a, staged);
+  launch_pdl(fn, grid_for(a.n, G), sm, s, a, staged);
   count_launch();
 }
 
@@ -660,8 +663,10 @@ void prepare_kernels() {
   allow_max_dyn_smem(k_pass1<zc, 4>);
   allow_max_dyn_smem(k_pass1<zc, 5>);
   allow_max_dyn_smem(k_pass1<zc, 6>);
-  allow_max_dyn_smem(k_pass2<double>);
-  allow_max_dyn_smem(k_pass2<zc>);
+  allow_max_dyn_smem(k_pass2<double, 3>);
+  allow_max_dyn_smem(k_pass2<double, 4>);
+  allow_max_dyn_smem(k_pass2<zc, 3>);
+  allow_max_dyn_smem(k_pass2<zc, 4>);
   prepare_block_kernels();
   prepare_loop_kernels();
 }
