@@ -238,8 +238,14 @@ def run_gpu(args, rank, world):
     w = 16 if cfg.complex else 8
     p1, p2 = alg_bytes(cfg.n, cfg.nnz, kt["k"], w, kt["lazy_x"])
     peak, peak_kind = hbm_peak()
-    dom_bytes, dom_ms, dom = (p1, kt["pass1_ms"], "pass1") \
-        if kt["pass1_ms"] >= kt["pass2_ms"] else (p2, kt["pass2_ms"], "pass2")
+    # kernel durations: each kernel as back-to-back launches in one CUDA graph
+    # (CUDA events around the graph on the library stream) -- its duration
+    # inside the solver's loop graph; the event-bracketed single launches
+    # (which add the host launch gap) are reported beside them
+    ok = kt["graph_each_done_flag"] == 0 and kt["pass1_graph_ms"] > 0
+    k1 = kt["pass1_graph_ms"] if ok else kt["pass1_ms"]
+    k2 = kt["pass2_graph_ms"] if ok else kt["pass2_ms"]
+    dom_bytes, dom_ms, dom = (p1, k1, "pass1") if k1 >= k2 else (p2, k2, "pass2")
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = None   # ncu DRAM bytes per launch, recorded for the config it was captured on
     try:
@@ -329,10 +335,14 @@ def run_gpu(args, rank, world):
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": dom_bytes,
-                     "pass1_ms": kt["pass1_ms"], "pass2_ms": kt["pass2_ms"],
+                     "timing": ("each kernel as %d back-to-back launches in one CUDA graph"
+                                % args.kernel_iters) if ok else "event-bracketed single launches",
+                     "pass1_ms": k1, "pass2_ms": k2,
+                     "pass1_event_ms": kt["pass1_ms"], "pass2_event_ms": kt["pass2_ms"],
+                     "loop_graph_iter_ms": kt["graph_iter_ms"],
                      "k_active": kt["k"], "lazy_x": kt["lazy_x"],
                      "tma_pass1": kt["tma_pass1"],
-                     "iter_GBps": (p1 + p2) / ((kt["pass1_ms"] + kt["pass2_ms"]) * 1e-3) / 1e9},
+                     "iter_GBps": (p1 + p2) / (kt["graph_iter_ms"] * 1e-3) / 1e9},
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clocks,

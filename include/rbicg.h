@@ -180,7 +180,7 @@ int rbicg_dbg_project(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
 
 /* Per-kernel CUDA-event timing of `iters` hot-loop iterations (stop test off)
  * on a fresh state for this matrix and R's recycle space (bench roofline).
- * ms[10] out: [0] average duration (ms) of the SpMV-pair + coefficient kernel,
+ * ms[13] out: [0] average duration (ms) of the SpMV-pair + coefficient kernel,
  * [1] of the update kernel, [2] 0 if every timed launch did full work,
  * [3] active recycle width k, [4] 1 if x is rebuilt lazily (the update kernel
  * does not touch x, p), [5] 1 if pass 1 stages matrix tiles via TMA,
@@ -189,7 +189,10 @@ int rbicg_dbg_project(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
  * kernels, the way the solver runs its cycles, [7] 0 if that graph run did
  * full work, [8] ms per iteration of the same iterations as one persistent
  * cooperative launch (-1 if that form cannot be launched here), [9] 0 if it
- * did exactly `iters` full iterations. */
+ * did exactly `iters` full iterations, [10] ms per launch of the SpMV-pair
+ * kernel alone as `iters` back-to-back launches in one graph (its duration
+ * inside the solver's graph, without host launch gaps), [11] the same for the
+ * update kernel, [12] 0 if those launches all did full work. */
 int rbicg_dbg_time_kernels(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
                            const rbicg_opts *opts, int iters, double *ms);
 

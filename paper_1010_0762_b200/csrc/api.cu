@@ -2039,6 +2039,50 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
     ms[8] = a / std::max(iters, 1);
     ms[9] = (S.hst->done == 2 && S.hst->iter == iters) ? 0.0 : 1.0;
   }
+  // each kernel alone as `iters` back-to-back launches in one graph (with the
+  // programmatic launch overlap of the solver's graph): its duration inside
+  // the loop, without the host launch gaps of the event-bracketed launches
+  // above.  Pass 1 re-reads the same state; pass 2 advances it (stop test
+  // off), so this runs last.
+  auto graph_one = [&](int which) {
+    S.hst->iter = 0;
+    S.hst->done = 0;
+    S.hst->seg_start = 0;
+    S.hst->stop_at = 1 << 30;
+    S.push();
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    const int64_t l0 = g_launches.load();
+    RB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < iters; ++i) {
+      if (which == 1) launch_pass1<T>(S.la, ctx->stream);
+      else launch_pass2<T>(S.la, ctx->stream);
+    }
+    RB_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+    RB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    RB_CUDA(cudaGraphDestroy(g));
+    g_launches.store(l0);
+    RB_CUDA(cudaGraphLaunch(ge, ctx->stream));   // warm
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    S.hst->iter = 0;
+    S.hst->done = 0;
+    S.push();
+    RB_CUDA(cudaEventRecord(ev[0], ctx->stream));
+    RB_CUDA(cudaGraphLaunch(ge, ctx->stream));
+    g_launches.fetch_add(iters);
+    RB_CUDA(cudaEventRecord(ev[1], ctx->stream));
+    RB_CUDA(cudaEventSynchronize(ev[1]));
+    float a = 0;
+    RB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    RB_CUDA(cudaGraphExecDestroy(ge));
+    S.pull();
+    return std::make_pair((double)a / std::max(iters, 1), S.hst->done);
+  };
+  const auto g1r = graph_one(1);
+  const auto g2r = graph_one(2);
+  ms[10] = g1r.first;
+  ms[11] = g2r.first;
+  ms[12] = (g1r.second == 0 && g2r.second == 0) ? 0.0 : 1.0;
   for (auto &e : ev) cudaEventDestroy(e);
   ms[0] = t1 / std::max(iters, 1);
   ms[1] = t2 / std::max(iters, 1);
