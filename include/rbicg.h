@@ -87,7 +87,9 @@ typedef struct {
   uint8_t nccl_id[128];
   int64_t row_begin, row_end;
   int32_t mode;
-  int32_t reserved;
+  int32_t force_partition; /* 1: the partitioned code path even with nranks == 1
+                              (one-rank NCCL communicator: the collective plumbing,
+                              graph capture and split reductions on one GPU) */
 } rbicg_dist;
 
 typedef struct {

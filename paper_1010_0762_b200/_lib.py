@@ -65,7 +65,7 @@ class Dist(C.Structure):
     _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32),
                 ("nccl_id", C.c_uint8 * 128), ("row_begin", C.c_int64),
                 ("row_end", C.c_int64), ("mode", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("force_partition", C.c_int32)]
 
 
 class Opts(C.Structure):

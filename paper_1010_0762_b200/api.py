@@ -70,6 +70,7 @@ class Context:
             d = _lib.Dist()
             d.rank, d.nranks = int(dist["rank"]), int(dist["nranks"])
             d.mode = int(dist.get("mode", 0))
+            d.force_partition = int(dist.get("force_partition", 0))
             key = bytes(dist["key"])[:128].ljust(128, b"\0")
             for i in range(128):
                 d.nccl_id[i] = key[i]

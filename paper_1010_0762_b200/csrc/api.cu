@@ -317,10 +317,10 @@ struct Solver {
     if (dist) ctx->comm->allreduce_dev((double *)red, (int64_t)cnt * (int64_t)(sizeof(T) / 8), s);
   }
   static void sum_host(Comm *cm, std::vector<cplx> &v) {
-    if (cm && cm->nranks > 1) cm->allreduce_host((double *)v.data(), (int64_t)2 * v.size());
+    if (cm) cm->allreduce_host((double *)v.data(), (int64_t)2 * v.size());
   }
   template <typename V> static void bcast_vec(Comm *cm, std::vector<V> &v) {
-    if (!cm || cm->nranks <= 1) return;
+    if (!cm) return;
     int64_t sz = (int64_t)v.size();
     cm->bcast_host(&sz, sizeof(sz), 0);
     v.resize(sz);
@@ -1417,9 +1417,10 @@ int rbicg_init(rbicg_ctx **out, int device, void *stream, const rbicg_dist *dist
       if (const char *e = getenv("RBICG_BLOCKS_PER_SM")) mult = std::min(8, std::max(1, atoi(e)));
       c->grid_stream = c->nsm * mult;
     }
-    if (dist && dist->nranks > 1) {   // row partition
+    if (dist && (dist->nranks > 1 || dist->force_partition)) {   // row partition
       c->rank = dist->rank;
       c->nranks = dist->nranks;
+      c->partitioned = true;
       try {
         if (dist->mode == 0) {
           c->comm = make_comm_nccl(dist->rank, dist->nranks, dist->nccl_id, device);

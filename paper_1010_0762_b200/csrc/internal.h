@@ -118,7 +118,8 @@ struct rbicg_ctx {
   // comm_side (cycle-end worker) are set
   int rank = 0, nranks = 1;
   std::unique_ptr<rbicg::Comm> comm, comm_side;
-  bool dist() const { return nranks > 1; }
+  bool partitioned = false;   // nranks > 1, or forced (rbicg_dist.force_partition)
+  bool dist() const { return partitioned; }
   // device buffers of the last solve (bytes, pointer), reused by the next
   std::vector<std::pair<size_t, void *>> arena;
   cudaStream_t side = nullptr;   // cycle-end stream (low priority), kept across solves

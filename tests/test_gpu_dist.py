@@ -239,3 +239,38 @@ def test_nccl_unique_id_loads():
     from paper_1010_0762_b200 import api
     uid = api.nccl_unique_id()
     assert len(uid) == 128 and any(uid)
+
+
+def test_nccl_one_rank_partitioned_path_matches_plain():
+    """The NCCL mode's plumbing on one GPU: a ONE-rank NCCL communicator with
+    the partitioned code path forced (rbicg_dist.force_partition) -- partitioned
+    matrix store, halo exchange with no neighbours, stream-ordered NCCL
+    allreduces captured in the cycle's CUDA graph, one-block scalar steps, the
+    cycle-end worker's second channel (ncclCommSplit) with host allreduce and
+    broadcast.  One rank sums nothing, so every iterate and the returned
+    recycle space must equal the plain single-GPU context's bitwise."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1010_0762_b200 import api
+    cfg = CONFIGS["C1"].scaled(24, systems=3, s=10)
+    items = list(system_sequence(cfg))
+    plain = api.Context(0)
+    part = api.Context(0, dist=dict(rank=0, nranks=1, mode=0, key=api.nccl_unique_id(),
+                                    force_partition=1))
+    out = []
+    for ctx in (plain, part):
+        rec = ctx.recycle(cfg.n, cfg.k)
+        runs = []
+        for item in items:
+            M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+            x, xt, res, h = ctx.solve_dual(M, item["b"], item["bt"], R=rec, k=cfg.k, s=cfg.s,
+                                           tol=cfg.tol, max_itn=cfg.max_itn,
+                                           trunc_tol=cfg.trunc_tol, history=True)
+            runs.append((x, xt, res["iterations"], res["k_in"], h, rec.export()[0]))
+        out.append(runs)
+    for a, b in zip(*out):
+        assert a[2] == b[2] and a[3] == b[3]
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        assert np.array_equal(a[4], b[4])
+        assert np.array_equal(a[5], b[5])
