@@ -1,0 +1,101 @@
+"""IRKA (Algorithm 3) over the B200 RBiCG library.
+
+The model is G(s) = c^*(sE - A)^{-1} b with E = I (PAPER.md:963-977,
+:1186-1194).  Every dual pair (σ_i I - A) v_i = b, (σ_i I - A)^* w_i = c runs
+through ``Context.solve_dual`` (the sm_100a hot path) with recycling strategy
+1: shift slot i keeps its recycle handle and its previous
+solutions from one IRKA step to the next.  The products A v_i use the
+library's SpMV kernels; the reduced model A_r = W_r^*AV_r, E_r = W_r^*V_r
+(reading Q20: E_r = W_r^*EV_r), its r x r eigenproblem and the shift update
+σ_i ← -λ_i(A_r, E_r) are host control work of r x r size (as the cycle-end
+pencil is for the solver).  Readings (Q29): convergence on the
+relative shift change, slots paired by sorting shifts by (|σ|, arg σ).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg as sla
+import scipy.sparse as sp
+
+
+def order_shifts(sig):
+    """Slot order: by |σ| (10 significant digits, so conjugate pairs tie),
+    then arg σ."""
+    sig = np.asarray(sig, dtype=np.complex128)
+    mag = np.abs(sig)
+    key = np.round(mag / max(float(mag.max()), 1e-300), 10) if len(sig) else mag
+    return sig[np.lexsort((np.angle(sig), key))]
+
+
+@dataclass
+class IrkaRun:
+    shifts: np.ndarray
+    steps: int
+    converged: bool
+    history: list = field(default_factory=list)      # shift set per step
+    iterations: list = field(default_factory=list)   # per step: RBiCG iterations per slot
+    Ar: np.ndarray = None
+    Er: np.ndarray = None
+    br: np.ndarray = None
+    cr: np.ndarray = None
+
+
+def irka(ctx, indptr, indices, data, b, c, shifts0, *, k=8, s=40, tol=1e-10,
+         max_itn=20000, trunc_tol=1e-2, shift_tol=1e-6, max_steps=30, recycle=True):
+    """Algorithm 3 on the GPU; (indptr, indices, data) is the CSR of A."""
+    A = sp.csr_matrix((np.asarray(data, np.complex128), indices, indptr))
+    n = A.shape[0]
+    I = sp.identity(n, dtype=np.complex128, format="csr")
+    MA = ctx.matrix(A.indptr, A.indices, A.data)          # for the products A v_i
+    b = np.asarray(b, np.complex128)
+    c = np.asarray(c, np.complex128)
+    sig = order_shifts(shifts0)
+    r = len(sig)
+    slots = [dict(R=ctx.recycle(n, max(k, 1), True), x=None, xt=None) for _ in range(r)]
+    run = IrkaRun(shifts=sig, steps=0, converged=False)
+
+    def solve_all(sig):
+        V = np.zeros((n, r), np.complex128)
+        W = np.zeros((n, r), np.complex128)
+        its = []
+        for i, si in enumerate(sig):
+            st = slots[i]
+            As = (si * I - A).tocsr()
+            As.sort_indices()
+            M = ctx.matrix(As.indptr, As.indices, As.data)
+            x, xt, res, _ = ctx.solve_dual(M, b, c, st["x"], st["xt"],
+                                           R=st["R"] if recycle else None,
+                                           k=k if recycle else 0, s=s, tol=tol,
+                                           max_itn=max_itn, trunc_tol=trunc_tol)
+            M.free()
+            V[:, i], W[:, i] = x, xt
+            st["x"], st["xt"] = x, xt                     # previous solution
+            its.append(res["iterations"])
+        return V, W, its
+
+    def reduced(V, W):
+        AV = np.column_stack([ctx.spmv_pair(MA, V[:, i].copy(), V[:, i].copy())[0]
+                              for i in range(r)])
+        return W.conj().T @ AV, W.conj().T @ V, W.conj().T @ b, V.conj().T @ c
+
+    V, W, its = solve_all(sig)
+    run.history.append(sig.copy())
+    run.iterations.append(its)
+    for step in range(max_steps):
+        Ar, Er, _, _ = reduced(V, W)
+        new = order_shifts(-sla.eigvals(Ar, Er))
+        change = np.max(np.abs(new - sig) / np.abs(sig))
+        sig = new
+        run.steps = step + 1
+        V, W, its = solve_all(sig)
+        run.history.append(sig.copy())
+        run.iterations.append(its)
+        if change < shift_tol:
+            run.converged = True
+            break
+    run.shifts = sig
+    run.Ar, run.Er, run.br, run.cr = reduced(V, W)
+    MA.free()
+    return run

@@ -464,3 +464,34 @@ def test_full_size_c4_bilinear_conjugate_pair(ctx):
         vals.append(val_g)
         M.free()
     assert abs(vals[1] - np.conj(vals[0])) <= 1e-8 * abs(vals[0])
+
+
+def test_irka_gpu_matches_oracle(ctx):
+    """NEXT-3: IRKA (Algorithm 3) with the dual solves on the GPU vs the IRKA
+    oracle on a stable conv-diff model: same number of IRKA steps, shift
+    trajectories to 1e-6, the same per-solve iterations (max(2, 3%)), and the
+    GPU's reduced model Hermite-interpolates G at its final shifts
+    (Theorem 3.1, dense check)."""
+    from oracle import irka as OI
+    from paper_1010_0762_b200 import irka as GI
+    from synth.convdiff import convdiff_csr
+    indptr, indices, data = convdiff_csr(8, 2, (10.0, 10.0), "central")[:3]
+    n = 64
+    A = -sp.csr_matrix((data, indices, indptr), shape=(n, n))
+    A.sort_indices()
+    b, c = vec(n, 81, dist="normal"), vec(n, 82, dist="normal")
+    kw = dict(k=4, s=10, tol=1e-12, shift_tol=1e-8, max_steps=40)
+    ref = OI.irka(A, b, c, [0.05, 0.4, 2.0], **kw)
+    got = GI.irka(ctx, A.indptr, A.indices, A.data, b, c, [0.05, 0.4, 2.0], **kw)
+    assert ref.converged and got.converged and got.steps == ref.steps
+    for sg, so in zip(got.history, ref.history):
+        np.testing.assert_allclose(sg, so, rtol=1e-6)
+    for ig, io in zip(got.iterations, ref.iterations):
+        assert all(iters_close(a, b_) for a, b_ in zip(ig, io)), (ig, io)
+    Ad = A.toarray()
+    for si in got.shifts:
+        M = si * np.eye(n) - Ad
+        y = np.linalg.solve(M, b)
+        g, dg = np.vdot(c, y), -np.vdot(c, np.linalg.solve(M, y))
+        gr, dgr = OI.transfer(got.Ar, got.Er, got.br, got.cr, si)
+        assert abs(gr - g) <= 1e-8 * abs(g) and abs(dgr - dg) <= 1e-6 * abs(dg)
