@@ -833,24 +833,24 @@ __device__ __forceinline__ void p1_partials(const LoopArgs<T> &a, P1Scratch<T> &
   if (tid == 0) a.part[(int64_t)(3 * k) * G + blockIdx.x] = bptz;
 }
 
-// Phase-2 TMA of one full 256-row tile of the input streams into stage `b`:
-// z, z~, r, r~ (+ p, p~, x, x~ when x is eager) and the C, C~ rows.
+// Phase-2 TMA of one full 256-row tile of the input streams into stage `b`,
+// in two parts that arrive separately on the stage's mbarrier (count 2):
+//   A: r, r~ (+ x, x~ when x is eager) and the C, C~ rows -- written before
+//      the preceding pass 1 started, so pass 2 may issue them before its
+//      programmatic-launch wait;
+//   B: z, z~ (+ p, p~ when x is eager) -- written by that pass 1.
 template <typename T>
-__device__ __forceinline__ void p2_issue(const LoopArgs<T> &a, T *b, uint64_t *bar, int64_t t,
-                                         const T *rold, const T *rtold, const T *pn, const T *ptn) {
+__device__ __forceinline__ void p2_issue_a(const LoopArgs<T> &a, T *b, uint64_t *bar, int64_t t,
+                                           const T *rold, const T *rtold) {
   const int k = a.k;
   const bool lazy = a.lazy_x != 0;
   const int64_t r0 = t * BS;
   const uint32_t vb = BS * (uint32_t)sizeof(T);
   const uint32_t cbytes = (uint32_t)(BS * k * sizeof(T));
-  mbar_expect_tx(bar, (lazy ? 4u : 8u) * vb + 2u * cbytes);
-  tma_load_1d(b + 0 * BS, a.z + r0, vb, bar);
-  tma_load_1d(b + 1 * BS, a.zt + r0, vb, bar);
+  mbar_expect_tx(bar, (lazy ? 2u : 4u) * vb + 2u * cbytes);
   tma_load_1d(b + 2 * BS, rold + r0, vb, bar);
   tma_load_1d(b + 3 * BS, rtold + r0, vb, bar);
   if (!lazy) {
-    tma_load_1d(b + 4 * BS, pn + r0, vb, bar);
-    tma_load_1d(b + 5 * BS, ptn + r0, vb, bar);
     tma_load_1d(b + 6 * BS, a.x + r0, vb, bar);
     tma_load_1d(b + 7 * BS, a.xt + r0, vb, bar);
   }
@@ -860,18 +860,39 @@ __device__ __forceinline__ void p2_issue(const LoopArgs<T> &a, T *b, uint64_t *b
     tma_load_1d(b + nv * BS + BS * k, a.Ct + r0 * k, cbytes, bar);
   }
 }
+template <typename T>
+__device__ __forceinline__ void p2_issue_b(const LoopArgs<T> &a, T *b, uint64_t *bar, int64_t t,
+                                           const T *pn, const T *ptn) {
+  const bool lazy = a.lazy_x != 0;
+  const int64_t r0 = t * BS;
+  const uint32_t vb = BS * (uint32_t)sizeof(T);
+  mbar_expect_tx(bar, (lazy ? 2u : 4u) * vb);
+  tma_load_1d(b + 0 * BS, a.z + r0, vb, bar);
+  tma_load_1d(b + 1 * BS, a.zt + r0, vb, bar);
+  if (!lazy) {
+    tma_load_1d(b + 4 * BS, pn + r0, vb, bar);
+    tma_load_1d(b + 5 * BS, ptn + r0, vb, bar);
+  }
+}
+template <typename T>
+__device__ __forceinline__ void p2_issue(const LoopArgs<T> &a, T *b, uint64_t *bar, int64_t t,
+                                         const T *rold, const T *rtold, const T *pn, const T *ptn) {
+  p2_issue_a<T>(a, b, bar, t, rold, rtold);
+  p2_issue_b<T>(a, b, bar, t, pn, ptn);
+}
 // elements of one phase-2 stage: 4 (lazy x) or 8 vector tiles + C, C~ tiles
 template <typename T> __host__ __device__ __forceinline__ int64_t p2_stage_elems(int k, int lazy) {
   return (int64_t)(lazy ? 4 : 8) * BS + (int64_t)2 * BS * k;
 }
 
 // Phase 2 over this block's tiles.  With `staged` the full tiles come through
-// two TMA stages at sb (bars2[0..1], parity bits 0..1 of par2); if
-// `first_issued` the caller has already put the block's first full tile into
-// stage 0.  Accumulates ρ, ||r||², ||r~||² partials.
+// two TMA stages at sb (bars2[0..1], each expecting two arrivals, parity bits
+// 0..1 of par2); `first` = 0: nothing of the block's first full tile issued
+// yet, 1: all of it issued into stage 0, 2: its part A issued.
+// Accumulates ρ, ||r||², ||r~||² partials.
 template <typename T>
 __device__ __forceinline__ void p2_tiles(const LoopArgs<T> &a, bool staged, T *sb, uint64_t *bars2,
-                                         uint32_t &par2, bool first_issued, int it, T alpha,
+                                         uint32_t &par2, int first, int it, T alpha,
                                          const T *s_zeta, const T *s_zetat, T &arho, double &an,
                                          double &ant) {
   const int tid = threadIdx.x;
@@ -916,8 +937,10 @@ __device__ __forceinline__ void p2_tiles(const LoopArgs<T> &a, bool staged, T *s
     // bulk-copied into shared memory while the previous tile is processed.
     const int64_t stage = p2_stage_elems<T>(k, lazy);
     const int nv = lazy ? 4 : 8;
-    if (tid == 0 && !first_issued && (int64_t)blockIdx.x < nfull)
-      p2_issue<T>(a, sb, &bars2[0], blockIdx.x, rold, rtold, pn, ptn);
+    if (tid == 0 && (int64_t)blockIdx.x < nfull) {
+      if (first == 0) p2_issue<T>(a, sb, &bars2[0], blockIdx.x, rold, rtold, pn, ptn);
+      else if (first == 2) p2_issue_b<T>(a, sb, &bars2[0], blockIdx.x, pn, ptn);
+    }
     int i = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += G64, ++i) {
       const int si = i & 1;

@@ -149,22 +149,38 @@ __global__ void __launch_bounds__(BS, MINB) k_pass2(LoopArgs<T> a, int staged) {
   __shared__ uint64_t bars2[2];
   DevState<T> *st = a.st;
   const int tid = threadIdx.x;
-  pdl_wait();
-  snap_load(st, a.k, sn);
-  if (sn.done) return;
+  T *sb = reinterpret_cast<T *>(smem_raw);
+  const bool pre = staged && (int64_t)blockIdx.x < a.n / BS;
   if (staged) {
     if (tid == 0) {
-      mbar_init(&bars2[0], 1);
-      mbar_init(&bars2[1], 1);
+      mbar_init(&bars2[0], 2);
+      mbar_init(&bars2[1], 2);
       fence_mbar_init();
     }
     __syncthreads();
+    // Part A of the first tile before the programmatic-launch wait: r_{i-1},
+    // r~_{i-1} and C, C~ were written before the preceding pass 1 started
+    // (it waited for the previous pass 2), so they are complete here.
+    if (pre && tid == 0) {
+      const int it0 = __ldcg(&st->iter);
+      p2_issue_a<T>(a, sb, &bars2[0], blockIdx.x, a.rring + (int64_t)(it0 % a.ring) * a.ldr,
+                    a.rtring + (int64_t)(it0 % a.ring) * a.ldr);
+    }
+  }
+  pdl_wait();
+  snap_load(st, a.k, sn);
+  if (sn.done) {
+    if (pre) {   // complete the stage's second arrival and drain the copy
+      if (tid == 0) mbar_arrive(&bars2[0]);
+      mbar_wait(&bars2[0], 0);
+    }
+    return;
   }
   uint32_t par2 = 0;
   T arho = zero<T>();
   double an = 0.0, ant = 0.0;
-  p2_tiles<T>(a, staged != 0, reinterpret_cast<T *>(smem_raw), bars2, par2, false, sn.iter,
-              sn.alpha, sn.zeta, sn.zetat, arho, an, ant);
+  p2_tiles<T>(a, staged != 0, sb, bars2, par2, pre ? 2 : 0, sn.iter, sn.alpha, sn.zeta, sn.zetat,
+              arho, an, ant);
   pdl_trigger();
   p2_partials<T>(a, s_w, arho, an, ant);
   if (!last_block(&st->cnt[1], &s_last)) return;

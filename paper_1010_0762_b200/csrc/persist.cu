@@ -93,8 +93,8 @@ __global__ void __launch_bounds__(BS, MINB) k_loop(LoopArgs<T> a, int p2_staged)
     mbar_init(&bars[0], stage_v ? 2 : 1);
     mbar_init(&bars[1], stage_v ? 2 : 1);
     mbar_init(&bars[2], 1);
-    mbar_init(&bars2[0], 1);
-    mbar_init(&bars2[1], 1);
+    mbar_init(&bars2[0], 2);   // phase-2 stages: two arrivals (p2_issue_a/_b)
+    mbar_init(&bars2[1], 2);
     fence_mbar_init();
     s_gen = ld_relaxed_u32(&st->gen);
   }
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(BS, MINB) k_loop(LoopArgs<T> a, int p2_staged)
     // ---------------- phase 2: corrections, updates, ρ_i
     T arho = zero<T>();
     double an = 0.0, ant = 0.0;
-    p2_tiles<T>(a, p2_staged != 0, sb2, bars2, par2, true, it, sn.alpha, sn.zeta, sn.zetat, arho,
+    p2_tiles<T>(a, p2_staged != 0, sb2, bars2, par2, pre2 ? 1 : 0, it, sn.alpha, sn.zeta, sn.zetat, arho,
                 an, ant);
     p2_partials<T>(a, s_w, arho, an, ant);
     __syncthreads();     // phase-2 buffers consumed

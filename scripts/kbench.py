@@ -31,5 +31,6 @@ for k in (0, cfg.k):
                           iter_GBps=(b1 + b2) / (t["pass1_ms"] + t["pass2_ms"]) / 1e6, done=t["done_flag"],
                           graph_iter_ms=t["graph_iter_ms"], graph_GBps=(b1 + b2) / t["graph_iter_ms"] / 1e6,
                           graph_done=t["graph_done_flag"], loop_iter_ms=t["loop_iter_ms"],
+                          p1g=t["pass1_graph_ms"], p2g=t["pass2_graph_ms"],
                           loop_GBps=(b1 + b2) / t["loop_iter_ms"] / 1e6 if t["loop_iter_ms"] > 0 else None,
                           loop_done=t["loop_done_flag"])))
