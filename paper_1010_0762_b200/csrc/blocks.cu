@@ -530,12 +530,18 @@ struct OutSegs {
   int nc[4];
   int ns;
 };
+// Two rows per thread (rows q*256 + tid of a 512-row tile, coalesced per
+// column) so each shared-memory read of M feeds two FMAs, and M is read in
+// 16-byte pairs: the broadcast LDS, not the FMAs or HBM, bounded the
+// one-row-per-thread form (281 us for 44 -> 21 columns at n = 1M).
+template <typename T> struct MPair { T a, b; };
 template <typename T, int PB>
-__global__ void __launch_bounds__(256) k_gemm_multi(const ColDesc *__restrict__ X, int mX,
-                                                    const T *__restrict__ M, int p, int64_t n,
-                                                    OutSegs O) {
+__global__ void __launch_bounds__(256, 2) k_gemm_multi(const ColDesc *__restrict__ X, int mX,
+                                                       const T *__restrict__ M, int p, int64_t n,
+                                                       OutSegs O) {
+  constexpr int RPT = (sizeof(T) == 8 && PB <= 24) ? 2 : 1;   // registers (complex: 1)
   extern __shared__ __align__(16) unsigned char sm_raw[];
-  T *sM = reinterpret_cast<T *>(sm_raw);   // [mX][PB], zero padded
+  T *sM = reinterpret_cast<T *>(sm_raw);   // [mX][PB], zero padded (PB even)
   ColDesc *sX = reinterpret_cast<ColDesc *>(sM + (size_t)mX * PB);
   for (int e = threadIdx.x; e < mX * PB; e += blockDim.x) {
     const int a = e / PB, c = e % PB;
@@ -543,25 +549,48 @@ __global__ void __launch_bounds__(256) k_gemm_multi(const ColDesc *__restrict__ 
   }
   for (int e = threadIdx.x; e < mX; e += blockDim.x) sX[e] = X[e];
   __syncthreads();
-  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
-       row += (int64_t)gridDim.x * blockDim.x) {
-    T acc[PB];
+  const int64_t ntiles = (n + 256 * RPT - 1) / (256 * RPT);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int64_t row[RPT];
+    bool ok[RPT];
 #pragma unroll
-    for (int c = 0; c < PB; ++c) acc[c] = zero<T>();
-#pragma unroll 4
-    for (int a = 0; a < mX; ++a) {
-      const T xv = ldp<T>(sX[a].p, row * sX[a].stride);
-#pragma unroll
-      for (int c = 0; c < PB; ++c) acc[c] = mad(xv, sM[a * PB + c], acc[c]);
+    for (int q = 0; q < RPT; ++q) {
+      row[q] = tile * 256 * RPT + q * 256 + threadIdx.x;
+      ok[q] = row[q] < n;
     }
-    int c0 = 0;
-    for (int q = 0; q < O.ns; ++q) {
-      T *out = reinterpret_cast<T *>(O.p[q]);
-      const int nc = O.nc[q];
+    T acc[RPT][PB];
 #pragma unroll
-      for (int c = 0; c < PB; ++c)
-        if (c >= c0 && c < c0 + nc) out[row * nc + (c - c0)] = acc[c];
-      c0 += nc;
+    for (int q = 0; q < RPT; ++q)
+#pragma unroll
+      for (int c = 0; c < PB; ++c) acc[q][c] = zero<T>();
+#pragma unroll 2
+    for (int a = 0; a < mX; ++a) {
+      T xv[RPT];
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) xv[q] = ok[q] ? ldp<T>(sX[a].p, row[q] * sX[a].stride) : zero<T>();
+      const MPair<T> *mp = reinterpret_cast<const MPair<T> *>(sM + a * PB);
+#pragma unroll
+      for (int c2 = 0; c2 < PB / 2; ++c2) {
+        const MPair<T> m = mp[c2];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          acc[q][2 * c2] = mad(xv[q], m.a, acc[q][2 * c2]);
+          acc[q][2 * c2 + 1] = mad(xv[q], m.b, acc[q][2 * c2 + 1]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      if (!ok[q]) continue;
+      int c0 = 0;
+      for (int sg = 0; sg < O.ns; ++sg) {
+        T *out = reinterpret_cast<T *>(O.p[sg]);
+        const int nc = O.nc[sg];
+#pragma unroll
+        for (int c = 0; c < PB; ++c)
+          if (c >= c0 && c < c0 + nc) out[row[q] * nc + (c - c0)] = acc[q][c];
+        c0 += nc;
+      }
     }
   }
 }
@@ -595,10 +624,14 @@ void gemm_multi(const std::vector<ColDesc> &X, const std::vector<cplx> &M,
   T *dM = (T *)(buf + ((desc_bytes + 15) / 16) * 16);
   RB_CUDA(cudaMemcpyAsync(dX, X.data(), desc_bytes, cudaMemcpyHostToDevice, strm));
   RB_CUDA(cudaMemcpyAsync(dM, hM.data(), sizeof(T) * hM.size(), cudaMemcpyHostToDevice, strm));
-  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 8);
   auto go = [&](auto kern, int PB) {
     const size_t sm = sizeof(T) * (size_t)mX * PB + sizeof(ColDesc) * mX;
     RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
+    int per = 1;
+    RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, sm));
+    const int rows_per_block = (sizeof(T) == 8 && PB <= 24) ? 512 : 256;
+    const int grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((n + rows_per_block - 1) / rows_per_block, (int64_t)std::max(1, per) * ctx->nsm));
     kern<<<grid, 256, sm, strm>>>(dX, mX, dM, p, n, O);
   };
   if (p <= 12) go(k_gemm_multi<T, 12>, 12);
