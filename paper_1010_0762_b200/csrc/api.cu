@@ -342,7 +342,7 @@ struct Solver {
     T *U = nullptr, *Ut = nullptr, *C = nullptr, *Ct = nullptr;
     int k = 0;
     std::vector<double> d;
-  } cur, cand[2], tmp;
+  } cur, cand[1], tmp;   // cand keeps U, Ũ only (C, C~ are recomputed where needed)
   int cand_cur = -1;
   DevState<T> *st = nullptr;
   DevState<T> *hst = nullptr;   // pinned host mirror
@@ -431,7 +431,7 @@ struct Solver {
       // decision is kept per (ctx, n, k, s) so a sequence does not query the
       // allocator every system (cudaMemGetInfo measured up to 20 ms)
       const size_t extra = (size_t)2 * ring * n * sizeof(T);
-      const size_t need = extra + (size_t)(16 * kmax + 2 * ring + 16) * n * sizeof(T);
+      const size_t need = extra + (size_t)(10 * kmax + 2 * ring + 20) * n * sizeof(T);
       const uint64_t key = ((uint64_t)n << 20) ^ ((uint64_t)kmax << 10) ^ (uint64_t)o.s ^ (sizeof(T) << 60);
       if (ctx->async_key != key) {
         size_t fr = 0, tot = 0;
@@ -500,9 +500,13 @@ struct Solver {
       psegs[q] = alloc(n);
       ptsegs[q] = alloc(n);
     }
-    for (Basis *B : {&cur, &cand[0], &cand[1], &tmp}) {
+    // bases: cur (U, Ũ, C, C~), the cycle-end candidate (U, Ũ), the cycle-end
+    // temporaries (U_j, Ũ_j, C_j, C~_j) -- ten n x k blocks (C5: 91 GB)
+    for (Basis *B : {&cur, &cand[0], &tmp}) {
       B->U = alloc((size_t)nx * kmax);
       B->Ut = alloc((size_t)nx * kmax);
+      B->k = 0;
+      if (B == &cand[0]) continue;
       B->C = alloc((size_t)n * kmax);
       B->Ct = alloc((size_t)n * kmax);
       B->k = 0;
@@ -605,8 +609,9 @@ struct Solver {
 
   // Bi-orthogonalise (U, Ũ, C = AU, C~ = A^*Ũ) of width kin into `out`
   // (Q13: unit columns, absolute cut on the singular values).
+  // with_c = false: out keeps U, Ũ only (the cycle-end candidate)
   void biorth(const T *U, const T *Ut, const T *C, const T *Ct, int kin, Basis &out,
-              cudaStream_t bs, Comm *cm) {
+              cudaStream_t bs, Comm *cm, bool with_c = true) {
     // only ||c_j||^2, ||c~_j||^2 and C~^*C are needed (Q13 scaling + SVD)
     std::vector<ColDesc> X;
     for (int c = 0; c < kin; ++c) X.push_back(col(C, c, kin));
@@ -672,9 +677,11 @@ struct Solver {
     };
     Phase ph("biorth.gemm4", bs);
     gemm_panels<T>(cols_of(U), Fu, pk, n, out.U, ctx, bs);
-    gemm_panels<T>(cols_of(C), Fu, pk, n, out.C, ctx, bs);
     gemm_panels<T>(cols_of(Ut), Fut, pk, n, out.Ut, ctx, bs);
-    gemm_panels<T>(cols_of(Ct), Fut, pk, n, out.Ct, ctx, bs);
+    if (with_c) {
+      gemm_panels<T>(cols_of(C), Fu, pk, n, out.C, ctx, bs);
+      gemm_panels<T>(cols_of(Ct), Fut, pk, n, out.Ct, ctx, bs);
+    }
   }
 
   // Per-system refresh: C = AU, C~ = A^*Ũ, then biorth into cur.
@@ -1018,11 +1025,14 @@ struct Solver {
     auto svt = [&](int m) { return rn(m - 1) / std::conj(rh(m - 1)); };
 
     const bool haveC = kc > 0;
-    const bool havePrev = cand_cur >= 0 && cand[cand_cur].k > 0;
-    Basis *prev = havePrev ? &cand[cand_cur] : nullptr;
+    // one candidate buffer: U_{j-1} (prev) is consumed by the Φ_j GEMM before
+    // biorth writes U_j over it; C_{j-1} = A U_{j-1} is recomputed below
+    const bool havePrev = cand_cur >= 0 && cand[0].k > 0;
+    Basis *prev = havePrev ? &cand[0] : nullptr;
     const int kp = havePrev ? prev->k : 0;
-    const int nxt = cand_cur < 0 ? 0 : 1 - cand_cur;
-    Basis &out = cand[nxt];
+    const int nxt = 0;
+    Basis &out = cand[0];
+    Comm *cms_pre = dist ? ctx->comm_side.get() : nullptr;
 
     std::vector<ColDesc> PhiCols, PhitCols;
     std::vector<cplx> Wrow, Wtrow;   // scaled selection matrices (row-major mphi x ksel)
@@ -1070,13 +1080,20 @@ struct Solver {
           sx.push_back(1.0);
           sy.push_back(1.0);
         }
-      if (havePrev)
+      if (havePrev) {
+        // C_{j-1} = A U_{j-1}, C~_{j-1} = A^* Ũ_{j-1} into the temporaries (free
+        // until the new U_j, C_j are formed, after this Gram)
+        halo_rows(prev->U, kp, cms_pre, hsend_side, cs);
+        halo_rows(prev->Ut, kp, cms_pre, hsend_side, cs);
+        launch_spmm<T>(M->A, prev->U, tmp.C, kp, cs);
+        launch_spmm<T>(M->AH, prev->Ut, tmp.Ct, kp, cs);
         for (int c = 0; c < kp; ++c) {
-          X.push_back(col(prev->Ct, c, kp));
-          Y.push_back(col(prev->C, c, kp));
+          X.push_back(col(tmp.Ct, c, kp));
+          Y.push_back(col(tmp.C, c, kp));
           sx.push_back(1.0);
           sy.push_back(1.0);
         }
+      }
       const int offU = (int)X.size();
       for (int a = 0; a < nr; ++a) {
         X.push_back(rtcol(rows[a] - 1));
@@ -1221,7 +1238,7 @@ struct Solver {
           fprintf(stderr, "rbicg C_j relation vs SpMM: cycle %d ksel %d rel diff %.3e\n", j, ksel,
                   std::sqrt(dn / std::max(nn, 1e-300)));
         }
-        biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms);
+        biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false);
       } else {
       {
         Phase ph("cycle.gemm_UW", cs);
@@ -1240,7 +1257,7 @@ struct Solver {
         launch_spmm<T>(M->A, tmp.U, tmp.C, ksel, cs);
         launch_spmm<T>(M->AH, tmp.Ut, tmp.Ct, ksel, cs);
       }
-      biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms);
+      biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false);
       }
     }
     if (fb > fa)   // no selection: the deferred flush alone
