@@ -151,13 +151,15 @@ def run_gpu(args, rank, world):
     systems = build_systems(cfg, list(range(steps)))
     # inputs resident in HBM before the timed region (the matrix is passed
     # whole; vectors are this rank's rows)
-    dsys = []
-    for it in systems:
+    def upload(it):
         d = {k: torch.from_numpy(np.ascontiguousarray(it[k])).to(f"cuda:{dev}")
              for k in ("indptr", "indices", "data")}
         for k in ("b", "bt"):
             d[k] = torch.from_numpy(np.ascontiguousarray(it[k][r0:r1])).to(f"cuda:{dev}")
-        dsys.append(d)
+        return d
+    # the timed systems are resident before the timed region; a warm-up
+    # system is uploaded for its step and dropped after it (C5: ~6 GB each)
+    dsys = [None] * args.warmup + [upload(it) for it in systems[args.warmup:]]
     torch.cuda.synchronize()
     R = ctx.recycle(r1 - r0, cfg.k, cfg.complex)
     stream = torch.cuda.current_stream()
@@ -169,7 +171,7 @@ def run_gpu(args, rank, world):
     prev = {}   # C4 (Q7): previous sweep's solution of the same shift slot
 
     def one(i, timed):
-        d = dsys[i]
+        d = dsys[i] if dsys[i] is not None else upload(systems[i])
         slot = systems[i].get("slot")
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         eb = torch.cuda.Event(enable_timing=True)
@@ -197,6 +199,7 @@ def run_gpu(args, rank, world):
 
     for i in range(args.warmup):
         one(i, False)
+    torch.cuda.empty_cache()   # the dropped warm-up inputs go back to the device
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -234,6 +237,36 @@ def run_gpu(args, rank, world):
     A = kctx.matrix(last["indptr"], last["indices"], last["data"])
     kt = kctx.time_kernels(A, kR, k=cfg.k, s=cfg.s, iters=args.kernel_iters,
                            trunc_tol=cfg.trunc_tol)
+    # the same kernels with the projections active (k = cfg.k): the timed
+    # sequence ends with an empty recycle space (DESIGN §3 Q13 / §9), so the
+    # C~^*v / U y terms are probed on a seeded random space of cfg.k columns
+    probe = None
+    if cfg.k > 0 and not args.no_k_probe:
+        rng = np.random.default_rng(cfg.seed + 777)
+        shp = (cfg.n, cfg.k)
+        if cfg.complex:
+            Uq = rng.standard_normal(shp) + 1j * rng.standard_normal(shp)
+            Utq = rng.standard_normal(shp) + 1j * rng.standard_normal(shp)
+        else:
+            Uq, Utq = rng.standard_normal(shp), rng.standard_normal(shp)
+        Rq = kctx.recycle(cfg.n, cfg.k, cfg.complex)
+        Rq.import_(Uq, Utq)
+        del Uq, Utq
+        kq = kctx.time_kernels(A, Rq, k=cfg.k, s=cfg.s, iters=args.kernel_iters,
+                               trunc_tol=1e-300)
+        wq = 16 if cfg.complex else 8
+        q1, q2 = alg_bytes(cfg.n, cfg.nnz, kq["k"], wq, kq["lazy_x"])
+        okq = kq["graph_each_done_flag"] == 0 and kq["pass1_graph_ms"] > 0
+        m1 = kq["pass1_graph_ms"] if okq else kq["pass1_ms"]
+        m2 = kq["pass2_graph_ms"] if okq else kq["pass2_ms"]
+        pk, _ = hbm_peak()
+        probe = {"k_active": kq["k"], "pass1_ms": m1, "pass2_ms": m2,
+                 "pass1_GBps": q1 / (m1 * 1e-3) / 1e9, "pass2_GBps": q2 / (m2 * 1e-3) / 1e9,
+                 "loop_graph_iter_ms": kq["graph_iter_ms"],
+                 "iter_GBps": (q1 + q2) / (kq["graph_iter_ms"] * 1e-3) / 1e9,
+                 "iter_frac": (q1 + q2) / (kq["graph_iter_ms"] * 1e-3) / 1e9 / pk,
+                 "alg_bytes_per_iter": q1 + q2,
+                 "space": "seeded N(0,1) U, U~ (%d columns), truncation off" % cfg.k}
     A.free()
     w = 16 if cfg.complex else 8
     p1, p2 = alg_bytes(cfg.n, cfg.nnz, kt["k"], w, kt["lazy_x"])
@@ -342,7 +375,8 @@ def run_gpu(args, rank, world):
                      "loop_graph_iter_ms": kt["graph_iter_ms"],
                      "k_active": kt["k"], "lazy_x": kt["lazy_x"],
                      "tma_pass1": kt["tma_pass1"],
-                     "iter_GBps": (p1 + p2) / (kt["graph_iter_ms"] * 1e-3) / 1e9},
+                     "iter_GBps": (p1 + p2) / (kt["graph_iter_ms"] * 1e-3) / 1e9,
+                     "k_probe": probe},
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clocks,
@@ -425,8 +459,12 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C2")
     ap.add_argument("--kernel-iters", type=int, default=20)
-    ap.add_argument("--cpu-sample-iters", type=int, default=80)
+    ap.add_argument("--cpu-sample-iters", type=int, default=0,
+                    help="oracle sample length (0: 80 iterations at n ~ 1M, scaled "
+                         "down with n to keep the sample near 10-30 s, at least 8)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-k-probe", action="store_true",
+                    help="skip the k = cfg.k kernel probe in the roofline block")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-update", action="store_true",
                     help="diagnostic only: no recycle-space updates (not the method's workload)")
@@ -446,8 +484,9 @@ def main():
     if rank == 0:
         if not args.no_cpu and world == 1:
             from synth import CONFIGS
-            out["cpu_baseline"] = cpu_baseline(args, CONFIGS[args.config],
-                                               args.cpu_sample_iters)
+            cfg = CONFIGS[args.config]
+            m = args.cpu_sample_iters or max(8, min(80, int(80 * 3.2e6 / cfg.n)))
+            out["cpu_baseline"] = cpu_baseline(args, cfg, m)
         elif not args.no_cpu:
             out["cpu_baseline"] = None
         print(json.dumps(out), flush=True)

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <set>
 #include <string>
 #include <mutex>
 #include <thread>
@@ -30,6 +31,28 @@ namespace rbicg {
 static std::mutex g_pool_mu;
 static std::multimap<size_t, void *> g_pool;
 static std::map<void *, size_t> g_sizes;
+
+// Idle solve buffers kept by contexts for their next solve (rbicg_ctx::arena)
+// are given back to the device when an allocation would otherwise fail.
+static std::mutex g_arena_mu;
+static std::set<rbicg_ctx *> g_ctxs;
+
+static bool reclaim_arenas() {
+  std::lock_guard<std::mutex> la(g_arena_mu);
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  bool any = false;
+  for (rbicg_ctx *c : g_ctxs) {
+    for (auto &kv : c->arena)
+      if (kv.second) {
+        cudaFree(kv.second);
+        g_sizes.erase(kv.second);
+        kv.second = nullptr;
+        any = true;
+      }
+    c->async_key = 0;
+  }
+  return any;
+}
 
 void *ws_alloc(size_t bytes) {
   bytes = (bytes + 255) / 256 * 256;
@@ -62,6 +85,10 @@ void *ws_alloc(size_t bytes) {
     }
     cudaGetLastError();
     e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess && reclaim_arenas()) {
+      cudaGetLastError();
+      e = cudaMalloc(&p, bytes);
+    }
     if (e != cudaSuccess) {
       cudaGetLastError();
       throw Err{RBICG_ENOMEM};
@@ -365,7 +392,8 @@ struct Solver {
   void *alloc_bytes(size_t bytes) {
     bytes = std::max<size_t>(bytes, 1);
     void *q = nullptr;
-    if (ctx)
+    if (ctx) {
+      std::lock_guard<std::mutex> la(g_arena_mu);
       for (size_t i = arena_pos; i < ctx->arena.size(); ++i)   // same size, first free one
         if (ctx->arena[i].second && ctx->arena[i].first == bytes) {
           q = ctx->arena[i].second;
@@ -373,6 +401,7 @@ struct Solver {
           if (i == arena_pos) ++arena_pos;
           break;
         }
+    }
     if (!q) q = ws_alloc(bytes);
     owned.push_back(q);
     owned_bytes.push_back(bytes);
@@ -389,6 +418,7 @@ struct Solver {
     if (gexec) cudaGraphExecDestroy(gexec);
     const double t3 = tm ? now_ms() : 0;
     if (ctx) {   // keep this solve's buffers for the next solve on the ctx
+      std::lock_guard<std::mutex> la(g_arena_mu);
       for (auto &kv : ctx->arena)
         if (kv.second) ws_free(kv.second);
       ctx->arena.clear();
@@ -431,8 +461,9 @@ struct Solver {
       // decision is kept per (ctx, n, k, s) so a sequence does not query the
       // allocator every system (cudaMemGetInfo measured up to 20 ms)
       const size_t extra = (size_t)2 * ring * n * sizeof(T);
-      const size_t need = extra + (size_t)(10 * kmax + 2 * ring + 20) * n * sizeof(T);
-      const uint64_t key = ((uint64_t)n << 20) ^ ((uint64_t)kmax << 10) ^ (uint64_t)o.s ^ (sizeof(T) << 60);
+      const size_t need = extra + (size_t)(6 * kmax + 4 * std::max(k_basis, 0) + 2 * ring + 20) * n * sizeof(T);
+      const uint64_t key = ((uint64_t)n << 20) ^ ((uint64_t)kmax << 10) ^ ((uint64_t)k_basis << 40) ^
+                           (uint64_t)o.s ^ (sizeof(T) << 60);
       if (ctx->async_key != key) {
         size_t fr = 0, tot = 0;
         RB_CUDA(cudaMemGetInfo(&fr, &tot));
@@ -500,16 +531,18 @@ struct Solver {
       psegs[q] = alloc(n);
       ptsegs[q] = alloc(n);
     }
-    // bases: cur (U, Ũ, C, C~), the cycle-end candidate (U, Ũ), the cycle-end
-    // temporaries (U_j, Ũ_j, C_j, C~_j) -- ten n x k blocks (C5: 91 GB)
+    // bases: cur (U, Ũ, C, C~: the refreshed input space, k_basis columns,
+    // none for a first system), the cycle-end candidate (U, Ũ), the
+    // cycle-end temporaries (U_j, Ũ_j, C_j, C~_j): 6 n x k blocks + 4 n x k_in
+    // (C5 first system: 54 GB)
     for (Basis *B : {&cur, &cand[0], &tmp}) {
-      B->U = alloc((size_t)nx * kmax);
-      B->Ut = alloc((size_t)nx * kmax);
+      const size_t kb = B == &cur ? (size_t)std::max(k_basis, 0) : (size_t)kmax;
+      B->U = kb ? alloc((size_t)nx * kb) : nullptr;
+      B->Ut = kb ? alloc((size_t)nx * kb) : nullptr;
       B->k = 0;
       if (B == &cand[0]) continue;
-      B->C = alloc((size_t)n * kmax);
-      B->Ct = alloc((size_t)n * kmax);
-      B->k = 0;
+      B->C = kb ? alloc((size_t)n * kb) : nullptr;
+      B->Ct = kb ? alloc((size_t)n * kb) : nullptr;
     }
     tmark("vectors+bases");
     st = (DevState<T> *)alloc_bytes(sizeof(DevState<T>));
@@ -1453,6 +1486,10 @@ int rbicg_init(rbicg_ctx **out, int device, void *stream, const rbicg_dist *dist
         throw;
       }
     }
+    {
+      std::lock_guard<std::mutex> la(g_arena_mu);
+      g_ctxs.insert(c);
+    }
     *out = c;
   });
 }
@@ -1465,9 +1502,13 @@ int rbicg_nccl_unique_id(uint8_t *id) {
 int rbicg_finalize(rbicg_ctx *ctx) {
   if (!ctx) return RBICG_EINVAL;
   cudaStreamSynchronize(ctx->stream);
-  for (auto &kv : ctx->arena)
-    if (kv.second) ws_free(kv.second);
-  ctx->arena.clear();
+  {
+    std::lock_guard<std::mutex> la(g_arena_mu);
+    for (auto &kv : ctx->arena)
+      if (kv.second) ws_free(kv.second);
+    ctx->arena.clear();
+    g_ctxs.erase(ctx);
+  }
   if (ctx->side) cudaStreamDestroy(ctx->side);
   ws_release_all();
   cudaEventDestroy(ctx->order_ev);
@@ -1536,8 +1577,12 @@ int rbicg_recycle_new(rbicg_ctx *ctx, int64_t n, int32_t k_max, rbicg_dtype dtyp
     r->k = 0;
     r->dtype = dtype;
     const size_t bytes = wbytes(dtype) * n * std::max(k_max, 1);
-    RB_CUDA(cudaMalloc(&r->U, bytes));
-    RB_CUDA(cudaMalloc(&r->Ut, bytes));
+    for (void **q : {(void **)&r->U, (void **)&r->Ut})
+      if (cudaMalloc(q, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        reclaim_arenas();
+        RB_CUDA(cudaMalloc(q, bytes));
+      }
     *R = r;
   });
 }

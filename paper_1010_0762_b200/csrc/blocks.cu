@@ -610,7 +610,27 @@ void gemm_multi(const std::vector<ColDesc> &X, const std::vector<cplx> &M,
   }
   O.ns = (int)outs.size();
   if (p <= 0 || mX == 0) return;
-  RB_CHECK(p <= 32 && (int)M.size() == mX * p, RBICG_EINVAL);
+  RB_CHECK((int)M.size() == mX * p, RBICG_EINVAL);
+  if (p > 32) {
+    // wider than one launch's register tile: split the output segments into
+    // groups of <= 32 columns, one launch per group (X is read once per group)
+    size_t q0 = 0;
+    int c0 = 0;
+    while (q0 < outs.size()) {
+      size_t q1 = q0;
+      int w = 0;
+      while (q1 < outs.size() && w + outs[q1].second <= 32) w += outs[q1++].second;
+      RB_CHECK(q1 > q0, RBICG_EINVAL);   // one segment wider than 32
+      std::vector<cplx> Mg((size_t)mX * w);
+      for (int a = 0; a < mX; ++a)
+        for (int c = 0; c < w; ++c) Mg[(size_t)a * w + c] = M[(size_t)a * p + c0 + c];
+      gemm_multi<T>(X, Mg, std::vector<std::pair<T *, int>>(outs.begin() + q0, outs.begin() + q1),
+                    n, ctx, strm);
+      q0 = q1;
+      c0 += w;
+    }
+    return;
+  }
   std::vector<T> hM((size_t)mX * p);
   for (size_t i = 0; i < hM.size(); ++i) {
     T v = zero<T>();

@@ -365,8 +365,7 @@ def test_edge_cases(ctx):
 def test_full_size_spmv_pair(ctx, name):
     """BASELINE sizes (C2: n = 1,048,576; C3: n = 7,077,888; C4: n = 10^6
     complex; C5: n = 56,623,104, nnz = 395,476,992): the SpMV pair of the
-    device SELL store vs scipy, 1e-12 norm-wise.  (C5's solve does not fit one
-    GPU -- DESIGN §9 -- but its matrix store does.)"""
+    device SELL store vs scipy, 1e-12 norm-wise."""
     cfg = CONFIGS[name]
     if name == "C5":
         import psutil
@@ -440,6 +439,70 @@ def test_full_size_c3_matched_iterations(ctx):
                                np.linalg.norm(item["b"]), rtol=1e-6)
     assert res["k_out"] == ref.basis_out.k
     M.free()
+
+
+def test_c5_family_k20_sequence(ctx):
+    """C5's solver parameters (k = 20, s = 50: the widest recycle space of the
+    five configs, cycle-end GEMMs wider than one 32-column launch) on the C5
+    operator family at 24^3, three systems in sequence (Q27 protocol)."""
+    cfg = CONFIGS["C5"].scaled(24, systems=3)
+    items = list(system_sequence(cfg))
+    its = _carry_from_oracle(ctx, cfg.k, cfg.s, cfg.tol, cfg.trunc_tol, items,
+                             lambda it: _csr((it["indptr"], it["indices"], it["data"])),
+                             cfg.max_itn, check_space=0.99)
+    assert len(its) == 3
+
+
+def _c5_host_ok(extra_gb):
+    import psutil
+    return psutil.virtual_memory().available >= extra_gb * 2**30
+
+
+def test_full_size_c5_matched_iterations(ctx):
+    """C5 system 0 at full size (n = 56,623,104, nnz = 395,476,992, k = 20,
+    s = 50) on ONE GPU: 12 forced iterations vs the oracle (iterates 1e-7,
+    residual histories 1e-6)."""
+    from oracle import rbicg as R
+    if not _c5_host_ok(48):
+        pytest.skip("the C5 oracle run needs ~40 GB of host memory")
+    cfg = CONFIGS["C5"]
+    item = next(system_sequence(cfg, systems=[0]))
+    m = 12
+    A = _csr((item["indptr"], item["indices"], item["data"]))
+    ref = R.solve_dual(A, item["b"], item["bt"], k=cfg.k, s=cfg.s, tol=cfg.tol,
+                       max_itn=m, trunc_tol=cfg.trunc_tol, force_iters=m)
+    rec = ctx.recycle(cfg.n, cfg.k)
+    M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+    x, xt, res, h = ctx.solve_dual(M, item["b"], item["bt"], R=rec, k=cfg.k,
+                                   s=cfg.s, tol=cfg.tol, max_itn=m,
+                                   trunc_tol=cfg.trunc_tol, force_iters=m,
+                                   history=True)
+    assert res["iterations"] == m
+    assert np.linalg.norm(x - ref.x) <= 1e-7 * np.linalg.norm(ref.x)
+    assert np.linalg.norm(xt - ref.xt) <= 1e-7 * np.linalg.norm(ref.xt)
+    np.testing.assert_allclose(h[:, 0], np.array(ref.hist["rnorm"][1:]) /
+                               np.linalg.norm(item["b"]), rtol=1e-6)
+    M.free()
+
+
+def test_full_size_c5_sequence_converges(ctx):
+    """C5 systems 0 and 1 at full size on ONE GPU, the GPU's own recycle
+    chain: both converge (status 0 or recycle_empty, P:702 footnote) and the
+    true residuals recomputed on the host with scipy are <= tol = 1e-8."""
+    if not _c5_host_ok(24):
+        pytest.skip("host-side residuals need ~16 GB of host memory")
+    cfg = CONFIGS["C5"]
+    rec = ctx.recycle(cfg.n, cfg.k)
+    for item in system_sequence(cfg, systems=[0, 1]):
+        A = _csr((item["indptr"], item["indices"], item["data"]))
+        M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+        x, xt, res, _ = ctx.solve_dual(M, item["b"], item["bt"], R=rec, k=cfg.k,
+                                       s=cfg.s, tol=cfg.tol, max_itn=cfg.max_itn,
+                                       trunc_tol=cfg.trunc_tol)
+        M.free()
+        assert res["status_name"] in ("ok", "recycle_empty"), res
+        for rhs, op, v in ((item["b"], A, x), (item["bt"], A.conj().T, xt)):
+            assert np.linalg.norm(rhs - op @ v) <= cfg.tol * np.linalg.norm(rhs)
 
 
 def test_full_size_c4_bilinear_conjugate_pair(ctx):
