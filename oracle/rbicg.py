@@ -27,6 +27,8 @@ from .bicg import (inner, breakdown, OK, MAXITER, BREAKDOWN_SERIOUS,
                    BREAKDOWN_SECOND, BREAKDOWN_EPS)
 
 RECYCLE_EMPTY = 4
+STATUS_NAMES = {OK: "ok", MAXITER: "maxiter", BREAKDOWN_SERIOUS: "breakdown_serious",
+                BREAKDOWN_SECOND: "breakdown_second", RECYCLE_EMPTY: "recycle_empty"}
 
 
 @dataclass
@@ -267,10 +269,26 @@ class SolveResult:
 def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
                s=40, tol=1e-8, max_itn=20000, trunc_tol=1e-6,
                xt_redraw=None, update_recycle=True, force_iters=None,
-               keep_pencils=False, breakdown_tol=BREAKDOWN_EPS):
+               keep_pencils=False, breakdown_tol=BREAKDOWN_EPS,
+               variant="standard"):
     """Solve A x = b and A^* x~ = b~ with RBiCG (Algorithm 2)
     using the recycle space (U, Ũ) (may be None/empty: first system), and
-    build the recycle space for the next system (§4)."""
+    build the recycle space for the next system (§4).
+
+    variant="single_reduction" (DESIGN §3 Q30): the same
+    iteration re-associated so that one batch of inner products per iteration
+    yields both β_i and α_{i+1}.  With w_i = A r_i and ω_i = Ĉ^*w_i (exact
+    arithmetic, using z_{i+1} = w_i + β_i z_i, C~^*r_i = 0, C^*r~_i = 0 and the
+    bi-orthogonality of the residuals):
+        ζ_{i+1} = ω_i + β_i ζ_i,   q_{i+1} = (w_i - Cω_i) + β_i q_i,
+        δ_i = (r~_i, w_i - Cω_i),  σ_{i+1} = δ_i - β_i ρ_i / α_i,
+    and the duals with ω~_i = Č^*A^*r~_i, β̄_i.  Every other step (x, r, the
+    stop test, ζ_c, the recycle-space update) is Algorithm 2's.  The
+    second-kind breakdown test (σ_{i+1} = 0, Q3) is taken at the end of
+    iteration i, before its cycle end."""
+    if variant not in ("standard", "single_reduction"):
+        raise ValueError(variant)
+    pipe = variant == "single_reduction"
     n = A.shape[0]
     AH = adjoint(A)
     dt = np.result_type(A.dtype, b.dtype, bt.dtype)
@@ -333,29 +351,52 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
 
     Chat = basis.Ct / basis.d if kc else None
     Ccheck = basis.C / basis.d if kc else None
+
+    def project_w(w, wt):
+        """ω = Ĉ^*w, ω~ = Č^*w~ and the projected w - Cω, w~ - C~ω~."""
+        if not kc:
+            return np.zeros(0, dt), np.zeros(0, dt), w, wt
+        om = Chat.conj().T @ w
+        omt = Ccheck.conj().T @ wt
+        return om, omt, w - basis.C @ om, wt - basis.Ct @ omt
+
+    if pipe and n_iter > 0:
+        # prologue: w_0 = A r_0, σ_1 = δ_0 = (r~_0, (I - CĈ^*) A r_0)
+        w, wt = A @ r, AH @ rt
+        om, omt, wp, wtp = project_w(w, wt)
+        sigma_next = inner(rt, wp)
+        zeta_next, zetat_next = om, omt
+        q = np.zeros(n, dt)
+        qt = np.zeros(n, dt)
     i = 0
     while i < n_iter:
         i += 1
         # Step 5 (PAPER.md:455-473)
         p = r + beta * p
         pt = rt + np.conj(beta) * pt
-        z = A @ p
-        zt = AH @ pt
-        if kc:
-            zeta = Chat.conj().T @ z          # ζ_i = Ĉ^* z_i
-            zetat = Ccheck.conj().T @ zt      # ζ~_i = Č^* z~_i
-            q = z - basis.C @ zeta
-            qt = zt - basis.Ct @ zetat
+        if pipe:
+            zeta, zetat = zeta_next, zetat_next        # ζ_i = ω_{i-1} + β_{i-1}ζ_{i-1}
+            q = wp + beta * q                          # q_i = (w_{i-1} - Cω_{i-1}) + β q_{i-1}
+            qt = wtp + np.conj(beta) * qt
+            sigma = sigma_next                         # σ_i (recurrence)
         else:
-            zeta = np.zeros(0, dt)
-            zetat = np.zeros(0, dt)
-            q, qt = z, zt
-        sigma = inner(pt, q)                  # (p~_i, q_i)  (Q23)
-        if breakdown(sigma, np.linalg.norm(pt), np.linalg.norm(q),
-                     breakdown_tol):
-            status = BREAKDOWN_SECOND
-            i -= 1
-            break
+            z = A @ p
+            zt = AH @ pt
+            if kc:
+                zeta = Chat.conj().T @ z          # ζ_i = Ĉ^* z_i
+                zetat = Ccheck.conj().T @ zt      # ζ~_i = Č^* z~_i
+                q = z - basis.C @ zeta
+                qt = zt - basis.Ct @ zetat
+            else:
+                zeta = np.zeros(0, dt)
+                zetat = np.zeros(0, dt)
+                q, qt = z, zt
+            sigma = inner(pt, q)                  # (p~_i, q_i)  (Q23)
+            if breakdown(sigma, np.linalg.norm(pt), np.linalg.norm(q),
+                         breakdown_tol):
+                status = BREAKDOWN_SECOND
+                i -= 1
+                break
         alpha = rho / sigma
         zc = zc + alpha * zeta
         ztc = ztc + np.conj(alpha) * zetat
@@ -383,6 +424,21 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
         L.beta[i] = beta_new              # Γ~_j's bottom row needs β_{js}
         hist["rho"].append(rho_new)
         serious = breakdown(rho_new, rn, rtn, breakdown_tol)
+        second = False
+        if pipe:
+            # the one batch of inner products of iteration i: ρ_i, the norms,
+            # and δ_i, ω_i, ω~_i from w_i = A r_i, w~_i = A^* r~_i
+            w, wt = A @ r, AH @ rt
+            om, omt, wp, wtp = project_w(w, wt)
+            delta = inner(rt, wp)
+            sigma_next = delta - beta_new * rho_new / alpha
+            zeta_next = om + beta_new * zeta
+            zetat_next = omt + np.conj(beta_new) * zetat
+            second = not converged and not serious and i < n_iter and \
+                breakdown(sigma_next, 1.0, 1.0, breakdown_tol)
+        if second:   # σ_{i+1} = 0: iteration i+1 cannot start
+            status = BREAKDOWN_SECOND
+            break
         # cycle end (full cycles only, Q14)
         if update_recycle and k > 0 and i % s == 0 and (converged or not serious):
             j = i // s

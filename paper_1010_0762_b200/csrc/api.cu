@@ -1314,6 +1314,8 @@ struct Solver {
     worker = std::thread([this, j, fa, fb] {
       try {
         cudaSetDevice(ctx->device);
+        static const int cap = getenv("RBICG_SIDE_SMS") ? atoi(getenv("RBICG_SIDE_SMS")) : 0;
+        g_sm_cap = cap;
         cycle_end(j, fa, fb);
       } catch (Err &e) {
         worker_err = e.code;

@@ -89,6 +89,12 @@ __device__ __forceinline__ zc ldcg(const zc *p) {
 extern std::atomic<int64_t> g_launches;
 inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// SM budget for the grids of the blocked kernels launched by this host thread
+// (0: all SMs).  The overlapped cycle end runs its kernels under a cap so the
+// loop's kernels keep SMs to dispatch onto (RBICG_SIDE_SMS).
+extern thread_local int g_sm_cap;
+inline int sm_budget(int nsm) { return g_sm_cap > 0 && g_sm_cap < nsm ? g_sm_cap : nsm; }
+
 // ---------------------------------------------------------------- errors
 struct Err {
   int code;

@@ -13,6 +13,7 @@
 namespace rbicg {
 
 std::atomic<int64_t> g_launches{0};
+thread_local int g_sm_cap = 0;
 template <typename T> __device__ void resid_leader(DevState<T> *st, const T *s_fin, int k);
 template <typename T> __device__ void init2_leader(const LoopArgs<T> &a, DevState<T> *st, const T *s_fin);
 static const bool g_pdl = getenv("RBICG_PDL") ? atoi(getenv("RBICG_PDL")) != 0 : true;

@@ -447,3 +447,46 @@ def test_convdiff_stencil_values():
     for c in ("C1", "C2", "C3", "C5"):
         cfg = CONFIGS[c]
         assert cfg.nnz == (2 * cfg.d + 1) * cfg.n - 2 * cfg.d * cfg.N ** (cfg.d - 1)
+
+
+# --------------------------------------------------------------- NEXT-1 study variant
+def test_next1_single_reduction_spd_is_cg():
+    """The single-reduction variant (oracle only, DESIGN §6 NEXT-1) on real
+    SPD A with b~ = b, k = 0: its iterates are scipy's CG iterates."""
+    A = csr(spd_sparse(80, seed=4))
+    b = vec(80, 5)
+    iters = []
+    spla.cg(A, b, rtol=1e-30, maxiter=12, callback=lambda xk: iters.append(xk.copy()))
+    for i in (3, 7, 12):
+        r = R.solve_dual(A, b, b, k=0, s=20, tol=1e-10, max_itn=20, force_iters=i,
+                         variant="single_reduction")
+        np.testing.assert_allclose(r.x, iters[i - 1], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_next1_single_reduction_matches_algorithm2(cplx):
+    """With a recycle space (k = 4 requested from a first solve of a
+    diagonally shifted random sparse matrix) the re-associated recurrences
+    reproduce Algorithm 2 as written: the same iteration count, σ_i = (p~_i,
+    q_i) histories to 1e-8 (of the largest |σ|), the α_i of the first 12
+    iterations to 1e-8, the same solution, the dense-LU solution
+    (P4).  (On near-breakdown problems the recurrence σ_{i+1} = δ_i -
+    β_iρ_i/α_i cancels and the variants part -- the DESIGN §6 study.)"""
+    n = 300
+    As = csr(random_sparse(n, 0.03, seed=5, shift=3.0, complex_=cplx))
+    first = R.solve_dual(As, vec(n, 1, cplx), vec(n, 2, cplx), k=4, s=12, tol=1e-12,
+                         max_itn=300, trunc_tol=1e-8)
+    assert first.basis_out.k >= 2
+    kw = dict(U=first.basis_out.U, Ut=first.basis_out.Ut, k=4, s=12, tol=1e-12,
+              max_itn=300, trunc_tol=1e-8)
+    b2, bt2 = vec(n, 3, cplx), vec(n, 4, cplx)
+    ref = R.solve_dual(As, b2, bt2, **kw)
+    got = R.solve_dual(As, b2, bt2, variant="single_reduction", **kw)
+    assert got.basis_in.k >= 2
+    assert got.iterations == ref.iterations and got.status == ref.status
+    sg, sr = np.array(got.hist["sigma"]), np.array(ref.hist["sigma"])
+    np.testing.assert_allclose(sg, sr, rtol=1e-8, atol=1e-10 * np.abs(sr).max())
+    np.testing.assert_allclose(got.hist["alpha"][:12], ref.hist["alpha"][:12], rtol=1e-8)
+    np.testing.assert_allclose(got.x, ref.x, rtol=1e-8)
+    xd = np.linalg.solve(As.toarray(), b2)
+    assert np.linalg.norm(got.x - xd) <= 1e-9 * np.linalg.norm(xd)
