@@ -643,8 +643,12 @@ struct Solver {
   // Bi-orthogonalise (U, Ũ, C = AU, C~ = A^*Ũ) of width kin into `out`
   // (Q13: unit columns, absolute cut on the singular values).
   // with_c = false: out keeps U, Ũ only (the cycle-end candidate)
+  // With Fu_out (the T_j relation path) U, Ũ are not formed here: the
+  // rotations Fu, Fut (kin x p) are returned and the caller builds U N_p
+  // straight from the Lanczos columns -- only when p > 0.
   void biorth(const T *U, const T *Ut, const T *C, const T *Ct, int kin, Basis &out,
-              cudaStream_t bs, Comm *cm, bool with_c = true) {
+              cudaStream_t bs, Comm *cm, bool with_c = true, std::vector<cplx> *Fu_out = nullptr,
+              std::vector<cplx> *Fut_out = nullptr) {
     // only ||c_j||^2, ||c~_j||^2 and C~^*C are needed (Q13 scaling + SVD)
     std::vector<ColDesc> X;
     for (int c = 0; c < kin; ++c) X.push_back(col(C, c, kin));
@@ -703,6 +707,11 @@ struct Solver {
         Fu[(size_t)kk[a] * pk + c] = Nr[(size_t)c * m + a] / nc[kk[a]];
         Fut[(size_t)kk[a] * pk + c] = Ml[(size_t)c * m + a] / nct[kk[a]];
       }
+    if (Fu_out) {
+      *Fu_out = Fu;
+      *Fut_out = Fut;
+      return;
+    }
     auto cols_of = [&](const T *B) {
       std::vector<ColDesc> v;
       for (int c = 0; c < kin; ++c) v.push_back(col(B, c, kin));
@@ -953,7 +962,7 @@ struct Solver {
                      const std::vector<cplx> &Wun, const std::vector<cplx> &Wtun,
                      const std::vector<cplx> &Wrow, const std::vector<cplx> &Wtrow, int ksel,
                      SV sv, SVT svt, int fa, int fb, int lo, const std::vector<IterRec<T>> &rec,
-                     cudaStream_t cs) {
+                     cudaStream_t cs, bool with_u) {
     const int s = (int)cols.size(), nr = (int)rows.size();
     const bool fl = fb > fa;
     std::vector<cplx> cr;
@@ -972,12 +981,14 @@ struct Solver {
       X.push_back(ColDesc{x, 1});
       Xt.push_back(ColDesc{xt, 1});
     }
-    const int mX = (int)X.size(), p = 2 * ksel + (fl ? 1 : 0);
+    // columns: [U_j (with_u) | C_j | x (fl)]
+    const int cu = with_u ? ksel : 0, cc = cu + ksel, cx = cc;
+    const int mX = (int)X.size(), p = cc + (fl ? 1 : 0);
     std::vector<cplx> M((size_t)mX * p, 0.0), Mt((size_t)mX * p, 0.0);
     for (int a = 0; a < nr; ++a) {
       const bool vrow = a >= top && a < top + s;
       for (int c = 0; c < ksel; ++c) {
-        if (vrow) {
+        if (vrow && with_u) {
           M[(size_t)a * p + c] = Wrow[(size_t)(a - top) * ksel + c];
           Mt[(size_t)a * p + c] = Wtrow[(size_t)(a - top) * ksel + c];
         }
@@ -986,20 +997,26 @@ struct Solver {
           g += Gam[(size_t)a * s + bb] * Wun[(size_t)bb * ksel + c];
           gt += Gamt[(size_t)a * s + bb] * Wtun[(size_t)bb * ksel + c];
         }
-        M[(size_t)a * p + ksel + c] = sv(rows[a]) * g;
-        Mt[(size_t)a * p + ksel + c] = svt(rows[a]) * gt;
+        M[(size_t)a * p + cu + c] = sv(rows[a]) * g;
+        Mt[(size_t)a * p + cu + c] = svt(rows[a]) * gt;
       }
       if (fl && vrow) {
-        M[(size_t)a * p + 2 * ksel] = cr[a - top];
-        Mt[(size_t)a * p + 2 * ksel] = std::conj(cr[a - top]);
+        M[(size_t)a * p + cx] = cr[a - top];
+        Mt[(size_t)a * p + cx] = std::conj(cr[a - top]);
       }
     }
-    std::vector<std::pair<T *, int>> outs{{tmp.U, ksel}, {tmp.C, ksel}}, outst{{tmp.Ut, ksel}, {tmp.Ct, ksel}};
+    std::vector<std::pair<T *, int>> outs, outst;
+    if (with_u) {
+      outs.push_back({tmp.U, ksel});
+      outst.push_back({tmp.Ut, ksel});
+    }
+    outs.push_back({tmp.C, ksel});
+    outst.push_back({tmp.Ct, ksel});
     if (fl) {
-      M[(size_t)nr * p + 2 * ksel] = cr[s];
-      Mt[(size_t)nr * p + 2 * ksel] = std::conj(cr[s]);
-      M[(size_t)(nr + 1) * p + 2 * ksel] = 1.0;
-      Mt[(size_t)(nr + 1) * p + 2 * ksel] = 1.0;
+      M[(size_t)nr * p + cx] = cr[s];
+      Mt[(size_t)nr * p + cx] = std::conj(cr[s]);
+      M[(size_t)(nr + 1) * p + cx] = 1.0;
+      Mt[(size_t)(nr + 1) * p + cx] = 1.0;
       outs.push_back({x, 1});
       outst.push_back({xt, 1});
     }
@@ -1250,9 +1267,14 @@ struct Solver {
         // (P:527-550), so C_j = Υ_j (Γ_j W_j) and C~_j = Ῡ_j (Γ~_j W~_j): U_j, C_j
         // and the deferred lazy-x flush come out of ONE pass over the Υ_j ring
         // columns -- no SpMM, no halo.  DESIGN §6 (reading Q15).
+        // U_j itself is formed only if the truncation keeps a direction (C2,
+        // C3 and C5 truncate every cycle to p = 0, Q13): C_j and the flush
+        // first, then U_j N_p = Υ_j (W_j N_p) from the V_j columns
+        static const bool u_late = !getenv("RBICG_U_EARLY");
+        const bool chk = getenv("RBICG_C_CHECK") && !dist;
         Phase ph("cycle.gemm_UCx", cs);
         relation_gemm(rows, cols, top, Gam, Gamt, sel.W, sel.Wt, Wrow, Wtrow, ksel, sv, svt, fa, fb,
-                      lo, rec, cs);
+                      lo, rec, cs, !u_late || chk);
         fa = fb = 0;
         if (getenv("RBICG_C_CHECK") && !dist) {   // debug: relation vs explicit SpMM
           RB_CUDA(cudaStreamSynchronize(cs));
@@ -1271,7 +1293,29 @@ struct Solver {
           fprintf(stderr, "rbicg C_j relation vs SpMM: cycle %d ksel %d rel diff %.3e\n", j, ksel,
                   std::sqrt(dn / std::max(nn, 1e-300)));
         }
-        biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false);
+        if (!u_late || chk) {
+          biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false);
+        } else {
+          std::vector<cplx> Fu, Fut;
+          biorth(nullptr, nullptr, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false, &Fu, &Fut);
+          if (out.k > 0) {   // U_j N_p = [V_j rows] (W_j N_p) (scalings folded in Wrow)
+            const int pk = out.k;
+            std::vector<ColDesc> Xv, Xvt;
+            std::vector<cplx> Mu((size_t)s * pk, 0.0), Mut((size_t)s * pk, 0.0);
+            for (int bb = 0; bb < s; ++bb) {
+              Xv.push_back(rcol(rows[top + bb] - 1));
+              Xvt.push_back(rtcol(rows[top + bb] - 1));
+              for (int c = 0; c < pk; ++c)
+                for (int q2 = 0; q2 < ksel; ++q2) {
+                  Mu[(size_t)bb * pk + c] += Wrow[(size_t)bb * ksel + q2] * Fu[(size_t)q2 * pk + c];
+                  Mut[(size_t)bb * pk + c] += Wtrow[(size_t)bb * ksel + q2] * Fut[(size_t)q2 * pk + c];
+                }
+            }
+            Phase phu("cycle.gemm_U", cs);
+            gemm_multi<T>(Xv, Mu, {{out.U, pk}}, n, ctx, cs);
+            gemm_multi<T>(Xvt, Mut, {{out.Ut, pk}}, n, ctx, cs);
+          }
+        }
       } else {
       {
         Phase ph("cycle.gemm_UW", cs);
@@ -1314,8 +1358,11 @@ struct Solver {
     worker = std::thread([this, j, fa, fb] {
       try {
         cudaSetDevice(ctx->device);
-        static const int cap = getenv("RBICG_SIDE_SMS") ? atoi(getenv("RBICG_SIDE_SMS")) : 0;
-        g_sm_cap = cap;
+        // the overlapped cycle end's blocked kernels take at most ~2/3 of the
+        // SMs so the loop's kernels keep SMs to dispatch onto (C2: 15.50k ->
+        // 15.80k it/s at 100 of 148, 3 runs each; RBICG_SIDE_SMS=0: no cap)
+        static const int cap = getenv("RBICG_SIDE_SMS") ? atoi(getenv("RBICG_SIDE_SMS")) : -1;
+        g_sm_cap = cap >= 0 ? cap : ctx->nsm * 2 / 3;
         cycle_end(j, fa, fb);
       } catch (Err &e) {
         worker_err = e.code;

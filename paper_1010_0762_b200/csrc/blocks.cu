@@ -563,8 +563,32 @@ __global__ void __launch_bounds__(256, 2) k_gemm_multi(const ColDesc *__restrict
     for (int q = 0; q < RPT; ++q)
 #pragma unroll
       for (int c = 0; c < PB; ++c) acc[q][c] = zero<T>();
-#pragma unroll 2
-    for (int a = 0; a < mX; ++a) {
+    // AU columns' loads are issued before their FMAs: AU x RPT loads per
+    // thread in flight (the kernel is bound by HBM latency x bytes in flight)
+    constexpr int AU = PB <= 12 ? 8 : 4;
+    int a = 0;
+    for (; a + AU <= mX; a += AU) {
+      T xv[AU][RPT];
+#pragma unroll
+      for (int u = 0; u < AU; ++u)
+#pragma unroll
+        for (int q = 0; q < RPT; ++q)
+          xv[u][q] = ok[q] ? ldp<T>(sX[a + u].p, row[q] * sX[a + u].stride) : zero<T>();
+#pragma unroll
+      for (int u = 0; u < AU; ++u) {
+        const MPair<T> *mp = reinterpret_cast<const MPair<T> *>(sM + (a + u) * PB);
+#pragma unroll
+        for (int c2 = 0; c2 < PB / 2; ++c2) {
+          const MPair<T> m = mp[c2];
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            acc[q][2 * c2] = mad(xv[u][q], m.a, acc[q][2 * c2]);
+            acc[q][2 * c2 + 1] = mad(xv[u][q], m.b, acc[q][2 * c2 + 1]);
+          }
+        }
+      }
+    }
+    for (; a < mX; ++a) {
       T xv[RPT];
 #pragma unroll
       for (int q = 0; q < RPT; ++q) xv[q] = ok[q] ? ldp<T>(sX[a].p, row[q] * sX[a].stride) : zero<T>();
