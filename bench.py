@@ -115,13 +115,14 @@ def workload_name(cfg):
             f"tol={cfg.tol}, trunc_tol={cfg.trunc_tol}")
 
 
-def alg_bytes(cfg_n, nnz, k, w=8, lazy_x=True):
+def alg_bytes(cfg_n, nnz, k, w=8, lazy_x=True, shared_cols=False):
     """Algorithmic HBM bytes per launch of the two hot kernels:
     pass 1 streams A and A^* (CSR-equivalent: values + int32 column indices +
-    row pointers), C and C~ once, reads r, p, r~, p~ and writes p, p~, z, z~;
+    row pointers; one column array for both when A is structurally symmetric),
+    C and C~ once, reads r, p, r~, p~ and writes p, p~, z, z~;
     pass 2 reads C, C~, z, z~, r, r~ and writes r, r~ (with lazy x; eager x
     adds reads of x, x~, p, p~ and writes of x, x~)."""
-    mat = 2 * (nnz * (w + 4) + 4 * (cfg_n + 1))
+    mat = 2 * (nnz * (w + 4) + 4 * (cfg_n + 1)) - (4 * nnz if shared_cols else 0)
     p1 = mat + 2 * k * cfg_n * w + 8 * cfg_n * w
     p2 = 2 * k * cfg_n * w + (6 if lazy_x else 12) * cfg_n * w
     return p1, p2
@@ -255,7 +256,7 @@ def run_gpu(args, rank, world):
         kq = kctx.time_kernels(A, Rq, k=cfg.k, s=cfg.s, iters=args.kernel_iters,
                                trunc_tol=1e-300)
         wq = 16 if cfg.complex else 8
-        q1, q2 = alg_bytes(cfg.n, cfg.nnz, kq["k"], wq, kq["lazy_x"])
+        q1, q2 = alg_bytes(cfg.n, cfg.nnz, kq["k"], wq, kq["lazy_x"], kq["shared_cols"])
         okq = kq["graph_each_done_flag"] == 0 and kq["pass1_graph_ms"] > 0
         m1 = kq["pass1_graph_ms"] if okq else kq["pass1_ms"]
         m2 = kq["pass2_graph_ms"] if okq else kq["pass2_ms"]
@@ -269,7 +270,7 @@ def run_gpu(args, rank, world):
                  "space": "seeded N(0,1) U, U~ (%d columns), truncation off" % cfg.k}
     A.free()
     w = 16 if cfg.complex else 8
-    p1, p2 = alg_bytes(cfg.n, cfg.nnz, kt["k"], w, kt["lazy_x"])
+    p1, p2 = alg_bytes(cfg.n, cfg.nnz, kt["k"], w, kt["lazy_x"], kt["shared_cols"])
     peak, peak_kind = hbm_peak()
     # kernel durations: each kernel as back-to-back launches in one CUDA graph
     # (CUDA events around the graph on the library stream) -- its duration
@@ -373,7 +374,7 @@ def run_gpu(args, rank, world):
                      "pass1_ms": k1, "pass2_ms": k2,
                      "pass1_event_ms": kt["pass1_ms"], "pass2_event_ms": kt["pass2_ms"],
                      "loop_graph_iter_ms": kt["graph_iter_ms"],
-                     "k_active": kt["k"], "lazy_x": kt["lazy_x"],
+                     "k_active": kt["k"], "lazy_x": kt["lazy_x"], "shared_cols": kt["shared_cols"],
                      "tma_pass1": kt["tma_pass1"],
                      "iter_GBps": (p1 + p2) / (kt["graph_iter_ms"] * 1e-3) / 1e9,
                      "k_probe": probe},

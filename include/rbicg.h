@@ -194,7 +194,9 @@ int rbicg_dbg_project(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
  * did exactly `iters` full iterations, [10] ms per launch of the SpMV-pair
  * kernel alone as `iters` back-to-back launches in one graph (its duration
  * inside the solver's graph, without host launch gaps), [11] the same for the
- * update kernel, [12] 0 if those launches all did full work. */
+ * update kernel, [12] 0 if those launches all did full work, [13] 1 if A and
+ * A^* share one SELL column array (structurally symmetric A: pass 1 streams
+ * one pattern and two value arrays).  ms must hold 14 doubles. */
 int rbicg_dbg_time_kernels(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
                            const rbicg_opts *opts, int iters, double *ms);
 

@@ -582,6 +582,7 @@ struct Solver {
     la.pf = envi("RBICG_PF", 0);
     la.abl = 0;
     la.pass2_tma = getenv("RBICG_NO_TMA2") ? 0 : 1;
+    la.shared_cols = M->A.cols == M->AH.cols ? 1 : 0;
     const bool tma_ok = !getenv("RBICG_NO_TMA");
     if (la.split) {
       const double st_h = 2.0 * la.tile_max_h * (4 + sizeof(T)) + (la.stage_v ? 4.0 * TRH * sizeof(T) : 0.0);
@@ -1877,7 +1878,7 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
     res->t_refresh_ms = S.t_refresh;
     res->t_total_ms = now_ms() - t_start;
     const double w = sizeof(T), kk = S.cur.k;
-    const double mat = 2.0 * (A->nnz * (w + 4) + 4.0 * (n + 1));
+    const double mat = 2.0 * (A->nnz * (w + 4) + 4.0 * (n + 1)) - (S.la.shared_cols ? 4.0 * A->nnz : 0.0);
     res->alg_bytes = fin.iter * (mat + 4.0 * kk * n * w + 20.0 * n * w);
     res->kernel_launches = (int32_t)(g_launches.load() - S.launches0);
   }
@@ -2195,6 +2196,7 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
   ms[10] = g1r.first;
   ms[11] = g2r.first;
   ms[12] = (g1r.second == 0 && g2r.second == 0) ? 0.0 : 1.0;
+  ms[13] = S.la.shared_cols ? 1.0 : 0.0;
   for (auto &e : ev) cudaEventDestroy(e);
   ms[0] = t1 / std::max(iters, 1);
   ms[1] = t2 / std::max(iters, 1);

@@ -429,7 +429,8 @@ __device__ __forceinline__ void p1_issue(const LoopArgs<T> &a, unsigned char *st
   const int64_t oA = a.A.sptr[s0], eA = a.A.sptr[s1];
   const int64_t oH = a.AH.sptr[s0], eH = a.AH.sptr[s1];
   const uint32_t nA = (uint32_t)(eA - oA), nH = (uint32_t)(eH - oH);
-  mbar_expect_tx(bar, (nA + nH) * (4u + (uint32_t)sizeof(T)));
+  const uint32_t nHc = a.shared_cols ? 0u : nH;   // A^*'s columns: A's (structurally symmetric)
+  mbar_expect_tx(bar, (nA + nH) * (uint32_t)sizeof(T) + (nA + nHc) * 4u);
   if (a.l2ef) {   // the matrix pair is streamed once per pass: evict it first
     const uint64_t pol = policy_evict_first();
     if (nA) {
@@ -437,7 +438,7 @@ __device__ __forceinline__ void p1_issue(const LoopArgs<T> &a, unsigned char *st
       tma_load_1d_hint(vA, reinterpret_cast<const T *>(a.A.vals) + oA, nA * (uint32_t)sizeof(T), bar, pol);
     }
     if (nH) {
-      tma_load_1d_hint(cH, a.AH.cols + oH, nH * 4u, bar, pol);
+      if (nHc) tma_load_1d_hint(cH, a.AH.cols + oH, nH * 4u, bar, pol);
       tma_load_1d_hint(vH, reinterpret_cast<const T *>(a.AH.vals) + oH, nH * (uint32_t)sizeof(T), bar, pol);
     }
     return;
@@ -447,7 +448,7 @@ __device__ __forceinline__ void p1_issue(const LoopArgs<T> &a, unsigned char *st
     tma_load_1d(vA, reinterpret_cast<const T *>(a.A.vals) + oA, nA * (uint32_t)sizeof(T), bar);
   }
   if (nH) {
-    tma_load_1d(cH, a.AH.cols + oH, nH * 4u, bar);
+    if (nHc) tma_load_1d(cH, a.AH.cols + oH, nH * 4u, bar);
     tma_load_1d(vH, reinterpret_cast<const T *>(a.AH.vals) + oH, nH * (uint32_t)sizeof(T), bar);
   }
 }
@@ -525,8 +526,8 @@ __device__ __forceinline__ void p1_tiles(const LoopArgs<T> &a, unsigned char *ds
       const int si = nst == 2 ? (i & 1) : 0;
       const unsigned char *base = dsm + si * stage_bytes;
       const int32_t *scA = reinterpret_cast<const int32_t *>(base);
-      const int32_t *scH = scA + TM;
-      const T *svA = reinterpret_cast<const T *>(scH + TM);
+      const int32_t *scH = a.shared_cols ? scA : scA + TM;
+      const T *svA = reinterpret_cast<const T *>(scA + 2 * TM);
       const T *svH = svA + TM;
       // slice geometry (global loads overlap the bulk copy)
       const int64_t sl = (row0 >> 5) + (tid >> 5);
@@ -637,14 +638,15 @@ __device__ __forceinline__ void p1s_issue(const LoopArgs<T> &a, unsigned char *s
   const int64_t oA = a.A.sptr[s0], eA = a.A.sptr[s1];
   const int64_t oH = a.AH.sptr[s0], eH = a.AH.sptr[s1];
   const uint32_t nA = (uint32_t)(eA - oA), nH = (uint32_t)(eH - oH);
-  mbar_expect_tx(bar, (nA + nH) * (4u + (uint32_t)sizeof(T)));
+  const uint32_t nHc = a.shared_cols ? 0u : nH;
+  mbar_expect_tx(bar, (nA + nH) * (uint32_t)sizeof(T) + (nA + nHc) * 4u);
   const uint64_t pol = policy_evict_first();   // streamed once per pass
   if (nA) {
     tma_load_1d_hint(cA, a.A.cols + oA, nA * 4u, bar, pol);
     tma_load_1d_hint(vA, reinterpret_cast<const T *>(a.A.vals) + oA, nA * (uint32_t)sizeof(T), bar, pol);
   }
   if (nH) {
-    tma_load_1d_hint(cH, a.AH.cols + oH, nH * 4u, bar, pol);
+    if (nHc) tma_load_1d_hint(cH, a.AH.cols + oH, nH * 4u, bar, pol);
     tma_load_1d_hint(vH, reinterpret_cast<const T *>(a.AH.vals) + oH, nH * (uint32_t)sizeof(T), bar, pol);
   }
 }
@@ -736,7 +738,7 @@ __device__ __forceinline__ void p1_tiles_split(const LoopArgs<T> &a, unsigned ch
     }
     const int si = nst == 2 ? (i & 1) : 0;
     const unsigned char *base = dsm + si * stage_bytes;
-    const int32_t *sc0 = reinterpret_cast<const int32_t *>(base) + (side ? TM : 0);
+    const int32_t *sc0 = reinterpret_cast<const int32_t *>(base) + (side && !a.shared_cols ? TM : 0);
     const T *sv0 = reinterpret_cast<const T *>(base + (size_t)2 * TM * 4) + (side ? TM : 0);
     const int64_t slc = min((row0 >> 5) + (lr >> 5), ns - 1);
     const int64_t bM = M.sptr[tile * (TRH / 32)];

@@ -27,6 +27,8 @@ struct DevMat {
   int64_t *sptr = nullptr;  // nslices + 1 element offsets (multiples of 32)
   int32_t *cols = nullptr;
   void *vals = nullptr;
+  int cols_shared = 0;      // cols aliases the other matrix's (A^* of a structurally
+                            // symmetric A: same SELL column array, build_t)
 };
 
 // Device-resident iteration state (one per solve; scalars of Algorithm 2).
@@ -72,6 +74,7 @@ struct LoopArgs {
   int pf;                  // pass 1 prefetches the next tile's vector rows into L2
   int abl;                 // timing ablations (RBICG_ABL, never set in a solve): 1 no gathers
   int pass2_tma;           // pass 2 streams its tiles through smem via TMA
+  int shared_cols;         // A and A^* share one SELL column array (structurally symmetric A)
   int lazy_x;              // x, x~ rebuilt per segment from the Lanczos ring
   T *pseg[2], *ptseg[2];   // p_a, p~_a at the start of the open segment, by segment parity
   int cyc;                 // cycle length s (segment parity = (seg_start / s) & 1)

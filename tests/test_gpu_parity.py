@@ -558,3 +558,26 @@ def test_irka_gpu_matches_oracle(ctx):
         g, dg = np.vdot(c, y), -np.vdot(c, np.linalg.solve(M, y))
         gr, dgr = OI.transfer(got.Ar, got.Er, got.br, got.cr, si)
         assert abs(gr - g) <= 1e-8 * abs(g) and abs(dgr - dg) <= 1e-6 * abs(dg)
+
+
+def test_shared_column_array_bitwise(ctx, monkeypatch):
+    """A structurally symmetric A (the conv-diff stencils) keeps one SELL
+    column array for A and A^* (matrix.cu share_cols): the solve must be
+    bitwise identical to the one with two column arrays."""
+    cfg = CONFIGS["C3"].scaled(20, systems=1)
+    item = next(system_sequence(cfg))
+    outs = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("RBICG_NO_SHARED_COLS", "1")
+        M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+        kt = ctx.time_kernels(M, None, k=0, s=cfg.s, iters=3)
+        assert kt["shared_cols"] == (not off)
+        rec = ctx.recycle(cfg.n, cfg.k)
+        x, xt, res, _ = ctx.solve_dual(M, item["b"], item["bt"], R=rec, k=cfg.k, s=cfg.s,
+                                       tol=cfg.tol, max_itn=cfg.max_itn,
+                                       trunc_tol=cfg.trunc_tol)
+        outs.append((x, xt, res["iterations"]))
+        M.free()
+    assert outs[0][2] == outs[1][2]
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
