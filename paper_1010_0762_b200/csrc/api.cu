@@ -1760,8 +1760,9 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
     // stream (same ring columns as the U_j GEMM); otherwise it runs here,
     // after any flush still in flight
     const int seg_a = S.hst->seg_start;
-    const bool defer = S.lazy_x && S.async_cycle && will_cycle && S.hst->done == 2 &&
-                       seg_a == it - opts->s;
+    // (in stream order too: the cycle end then runs at once, and its GEMM
+    // still saves the flush's own pass over the ring -- C5)
+    const bool defer = S.lazy_x && will_cycle && S.hst->done == 2 && seg_a == it - opts->s;
     const double tf0 = now_ms();
     if (defer) {
       S.hst->seg_start = it;

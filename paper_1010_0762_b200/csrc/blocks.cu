@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_multi(const ColDesc *__restrict
       for (int c = 0; c < PB; ++c) acc[q][c] = zero<T>();
     // AU columns' loads are issued before their FMAs: AU x RPT loads per
     // thread in flight (the kernel is bound by HBM latency x bytes in flight)
-    constexpr int AU = PB <= 12 ? 8 : 4;
+    constexpr int AU = PB <= 12 ? 8 : 4;   // (PB 24 with 1 row and 8 ahead: C5 12.4 vs 11.3 ms)
     int a = 0;
     for (; a + AU <= mX; a += AU) {
       T xv[AU][RPT];
