@@ -275,7 +275,7 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
     using the recycle space (U, Ũ) (may be None/empty: first system), and
     build the recycle space for the next system (§4).
 
-    variant="single_reduction" (DESIGN §3 Q30): the same
+    variant="single_reduction": the same
     iteration re-associated so that one batch of inner products per iteration
     yields both β_i and α_{i+1}.  With w_i = A r_i and ω_i = Ĉ^*w_i (exact
     arithmetic, using z_{i+1} = w_i + β_i z_i, C~^*r_i = 0, C^*r~_i = 0 and the
@@ -285,10 +285,21 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
     and the duals with ω~_i = Č^*A^*r~_i, β̄_i.  Every other step (x, r, the
     stop test, ζ_c, the recycle-space update) is Algorithm 2's.  The
     second-kind breakdown test (σ_{i+1} = 0, Q3) is taken at the end of
-    iteration i, before its cycle end."""
-    if variant not in ("standard", "single_reduction"):
+    iteration i, before its cycle end.
+
+    variant="lookahead" (the fused single-kernel iteration of the
+    GPU path when no recycle space is active): Algorithm 2 except that β_i is
+    formed from the one-step expansion of ρ_i = (r~_i, r_i) with r_i = r_{i-1}
+    - α_i q_i,
+        ρ_i ≈ ρ_{i-1} - α_i (r~_{i-1}, q_i) - α_i (q~_i, r_{i-1}) + α_i² (q~_i, q_i),
+    whose inner products belong to iteration i's first reduction; ρ_i itself
+    (for α_{i+1}, the breakdown test) and the norms stay exact -- on the GPU
+    they complete one kernel later, which does not change the arithmetic.
+    """
+    if variant not in ("standard", "single_reduction", "lookahead"):
         raise ValueError(variant)
     pipe = variant == "single_reduction"
+    look = variant == "lookahead"
     n = A.shape[0]
     AH = adjoint(A)
     dt = np.result_type(A.dtype, b.dtype, bt.dtype)
@@ -402,6 +413,9 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
         ztc = ztc + np.conj(alpha) * zetat
         x = x + alpha * p
         xt = xt + np.conj(alpha) * pt
+        if look:   # ρ_i from iteration i's first reduction (before the update)
+            rho_ext = rho - alpha * inner(rt, q) - alpha * inner(qt, r) \
+                + alpha * alpha * inner(qt, q)
         r = r - alpha * q
         rt = rt - np.conj(alpha) * qt
         it = i
@@ -420,6 +434,8 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
         # loop stops at a cycle boundary
         rho_new = inner(rt, r)
         beta_new = rho_new / rho          # β_i
+        if look:
+            beta_new = rho_ext / rho
         L.rho[i] = rho_new
         L.beta[i] = beta_new              # Γ~_j's bottom row needs β_{js}
         hist["rho"].append(rho_new)

@@ -450,21 +450,24 @@ def test_convdiff_stencil_values():
 
 
 # --------------------------------------------------------------- NEXT-1 study variant
-def test_next1_single_reduction_spd_is_cg():
-    """The single-reduction variant (oracle only, DESIGN §6 NEXT-1) on real
-    SPD A with b~ = b, k = 0: its iterates are scipy's CG iterates."""
+@pytest.mark.parametrize("variant", ["single_reduction", "lookahead"])
+def test_next1_single_reduction_spd_is_cg(variant):
+    """The re-associated variants (DESIGN §6: single reduction, oracle only;
+    lookahead ρ, the fused GPU iteration) on real SPD A with b~ = b, k = 0:
+    their iterates are scipy's CG iterates."""
     A = csr(spd_sparse(80, seed=4))
     b = vec(80, 5)
     iters = []
     spla.cg(A, b, rtol=1e-30, maxiter=12, callback=lambda xk: iters.append(xk.copy()))
     for i in (3, 7, 12):
         r = R.solve_dual(A, b, b, k=0, s=20, tol=1e-10, max_itn=20, force_iters=i,
-                         variant="single_reduction")
+                         variant=variant)
         np.testing.assert_allclose(r.x, iters[i - 1], rtol=1e-9, atol=1e-12)
 
 
+@pytest.mark.parametrize("variant", ["single_reduction", "lookahead"])
 @pytest.mark.parametrize("cplx", [False, True])
-def test_next1_single_reduction_matches_algorithm2(cplx):
+def test_next1_single_reduction_matches_algorithm2(cplx, variant):
     """With a recycle space (k = 4 requested from a first solve of a
     diagonally shifted random sparse matrix) the re-associated recurrences
     reproduce Algorithm 2 as written: the same iteration count, σ_i = (p~_i,
@@ -481,7 +484,7 @@ def test_next1_single_reduction_matches_algorithm2(cplx):
               max_itn=300, trunc_tol=1e-8)
     b2, bt2 = vec(n, 3, cplx), vec(n, 4, cplx)
     ref = R.solve_dual(As, b2, bt2, **kw)
-    got = R.solve_dual(As, b2, bt2, variant="single_reduction", **kw)
+    got = R.solve_dual(As, b2, bt2, variant=variant, **kw)
     assert got.basis_in.k >= 2
     assert got.iterations == ref.iterations and got.status == ref.status
     sg, sr = np.array(got.hist["sigma"]), np.array(ref.hist["sigma"])
