@@ -128,6 +128,14 @@ def alg_bytes(cfg_n, nnz, k, w=8, lazy_x=True, shared_cols=False):
     return p1, p2
 
 
+def alg_bytes_fused(cfg_n, nnz, w=8, shared_cols=False):
+    """Algorithmic HBM bytes per launch of the fused iteration kernel (k = 0,
+    DESIGN.md §6): the A, A^* streams as in pass 1, reads r_{i-2}, z_{i-1},
+    p_{i-1} and writes r_{i-1}, z_i, p_i on both sides (12 n-vectors)."""
+    mat = 2 * (nnz * (w + 4) + 4 * (cfg_n + 1)) - (4 * nnz if shared_cols else 0)
+    return mat + 12 * cfg_n * w
+
+
 def run_gpu(args, rank, world):
     import torch
     from paper_1010_0762_b200 import api
@@ -280,6 +288,12 @@ def run_gpu(args, rank, world):
     k1 = kt["pass1_graph_ms"] if ok else kt["pass1_ms"]
     k2 = kt["pass2_graph_ms"] if ok else kt["pass2_ms"]
     dom_bytes, dom_ms, dom = (p1, k1, "pass1") if k1 >= k2 else (p2, k2, "pass2")
+    # the solver's loop runs the fused iteration kernel while no recycle space
+    # is active (every timed system of C2, C3, C5): that kernel is the dominant one
+    fused = kt["k"] == 0 and kt["fused_ms"] > 0 and kt["fused_done_flag"] == 0
+    pf = alg_bytes_fused(cfg.n, cfg.nnz, w, kt["shared_cols"])
+    if fused:
+        dom_bytes, dom_ms, dom = pf, kt["fused_ms"], "fused"
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = None   # ncu DRAM bytes per launch, recorded for the config it was captured on
     try:
@@ -377,6 +391,8 @@ def run_gpu(args, rank, world):
                      "k_active": kt["k"], "lazy_x": kt["lazy_x"], "shared_cols": kt["shared_cols"],
                      "tma_pass1": kt["tma_pass1"],
                      "iter_GBps": (p1 + p2) / (kt["graph_iter_ms"] * 1e-3) / 1e9,
+                     "fused_ms": kt["fused_ms"] if kt["fused_ms"] > 0 else None,
+                     "fused_alg_bytes": pf,
                      "k_probe": probe},
         "e2e": e2e,
         "gpu_launches": int(launches),

@@ -196,7 +196,10 @@ int rbicg_dbg_project(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
  * inside the solver's graph, without host launch gaps), [11] the same for the
  * update kernel, [12] 0 if those launches all did full work, [13] 1 if A and
  * A^* share one SELL column array (structurally symmetric A: pass 1 streams
- * one pattern and two value arrays).  ms must hold 14 doubles. */
+ * one pattern and two value arrays), [14] ms per launch of the fused
+ * iteration kernel (one kernel per iteration while no recycle space is
+ * active; -1 when that form does not apply) as `iters` launches in one graph,
+ * [15] 0 if those launches all did full work.  ms must hold 16 doubles. */
 int rbicg_dbg_time_kernels(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
                            const rbicg_opts *opts, int iters, double *ms);
 

@@ -355,6 +355,7 @@ struct Solver {
   }
   std::vector<void *> owned;
   T *rring = nullptr, *rtring = nullptr, *p[2] = {}, *pt[2] = {}, *z = nullptr, *zt = nullptr;
+  T *z2 = nullptr, *zt2 = nullptr;   // fused iteration: z_i by parity
   T *x = nullptr, *xt = nullptr, *b = nullptr, *bt = nullptr, *xo = nullptr, *xto = nullptr;
   T *psegs[2] = {}, *ptsegs[2] = {};
   T *pring = nullptr, *ptring = nullptr;
@@ -520,6 +521,10 @@ struct Solver {
     tmark("ring+p");
     z = alloc(n);
     zt = alloc(n);
+    if (k_basis == 0 && !dist) {   // fused iteration: z_i by parity (z, z2)
+      z2 = alloc(n);
+      zt2 = alloc(n);
+    }
     x = alloc(nx);
     xt = alloc(nx);
     b = alloc(n);
@@ -616,6 +621,10 @@ struct Solver {
     la.pt[1] = pt[1];
     la.z = z;
     la.zt = zt;
+    la.zb[0] = z;
+    la.zb[1] = z2;
+    la.ztb[0] = zt;
+    la.ztb[1] = zt2;
     la.x = x;
     la.xt = xt;
     la.C = cur.C;
@@ -859,6 +868,13 @@ struct Solver {
   // launch overlap on C2, so the graph is the default.
   bool persistent = false;
   bool uncaptured = false;   // partitioned with host-synchronised collectives
+  // Fused iteration (one kernel per iteration, k_fused) while no recycle
+  // space is active: single GPU, TMA-staged tiles, lazy x.
+  bool fused = false;
+  bool fused_ok() const {
+    const bool off = getenv("RBICG_FUSED") && atoi(getenv("RBICG_FUSED")) == 0;   // per solve
+    return !off && z2 && la.k == 0 && la.staged && !la.split && lazy_x && !dist && pring_len == 0;
+  }
   void capture_graph() {
     if (dist && !ctx->comm->capturable()) {
       uncaptured = true;
@@ -870,12 +886,21 @@ struct Solver {
       if (persistent) return;
     }
     if (gexec) return;
+    fused = fused_ok();
+    if (fused) {   // z_0 = 0, p_0 = 0 (K(1) forms p_1 = r_0 + β_0 p_0 with α_0 = β_0 = 0)
+      T *zv[4] = {z, zt, p[0], pt[0]};
+      for (T *v : zv) RB_CUDA(cudaMemsetAsync(v, 0, sizeof(T) * n, ctx->stream));
+    }
     cudaGraph_t g;
     const int64_t l0 = g_launches.load();
     RB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    for (int it = 0; it < o.s; ++it) {
+    // the fused kernel K(i) completes iteration i-1: s + 1 launches reach the
+    // cycle boundary from any start (the extra one is a no-op after a pause)
+    for (int it = 0; it < o.s + (fused ? 1 : 0); ++it) {
       if (dist) {
         dist_iteration(ctx->stream);
+      } else if (fused) {
+        launch_fused<T>(la, ctx->stream);
       } else {
         launch_pass1<T>(la, ctx->stream);
         launch_pass2<T>(la, ctx->stream);
@@ -2198,6 +2223,47 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
   ms[11] = g2r.first;
   ms[12] = (g1r.second == 0 && g2r.second == 0) ? 0.0 : 1.0;
   ms[13] = S.la.shared_cols ? 1.0 : 0.0;
+  // the fused iteration (k = 0): `iters` launches of k_fused in one graph
+  ms[14] = -1.0;
+  ms[15] = -1.0;
+  if (S.fused_ok()) {
+    T *zv[4] = {S.z, S.zt, S.p[0], S.pt[0]};
+    for (T *v : zv) RB_CUDA(cudaMemsetAsync(v, 0, sizeof(T) * n, ctx->stream));
+    auto reset = [&] {
+      S.hst->iter = 0;
+      S.hst->kidx = 0;
+      S.hst->done = 0;
+      S.hst->seg_start = 0;
+      S.hst->stop_at = 1 << 30;
+      S.hst->alpha = zero<T>();
+      S.hst->beta = zero<T>();
+      S.push();
+    };
+    reset();
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    const int64_t l0 = g_launches.load();
+    RB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < iters; ++i) launch_fused<T>(S.la, ctx->stream);
+    RB_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+    RB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    RB_CUDA(cudaGraphDestroy(g));
+    g_launches.store(l0);
+    RB_CUDA(cudaGraphLaunch(ge, ctx->stream));   // warm
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    reset();
+    RB_CUDA(cudaEventRecord(ev[0], ctx->stream));
+    RB_CUDA(cudaGraphLaunch(ge, ctx->stream));
+    g_launches.fetch_add(iters);
+    RB_CUDA(cudaEventRecord(ev[1], ctx->stream));
+    RB_CUDA(cudaEventSynchronize(ev[1]));
+    float a = 0;
+    RB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    RB_CUDA(cudaGraphExecDestroy(ge));
+    S.pull();
+    ms[14] = (double)a / std::max(iters, 1);
+    ms[15] = S.hst->done;
+  }
   for (auto &e : ev) cudaEventDestroy(e);
   ms[0] = t1 / std::max(iters, 1);
   ms[1] = t2 / std::max(iters, 1);

@@ -59,6 +59,11 @@ __host__ __device__ __forceinline__ zc divd(zc a, zc b) {
 template <typename T> __host__ __device__ __forceinline__ T zero();
 template <> __host__ __device__ __forceinline__ double zero<double>() { return 0.0; }
 template <> __host__ __device__ __forceinline__ zc zero<zc>() { return mk(0.0, 0.0); }
+template <typename T> __host__ __device__ __forceinline__ T mk_re(double a);
+template <> __host__ __device__ __forceinline__ double mk_re<double>(double a) { return a; }
+template <> __host__ __device__ __forceinline__ zc mk_re<zc>(double a) { return mk(a, 0.0); }
+__host__ __device__ __forceinline__ double neg(double a) { return -a; }
+__host__ __device__ __forceinline__ zc neg(zc a) { return mk(-a.x, -a.y); }
 __host__ __device__ __forceinline__ bool finite(double a) { return isfinite(a); }
 __host__ __device__ __forceinline__ bool finite(zc a) { return isfinite(a.x) && isfinite(a.y); }
 __host__ __device__ __forceinline__ bool iszero(double a) { return a == 0.0; }

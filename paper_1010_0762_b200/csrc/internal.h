@@ -35,6 +35,7 @@ struct DevMat {
 template <typename T>
 struct DevState {
   int iter;      // completed iterations i
+  int kidx;      // fused form: k_fused launches that did work (K(i), i = kidx + 1 next)
   int done;      // 0 running, 1 finished, 2 paused at a cycle boundary
   int status;    // RBICG_* of the finished iteration
   int max_itn;
@@ -85,6 +86,7 @@ struct LoopArgs {
   T *pring, *ptring;       // or a ring of direction columns: p_i in column i % pring_len
   int pring_len;           //   (stride ldr), never rewritten within one launch
   T *z, *zt;
+  T *zb[2], *ztb[2];       // fused form: z_i, z~_i by iteration parity (z_0 = 0)
   T *x, *xt;
   const T *C, *Ct;         // row-major n x k
   DevState<T> *st;
@@ -165,6 +167,7 @@ void prepare_block_kernels();
 int stream_blocks_per_sm();    // occupancy of the streaming kernels
 template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_pass2(const LoopArgs<T> &a, cudaStream_t s);
+template <typename T> void launch_fused(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T>
 void launch_resid(const LoopArgs<T> &a, const T *b, const T *bt, const T *x, const T *xt,
                   T *r, T *rt, int with_coef, cudaStream_t s);

@@ -505,6 +505,249 @@ __global__ void __launch_bounds__(BS) k_spmv_pair(DevMat A, DevMat AH, const T *
   }
 }
 
+// ============================================================== fused form
+// One kernel per iteration while no recycle space is active (k = 0; DESIGN §6
+// "fused iteration"; oracle variant "lookahead").  K(i) completes iteration
+// i-1 and runs the SpMV pair of iteration i:
+//   r_{i-1} = r_{i-2} - α_{i-1} z_{i-1},   p_i = r_{i-1} + β_{i-1} p_{i-1},
+//   z_i = A p_i   (r_{i-1}, p_i formed on the fly in the gather from the stored
+//                  r_{i-2}, z_{i-1}, p_{i-1} of the neighbour columns)
+// and the duals; one reduction gives ρ_{i-1} (exact), ||r_{i-1}||, ||r~_{i-1}||
+// (the stop test of iteration i-1), σ_i = (p~_i, z_i), and (r~_{i-1}, z_i),
+// (z~_i, r_{i-1}), (z~_i, z_i) for ρ_i's one-step expansion, which gives β_i
+// with α_i = ρ_{i-1}/σ_i.  r_{i-1} lands in ring column i-1 (K(1) reads r_0
+// from column 0 and writes nothing there).
+constexpr int NFUSED = 7;
+template <typename T, bool COH>
+__device__ __forceinline__ void fused_pair_smem(const int32_t *__restrict__ cA, const T *__restrict__ vA,
+                                                int wA, const int32_t *__restrict__ cH,
+                                                const T *__restrict__ vH, int wH,
+                                                const T *__restrict__ r, const T *__restrict__ z,
+                                                const T *__restrict__ p, const T *__restrict__ rt,
+                                                const T *__restrict__ zt, const T *__restrict__ pt,
+                                                T malpha, T beta, T cmalpha, T cb, T &zo, T &zto) {
+  zo = zero<T>();
+  zto = zero<T>();
+  const int wm = max(wA, wH);
+  for (int j0 = 0; j0 < wm; j0 += 4) {
+    int ca[4], ch[4];
+    T va[4], vh[4], ra[4], za[4], pa[4], rh[4], zh[4], ph[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int jj = j0 + q;
+      const bool ia = jj < wA, ih = jj < wH;
+      ca[q] = ia ? cA[jj * 32] : 0;
+      va[q] = ia ? vA[jj * 32] : zero<T>();
+      ch[q] = ih ? cH[jj * 32] : 0;
+      vh[q] = ih ? vH[jj * 32] : zero<T>();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ra[q] = ldg(r + ca[q]);
+      za[q] = ldv<COH>(z + ca[q]);
+      pa[q] = ldv<COH>(p + ca[q]);
+      rh[q] = ldg(rt + ch[q]);
+      zh[q] = ldv<COH>(zt + ch[q]);
+      ph[q] = ldv<COH>(pt + ch[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      zo = mad(va[q], mad(beta, pa[q], mad(malpha, za[q], ra[q])), zo);
+      zto = mad(vh[q], mad(cb, ph[q], mad(cmalpha, zh[q], rh[q])), zto);
+    }
+  }
+}
+
+template <typename T, int MINB>
+__global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
+  __shared__ T s_fin[NFUSED + 1];
+  __shared__ T s_w[NFUSED][BS / 32];
+  __shared__ int s_last;
+  __shared__ uint64_t bars[2];
+  __shared__ T s_ab[2];
+  __shared__ int s_i[5];   // kidx, done, seg_start, iter, stop_at
+  extern __shared__ __align__(128) unsigned char f_smem[];
+  DevState<T> *st = a.st;
+  const int tid = threadIdx.x;
+  const int64_t n = a.n;
+  const int64_t ntiles = (n + BS - 1) / BS;
+  const int64_t G64 = gridDim.x;
+  const size_t stage_bytes = p1_mat_bytes<T>(a.tile_max);
+  const int nst = a.p1_stages;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int q = 0; q < nst; ++q)
+      if ((int64_t)blockIdx.x + q * G64 < ntiles)
+        p1_issue<T>(a, f_smem + q * stage_bytes, stage_bytes, &bars[q], blockIdx.x + q * G64);
+  pdl_wait();
+  if (tid == 0) {
+    s_i[0] = __ldcg(&st->kidx);
+    s_i[1] = __ldcg(&st->done);
+    s_i[2] = __ldcg(&st->seg_start);
+    s_ab[0] = ldcg(&st->alpha);
+    s_ab[1] = ldcg(&st->beta);
+  }
+  __syncthreads();
+  if (s_i[1]) {   // finished or paused: drain the copies in flight
+    for (int q = 0; q < nst; ++q)
+      if ((int64_t)blockIdx.x + q * G64 < ntiles) mbar_wait(&bars[q], 0);
+    return;
+  }
+  const int i = s_i[0] + 1;
+  const T alpha = s_ab[0], beta = s_ab[1];
+  const T malpha = neg(alpha), cmalpha = conj(malpha), cb = conj(beta);
+  const T *__restrict__ r = a.rring + (int64_t)(max(i - 2, 0) % a.ring) * a.ldr;
+  const T *__restrict__ rt = a.rtring + (int64_t)(max(i - 2, 0) % a.ring) * a.ldr;
+  T *__restrict__ rw = a.rring + (int64_t)((i - 1) % a.ring) * a.ldr;
+  T *__restrict__ rtw = a.rtring + (int64_t)((i - 1) % a.ring) * a.ldr;
+  const T *__restrict__ zo = a.zb[(i - 1) & 1];
+  const T *__restrict__ zto = a.ztb[(i - 1) & 1];
+  const T *__restrict__ po = a.p[(i - 1) & 1];
+  const T *__restrict__ pto = a.pt[(i - 1) & 1];
+  T *__restrict__ zn = a.zb[i & 1];
+  T *__restrict__ ztn = a.ztb[i & 1];
+  T *__restrict__ pn = a.p[i & 1];
+  T *__restrict__ ptn = a.pt[i & 1];
+  const bool wr = i >= 2;   // K(1): r_0 is already in column 0
+  const bool segcopy = a.lazy_x && i - 2 == s_i[2];
+  T *__restrict__ pseg = a.pseg[(s_i[2] / a.cyc) & 1];
+  T *__restrict__ ptseg = a.ptseg[(s_i[2] / a.cyc) & 1];
+  T acc[NFUSED];
+#pragma unroll
+  for (int o = 0; o < NFUSED; ++o) acc[o] = zero<T>();
+  const int TM = a.tile_max;
+  const int64_t ns = a.A.nslices;
+  uint32_t par = 0;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += G64, ++it) {
+    const int64_t row0 = tile * BS;
+    const int rows = (int)min((int64_t)BS, n - row0);
+    const int si = nst == 2 ? (it & 1) : 0;
+    const unsigned char *base = f_smem + si * stage_bytes;
+    const int32_t *scA = reinterpret_cast<const int32_t *>(base);
+    const int32_t *scH = a.shared_cols ? scA : scA + TM;
+    const T *svA = reinterpret_cast<const T *>(scA + 2 * TM);
+    const T *svH = svA + TM;
+    const int64_t sl = (row0 >> 5) + (tid >> 5);
+    const int64_t slc = min(sl, ns - 1);
+    const int64_t bA = a.A.sptr[tile * (BS / 32)], bH = a.AH.sptr[tile * (BS / 32)];
+    const int64_t oA = a.A.sptr[slc], oH = a.AH.sptr[slc];
+    const int wA = (int)((a.A.sptr[slc + 1] - oA) >> 5), wH = (int)((a.AH.sptr[slc + 1] - oH) >> 5);
+    const int lane = tid & 31;
+    mbar_wait(&bars[si], (par >> si) & 1u);
+    par ^= 1u << si;
+    if (tid < rows) {
+      const int64_t row = row0 + tid;
+      T z, zt;
+      fused_pair_smem<T, false>(scA + (oA - bA) + lane, svA + (oA - bA) + lane, wA,
+                                scH + (oH - bH) + lane, svH + (oH - bH) + lane, wH, r, zo, po, rt,
+                                zto, pto, malpha, beta, cmalpha, cb, z, zt);
+      const T rr = mad(malpha, ldg(zo + row), ldg(r + row));
+      const T rtr = mad(cmalpha, ldg(zto + row), ldg(rt + row));
+      const T pr = mad(beta, ldg(po + row), rr);
+      const T ptr = mad(cb, ldg(pto + row), rtr);
+      if (segcopy) {   // lazy x: p_a of the open segment (a = i - 2), before it is overwritten
+        pseg[row] = pn[row];
+        ptseg[row] = ptn[row];
+      }
+      if (wr) {
+        rw[row] = rr;
+        rtw[row] = rtr;
+      }
+      pn[row] = pr;
+      ptn[row] = ptr;
+      zn[row] = z;
+      ztn[row] = zt;
+      acc[0] = cmad(rtr, rr, acc[0]);      // ρ_{i-1}
+      acc[1] = add(acc[1], mk_re<T>(abs2(rr)));
+      acc[2] = add(acc[2], mk_re<T>(abs2(rtr)));
+      acc[3] = cmad(ptr, z, acc[3]);       // σ_i
+      acc[4] = cmad(rtr, z, acc[4]);       // (r~_{i-1}, z_i)
+      acc[5] = cmad(zt, rr, acc[5]);       // (z~_i, r_{i-1})
+      acc[6] = cmad(zt, z, acc[6]);        // (z~_i, z_i)
+    }
+    __syncthreads();   // stage si consumed
+    if (tid == 0 && tile + nst * G64 < ntiles)
+      p1_issue<T>(a, f_smem + si * stage_bytes, stage_bytes, &bars[si], tile + nst * G64);
+  }
+  pdl_trigger();
+  // block partials (fixed order) -> part[o * G + b]
+  const int w = tid >> 5, l = tid & 31;
+#pragma unroll
+  for (int o = 0; o < NFUSED; ++o) {
+    const T v = warp_sum(acc[o]);
+    if (l == 0) s_w[o][w] = v;
+  }
+  __syncthreads();
+  if (tid < NFUSED) {
+    T sum = zero<T>();
+    for (int q = 0; q < BS / 32; ++q) sum = add(sum, s_w[tid][q]);
+    a.part[(int64_t)tid * gridDim.x + blockIdx.x] = sum;
+  }
+  if (!last_block(&st->cnt[0], &s_last)) return;
+  final_reduce(a.part, NFUSED, gridDim.x, s_fin);
+  if (tid != 0) return;
+  st->cnt[0] = 0;
+  const T rho_prev = s_fin[0];
+  const double rn = sqrt(re(s_fin[1])), rtn = sqrt(re(s_fin[2]));
+  const T sigma = s_fin[3];
+  int done = 0, status = RBICG_OK;
+  if (i >= 2) {   // iteration i-1 completes here
+    const int m = i - 1;
+    IterRec<T> rec;
+    rec.alpha = alpha;
+    rec.beta = beta;
+    rec.rho = rho_prev;
+    rec.sigma = ldcg(&st->sigma);
+    rec.rnorm = rn;
+    rec.rtnorm = rtn;
+    a.hist[m] = rec;
+    const int force = __ldcg(&st->force);
+    const bool conv = !force && rn <= __ldcg(&st->tolb) && rtn <= __ldcg(&st->tolbt);
+    if (conv) {
+      done = 1;
+    } else if (iszero(rho_prev) || !finite(divd(rho_prev, ldcg(&st->rho)))) {
+      done = 1;
+      status = RBICG_BREAKDOWN_SERIOUS;
+    } else if (m >= __ldcg(&st->max_itn)) {
+      done = 1;
+      status = force ? RBICG_OK : RBICG_MAXITER;
+    } else if (m == __ldcg(&st->stop_at)) {
+      done = 2;
+    }
+    st->iter = m;
+    st->rnorm = rn;
+    st->rtnorm = rtn;
+    st->rho = rho_prev;
+  }
+  // iteration i's scalars (kept also when finishing: a retry resumes with them)
+  const T alpha_i = divd(rho_prev, sigma);
+  if (!done && (iszero(sigma) || !finite(alpha_i))) {
+    done = 1;
+    status = RBICG_BREAKDOWN_SECOND;
+  }
+  // ρ_i ≈ ρ_{i-1} - α_i (r~, z) - α_i (z~, r) + α_i² (z~, z)
+  const T rho_ext = add(sub(sub(rho_prev, mul(alpha_i, s_fin[4])), mul(alpha_i, s_fin[5])),
+                        mul(mul(alpha_i, alpha_i), s_fin[6]));
+  st->alpha = alpha_i;
+  st->beta = divd(rho_ext, rho_prev);
+  st->sigma = sigma;
+  st->kidx = i;
+  if (done) {
+    st->status = status;
+    st->done = done;
+  }
+}
+
+template <typename T> size_t fused_smem(const LoopArgs<T> &a) {
+  return (size_t)a.p1_stages * p1_mat_bytes<T>(a.tile_max);
+}
+
 // ============================================================== launchers
 static int grid_for(int64_t n, int G) {
   const int64_t tiles = (n + BS - 1) / BS;
@@ -582,6 +825,19 @@ template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s) {
 // two stages of (8 vector tiles + C, C~ tiles)
 template <typename T> size_t pass2_smem(int k, int lazy) {
   return (size_t)2 * p2_stage_elems<T>(k, lazy) * sizeof(T);
+}
+
+// fused iteration (k = 0, staged SELL tiles): RBICG_FUSED_MINB = 3/4 (registers)
+template <typename T> void launch_fused(const LoopArgs<T> &a, cudaStream_t s) {
+  const size_t sm = fused_smem<T>(a);
+  // 4 CTAs/SM at 64 registers (C2: 46.3 us per iteration; 3 CTAs at 80: 56.3 us)
+  static const int minb = getenv("RBICG_FUSED_MINB") ? atoi(getenv("RBICG_FUSED_MINB")) : 4;
+  auto fn = minb >= 4 ? k_fused<T, 4> : k_fused<T, 3>;
+  int per_sm = 1;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BS, sm));
+  const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
+  launch_pdl(fn, grid_for(a.n, G), sm, s, a);
+  count_launch();
 }
 
 template <typename T> void launch_pass2(const LoopArgs<T> &a, cudaStream_t s) {
@@ -684,6 +940,10 @@ void prepare_kernels() {
   allow_max_dyn_smem(k_pass2<double, 4>);
   allow_max_dyn_smem(k_pass2<zc, 3>);
   allow_max_dyn_smem(k_pass2<zc, 4>);
+  allow_max_dyn_smem(k_fused<double, 3>);
+  allow_max_dyn_smem(k_fused<double, 4>);
+  allow_max_dyn_smem(k_fused<zc, 3>);
+  allow_max_dyn_smem(k_fused<zc, 4>);
   prepare_block_kernels();
   prepare_loop_kernels();
 }
@@ -691,6 +951,7 @@ void prepare_kernels() {
 #define RB_INST(T)                                                                          \
   template void launch_pass1<T>(const LoopArgs<T> &, cudaStream_t);                          \
   template void launch_pass2<T>(const LoopArgs<T> &, cudaStream_t);                          \
+  template void launch_fused<T>(const LoopArgs<T> &, cudaStream_t);                          \
   template void launch_resid<T>(const LoopArgs<T> &, const T *, const T *, const T *,        \
                                 const T *, T *, T *, int, cudaStream_t);                     \
   template void launch_init2<T>(const LoopArgs<T> &, const T *, const T *, cudaStream_t);    \

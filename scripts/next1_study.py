@@ -1,5 +1,6 @@
 """NEXT-1 study: the single-reduction (re-associated) RBiCG
-iteration vs Algorithm 2 as written, on the BASELINE operator families at
+iteration and the look-ahead-ρ iteration of the fused GPU kernel vs
+Algorithm 2 as written, on the BASELINE operator families at
 oracle-size grids -- iteration counts, statuses, recycle widths and true
 residuals per system.  Oracle only (CPU); the table is quoted in DESIGN §6.
 
@@ -19,7 +20,7 @@ from synth import CONFIGS, system_sequence  # noqa: E402
 def run(name, N, nsys):
     cfg = CONFIGS[name].scaled(N, systems=nsys) if N else CONFIGS[name]
     kw = {"lam_r": 0.0} if cfg.kind == "irka" else {}
-    for var in ("standard", "single_reduction"):
+    for var in ("standard", "single_reduction", "lookahead"):
         U = Ut = None
         out = []
         for item in system_sequence(cfg, **kw):

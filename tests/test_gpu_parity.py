@@ -581,3 +581,78 @@ def test_shared_column_array_bitwise(ctx, monkeypatch):
         M.free()
     assert outs[0][2] == outs[1][2]
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+# ------------------------------------------------------------------ fused iteration
+@pytest.mark.parametrize("name,N", [("C1", 0), ("C3", 20), ("C4", 10), ("C5", 16)])
+def test_fused_iteration_matches_lookahead_oracle(ctx, name, N):
+    """First systems (no recycle space) run the fused one-kernel iteration
+    (DESIGN §6): against the oracle's "lookahead" variant -- the same
+    arithmetic -- iterations within max(2, 3 %) and the same status (the same
+    count, recycle width and residual history (1e-5) when they agree),
+    solutions at matched counts to 1e-8."""
+    from oracle import rbicg as R
+    cfg = CONFIGS[name].scaled(N, systems=1) if N else CONFIGS[name]
+    item = next(system_sequence(cfg, **({"lam_r": 0.0} if cfg.kind == "irka" else {})))
+    A = _csr((item["indptr"], item["indices"], item["data"]))
+    M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+    kt = ctx.time_kernels(M, None, k=0, s=cfg.s, iters=3)
+    assert kt["fused_ms"] > 0 and kt["fused_done_flag"] == 0
+    rec = ctx.recycle(cfg.n, cfg.k, cfg.complex)
+    x, xt, res, h = ctx.solve_dual(M, item["b"], item["bt"], R=rec, k=cfg.k, s=cfg.s,
+                                   tol=cfg.tol, max_itn=cfg.max_itn,
+                                   trunc_tol=cfg.trunc_tol, history=True)
+    M.free()
+    ref = R.solve_dual(A, item["b"], item["bt"], k=cfg.k, s=cfg.s, tol=cfg.tol,
+                       max_itn=cfg.max_itn, trunc_tol=cfg.trunc_tol, variant="lookahead")
+    m = res["iterations"]
+    assert iters_close(m, ref.iterations) and res["status"] == ref.status, (m, ref.iterations)
+    if m != ref.iterations:   # Q27: the oracle at the GPU's count
+        ref = R.solve_dual(A, item["b"], item["bt"], k=cfg.k, s=cfg.s, tol=cfg.tol,
+                           max_itn=m, trunc_tol=cfg.trunc_tol, force_iters=m,
+                           variant="lookahead")
+    else:
+        assert res["k_out"] == ref.basis_out.k
+        np.testing.assert_allclose(h[:, 0], np.array(ref.hist["rnorm"][1:]) /
+                                   np.linalg.norm(item["b"]), rtol=1e-5, atol=1e-11)
+    assert np.linalg.norm(x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+    assert np.linalg.norm(xt - ref.xt) <= 1e-8 * np.linalg.norm(ref.xt)
+    assert res["relres_true"] <= cfg.tol and res["relres_dual_true"] <= cfg.tol
+
+
+def test_fused_and_two_kernel_forms_agree(ctx, monkeypatch):
+    """The fused iteration vs the two-kernel iteration (RBICG_FUSED=0) on a
+    3-D conv-diff system: the same iteration count and solutions to 1e-8
+    (they differ only in how β_i's ρ_i is formed), and the fused
+    form also at the bench configuration's cycle length with forced
+    iterations across two cycle ends (Q27) against the lookahead oracle."""
+    from oracle import rbicg as R
+    cfg = CONFIGS["C3"].scaled(24, systems=1)
+    item = next(system_sequence(cfg))
+    outs = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("RBICG_FUSED", "0")
+        M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+        rec = ctx.recycle(cfg.n, cfg.k)
+        x, xt, res, _ = ctx.solve_dual(M, item["b"], item["bt"], R=rec, k=cfg.k, s=cfg.s,
+                                       tol=cfg.tol, max_itn=cfg.max_itn,
+                                       trunc_tol=cfg.trunc_tol)
+        outs.append((x, xt, res["iterations"]))
+        M.free()
+    assert outs[0][2] == outs[1][2]
+    assert np.linalg.norm(outs[0][0] - outs[1][0]) <= 1e-8 * np.linalg.norm(outs[1][0])
+    monkeypatch.delenv("RBICG_FUSED")
+    m = 2 * cfg.s + 3
+    A = _csr((item["indptr"], item["indices"], item["data"]))
+    ref = R.solve_dual(A, item["b"], item["bt"], k=cfg.k, s=cfg.s, tol=cfg.tol, max_itn=m,
+                       trunc_tol=cfg.trunc_tol, force_iters=m, variant="lookahead")
+    M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+    rec = ctx.recycle(cfg.n, cfg.k)
+    x, xt, res, _ = ctx.solve_dual(M, item["b"], item["bt"], R=rec, k=cfg.k, s=cfg.s,
+                                   tol=cfg.tol, max_itn=m, trunc_tol=cfg.trunc_tol,
+                                   force_iters=m)
+    M.free()
+    assert res["iterations"] == m and res["cycles"] == ref.cycles == 2
+    assert np.linalg.norm(x - ref.x) <= 1e-9 * np.linalg.norm(ref.x)
+    assert res["k_out"] == ref.basis_out.k
