@@ -355,7 +355,7 @@ struct Solver {
   }
   std::vector<void *> owned;
   T *rring = nullptr, *rtring = nullptr, *p[2] = {}, *pt[2] = {}, *z = nullptr, *zt = nullptr;
-  T *z2 = nullptr, *zt2 = nullptr;   // fused iteration: z_i by parity
+  T *zp[2] = {}, *ztp[2] = {};   // fused iteration: (z_i, p_i) pairs by parity
   T *x = nullptr, *xt = nullptr, *b = nullptr, *bt = nullptr, *xo = nullptr, *xto = nullptr;
   T *psegs[2] = {}, *ptsegs[2] = {};
   T *pring = nullptr, *ptring = nullptr;
@@ -521,9 +521,11 @@ struct Solver {
     tmark("ring+p");
     z = alloc(n);
     zt = alloc(n);
-    if (k_basis == 0 && !dist) {   // fused iteration: z_i by parity (z, z2)
-      z2 = alloc(n);
-      zt2 = alloc(n);
+    if (k_basis == 0 && !dist) {   // fused iteration: (z_i, p_i) pairs by parity
+      for (int q = 0; q < 2; ++q) {
+        zp[q] = alloc(2 * (size_t)n);
+        ztp[q] = alloc(2 * (size_t)n);
+      }
     }
     x = alloc(nx);
     xt = alloc(nx);
@@ -621,10 +623,10 @@ struct Solver {
     la.pt[1] = pt[1];
     la.z = z;
     la.zt = zt;
-    la.zb[0] = z;
-    la.zb[1] = z2;
-    la.ztb[0] = zt;
-    la.ztb[1] = zt2;
+    la.zp[0] = zp[0];
+    la.zp[1] = zp[1];
+    la.ztp[0] = ztp[0];
+    la.ztp[1] = ztp[1];
     la.x = x;
     la.xt = xt;
     la.C = cur.C;
@@ -873,7 +875,7 @@ struct Solver {
   bool fused = false;
   bool fused_ok() const {
     const bool off = getenv("RBICG_FUSED") && atoi(getenv("RBICG_FUSED")) == 0;   // per solve
-    return !off && z2 && la.k == 0 && la.staged && !la.split && lazy_x && !dist && pring_len == 0;
+    return !off && zp[0] && la.k == 0 && la.staged && !la.split && lazy_x && !dist && pring_len == 0;
   }
   void capture_graph() {
     if (dist && !ctx->comm->capturable()) {
@@ -887,9 +889,9 @@ struct Solver {
     }
     if (gexec) return;
     fused = fused_ok();
-    if (fused) {   // z_0 = 0, p_0 = 0 (K(1) forms p_1 = r_0 + β_0 p_0 with α_0 = β_0 = 0)
-      T *zv[4] = {z, zt, p[0], pt[0]};
-      for (T *v : zv) RB_CUDA(cudaMemsetAsync(v, 0, sizeof(T) * n, ctx->stream));
+    if (fused) {   // z_0 = p_0 = 0 (K(1) forms p_1 = r_0 + β_0 p_0 with α_0 = β_0 = 0)
+      RB_CUDA(cudaMemsetAsync(zp[0], 0, sizeof(T) * 2 * n, ctx->stream));
+      RB_CUDA(cudaMemsetAsync(ztp[0], 0, sizeof(T) * 2 * n, ctx->stream));
     }
     cudaGraph_t g;
     const int64_t l0 = g_launches.load();
@@ -2227,8 +2229,8 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
   ms[14] = -1.0;
   ms[15] = -1.0;
   if (S.fused_ok()) {
-    T *zv[4] = {S.z, S.zt, S.p[0], S.pt[0]};
-    for (T *v : zv) RB_CUDA(cudaMemsetAsync(v, 0, sizeof(T) * n, ctx->stream));
+    RB_CUDA(cudaMemsetAsync(S.zp[0], 0, sizeof(T) * 2 * n, ctx->stream));
+    RB_CUDA(cudaMemsetAsync(S.ztp[0], 0, sizeof(T) * 2 * n, ctx->stream));
     auto reset = [&] {
       S.hst->iter = 0;
       S.hst->kidx = 0;

@@ -387,11 +387,15 @@ struct P1Scratch {
 // with stage_v, the tile's own rows of r, p, r~, p~ (BS each).  The stage's
 // mbarrier expects two arrivals when stage_v (matrix part, vector part: the
 // vector part depends on the previous phase, the matrix part does not).
-template <typename T> __host__ __device__ __forceinline__ size_t p1_mat_bytes(int tile_max) {
-  return (size_t)2 * tile_max * (4 + sizeof(T));
+// [cols A | cols A^* (unless shared) | vals A | vals A^*]
+template <typename T> __host__ __device__ __forceinline__ int p1_ncols(const LoopArgs<T> &a) {
+  return a.shared_cols ? 1 : 2;
+}
+template <typename T> __host__ __device__ __forceinline__ size_t p1_mat_bytes(const LoopArgs<T> &a) {
+  return (size_t)a.tile_max * (4 * p1_ncols(a) + 2 * sizeof(T));
 }
 template <typename T> __host__ __device__ __forceinline__ size_t p1_stage_bytes(const LoopArgs<T> &a) {
-  return p1_mat_bytes<T>(a.tile_max) + (a.stage_v ? (size_t)4 * BS * sizeof(T) : 0);
+  return p1_mat_bytes<T>(a) + (a.stage_v ? (size_t)4 * BS * sizeof(T) : 0);
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -405,7 +409,7 @@ __device__ __forceinline__ void p1_issue_vec(const LoopArgs<T> &a, unsigned char
     mbar_arrive(bar);
     return;
   }
-  T *v = reinterpret_cast<T *>(stage + p1_mat_bytes<T>(a.tile_max));
+  T *v = reinterpret_cast<T *>(stage + p1_mat_bytes<T>(a));
   const uint32_t vb = BS * (uint32_t)sizeof(T);
   const int64_t r0 = t * BS;
   mbar_expect_tx(bar, 4u * vb);
@@ -422,7 +426,7 @@ __device__ __forceinline__ void p1_issue(const LoopArgs<T> &a, unsigned char *st
   const int TM = a.tile_max;
   int32_t *cA = reinterpret_cast<int32_t *>(stages);
   int32_t *cH = cA + TM;
-  T *vA = reinterpret_cast<T *>(cH + TM);
+  T *vA = reinterpret_cast<T *>(cA + p1_ncols(a) * TM);
   T *vH = vA + TM;
   const int64_t ns = a.A.nslices;
   const int64_t s0 = t * (BS / 32), s1 = min(s0 + BS / 32, ns);
@@ -527,7 +531,7 @@ __device__ __forceinline__ void p1_tiles(const LoopArgs<T> &a, unsigned char *ds
       const unsigned char *base = dsm + si * stage_bytes;
       const int32_t *scA = reinterpret_cast<const int32_t *>(base);
       const int32_t *scH = a.shared_cols ? scA : scA + TM;
-      const T *svA = reinterpret_cast<const T *>(scA + 2 * TM);
+      const T *svA = reinterpret_cast<const T *>(scA + p1_ncols(a) * TM);
       const T *svH = svA + TM;
       // slice geometry (global loads overlap the bulk copy)
       const int64_t sl = (row0 >> 5) + (tid >> 5);
@@ -542,7 +546,7 @@ __device__ __forceinline__ void p1_tiles(const LoopArgs<T> &a, unsigned char *ds
         T z, zt;
         if (a.abl & 1) {   // timing ablation: no gathers (row-local operands)
           const int64_t row = row0 + tid;
-          const T *sv = reinterpret_cast<const T *>(base + p1_mat_bytes<T>(TM));
+          const T *sv = reinterpret_cast<const T *>(base + p1_mat_bytes<T>(a));
           const bool vs = stage_v && rows == BS;
           const T xr = vs ? mad(beta, sv[BS + tid], sv[tid]) : mad(beta, ldg(pold + row), ldg(r + row));
           const T xrt = vs ? mad(cb, sv[3 * BS + tid], sv[2 * BS + tid]) : mad(cb, ldg(ptold + row), ldg(rt + row));
@@ -557,7 +561,7 @@ __device__ __forceinline__ void p1_tiles(const LoopArgs<T> &a, unsigned char *ds
         }
         const int64_t row = row0 + tid;
         if (stage_v && rows == BS) {
-          const T *sv = reinterpret_cast<const T *>(base + p1_mat_bytes<T>(TM));
+          const T *sv = reinterpret_cast<const T *>(base + p1_mat_bytes<T>(a));
           finish_row(row, z, zt, sv[tid], sv[BS + tid], sv[2 * BS + tid], sv[3 * BS + tid]);
         } else {
           finish_row(row, z, zt, ldg(r + row), ldv<COH>(pold + row), ldg(rt + row),

@@ -518,20 +518,36 @@ __global__ void __launch_bounds__(BS) k_spmv_pair(DevMat A, DevMat AH, const T *
 // with α_i = ρ_{i-1}/σ_i.  r_{i-1} lands in ring column i-1 (K(1) reads r_0
 // from column 0 and writes nothing there).
 constexpr int NFUSED = 7;
-template <typename T, bool COH>
+// (z, p) of column c: one 16-byte load for real data
+template <typename T> struct ZP { T z, p; };
+__device__ __forceinline__ ZP<double> ld_zp(const double *zp, int64_t c) {
+  const double2 v = __ldg(reinterpret_cast<const double2 *>(zp) + c);
+  return ZP<double>{v.x, v.y};
+}
+__device__ __forceinline__ ZP<zc> ld_zp(const zc *zp, int64_t c) {
+  return ZP<zc>{ldg(zp + 2 * c), ldg(zp + 2 * c + 1)};
+}
+__device__ __forceinline__ void st_zp(double *zp, int64_t c, double z, double p) {
+  reinterpret_cast<double2 *>(zp)[c] = make_double2(z, p);
+}
+__device__ __forceinline__ void st_zp(zc *zp, int64_t c, zc z, zc p) {
+  zp[2 * c] = z;
+  zp[2 * c + 1] = p;
+}
+template <typename T>
 __device__ __forceinline__ void fused_pair_smem(const int32_t *__restrict__ cA, const T *__restrict__ vA,
                                                 int wA, const int32_t *__restrict__ cH,
                                                 const T *__restrict__ vH, int wH,
-                                                const T *__restrict__ r, const T *__restrict__ z,
-                                                const T *__restrict__ p, const T *__restrict__ rt,
-                                                const T *__restrict__ zt, const T *__restrict__ pt,
+                                                const T *__restrict__ r, const T *__restrict__ zp,
+                                                const T *__restrict__ rt, const T *__restrict__ ztp,
                                                 T malpha, T beta, T cmalpha, T cb, T &zo, T &zto) {
   zo = zero<T>();
   zto = zero<T>();
   const int wm = max(wA, wH);
   for (int j0 = 0; j0 < wm; j0 += 4) {
     int ca[4], ch[4];
-    T va[4], vh[4], ra[4], za[4], pa[4], rh[4], zh[4], ph[4];
+    T va[4], vh[4], ra[4], rh[4];
+    ZP<T> za[4], zh[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int jj = j0 + q;
@@ -544,16 +560,14 @@ __device__ __forceinline__ void fused_pair_smem(const int32_t *__restrict__ cA, 
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       ra[q] = ldg(r + ca[q]);
-      za[q] = ldv<COH>(z + ca[q]);
-      pa[q] = ldv<COH>(p + ca[q]);
+      za[q] = ld_zp(zp, ca[q]);
       rh[q] = ldg(rt + ch[q]);
-      zh[q] = ldv<COH>(zt + ch[q]);
-      ph[q] = ldv<COH>(pt + ch[q]);
+      zh[q] = ld_zp(ztp, ch[q]);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      zo = mad(va[q], mad(beta, pa[q], mad(malpha, za[q], ra[q])), zo);
-      zto = mad(vh[q], mad(cb, ph[q], mad(cmalpha, zh[q], rh[q])), zto);
+      zo = mad(va[q], mad(beta, za[q].p, mad(malpha, za[q].z, ra[q])), zo);
+      zto = mad(vh[q], mad(cb, zh[q].p, mad(cmalpha, zh[q].z, rh[q])), zto);
     }
   }
 }
@@ -572,7 +586,7 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   const int64_t n = a.n;
   const int64_t ntiles = (n + BS - 1) / BS;
   const int64_t G64 = gridDim.x;
-  const size_t stage_bytes = p1_mat_bytes<T>(a.tile_max);
+  const size_t stage_bytes = p1_mat_bytes<T>(a);
   const int nst = a.p1_stages;
   if (tid == 0) {
     mbar_init(&bars[0], 1);
@@ -605,14 +619,10 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   const T *__restrict__ rt = a.rtring + (int64_t)(max(i - 2, 0) % a.ring) * a.ldr;
   T *__restrict__ rw = a.rring + (int64_t)((i - 1) % a.ring) * a.ldr;
   T *__restrict__ rtw = a.rtring + (int64_t)((i - 1) % a.ring) * a.ldr;
-  const T *__restrict__ zo = a.zb[(i - 1) & 1];
-  const T *__restrict__ zto = a.ztb[(i - 1) & 1];
-  const T *__restrict__ po = a.p[(i - 1) & 1];
-  const T *__restrict__ pto = a.pt[(i - 1) & 1];
-  T *__restrict__ zn = a.zb[i & 1];
-  T *__restrict__ ztn = a.ztb[i & 1];
-  T *__restrict__ pn = a.p[i & 1];
-  T *__restrict__ ptn = a.pt[i & 1];
+  const T *__restrict__ zpo = a.zp[(i - 1) & 1];
+  const T *__restrict__ ztpo = a.ztp[(i - 1) & 1];
+  T *__restrict__ zpn = a.zp[i & 1];
+  T *__restrict__ ztpn = a.ztp[i & 1];
   const bool wr = i >= 2;   // K(1): r_0 is already in column 0
   const bool segcopy = a.lazy_x && i - 2 == s_i[2];
   T *__restrict__ pseg = a.pseg[(s_i[2] / a.cyc) & 1];
@@ -631,7 +641,7 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
     const unsigned char *base = f_smem + si * stage_bytes;
     const int32_t *scA = reinterpret_cast<const int32_t *>(base);
     const int32_t *scH = a.shared_cols ? scA : scA + TM;
-    const T *svA = reinterpret_cast<const T *>(scA + 2 * TM);
+    const T *svA = reinterpret_cast<const T *>(scA + p1_ncols(a) * TM);
     const T *svH = svA + TM;
     const int64_t sl = (row0 >> 5) + (tid >> 5);
     const int64_t slc = min(sl, ns - 1);
@@ -644,25 +654,24 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
     if (tid < rows) {
       const int64_t row = row0 + tid;
       T z, zt;
-      fused_pair_smem<T, false>(scA + (oA - bA) + lane, svA + (oA - bA) + lane, wA,
-                                scH + (oH - bH) + lane, svH + (oH - bH) + lane, wH, r, zo, po, rt,
-                                zto, pto, malpha, beta, cmalpha, cb, z, zt);
-      const T rr = mad(malpha, ldg(zo + row), ldg(r + row));
-      const T rtr = mad(cmalpha, ldg(zto + row), ldg(rt + row));
-      const T pr = mad(beta, ldg(po + row), rr);
-      const T ptr = mad(cb, ldg(pto + row), rtr);
+      fused_pair_smem<T>(scA + (oA - bA) + lane, svA + (oA - bA) + lane, wA,
+                         scH + (oH - bH) + lane, svH + (oH - bH) + lane, wH, r, zpo, rt, ztpo,
+                         malpha, beta, cmalpha, cb, z, zt);
+      const ZP<T> o = ld_zp(zpo, row), ot = ld_zp(ztpo, row);
+      const T rr = mad(malpha, o.z, ldg(r + row));
+      const T rtr = mad(cmalpha, ot.z, ldg(rt + row));
+      const T pr = mad(beta, o.p, rr);
+      const T ptr = mad(cb, ot.p, rtr);
       if (segcopy) {   // lazy x: p_a of the open segment (a = i - 2), before it is overwritten
-        pseg[row] = pn[row];
-        ptseg[row] = ptn[row];
+        pseg[row] = ld_zp(zpn, row).p;
+        ptseg[row] = ld_zp(ztpn, row).p;
       }
       if (wr) {
         rw[row] = rr;
         rtw[row] = rtr;
       }
-      pn[row] = pr;
-      ptn[row] = ptr;
-      zn[row] = z;
-      ztn[row] = zt;
+      st_zp(zpn, row, z, pr);
+      st_zp(ztpn, row, zt, ptr);
       acc[0] = cmad(rtr, rr, acc[0]);      // ρ_{i-1}
       acc[1] = add(acc[1], mk_re<T>(abs2(rr)));
       acc[2] = add(acc[2], mk_re<T>(abs2(rtr)));
@@ -745,7 +754,7 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
 }
 
 template <typename T> size_t fused_smem(const LoopArgs<T> &a) {
-  return (size_t)a.p1_stages * p1_mat_bytes<T>(a.tile_max);
+  return (size_t)a.p1_stages * p1_mat_bytes<T>(a);
 }
 
 // ============================================================== launchers
@@ -828,7 +837,12 @@ template <typename T> size_t pass2_smem(int k, int lazy) {
 }
 
 // fused iteration (k = 0, staged SELL tiles): RBICG_FUSED_MINB = 3/4 (registers)
-template <typename T> void launch_fused(const LoopArgs<T> &a, cudaStream_t s) {
+template <typename T> void launch_fused(const LoopArgs<T> &a0, cudaStream_t s) {
+  // one TMA stage of matrix tiles (RBICG_FUSED_STAGES=2 measured C2 50.5 vs
+  // 46.5 us per iteration at 4 CTAs/SM)
+  LoopArgs<T> a = a0;
+  static const int fst = getenv("RBICG_FUSED_STAGES") ? atoi(getenv("RBICG_FUSED_STAGES")) : 1;
+  a.p1_stages = std::min(2, std::max(1, fst));
   const size_t sm = fused_smem<T>(a);
   // 4 CTAs/SM at 64 registers (C2: 46.3 us per iteration; 3 CTAs at 80: 56.3 us)
   static const int minb = getenv("RBICG_FUSED_MINB") ? atoi(getenv("RBICG_FUSED_MINB")) : 4;
