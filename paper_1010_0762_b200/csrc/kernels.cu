@@ -846,7 +846,7 @@ template <typename T> void launch_fused(const LoopArgs<T> &a0, cudaStream_t s) {
   const size_t sm = fused_smem<T>(a);
   // 4 CTAs/SM at 64 registers (C2: 46.3 us per iteration; 3 CTAs at 80: 56.3 us)
   static const int minb = getenv("RBICG_FUSED_MINB") ? atoi(getenv("RBICG_FUSED_MINB")) : 4;
-  auto fn = minb >= 4 ? k_fused<T, 4> : k_fused<T, 3>;
+  auto fn = minb >= 6 ? k_fused<T, 6> : minb == 5 ? k_fused<T, 5> : minb == 4 ? k_fused<T, 4> : k_fused<T, 3>;
   int per_sm = 1;
   RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BS, sm));
   const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
@@ -956,6 +956,10 @@ void prepare_kernels() {
   allow_max_dyn_smem(k_pass2<zc, 4>);
   allow_max_dyn_smem(k_fused<double, 3>);
   allow_max_dyn_smem(k_fused<double, 4>);
+  allow_max_dyn_smem(k_fused<double, 5>);
+  allow_max_dyn_smem(k_fused<double, 6>);
+  allow_max_dyn_smem(k_fused<zc, 5>);
+  allow_max_dyn_smem(k_fused<zc, 6>);
   allow_max_dyn_smem(k_fused<zc, 3>);
   allow_max_dyn_smem(k_fused<zc, 4>);
   prepare_block_kernels();

@@ -22,7 +22,7 @@ for k in (0, cfg.k):
         if cfg.complex: U = U + 1j * rng.standard_normal((n, k)); Ut = Ut + 1j * rng.standard_normal((n, k))
         R.import_(U, Ut)
     t = ctx.time_kernels(A, R if k else None, k=k, s=cfg.s, iters=30, trunc_tol=1e-12)
-    mat = 2 * (nnz * (w + 4) + 4 * (n + 1))
+    mat = 2 * (nnz * (w + 4) + 4 * (n + 1)) - (4 * nnz if t["shared_cols"] else 0)
     kk = t["k"]
     b1 = mat + 2 * kk * n * w + 8 * n * w
     b2 = 2 * kk * n * w + (6 if t["lazy_x"] else 12) * n * w
@@ -33,4 +33,5 @@ for k in (0, cfg.k):
                           graph_done=t["graph_done_flag"], loop_iter_ms=t["loop_iter_ms"],
                           p1g=t["pass1_graph_ms"], p2g=t["pass2_graph_ms"],
                           loop_GBps=(b1 + b2) / t["loop_iter_ms"] / 1e6 if t["loop_iter_ms"] > 0 else None,
-                          loop_done=t["loop_done_flag"])))
+                          loop_done=t["loop_done_flag"], fused_ms=t["fused_ms"],
+                          fused_GBps=(mat + 12 * n * w) / t["fused_ms"] / 1e6 if t["fused_ms"] > 0 else None)))
