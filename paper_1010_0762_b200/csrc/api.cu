@@ -673,7 +673,9 @@ struct Solver {
     std::vector<cplx> G((size_t)4 * kin * kin, 0.0), gv;
     {
       Phase ph("biorth.gram", bs);
-      gram_pairs<T>({C, Ct}, {kin, kin}, pairs, n, gv, ctx, bs);
+      static const bool old_gram = getenv("RBICG_GRAM_PAIRS") != nullptr;
+      if (old_gram) gram_pairs<T>({C, Ct}, {kin, kin}, pairs, n, gv, ctx, bs);
+      else gram_cc<T>(C, Ct, kin, n, gv, ctx, bs);   // same outputs, register-tiled
     }
     sum_host(dist ? cm : nullptr, gv);   // partial Grams of the row blocks (C-4)
     {

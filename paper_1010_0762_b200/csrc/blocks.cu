@@ -432,6 +432,146 @@ void gram_pairs(const std::vector<const T *> &panels, const std::vector<int> &nc
   for (int i = 0; i < np; ++i) out[i] = cplx(re(h[i]), im(h[i]));
 }
 
+// ------------------------------------------------------------------ C~^*C Gram
+// The bi-orthogonalisation Gram of two row-major n x k blocks (C, C~): the
+// column norms of both and C~^*C, register-tiled -- each thread owns a 4 x 4
+// tile of C~^*C (or 4 norms) over a strided subset of the staged rows, so a
+// shared-memory load feeds 2 (not 0.5) FMAs.  Rows arrive in 64-row
+// sub-tiles by cp.async, double buffered (both blocks' sub-tiles are single
+// contiguous ranges).  Output order: |c_j|^2, |c~_j|^2, then c~_a^* c_b (a-major).
+// GCR rows per sub-tile (64; 288-row sub-tiles measured no faster at k = 10:
+// 93 vs 87 us on C2)
+static int gcr_rows(int) { return 64; }
+template <typename T>
+__global__ void __launch_bounds__(256) k_gram_cc(const T *__restrict__ C, const T *__restrict__ Ct, int k,
+                                                 int64_t n, int64_t chunk, int GCR, T *__restrict__ part) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  T *sbase = reinterpret_cast<T *>(sm_raw);   // 2 stages x [C rows | C~ rows], GCR * k each
+  const int stage = 2 * GCR * k;
+  const int tid = threadIdx.x;
+  const int kb = (k + 3) / 4, W = kb * kb + 2 * kb, R = max(1, 256 / W);
+  const int item = tid % W, grp = tid / W;
+  const bool act = grp < R;
+  const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(n, r0 + chunk);
+  auto load = [&](int64_t rb, int buf) {
+    T *st = sbase + buf * stage;
+    const int rows = (int)min((int64_t)GCR, r1 - rb);
+    const int ne = GCR * k, nv = rows * k;
+    constexpr int PER = 16 / sizeof(T);
+    for (int q = 0; q < 2; ++q) {
+      const T *src = (q ? Ct : C) + rb * k;
+      T *dst = st + q * GCR * k;
+      for (int e = tid * PER; e < ne; e += 256 * PER) {
+        const int valid = max(0, min(PER, nv - e)) * (int)sizeof(T);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst + e)),
+                     "l"(valid ? src + e : src), "r"(valid)
+                     : "memory");
+      }
+    }
+    cp_async_commit();
+  };
+  // item -> (kind, A, B): tiles first, then the C norms, then the C~ norms
+  const bool tile = item < kb * kb;
+  const int A = tile ? item / kb : 0, B = tile ? item % kb : (item - kb * kb) % kb;
+  const int side = tile ? 0 : (item - kb * kb) / kb;   // norms: 0 C, 1 C~
+  T acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = zero<T>();
+  if (r0 < r1) load(r0, 0);
+  int buf = 0;
+  for (int64_t rb = r0; rb < r1; rb += GCR, buf ^= 1) {
+    if (rb + GCR < r1) load(rb + GCR, buf ^ 1);
+    else cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const T *sc = sbase + buf * stage;
+    const T *sct = sc + GCR * k;
+    const int rows = (int)min((int64_t)GCR, r1 - rb);
+    if (act) {
+      if (tile) {
+        for (int rr = grp; rr < rows; rr += R) {
+          T a[4], b[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int ca = 4 * A + i, cb = 4 * B + i;
+            a[i] = ca < k ? sct[rr * k + ca] : zero<T>();
+            b[i] = cb < k ? sc[rr * k + cb] : zero<T>();
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = cmad(a[i], b[j], acc[i][j]);
+        }
+      } else {
+        const T *sx = side ? sct : sc;
+        for (int rr = grp; rr < rows; rr += R) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int cj = 4 * B + j;
+            const T v = cj < k ? sx[rr * k + cj] : zero<T>();
+            acc[0][j] = cmad(v, v, acc[0][j]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // reduce over the row groups: red[grp][item][16], then one sum per output
+  T *red = sbase;   // reuses the stages (>= 256 * 16 elements: checked by the host)
+  if (act)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) red[((size_t)grp * W + item) * 16 + e] = acc[e / 4][e % 4];
+  __syncthreads();
+  const int np = 2 * k + k * k;
+  for (int o = tid; o < np; o += 256) {
+    int it, e;
+    if (o < k) {   // |c_o|^2
+      it = kb * kb + o / 4;
+      e = o % 4;
+    } else if (o < 2 * k) {
+      it = kb * kb + kb + (o - k) / 4;
+      e = (o - k) % 4;
+    } else {
+      const int a2 = (o - 2 * k) / k, b2 = (o - 2 * k) % k;
+      it = (a2 / 4) * kb + b2 / 4;
+      e = (a2 % 4) * 4 + b2 % 4;
+    }
+    T sum = zero<T>();
+    for (int g = 0; g < R; ++g) sum = add(sum, red[((size_t)g * W + it) * 16 + e]);
+    part[(int64_t)blockIdx.x * np + o] = sum;
+  }
+}
+
+template <typename T>
+void gram_cc(const T *C, const T *Ct, int k, int64_t n, std::vector<cplx> &out, rbicg_ctx *ctx,
+             cudaStream_t strm) {
+  const int np = 2 * k + k * k;
+  out.assign(np, cplx(0, 0));
+  if (k == 0) return;
+  const int kb = (k + 3) / 4, W = kb * kb + 2 * kb;
+  RB_CHECK(W <= 256, RBICG_EINVAL);
+  const int GCR = gcr_rows(k);
+  const size_t sm = std::max(sizeof(T) * 2 * 2 * GCR * (size_t)k,
+                             sizeof(T) * 16 * (size_t)W * std::max(1, 256 / W));
+  RB_CHECK(sm <= 160 * 1024, RBICG_EINVAL);
+  const int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, 4 * sm_budget(ctx->nsm)));
+  const int64_t chunk = ((n + nchunks - 1) / nchunks + GCR - 1) / GCR * GCR;
+  const int nb = (int)((n + chunk - 1) / chunk);
+  char *buf = (char *)ws_alloc(sizeof(T) * ((size_t)nb * np + np) + 64);
+  T *dpart = (T *)buf;
+  T *dG = dpart + (size_t)nb * np;
+  k_gram_cc<T><<<nb, 256, sm, strm>>>(C, Ct, k, n, chunk, GCR, dpart);
+  k_gram_reduce<T><<<(np * 32 + 255) / 256, 256, 0, strm>>>(dpart, nb, np, dG);
+  count_launch(2);
+  std::vector<T> h(np);
+  RB_CUDA(cudaMemcpyAsync(h.data(), dG, sizeof(T) * np, cudaMemcpyDeviceToHost, strm));
+  RB_CUDA(cudaStreamSynchronize(strm));
+  ws_free(buf);
+  for (int i = 0; i < np; ++i) out[i] = cplx(re(h[i]), im(h[i]));
+}
+
 // ------------------------------------------------------------------ panels x M
 // out[row, c] = Σ_a X_a[row] M[a, c]; one thread per row keeps the whole output
 // row in registers (PB >= p accumulators), so out may alias an input panel
@@ -875,6 +1015,8 @@ void prepare_block_kernels() {
   RB_CUDA(cudaFuncSetAttribute(k_gram<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_gram_pairs<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_gram_pairs<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_gram_cc<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_gram_cc<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_spmm<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_spmm<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 #define RB_GATTR(T, PB)                                                                      \
@@ -899,6 +1041,8 @@ void prepare_block_kernels() {
 }
 
 #define RB_BINST(T)                                                                        \
+  template void gram_cc<T>(const T *, const T *, int, int64_t, std::vector<cplx> &, rbicg_ctx *, \
+                           cudaStream_t);                                                     \
   template void gram_pairs<T>(const std::vector<const T *> &, const std::vector<int> &,        \
                               const std::vector<std::pair<int, int>> &, int64_t,              \
                               std::vector<cplx> &, rbicg_ctx *, cudaStream_t);               \

@@ -210,6 +210,9 @@ template <typename T>
 void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
           std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t s);   // G = X^H Y (row-major mX x mY)
 template <typename T>
+void gram_cc(const T *C, const T *Ct, int k, int64_t n, std::vector<cplx> &out, rbicg_ctx *ctx,
+             cudaStream_t strm);
+template <typename T>
 void gram_pairs(const std::vector<const T *> &panels, const std::vector<int> &ncols,
                 const std::vector<std::pair<int, int>> &pairs, int64_t n, std::vector<cplx> &out,
                 rbicg_ctx *ctx, cudaStream_t s);   // out[i] = x_{a_i}^H x_{b_i}, compact panels
