@@ -675,11 +675,15 @@ struct OutSegs {
 // 16-byte pairs: the broadcast LDS, not the FMAs or HBM, bounded the
 // one-row-per-thread form (281 us for 44 -> 21 columns at n = 1M).
 template <typename T> struct MPair { T a, b; };
-template <typename T, int PB>
-__global__ void __launch_bounds__(256, 2) k_gemm_multi(const ColDesc *__restrict__ X, int mX,
+template <typename T, int PB, int RX>
+constexpr int gm_rpt() { return RX ? RX : ((sizeof(T) == 8 && PB <= 24) ? 2 : 1); }
+template <typename T, int PB, int RX>
+constexpr int gm_minb() { return sizeof(T) == 8 && gm_rpt<T, PB, RX>() == 1 && PB <= 12 ? 4 : 2; }
+template <typename T, int PB, int RX = 0>
+__global__ void __launch_bounds__(256, (gm_minb<T, PB, RX>())) k_gemm_multi(const ColDesc *__restrict__ X, int mX,
                                                        const T *__restrict__ M, int p, int64_t n,
                                                        OutSegs O) {
-  constexpr int RPT = (sizeof(T) == 8 && PB <= 24) ? 2 : 1;   // registers (complex: 1)
+  constexpr int RPT = gm_rpt<T, PB, RX>();   // rows per thread (registers; complex: 1)
   extern __shared__ __align__(16) unsigned char sm_raw[];
   T *sM = reinterpret_cast<T *>(sm_raw);   // [mX][PB], zero padded (PB even)
   ColDesc *sX = reinterpret_cast<ColDesc *>(sM + (size_t)mX * PB);
@@ -992,19 +996,26 @@ void gemm_multi(const std::vector<ColDesc> &X, const std::vector<cplx> &M,
     ws_free(buf);
     return;
   }
-  auto go = [&](auto kern, int PB) {
+  auto go = [&](auto kern, int PB, int rpt) {
     const size_t sm = sizeof(T) * (size_t)mX * PB + sizeof(ColDesc) * mX;
     RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
     int per = 1;
     RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, sm));
-    const int rows_per_block = (sizeof(T) == 8 && PB <= 24) ? 512 : 256;
+    const int rows_per_block = 256 * rpt;
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((n + rows_per_block - 1) / rows_per_block, (int64_t)std::max(1, per) * sm_budget(ctx->nsm)));
     kern<<<grid, 256, sm, strm>>>(dX, mX, dM, p, n, O);
   };
-  if (p <= 12) go(k_gemm_multi<T, 12>, 12);
-  else if (p <= 24) go(k_gemm_multi<T, 24>, 24);
-  else go(k_gemm_multi<T, 32>, 32);
+  static const int rx = getenv("RBICG_GEMM_RPT") ? atoi(getenv("RBICG_GEMM_RPT")) : 0;
+  const int r2 = sizeof(T) == 8 ? 2 : 1;
+  if (p <= 12) {
+    if (rx == 1) go(k_gemm_multi<T, 12, 1>, 12, 1);
+    else go(k_gemm_multi<T, 12>, 12, r2);
+  } else if (p <= 24) {
+    go(k_gemm_multi<T, 24>, 24, r2);
+  } else {
+    go(k_gemm_multi<T, 32>, 32, 1);
+  }
   count_launch();
   RB_CUDA(cudaStreamSynchronize(strm));   // hM (pageable) must outlive its copy
   ws_free(buf);
@@ -1029,7 +1040,8 @@ void prepare_block_kernels() {
 #undef RB_GATTR
   for (auto f : {(const void *)k_gemm_multi<double, 12>, (const void *)k_gemm_multi<double, 24>,
                  (const void *)k_gemm_multi<double, 32>, (const void *)k_gemm_multi<zc, 12>,
-                 (const void *)k_gemm_multi<zc, 24>, (const void *)k_gemm_multi<zc, 32>})
+                 (const void *)k_gemm_multi<zc, 24>, (const void *)k_gemm_multi<zc, 32>,
+                 (const void *)k_gemm_multi<double, 12, 1>, (const void *)k_gemm_multi<zc, 12, 1>})
     RB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   for (auto f : {(const void *)k_gemm_multi_tma<double, 12, 1>, (const void *)k_gemm_multi_tma<double, 24, 1>,
                  (const void *)k_gemm_multi_tma<double, 32, 1>, (const void *)k_gemm_multi_tma<zc, 12, 1>,

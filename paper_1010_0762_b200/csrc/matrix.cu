@@ -153,11 +153,61 @@ static void share_cols(rbicg_ctx *ctx, rbicg_mat *M) {
   H.cols_shared = 1;
 }
 
+// Structurally symmetric A with sorted rows: A^*'s pattern is A's, and the
+// value of A^*[j][i] = conj(A[i][j]) sits at the position of column i in row j
+// (binary search) -- no sort.  flag = 1 if a row is unsorted or has a
+// duplicate, or an (i, j) has no (j, i): the caller then takes the sort path.
+template <typename T>
+__global__ void k_sym_transpose(const int32_t *rowptr, const int32_t *col, const T *val, int64_t n,
+                                T *valT, int *flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t b = rowptr[i], e = rowptr[i + 1];
+    for (int32_t q = b; q < e; ++q) {
+      const int32_t j = col[q];
+      if (q > b && col[q - 1] >= j) {
+        *flag = 1;
+        return;
+      }
+      int32_t lo = rowptr[j], hi = rowptr[j + 1] - 1;
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (col[mid] < (int32_t)i) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo > hi || col[lo] != (int32_t)i) {
+        *flag = 1;
+        return;
+      }
+      valT[lo] = conj(val[q]);
+    }
+  }
+}
+
 template <typename T>
 static void build_t(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr,
                     const int32_t *col, const T *val, rbicg_mat *M) {
   cudaStream_t st = ctx->stream;
   csr_to_sell<T>(ctx, n, rowptr, col, val, M->A);
+  if (!getenv("RBICG_NO_SYM_T") && nnz > 0) {   // structurally symmetric fast path
+    T *valT = (T *)ws_alloc(sizeof(T) * nnz);
+    int *flag = (int *)ws_alloc(sizeof(int));
+    RB_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    k_sym_transpose<T><<<grid1d(n), 256, 0, st>>>(rowptr, col, val, n, valT, flag);
+    count_launch();
+    int h = 1;
+    RB_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaStreamSynchronize(st));
+    ws_free(flag);
+    if (!h) {
+      csr_to_sell<T>(ctx, n, rowptr, col, valT, M->AH);
+      share_cols(ctx, M);
+      RB_CUDA(cudaStreamSynchronize(st));
+      ws_free(valT);
+      return;
+    }
+    ws_free(valT);
+  }
   // ---- conjugate transpose
   int32_t *rowidx = (int32_t *)ws_alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
   int32_t *iota = (int32_t *)ws_alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
