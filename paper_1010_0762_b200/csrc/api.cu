@@ -522,9 +522,10 @@ struct Solver {
     z = alloc(n);
     zt = alloc(n);
     if (k_basis == 0 && !dist) {   // fused iteration: (z_i, p_i) pairs by parity
+      const size_t nl = 2;   // node {z, p} (kernels.cu)
       for (int q = 0; q < 2; ++q) {
-        zp[q] = alloc(2 * (size_t)n);
-        ztp[q] = alloc(2 * (size_t)n);
+        zp[q] = alloc(nl * (size_t)n);
+        ztp[q] = alloc(nl * (size_t)n);
       }
     }
     x = alloc(nx);
@@ -875,6 +876,11 @@ struct Solver {
   // Fused iteration (one kernel per iteration, k_fused) while no recycle
   // space is active: single GPU, TMA-staged tiles, lazy x.
   bool fused = false;
+  // K(1)'s gathered state: z_0 = p_0 = 0
+  void init_nodes(cudaStream_t s) {
+    RB_CUDA(cudaMemsetAsync(zp[0], 0, sizeof(T) * 2 * n, s));
+    RB_CUDA(cudaMemsetAsync(ztp[0], 0, sizeof(T) * 2 * n, s));
+  }
   bool fused_ok() const {
     const bool off = getenv("RBICG_FUSED") && atoi(getenv("RBICG_FUSED")) == 0;   // per solve
     return !off && zp[0] && la.k == 0 && la.staged && !la.split && lazy_x && !dist && pring_len == 0;
@@ -892,8 +898,7 @@ struct Solver {
     if (gexec) return;
     fused = fused_ok();
     if (fused) {   // z_0 = p_0 = 0 (K(1) forms p_1 = r_0 + β_0 p_0 with α_0 = β_0 = 0)
-      RB_CUDA(cudaMemsetAsync(zp[0], 0, sizeof(T) * 2 * n, ctx->stream));
-      RB_CUDA(cudaMemsetAsync(ztp[0], 0, sizeof(T) * 2 * n, ctx->stream));
+      init_nodes(ctx->stream);
     }
     cudaGraph_t g;
     const int64_t l0 = g_launches.load();
@@ -2231,8 +2236,7 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
   ms[14] = -1.0;
   ms[15] = -1.0;
   if (S.fused_ok()) {
-    RB_CUDA(cudaMemsetAsync(S.zp[0], 0, sizeof(T) * 2 * n, ctx->stream));
-    RB_CUDA(cudaMemsetAsync(S.ztp[0], 0, sizeof(T) * 2 * n, ctx->stream));
+    S.init_nodes(ctx->stream);
     auto reset = [&] {
       S.hst->iter = 0;
       S.hst->kidx = 0;

@@ -86,8 +86,8 @@ struct LoopArgs {
   T *pring, *ptring;       // or a ring of direction columns: p_i in column i % pring_len
   int pring_len;           //   (stride ldr), never rewritten within one launch
   T *z, *zt;
-  T *zp[2], *ztp[2];       // fused form: interleaved (z_i, p_i) pairs by iteration parity
-                           //   ([row][2]; z_0 = p_0 = 0), one 16-byte gather per column
+  T *zp[2], *ztp[2];       // fused form: per-row nodes {z_i, p_i} by iteration parity, one
+                           //   gather per column (128-bit real, 256-bit complex)
   T *x, *xt;
   const T *C, *Ct;         // row-major n x k
   DevState<T> *st;

@@ -518,36 +518,52 @@ __global__ void __launch_bounds__(BS) k_spmv_pair(DevMat A, DevMat AH, const T *
 // with α_i = ρ_{i-1}/σ_i.  r_{i-1} lands in ring column i-1 (K(1) reads r_0
 // from column 0 and writes nothing there).
 constexpr int NFUSED = 7;
-// (z, p) of column c: one 16-byte load for real data
-template <typename T> struct ZP { T z, p; };
-__device__ __forceinline__ ZP<double> ld_zp(const double *zp, int64_t c) {
-  const double2 v = __ldg(reinterpret_cast<const double2 *>(zp) + c);
-  return ZP<double>{v.x, v.y};
+// The gathered (z, p) of column c in one load: 16 bytes for real data
+// (LDG.128), 32 bytes for complex (a 256-bit LDG); r comes from the ring
+// column.  (Real nodes {r, z, p, pad} read as one 256-bit load measured
+// slower: C2 59.8 vs 46.4 us per iteration.)
+template <typename T> struct RZP { T r, z, p; };
+__device__ __forceinline__ void ld256(const void *p, double &a, double &b, double &c, double &d) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p));
 }
-__device__ __forceinline__ ZP<zc> ld_zp(const zc *zp, int64_t c) {
-  return ZP<zc>{ldg(zp + 2 * c), ldg(zp + 2 * c + 1)};
+__device__ __forceinline__ void st256(void *p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
 }
-__device__ __forceinline__ void st_zp(double *zp, int64_t c, double z, double p) {
-  reinterpret_cast<double2 *>(zp)[c] = make_double2(z, p);
+__device__ __forceinline__ RZP<double> ld_node(const double *nodes, const double *ring, int64_t c) {
+  const double2 v = __ldg(reinterpret_cast<const double2 *>(nodes) + c);
+  return RZP<double>{ldg(ring + c), v.x, v.y};
 }
-__device__ __forceinline__ void st_zp(zc *zp, int64_t c, zc z, zc p) {
-  zp[2 * c] = z;
-  zp[2 * c + 1] = p;
+// (all four words are consumed by every caller: ptxas masks a 256-bit load
+// whose words are not all used, and masks finer than 128 bits faulted on B200
+// with cudaErrorInvalidAddressSpace)
+__device__ __forceinline__ RZP<zc> ld_node(const zc *nodes, const zc *ring, int64_t c) {
+  double zx, zy, px, py;
+  ld256(nodes + 2 * c, zx, zy, px, py);
+  return RZP<zc>{ldg(ring + c), mk(zx, zy), mk(px, py)};
+}
+__device__ __forceinline__ void st_node(double *nodes, int64_t c, double, double z, double p) {
+  reinterpret_cast<double2 *>(nodes)[c] = make_double2(z, p);
+}
+__device__ __forceinline__ void st_node(zc *nodes, int64_t c, zc, zc z, zc p) {
+  st256(nodes + 2 * c, z.x, z.y, p.x, p.y);
 }
 template <typename T>
 __device__ __forceinline__ void fused_pair_smem(const int32_t *__restrict__ cA, const T *__restrict__ vA,
                                                 int wA, const int32_t *__restrict__ cH,
                                                 const T *__restrict__ vH, int wH,
-                                                const T *__restrict__ r, const T *__restrict__ zp,
-                                                const T *__restrict__ rt, const T *__restrict__ ztp,
+                                                const T *__restrict__ r, const T *__restrict__ nd,
+                                                const T *__restrict__ rt, const T *__restrict__ ndt,
                                                 T malpha, T beta, T cmalpha, T cb, T &zo, T &zto) {
   zo = zero<T>();
   zto = zero<T>();
   const int wm = max(wA, wH);
   for (int j0 = 0; j0 < wm; j0 += 4) {
     int ca[4], ch[4];
-    T va[4], vh[4], ra[4], rh[4];
-    ZP<T> za[4], zh[4];
+    T va[4], vh[4];
+    RZP<T> xa[4], xh[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int jj = j0 + q;
@@ -559,15 +575,13 @@ __device__ __forceinline__ void fused_pair_smem(const int32_t *__restrict__ cA, 
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      ra[q] = ldg(r + ca[q]);
-      za[q] = ld_zp(zp, ca[q]);
-      rh[q] = ldg(rt + ch[q]);
-      zh[q] = ld_zp(ztp, ch[q]);
+      xa[q] = ld_node(nd, r, ca[q]);
+      xh[q] = ld_node(ndt, rt, ch[q]);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      zo = mad(va[q], mad(beta, za[q].p, mad(malpha, za[q].z, ra[q])), zo);
-      zto = mad(vh[q], mad(cb, zh[q].p, mad(cmalpha, zh[q].z, rh[q])), zto);
+      zo = mad(va[q], mad(beta, xa[q].p, mad(malpha, xa[q].z, xa[q].r)), zo);
+      zto = mad(vh[q], mad(cb, xh[q].p, mad(cmalpha, xh[q].z, xh[q].r)), zto);
     }
   }
 }
@@ -657,21 +671,23 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
       fused_pair_smem<T>(scA + (oA - bA) + lane, svA + (oA - bA) + lane, wA,
                          scH + (oH - bH) + lane, svH + (oH - bH) + lane, wH, r, zpo, rt, ztpo,
                          malpha, beta, cmalpha, cb, z, zt);
-      const ZP<T> o = ld_zp(zpo, row), ot = ld_zp(ztpo, row);
-      const T rr = mad(malpha, o.z, ldg(r + row));
-      const T rtr = mad(cmalpha, ot.z, ldg(rt + row));
+      const RZP<T> o = ld_node(zpo, r, row), ot = ld_node(ztpo, rt, row);
+      const T rr = mad(malpha, o.z, o.r);
+      const T rtr = mad(cmalpha, ot.z, ot.r);
       const T pr = mad(beta, o.p, rr);
       const T ptr = mad(cb, ot.p, rtr);
       if (segcopy) {   // lazy x: p_a of the open segment (a = i - 2), before it is overwritten
-        pseg[row] = ld_zp(zpn, row).p;
-        ptseg[row] = ld_zp(ztpn, row).p;
+        const RZP<T> q = ld_node(zpn, r, row), qt = ld_node(ztpn, rt, row);
+        const T z0 = zero<T>();   // (z consumed too: a whole-node load, see ld_node)
+        pseg[row] = mad(z0, q.z, q.p);
+        ptseg[row] = mad(z0, qt.z, qt.p);
       }
       if (wr) {
         rw[row] = rr;
         rtw[row] = rtr;
       }
-      st_zp(zpn, row, z, pr);
-      st_zp(ztpn, row, zt, ptr);
+      st_node(zpn, row, rr, z, pr);
+      st_node(ztpn, row, rtr, zt, ptr);
       acc[0] = cmad(rtr, rr, acc[0]);      // ρ_{i-1}
       acc[1] = add(acc[1], mk_re<T>(abs2(rr)));
       acc[2] = add(acc[2], mk_re<T>(abs2(rtr)));
@@ -845,7 +861,9 @@ template <typename T> void launch_fused(const LoopArgs<T> &a0, cudaStream_t s) {
   a.p1_stages = std::min(2, std::max(1, fst));
   const size_t sm = fused_smem<T>(a);
   // 4 CTAs/SM at 64 registers (C2: 46.3 us per iteration; 3 CTAs at 80: 56.3 us)
-  static const int minb = getenv("RBICG_FUSED_MINB") ? atoi(getenv("RBICG_FUSED_MINB")) : 4;
+  // (complex: 3 CTAs/SM, 80 registers -- 64 spill with the 256-bit node loads)
+  static const int minb_env = getenv("RBICG_FUSED_MINB") ? atoi(getenv("RBICG_FUSED_MINB")) : 0;
+  const int minb = minb_env ? minb_env : (sizeof(T) == 8 ? 4 : 3);
   auto fn = minb >= 6 ? k_fused<T, 6> : minb == 5 ? k_fused<T, 5> : minb == 4 ? k_fused<T, 4> : k_fused<T, 3>;
   int per_sm = 1;
   RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BS, sm));
