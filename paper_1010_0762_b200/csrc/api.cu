@@ -661,7 +661,7 @@ struct Solver {
   // straight from the Lanczos columns -- only when p > 0.
   void biorth(const T *U, const T *Ut, const T *C, const T *Ct, int kin, Basis &out,
               cudaStream_t bs, Comm *cm, bool with_c = true, std::vector<cplx> *Fu_out = nullptr,
-              std::vector<cplx> *Fut_out = nullptr) {
+              std::vector<cplx> *Fut_out = nullptr, const std::vector<cplx> *gv_in = nullptr) {
     // only ||c_j||^2, ||c~_j||^2 and C~^*C are needed (Q13 scaling + SVD)
     std::vector<ColDesc> X;
     for (int c = 0; c < kin; ++c) X.push_back(col(C, c, kin));
@@ -672,7 +672,9 @@ struct Solver {
     for (int a2 = 0; a2 < kin; ++a2)
       for (int b2 = 0; b2 < kin; ++b2) pairs.emplace_back(kin + a2, b2);
     std::vector<cplx> G((size_t)4 * kin * kin, 0.0), gv;
-    {
+    if (gv_in) {   // the Gram came out of the fused relation pass (k_relgram)
+      gv = *gv_in;
+    } else {
       Phase ph("biorth.gram", bs);
       static const bool old_gram = getenv("RBICG_GRAM_PAIRS") != nullptr;
       if (old_gram) gram_pairs<T>({C, Ct}, {kin, kin}, pairs, n, gv, ctx, bs);
@@ -997,7 +999,7 @@ struct Solver {
                      const std::vector<cplx> &Wun, const std::vector<cplx> &Wtun,
                      const std::vector<cplx> &Wrow, const std::vector<cplx> &Wtrow, int ksel,
                      SV sv, SVT svt, int fa, int fb, int lo, const std::vector<IterRec<T>> &rec,
-                     cudaStream_t cs, bool with_u) {
+                     cudaStream_t cs, bool with_u, std::vector<cplx> *gram_out = nullptr) {
     const int s = (int)cols.size(), nr = (int)rows.size();
     const bool fl = fb > fa;
     std::vector<cplx> cr;
@@ -1055,6 +1057,10 @@ struct Solver {
       outs.push_back({x, 1});
       outst.push_back({xt, 1});
     }
+    if (gram_out && !with_u &&
+        relgram<T>(X, Xt, M, Mt, p, ksel, fl ? 1 : 0, n, x, xt, *gram_out, ctx, cs))
+      return;   // C_j, C~_j stayed on chip; the Gram is in *gram_out
+    if (gram_out) gram_out->clear();
     gemm_multi<T>(X, M, outs, n, ctx, cs);
     gemm_multi<T>(Xt, Mt, outst, n, ctx, cs);
   }
@@ -1308,8 +1314,13 @@ struct Solver {
         static const bool u_late = !getenv("RBICG_U_EARLY");
         const bool chk = getenv("RBICG_C_CHECK") && !dist;
         Phase ph("cycle.gemm_UCx", cs);
+        // (opt-in, RBICG_RELGRAM=1: the one-pass relation GEMM + Gram keeping C_j
+        // on chip measured slower -- C2 330 us vs 311 us for the two GEMMs and
+        // the Gram; C5 cycle ends 1.43 vs 1.00 s)
+        static const bool fuse_gram = getenv("RBICG_RELGRAM") != nullptr;
+        std::vector<cplx> gvf;
         relation_gemm(rows, cols, top, Gam, Gamt, sel.W, sel.Wt, Wrow, Wtrow, ksel, sv, svt, fa, fb,
-                      lo, rec, cs, !u_late || chk);
+                      lo, rec, cs, !u_late || chk, (u_late && !chk && !dist && fuse_gram) ? &gvf : nullptr);
         fa = fb = 0;
         if (getenv("RBICG_C_CHECK") && !dist) {   // debug: relation vs explicit SpMM
           RB_CUDA(cudaStreamSynchronize(cs));
@@ -1332,7 +1343,8 @@ struct Solver {
           biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false);
         } else {
           std::vector<cplx> Fu, Fut;
-          biorth(nullptr, nullptr, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false, &Fu, &Fut);
+          biorth(nullptr, nullptr, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false, &Fu, &Fut,
+                 gvf.empty() ? nullptr : &gvf);
           if (out.k > 0) {   // U_j N_p = [V_j rows] (W_j N_p) (scalings folded in Wrow)
             const int pk = out.k;
             std::vector<ColDesc> Xv, Xvt;

@@ -572,6 +572,191 @@ void gram_cc(const T *C, const T *Ct, int k, int64_t n, std::vector<cplx> &out, 
   for (int i = 0; i < np; ++i) out[i] = cplx(re(h[i]), im(h[i]));
 }
 
+// ------------------------------------------------------------------ relation GEMM + Gram
+// The T_j-pencil cycle end without storing C_j: one pass over the Υ_j, Ῡ_j
+// ring columns forms, per 256-row tile, the rows of C_j = Υ_j M and
+// C~_j = Ῡ_j M~ (and the lazy-x flush column, written to x, x~), keeps them in
+// shared memory only, and accumulates the bi-orthogonality Gram (|c_j|^2,
+// |c~_j|^2, c~_a^* c_b) with 4 x 4 register tiles as k_gram_cc does.  C_j is
+// never written: with p = 0 after the truncation (every C2/C3/C5 cycle) it is
+// not needed, and with p > 0 U_j N_p is formed from the V_j columns and the
+// next system's refresh computes C = A U.
+template <typename T, int PB>
+__global__ void __launch_bounds__(256, 2) k_relgram(const ColDesc *__restrict__ X, const ColDesc *__restrict__ Xt,
+                                                    int mX, const T *__restrict__ M, const T *__restrict__ Mt,
+                                                    int p, int k, int fl, int64_t n, T *__restrict__ xo,
+                                                    T *__restrict__ xto, T *__restrict__ part) {
+  constexpr int AU = PB <= 12 ? 8 : 4;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  T *sM = reinterpret_cast<T *>(sm_raw);   // [2][mX][PB]
+  T *sG = sM + (size_t)2 * mX * PB;        // [16][256]: each thread's Gram tile (kept out of registers)
+  T *sC = sG + (size_t)16 * 256;           // [256][k + 1], then C~ [256][k + 1]
+  const int ld = k + 1;
+  T *sCt = sC + (size_t)256 * ld;
+  ColDesc *sX = reinterpret_cast<ColDesc *>(sCt + (size_t)256 * ld);   // [2][mX]
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 2 * mX * PB; e += 256) {
+    const int side = e / (mX * PB), r = e % (mX * PB), a = r / PB, c = r % PB;
+    sM[e] = c < p ? (side ? Mt : M)[a * p + c] : zero<T>();
+  }
+  for (int e = tid; e < 2 * mX; e += 256) sX[e] = e < mX ? X[e] : Xt[e - mX];
+  const int kb = (k + 3) / 4, W = kb * kb + 2 * kb, R = max(1, 256 / W);
+  const int item = tid % W, grp = tid / W;
+  const bool act = grp < R;
+  const bool tile = item < kb * kb;
+  const int A = tile ? item / kb : 0, B = tile ? item % kb : (item - kb * kb) % kb;
+  const int nside = tile ? 0 : (item - kb * kb) / kb;
+  for (int e = 0; e < 16; ++e) sG[e * 256 + tid] = zero<T>();
+  __syncthreads();
+  const int64_t ntiles = (n + 255) / 256;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t row = t * 256 + tid;
+    const bool ok = row < n;
+    const int rows = (int)min((int64_t)256, n - t * 256);
+    for (int side = 0; side < 2; ++side) {
+      const ColDesc *cx = sX + side * mX;
+      const T *mm = sM + (size_t)side * mX * PB;
+      T acc[PB];
+#pragma unroll
+      for (int c = 0; c < PB; ++c) acc[c] = zero<T>();
+      int a = 0;
+      for (; a + AU <= mX; a += AU) {
+        T xv[AU];
+#pragma unroll
+        for (int u = 0; u < AU; ++u)
+          xv[u] = ok ? reinterpret_cast<const T *>(cx[a + u].p)[row * cx[a + u].stride] : zero<T>();
+#pragma unroll
+        for (int u = 0; u < AU; ++u)
+#pragma unroll
+          for (int c = 0; c < PB; ++c) acc[c] = mad(xv[u], mm[(a + u) * PB + c], acc[c]);
+      }
+      for (; a < mX; ++a) {
+        const T xv = ok ? reinterpret_cast<const T *>(cx[a].p)[row * cx[a].stride] : zero<T>();
+#pragma unroll
+        for (int c = 0; c < PB; ++c) acc[c] = mad(xv, mm[a * PB + c], acc[c]);
+      }
+      T *dst = side ? sCt : sC;
+#pragma unroll
+      for (int c = 0; c < PB; ++c)
+        if (c < k) dst[tid * ld + c] = ok ? acc[c] : zero<T>();
+      if (fl && ok) {
+        T fx = zero<T>();
+#pragma unroll
+        for (int c = 0; c < PB; ++c)
+          if (c == k) fx = acc[c];
+        (side ? xto : xo)[row] = fx;
+      }
+    }
+    __syncthreads();
+    if (act) {
+      T g[4][4];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) g[e / 4][e % 4] = sG[e * 256 + tid];
+      if (tile) {
+        for (int rr = grp; rr < rows; rr += R) {
+          T av[4], bv[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int ca = 4 * A + i, cb = 4 * B + i;
+            av[i] = ca < k ? sCt[rr * ld + ca] : zero<T>();
+            bv[i] = cb < k ? sC[rr * ld + cb] : zero<T>();
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) g[i][j] = cmad(av[i], bv[j], g[i][j]);
+        }
+      } else {
+        const T *sx = nside ? sCt : sC;
+        for (int rr = grp; rr < rows; rr += R) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int cj = 4 * B + j;
+            const T v = cj < k ? sx[rr * ld + cj] : zero<T>();
+            g[0][j] = cmad(v, v, g[0][j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) sG[e * 256 + tid] = g[e / 4][e % 4];
+    }
+    __syncthreads();
+  }
+  T *red = sC;   // >= R * W * 16 elements (checked by the host)
+  if (act)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) red[((size_t)grp * W + item) * 16 + e] = sG[e * 256 + tid];
+  __syncthreads();
+  const int np = 2 * k + k * k;
+  for (int o = tid; o < np; o += 256) {
+    int it, e;
+    if (o < k) {
+      it = kb * kb + o / 4;
+      e = o % 4;
+    } else if (o < 2 * k) {
+      it = kb * kb + kb + (o - k) / 4;
+      e = (o - k) % 4;
+    } else {
+      const int a2 = (o - 2 * k) / k, b2 = (o - 2 * k) % k;
+      it = (a2 / 4) * kb + b2 / 4;
+      e = (a2 % 4) * 4 + b2 % 4;
+    }
+    T sum = zero<T>();
+    for (int gg = 0; gg < R; ++gg) sum = add(sum, red[((size_t)gg * W + it) * 16 + e]);
+    part[(int64_t)blockIdx.x * np + o] = sum;
+  }
+}
+
+template <typename T>
+bool relgram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Xt, const std::vector<cplx> &M,
+             const std::vector<cplx> &Mt, int p, int k, int fl, int64_t n, T *x, T *xt,
+             std::vector<cplx> &gv, rbicg_ctx *ctx, cudaStream_t strm) {
+  const int mX = (int)X.size();
+  const int PB = p <= 12 ? 12 : (p <= 24 && sizeof(T) == 8 ? 24 : 0);
+  if (!PB || (int)Xt.size() != mX || k < 1) return false;   // caller: GEMM + Gram
+  const int kb = (k + 3) / 4, W = kb * kb + 2 * kb, R = std::max(1, 256 / W);
+  const size_t ctile = (size_t)2 * 256 * (k + 1);
+  const size_t sm = sizeof(T) * ((size_t)2 * mX * PB + 16 * 256 + std::max(ctile, (size_t)16 * W * R)) +
+                    sizeof(ColDesc) * 2 * mX + 16;
+  if (sm > 200 * 1024) return false;
+  const int np = 2 * k + k * k;
+  std::vector<T> hM((size_t)2 * mX * p);
+  for (size_t i = 0; i < (size_t)mX * p; ++i) {
+    for (int side = 0; side < 2; ++side) {
+      T v = zero<T>();
+      const cplx c = side ? Mt[i] : M[i];
+      reinterpret_cast<double *>(&v)[0] = c.real();
+      if (sizeof(T) == 16) reinterpret_cast<double *>(&v)[1] = c.imag();
+      hM[side * (size_t)mX * p + i] = v;
+    }
+  }
+  auto kern = PB == 12 ? k_relgram<T, 12> : k_relgram<T, 24>;
+  int per = 1;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, sm));
+  const int64_t tiles = (n + 255) / 256;
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)std::max(1, per) * sm_budget(ctx->nsm)));
+  const size_t db = sizeof(ColDesc) * 2 * mX, mb = sizeof(T) * hM.size();
+  char *buf = (char *)ws_alloc(db + 16 + mb + 16 + sizeof(T) * ((size_t)nb * np + np) + 64);
+  ColDesc *dX = (ColDesc *)buf;
+  T *dM = (T *)(buf + (db + 15) / 16 * 16);
+  T *dpart = (T *)((char *)dM + (mb + 15) / 16 * 16);
+  T *dG = dpart + (size_t)nb * np;
+  std::vector<ColDesc> XX(X);
+  XX.insert(XX.end(), Xt.begin(), Xt.end());
+  RB_CUDA(cudaMemcpyAsync(dX, XX.data(), db, cudaMemcpyHostToDevice, strm));
+  RB_CUDA(cudaMemcpyAsync(dM, hM.data(), mb, cudaMemcpyHostToDevice, strm));
+  kern<<<nb, 256, sm, strm>>>(dX, dX + mX, mX, dM, dM + (size_t)mX * p, p, k, fl, n, x, xt, dpart);
+  k_gram_reduce<T><<<(np * 32 + 255) / 256, 256, 0, strm>>>(dpart, nb, np, dG);
+  count_launch(2);
+  std::vector<T> h(np);
+  RB_CUDA(cudaMemcpyAsync(h.data(), dG, sizeof(T) * np, cudaMemcpyDeviceToHost, strm));
+  RB_CUDA(cudaStreamSynchronize(strm));
+  ws_free(buf);
+  gv.resize(np);
+  for (int i = 0; i < np; ++i) gv[i] = cplx(re(h[i]), im(h[i]));
+  return true;
+}
+
 // ------------------------------------------------------------------ panels x M
 // out[row, c] = Σ_a X_a[row] M[a, c]; one thread per row keeps the whole output
 // row in registers (PB >= p accumulators), so out may alias an input panel
@@ -1028,6 +1213,10 @@ void prepare_block_kernels() {
   RB_CUDA(cudaFuncSetAttribute(k_gram_pairs<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_gram_cc<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_gram_cc<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_relgram<double, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_relgram<double, 24>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_relgram<zc, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  RB_CUDA(cudaFuncSetAttribute(k_relgram<zc, 24>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_spmm<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_spmm<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 #define RB_GATTR(T, PB)                                                                      \
@@ -1053,6 +1242,9 @@ void prepare_block_kernels() {
 }
 
 #define RB_BINST(T)                                                                        \
+  template bool relgram<T>(const std::vector<ColDesc> &, const std::vector<ColDesc> &,            \
+                           const std::vector<cplx> &, const std::vector<cplx> &, int, int, int,    \
+                           int64_t, T *, T *, std::vector<cplx> &, rbicg_ctx *, cudaStream_t);    \
   template void gram_cc<T>(const T *, const T *, int, int64_t, std::vector<cplx> &, rbicg_ctx *, \
                            cudaStream_t);                                                     \
   template void gram_pairs<T>(const std::vector<const T *> &, const std::vector<int> &,        \
