@@ -17,6 +17,17 @@ family; PAPER.md:1186-1194 discusses E = I).  Step by step:
 5. A_r, E_r, b_r = W_r^* b, c_r = V_r^* c (reading: the paper's "c_r = V_r^*c_r"
    is a typo for V_r^* c, (red_projection) PAPER.md:1004-1007).
 
+Recycling strategies, ``strategy=``:
+1. slot i of step m+1 recycles the space of slot i of step m;
+2. within a step, each solve recycles the space of the previous solve (the
+   chain continues across steps: column 1 of step m+1 takes the last column's
+   space of step m);
+3. each solve picks, from the spaces of sigma^(m)_1..r and sigma^(m+1)_1..i-1,
+   the one whose shift has the smallest relative change |sigma' - sigma_i| /
+   |sigma_i|, if that change is below ``reuse_tol`` (else no recycle space).
+In all three the initial guesses are the previous step's solutions of the
+same slot.
+
 Readings for what the paper leaves open (Q29):
 * convergence: max_i |σ_i^new - σ_i| / |σ_i| < shift_tol (relative change of
   the shifts, PAPER.md:1388, 10^-6), at most max_steps steps;
@@ -79,8 +90,19 @@ class IrkaResult:
     cr: np.ndarray = None
 
 
+def pick_space(pool, si, reuse_tol):
+    """Strategy 3: the pool entry (sigma', space) with the smallest relative
+    shift change below reuse_tol (first such entry on ties), else None."""
+    best, bd = None, reuse_tol
+    for sp_, sp in pool:
+        d = abs(sp_ - si) / abs(si)
+        if d < bd:
+            best, bd = sp, d
+    return best
+
+
 def irka(A, b, c, shifts0, *, k=8, s=40, tol=1e-10, max_itn=20000, trunc_tol=1e-2,
-         shift_tol=1e-6, max_steps=30, recycle=True):
+         shift_tol=1e-6, max_steps=30, recycle=True, strategy=1, reuse_tol=np.inf):
     """Algorithm 3 with E = I; A is the (sparse) state matrix of the model."""
     A = sp.csr_matrix(A, dtype=np.complex128)
     n = A.shape[0]
@@ -91,21 +113,33 @@ def irka(A, b, c, shifts0, *, k=8, s=40, tol=1e-10, max_itn=20000, trunc_tol=1e-
     r = len(sig)
     slots = [dict(U=None, Ut=None, x=None, xt=None) for _ in range(r)]
     res = IrkaResult(shifts=sig, steps=0, converged=False)
+    chain = [None]       # strategy 2: the last solve's space
+    prev_pool = []       # strategy 3: (sigma, space) of the previous step
 
     def solve_all(sig):
         V = np.zeros((n, r), np.complex128)
         W = np.zeros((n, r), np.complex128)
         its = []
+        cur_pool = []
         for i, si in enumerate(sig):
             st = slots[i]
-            out = R.solve_dual(si * I - A, b, c, st["x"], st["xt"],
-                               U=st["U"] if recycle else None, Ut=st["Ut"] if recycle else None,
+            if strategy == 1:
+                space = (st["U"], st["Ut"])
+            elif strategy == 2:
+                space = chain[0]
+            else:
+                space = pick_space(prev_pool + cur_pool, si, reuse_tol)
+            U0, Ut0 = space if (recycle and space is not None) else (None, None)
+            out = R.solve_dual(si * I - A, b, c, st["x"], st["xt"], U=U0, Ut=Ut0,
                                k=k if recycle else 0, s=s, tol=tol, max_itn=max_itn,
                                trunc_tol=trunc_tol)
             V[:, i], W[:, i] = out.x, out.xt
             st["x"], st["xt"] = out.x, out.xt          # previous solution
             st["U"], st["Ut"] = out.basis_out.U, out.basis_out.Ut
+            chain[0] = (out.basis_out.U, out.basis_out.Ut)
+            cur_pool.append((si, (out.basis_out.U, out.basis_out.Ut)))
             its.append(out.iterations)
+        prev_pool[:] = cur_pool
         return V, W, its
 
     V, W, its = solve_all(sig)                          # steps 2-3

@@ -266,6 +266,26 @@ class Recycle:
         Utc = np.ascontiguousarray(np.asarray(Ut, dt).T)
         check(lib.rbicg_recycle_import(self._h, k, _ptr(Uc), _ptr(Utc), 0))
 
+    def clear(self):
+        """Empty the space (k = 0)."""
+        check(lib.rbicg_recycle_import(self._h, 0, None, None, 0))
+
+    def copy_from(self, other):
+        """This handle's space := other's (device to device, through the C ABI
+        export/import with on_device = 1)."""
+        import torch
+        k = other.k
+        if k == 0:
+            self.clear()
+            return
+        dt = torch.complex128 if other.complex_ else torch.float64
+        dev = f"cuda:{self.ctx.device}"
+        U = torch.empty((k, other.n), dtype=dt, device=dev)
+        Ut = torch.empty((k, other.n), dtype=dt, device=dev)
+        kk = C.c_int32()
+        check(lib.rbicg_recycle_export(other._h, C.byref(kk), _ptr(U), _ptr(Ut), 1))
+        check(lib.rbicg_recycle_import(self._h, k, _ptr(U), _ptr(Ut), 1))
+
     def free(self):
         if self._h:
             lib.rbicg_recycle_free(self._h)

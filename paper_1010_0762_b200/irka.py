@@ -20,6 +20,17 @@ import scipy.linalg as sla
 import scipy.sparse as sp
 
 
+def pick_space(pool, si, reuse_tol):
+    """Strategy 3: the pool entry with the smallest relative shift change below
+    reuse_tol (first on ties), else None (the oracle's rule)."""
+    best, bd = None, reuse_tol
+    for sp_, h in pool:
+        d = abs(sp_ - si) / abs(si)
+        if d < bd:
+            best, bd = h, d
+    return best
+
+
 def order_shifts(sig):
     """Slot order: by |σ| (10 significant digits, so conjugate pairs tie),
     then arg σ."""
@@ -43,8 +54,12 @@ class IrkaRun:
 
 
 def irka(ctx, indptr, indices, data, b, c, shifts0, *, k=8, s=40, tol=1e-10,
-         max_itn=20000, trunc_tol=1e-2, shift_tol=1e-6, max_steps=30, recycle=True):
-    """Algorithm 3 on the GPU; (indptr, indices, data) is the CSR of A."""
+         max_itn=20000, trunc_tol=1e-2, shift_tol=1e-6, max_steps=30, recycle=True,
+         strategy=1, reuse_tol=np.inf):
+    """Algorithm 3 on the GPU; (indptr, indices, data) is the CSR of A.
+    strategy 1/2/3: the recycling strategies of PAPER.md:1196-1235 (see
+    oracle/irka.py for the readings); strategies 2 and 3 copy the chosen
+    space into the solve's own handle on the device (Recycle.copy_from)."""
     A = sp.csr_matrix((np.asarray(data, np.complex128), indices, indptr))
     n = A.shape[0]
     I = sp.identity(n, dtype=np.complex128, format="csr")
@@ -55,24 +70,45 @@ def irka(ctx, indptr, indices, data, b, c, shifts0, *, k=8, s=40, tol=1e-10,
     r = len(sig)
     slots = [dict(R=ctx.recycle(n, max(k, 1), True), x=None, xt=None) for _ in range(r)]
     run = IrkaRun(shifts=sig, steps=0, converged=False)
+    chain = [None]       # strategy 2: handle holding the last solve's space
+    prev_pool = []       # strategy 3: (sigma, handle) of the previous step
+    spare = []           # handles of the pool two steps back, reused
 
     def solve_all(sig):
         V = np.zeros((n, r), np.complex128)
         W = np.zeros((n, r), np.complex128)
         its = []
+        cur_pool = []
         for i, si in enumerate(sig):
             st = slots[i]
+            if strategy == 1:
+                Rh = st["R"]
+            else:
+                Rh = spare.pop() if spare else ctx.recycle(n, max(k, 1), True)
+                src = chain[0] if strategy == 2 else \
+                    pick_space(prev_pool + cur_pool, si, reuse_tol)
+                if src is not None:
+                    Rh.copy_from(src)
+                else:
+                    Rh.clear()
             As = (si * I - A).tocsr()
             As.sort_indices()
             M = ctx.matrix(As.indptr, As.indices, As.data)
             x, xt, res, _ = ctx.solve_dual(M, b, c, st["x"], st["xt"],
-                                           R=st["R"] if recycle else None,
+                                           R=Rh if recycle else None,
                                            k=k if recycle else 0, s=s, tol=tol,
                                            max_itn=max_itn, trunc_tol=trunc_tol)
             M.free()
             V[:, i], W[:, i] = x, xt
             st["x"], st["xt"] = x, xt                     # previous solution
+            if strategy == 2 and chain[0] is not None:
+                spare.append(chain[0])
+            chain[0] = Rh
+            cur_pool.append((si, Rh))
             its.append(res["iterations"])
+        if strategy == 3:
+            spare.extend(h for _, h in prev_pool)
+            prev_pool[:] = cur_pool
         return V, W, its
 
     def reduced(V, W):

@@ -529,12 +529,14 @@ def test_full_size_c4_bilinear_conjugate_pair(ctx):
     assert abs(vals[1] - np.conj(vals[0])) <= 1e-8 * abs(vals[0])
 
 
-def test_irka_gpu_matches_oracle(ctx):
+@pytest.mark.parametrize("strategy,reuse_tol", [(1, np.inf), (2, np.inf), (3, 0.5)])
+def test_irka_gpu_matches_oracle(ctx, strategy, reuse_tol):
     """NEXT-3: IRKA (Algorithm 3) with the dual solves on the GPU vs the IRKA
     oracle on a stable conv-diff model: same number of IRKA steps, shift
     trajectories to 1e-6, the same per-solve iterations (max(2, 3%)), and the
     GPU's reduced model Hermite-interpolates G at its final shifts
-    (Theorem 3.1, dense check)."""
+    (Theorem 3.1, dense check); recycling strategies 1, 2 and 3
+    (PAPER.md:1196-1235)."""
     from oracle import irka as OI
     from paper_1010_0762_b200 import irka as GI
     from synth.convdiff import convdiff_csr
@@ -543,7 +545,8 @@ def test_irka_gpu_matches_oracle(ctx):
     A = -sp.csr_matrix((data, indices, indptr), shape=(n, n))
     A.sort_indices()
     b, c = vec(n, 81, dist="normal"), vec(n, 82, dist="normal")
-    kw = dict(k=4, s=10, tol=1e-12, shift_tol=1e-8, max_steps=40)
+    kw = dict(k=4, s=10, tol=1e-12, shift_tol=1e-8, max_steps=40, strategy=strategy,
+              reuse_tol=reuse_tol)
     ref = OI.irka(A, b, c, [0.05, 0.4, 2.0], **kw)
     got = GI.irka(ctx, A.indptr, A.indices, A.data, b, c, [0.05, 0.4, 2.0], **kw)
     assert ref.converged and got.converged and got.steps == ref.steps

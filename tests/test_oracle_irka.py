@@ -102,3 +102,39 @@ def test_bicg_and_rbicg_trajectories_agree():
     assert len(r1.history) == len(r0.history)
     for s1, s0 in zip(r1.history, r0.history):
         np.testing.assert_allclose(s1, s0, rtol=1e-6)
+
+
+def test_pick_space_rule():
+    """Strategy 3's choice: smallest relative shift
+    change below the tolerance, first on ties, none above it."""
+    pool = [(1.0, "a"), (2.0 + 0.1j, "b"), (2.1, "c"), (2.1, "d")]
+    assert I.pick_space(pool, 2.0, np.inf) == "b"          # |0.1j|/2 = 0.05 < 0.1/2
+    assert I.pick_space(pool, 2.1, np.inf) == "c"          # exact match, first of the tie
+    assert I.pick_space(pool, 2.0, 0.01) is None           # nothing within 1 %
+    assert I.pick_space([], 2.0, np.inf) is None
+
+
+@pytest.mark.parametrize("strategy", [2, 3])
+def test_strategies_reach_the_same_fixed_point(strategy):
+    """Recycling changes how the dual pairs are solved, not what they solve:
+    strategies 2 and 3 converge to the shifts of strategy 1 and of the dense
+    textbook IRKA."""
+    A, b, c = _model()
+    kw = dict(k=4, s=10, tol=1e-12, shift_tol=1e-8, max_steps=60)
+    ref = I.irka(A, b, c, [0.05, 0.4, 2.0], strategy=1, **kw)
+    got = I.irka(A, b, c, [0.05, 0.4, 2.0], strategy=strategy, **kw)
+    assert got.converged and ref.converged
+    np.testing.assert_allclose(got.shifts, ref.shifts, rtol=1e-6)
+    np.testing.assert_allclose(got.shifts, _dense_irka(A, b, c, [0.05, 0.4, 2.0], tol=1e-8),
+                               rtol=1e-6)
+
+
+def test_strategy3_zero_tolerance_is_plain_bicg():
+    """Strategy 3 with reuse_tol = 0 never hands a space to a solve: every
+    solve is BiCG (Algorithm 1 = Algorithm 2 with k = 0), so the iteration
+    counts equal those of the non-recycling run."""
+    A, b, c = _model()
+    kw = dict(s=10, tol=1e-12, shift_tol=1e-8, max_steps=5)
+    r3 = I.irka(A, b, c, [0.05, 0.4, 2.0], k=4, strategy=3, reuse_tol=0.0, **kw)
+    r0 = I.irka(A, b, c, [0.05, 0.4, 2.0], k=0, recycle=False, **kw)
+    assert r3.iterations == r0.iterations
