@@ -498,9 +498,9 @@ struct Solver {
     }
     if (dist) {
       const int64_t ns = std::max<int64_t>(m->halo.nsend, 1), ng = std::max<int64_t>(m->halo.nghost, 1);
-      hsend = alloc((size_t)std::max(4, kmax) * ns);
+      hsend = alloc((size_t)std::max(6, kmax) * ns);   // (fused form: 6 vectors)
       hsend_side = alloc((size_t)kmax * ns);
-      hrecv = alloc((size_t)4 * ng);
+      hrecv = alloc((size_t)6 * ng);
       red = alloc((size_t)4 * KMAX + 8);
     }
     // directions as ring columns when memory allows (the persistent loop
@@ -521,11 +521,11 @@ struct Solver {
     tmark("ring+p");
     z = alloc(n);
     zt = alloc(n);
-    if (k_basis == 0 && !dist) {   // fused iteration: (z_i, p_i) pairs by parity
+    if (k_basis == 0) {   // fused iteration: (z_i, p_i) nodes by parity (+ ghost rows)
       const size_t nl = 2;   // node {z, p} (kernels.cu)
       for (int q = 0; q < 2; ++q) {
-        zp[q] = alloc(nl * (size_t)n);
-        ztp[q] = alloc(nl * (size_t)n);
+        zp[q] = alloc(nl * (size_t)nx);
+        ztp[q] = alloc(nl * (size_t)nx);
       }
     }
     x = alloc(nx);
@@ -808,6 +808,16 @@ struct Solver {
   // one iteration of the partitioned loop: halo of r, p, r~, p~ (C-1), SpMV
   // pair + coefficients, allreduce #1 (C-2), α step, updates, allreduce #2
   // (C-3), β step and stop test.
+  // fused form over the row partition: ONE allreduce per iteration (the
+  // halo carries r, z, p and the duals of the iteration's gathered state)
+  void dist_iteration_fused(cudaStream_t s) {
+    launch_halo_fused<T>(la, M->halo.send_idx, M->halo.nsend, hsend, nullptr, 0, 1, s);
+    ctx->comm->exchange(M->halo, hsend, hrecv, (int64_t)M->halo.nghost * sizeof(T), sizeof(T), 6, s);
+    launch_halo_fused<T>(la, nullptr, 0, nullptr, hrecv, M->halo.nghost, 0, s);
+    launch_fused<T>(la, s);
+    allreduce_red(7, s);
+    launch_leader_fused<T>(la, s);
+  }
   void dist_iteration(cudaStream_t s) {
     launch_halo_pack_loop<T>(la, M->halo.send_idx, M->halo.nsend, hsend, s);
     ctx->comm->exchange(M->halo, hsend, hrecv, (int64_t)M->halo.nghost * sizeof(T), sizeof(T), 4, s);
@@ -880,16 +890,18 @@ struct Solver {
   bool fused = false;
   // K(1)'s gathered state: z_0 = p_0 = 0
   void init_nodes(cudaStream_t s) {
-    RB_CUDA(cudaMemsetAsync(zp[0], 0, sizeof(T) * 2 * n, s));
-    RB_CUDA(cudaMemsetAsync(ztp[0], 0, sizeof(T) * 2 * n, s));
+    RB_CUDA(cudaMemsetAsync(zp[0], 0, sizeof(T) * 2 * nx, s));
+    RB_CUDA(cudaMemsetAsync(ztp[0], 0, sizeof(T) * 2 * nx, s));
   }
   bool fused_ok() const {
     const bool off = getenv("RBICG_FUSED") && atoi(getenv("RBICG_FUSED")) == 0;   // per solve
-    return !off && zp[0] && la.k == 0 && la.staged && !la.split && lazy_x && !dist && pring_len == 0;
+    return !off && zp[0] && la.k == 0 && la.staged && !la.split && lazy_x && pring_len == 0;
   }
   void capture_graph() {
     if (dist && !ctx->comm->capturable()) {
       uncaptured = true;
+      fused = fused_ok();
+      if (fused) init_nodes(ctx->stream);
       return;
     }
     if (!dist && getenv("RBICG_PERSIST") && atoi(getenv("RBICG_PERSIST")) != 0) {
@@ -909,7 +921,8 @@ struct Solver {
     // cycle boundary from any start (the extra one is a no-op after a pause)
     for (int it = 0; it < o.s + (fused ? 1 : 0); ++it) {
       if (dist) {
-        dist_iteration(ctx->stream);
+        if (fused) dist_iteration_fused(ctx->stream);
+        else dist_iteration(ctx->stream);
       } else if (fused) {
         launch_fused<T>(la, ctx->stream);
       } else {
@@ -927,8 +940,9 @@ struct Solver {
 
   void run_graph() {
     if (uncaptured) {   // virtual ranks: iteration by iteration
-      for (int it = 0; it < o.s; ++it) {
-        dist_iteration(ctx->stream);
+      for (int it = 0; it < o.s + (fused ? 1 : 0); ++it) {
+        if (fused) dist_iteration_fused(ctx->stream);
+        else dist_iteration(ctx->stream);
         pull();
         if (hst->done) break;
       }

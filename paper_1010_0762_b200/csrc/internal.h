@@ -169,6 +169,10 @@ int stream_blocks_per_sm();    // occupancy of the streaming kernels
 template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_pass2(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_fused(const LoopArgs<T> &a, cudaStream_t s);
+template <typename T> void launch_leader_fused(const LoopArgs<T> &a, cudaStream_t s);
+template <typename T>
+void launch_halo_fused(const LoopArgs<T> &a, const int32_t *idx, int64_t nsend, T *sendbuf,
+                       const T *recvbuf, int64_t nghost, int pack, cudaStream_t s);
 template <typename T>
 void launch_resid(const LoopArgs<T> &a, const T *b, const T *bt, const T *x, const T *xt,
                   T *r, T *rt, int with_coef, cudaStream_t s);

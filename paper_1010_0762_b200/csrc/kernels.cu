@@ -586,6 +586,62 @@ __device__ __forceinline__ void fused_pair_smem(const int32_t *__restrict__ cA, 
   }
 }
 
+// The scalar step of K(i) (one thread): completes iteration i-1 (record,
+// stop test, breakdowns, cycle pause) and prepares α_i, β_i (look-ahead ρ_i).
+template <typename T>
+__device__ __forceinline__ void fused_leader(const LoopArgs<T> &a, DevState<T> *st, const T *s_fin, int i,
+                                             T alpha, T beta) {
+  const T rho_prev = s_fin[0];
+  const double rn = sqrt(re(s_fin[1])), rtn = sqrt(re(s_fin[2]));
+  const T sigma = s_fin[3];
+  int done = 0, status = RBICG_OK;
+  if (i >= 2) {   // iteration i-1 completes here
+    const int m = i - 1;
+    IterRec<T> rec;
+    rec.alpha = alpha;
+    rec.beta = beta;
+    rec.rho = rho_prev;
+    rec.sigma = ldcg(&st->sigma);
+    rec.rnorm = rn;
+    rec.rtnorm = rtn;
+    a.hist[m] = rec;
+    const int force = __ldcg(&st->force);
+    const bool conv = !force && rn <= __ldcg(&st->tolb) && rtn <= __ldcg(&st->tolbt);
+    if (conv) {
+      done = 1;
+    } else if (iszero(rho_prev) || !finite(divd(rho_prev, ldcg(&st->rho)))) {
+      done = 1;
+      status = RBICG_BREAKDOWN_SERIOUS;
+    } else if (m >= __ldcg(&st->max_itn)) {
+      done = 1;
+      status = force ? RBICG_OK : RBICG_MAXITER;
+    } else if (m == __ldcg(&st->stop_at)) {
+      done = 2;
+    }
+    st->iter = m;
+    st->rnorm = rn;
+    st->rtnorm = rtn;
+    st->rho = rho_prev;
+  }
+  // iteration i's scalars (kept also when finishing: a retry resumes with them)
+  const T alpha_i = divd(rho_prev, sigma);
+  if (!done && (iszero(sigma) || !finite(alpha_i))) {
+    done = 1;
+    status = RBICG_BREAKDOWN_SECOND;
+  }
+  // ρ_i ≈ ρ_{i-1} - α_i (r~, z) - α_i (z~, r) + α_i² (z~, z)
+  const T rho_ext = add(sub(sub(rho_prev, mul(alpha_i, s_fin[4])), mul(alpha_i, s_fin[5])),
+                        mul(mul(alpha_i, alpha_i), s_fin[6]));
+  st->alpha = alpha_i;
+  st->beta = divd(rho_ext, rho_prev);
+  st->sigma = sigma;
+  st->kidx = i;
+  if (done) {
+    st->status = status;
+    st->done = done;
+  }
+}
+
 template <typename T, int MINB>
 __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   __shared__ T s_fin[NFUSED + 1];
@@ -716,56 +772,60 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   }
   if (!last_block(&st->cnt[0], &s_last)) return;
   final_reduce(a.part, NFUSED, gridDim.x, s_fin);
-  if (tid != 0) return;
-  st->cnt[0] = 0;
-  const T rho_prev = s_fin[0];
-  const double rn = sqrt(re(s_fin[1])), rtn = sqrt(re(s_fin[2]));
-  const T sigma = s_fin[3];
-  int done = 0, status = RBICG_OK;
-  if (i >= 2) {   // iteration i-1 completes here
-    const int m = i - 1;
-    IterRec<T> rec;
-    rec.alpha = alpha;
-    rec.beta = beta;
-    rec.rho = rho_prev;
-    rec.sigma = ldcg(&st->sigma);
-    rec.rnorm = rn;
-    rec.rtnorm = rtn;
-    a.hist[m] = rec;
-    const int force = __ldcg(&st->force);
-    const bool conv = !force && rn <= __ldcg(&st->tolb) && rtn <= __ldcg(&st->tolbt);
-    if (conv) {
-      done = 1;
-    } else if (iszero(rho_prev) || !finite(divd(rho_prev, ldcg(&st->rho)))) {
-      done = 1;
-      status = RBICG_BREAKDOWN_SERIOUS;
-    } else if (m >= __ldcg(&st->max_itn)) {
-      done = 1;
-      status = force ? RBICG_OK : RBICG_MAXITER;
-    } else if (m == __ldcg(&st->stop_at)) {
-      done = 2;
-    }
-    st->iter = m;
-    st->rnorm = rn;
-    st->rtnorm = rtn;
-    st->rho = rho_prev;
+  if (tid == 0) st->cnt[0] = 0;
+  if (a.dist) {   // local sums -> allreduce -> k_leader_fused
+    if (tid < NFUSED) a.red[tid] = s_fin[tid];
+    return;
   }
-  // iteration i's scalars (kept also when finishing: a retry resumes with them)
-  const T alpha_i = divd(rho_prev, sigma);
-  if (!done && (iszero(sigma) || !finite(alpha_i))) {
-    done = 1;
-    status = RBICG_BREAKDOWN_SECOND;
+  if (tid == 0) fused_leader<T>(a, st, s_fin, i, alpha, beta);
+}
+
+// partitioned form: the scalar step after the allreduce of the block sums
+template <typename T>
+__global__ void __launch_bounds__(32) k_leader_fused(LoopArgs<T> a) {
+  DevState<T> *st = a.st;
+  if (threadIdx.x != 0 || __ldcg(&st->done)) return;
+  T s_fin[NFUSED];
+  for (int o = 0; o < NFUSED; ++o) s_fin[o] = ldcg(a.red + o);
+  fused_leader<T>(a, st, s_fin, __ldcg(&st->kidx) + 1, ldcg(&st->alpha), ldcg(&st->beta));
+}
+
+// halo of the fused form: the own rows of r_{i-2}, z_{i-1}, p_{i-1} and the
+// duals that the neighbours gather, into ghost rows [n, nx)
+template <typename T>
+__global__ void k_halo_pack_fused(LoopArgs<T> a, const int32_t *idx, int64_t nsend, T *sendbuf) {
+  const int i = __ldcg(&a.st->kidx) + 1;
+  if (__ldcg(&a.st->done)) return;
+  const T *r = a.rring + (int64_t)(max(i - 2, 0) % a.ring) * a.ldr;
+  const T *rt = a.rtring + (int64_t)(max(i - 2, 0) % a.ring) * a.ldr;
+  const T *nd = a.zp[(i - 1) & 1], *ndt = a.ztp[(i - 1) & 1];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nsend;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx[j];
+    sendbuf[0 * nsend + j] = r[row];
+    sendbuf[1 * nsend + j] = nd[2 * row];
+    sendbuf[2 * nsend + j] = nd[2 * row + 1];
+    sendbuf[3 * nsend + j] = rt[row];
+    sendbuf[4 * nsend + j] = ndt[2 * row];
+    sendbuf[5 * nsend + j] = ndt[2 * row + 1];
   }
-  // ρ_i ≈ ρ_{i-1} - α_i (r~, z) - α_i (z~, r) + α_i² (z~, z)
-  const T rho_ext = add(sub(sub(rho_prev, mul(alpha_i, s_fin[4])), mul(alpha_i, s_fin[5])),
-                        mul(mul(alpha_i, alpha_i), s_fin[6]));
-  st->alpha = alpha_i;
-  st->beta = divd(rho_ext, rho_prev);
-  st->sigma = sigma;
-  st->kidx = i;
-  if (done) {
-    st->status = status;
-    st->done = done;
+}
+template <typename T>
+__global__ void k_halo_unpack_fused(LoopArgs<T> a, const T *recvbuf, int64_t nghost) {
+  const int i = __ldcg(&a.st->kidx) + 1;
+  if (__ldcg(&a.st->done)) return;
+  T *r = a.rring + (int64_t)(max(i - 2, 0) % a.ring) * a.ldr;
+  T *rt = a.rtring + (int64_t)(max(i - 2, 0) % a.ring) * a.ldr;
+  T *nd = a.zp[(i - 1) & 1], *ndt = a.ztp[(i - 1) & 1];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nghost;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = a.n + g;
+    r[row] = recvbuf[0 * nghost + g];
+    nd[2 * row] = recvbuf[1 * nghost + g];
+    nd[2 * row + 1] = recvbuf[2 * nghost + g];
+    rt[row] = recvbuf[3 * nghost + g];
+    ndt[2 * row] = recvbuf[4 * nghost + g];
+    ndt[2 * row + 1] = recvbuf[5 * nghost + g];
   }
 }
 
@@ -870,6 +930,23 @@ template <typename T> void launch_fused(const LoopArgs<T> &a0, cudaStream_t s) {
   const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
   launch_pdl(fn, grid_for(a.n, G), sm, s, a);
   count_launch();
+}
+
+template <typename T> void launch_leader_fused(const LoopArgs<T> &a, cudaStream_t s) {
+  k_leader_fused<T><<<1, 32, 0, s>>>(a);
+  count_launch();
+}
+template <typename T>
+void launch_halo_fused(const LoopArgs<T> &a, const int32_t *idx, int64_t nsend, T *sendbuf,
+                       const T *recvbuf, int64_t nghost, int pack, cudaStream_t s) {
+  if (pack && nsend > 0) {
+    k_halo_pack_fused<T><<<(int)std::min<int64_t>((nsend + 255) / 256, 1184), 256, 0, s>>>(a, idx, nsend, sendbuf);
+    count_launch();
+  }
+  if (!pack && nghost > 0) {
+    k_halo_unpack_fused<T><<<(int)std::min<int64_t>((nghost + 255) / 256, 1184), 256, 0, s>>>(a, recvbuf, nghost);
+    count_launch();
+  }
 }
 
 template <typename T> void launch_pass2(const LoopArgs<T> &a, cudaStream_t s) {
@@ -988,6 +1065,9 @@ void prepare_kernels() {
   template void launch_pass1<T>(const LoopArgs<T> &, cudaStream_t);                          \
   template void launch_pass2<T>(const LoopArgs<T> &, cudaStream_t);                          \
   template void launch_fused<T>(const LoopArgs<T> &, cudaStream_t);                          \
+  template void launch_leader_fused<T>(const LoopArgs<T> &, cudaStream_t);                   \
+  template void launch_halo_fused<T>(const LoopArgs<T> &, const int32_t *, int64_t, T *,      \
+                                     const T *, int64_t, int, cudaStream_t);                 \
   template void launch_resid<T>(const LoopArgs<T> &, const T *, const T *, const T *,        \
                                 const T *, T *, T *, int, cudaStream_t);                     \
   template void launch_init2<T>(const LoopArgs<T> &, const T *, const T *, cudaStream_t);    \

@@ -241,20 +241,21 @@ def test_nccl_unique_id_loads():
     assert len(uid) == 128 and any(uid)
 
 
-def test_nccl_one_rank_partitioned_path_matches_plain(monkeypatch):
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_nccl_one_rank_partitioned_path_matches_plain(monkeypatch, fused):
     """The NCCL mode's plumbing on one GPU: a ONE-rank NCCL communicator with
     the partitioned code path forced (rbicg_dist.force_partition) -- partitioned
     matrix store, halo exchange with no neighbours, stream-ordered NCCL
     allreduces captured in the cycle's CUDA graph, one-block scalar steps, the
     cycle-end worker's second channel (ncclCommSplit) with host allreduce and
     broadcast.  One rank sums nothing, so every iterate and the returned
-    recycle space must equal the plain single-GPU context's bitwise (the
-    plain context's two-kernel iteration: the partitioned path has no fused
-    form)."""
+    recycle space must equal the plain single-GPU context's bitwise -- in the
+    fused one-kernel iteration (one allreduce per iteration) and in the
+    two-kernel iteration."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
-    monkeypatch.setenv("RBICG_FUSED", "0")
+    monkeypatch.setenv("RBICG_FUSED", fused)
     from paper_1010_0762_b200 import api
     cfg = CONFIGS["C1"].scaled(24, systems=3, s=10)
     items = list(system_sequence(cfg))
