@@ -460,8 +460,10 @@ def run_reference(args):
             "value": v, "unit": "iterations/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / max(1, args.steps),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name} (bounded sample)"},
+            "dtype": "c128" if cfg.complex else "f64",
+            "data": f"synthetic (seeded {'IRKA-like shifted' if cfg.kind == 'irka' else 'conv-diff'} sequence, SURVEY §8(d))",
+            "config": {"workload": workload_name(cfg), "sample": sample,
+                       "parallelism": "CPU oracle (host cores)"},
             "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": int(blas_threads),
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0,
