@@ -550,12 +550,27 @@ __device__ __forceinline__ void st_node(double *nodes, int64_t c, double, double
 __device__ __forceinline__ void st_node(zc *nodes, int64_t c, zc, zc z, zc p) {
   st256(nodes + 2 * c, z.x, z.y, p.x, p.y);
 }
+// staged copy of the tile's (r, {z, p}) rows [lo, lo + cnt) (fused form,
+// VS): columns inside come from shared memory, the others from global memory
+template <typename T> struct VStage {
+  const T *r, *nd, *rt, *ndt;
+  int lo, cnt;
+};
 template <typename T>
+__device__ __forceinline__ RZP<T> node_at(const T *__restrict__ nd, const T *__restrict__ r,
+                                          const T *__restrict__ snd, const T *__restrict__ sr, int lo,
+                                          int cnt, int c) {
+  const int q = c - lo;
+  if ((unsigned)q < (unsigned)cnt) return RZP<T>{sr[q], snd[2 * q], snd[2 * q + 1]};
+  return ld_node(nd, r, c);
+}
+template <typename T, bool VS>
 __device__ __forceinline__ void fused_pair_smem(const int32_t *__restrict__ cA, const T *__restrict__ vA,
                                                 int wA, const int32_t *__restrict__ cH,
                                                 const T *__restrict__ vH, int wH,
                                                 const T *__restrict__ r, const T *__restrict__ nd,
                                                 const T *__restrict__ rt, const T *__restrict__ ndt,
+                                                const VStage<T> &vs,
                                                 T malpha, T beta, T cmalpha, T cb, T &zo, T &zto) {
   zo = zero<T>();
   zto = zero<T>();
@@ -575,8 +590,13 @@ __device__ __forceinline__ void fused_pair_smem(const int32_t *__restrict__ cA, 
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      xa[q] = ld_node(nd, r, ca[q]);
-      xh[q] = ld_node(ndt, rt, ch[q]);
+      if (VS) {
+        xa[q] = node_at(nd, r, vs.nd, vs.r, vs.lo, vs.cnt, ca[q]);
+        xh[q] = node_at(ndt, rt, vs.ndt, vs.rt, vs.lo, vs.cnt, ch[q]);
+      } else {
+        xa[q] = ld_node(nd, r, ca[q]);
+        xh[q] = ld_node(ndt, rt, ch[q]);
+      }
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -642,7 +662,33 @@ __device__ __forceinline__ void fused_leader(const LoopArgs<T> &a, DevState<T> *
   }
 }
 
-template <typename T, int MINB>
+constexpr int TRV = BS + 4;   // staged vector rows per tile: the tile and 2 rows each side
+template <typename T> __host__ __device__ __forceinline__ size_t fused_vec_bytes() {
+  return (size_t)6 * TRV * sizeof(T);   // r, {z, p} (2), r~, {z~, p~} (2)
+}
+// vector part of stage `stage` for tile t: the ranges [lo, lo + cnt) of
+// r_{i-2} and of the {z, p} nodes (both sides); cnt even so every copy is a
+// multiple of 16 bytes
+__device__ __forceinline__ void fused_vrange(int64_t t, int64_t n, int &lo, int &cnt) {
+  const int64_t a0 = max((int64_t)0, t * BS - 2), a1 = min(n, t * BS + BS + 2);
+  lo = (int)a0;
+  cnt = (int)((a1 - a0) & ~(int64_t)1);
+}
+template <typename T>
+__device__ __forceinline__ void fused_issue_vec(unsigned char *vb, uint64_t *bar, int64_t t, int64_t n,
+                                                const T *r, const T *nd, const T *rt, const T *ndt) {
+  int lo, cnt;
+  fused_vrange(t, n, lo, cnt);
+  T *d = reinterpret_cast<T *>(vb);
+  const uint32_t rb = (uint32_t)(cnt * sizeof(T)), nb = 2 * rb;
+  mbar_expect_tx(bar, 2 * (rb + nb));
+  tma_load_1d(d, r + lo, rb, bar);
+  tma_load_1d(d + TRV, nd + 2 * (int64_t)lo, nb, bar);
+  tma_load_1d(d + 3 * TRV, rt + lo, rb, bar);
+  tma_load_1d(d + 4 * TRV, ndt + 2 * (int64_t)lo, nb, bar);
+}
+
+template <typename T, int MINB, bool VS = false>
 __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   __shared__ T s_fin[NFUSED + 1];
   __shared__ T s_w[NFUSED][BS / 32];
@@ -656,11 +702,12 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   const int64_t n = a.n;
   const int64_t ntiles = (n + BS - 1) / BS;
   const int64_t G64 = gridDim.x;
-  const size_t stage_bytes = p1_mat_bytes<T>(a);
+  const size_t mat_bytes = p1_mat_bytes<T>(a);
+  const size_t stage_bytes = mat_bytes + (VS ? fused_vec_bytes<T>() : 0);
   const int nst = a.p1_stages;
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+  if (tid == 0) {   // VS: two arrivals per stage (matrix part, vector part)
+    mbar_init(&bars[0], VS ? 2 : 1);
+    mbar_init(&bars[1], VS ? 2 : 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -679,7 +726,10 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   __syncthreads();
   if (s_i[1]) {   // finished or paused: drain the copies in flight
     for (int q = 0; q < nst; ++q)
-      if ((int64_t)blockIdx.x + q * G64 < ntiles) mbar_wait(&bars[q], 0);
+      if ((int64_t)blockIdx.x + q * G64 < ntiles) {
+        if (VS && tid == 0) mbar_arrive(&bars[q]);   // the vector part never comes
+        mbar_wait(&bars[q], 0);
+      }
     return;
   }
   const int i = s_i[0] + 1;
@@ -697,6 +747,11 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   const bool segcopy = a.lazy_x && i - 2 == s_i[2];
   T *__restrict__ pseg = a.pseg[(s_i[2] / a.cyc) & 1];
   T *__restrict__ ptseg = a.ptseg[(s_i[2] / a.cyc) & 1];
+  if (VS && tid == 0)   // the vector parts of the first tiles (written by the previous kernel)
+    for (int q = 0; q < nst; ++q)
+      if ((int64_t)blockIdx.x + q * G64 < ntiles)
+        fused_issue_vec<T>(f_smem + q * stage_bytes + mat_bytes, &bars[q], blockIdx.x + q * G64, n, r,
+                           zpo, rt, ztpo);
   T acc[NFUSED];
 #pragma unroll
   for (int o = 0; o < NFUSED; ++o) acc[o] = zero<T>();
@@ -721,13 +776,23 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
     const int lane = tid & 31;
     mbar_wait(&bars[si], (par >> si) & 1u);
     par ^= 1u << si;
+    VStage<T> vs{};
+    if (VS) {
+      const T *vb = reinterpret_cast<const T *>(base + mat_bytes);
+      vs.r = vb;
+      vs.nd = vb + TRV;
+      vs.rt = vb + 3 * TRV;
+      vs.ndt = vb + 4 * TRV;
+      fused_vrange(tile, n, vs.lo, vs.cnt);
+    }
     if (tid < rows) {
       const int64_t row = row0 + tid;
       T z, zt;
-      fused_pair_smem<T>(scA + (oA - bA) + lane, svA + (oA - bA) + lane, wA,
-                         scH + (oH - bH) + lane, svH + (oH - bH) + lane, wH, r, zpo, rt, ztpo,
-                         malpha, beta, cmalpha, cb, z, zt);
-      const RZP<T> o = ld_node(zpo, r, row), ot = ld_node(ztpo, rt, row);
+      fused_pair_smem<T, VS>(scA + (oA - bA) + lane, svA + (oA - bA) + lane, wA,
+                             scH + (oH - bH) + lane, svH + (oH - bH) + lane, wH, r, zpo, rt, ztpo, vs,
+                             malpha, beta, cmalpha, cb, z, zt);
+      const RZP<T> o = VS ? node_at(zpo, r, vs.nd, vs.r, vs.lo, vs.cnt, (int)row) : ld_node(zpo, r, row);
+      const RZP<T> ot = VS ? node_at(ztpo, rt, vs.ndt, vs.rt, vs.lo, vs.cnt, (int)row) : ld_node(ztpo, rt, row);
       const T rr = mad(malpha, o.z, o.r);
       const T rtr = mad(cmalpha, ot.z, ot.r);
       const T pr = mad(beta, o.p, rr);
@@ -753,8 +818,12 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
       acc[6] = cmad(zt, z, acc[6]);        // (z~_i, z_i)
     }
     __syncthreads();   // stage si consumed
-    if (tid == 0 && tile + nst * G64 < ntiles)
+    if (tid == 0 && tile + nst * G64 < ntiles) {
       p1_issue<T>(a, f_smem + si * stage_bytes, stage_bytes, &bars[si], tile + nst * G64);
+      if (VS)
+        fused_issue_vec<T>(f_smem + si * stage_bytes + mat_bytes, &bars[si], tile + nst * G64, n, r, zpo,
+                           rt, ztpo);
+    }
   }
   pdl_trigger();
   // block partials (fixed order) -> part[o * G + b]
@@ -829,8 +898,8 @@ __global__ void k_halo_unpack_fused(LoopArgs<T> a, const T *recvbuf, int64_t ngh
   }
 }
 
-template <typename T> size_t fused_smem(const LoopArgs<T> &a) {
-  return (size_t)a.p1_stages * p1_mat_bytes<T>(a);
+template <typename T> size_t fused_smem(const LoopArgs<T> &a, bool vs) {
+  return (size_t)a.p1_stages * (p1_mat_bytes<T>(a) + (vs ? fused_vec_bytes<T>() : 0));
 }
 
 // ============================================================== launchers
@@ -919,12 +988,18 @@ template <typename T> void launch_fused(const LoopArgs<T> &a0, cudaStream_t s) {
   LoopArgs<T> a = a0;
   static const int fst = getenv("RBICG_FUSED_STAGES") ? atoi(getenv("RBICG_FUSED_STAGES")) : 1;
   a.p1_stages = std::min(2, std::max(1, fst));
-  const size_t sm = fused_smem<T>(a);
+  // vector rows of each tile staged by TMA too, in-tile gathers from shared
+  // memory (opt-in: measured slower, C2 50.8 vs 46.8 us, C3 296 vs 278 us --
+  // those gathers were L1 hits already)
+  static const int vse = getenv("RBICG_FUSED_VS") ? atoi(getenv("RBICG_FUSED_VS")) : 0;
+  const bool vs = vse != 0;
+  const size_t sm = fused_smem<T>(a, vs);
   // 4 CTAs/SM at 64 registers (C2: 46.3 us per iteration; 3 CTAs at 80: 56.3 us)
   // (complex: 3 CTAs/SM, 80 registers -- 64 spill with the 256-bit node loads)
   static const int minb_env = getenv("RBICG_FUSED_MINB") ? atoi(getenv("RBICG_FUSED_MINB")) : 0;
   const int minb = minb_env ? minb_env : (sizeof(T) == 8 ? 4 : 3);
-  auto fn = minb >= 6 ? k_fused<T, 6> : minb == 5 ? k_fused<T, 5> : minb == 4 ? k_fused<T, 4> : k_fused<T, 3>;
+  auto fn = vs ? (minb >= 4 ? k_fused<T, 4, true> : k_fused<T, 3, true>)
+              : (minb >= 6 ? k_fused<T, 6> : minb == 5 ? k_fused<T, 5> : minb == 4 ? k_fused<T, 4> : k_fused<T, 3>);
   int per_sm = 1;
   RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BS, sm));
   const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
@@ -1051,6 +1126,10 @@ void prepare_kernels() {
   allow_max_dyn_smem(k_pass2<zc, 4>);
   allow_max_dyn_smem(k_fused<double, 3>);
   allow_max_dyn_smem(k_fused<double, 4>);
+  allow_max_dyn_smem(k_fused<double, 4, true>);
+  allow_max_dyn_smem(k_fused<double, 3, true>);
+  allow_max_dyn_smem(k_fused<zc, 4, true>);
+  allow_max_dyn_smem(k_fused<zc, 3, true>);
   allow_max_dyn_smem(k_fused<double, 5>);
   allow_max_dyn_smem(k_fused<double, 6>);
   allow_max_dyn_smem(k_fused<zc, 5>);
