@@ -390,7 +390,9 @@ struct Solver {
   // a sequence keeps n, k, s -- so the per-system setup makes no allocations.
   size_t arena_pos = 0;
   std::vector<size_t> owned_bytes;
+  std::mutex alloc_mu;   // the cycle-end worker may allocate lazily (ensure_tmp_u)
   void *alloc_bytes(size_t bytes) {
+    std::lock_guard<std::mutex> lk(alloc_mu);
     bytes = std::max<size_t>(bytes, 1);
     void *q = nullptr;
     if (ctx) {
@@ -409,6 +411,13 @@ struct Solver {
     return q;
   }
   T *alloc(size_t elems) { return (T *)alloc_bytes(sizeof(T) * elems); }
+  int setup_k_basis = 0;
+  bool tmp_u_lazy() const { return setup_k_basis == 0 && !dist && !getenv("RBICG_TMP_U_EAGER"); }
+  void ensure_tmp_u() {
+    if (tmp.U) return;
+    tmp.U = alloc((size_t)nx * kmax);
+    tmp.Ut = alloc((size_t)nx * kmax);
+  }
   ~Solver() {
     static const bool tm = getenv("RBICG_TIMING") != nullptr;
     const double t0 = tm ? now_ms() : 0;
@@ -456,13 +465,15 @@ struct Solver {
     n = m->n;
     real = (m->dtype == RBICG_F64);
     kmax = std::max(std::max(o.k, k_basis), 1);
+    setup_k_basis = k_basis;
     ring = o.s + 2;
     if (o.k > 0 && o.update_recycle && !getenv("RBICG_SYNC_CYCLE")) {
       // doubled ring for the overlapped cycle end when memory allows; the
       // decision is kept per (ctx, n, k, s) so a sequence does not query the
       // allocator every system (cudaMemGetInfo measured up to 20 ms)
       const size_t extra = (size_t)2 * ring * n * sizeof(T);
-      const size_t need = extra + (size_t)(6 * kmax + 4 * std::max(k_basis, 0) + 2 * ring + 20) * n * sizeof(T);
+      const int nblk = (k_basis == 0 ? 4 : 6) * kmax + 4 * std::max(k_basis, 0);   // (lazy U_j temporaries)
+      const size_t need = extra + (size_t)(nblk + 2 * ring + 24) * n * sizeof(T);
       const uint64_t key = ((uint64_t)n << 20) ^ ((uint64_t)kmax << 10) ^ ((uint64_t)k_basis << 40) ^
                            (uint64_t)o.s ^ (sizeof(T) << 60);
       if (ctx->async_key != key) {
@@ -545,8 +556,13 @@ struct Solver {
     // (C5 first system: 54 GB)
     for (Basis *B : {&cur, &cand[0], &tmp}) {
       const size_t kb = B == &cur ? (size_t)std::max(k_basis, 0) : (size_t)kmax;
-      B->U = kb ? alloc((size_t)nx * kb) : nullptr;
-      B->Ut = kb ? alloc((size_t)nx * kb) : nullptr;
+      // U_j, Ũ_j temporaries: only the general cycle-end path (recycle data
+      // present) and the partitioned refresh write them -- allocated on first
+      // use when the system starts without a space (C5 fits the overlapped
+      // cycle end on one GPU thanks to the 2 n x k blocks saved)
+      const bool lazy_u = B == &tmp && tmp_u_lazy();
+      B->U = kb && !lazy_u ? alloc((size_t)nx * kb) : nullptr;
+      B->Ut = kb && !lazy_u ? alloc((size_t)nx * kb) : nullptr;
       B->k = 0;
       if (B == &cand[0]) continue;
       B->C = kb ? alloc((size_t)n * kb) : nullptr;
@@ -750,6 +766,7 @@ struct Solver {
     if (kin > 0) {
       const T *Uh = U, *Uth = Ut;
       if (dist) {   // ghost rows of U, Ũ for the SpMM (C-6)
+        ensure_tmp_u();
         RB_CUDA(cudaMemcpyAsync(tmp.U, U, sizeof(T) * n * kin, cudaMemcpyDeviceToDevice, ctx->stream));
         RB_CUDA(cudaMemcpyAsync(tmp.Ut, Ut, sizeof(T) * n * kin, cudaMemcpyDeviceToDevice, ctx->stream));
         halo_rows(tmp.U, kin, ctx->comm.get(), hsend, ctx->stream);
@@ -999,6 +1016,7 @@ struct Solver {
     Mt[(size_t)(kx + m) * p + ksel] = std::conj(cr[m]);
     M[(size_t)(kx + m + 1) * p + ksel] = 1.0;
     Mt[(size_t)(kx + m + 1) * p + ksel] = 1.0;
+    if (ksel > 0) ensure_tmp_u();
     gemm_panels<T>(X, M, ksel, n, tmp.U, ctx, cs, true, x);
     gemm_panels<T>(Xt, Mt, ksel, n, tmp.Ut, ctx, cs, true, xt);
   }
@@ -1058,6 +1076,7 @@ struct Solver {
     }
     std::vector<std::pair<T *, int>> outs, outst;
     if (with_u) {
+      ensure_tmp_u();
       outs.push_back({tmp.U, ksel});
       outst.push_back({tmp.Ut, ksel});
     }
@@ -1380,6 +1399,7 @@ struct Solver {
       } else {
       {
         Phase ph("cycle.gemm_UW", cs);
+        ensure_tmp_u();
         if (fb > fa) {
           fused_flush_gemm(PhiCols, PhitCols, Wrow, Wtrow, ksel, mphi - s, fa, fb, lo, rec, cs);
         } else {
