@@ -607,6 +607,15 @@ struct Solver {
     la.abl = 0;
     la.pass2_tma = getenv("RBICG_NO_TMA2") ? 0 : 1;
     la.shared_cols = M->A.cols == M->AH.cols ? 1 : 0;
+    // contiguous tile runs per CTA when the SpMV reaches at most 4 tiles away:
+    // the neighbour tiles' vector rows are then L1 hits of the same SM (C2, 2-D
+    // 1024^2: 46.2 -> 45.0 us); with a wide band (C3's +-36,864 rows) the
+    // grid-strided order keeps the wave of neighbouring tiles in L2 instead
+    // (contiguous runs: 277.8 -> 346.8 us)
+    {
+      const int64_t bw = M->A.bandwidth;
+      la.tile_contig = envi("RBICG_TILE_CONTIG", bw >= 0 && bw <= 4 * BS ? 1 : 0);
+    }
     const bool tma_ok = !getenv("RBICG_NO_TMA");
     if (la.split) {
       const double st_h = 2.0 * la.tile_max_h * (4 + sizeof(T)) + (la.stage_v ? 4.0 * TRH * sizeof(T) : 0.0);

@@ -27,6 +27,7 @@ struct DevMat {
   int64_t *sptr = nullptr;  // nslices + 1 element offsets (multiples of 32)
   int32_t *cols = nullptr;
   void *vals = nullptr;
+  int64_t bandwidth = -1;   // max |col - row| of A (-1: unknown, e.g. a row partition)
   int cols_shared = 0;      // cols aliases the other matrix's (A^* of a structurally
                             // symmetric A: same SELL column array, build_t)
 };
@@ -76,6 +77,7 @@ struct LoopArgs {
   int abl;                 // timing ablations (RBICG_ABL, never set in a solve): 1 no gathers
   int pass2_tma;           // pass 2 streams its tiles through smem via TMA
   int shared_cols;         // A and A^* share one SELL column array (structurally symmetric A)
+  int tile_contig;         // fused form: contiguous tile runs per CTA instead of grid-strided
   int lazy_x;              // x, x~ rebuilt per segment from the Lanczos ring
   T *pseg[2], *ptseg[2];   // p_a, p~_a at the start of the open segment, by segment parity
   int cyc;                 // cycle length s (segment parity = (seg_start / s) & 1)

@@ -702,6 +702,11 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   const int64_t n = a.n;
   const int64_t ntiles = (n + BS - 1) / BS;
   const int64_t G64 = gridDim.x;
+  // this CTA's tiles: grid-strided (b, b + G, ...) or one contiguous run
+  // (a.tile_contig: neighbouring tiles' vector rows stay in this SM's L1)
+  const int64_t t0 = a.tile_contig ? (ntiles * blockIdx.x) / G64 : blockIdx.x;
+  const int64_t t1 = a.tile_contig ? (ntiles * (blockIdx.x + 1)) / G64 : ntiles;
+  const int64_t tstep = a.tile_contig ? 1 : G64;
   const size_t mat_bytes = p1_mat_bytes<T>(a);
   const size_t stage_bytes = mat_bytes + (VS ? fused_vec_bytes<T>() : 0);
   const int nst = a.p1_stages;
@@ -713,8 +718,8 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   __syncthreads();
   if (tid == 0)
     for (int q = 0; q < nst; ++q)
-      if ((int64_t)blockIdx.x + q * G64 < ntiles)
-        p1_issue<T>(a, f_smem + q * stage_bytes, stage_bytes, &bars[q], blockIdx.x + q * G64);
+      if (t0 + q * tstep < t1)
+        p1_issue<T>(a, f_smem + q * stage_bytes, stage_bytes, &bars[q], t0 + q * tstep);
   pdl_wait();
   if (tid == 0) {
     s_i[0] = __ldcg(&st->kidx);
@@ -726,7 +731,7 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   __syncthreads();
   if (s_i[1]) {   // finished or paused: drain the copies in flight
     for (int q = 0; q < nst; ++q)
-      if ((int64_t)blockIdx.x + q * G64 < ntiles) {
+      if (t0 + q * tstep < t1) {
         if (VS && tid == 0) mbar_arrive(&bars[q]);   // the vector part never comes
         mbar_wait(&bars[q], 0);
       }
@@ -749,8 +754,8 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   T *__restrict__ ptseg = a.ptseg[(s_i[2] / a.cyc) & 1];
   if (VS && tid == 0)   // the vector parts of the first tiles (written by the previous kernel)
     for (int q = 0; q < nst; ++q)
-      if ((int64_t)blockIdx.x + q * G64 < ntiles)
-        fused_issue_vec<T>(f_smem + q * stage_bytes + mat_bytes, &bars[q], blockIdx.x + q * G64, n, r,
+      if (t0 + q * tstep < t1)
+        fused_issue_vec<T>(f_smem + q * stage_bytes + mat_bytes, &bars[q], t0 + q * tstep, n, r,
                            zpo, rt, ztpo);
   T acc[NFUSED];
 #pragma unroll
@@ -759,7 +764,7 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   const int64_t ns = a.A.nslices;
   uint32_t par = 0;
   int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += G64, ++it) {
+  for (int64_t tile = t0; tile < t1; tile += tstep, ++it) {
     const int64_t row0 = tile * BS;
     const int rows = (int)min((int64_t)BS, n - row0);
     const int si = nst == 2 ? (it & 1) : 0;
@@ -818,10 +823,10 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
       acc[6] = cmad(zt, z, acc[6]);        // (z~_i, z_i)
     }
     __syncthreads();   // stage si consumed
-    if (tid == 0 && tile + nst * G64 < ntiles) {
-      p1_issue<T>(a, f_smem + si * stage_bytes, stage_bytes, &bars[si], tile + nst * G64);
+    if (tid == 0 && tile + nst * tstep < t1) {
+      p1_issue<T>(a, f_smem + si * stage_bytes, stage_bytes, &bars[si], tile + nst * tstep);
       if (VS)
-        fused_issue_vec<T>(f_smem + si * stage_bytes + mat_bytes, &bars[si], tile + nst * G64, n, r, zpo,
+        fused_issue_vec<T>(f_smem + si * stage_bytes + mat_bytes, &bars[si], tile + nst * tstep, n, r, zpo,
                            rt, ztpo);
     }
   }

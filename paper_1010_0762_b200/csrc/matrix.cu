@@ -88,6 +88,15 @@ __global__ void k_differ(const I *a, const I *b, int64_t m, int *flag) {
     if (a[i] != b[i]) *flag = 1;
 }
 
+// max |col - row| over the stored entries (the SpMV's reach in rows)
+__global__ void k_bandwidth(const int32_t *rowptr, const int32_t *col, int64_t n, int *bw) {
+  int m = 0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    for (int32_t e = rowptr[r]; e < rowptr[r + 1]; ++e) m = max(m, abs(col[e] - (int)r));
+  atomicMax(bw, m);
+}
+
 static int grid1d(int64_t m) { return (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 148 * 32)); }
 
 template <typename T>
@@ -189,6 +198,17 @@ static void build_t(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowpt
                     const int32_t *col, const T *val, rbicg_mat *M) {
   cudaStream_t st = ctx->stream;
   csr_to_sell<T>(ctx, n, rowptr, col, val, M->A);
+  {
+    int *bw = (int *)ws_alloc(sizeof(int));
+    RB_CUDA(cudaMemsetAsync(bw, 0, sizeof(int), st));
+    k_bandwidth<<<grid1d(n), 256, 0, st>>>(rowptr, col, n, bw);
+    count_launch();
+    int h = 0;
+    RB_CUDA(cudaMemcpyAsync(&h, bw, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaStreamSynchronize(st));
+    ws_free(bw);
+    M->A.bandwidth = h;
+  }
   if (!getenv("RBICG_NO_SYM_T") && nnz > 0) {   // structurally symmetric fast path
     T *valT = (T *)ws_alloc(sizeof(T) * nnz);
     int *flag = (int *)ws_alloc(sizeof(int));
