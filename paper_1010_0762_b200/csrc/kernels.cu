@@ -1005,6 +1005,8 @@ template <typename T> void launch_fused(const LoopArgs<T> &a0, cudaStream_t s) {
   const int minb = minb_env ? minb_env : (sizeof(T) == 8 ? 4 : 3);
   auto fn = vs ? (minb >= 4 ? k_fused<T, 4, true> : k_fused<T, 3, true>)
               : (minb >= 6 ? k_fused<T, 6> : minb == 5 ? k_fused<T, 5> : minb == 4 ? k_fused<T, 4> : k_fused<T, 3>);
+  static const int carve = getenv("RBICG_FUSED_CARVEOUT") ? atoi(getenv("RBICG_FUSED_CARVEOUT")) : -1;
+  if (carve >= 0) RB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
   int per_sm = 1;
   RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BS, sm));
   const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
