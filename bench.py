@@ -65,6 +65,12 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's own start-up (driver queries) must not fall into the
+            # timed region: wait for its first sample (it stalled the first
+            # timed C4 solve by up to 40 ms otherwise)
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 3.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
