@@ -281,6 +281,7 @@ def run_gpu(args, rank, world):
                  "iter_GBps": (q1 + q2) / (kq["graph_iter_ms"] * 1e-3) / 1e9,
                  "iter_frac": (q1 + q2) / (kq["graph_iter_ms"] * 1e-3) / 1e9 / pk,
                  "alg_bytes_per_iter": q1 + q2,
+                 "fused_k_ms": kq["fused_ms"] if kq["fused_ms"] > 0 else None,
                  "space": "seeded N(0,1) U, U~ (%d columns), truncation off" % cfg.k}
     A.free()
     w = 16 if cfg.complex else 8

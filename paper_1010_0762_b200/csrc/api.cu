@@ -356,6 +356,11 @@ struct Solver {
   std::vector<void *> owned;
   T *rring = nullptr, *rtring = nullptr, *p[2] = {}, *pt[2] = {}, *z = nullptr, *zt = nullptr;
   T *zp[2] = {}, *ztp[2] = {};   // fused iteration: (z_i, p_i) pairs by parity
+  T *AC = nullptr, *AHCt = nullptr;   // fused iteration with k > 0: A C, A^* C~
+  static bool fusedk_env() {
+    static const bool on = getenv("RBICG_FUSEDK") && atoi(getenv("RBICG_FUSEDK")) != 0;
+    return on;
+  }
   T *x = nullptr, *xt = nullptr, *b = nullptr, *bt = nullptr, *xo = nullptr, *xto = nullptr;
   T *psegs[2] = {}, *ptsegs[2] = {};
   T *pring = nullptr, *ptring = nullptr;
@@ -532,12 +537,16 @@ struct Solver {
     tmark("ring+p");
     z = alloc(n);
     zt = alloc(n);
-    if (k_basis == 0) {   // fused iteration: (z_i, p_i) nodes by parity (+ ghost rows)
+    if (k_basis == 0 || (fusedk_env() && !dist)) {   // fused iteration: (z_i, p_i) nodes by parity (+ ghost rows)
       const size_t nl = 2;   // node {z, p} (kernels.cu)
       for (int q = 0; q < 2; ++q) {
         zp[q] = alloc(nl * (size_t)nx);
         ztp[q] = alloc(nl * (size_t)nx);
       }
+    }
+    if (k_basis > 0 && fusedk_env() && !dist) {   // A C, A^* C~ for the fused form with k > 0
+      AC = alloc((size_t)n * k_basis);
+      AHCt = alloc((size_t)n * k_basis);
     }
     x = alloc(nx);
     xt = alloc(nx);
@@ -649,6 +658,8 @@ struct Solver {
     la.pt[1] = pt[1];
     la.z = z;
     la.zt = zt;
+    la.AC = AC;
+    la.AHCt = AHCt;
     la.zp[0] = zp[0];
     la.zp[1] = zp[1];
     la.ztp[0] = ztp[0];
@@ -786,6 +797,10 @@ struct Solver {
       launch_spmm<T>(M->A, Uh, tmp.C, kin, ctx->stream);
       launch_spmm<T>(M->AH, Uth, tmp.Ct, kin, ctx->stream);
       biorth(U, Ut, tmp.C, tmp.Ct, kin, cur, ctx->stream, ctx->comm.get());
+      if (AC && cur.k > 0) {   // fused form: the neighbours' C ζ term through A C
+        launch_spmm<T>(M->A, cur.C, AC, cur.k, ctx->stream);
+        launch_spmm<T>(M->AH, cur.Ct, AHCt, cur.k, ctx->stream);
+      }
     }
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
     t_refresh += now_ms() - t0;
@@ -923,6 +938,12 @@ struct Solver {
     const bool off = getenv("RBICG_FUSED") && atoi(getenv("RBICG_FUSED")) == 0;   // per solve
     return !off && zp[0] && la.k == 0 && la.staged && !la.split && lazy_x && pring_len == 0;
   }
+  // k > 0: RBICG_FUSEDK=1 (single GPU; the split pass-1 layout is not used)
+  bool fusedk = false;
+  bool fusedk_ok() const {
+    return fusedk_env() && zp[0] && AC && la.k > 0 && la.k <= KMAX && lazy_x && !dist && pring_len == 0 &&
+           !getenv("RBICG_NO_TMA") && 2.0 * la.tile_max * (4 + sizeof(T)) <= 150 * 1024;
+  }
   void capture_graph() {
     if (dist && !ctx->comm->capturable()) {
       uncaptured = true;
@@ -937,7 +958,12 @@ struct Solver {
     }
     if (gexec) return;
     fused = fused_ok();
-    if (fused) {   // z_0 = p_0 = 0 (K(1) forms p_1 = r_0 + β_0 p_0 with α_0 = β_0 = 0)
+    fusedk = !fused && fusedk_ok();
+    if (fusedk) {   // the fused kernel stages SELL tiles with the k = 0 layout
+      la.split = 0;
+      la.staged = 1;
+    }
+    if (fused || fusedk) {   // z_0 = p_0 = 0 (K(1) forms p_1 = r_0 + β_0 p_0 with α_0 = β_0 = 0)
       init_nodes(ctx->stream);
     }
     cudaGraph_t g;
@@ -945,12 +971,14 @@ struct Solver {
     RB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     // the fused kernel K(i) completes iteration i-1: s + 1 launches reach the
     // cycle boundary from any start (the extra one is a no-op after a pause)
-    for (int it = 0; it < o.s + (fused ? 1 : 0); ++it) {
+    for (int it = 0; it < o.s + (fused || fusedk ? 1 : 0); ++it) {
       if (dist) {
         if (fused) dist_iteration_fused(ctx->stream);
         else dist_iteration(ctx->stream);
       } else if (fused) {
         launch_fused<T>(la, ctx->stream);
+      } else if (fusedk) {
+        launch_fusedk<T>(la, ctx->stream);
       } else {
         launch_pass1<T>(la, ctx->stream);
         launch_pass2<T>(la, ctx->stream);
@@ -2290,7 +2318,12 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
   // the fused iteration (k = 0): `iters` launches of k_fused in one graph
   ms[14] = -1.0;
   ms[15] = -1.0;
-  if (S.fused_ok()) {
+  const bool tk = S.fusedk_ok();
+  if (tk) {
+    S.la.split = 0;
+    S.la.staged = 1;
+  }
+  if (S.fused_ok() || tk) {
     S.init_nodes(ctx->stream);
     auto reset = [&] {
       S.hst->iter = 0;
@@ -2307,7 +2340,10 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
     cudaGraphExec_t ge;
     const int64_t l0 = g_launches.load();
     RB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < iters; ++i) launch_fused<T>(S.la, ctx->stream);
+    for (int i = 0; i < iters; ++i) {
+      if (tk) launch_fusedk<T>(S.la, ctx->stream);
+      else launch_fused<T>(S.la, ctx->stream);
+    }
     RB_CUDA(cudaStreamEndCapture(ctx->stream, &g));
     RB_CUDA(cudaGraphInstantiate(&ge, g, 0));
     RB_CUDA(cudaGraphDestroy(g));

@@ -92,6 +92,7 @@ struct LoopArgs {
                            //   gather per column (128-bit real, 256-bit complex)
   T *x, *xt;
   const T *C, *Ct;         // row-major n x k
+  const T *AC, *AHCt;      // fused form with k > 0: A C and A^* C~ (row-major n x k)
   DevState<T> *st;
   IterRec<T> *hist;        // [max_itn + 1]
   T *zhist, *zthist;       // [max_itn + 1][k]
@@ -172,6 +173,7 @@ template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_pass2(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_fused(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_leader_fused(const LoopArgs<T> &a, cudaStream_t s);
+template <typename T> void launch_fusedk(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T>
 void launch_halo_fused(const LoopArgs<T> &a, const int32_t *idx, int64_t nsend, T *sendbuf,
                        const T *recvbuf, int64_t nghost, int pack, cudaStream_t s);
