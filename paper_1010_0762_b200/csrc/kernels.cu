@@ -608,9 +608,27 @@ __device__ __forceinline__ void fused_pair_smem(const int32_t *__restrict__ cA, 
 
 // The scalar step of K(i) (one thread): completes iteration i-1 (record,
 // stop test, breakdowns, cycle pause) and prepares α_i, β_i (look-ahead ρ_i).
+// The device-state fields the fused leader reads, loaded at kernel start (in
+// parallel, off the tail: a dependent chain of L2 loads in the one leader
+// thread sat on the critical path of every iteration)
+template <typename T> struct FSnap {
+  T sigma, rho;
+  double tolb, tolbt;
+  int force, max_itn, stop_at;
+};
+template <typename T>
+__device__ __forceinline__ void fsnap_load(const DevState<T> *st, FSnap<T> &f) {
+  f.sigma = ldcg(&st->sigma);
+  f.rho = ldcg(&st->rho);
+  f.tolb = __ldcg(&st->tolb);
+  f.tolbt = __ldcg(&st->tolbt);
+  f.force = __ldcg(&st->force);
+  f.max_itn = __ldcg(&st->max_itn);
+  f.stop_at = __ldcg(&st->stop_at);
+}
 template <typename T>
 __device__ __forceinline__ void fused_leader(const LoopArgs<T> &a, DevState<T> *st, const T *s_fin, int i,
-                                             T alpha, T beta) {
+                                             T alpha, T beta, const FSnap<T> &fs) {
   const T rho_prev = s_fin[0];
   const double rn = sqrt(re(s_fin[1])), rtn = sqrt(re(s_fin[2]));
   const T sigma = s_fin[3];
@@ -621,21 +639,21 @@ __device__ __forceinline__ void fused_leader(const LoopArgs<T> &a, DevState<T> *
     rec.alpha = alpha;
     rec.beta = beta;
     rec.rho = rho_prev;
-    rec.sigma = ldcg(&st->sigma);
+    rec.sigma = fs.sigma;
     rec.rnorm = rn;
     rec.rtnorm = rtn;
     a.hist[m] = rec;
-    const int force = __ldcg(&st->force);
-    const bool conv = !force && rn <= __ldcg(&st->tolb) && rtn <= __ldcg(&st->tolbt);
+    const int force = fs.force;
+    const bool conv = !force && rn <= fs.tolb && rtn <= fs.tolbt;
     if (conv) {
       done = 1;
-    } else if (iszero(rho_prev) || !finite(divd(rho_prev, ldcg(&st->rho)))) {
+    } else if (iszero(rho_prev) || !finite(divd(rho_prev, fs.rho))) {
       done = 1;
       status = RBICG_BREAKDOWN_SERIOUS;
-    } else if (m >= __ldcg(&st->max_itn)) {
+    } else if (m >= fs.max_itn) {
       done = 1;
       status = force ? RBICG_OK : RBICG_MAXITER;
-    } else if (m == __ldcg(&st->stop_at)) {
+    } else if (m == fs.stop_at) {
       done = 2;
     }
     st->iter = m;
@@ -696,6 +714,7 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   __shared__ uint64_t bars[2];
   __shared__ T s_ab[2];
   __shared__ int s_i[5];   // kidx, done, seg_start, iter, stop_at
+  __shared__ FSnap<T> s_fs;
   extern __shared__ __align__(128) unsigned char f_smem[];
   DevState<T> *st = a.st;
   const int tid = threadIdx.x;
@@ -728,6 +747,7 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
     s_ab[0] = ldcg(&st->alpha);
     s_ab[1] = ldcg(&st->beta);
   }
+  if (tid == 32) fsnap_load(st, s_fs);
   __syncthreads();
   if (s_i[1]) {   // finished or paused: drain the copies in flight
     for (int q = 0; q < nst; ++q)
@@ -851,7 +871,7 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
     if (tid < NFUSED) a.red[tid] = s_fin[tid];
     return;
   }
-  if (tid == 0) fused_leader<T>(a, st, s_fin, i, alpha, beta);
+  if (tid == 0) fused_leader<T>(a, st, s_fin, i, alpha, beta, s_fs);
 }
 
 // partitioned form: the scalar step after the allreduce of the block sums
@@ -861,7 +881,9 @@ __global__ void __launch_bounds__(32) k_leader_fused(LoopArgs<T> a) {
   if (threadIdx.x != 0 || __ldcg(&st->done)) return;
   T s_fin[NFUSED];
   for (int o = 0; o < NFUSED; ++o) s_fin[o] = ldcg(a.red + o);
-  fused_leader<T>(a, st, s_fin, __ldcg(&st->kidx) + 1, ldcg(&st->alpha), ldcg(&st->beta));
+  FSnap<T> fs;
+  fsnap_load(st, fs);
+  fused_leader<T>(a, st, s_fin, __ldcg(&st->kidx) + 1, ldcg(&st->alpha), ldcg(&st->beta), fs);
 }
 
 // halo of the fused form: the own rows of r_{i-2}, z_{i-1}, p_{i-1} and the
