@@ -134,11 +134,14 @@ def alg_bytes(cfg_n, nnz, k, w=8, lazy_x=True, shared_cols=False):
     return p1, p2
 
 
-def alg_bytes_fused(cfg_n, nnz, w=8, shared_cols=False):
+def alg_bytes_fused(cfg_n, nnz, w=8, shared_cols=False, dcols=False):
     """Algorithmic HBM bytes per launch of the fused iteration kernel (k = 0,
     DESIGN.md §6): the A, A^* streams as in pass 1, reads r_{i-2}, z_{i-1},
-    p_{i-1} and writes r_{i-1}, z_i, p_i on both sides (12 n-vectors)."""
+    p_{i-1} and writes r_{i-1}, z_i, p_i on both sides (12 n-vectors); with
+    int16 column deltas (banded A) the shared pattern costs 2 bytes per nonzero."""
     mat = 2 * (nnz * (w + 4) + 4 * (cfg_n + 1)) - (4 * nnz if shared_cols else 0)
+    if shared_cols and dcols:
+        mat -= 2 * nnz
     return mat + 12 * cfg_n * w
 
 
@@ -298,7 +301,7 @@ def run_gpu(args, rank, world):
     # the solver's loop runs the fused iteration kernel while no recycle space
     # is active (every timed system of C2, C3, C5): that kernel is the dominant one
     fused = kt["k"] == 0 and kt["fused_ms"] > 0 and kt["fused_done_flag"] == 0
-    pf = alg_bytes_fused(cfg.n, cfg.nnz, w, kt["shared_cols"])
+    pf = alg_bytes_fused(cfg.n, cfg.nnz, w, kt["shared_cols"], kt["dcols"])
     if fused:
         dom_bytes, dom_ms, dom = pf, kt["fused_ms"], "fused"
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
@@ -396,6 +399,7 @@ def run_gpu(args, rank, world):
                      "pass1_event_ms": kt["pass1_ms"], "pass2_event_ms": kt["pass2_ms"],
                      "loop_graph_iter_ms": kt["graph_iter_ms"],
                      "k_active": kt["k"], "lazy_x": kt["lazy_x"], "shared_cols": kt["shared_cols"],
+                     "int16_col_deltas": kt["dcols"],
                      "tma_pass1": kt["tma_pass1"],
                      "iter_GBps": (p1 + p2) / (kt["graph_iter_ms"] * 1e-3) / 1e9,
                      "fused_ms": kt["fused_ms"] if kt["fused_ms"] > 0 else None,

@@ -199,7 +199,9 @@ int rbicg_dbg_project(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
  * one pattern and two value arrays), [14] ms per launch of the fused
  * iteration kernel (one kernel per iteration while no recycle space is
  * active; -1 when that form does not apply) as `iters` launches in one graph,
- * [15] 0 if those launches all did full work.  ms must hold 16 doubles. */
+ * [15] 0 if those launches all did full work, [16] 1 if the fused kernel
+ * streams int16 column deltas (banded A with a shared column array).  ms must
+ * hold 17 doubles. */
 int rbicg_dbg_time_kernels(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
                            const rbicg_opts *opts, int iters, double *ms);
 

@@ -189,7 +189,7 @@ class Context:
 
     def time_kernels(self, A, R=None, *, k=10, s=40, iters=20, trunc_tol=1e-6):
         o = Opts(k=k, s=s, max_itn=iters + 1, tol=0.0, trunc_tol=trunc_tol)
-        ms = (C.c_double * 16)()
+        ms = (C.c_double * 17)()
         check(lib.rbicg_dbg_time_kernels(self._h, A._h,
                                          R._h if R is not None else None,
                                          C.byref(o), iters, ms))
@@ -197,7 +197,8 @@ class Context:
                     lazy_x=bool(ms[4]), tma_pass1=bool(ms[5]), graph_iter_ms=ms[6],
                     graph_done_flag=ms[7], loop_iter_ms=ms[8], loop_done_flag=ms[9],
                     pass1_graph_ms=ms[10], pass2_graph_ms=ms[11], graph_each_done_flag=ms[12],
-                    shared_cols=bool(ms[13]), fused_ms=ms[14], fused_done_flag=ms[15])
+                    shared_cols=bool(ms[13]), fused_ms=ms[14], fused_done_flag=ms[15],
+                    dcols=bool(ms[16]))
 
 
 class Matrix:

@@ -616,6 +616,9 @@ struct Solver {
     la.abl = 0;
     la.pass2_tma = getenv("RBICG_NO_TMA2") ? 0 : 1;
     la.shared_cols = M->A.cols == M->AH.cols ? 1 : 0;
+    // int16 column deltas in the fused kernel for real data (C2 45.3 -> 44.3 us);
+    // complex measured slower with them (C4 94.5 -> 97.6 us)
+    la.dcols = (la.shared_cols && sizeof(T) == 8 && !getenv("RBICG_NO_DCOLS")) ? M->A.dcols : nullptr;
     // contiguous tile runs per CTA when the SpMV reaches at most 4 tiles away:
     // the neighbour tiles' vector rows are then L1 hits of the same SM (C2, 2-D
     // 1024^2: 46.2 -> 45.0 us); with a wide band (C3's +-36,864 rows) the
@@ -1996,7 +1999,8 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
     res->t_refresh_ms = S.t_refresh;
     res->t_total_ms = now_ms() - t_start;
     const double w = sizeof(T), kk = S.cur.k;
-    const double mat = 2.0 * (A->nnz * (w + 4) + 4.0 * (n + 1)) - (S.la.shared_cols ? 4.0 * A->nnz : 0.0);
+    const double mat = 2.0 * (A->nnz * (w + 4) + 4.0 * (n + 1)) - (S.la.shared_cols ? 4.0 * A->nnz : 0.0) -
+                       (S.fused && S.la.dcols ? 2.0 * A->nnz : 0.0);
     res->alg_bytes = fin.iter * (mat + 4.0 * kk * n * w + 20.0 * n * w);
     res->kernel_launches = (int32_t)(g_launches.load() - S.launches0);
   }
@@ -2315,6 +2319,7 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
   ms[11] = g2r.first;
   ms[12] = (g1r.second == 0 && g2r.second == 0) ? 0.0 : 1.0;
   ms[13] = S.la.shared_cols ? 1.0 : 0.0;
+  ms[16] = S.la.dcols ? 1.0 : 0.0;
   // the fused iteration (k = 0): `iters` launches of k_fused in one graph
   ms[14] = -1.0;
   ms[15] = -1.0;

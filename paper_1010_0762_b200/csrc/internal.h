@@ -28,6 +28,8 @@ struct DevMat {
   int32_t *cols = nullptr;
   void *vals = nullptr;
   int64_t bandwidth = -1;   // max |col - row| of A (-1: unknown, e.g. a row partition)
+  int16_t *dcols = nullptr; // col - row as int16 (banded A with one shared column array;
+                            // the fused kernel streams these instead of cols)
   int cols_shared = 0;      // cols aliases the other matrix's (A^* of a structurally
                             // symmetric A: same SELL column array, build_t)
 };
@@ -78,6 +80,7 @@ struct LoopArgs {
   int pass2_tma;           // pass 2 streams its tiles through smem via TMA
   int shared_cols;         // A and A^* share one SELL column array (structurally symmetric A)
   int tile_contig;         // fused form: contiguous tile runs per CTA instead of grid-strided
+  const int16_t *dcols;    // fused form: int16 column deltas (null: int32 columns)
   int lazy_x;              // x, x~ rebuilt per segment from the Lanczos ring
   T *pseg[2], *ptseg[2];   // p_a, p~_a at the start of the open segment, by segment parity
   int cyc;                 // cycle length s (segment parity = (seg_start / s) & 1)

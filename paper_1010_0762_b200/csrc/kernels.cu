@@ -680,6 +680,63 @@ __device__ __forceinline__ void fused_leader(const LoopArgs<T> &a, DevState<T> *
   }
 }
 
+// Banded A with one shared column array (DC): the tile's columns arrive as
+// int16 deltas col - row (2 bytes per nonzero instead of 4); A and A^* share
+// them, so one delta serves both gathers of a nonzero slot.
+template <typename T> __host__ __device__ __forceinline__ size_t dc_mat_bytes(const LoopArgs<T> &a) {
+  return (size_t)a.tile_max * (2 + 2 * sizeof(T));
+}
+template <typename T>
+__device__ __forceinline__ void fused_issue_dc(const LoopArgs<T> &a, unsigned char *stage, uint64_t *bar,
+                                               int64_t t) {
+  const int TM = a.tile_max;
+  int16_t *dA = reinterpret_cast<int16_t *>(stage);
+  T *vA = reinterpret_cast<T *>(stage + (size_t)TM * 2);
+  T *vH = vA + TM;
+  const int64_t ns = a.A.nslices;
+  const int64_t s0 = t * (BS / 32), s1 = min(s0 + BS / 32, ns);
+  const int64_t oA = a.A.sptr[s0], eA = a.A.sptr[s1];
+  const uint32_t nA = (uint32_t)(eA - oA);
+  mbar_expect_tx(bar, nA * (2u + 2u * (uint32_t)sizeof(T)));
+  if (!nA) return;
+  const uint64_t pol = policy_evict_first();
+  tma_load_1d_hint(dA, a.dcols + oA, nA * 2u, bar, pol);
+  tma_load_1d_hint(vA, reinterpret_cast<const T *>(a.A.vals) + oA, nA * (uint32_t)sizeof(T), bar, pol);
+  tma_load_1d_hint(vH, reinterpret_cast<const T *>(a.AH.vals) + oA, nA * (uint32_t)sizeof(T), bar, pol);
+}
+template <typename T>
+__device__ __forceinline__ void fused_pair_dc(const int16_t *__restrict__ dA, const T *__restrict__ vA,
+                                              const T *__restrict__ vH, int w, int row,
+                                              const T *__restrict__ r, const T *__restrict__ nd,
+                                              const T *__restrict__ rt, const T *__restrict__ ndt,
+                                              T malpha, T beta, T cmalpha, T cb, T &zo, T &zto) {
+  zo = zero<T>();
+  zto = zero<T>();
+  for (int j0 = 0; j0 < w; j0 += 4) {
+    int cc[4];
+    T va[4], vh[4];
+    RZP<T> xa[4], xh[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int jj = j0 + q;
+      const bool in = jj < w;
+      cc[q] = in ? row + (int)dA[jj * 32] : 0;
+      va[q] = in ? vA[jj * 32] : zero<T>();
+      vh[q] = in ? vH[jj * 32] : zero<T>();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      xa[q] = ld_node(nd, r, cc[q]);
+      xh[q] = ld_node(ndt, rt, cc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      zo = mad(va[q], mad(beta, xa[q].p, mad(malpha, xa[q].z, xa[q].r)), zo);
+      zto = mad(vh[q], mad(cb, xh[q].p, mad(cmalpha, xh[q].z, xh[q].r)), zto);
+    }
+  }
+}
+
 constexpr int TRV = BS + 4;   // staged vector rows per tile: the tile and 2 rows each side
 template <typename T> __host__ __device__ __forceinline__ size_t fused_vec_bytes() {
   return (size_t)6 * TRV * sizeof(T);   // r, {z, p} (2), r~, {z~, p~} (2)
@@ -706,7 +763,7 @@ __device__ __forceinline__ void fused_issue_vec(unsigned char *vb, uint64_t *bar
   tma_load_1d(d + 4 * TRV, ndt + 2 * (int64_t)lo, nb, bar);
 }
 
-template <typename T, int MINB, bool VS = false>
+template <typename T, int MINB, bool VS = false, bool DC = false>
 __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   __shared__ T s_fin[NFUSED + 1];
   __shared__ T s_w[NFUSED][BS / 32];
@@ -726,7 +783,7 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   const int64_t t0 = a.tile_contig ? (ntiles * blockIdx.x) / G64 : blockIdx.x;
   const int64_t t1 = a.tile_contig ? (ntiles * (blockIdx.x + 1)) / G64 : ntiles;
   const int64_t tstep = a.tile_contig ? 1 : G64;
-  const size_t mat_bytes = p1_mat_bytes<T>(a);
+  const size_t mat_bytes = DC ? dc_mat_bytes<T>(a) : p1_mat_bytes<T>(a);
   const size_t stage_bytes = mat_bytes + (VS ? fused_vec_bytes<T>() : 0);
   const int nst = a.p1_stages;
   if (tid == 0) {   // VS: two arrivals per stage (matrix part, vector part)
@@ -737,8 +794,10 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   __syncthreads();
   if (tid == 0)
     for (int q = 0; q < nst; ++q)
-      if (t0 + q * tstep < t1)
-        p1_issue<T>(a, f_smem + q * stage_bytes, stage_bytes, &bars[q], t0 + q * tstep);
+      if (t0 + q * tstep < t1) {
+        if (DC) fused_issue_dc<T>(a, f_smem + q * stage_bytes, &bars[q], t0 + q * tstep);
+        else p1_issue<T>(a, f_smem + q * stage_bytes, stage_bytes, &bars[q], t0 + q * tstep);
+      }
   pdl_wait();
   if (tid == 0) {
     s_i[0] = __ldcg(&st->kidx);
@@ -813,9 +872,16 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
     if (tid < rows) {
       const int64_t row = row0 + tid;
       T z, zt;
-      fused_pair_smem<T, VS>(scA + (oA - bA) + lane, svA + (oA - bA) + lane, wA,
-                             scH + (oH - bH) + lane, svH + (oH - bH) + lane, wH, r, zpo, rt, ztpo, vs,
-                             malpha, beta, cmalpha, cb, z, zt);
+      if (DC) {
+        const int16_t *sdc = reinterpret_cast<const int16_t *>(base);
+        const T *dvA = reinterpret_cast<const T *>(base + (size_t)TM * 2);
+        fused_pair_dc<T>(sdc + (oA - bA) + lane, dvA + (oA - bA) + lane, dvA + TM + (oA - bA) + lane, wA,
+                         (int)row, r, zpo, rt, ztpo, malpha, beta, cmalpha, cb, z, zt);
+      } else {
+        fused_pair_smem<T, VS>(scA + (oA - bA) + lane, svA + (oA - bA) + lane, wA,
+                               scH + (oH - bH) + lane, svH + (oH - bH) + lane, wH, r, zpo, rt, ztpo, vs,
+                               malpha, beta, cmalpha, cb, z, zt);
+      }
       const RZP<T> o = VS ? node_at(zpo, r, vs.nd, vs.r, vs.lo, vs.cnt, (int)row) : ld_node(zpo, r, row);
       const RZP<T> ot = VS ? node_at(ztpo, rt, vs.ndt, vs.rt, vs.lo, vs.cnt, (int)row) : ld_node(ztpo, rt, row);
       const T rr = mad(malpha, o.z, o.r);
@@ -844,7 +910,8 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
     }
     __syncthreads();   // stage si consumed
     if (tid == 0 && tile + nst * tstep < t1) {
-      p1_issue<T>(a, f_smem + si * stage_bytes, stage_bytes, &bars[si], tile + nst * tstep);
+      if (DC) fused_issue_dc<T>(a, f_smem + si * stage_bytes, &bars[si], tile + nst * tstep);
+      else p1_issue<T>(a, f_smem + si * stage_bytes, stage_bytes, &bars[si], tile + nst * tstep);
       if (VS)
         fused_issue_vec<T>(f_smem + si * stage_bytes + mat_bytes, &bars[si], tile + nst * tstep, n, r, zpo,
                            rt, ztpo);
@@ -1212,7 +1279,8 @@ __global__ void __launch_bounds__(BS, MINB) k_fusedk(LoopArgs<T> a) {
 
 
 template <typename T> size_t fused_smem(const LoopArgs<T> &a, bool vs) {
-  return (size_t)a.p1_stages * (p1_mat_bytes<T>(a) + (vs ? fused_vec_bytes<T>() : 0));
+  const size_t mat = (a.dcols && !vs) ? dc_mat_bytes<T>(a) : p1_mat_bytes<T>(a);
+  return (size_t)a.p1_stages * (mat + (vs ? fused_vec_bytes<T>() : 0));
 }
 
 // ============================================================== launchers
@@ -1311,8 +1379,10 @@ template <typename T> void launch_fused(const LoopArgs<T> &a0, cudaStream_t s) {
   // (complex: 3 CTAs/SM, 80 registers -- 64 spill with the 256-bit node loads)
   static const int minb_env = getenv("RBICG_FUSED_MINB") ? atoi(getenv("RBICG_FUSED_MINB")) : 0;
   const int minb = minb_env ? minb_env : (sizeof(T) == 8 ? 4 : 3);
-  auto fn = vs ? (minb >= 4 ? k_fused<T, 4, true> : k_fused<T, 3, true>)
-              : (minb >= 6 ? k_fused<T, 6> : minb == 5 ? k_fused<T, 5> : minb == 4 ? k_fused<T, 4> : k_fused<T, 3>);
+  const bool dc = a.dcols != nullptr && !vs;
+  auto fn = dc ? (minb >= 4 ? k_fused<T, 4, false, true> : k_fused<T, 3, false, true>)
+          : vs ? (minb >= 4 ? k_fused<T, 4, true> : k_fused<T, 3, true>)
+               : (minb >= 6 ? k_fused<T, 6> : minb == 5 ? k_fused<T, 5> : minb == 4 ? k_fused<T, 4> : k_fused<T, 3>);
   static const int carve = getenv("RBICG_FUSED_CARVEOUT") ? atoi(getenv("RBICG_FUSED_CARVEOUT")) : -1;
   if (carve >= 0) RB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
   int per_sm = 1;
@@ -1459,6 +1529,10 @@ void prepare_kernels() {
   allow_max_dyn_smem(k_fusedk<double, 3>);
   allow_max_dyn_smem(k_fusedk<zc, 4>);
   allow_max_dyn_smem(k_fusedk<zc, 3>);
+  allow_max_dyn_smem(k_fused<double, 4, false, true>);
+  allow_max_dyn_smem(k_fused<double, 3, false, true>);
+  allow_max_dyn_smem(k_fused<zc, 4, false, true>);
+  allow_max_dyn_smem(k_fused<zc, 3, false, true>);
   allow_max_dyn_smem(k_fused<double, 4, true>);
   allow_max_dyn_smem(k_fused<double, 3, true>);
   allow_max_dyn_smem(k_fused<zc, 4, true>);

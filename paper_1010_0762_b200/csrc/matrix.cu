@@ -97,6 +97,17 @@ __global__ void k_bandwidth(const int32_t *rowptr, const int32_t *col, int64_t n
   atomicMax(bw, m);
 }
 
+// SELL column deltas col - row (row = slice * 32 + lane), int16
+__global__ void k_make_dcols(const int32_t *cols, const int64_t *sptr, int64_t nslices, int16_t *dc) {
+  for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {
+    const int64_t o = sptr[sl], e = sptr[sl + 1];
+    for (int64_t q = o + threadIdx.x; q < e; q += blockDim.x) {
+      const int64_t row = sl * 32 + ((q - o) & 31);
+      dc[q] = (int16_t)(cols[q] - row);
+    }
+  }
+}
+
 static int grid1d(int64_t m) { return (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 148 * 32)); }
 
 template <typename T>
@@ -142,6 +153,15 @@ static void csr_to_sell(rbicg_ctx *ctx, int64_t n, const int32_t *rowptr, const 
 // sorted column list in row i of A and of A^*: the SELL column arrays are then
 // identical and A^* keeps only its values -- pass 1 streams 4 bytes less per
 // nonzero of A^* (DESIGN §6).  Decided by comparing the built arrays.
+static void make_dcols(rbicg_ctx *ctx, rbicg_mat *M) {
+  DevMat &A = M->A;
+  if (getenv("RBICG_NO_DCOLS") || !M->AH.cols_shared || A.bandwidth < 0 || A.bandwidth > 32767) return;
+  A.dcols = (int16_t *)ws_alloc(sizeof(int16_t) * std::max<int64_t>(A.padded, 1));
+  k_make_dcols<<<(int)std::min<int64_t>(std::max<int64_t>(A.nslices, 1), 4096), 256, 0, ctx->stream>>>(
+      A.cols, A.sptr, A.nslices, A.dcols);
+  count_launch();
+}
+
 static void share_cols(rbicg_ctx *ctx, rbicg_mat *M) {
   if (getenv("RBICG_NO_SHARED_COLS")) return;
   DevMat &A = M->A, &H = M->AH;
@@ -222,6 +242,7 @@ static void build_t(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowpt
     if (!h) {
       csr_to_sell<T>(ctx, n, rowptr, col, valT, M->AH);
       share_cols(ctx, M);
+      make_dcols(ctx, M);
       RB_CUDA(cudaStreamSynchronize(st));
       ws_free(valT);
       return;
@@ -254,6 +275,7 @@ static void build_t(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowpt
   count_launch(3);
   csr_to_sell<T>(ctx, n, rowptrT, colT, valT, M->AH);
   share_cols(ctx, M);
+  make_dcols(ctx, M);
   RB_CUDA(cudaStreamSynchronize(st));
   for (void *p : {(void *)rowidx, (void *)iota, (void *)keys_out, (void *)perm, (void *)cnt,
                   (void *)rowptrT, (void *)colT, (void *)valT, tmp})
@@ -291,6 +313,7 @@ void free_devmat(DevMat &m) {
   // pooled device memory (reused by the next system's store); no device sync
   ws_free(m.sptr);
   if (!m.cols_shared) ws_free(m.cols);
+  if (m.dcols) ws_free(m.dcols);
   ws_free(m.vals);
   m = DevMat();
 }
