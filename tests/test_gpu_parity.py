@@ -563,13 +563,13 @@ def test_irka_gpu_matches_oracle(ctx, strategy, reuse_tol):
         assert abs(gr - g) <= 1e-8 * abs(g) and abs(dgr - dg) <= 1e-6 * abs(dg)
 
 
-@pytest.mark.parametrize("env", ["RBICG_NO_SHARED_COLS", "RBICG_NO_SYM_T"])
+@pytest.mark.parametrize("env", ["RBICG_NO_SHARED_COLS", "RBICG_NO_SYM_T", "RBICG_NO_DCOLS"])
 def test_shared_column_array_bitwise(ctx, monkeypatch, env):
     """A structurally symmetric A (the conv-diff stencils) keeps one SELL
     column array for A and A^* (matrix.cu share_cols) and gets A^*'s values
-    by the search-based transpose (k_sym_transpose): the solve must be
-    bitwise identical to the one with two column arrays / the sorted
-    transpose."""
+    by the search-based transpose (k_sym_transpose), and the fused kernel
+    streams int16 column deltas: the solve must be bitwise identical to the
+    one with two column arrays / the sorted transpose / int32 columns."""
     cfg = CONFIGS["C3"].scaled(20, systems=1)
     item = next(system_sequence(cfg))
     outs = []
@@ -579,6 +579,8 @@ def test_shared_column_array_bitwise(ctx, monkeypatch, env):
         M = ctx.matrix(item["indptr"], item["indices"], item["data"])
         kt = ctx.time_kernels(M, None, k=0, s=cfg.s, iters=3)
         assert kt["shared_cols"] == (not off or env != "RBICG_NO_SHARED_COLS")
+        if env == "RBICG_NO_DCOLS":
+            assert kt["dcols"] == (not off)
         rec = ctx.recycle(cfg.n, cfg.k)
         x, xt, res, _ = ctx.solve_dual(M, item["b"], item["bt"], R=rec, k=cfg.k, s=cfg.s,
                                        tol=cfg.tol, max_itn=cfg.max_itn,
