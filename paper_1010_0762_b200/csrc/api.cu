@@ -423,6 +423,13 @@ struct Solver {
     tmp.U = alloc((size_t)nx * kmax);
     tmp.Ut = alloc((size_t)nx * kmax);
   }
+  // the cycle-end candidate's U, Ũ: written only when a truncation keeps
+  // directions (never on C2/C3/C5), so allocated then
+  template <typename BB> void ensure_basis_u(BB &B) {
+    if (B.U) return;
+    B.U = alloc((size_t)nx * kmax);
+    B.Ut = alloc((size_t)nx * kmax);
+  }
   ~Solver() {
     static const bool tm = getenv("RBICG_TIMING") != nullptr;
     const double t0 = tm ? now_ms() : 0;
@@ -477,7 +484,7 @@ struct Solver {
       // decision is kept per (ctx, n, k, s) so a sequence does not query the
       // allocator every system (cudaMemGetInfo measured up to 20 ms)
       const size_t extra = (size_t)2 * ring * n * sizeof(T);
-      const int nblk = (k_basis == 0 ? 4 : 6) * kmax + 4 * std::max(k_basis, 0);   // (lazy U_j temporaries)
+      const int nblk = (k_basis == 0 ? 2 : 6) * kmax + 4 * std::max(k_basis, 0);   // (lazy U_j, candidate blocks)
       const size_t need = extra + (size_t)(nblk + 2 * ring + 24) * n * sizeof(T);
       const uint64_t key = ((uint64_t)n << 20) ^ ((uint64_t)kmax << 10) ^ ((uint64_t)k_basis << 40) ^
                            (uint64_t)o.s ^ (sizeof(T) << 60);
@@ -569,7 +576,7 @@ struct Solver {
       // present) and the partitioned refresh write them -- allocated on first
       // use when the system starts without a space (C5 fits the overlapped
       // cycle end on one GPU thanks to the 2 n x k blocks saved)
-      const bool lazy_u = B == &tmp && tmp_u_lazy();
+      const bool lazy_u = (B == &tmp || B == &cand[0]) && tmp_u_lazy();
       B->U = kb && !lazy_u ? alloc((size_t)nx * kb) : nullptr;
       B->Ut = kb && !lazy_u ? alloc((size_t)nx * kb) : nullptr;
       B->k = 0;
@@ -774,6 +781,7 @@ struct Solver {
       return v;
     };
     Phase ph("biorth.gemm4", bs);
+    ensure_basis_u(out);
     gemm_panels<T>(cols_of(U), Fu, pk, n, out.U, ctx, bs);
     gemm_panels<T>(cols_of(Ut), Fut, pk, n, out.Ut, ctx, bs);
     if (with_c) {
@@ -1419,6 +1427,7 @@ struct Solver {
           biorth(nullptr, nullptr, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false, &Fu, &Fut,
                  gvf.empty() ? nullptr : &gvf);
           if (out.k > 0) {   // U_j N_p = [V_j rows] (W_j N_p) (scalings folded in Wrow)
+            ensure_basis_u(out);
             const int pk = out.k;
             std::vector<ColDesc> Xv, Xvt;
             std::vector<cplx> Mu((size_t)s * pk, 0.0), Mut((size_t)s * pk, 0.0);
