@@ -48,3 +48,21 @@ def test_gpu_arm_json():
     assert d["gpu_launches"] > 0
     assert "sm_mhz" in d["clocks"] and isinstance(d["clocks"]["reasons"], list)
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
+
+
+def test_algorithmic_byte_formulas():
+    """The roofline's algorithmic bytes on C2's sizes, by hand:
+    SELL-equivalent matrix pair = 2 (nnz (8 + 4) + 4 (n + 1)), one shared
+    column array saves 4 nnz, int16 deltas 2 nnz more; the fused kernel moves
+    12 n-vectors, pass 1 / pass 2 (k = 0, lazy x) 8 and 6."""
+    sys.path.insert(0, ROOT)
+    import bench
+    n, nnz = 1048576, 5238784
+    mat = 2 * (nnz * 12 + 4 * (n + 1))
+    assert bench.alg_bytes_fused(n, nnz, 8, False, False) == mat + 12 * n * 8
+    assert bench.alg_bytes_fused(n, nnz, 8, True, False) == mat - 4 * nnz + 12 * n * 8
+    assert bench.alg_bytes_fused(n, nnz, 8, True, True) == 203350024
+    p1, p2 = bench.alg_bytes(n, nnz, 0, 8, True, True)
+    assert p1 == mat - 4 * nnz + 8 * n * 8 and p2 == 6 * n * 8
+    p1k, p2k = bench.alg_bytes(n, nnz, 10, 8, True, True)
+    assert p1k - p1 == 2 * 10 * n * 8 and p2k - p2 == 2 * 10 * n * 8
