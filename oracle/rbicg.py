@@ -14,7 +14,11 @@ bilinear form u^*A^{-1}w                PAPER.md:63-67 (+Q19)
 
 The pencil is assembled with plain explicit products (Q15): B_j = Ĉ^*AV_j is
 formed by explicit sparse products of the stored Lanczos vectors, and
-P = H~^*(Ψ~^*Ψ)H, Q = H~^*(Ψ~^*Φ) by dense products.
+P = H~^*(Ψ~^*Ψ)H, Q = H~^*(Ψ~^*Φ) by dense products.  ``pencil="fast"``
+ takes Ψ~^*Ψ and Ψ~^*Φ from the §4.4 recurrences instead
+(fast_grams): the paper's exact-arithmetic identities, so
+the two agree while the Lanczos vectors stay bi-orthogonal (pinned against
+the plain products in tests/test_oracle_fast_pencil.py).
 """
 from __future__ import annotations
 
@@ -58,15 +62,20 @@ def adjoint(A):
 # ----------------------------------------------------------------------------
 # R1 / R6: bi-orthogonal C, C~, truncation reading Q13
 # ----------------------------------------------------------------------------
-def biorthogonalize(A, AH, U, Ut, trunc_tol):
+def biorthogonalize(A, AH, U, Ut, trunc_tol, return_maps=False):
     """C = AU, C~ = A^*Ũ; scale column pairs to unit norm (Q13); SVD
     C~^*C = M Σ N^* (equationSVD, PAPER.md:691-694); keep σ_i >= trunc_tol σ_1;
     U <- U N_p, Ũ <- Ũ M_p, C <- C N_p, C~ <- C~ M_p (equationForUC,
-    PAPER.md:695-700); D_c = Σ_p."""
+    PAPER.md:695-700); D_c = Σ_p.
+
+    return_maps=True also returns the column maps (T, T~) with U_out = U T,
+    Ũ_out = Ũ T~ (the §4.4 recurrences carry them)."""
     n = U.shape[0]
+    kin = U.shape[1]
     dt = np.result_type(U.dtype, Ut.dtype, A.dtype)
-    if U.shape[1] == 0:
-        return empty_basis(n, dt)
+    none = (np.zeros((kin, 0), dt), np.zeros((kin, 0), dt))
+    if kin == 0:
+        return (empty_basis(n, dt), none) if return_maps else empty_basis(n, dt)
     C = np.asarray(A @ U, dtype=dt)
     Ct = np.asarray(AH @ Ut, dtype=dt)
     nc = np.linalg.norm(C, axis=0)
@@ -75,7 +84,7 @@ def biorthogonalize(A, AH, U, Ut, trunc_tol):
     U, Ut, C, Ct = U[:, keep], Ut[:, keep], C[:, keep], Ct[:, keep]
     nc, nct = nc[keep], nct[keep]
     if U.shape[1] == 0:
-        return empty_basis(n, dt)
+        return (empty_basis(n, dt), none) if return_maps else empty_basis(n, dt)
     U = U / nc
     C = C / nc
     Ut = Ut / nct
@@ -86,8 +95,15 @@ def biorthogonalize(A, AH, U, Ut, trunc_tol):
     # "pick p such that σ_p >= tol > σ_{p+1}": absolute test on
     # the Gram of unit-norm columns, i.e. on cosines (reading Q13)
     p = int(np.sum(S >= trunc_tol))
-    return Basis(U @ N[:, :p], Ut @ M[:, :p], C @ N[:, :p], Ct @ M[:, :p],
-                 S[:p].copy())
+    out = Basis(U @ N[:, :p], Ut @ M[:, :p], C @ N[:, :p], Ct @ M[:, :p],
+                S[:p].copy())
+    if not return_maps:
+        return out
+    Tm = np.zeros((kin, p), dt)
+    Ttm = np.zeros((kin, p), dt)
+    Tm[keep, :] = N[:, :p] / nc[:, None]
+    Ttm[keep, :] = M[:, :p] / nct[:, None]
+    return out, (Tm, Ttm)
 
 
 # ----------------------------------------------------------------------------
@@ -270,7 +286,7 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
                s=40, tol=1e-8, max_itn=20000, trunc_tol=1e-6,
                xt_redraw=None, update_recycle=True, force_iters=None,
                keep_pencils=False, breakdown_tol=BREAKDOWN_EPS,
-               variant="standard"):
+               variant="standard", pencil="plain"):
     """Solve A x = b and A^* x~ = b~ with RBiCG (Algorithm 2)
     using the recycle space (U, Ũ) (may be None/empty: first system), and
     build the recycle space for the next system (§4).
@@ -298,6 +314,8 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
     """
     if variant not in ("standard", "single_reduction", "lookahead"):
         raise ValueError(variant)
+    if pencil not in ("plain", "fast"):
+        raise ValueError(pencil)
     pipe = variant == "single_reduction"
     look = variant == "lookahead"
     n = A.shape[0]
@@ -343,6 +361,12 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
 
     # recycle-space update state
     cand = None           # (U_j, Ũ_j, C_j, C~_j) from the last full cycle
+    # pencil="fast" (§4.4): the blocks carried from cycle to
+    # cycle; C~^*U "must be computed at most once per linear system"
+    fast = None
+    if pencil == "fast":
+        fast = dict(prev=None,
+                    CtU=basis.Ct.conj().T @ basis.U if kc else None)
     cycles = 0
     pencils = []
 
@@ -459,7 +483,7 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
         if update_recycle and k > 0 and i % s == 0 and (converged or not serious):
             j = i // s
             cand = _cycle_end(A, AH, L, j, s, basis, cand, k, trunc_tol, dt,
-                              real, pencils if keep_pencils else None)
+                              real, pencils if keep_pencils else None, fast)
             cycles += 1
             L.forget_before((j * s) - 1)
         if converged:
@@ -506,11 +530,89 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
                        pencils=pencils, r=r, rt=rt)
 
 
-def _cycle_end(A, AH, L, j, s, basis, cand, k, trunc_tol, dt, real, pencils):
-    """Build U_j, Ũ_j at the end of cycle j (R5/R6)."""
+def _lanczos_biorth(rows_a, rows_b, dt):
+    """Ῡ_a^*Υ_b in exact arithmetic: ṽ_m^*v_l = δ_ml, the bi-orthogonality of
+    the Lanczos vectors under the scaling (scalingfactor) of PAPER.md:506-512
+    -- the shifted identities of PAPER.md:853-868 and :883-897."""
+    return np.array([[1.0 if ra == rb else 0.0 for rb in rows_b] for ra in rows_a],
+                    dtype=dt).reshape(len(rows_a), len(rows_b))
+
+
+def fast_grams(j, s, basis, cand, fast, Upst, X0, dt):
+    """Ψ~_j^*Ψ_j and Ψ~_j^*Φ_j by the recurrences of §4.4.
+
+    Ψ_j = [C, C_{j-1}, Υ_j] and Φ_j = [X0, V_j] with X0 = U_{j-1} (or U in the
+    first cycle of a later system); blocks absent in a case are dropped.  With
+    AΦ_{j-1} = Ψ_{j-1}H_{j-1} and U_{j-1} = Φ_{j-1}F_{j-1} (F = W_{j-1}N_{j-1}
+    incl. the Q13 column scaling), every block follows from cycle j-1's small
+    matrices (carried in ``fast["prev"]``) and the exact relations
+    C~^*Υ_j = 0, Ῡ_j^*C = 0 (the residuals are kept ⊥ C~, ⊥ C),
+    C~_{j-2} ⊥ Υ_j, C_{j-2} ⊥ Ῡ_j (biorthj), Ῡ^*Υ = shifted
+    identities, C~^*C = D_c, C~_{j-1}^*C_{j-1} = Σ_{j-1}:
+      C~^*C_{j-1}      = [C~^*C_{j-2}, D_cB_{j-1}] W_{j-1}N_{j-1}        (P:785-810)
+      C~_{j-1}^*C      = N~^*W~^*[C~_{j-2}^*C; B~^*D_c]                  (P:818-826)
+      C~_{j-1}^*Υ_j    = N~^*W~^*[0; Γ~_{j-1}^*Ῡ_{j-1}^*Υ_j]
+      Ῡ_j^*C_{j-1}     = [0, Ῡ_j^*Υ_{j-1}Γ_{j-1}] W_{j-1}N_{j-1}
+      C~^*U_{j-1}      = [C~^*U_{j-2}, 0] W_{j-1}N_{j-1}                 (P:899-913)
+      C~_{j-1}^*U_{j-1} = N~^*W~^*[[C~_{j-2}^*U_{j-2}, C~_{j-2}^*V_{j-1}],
+                                  [Ṽ_{j-1}^*C_{j-2}, T~_{j-1}]] W N
+    written here in the compact form F~^*H~^*(Ψ~_{j-1}^*·) and (·Ψ_{j-1})HF
+    of the same products.  The one O(n) product is Ῡ_j^*X0; C~^*U in
+    the first cycle of a later system is the once-per-system block."""
+    kc = basis.k
+    have_prev = cand is not None and cand.k > 0
+    ps = fast["prev"] if have_prev else None
+    kp = cand.k if have_prev else 0
+    rows = list(fast["rows"])
+    cols = list(fast["cols"])
+    nr = len(rows)
+    top = 1 if j > 1 else 0
+    kx = X0.shape[1]
+    iC = slice(0, kc)
+    iP = slice(kc, kc + kp)
+    iU = slice(kc + kp, kc + kp + nr)
+    m = kc + kp + nr
+    G1 = np.zeros((m, m), dt)
+    G2 = np.zeros((m, kx + s), dt)
+    if kc:
+        G1[iC, iC] = np.diag(basis.d)                       # D_c
+    G1[iU, iU] = np.eye(nr)                                 # Ῡ_j^*Υ_j = I
+    if have_prev:
+        pC = slice(0, ps["kc"])
+        pU = slice(ps["kc"] + ps["kp"], ps["m"])
+        HF = ps["H"] @ ps["F"]                              # C_{j-1} = Ψ_{j-1}(H F)
+        HFt = ps["Ht"] @ ps["Ft"]                           # C~_{j-1} = Ψ~_{j-1}(H~ F~)
+        if kc:
+            G1[iC, iP] = ps["G1"][pC, :] @ HF               # C~^*C_{j-1}
+            G1[iP, iC] = HFt.conj().T @ ps["G1"][:, pC]     # C~_{j-1}^*C
+            G2[iC, :kx] = ps["G2"][pC, :] @ ps["F"]         # C~^*U_{j-1}
+        G1[iP, iP] = np.diag(cand.d)                        # Σ_{j-1}
+        Z = np.zeros((ps["m"], nr), dt)                     # Ψ~_{j-1}^*Υ_j
+        Z[pU, :] = _lanczos_biorth(ps["rows"], rows, dt)
+        G1[iP, iU] = HFt.conj().T @ Z                       # C~_{j-1}^*Υ_j
+        Zt = np.zeros((nr, ps["m"]), dt)                    # Ῡ_j^*Ψ_{j-1}
+        Zt[:, pU] = _lanczos_biorth(rows, ps["rows"], dt)
+        G1[iU, iP] = Zt @ HF                                # Ῡ_j^*C_{j-1}
+        G2[iP, :kx] = HFt.conj().T @ ps["G2"] @ ps["F"]     # C~_{j-1}^*U_{j-1}
+        G2[iP, kx:] = G1[iP, iU][:, top:top + s]            # C~_{j-1}^*V_j
+    elif kc:
+        G2[iC, :kx] = fast["CtU"]                           # C~^*U (once per system)
+    G2[iU, :kx] = Upst.conj().T @ X0                        # Ῡ_j^*X0: the O(n) product
+    G2[iU, kx:] = _lanczos_biorth(rows, cols, dt)           # Ῡ_j^*V_j = I with zero rows
+    return G1, G2
+
+
+def _cycle_end(A, AH, L, j, s, basis, cand, k, trunc_tol, dt, real, pencils,
+               fast=None):
+    """Build U_j, Ũ_j at the end of cycle j (R5/R6); with
+    ``fast`` the pencil's Grams come from fast_grams (§4.4)."""
     Ups, Upst, Gam, Gamt, V, Vt = cycle_blocks(L, j, s, dt)
     kc = basis.k
     have_prev = cand is not None and cand.k > 0
+    cols = list(range((j - 1) * s + 1, j * s + 1))
+    rows = ([(j - 1) * s] if j > 1 else []) + cols + [j * s + 1]
+    if fast is not None:
+        fast["rows"], fast["cols"] = rows, cols
     if not have_prev and kc == 0:
         # first system, no recycle data: eigenvectors of T_j (PAPER.md:615-627)
         top = 1 if j > 1 else 0
@@ -518,6 +620,11 @@ def _cycle_end(A, AH, L, j, s, basis, cand, k, trunc_tol, dt, real, pencils):
         W, Wt, lam = solve_tridiag_first(Tj, k, real)
         Phi, Phit = V, Vt
         info = dict(j=j, case="T", P=Tj, Q=np.eye(s), lam=lam, W=W, Wt=Wt)
+        # for the next cycle's recurrences: AV_j = Υ_jΓ_j, Ῡ_j^*Υ_j = I
+        H, Ht = Gam, Gamt
+        G1 = np.eye(len(rows), dtype=dt)
+        G2 = _lanczos_biorth(rows, cols, dt)
+        kcb = kpb = 0
     else:
         if kc:
             # B_j = Ĉ^*AV_j, B~_j = Č^*A^*Ṽ_j by explicit products
@@ -557,15 +664,29 @@ def _cycle_end(A, AH, L, j, s, basis, cand, k, trunc_tol, dt, real, pencils):
             Ht = _blk([[np.eye(kc), Bt],
                        [np.zeros((Gamt.shape[0], kc)), Gamt]], dt)
         # finalGenEigValue
-        P = Ht.conj().T @ (Psit.conj().T @ Psi) @ H
-        Q = Ht.conj().T @ (Psit.conj().T @ Phi)
+        kcb, kpb = kc, (cand.k if have_prev else 0)
+        if fast is None:
+            G1 = Psit.conj().T @ Psi
+            G2 = Psit.conj().T @ Phi
+        else:
+            X0 = Phi[:, :Phi.shape[1] - s]
+            G1, G2 = fast_grams(j, s, basis, cand, fast, Upst, X0, dt)
+        P = Ht.conj().T @ G1 @ H
+        Q = Ht.conj().T @ G2
         W, Wt, lam = solve_pencil(P, Q, k, real)
         info = dict(j=j, case="pencil", P=P, Q=Q, lam=lam, W=W, Wt=Wt,
-                    B=B if kc else None, Bt=Bt if kc else None)
+                    B=B if kc else None, Bt=Bt if kc else None, G1=G1, G2=G2,
+                    kc=kcb, kp=kpb)
+        if fast is not None and pencils is not None:   # the plain Grams, for the pins
+            info.update(G1_plain=Psit.conj().T @ Psi, G2_plain=Psit.conj().T @ Phi)
     Unew = Phi @ W.astype(dt)
     Utnew = Phit @ Wt.astype(dt)
     # §4.3: C_j = AU_j, C~_j = A^*Ũ_j, SVD, truncation
-    out = biorthogonalize(A, AH, Unew, Utnew, trunc_tol)
+    out, (Tm, Ttm) = biorthogonalize(A, AH, Unew, Utnew, trunc_tol, return_maps=True)
+    if fast is not None:
+        fast["prev"] = dict(G1=G1, G2=G2, H=np.asarray(H, dt), Ht=np.asarray(Ht, dt),
+                            F=W.astype(dt) @ Tm, Ft=Wt.astype(dt) @ Ttm,
+                            kc=kcb, kp=kpb, m=G1.shape[0], rows=rows)
     if pencils is not None:
         info.update(Phi=Phi, Phit=Phit, Unew=Unew, Utnew=Utnew, Gam=Gam,
                     Gamt=Gamt, V=V, Vt=Vt, Ups=Ups, Upst=Upst,

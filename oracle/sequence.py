@@ -20,7 +20,7 @@ def csr_matrix(item):
 
 
 def run_sequence(cfg, items, k=None, s=None, tol=None, max_itn=None,
-                 recycle=True, callback=None, force_iters=None):
+                 recycle=True, callback=None, force_iters=None, pencil="plain"):
     """Solve every system in ``items`` (dicts from synth.system_sequence) in
     order, carrying the recycle space.  Returns a list of SolveResult."""
     from synth import redraw_vector  # inputs only
@@ -43,7 +43,8 @@ def run_sequence(cfg, items, k=None, s=None, tol=None, max_itn=None,
                          k=k if recycle else 0, s=s, tol=tol, max_itn=max_itn,
                          trunc_tol=cfg.trunc_tol,
                          xt_redraw=redraw_vector(cfg, item["j"], n),
-                         update_recycle=recycle and k > 0, force_iters=fi)
+                         update_recycle=recycle and k > 0, force_iters=fi,
+                         pencil=pencil)
         if recycle:
             U, Ut = res.basis_out.U, res.basis_out.Ut
         if cfg.kind == "irka":
