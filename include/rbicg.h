@@ -104,7 +104,12 @@ typedef struct {
   int32_t record_history; /* fill `hist` when non-NULL                         */
   int32_t force_iters;    /* > 0: run exactly this many iterations, stop test
                              off (parity protocol Q27); 0 = normal            */
-  int32_t reserved;
+  int32_t pencil;         /* cycle-end pencil assembly with a recycle space:
+                             0 = explicit Grams Ψ~^*Ψ, Ψ~^*Φ of the stored
+                             vectors (plain, reading Q15); 1 = the §4.4
+                             recurrences: carried small blocks,
+                             only Ῡ_j^*U_{j-1} and, once per system,
+                             C~^*U are O(n) products                       */
 } rbicg_opts;
 
 typedef struct {

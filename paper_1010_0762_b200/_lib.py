@@ -73,7 +73,7 @@ class Opts(C.Structure):
                 ("tol", C.c_double), ("trunc_tol", C.c_double),
                 ("seed", C.c_uint64), ("update_recycle", C.c_int32),
                 ("record_history", C.c_int32), ("force_iters", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("pencil", C.c_int32)]
 
 
 class Result(C.Structure):

@@ -105,9 +105,14 @@ class Context:
     # ------------------------------------------------------------ solve
     def solve_dual(self, A, b, bt, x=None, xt=None, R=None, *, k=10, s=40,
                    tol=1e-8, max_itn=20000, trunc_tol=1e-6, update_recycle=True,
-                   force_iters=0, xt_redraw=None, history=False, inplace=False):
+                   force_iters=0, xt_redraw=None, history=False, inplace=False,
+                   pencil="plain"):
         """inplace=True: x, xt (given, contiguous, b's dtype) are the in/out
-        buffers themselves (e.g. page-locked host arrays); otherwise copies."""
+        buffers themselves (e.g. page-locked host arrays); otherwise copies.
+        pencil: "plain" (explicit Grams) or "fast" (§4.4 recurrences,
+        rbicg_opts.pencil = 1)."""
+        if pencil not in ("plain", "fast"):
+            raise ValueError(pencil)
         dev = _is_torch(b)
         if inplace:
             assert x is not None and xt is not None
@@ -124,7 +129,8 @@ class Context:
                 xt = np.array(xt, dtype=b.dtype, copy=True)
         o = Opts(k=k, s=s, max_itn=max_itn, tol=tol, trunc_tol=trunc_tol, seed=0,
                  update_recycle=1 if update_recycle else 0,
-                 record_history=1 if history else 0, force_iters=force_iters)
+                 record_history=1 if history else 0, force_iters=force_iters,
+                 pencil=1 if pencil == "fast" else 0)
         res = Result()
         hist = None
         if history:

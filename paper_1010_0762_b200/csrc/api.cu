@@ -377,6 +377,17 @@ struct Solver {
     std::vector<double> d;
   } cur, cand[1], tmp;   // cand keeps U, Ũ only (C, C~ are recomputed where needed)
   int cand_cur = -1;
+  // §4.4 (opts.pencil = 1): cycle j-1's small matrices for the recurrences of
+  // cycle j -- G1 = Ψ~^*Ψ (m x m), G2 = Ψ~^*Φ (m x mphi), H, H~ (m x mphi)
+  // with AΦ = ΨH, F, F~ (mphi x pk) with U_{j-1} = Φ F; Ψ = [C (kc), C_{j-2}
+  // (kp), Υ (rows)] -- all host, row-major
+  struct FastState {
+    bool valid = false;
+    int kc = 0, kp = 0, m = 0, mphi = 0, pk = 0;
+    std::vector<int> rows;
+    std::vector<cplx> G1, G2, H, Ht, F, Ft;
+  } fst;
+  std::vector<cplx> ctu;   // C~^*U (kc x kc), once per system
   DevState<T> *st = nullptr;
   DevState<T> *hst = nullptr;   // pinned host mirror
   IterRec<T> *hist = nullptr;
@@ -707,7 +718,8 @@ struct Solver {
   // straight from the Lanczos columns -- only when p > 0.
   void biorth(const T *U, const T *Ut, const T *C, const T *Ct, int kin, Basis &out,
               cudaStream_t bs, Comm *cm, bool with_c = true, std::vector<cplx> *Fu_out = nullptr,
-              std::vector<cplx> *Fut_out = nullptr, const std::vector<cplx> *gv_in = nullptr) {
+              std::vector<cplx> *Fut_out = nullptr, const std::vector<cplx> *gv_in = nullptr,
+              std::vector<cplx> *Fk = nullptr, std::vector<cplx> *Ftk = nullptr) {
     // only ||c_j||^2, ||c~_j||^2 and C~^*C are needed (Q13 scaling + SVD)
     std::vector<ColDesc> X;
     for (int c = 0; c < kin; ++c) X.push_back(col(C, c, kin));
@@ -770,6 +782,10 @@ struct Solver {
         Fu[(size_t)kk[a] * pk + c] = Nr[(size_t)c * m + a] / nc[kk[a]];
         Fut[(size_t)kk[a] * pk + c] = Ml[(size_t)c * m + a] / nct[kk[a]];
       }
+    if (Fk) {   // the column maps, for the §4.4 recurrences (U_out = U Fu)
+      *Fk = Fu;
+      *Ftk = Fut;
+    }
     if (Fu_out) {
       *Fu_out = Fu;
       *Fut_out = Fut;
@@ -1212,6 +1228,9 @@ struct Solver {
     std::vector<cplx> P, Q;
     int mp = 0;
     double teig0 = 0;
+    FastState nf;                        // this cycle's blocks for cycle j+1 (§4.4)
+    std::vector<cplx> Fk, Ftk;           // biorth's column maps
+    const bool keep_fast = o.pencil == 1;
     if (!haveC && !havePrev) {
       // first system, no recycle data: eigenvectors of T_j
       mp = s;
@@ -1226,6 +1245,20 @@ struct Solver {
         PhitCols.push_back(rtcol(cols[bb] - 1));
       }
       mphi = s;
+      if (keep_fast) {   // AV_j = Υ_jΓ_j, Ῡ_j^*Υ_j = I, Ῡ_j^*V_j = I with zero rows
+        nf.m = nr;
+        nf.mphi = s;
+        nf.rows = rows;
+        nf.G1.assign((size_t)nr * nr, 0.0);
+        nf.G2.assign((size_t)nr * s, 0.0);
+        for (int a = 0; a < nr; ++a) {
+          nf.G1[(size_t)a * nr + a] = 1.0;
+          for (int bb = 0; bb < s; ++bb)
+            if (rows[a] == cols[bb]) nf.G2[(size_t)a * s + bb] = 1.0;
+        }
+        nf.H = Gam;
+        nf.Ht = Gamt;
+      }
     } else {
       // B_j = Ĉ^*AV_j, B~_j = Č^*A^*Ṽ_j from the stored ζ (exact identity, R4)
       std::vector<cplx> B((size_t)kc * s), Bt((size_t)kc * s);
@@ -1242,6 +1275,15 @@ struct Solver {
           Bt[(size_t)q * s + bb] = ztm * rn(m - 1) / std::conj(rh(m - 1));
         }
       }
+      const bool fastp = o.pencil == 1;
+      const int offU = kc + kp;
+      const int mpsi = kc + kp + nr;
+      // Φ = [X0, V]: X0 = U_{j-1} (havePrev) else U (later system, cycle 1)
+      const T *X0 = havePrev ? prev->U : cur.U;
+      const T *X0t = havePrev ? prev->Ut : cur.Ut;
+      const int kx = havePrev ? kp : kc;
+      std::vector<cplx> G1((size_t)mpsi * mpsi, 0.0), G2((size_t)mpsi * (kx + s), 0.0);
+      if (!fastp) {
       // columns of Ψ~ (X) and [Ψ, X0] (Y) -- raw residual columns, scalings on host
       std::vector<ColDesc> X, Y;
       std::vector<cplx> sx, sy;
@@ -1266,18 +1308,12 @@ struct Solver {
           sy.push_back(1.0);
         }
       }
-      const int offU = (int)X.size();
       for (int a = 0; a < nr; ++a) {
         X.push_back(rtcol(rows[a] - 1));
         Y.push_back(rcol(rows[a] - 1));
         sx.push_back(svt(rows[a]));
         sy.push_back(sv(rows[a]));
       }
-      const int mpsi = (int)X.size();
-      // Φ = [X0, V]: X0 = U_{j-1} (havePrev) else U (later system, cycle 1)
-      const T *X0 = havePrev ? prev->U : cur.U;
-      const T *X0t = havePrev ? prev->Ut : cur.Ut;
-      const int kx = havePrev ? kp : kc;
       for (int c = 0; c < kx; ++c) {
         Y.push_back(col(X0, c, kx));
         sy.push_back(1.0);
@@ -1289,7 +1325,6 @@ struct Solver {
       }
       sum_host(dist ? ctx->comm_side.get() : nullptr, Graw);   // C-4
       const int mY = (int)Y.size();
-      std::vector<cplx> G1((size_t)mpsi * mpsi), G2((size_t)mpsi * (kx + s));
       for (int a = 0; a < mpsi; ++a) {
         for (int bb = 0; bb < mpsi; ++bb)
           G1[(size_t)a * mpsi + bb] = std::conj(sx[a]) * Graw[(size_t)a * mY + bb] * sy[bb];
@@ -1298,6 +1333,76 @@ struct Solver {
         for (int bb = 0; bb < s; ++bb) {
           const int yc = offU + top + bb;
           G2[(size_t)a * (kx + s) + kx + bb] = std::conj(sx[a]) * Graw[(size_t)a * mY + yc] * sy[yc];
+        }
+      }
+      } else {
+        // §4.4: the blocks from cycle j-1's small matrices and the
+        // exact relations; the O(n) work is ONE Gram, Ῡ_j^*X0, plus
+        // C~^*U in the first cycle of a later system (its Y is the
+        // same X0 = U).  Oracle: oracle.rbicg.fast_grams (same block formulas).
+        const int m2 = kx + s;
+        const bool need_ctu = haveC && !havePrev && ctu.empty();
+        std::vector<ColDesc> X, Y;
+        if (need_ctu)
+          for (int c = 0; c < kc; ++c) X.push_back(col(cur.Ct, c, kc));
+        for (int a = 0; a < nr; ++a) X.push_back(rtcol(rows[a] - 1));
+        for (int c = 0; c < kx; ++c) Y.push_back(col(X0, c, kx));
+        std::vector<cplx> Graw;
+        {
+          Phase ph("cycle.gram_fast", cs);
+          gram<T>(X, Y, n, Graw, ctx, cs);
+        }
+        sum_host(dist ? ctx->comm_side.get() : nullptr, Graw);   // C-4
+        const int x0r = need_ctu ? kc : 0;
+        if (need_ctu) ctu.assign(Graw.begin(), Graw.begin() + (size_t)kc * kx);
+        auto E = [&](int ra, int rb) { return ra == rb ? cplx(1.0) : cplx(0.0); };   // ṽ_a^*v_b
+        for (int q = 0; q < kc; ++q) G1[(size_t)q * mpsi + q] = cur.d[q];             // D_c
+        for (int a = 0; a < nr; ++a) G1[(size_t)(offU + a) * mpsi + offU + a] = 1.0;  // Ῡ^*Υ = I
+        if (havePrev) {
+          const FastState &ps = fst;
+          RB_CHECK(ps.valid && ps.pk == kp && ps.kc == kc, RBICG_ESTATE);
+          const int pm = ps.m, pU0 = ps.kc + ps.kp, pnr = (int)ps.rows.size();
+          auto HF = matmul(ps.H, ps.F, pm, ps.mphi, kp);     // C_{j-1} = Ψ_{j-1}(HF)
+          auto HFtA = adjoint(matmul(ps.Ht, ps.Ft, pm, ps.mphi, kp), pm, kp);
+          auto G2F = matmul(ps.G2, ps.F, pm, ps.mphi, kp);   // Ψ~_{j-1}^*U_{j-1}
+          for (int q = 0; q < kc; ++q)
+            for (int c = 0; c < kp; ++c) {
+              cplx a1 = 0.0, a2 = 0.0;
+              for (int t = 0; t < pm; ++t) {
+                a1 += ps.G1[(size_t)q * pm + t] * HF[(size_t)t * kp + c];      // C~^*C_{j-1}
+                a2 += HFtA[(size_t)c * pm + t] * ps.G1[(size_t)t * pm + q];    // C~_{j-1}^*C
+              }
+              G1[(size_t)q * mpsi + kc + c] = a1;
+              G1[(size_t)(kc + c) * mpsi + q] = a2;
+              G2[(size_t)q * m2 + c] = G2F[(size_t)q * kp + c];                // C~^*U_{j-1}
+            }
+          for (int c = 0; c < kp; ++c) G1[(size_t)(kc + c) * mpsi + kc + c] = prev->d[c];   // Σ_{j-1}
+          for (int c = 0; c < kp; ++c)
+            for (int b = 0; b < nr; ++b) {
+              cplx a1 = 0.0, a2 = 0.0;
+              for (int a = 0; a < pnr; ++a) {
+                const cplx e1 = E(ps.rows[a], rows[b]), e2 = E(rows[b], ps.rows[a]);
+                if (e1 != cplx(0.0)) a1 += HFtA[(size_t)c * pm + pU0 + a] * e1;   // C~_{j-1}^*Υ_j
+                if (e2 != cplx(0.0)) a2 += e2 * HF[(size_t)(pU0 + a) * kp + c];   // Ῡ_j^*C_{j-1}
+              }
+              G1[(size_t)(kc + c) * mpsi + offU + b] = a1;
+              G1[(size_t)(offU + b) * mpsi + kc + c] = a2;
+            }
+          auto CC = matmul(HFtA, G2F, kp, pm, kp);            // C~_{j-1}^*U_{j-1}
+          for (int c = 0; c < kp; ++c) {
+            for (int c2 = 0; c2 < kp; ++c2) G2[(size_t)(kc + c) * m2 + c2] = CC[(size_t)c * kp + c2];
+            for (int bb = 0; bb < s; ++bb)                     // C~_{j-1}^*V_j
+              G2[(size_t)(kc + c) * m2 + kx + bb] = G1[(size_t)(kc + c) * mpsi + offU + top + bb];
+          }
+        } else if (haveC) {
+          for (int q = 0; q < kc; ++q)
+            for (int c = 0; c < kx; ++c) G2[(size_t)q * m2 + c] = ctu[(size_t)q * kx + c];   // C~^*U
+        }
+        for (int a = 0; a < nr; ++a) {
+          const cplx sc = std::conj(svt(rows[a]));
+          for (int c = 0; c < kx; ++c)                           // Ῡ_j^*X0
+            G2[(size_t)(offU + a) * m2 + c] = sc * Graw[(size_t)(x0r + a) * kx + c];
+          for (int bb = 0; bb < s; ++bb) G2[(size_t)(offU + a) * m2 + kx + bb] = E(rows[a], cols[bb]);
         }
       }
       // H, H~ per case
@@ -1336,6 +1441,17 @@ struct Solver {
       P = matmul(matmul(HtH, G1, mphi, mpsi, mpsi), H, mphi, mpsi, mphi);
       Q = matmul(HtH, G2, mphi, mpsi, mphi);
       mp = mphi;
+      if (keep_fast) {
+        nf.kc = kc;
+        nf.kp = kp;
+        nf.m = mpsi;
+        nf.mphi = mphi;
+        nf.rows = rows;
+        nf.G1 = G1;
+        nf.G2 = G2;
+        nf.H = H;
+        nf.Ht = Ht;
+      }
       for (int c = 0; c < kx; ++c) {
         PhiCols.push_back(col(X0, c, kx));
         PhitCols.push_back(col(X0t, c, kx));
@@ -1421,11 +1537,12 @@ struct Solver {
                   std::sqrt(dn / std::max(nn, 1e-300)));
         }
         if (!u_late || chk) {
-          biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false);
+          biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false, nullptr, nullptr,
+                 nullptr, &Fk, &Ftk);
         } else {
           std::vector<cplx> Fu, Fut;
           biorth(nullptr, nullptr, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false, &Fu, &Fut,
-                 gvf.empty() ? nullptr : &gvf);
+                 gvf.empty() ? nullptr : &gvf, &Fk, &Ftk);
           if (out.k > 0) {   // U_j N_p = [V_j rows] (W_j N_p) (scalings folded in Wrow)
             ensure_basis_u(out);
             const int pk = out.k;
@@ -1464,7 +1581,18 @@ struct Solver {
         launch_spmm<T>(M->A, tmp.U, tmp.C, ksel, cs);
         launch_spmm<T>(M->AH, tmp.Ut, tmp.Ct, ksel, cs);
       }
-      biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false);
+      biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false, nullptr, nullptr,
+             nullptr, &Fk, &Ftk);
+      }
+    }
+    if (keep_fast) {   // U_j = Φ_j (W_j Fu): F = W Fu w.r.t. the normalised Φ_j
+      fst = FastState();
+      if (ksel > 0 && out.k > 0) {
+        nf.pk = out.k;
+        nf.F = matmul(sel.W, Fk, mphi, ksel, out.k);
+        nf.Ft = matmul(sel.Wt, Ftk, mphi, ksel, out.k);
+        nf.valid = true;
+        fst = std::move(nf);
       }
     }
     if (fb > fa)   // no selection: the deferred flush alone

@@ -165,7 +165,7 @@ def _residual_bound_check(Ad, item, x, xt, ref):
 
 
 def _carry_from_oracle(ctx, cfg_k, cfg_s, tol, trunc, items, csr_of, max_itn,
-                       lam_slots=False, check_space=0.0):
+                       lam_slots=False, check_space=0.0, pencil="plain"):
     """Q27 protocol: every system is solved by both sides from the ORACLE's
     input recycle space; iterations within max(2, 3%), solutions 1e-7 at
     matched counts (re-running the oracle with force_iters = m_gpu when the
@@ -180,7 +180,7 @@ def _carry_from_oracle(ctx, cfg_k, cfg_s, tol, trunc, items, csr_of, max_itn,
         x0, xt0 = prev.get(item.get("slot", -1), (None, None))
         ref = R.solve_dual(Ad, item["b"], item["bt"], x0, xt0, U=U, Ut=Ut,
                            k=cfg_k, s=cfg_s, tol=tol, max_itn=max_itn,
-                           trunc_tol=trunc)
+                           trunc_tol=trunc, pencil=pencil)
         cplx = np.iscomplexobj(item["b"])
         rec = ctx.recycle(Ad.shape[0], max(cfg_k, 1), cplx)
         if U is not None and U.shape[1]:
@@ -188,7 +188,8 @@ def _carry_from_oracle(ctx, cfg_k, cfg_s, tol, trunc, items, csr_of, max_itn,
         M = ctx.matrix(item["indptr"], item["indices"], item["data"])
         x, xt, res, _ = ctx.solve_dual(M, item["b"], item["bt"], x0, xt0, R=rec,
                                        k=cfg_k, s=cfg_s, tol=tol,
-                                       max_itn=max_itn, trunc_tol=trunc)
+                                       max_itn=max_itn, trunc_tol=trunc,
+                                       pencil=pencil)
         its.append((res["iterations"], ref.iterations))
         assert res["status"] == ref.status, (res, ref.status)
         assert res["relres_true"] <= tol and res["relres_dual_true"] <= tol
@@ -269,20 +270,56 @@ def test_rbicg_matched_iterations(ctx):
         np.testing.assert_allclose(h[:, 2], np.real(ref.hist["alpha"]), rtol=1e-8)
 
 
-def test_c1_sequence_parity(ctx):
+@pytest.mark.parametrize("pencil", ["plain", "fast"])
+def test_c1_sequence_parity(ctx, pencil):
     cfg = CONFIGS["C1"]
     items = list(system_sequence(cfg))
     _carry_from_oracle(ctx, cfg.k, cfg.s, cfg.tol, cfg.trunc_tol, items,
                        lambda it: _csr((it["indptr"], it["indices"], it["data"])),
-                       cfg.max_itn)
+                       cfg.max_itn, pencil=pencil)
 
 
-def test_c4_small_complex_sequence(ctx):
+@pytest.mark.parametrize("pencil", ["plain", "fast"])
+def test_c4_small_complex_sequence(ctx, pencil):
     cfg = CONFIGS["C4"].scaled(12, systems=12, s=20)
     items = list(system_sequence(cfg, lam_r=0.0))
     _carry_from_oracle(ctx, cfg.k, cfg.s, cfg.tol, cfg.trunc_tol, items,
                        lambda it: _csr((it["indptr"], it["indices"], it["data"])),
-                       cfg.max_itn, lam_slots=True, check_space=0.9999)
+                       cfg.max_itn, lam_slots=True, check_space=0.9999, pencil=pencil)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_fast_pencil_output_space(ctx, cplx):
+    """§4.4 assembly (rbicg_opts.pencil = 1): the
+    pencil only decides the space handed to the next system, so the
+    check is on that space.  A later system run for m iterations (Q27) over
+    three cycles -- the first cycle of a later system, then two general-case
+    cycles whose Grams come from the recurrences -- from the oracle's input
+    space: the exported U_j, Ũ_j span the oracle's (pencil="fast") to
+    principal-angle cosines >= 1 - 1e-8, and the iterates are unchanged."""
+    from oracle import rbicg as R
+    n, k, s, m = 250, 4, 10, 30
+    A, _, _ = deflation_matrix(n, k, seed=41, complex_=cplx)
+    Ad = sp.csr_matrix(A)
+    M = ctx.matrix(*dense_to_csr(A))
+    first = R.solve_dual(Ad, vec(n, 42, cplx), vec(n, 43, cplx), k=k, s=s, tol=1e-10,
+                         max_itn=1000, trunc_tol=1e-2)
+    U, Ut = first.basis_out.U, first.basis_out.Ut
+    assert U.shape[1] >= 2
+    b2, bt2 = vec(n, 44, cplx), vec(n, 45, cplx)
+    ref = R.solve_dual(Ad, b2, bt2, U=U, Ut=Ut, k=k, s=s, tol=1e-10, max_itn=1000,
+                       trunc_tol=1e-2, force_iters=m, pencil="fast", keep_pencils=True)
+    assert [(i["kc"] > 0, i["kp"] > 0) for i in ref.pencils][:2] == [(True, False), (True, True)]
+    rec = ctx.recycle(n, k, cplx)
+    rec.import_(U, Ut)
+    x, xt, res, _ = ctx.solve_dual(M, b2, bt2, R=rec, k=k, s=s, tol=1e-10, max_itn=1000,
+                                   trunc_tol=1e-2, force_iters=m, pencil="fast")
+    assert res["iterations"] == m and res["cycles"] == m // s
+    assert np.linalg.norm(x - ref.x) <= 1e-9 * np.linalg.norm(ref.x)
+    Ug, Utg = rec.export()
+    assert Ug.shape[1] == ref.basis_out.k > 0
+    assert _cosines(Ug, ref.basis_out.U).min() >= 1 - 1e-8
+    assert _cosines(Utg, ref.basis_out.Ut).min() >= 1 - 1e-8
 
 
 def test_gpu_own_chain_c4(ctx):
