@@ -86,7 +86,7 @@ def test_partitioned_spmv_pair(P, cplx):
 
 
 def _solve_group(P, t, b, bt, k, s, tol, max_itn, trunc, U=None, Ut=None, force=0,
-                 history=False):
+                 history=False, pencil="plain"):
     n = len(b)
 
     def fn(ctx, q):
@@ -97,7 +97,7 @@ def _solve_group(P, t, b, bt, k, s, tol, max_itn, trunc, U=None, Ut=None, force=
             rec.import_(U[r0:r1].copy(), Ut[r0:r1].copy())
         x, xt, res, h = ctx.solve_dual(M, b[r0:r1].copy(), bt[r0:r1].copy(), R=rec, k=k, s=s,
                                        tol=tol, max_itn=max_itn, trunc_tol=trunc,
-                                       force_iters=force, history=history)
+                                       force_iters=force, history=history, pencil=pencil)
         Uo, Uto = rec.export()
         return x, xt, res, h, Uo, Uto
 
@@ -130,6 +130,34 @@ def test_partitioned_bicg_matches_oracle(P):
     xr = ref.x if m == ref.iterations else R.solve_dual(
         Ad, it["b"], it["bt"], k=0, s=cfg.s, tol=cfg.tol, max_itn=cfg.max_itn, force_iters=m).x
     assert np.linalg.norm(x - xr) <= 1e-7 * np.linalg.norm(xr)
+
+
+@pytest.mark.parametrize("P,cplx", [(2, False), (3, True)])
+def test_partitioned_fast_pencil_output_space(P, cplx):
+    """§4.4 assembly (opts.pencil = 1) on the row partition: the one O(n)
+    Gram per cycle is a sum of the ranks' partial Grams and the carried blocks
+    are host state replicated on every rank; the exported space spans the
+    oracle's (pencil="fast") as on one GPU (test_fast_pencil_output_space)."""
+    from oracle import rbicg as R
+    n, k, s, m = 250, 4, 10, 30
+    A, _, _ = deflation_matrix(n, k, seed=41, complex_=cplx)
+    t = dense_to_csr(A)
+    Ad = sp.csr_matrix(A)
+    first = R.solve_dual(Ad, vec(n, 42, cplx), vec(n, 43, cplx), k=k, s=s, tol=1e-10,
+                         max_itn=1000, trunc_tol=1e-2)
+    U, Ut = first.basis_out.U, first.basis_out.Ut
+    b, bt = vec(n, 44, cplx), vec(n, 45, cplx)
+    ref = R.solve_dual(Ad, b, bt, U=U, Ut=Ut, k=k, s=s, tol=1e-10, max_itn=1000,
+                       trunc_tol=1e-2, force_iters=m, pencil="fast")
+    x, xt, res, _, Uo, Uto = _solve_group(P, t, b, bt, k, s, 1e-10, 1000, 1e-2, U, Ut,
+                                          force=m, pencil="fast")
+    assert res["iterations"] == m
+    assert np.linalg.norm(x - ref.x) <= 1e-7 * np.linalg.norm(ref.x)
+    assert Uo.shape[1] == ref.basis_out.k > 0
+    for X, Y in ((Uo, ref.basis_out.U), (Uto, ref.basis_out.Ut)):
+        Q1, _ = np.linalg.qr(X)
+        Q2, _ = np.linalg.qr(Y)
+        assert np.linalg.svd(Q1.conj().T @ Q2, compute_uv=False).min() >= 1 - 1e-8
 
 
 @pytest.mark.parametrize("P,cplx", [(2, False), (3, True)])
