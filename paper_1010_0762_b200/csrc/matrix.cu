@@ -242,7 +242,7 @@ static void build_t(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowpt
     if (!h) {
       csr_to_sell<T>(ctx, n, rowptr, col, valT, M->AH);
       share_cols(ctx, M);
-      make_dcols(ctx, M);
+      if (sizeof(T) == 8) make_dcols(ctx, M);
       RB_CUDA(cudaStreamSynchronize(st));
       ws_free(valT);
       return;
@@ -275,7 +275,7 @@ static void build_t(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowpt
   count_launch(3);
   csr_to_sell<T>(ctx, n, rowptrT, colT, valT, M->AH);
   share_cols(ctx, M);
-  make_dcols(ctx, M);
+  if (sizeof(T) == 8) make_dcols(ctx, M);   // int16 deltas: real data only (la.dcols)
   RB_CUDA(cudaStreamSynchronize(st));
   for (void *p : {(void *)rowidx, (void *)iota, (void *)keys_out, (void *)perm, (void *)cnt,
                   (void *)rowptrT, (void *)colT, (void *)valT, tmp})
