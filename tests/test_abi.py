@@ -38,3 +38,19 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_lib.Opts) == 4 * 3 + 4 + 8 * 2 + 8 + 4 * 4
     assert C.sizeof(_lib.Result) == 5 * 4 + 4 + 8 * 10 + 8
     assert C.sizeof(_lib.Dist) == 4 + 4 + 128 + 8 + 8 + 4 + 4
+
+
+def test_opts_field_order_matches_header():
+    """rbicg_opts fields in header order (include/rbicg.h), ending with
+    `pencil` (the §4.4 switch) at the last 4-byte slot."""
+    import re
+    import ctypes as C
+    from pathlib import Path
+    from paper_1010_0762_b200 import _lib
+    hdr = (Path(__file__).resolve().parents[1] / "include" / "rbicg.h").read_text()
+    body = hdr[:hdr.index("} rbicg_opts;")]
+    body = body[body.rindex("typedef struct {"):]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = re.findall(r"\b(?:int32_t|uint64_t|double)\s+(\w+);", body)
+    assert names == [f for f, _ in _lib.Opts._fields_]
+    assert _lib.Opts.pencil.offset == C.sizeof(_lib.Opts) - 4
