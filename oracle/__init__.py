@@ -15,8 +15,17 @@ Modules
   reading Q19).
 * ``sequence`` -- the system-to-system driver.
 
+Q26 (fixed reduction order): importing this package limits the BLAS thread
+pool to one thread (threadpoolctl), so every reduction (vdot, gemv^T, the
+Grams) runs in one fixed order whatever the core count, and the oracle is
+bitwise-reproducible on a given host.  SciPy's SpMV is single-threaded anyway.
+
 Every reading of an ambiguous passage is listed in
 DESIGN.md §3.  Pins: tests/test_oracle_*.py (all ``-m "not gpu"``).
 Parity unpinned: nothing in this package is unpinned except the paper's
 figure/table values that need unavailable data.
 """
+
+from threadpoolctl import threadpool_limits as _threadpool_limits
+
+_threadpool_limits(1)   # Q26: one fixed reduction order (see above)

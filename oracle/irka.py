@@ -101,7 +101,7 @@ def pick_space(pool, si, reuse_tol):
     return best
 
 
-def irka(A, b, c, shifts0, *, k=8, s=40, tol=1e-10, max_itn=20000, trunc_tol=1e-2,
+def irka(A, b, c, shifts0, *, k=8, s=40, tol=1e-10, max_itn=20000, trunc_tol=1e-6,
          shift_tol=1e-6, max_steps=30, recycle=True, strategy=1, reuse_tol=np.inf):
     """Algorithm 3 with E = I; A is the (sparse) state matrix of the model."""
     A = sp.csr_matrix(A, dtype=np.complex128)

@@ -64,7 +64,7 @@ def adjoint(A):
 # ----------------------------------------------------------------------------
 def biorthogonalize(A, AH, U, Ut, trunc_tol, return_maps=False):
     """C = AU, C~ = A^*Ũ; scale column pairs to unit norm (Q13); SVD
-    C~^*C = M Σ N^* (equationSVD, PAPER.md:691-694); keep σ_i >= trunc_tol σ_1;
+    C~^*C = M Σ N^* (equationSVD, PAPER.md:691-694); keep σ_i >= trunc_tol (absolute, P:694);
     U <- U N_p, Ũ <- Ũ M_p, C <- C N_p, C~ <- C~ M_p (equationForUC,
     PAPER.md:695-700); D_c = Σ_p.
 
@@ -286,7 +286,7 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
                s=40, tol=1e-8, max_itn=20000, trunc_tol=1e-6,
                xt_redraw=None, update_recycle=True, force_iters=None,
                keep_pencils=False, breakdown_tol=BREAKDOWN_EPS,
-               variant="standard", pencil="plain"):
+               variant="standard", pencil="plain", reproject=True):
     """Solve A x = b and A^* x~ = b~ with RBiCG (Algorithm 2)
     using the recycle space (U, Ũ) (may be None/empty: first system), and
     build the recycle space for the next system (§4).
@@ -302,6 +302,16 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
     stop test, ζ_c, the recycle-space update) is Algorithm 2's.  The
     second-kind breakdown test (σ_{i+1} = 0, Q3) is taken at the end of
     iteration i, before its cycle end.
+
+    reproject=True (reading Q32): keep the Petrov-Galerkin
+    condition r_i ⊥ C~, r~_i ⊥ C ((orth)) explicitly.  At the
+    start of iteration i, g_{i-1} = Ĉ^*r_{i-1}, g~_{i-1} = Č^*r~_{i-1} (zero in
+    exact arithmetic); the update becomes r_i = r_{i-1} - α_i q_i - C g_{i-1},
+    ζ_c += α_i ζ_i - g_{i-1} (so b - A(x_i - Uζ_c) = r_i still holds exactly,
+    C = AU), and the duals alike.  Without it the oblique component CĈ^*r --
+    left untouched by every later update because q_i ∈ null(Ĉ^*) -- keeps the
+    rounding injected while ||r|| is large (minusXR can inflate ||r_0|| by
+    1/σ_min) and the recursion stagnates at ≈ eps·max||r_i||/σ_min.
 
     variant="lookahead" (the fused single-kernel iteration of the
     GPU path when no recycle space is active): Algorithm 2 except that β_i is
@@ -407,6 +417,10 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
     while i < n_iter:
         i += 1
         # Step 5
+        reproj = reproject and kc and not pipe
+        if reproj:   # Q32: g_{i-1} = Ĉ^*r_{i-1}, g~_{i-1} = Č^*r~_{i-1}
+            g = Chat.conj().T @ r
+            gt = Ccheck.conj().T @ rt
         p = r + beta * p
         pt = rt + np.conj(beta) * pt
         if pipe:
@@ -442,6 +456,11 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
                 + alpha * alpha * inner(qt, q)
         r = r - alpha * q
         rt = rt - np.conj(alpha) * qt
+        if reproj:   # Q32: r_i ⊥ C~, r~_i ⊥ C ((orth))
+            r = r - basis.C @ g
+            rt = rt - basis.Ct @ gt
+            zc = zc - g
+            ztc = ztc - gt
         it = i
         rn, rtn = np.linalg.norm(r), np.linalg.norm(rt)
         L.alpha[i] = alpha

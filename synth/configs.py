@@ -40,7 +40,7 @@ class Config:
     s: int = 40
     tol: float = 1e-8
     max_itn: int = 20000
-    trunc_tol: float = 1e-2   # cosine threshold, DESIGN.md §3 (Q13)
+    trunc_tol: float = 1e-6   # PAPER.md:694, :1405 on unit-norm columns (Q13)
     complex: bool = False
 
     @property
