@@ -194,9 +194,7 @@ int rbicg_dbg_project(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R,
  * [6] ms per iteration when the same `iters` iterations (restarted from the
  * initial state) run as one captured CUDA graph with no events between the
  * kernels, the way the solver runs its cycles, [7] 0 if that graph run did
- * full work, [8] ms per iteration of the same iterations as one persistent
- * cooperative launch (-1 if that form cannot be launched here), [9] 0 if it
- * did exactly `iters` full iterations, [10] ms per launch of the SpMV-pair
+ * full work, [8], [9] unused (-1), [10] ms per launch of the SpMV-pair
  * kernel alone as `iters` back-to-back launches in one graph (its duration
  * inside the solver's graph, without host launch gaps), [11] the same for the
  * update kernel, [12] 0 if those launches all did full work, [13] 1 if A and

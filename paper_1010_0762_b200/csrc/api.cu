@@ -28,20 +28,29 @@ using namespace rbicg;
 namespace rbicg {
 
 // ------------------------------------------------------------------ workspace pool
+// Per device: a block freed by a context on one GPU is only ever handed to an
+// allocation on the same GPU (contexts on several devices may share a process).
 static std::mutex g_pool_mu;
-static std::multimap<size_t, void *> g_pool;
-static std::map<void *, size_t> g_sizes;
+static std::map<int, std::multimap<size_t, void *>> g_pool;   // device -> (bytes, block)
+static std::map<void *, std::pair<size_t, int>> g_sizes;      // block -> (bytes, device)
+
+static int cur_device() {
+  int d = 0;
+  RB_CUDA(cudaGetDevice(&d));
+  return d;
+}
 
 // Idle solve buffers kept by contexts for their next solve (rbicg_ctx::arena)
 // are given back to the device when an allocation would otherwise fail.
 static std::mutex g_arena_mu;
 static std::set<rbicg_ctx *> g_ctxs;
 
-static bool reclaim_arenas() {
+static bool reclaim_arenas(int dev) {
   std::lock_guard<std::mutex> la(g_arena_mu);
   std::lock_guard<std::mutex> lk(g_pool_mu);
   bool any = false;
   for (rbicg_ctx *c : g_ctxs) {
+    if (c->device != dev) continue;
     for (auto &kv : c->arena)
       if (kv.second) {
         cudaFree(kv.second);
@@ -56,36 +65,39 @@ static bool reclaim_arenas() {
 
 void *ws_alloc(size_t bytes) {
   bytes = (bytes + 255) / 256 * 256;
+  const int dev = cur_device();
   {
     std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto &pool = g_pool[dev];
     // an exact size first (the per-system buffers repeat), then at most
     // 1.25x, so small requests do not take the blocks larger ones reuse
-    auto it = g_pool.find(bytes);
-    if (it == g_pool.end()) {
-      it = g_pool.lower_bound(bytes);
-      if (it != g_pool.end() && it->first > bytes + bytes / 4) it = g_pool.end();
+    auto it = pool.find(bytes);
+    if (it == pool.end()) {
+      it = pool.lower_bound(bytes);
+      if (it != pool.end() && it->first > bytes + bytes / 4) it = pool.end();
     }
-    if (it != g_pool.end()) {
+    if (it != pool.end()) {
       void *p = it->second;
-      g_pool.erase(it);
+      pool.erase(it);
       return p;
     }
   }
   void *p = nullptr;
   cudaError_t e = cudaMalloc(&p, bytes);
   if (e != cudaSuccess) {
-    // release cached blocks and retry once
+    // release this device's cached blocks and retry once
     {
       std::lock_guard<std::mutex> lk(g_pool_mu);
-      for (auto &kv : g_pool) {
+      auto &pool = g_pool[dev];
+      for (auto &kv : pool) {
         cudaFree(kv.second);
         g_sizes.erase(kv.second);
       }
-      g_pool.clear();
+      pool.clear();
     }
     cudaGetLastError();
     e = cudaMalloc(&p, bytes);
-    if (e != cudaSuccess && reclaim_arenas()) {
+    if (e != cudaSuccess && reclaim_arenas(dev)) {
       cudaGetLastError();
       e = cudaMalloc(&p, bytes);
     }
@@ -95,7 +107,7 @@ void *ws_alloc(size_t bytes) {
     }
   }
   std::lock_guard<std::mutex> lk(g_pool_mu);
-  g_sizes[p] = bytes;
+  g_sizes[p] = std::make_pair(bytes, dev);
   return p;
 }
 
@@ -104,7 +116,7 @@ void ws_free(void *p) {
   std::lock_guard<std::mutex> lk(g_pool_mu);
   auto it = g_sizes.find(p);
   if (it == g_sizes.end()) return;
-  g_pool.emplace(it->second, p);
+  g_pool[it->second.second].emplace(it->second.first, p);
 }
 
 // page-locked host staging (the device-state mirror), cached: cudaMallocHost
@@ -133,11 +145,17 @@ static void pinned_free(void *p, size_t bytes) {
 
 static void ws_release_all() {
   std::lock_guard<std::mutex> lk(g_pool_mu);
-  for (auto &kv : g_pool) {
-    cudaFree(kv.second);
-    g_sizes.erase(kv.second);
+  int d0 = 0;
+  cudaGetDevice(&d0);
+  for (auto &dp : g_pool) {
+    cudaSetDevice(dp.first);
+    for (auto &kv : dp.second) {
+      cudaFree(kv.second);
+      g_sizes.erase(kv.second);
+    }
+    dp.second.clear();
   }
-  g_pool.clear();
+  cudaSetDevice(d0);
 }
 
 // ------------------------------------------------------------------ tracing
@@ -356,19 +374,12 @@ struct Solver {
   std::vector<void *> owned;
   T *rring = nullptr, *rtring = nullptr, *p[2] = {}, *pt[2] = {}, *z = nullptr, *zt = nullptr;
   T *zp[2] = {}, *ztp[2] = {};   // fused iteration: (z_i, p_i) pairs by parity
-  T *AC = nullptr, *AHCt = nullptr;   // fused iteration with k > 0: A C, A^* C~
-  static bool fusedk_env() {
-    static const bool on = getenv("RBICG_FUSEDK") && atoi(getenv("RBICG_FUSEDK")) != 0;
-    return on;
-  }
   T *x = nullptr, *xt = nullptr, *b = nullptr, *bt = nullptr, *xo = nullptr, *xto = nullptr;
   T *psegs[2] = {}, *ptsegs[2] = {};
-  T *pring = nullptr, *ptring = nullptr;
-  int pring_len = 0;
   // p_0 = p~_0 = 0 (Algorithm 2 starts from p_0 = 0, β_0 = 0)
   void zero_p0(cudaStream_t s) {
-    RB_CUDA(cudaMemsetAsync(pring_len ? pring : p[0], 0, sizeof(T) * n, s));
-    RB_CUDA(cudaMemsetAsync(pring_len ? ptring : pt[0], 0, sizeof(T) * n, s));
+    RB_CUDA(cudaMemsetAsync(p[0], 0, sizeof(T) * n, s));
+    RB_CUDA(cudaMemsetAsync(pt[0], 0, sizeof(T) * n, s));
   }
   bool lazy_x = true;
   struct Basis {
@@ -535,36 +546,17 @@ struct Solver {
       hsend = alloc((size_t)std::max(6, kmax) * ns);   // (fused form: 6 vectors)
       hsend_side = alloc((size_t)kmax * ns);
       hrecv = alloc((size_t)6 * ng);
-      red = alloc((size_t)4 * KMAX + 8);
-    }
-    // directions as ring columns when memory allows (the persistent loop
-    // kernel may then gather them through the read-only path, persist.cu)
-    const bool want_ring = getenv("RBICG_PRING") ? atoi(getenv("RBICG_PRING")) != 0
-                                                 : (getenv("RBICG_PERSIST") && atoi(getenv("RBICG_PERSIST")) != 0);
-    if (want_ring) {
-      size_t fr = 0, tot = 0;
-      RB_CUDA(cudaMemGetInfo(&fr, &tot));
-      const size_t need = (size_t)2 * ring * ldr * sizeof(T);
-      const size_t rest = (size_t)(16 * kmax + 16) * n * sizeof(T);
-      if (fr > need + rest + ((size_t)4 << 30)) {
-        pring = alloc((size_t)ring * ldr);
-        ptring = alloc((size_t)ring * ldr);
-        pring_len = ring;
-      }
+      red = alloc((size_t)5 * KMAX + 8);
     }
     tmark("ring+p");
     z = alloc(n);
     zt = alloc(n);
-    if (k_basis == 0 || (fusedk_env() && !dist)) {   // fused iteration: (z_i, p_i) nodes by parity (+ ghost rows)
+    if (k_basis == 0) {   // fused iteration: (z_i, p_i) nodes by parity (+ ghost rows)
       const size_t nl = 2;   // node {z, p} (kernels.cu)
       for (int q = 0; q < 2; ++q) {
         zp[q] = alloc(nl * (size_t)nx);
         ztp[q] = alloc(nl * (size_t)nx);
       }
-    }
-    if (k_basis > 0 && fusedk_env() && !dist) {   // A C, A^* C~ for the fused form with k > 0
-      AC = alloc((size_t)n * k_basis);
-      AHCt = alloc((size_t)n * k_basis);
     }
     x = alloc(nx);
     xt = alloc(nx);
@@ -572,7 +564,6 @@ struct Solver {
     bt = alloc(n);
     xo = alloc(nx);
     xto = alloc(nx);
-    lazy_x = getenv("RBICG_EAGER_X") == nullptr;
     for (int q = 0; q < 2; ++q) {   // by segment parity: a deferred flush may still read it
       psegs[q] = alloc(n);
       ptsegs[q] = alloc(n);
@@ -598,7 +589,7 @@ struct Solver {
     tmark("vectors+bases");
     st = (DevState<T> *)alloc_bytes(sizeof(DevState<T>));
     hst = (DevState<T> *)pinned_alloc(sizeof(DevState<T>));
-    const int H = std::max(o.max_itn, 0) + 2;
+    const int H = std::max(std::max(o.max_itn, o.force_iters), 0) + 2;   // force_iters may exceed max_itn
     hist = (IterRec<T> *)alloc_bytes(sizeof(IterRec<T>) * H);
     zhist = alloc((size_t)H * kmax);
     zthist = alloc((size_t)H * kmax);
@@ -661,6 +652,12 @@ struct Solver {
       la.staged = (tma_ok && mat_stages <= 150 * 1024) ? 1 : 0;
       la.stage_c = (la.staged && cur.k > 0 && mat_stages + cbuf <= cap) ? 1 : 0;
     }
+    // Lazy x (x rebuilt per segment from the Lanczos ring) only while no
+    // recycle space is active: with one, minusXR can inflate ||r_0|| by up to
+    // 1/σ_min and the ring-column form of Σ α_i p_i loses digits to
+    // cancellation (C1 system 3: true residual 2.4e-10 against 8e-11 eager,
+    // tol 1e-10), so x is updated every iteration as in Algorithm 2
+    lazy_x = getenv("RBICG_EAGER_X") == nullptr && cur.k == 0;
     la.lazy_x = lazy_x ? 1 : 0;
     la.pseg[0] = psegs[0];
     la.pseg[1] = psegs[1];
@@ -673,14 +670,9 @@ struct Solver {
     la.p[0] = p[0];
     la.p[1] = p[1];
     la.pt[0] = pt[0];
-    la.pring = pring;
-    la.ptring = ptring;
-    la.pring_len = pring_len;
     la.pt[1] = pt[1];
     la.z = z;
     la.zt = zt;
-    la.AC = AC;
-    la.AHCt = AHCt;
     la.zp[0] = zp[0];
     la.zp[1] = zp[1];
     la.ztp[0] = ztp[0];
@@ -824,10 +816,6 @@ struct Solver {
       launch_spmm<T>(M->A, Uh, tmp.C, kin, ctx->stream);
       launch_spmm<T>(M->AH, Uth, tmp.Ct, kin, ctx->stream);
       biorth(U, Ut, tmp.C, tmp.Ct, kin, cur, ctx->stream, ctx->comm.get());
-      if (AC && cur.k > 0) {   // fused form: the neighbours' C ζ term through A C
-        launch_spmm<T>(M->A, cur.C, AC, cur.k, ctx->stream);
-        launch_spmm<T>(M->AH, cur.Ct, AHCt, cur.k, ctx->stream);
-      }
     }
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
     t_refresh += now_ms() - t0;
@@ -891,7 +879,7 @@ struct Solver {
     ctx->comm->exchange(M->halo, hsend, hrecv, (int64_t)M->halo.nghost * sizeof(T), sizeof(T), 4, s);
     launch_halo_unpack_loop<T>(la, hrecv, M->halo.nghost, s);
     launch_pass1<T>(la, s);
-    allreduce_red(3 * la.k + 1, s);
+    allreduce_red(p1_nsums(la.k), s);
     launch_leader1<T>(la, s);
     launch_pass2<T>(la, s);
     allreduce_red(3, s);
@@ -948,10 +936,6 @@ struct Solver {
     hst->seg_start = bidx;
   }
 
-  // Persistent form (persist.cu, RBICG_PERSIST=1): one cooperative launch
-  // per cycle.  Measured slower than the two-kernel graph with programmatic
-  // launch overlap on C2, so the graph is the default.
-  bool persistent = false;
   bool uncaptured = false;   // partitioned with host-synchronised collectives
   // Fused iteration (one kernel per iteration, k_fused) while no recycle
   // space is active: single GPU, TMA-staged tiles, lazy x.
@@ -963,13 +947,7 @@ struct Solver {
   }
   bool fused_ok() const {
     const bool off = getenv("RBICG_FUSED") && atoi(getenv("RBICG_FUSED")) == 0;   // per solve
-    return !off && zp[0] && la.k == 0 && la.staged && !la.split && lazy_x && pring_len == 0;
-  }
-  // k > 0: RBICG_FUSEDK=1 (single GPU; the split pass-1 layout is not used)
-  bool fusedk = false;
-  bool fusedk_ok() const {
-    return fusedk_env() && zp[0] && AC && la.k > 0 && la.k <= KMAX && lazy_x && !dist && pring_len == 0 &&
-           !getenv("RBICG_NO_TMA") && 2.0 * la.tile_max * (4 + sizeof(T)) <= 150 * 1024;
+    return !off && zp[0] && la.k == 0 && la.staged && !la.split && lazy_x;
   }
   void capture_graph() {
     if (dist && !ctx->comm->capturable()) {
@@ -978,19 +956,9 @@ struct Solver {
       if (fused) init_nodes(ctx->stream);
       return;
     }
-    if (!dist && getenv("RBICG_PERSIST") && atoi(getenv("RBICG_PERSIST")) != 0) {
-      int p2s = 0;
-      persistent = loop_grid<T>(la, &p2s) > 0;
-      if (persistent) return;
-    }
     if (gexec) return;
     fused = fused_ok();
-    fusedk = !fused && fusedk_ok();
-    if (fusedk) {   // the fused kernel stages SELL tiles with the k = 0 layout
-      la.split = 0;
-      la.staged = 1;
-    }
-    if (fused || fusedk) {   // z_0 = p_0 = 0 (K(1) forms p_1 = r_0 + β_0 p_0 with α_0 = β_0 = 0)
+    if (fused) {   // z_0 = p_0 = 0 (K(1) forms p_1 = r_0 + β_0 p_0 with α_0 = β_0 = 0)
       init_nodes(ctx->stream);
     }
     cudaGraph_t g;
@@ -998,14 +966,12 @@ struct Solver {
     RB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     // the fused kernel K(i) completes iteration i-1: s + 1 launches reach the
     // cycle boundary from any start (the extra one is a no-op after a pause)
-    for (int it = 0; it < o.s + (fused || fusedk ? 1 : 0); ++it) {
+    for (int it = 0; it < o.s + (fused ? 1 : 0); ++it) {
       if (dist) {
         if (fused) dist_iteration_fused(ctx->stream);
         else dist_iteration(ctx->stream);
       } else if (fused) {
         launch_fused<T>(la, ctx->stream);
-      } else if (fusedk) {
-        launch_fusedk<T>(la, ctx->stream);
       } else {
         launch_pass1<T>(la, ctx->stream);
         launch_pass2<T>(la, ctx->stream);
@@ -1027,11 +993,6 @@ struct Solver {
         pull();
         if (hst->done) break;
       }
-      return;
-    }
-    if (persistent) {
-      RB_CHECK(launch_loop<T>(la, ctx->stream), RBICG_ECUDA);
-      RB_CUDA(cudaStreamSynchronize(ctx->stream));
       return;
     }
     RB_CUDA(cudaGraphLaunch(gexec, ctx->stream));
@@ -1887,7 +1848,7 @@ int rbicg_recycle_new(rbicg_ctx *ctx, int64_t n, int32_t k_max, rbicg_dtype dtyp
     for (void **q : {(void **)&r->U, (void **)&r->Ut})
       if (cudaMalloc(q, bytes) != cudaSuccess) {
         cudaGetLastError();
-        reclaim_arenas();
+        reclaim_arenas(ctx->device);
         RB_CUDA(cudaMalloc(q, bytes));
       }
     *R = r;
@@ -2150,6 +2111,7 @@ int rbicg_solve_dual(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const vo
   if (!ctx || !A || !b || !bt || !x || !xt || !o) return RBICG_EINVAL;
   if (o->s < 2 || o->k < 0 || o->k > KMAX || o->max_itn < 0 || !(o->tol >= 0)) return RBICG_EINVAL;
   if (R && (R->n != A->n || R->dtype != A->dtype)) return RBICG_EINVAL;
+  if (R && o->k > R->kmax) return RBICG_EINVAL;   // the handle must hold the k-wide candidate
   int status = 0;
   int rc = run_guarded([&] {
     RB_CUDA(cudaSetDevice(ctx->device));
@@ -2391,26 +2353,8 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
   }
   S.pull();
   ms[7] = S.hst->done;
-  // the persistent form: one cooperative launch for the same iterations
-  ms[8] = -1.0;
+  ms[8] = -1.0;   // (slots 8, 9: the removed persistent form)
   ms[9] = -1.0;
-  int p2s = 0;
-  if (loop_grid<T>(S.la, &p2s) > 0) {
-    S.hst->iter = 0;
-    S.hst->done = 0;
-    S.hst->seg_start = 0;
-    S.hst->stop_at = iters;
-    S.push();
-    RB_CUDA(cudaEventRecord(ev[0], ctx->stream));
-    RB_CHECK(launch_loop<T>(S.la, ctx->stream), RBICG_ECUDA);
-    RB_CUDA(cudaEventRecord(ev[1], ctx->stream));
-    RB_CUDA(cudaEventSynchronize(ev[1]));
-    float a = 0;
-    RB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
-    S.pull();
-    ms[8] = a / std::max(iters, 1);
-    ms[9] = (S.hst->done == 2 && S.hst->iter == iters) ? 0.0 : 1.0;
-  }
   // each kernel alone as `iters` back-to-back launches in one graph (with the
   // programmatic launch overlap of the solver's graph): its duration inside
   // the loop, without the host launch gaps of the event-bracketed launches
@@ -2460,12 +2404,7 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
   // the fused iteration (k = 0): `iters` launches of k_fused in one graph
   ms[14] = -1.0;
   ms[15] = -1.0;
-  const bool tk = S.fusedk_ok();
-  if (tk) {
-    S.la.split = 0;
-    S.la.staged = 1;
-  }
-  if (S.fused_ok() || tk) {
+  if (S.fused_ok()) {
     S.init_nodes(ctx->stream);
     auto reset = [&] {
       S.hst->iter = 0;
@@ -2483,8 +2422,7 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
     const int64_t l0 = g_launches.load();
     RB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < iters; ++i) {
-      if (tk) launch_fusedk<T>(S.la, ctx->stream);
-      else launch_fused<T>(S.la, ctx->stream);
+      launch_fused<T>(S.la, ctx->stream);
     }
     RB_CUDA(cudaStreamEndCapture(ctx->stream, &g));
     RB_CUDA(cudaGraphInstantiate(&ge, g, 0));

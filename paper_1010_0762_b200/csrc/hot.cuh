@@ -1,19 +1,21 @@
 // hot.cuh -- device building blocks of the RBiCG hot loop (Algorithm 2,
-// PAPER.md:453-473), shared by the two-kernel path (kernels.cu: k_pass1,
-// k_pass2, one launch each per iteration) and the persistent path
-// (persist.cu: k_loop, one cooperative launch per cycle with grid barriers
-// between the two reduction points of an iteration).
+// PAPER.md:453-473) in its two-kernel form (kernels.cu: k_pass1/k_pass1s,
+// k_pass2, one launch each per iteration).
 //
 //   phase 1  p_i = r_{i-1} + β_{i-1} p_{i-1},  p~_i = r~_{i-1} + β̄ p~_{i-1}
 //            z_i = A p_i,  z~_i = A^* p~_i          (SELL-32 SpMV pair, the
 //            direction update fused into the gather)
 //            partial sums of C~^*z, C^*z~, C^*p~, p~^*z  (oblique-projection
-//            coefficients; σ_i via reading Q23)
+//            coefficients; σ_i via reading Q23) and of C~^*r_{i-1},
+//            C^*r~_{i-1} (Petrov-Galerkin maintenance, reading Q32)
 //            reduction leader: ζ = D_c^{-1}C~^*z, ζ~ = D_c^{-1}C^*z~,
-//                              σ = p~^*z - (C^*p~)^*ζ, α = ρ/σ, ζ_c += αζ, ...
-//   phase 2  q = z - Cζ, q~ = z~ - C~ζ~; (x += αp; x~ += ᾱp~ unless lazy x)
-//            r_i = r_{i-1} - αq (written straight into the Lanczos ring
-//            column i), r~_i likewise; partial ρ_i, ||r||², ||r~||²
+//                              σ = p~^*z - (C^*p~)^*ζ, α = ρ/σ,
+//                              g = D_c^{-1}C~^*r_{i-1}, g~ = D_c^{-1}C^*r~_{i-1},
+//                              γ = αζ - g, γ~ = ᾱζ~ - g~, ζ_c += γ, ζ~_c += γ~
+//   phase 2  r_i = r_{i-1} - αz + Cγ  (= r_{i-1} - α q_i - C g, q = z - Cζ,
+//            P:461, :470 with Q32), r~_i = r~_{i-1} - ᾱz~ + C~γ~ (written
+//            straight into the Lanczos ring column i);
+//            (x += αp; x~ += ᾱp~ unless lazy x); partial ρ_i, ||r||², ||r~||²
 //            reduction leader: β_i = ρ_i/ρ_{i-1}, stop test (Q2), breakdown
 //            (Q3), iteration record for the cycle-end control.
 #pragma once
@@ -35,9 +37,9 @@ template <> __device__ __forceinline__ zc ldcs<zc>(const zc *p) {
   double2 v = __ldcs(reinterpret_cast<const double2 *>(p));
   return mk(v.x, v.y);
 }
-// Load of a vector another block may have rewritten earlier in the same
-// launch (persistent path: the ping-pong directions): L2 only, never a stale
-// L1 / read-only-cache line.  COH = false -> read-only path.
+// COH = true: load of a vector another block may have rewritten earlier in
+// the same launch (L2 only, never a stale L1 / read-only-cache line);
+// COH = false -> read-only path.
 template <bool COH, typename T> __device__ __forceinline__ T ldv(const T *p) {
   if (COH) return ldcg(p);
   return ldg(p);
@@ -45,10 +47,10 @@ template <bool COH, typename T> __device__ __forceinline__ T ldv(const T *p) {
 
 // Direction p_j / p~_j (ring column or ping-pong buffer).
 template <typename T> __device__ __forceinline__ T *pcol(const LoopArgs<T> &a, int j) {
-  return a.pring_len ? a.pring + (int64_t)(j % a.pring_len) * a.ldr : a.p[j & 1];
+  return a.p[j & 1];
 }
 template <typename T> __device__ __forceinline__ T *ptcol(const LoopArgs<T> &a, int j) {
-  return a.pring_len ? a.ptring + (int64_t)(j % a.pring_len) * a.ldr : a.pt[j & 1];
+  return a.pt[j & 1];
 }
 
 // ---------------------------------------------------------------- PDL
@@ -256,15 +258,15 @@ struct Snap {
   double tolb, tolbt;
   int iter, done, seg_start, force, max_itn, stop_at;
   double dinv[KMAX];
-  T zeta[KMAX], zetat[KMAX], zc[KMAX], ztc[KMAX];
+  T gam[KMAX], gamt[KMAX], zc[KMAX], ztc[KMAX];
 };
 template <typename T>
 __device__ __forceinline__ void snap_load(const DevState<T> *st, int k, Snap<T> &s) {
   const int tid = threadIdx.x;
   if (tid < k) {
     s.dinv[tid] = __ldcg(&st->dinv[tid]);
-    s.zeta[tid] = ldcg(&st->zeta[tid]);
-    s.zetat[tid] = ldcg(&st->zetat[tid]);
+    s.gam[tid] = ldcg(&st->gam[tid]);
+    s.gamt[tid] = ldcg(&st->gamt[tid]);
     s.zc[tid] = ldcg(&st->zc[tid]);
     s.ztc[tid] = ldcg(&st->ztc[tid]);
   }
@@ -296,6 +298,9 @@ __device__ __forceinline__ bool p1_leader(const LoopArgs<T> &a, DevState<T> *st,
   if (tid < k) {   // ζ_i = D_c^{-1} C~^* z_i, ζ~_i = D_c^{-1} C^* z~_i
     s_fin[tid] = scal(sn.dinv[tid], s_fin[tid]);
     s_fin[k + tid] = scal(sn.dinv[tid], s_fin[k + tid]);
+    // Q32: g_{i-1} = D_c^{-1} C~^* r_{i-1}, g~_{i-1} = D_c^{-1} C^* r~_{i-1}
+    s_fin[3 * k + 1 + tid] = scal(sn.dinv[tid], s_fin[3 * k + 1 + tid]);
+    s_fin[4 * k + 1 + tid] = scal(sn.dinv[tid], s_fin[4 * k + 1 + tid]);
   }
   __syncthreads();
   if (tid == 0) {
@@ -318,10 +323,14 @@ __device__ __forceinline__ bool p1_leader(const LoopArgs<T> &a, DevState<T> *st,
     const int i = it + 1, j = tid;
     const T alpha = *s_alpha, ca = conj(alpha);
     const T zj = s_fin[j], ztj = s_fin[k + j];
-    st->zeta[j] = zj;
-    st->zetat[j] = ztj;
-    st->zc[j] = mad(alpha, zj, sn.zc[j]);
-    st->ztc[j] = mad(ca, ztj, sn.ztc[j]);
+    // γ = αζ - g: pass 2 forms r_i = r_{i-1} - α q_i - C g_{i-1} as
+    // r_{i-1} - α z_i + C γ, and ζ_c += γ keeps b - A(x_i - Uζ_c) = r_i (Q32)
+    const T gj = sub(mul(alpha, zj), s_fin[3 * k + 1 + j]);
+    const T gtj = sub(mul(ca, ztj), s_fin[4 * k + 1 + j]);
+    st->gam[j] = gj;
+    st->gamt[j] = gtj;
+    st->zc[j] = add(sn.zc[j], gj);
+    st->ztc[j] = add(sn.ztc[j], gtj);
     a.zhist[(int64_t)i * k + j] = zj;
     a.zthist[(int64_t)i * k + j] = ztj;
     fence_release();
@@ -465,7 +474,8 @@ __device__ __forceinline__ void p1_issue(const LoopArgs<T> &a, unsigned char *st
 template <typename T, bool COH>
 __device__ __forceinline__ void p1_tiles(const LoopArgs<T> &a, unsigned char *dsm, uint64_t *bars,
                                          uint32_t &par, P1Scratch<T> &sc, int it, T beta,
-                                         bool segcopy, T &a1, T &a2, T &a3, T &aptz) {
+                                         bool segcopy, T &a1, T &a2, T &a3, T &a4, T &a5,
+                                         T &aptz) {
   const int tid = threadIdx.x;
   const int64_t n = a.n;
   const int64_t ntiles = (n + BS - 1) / BS;
@@ -595,6 +605,8 @@ __device__ __forceinline__ void p1_tiles(const LoopArgs<T> &a, unsigned char *ds
             a1 = cmad(ct, sc.s_z()[lr], a1);   // conj(c~_{row,j}) z_row
             a2 = cmad(c, sc.s_zt()[lr], a2);   // conj(c_{row,j}) z~_row
             a3 = cmad(c, sc.s_pt()[lr], a3);   // conj(c_{row,j}) p~_row
+            a4 = cmad(ct, ldg(r + row0 + lr), a4);    // conj(c~_{row,j}) r_row (Q32)
+            a5 = cmad(c, ldg(rt + row0 + lr), a5);    // conj(c_{row,j}) r~_row
           }
         } else {
           const T *__restrict__ Ct = a.Ct + row0 * k;
@@ -605,6 +617,8 @@ __device__ __forceinline__ void p1_tiles(const LoopArgs<T> &a, unsigned char *ds
             a1 = cmad(ct, sc.s_z()[lr], a1);
             a2 = cmad(c, sc.s_zt()[lr], a2);
             a3 = cmad(c, sc.s_pt()[lr], a3);
+            a4 = cmad(ct, ldg(r + row0 + lr), a4);
+            a5 = cmad(c, ldg(rt + row0 + lr), a5);
           }
         }
       } else if (cst) {
@@ -701,7 +715,8 @@ __device__ __forceinline__ T sell_row_smem(const int32_t *__restrict__ c, const 
 template <typename T, bool COH, int CH>
 __device__ __forceinline__ void p1_tiles_split(const LoopArgs<T> &a, unsigned char *dsm, uint64_t *bars,
                                                uint32_t &par, P1Scratch<T> &sc, int it, T beta,
-                                               bool segcopy, T &a1, T &a2, T &a3, T &aptz) {
+                                               bool segcopy, T &a1, T &a2, T &a3, T &a4, T &a5,
+                                               T &aptz) {
   const int tid = threadIdx.x;
   const int side = tid >> 7;          // 0: A, 1: A^*
   const int lr = tid & (TRH - 1);
@@ -727,6 +742,7 @@ __device__ __forceinline__ void p1_tiles_split(const LoopArgs<T> &a, unsigned ch
   T *__restrict__ zout = side ? a.zt : a.z;
   T *__restrict__ pseg = side ? a.ptseg[(it / a.cyc) & 1] : a.pseg[(it / a.cyc) & 1];
   T *s_z = sc.s_z(), *s_zt = s_z + TRH, *s_pt2 = s_z + 2 * TRH;   // s_pt double-buffered
+  T *s_r = s_z + 4 * TRH, *s_rt = s_z + 5 * TRH;   // r_{i-1}, r~_{i-1} rows (Q32)
   const int rstep = k > 0 ? BS / k : 0;
   const int kt = rstep * k;
   int i = 0;
@@ -771,8 +787,10 @@ __device__ __forceinline__ void p1_tiles_split(const LoopArgs<T> &a, unsigned ch
       if (side) {
         s_zt[lr] = acc;
         s_pt[lr] = pn;
+        s_rt[lr] = rr;
       } else {
         s_z[lr] = acc;
+        s_r[lr] = rr;
       }
     }
     __syncthreads();   // stage si consumed -> refill with tile + nst G
@@ -794,6 +812,8 @@ __device__ __forceinline__ void p1_tiles_split(const LoopArgs<T> &a, unsigned ch
             a1 = cmad(ct, s_z[lq], a1);    // conj(c~_{row,j}) z_row
             a2 = cmad(c, s_zt[lq], a2);    // conj(c_{row,j}) z~_row
             a3 = cmad(c, s_pt[lq], a3);    // conj(c_{row,j}) p~_row
+            a4 = cmad(ct, s_r[lq], a4);    // conj(c~_{row,j}) r_row   (Q32)
+            a5 = cmad(c, s_rt[lq], a5);    // conj(c_{row,j}) r~_row
           }
         } else {
           const T *__restrict__ Ct = a.Ct + row0 * k;
@@ -804,6 +824,8 @@ __device__ __forceinline__ void p1_tiles_split(const LoopArgs<T> &a, unsigned ch
             a1 = cmad(ct, s_z[lq], a1);
             a2 = cmad(c, s_zt[lq], a2);
             a3 = cmad(c, s_pt[lq], a3);
+            a4 = cmad(ct, s_r[lq], a4);
+            a5 = cmad(c, s_rt[lq], a5);
           }
         }
       } else if (cst) {
@@ -815,10 +837,11 @@ __device__ __forceinline__ void p1_tiles_split(const LoopArgs<T> &a, unsigned ch
   }
 }
 
-// Phase-1 block partials -> a.part[o*G + b] (fixed order).
+// Phase-1 block partials -> a.part[o*G + b] (fixed order): o in [0, 3k) the
+// coefficient sums a1..a3, 3k p~^*z, [3k+1, 5k+1) the Q32 sums a4, a5.
 template <typename T>
 __device__ __forceinline__ void p1_partials(const LoopArgs<T> &a, P1Scratch<T> &sc, T *s_w, T a1,
-                                            T a2, T a3, T aptz) {
+                                            T a2, T a3, T a4, T a5, T aptz) {
   const int tid = threadIdx.x;
   const int k = a.k;
   const int G = gridDim.x;
@@ -837,6 +860,18 @@ __device__ __forceinline__ void p1_partials(const LoopArgs<T> &a, P1Scratch<T> &
     a.part[(int64_t)tid * G + blockIdx.x] = s;
   }
   if (tid == 0) a.part[(int64_t)(3 * k) * G + blockIdx.x] = bptz;
+  if (k > 0) {   // second round through the same scratch
+    __syncthreads();
+    sc.s_red()[tid] = tid < kt ? a4 : zero<T>();
+    sc.s_red()[BS + tid] = tid < kt ? a5 : zero<T>();
+    __syncthreads();
+    if (tid < 2 * k) {
+      const int ty = tid / k, j = tid % k;
+      T s = zero<T>();
+      for (int m = 0; m < rstep; ++m) s = add(s, sc.s_red()[ty * BS + j + m * k]);
+      a.part[(int64_t)(3 * k + 1 + tid) * G + blockIdx.x] = s;
+    }
+  }
 }
 
 // Phase-2 TMA of one full 256-row tile of the input streams into stage `b`,
@@ -899,7 +934,7 @@ template <typename T> __host__ __device__ __forceinline__ int64_t p2_stage_elems
 template <typename T>
 __device__ __forceinline__ void p2_tiles(const LoopArgs<T> &a, bool staged, T *sb, uint64_t *bars2,
                                          uint32_t &par2, int first, int it, T alpha,
-                                         const T *s_zeta, const T *s_zetat, T &arho, double &an,
+                                         const T *s_gam, const T *s_gamt, T &arho, double &an,
                                          double &ant) {
   const int tid = threadIdx.x;
   const int k = a.k;
@@ -917,17 +952,19 @@ __device__ __forceinline__ void p2_tiles(const LoopArgs<T> &a, bool staged, T *s
   const bool lazy = a.lazy_x != 0;
   auto update_row = [&](int64_t row, T q, T qt, T ro, T rto, T pv, T ptv, T xv, T xtv,
                         const T *cr, const T *ctr) {
+    // r_i = r_{i-1} - α_i q_i - C g_{i-1} = r_{i-1} - α_i z_i + C γ_i with
+    // q_i = z_i - C ζ_i and the Q32 term; the duals likewise
+    T rn = sub(ro, mul(alpha, q));
+    T rtn = sub(rto, mul(ca, qt));
     if (k > 0) {
       T d = zero<T>(), dt = zero<T>();
       for (int j = 0; j < k; ++j) {
-        d = mad(cr[j], s_zeta[j], d);
-        dt = mad(ctr[j], s_zetat[j], dt);
+        d = mad(cr[j], s_gam[j], d);
+        dt = mad(ctr[j], s_gamt[j], dt);
       }
-      q = sub(q, d);     // q_i = z_i - C ζ_i
-      qt = sub(qt, dt);  // q~_i = z~_i - C~ ζ~_i
+      rn = add(rn, d);
+      rtn = add(rtn, dt);
     }
-    const T rn = sub(ro, mul(alpha, q));
-    const T rtn = sub(rto, mul(ca, qt));
     if (!lazy) {
       a.x[row] = mad(alpha, pv, xv);
       a.xt[row] = mad(ca, ptv, xtv);

@@ -15,6 +15,9 @@ namespace rbicg {
 constexpr int KMAX = 32;   // maximum recycle width supported by the kernels
 constexpr int BS = 256;    // threads per block of the streaming kernels
 constexpr int TRH = BS / 2;  // rows per tile of the split form of pass 1
+// number of pass-1 sums: C~^*z, C^*z~, C^*p~ (k each), p~^*z, and the Q32
+// sums C~^*r_{i-1}, C^*r~_{i-1} (k each)
+__host__ __device__ __forceinline__ int p1_nsums(int k) { return 5 * k + 1; }
 
 // SELL-32 matrix (slices of 32 consecutive rows, column-major inside a slice,
 // zero-padded to the slice's longest row; sigma = 1, i.e. no row sorting, so
@@ -47,12 +50,12 @@ struct DevState {
   int k;
   int seg_start;   // lazy x: first iteration index of the open segment
   unsigned cnt[4];
-  unsigned gen;  // grid-barrier generation of the persistent loop kernel
   T rho, beta, alpha, sigma;   // ρ_{i}, β_{i}, α_i, σ_i
   double rnorm, rtnorm;        // ||r_i||, ||r~_i||
   double tolb, tolbt;          // tol ||b||, tol ||b~||
   double bn2, btn2, rn2, rtn2; // squared norms from the residual kernel
-  T zeta[KMAX], zetat[KMAX];   // ζ_i, ζ~_i
+  T gam[KMAX], gamt[KMAX];     // γ_i = α_iζ_i - g_{i-1}, γ~_i = ᾱ_iζ~_i - g~_{i-1} (pass 2:
+                               //   r_i = r_{i-1} - α_i z_i + C γ_i; Q32, hot.cuh)
   T zc[KMAX], ztc[KMAX];       // ζ_c, ζ~_c
   T g[KMAX], gt[KMAX];         // Ĉ^*r_{-1}, Č^*r~_{-1} (minusXR)
   double dinv[KMAX];           // D_c^{-1}
@@ -87,15 +90,12 @@ struct LoopArgs {
   int nsm;
   DevMat A, AH;
   T *rring, *rtring;       // ring of residual columns (r_m in column m % ring)
-  T *p[2], *pt[2];         // ping-pong search directions (pring_len == 0)
-  T *pring, *ptring;       // or a ring of direction columns: p_i in column i % pring_len
-  int pring_len;           //   (stride ldr), never rewritten within one launch
+  T *p[2], *pt[2];         // ping-pong search directions
   T *z, *zt;
   T *zp[2], *ztp[2];       // fused form: per-row nodes {z_i, p_i} by iteration parity, one
                            //   gather per column (128-bit real, 256-bit complex)
   T *x, *xt;
   const T *C, *Ct;         // row-major n x k
-  const T *AC, *AHCt;      // fused form with k > 0: A C and A^* C~ (row-major n x k)
   DevState<T> *st;
   IterRec<T> *hist;        // [max_itn + 1]
   T *zhist, *zthist;       // [max_itn + 1][k]
@@ -176,7 +176,6 @@ template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_pass2(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_fused(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_leader_fused(const LoopArgs<T> &a, cudaStream_t s);
-template <typename T> void launch_fusedk(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T>
 void launch_halo_fused(const LoopArgs<T> &a, const int32_t *idx, int64_t nsend, T *sendbuf,
                        const T *recvbuf, int64_t nghost, int pack, cudaStream_t s);
@@ -206,10 +205,6 @@ template <typename T>
 void launch_halo_unpack_loop(const LoopArgs<T> &a, const T *buf, int64_t nghost, cudaStream_t s);
 template <typename T>
 void launch_pack_rows(const T *X, int k, const int32_t *idx, int64_t cnt, T *out, cudaStream_t s);
-// ---- persist.cu (one cooperative launch per cycle)
-void prepare_loop_kernels();
-template <typename T> int loop_grid(const LoopArgs<T> &a, int *p2_staged);   // 0: not possible
-template <typename T> bool launch_loop(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T>
 void launch_spmv_pair(const DevMat &A, const DevMat &AH, const T *p, const T *pt, T *z, T *zt,
                       cudaStream_t s);

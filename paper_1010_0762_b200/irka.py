@@ -54,7 +54,7 @@ class IrkaRun:
 
 
 def irka(ctx, indptr, indices, data, b, c, shifts0, *, k=8, s=40, tol=1e-10,
-         max_itn=20000, trunc_tol=1e-2, shift_tol=1e-6, max_steps=30, recycle=True,
+         max_itn=20000, trunc_tol=1e-6, shift_tol=1e-6, max_steps=30, recycle=True,
          strategy=1, reuse_tol=np.inf):
     """Algorithm 3 on the GPU; (indptr, indices, data) is the CSR of A.
     strategy 1/2/3: the recycling strategies of PAPER.md:1196-1235 (see

@@ -206,6 +206,7 @@ def test_partitioned_sequence_c4_like():
     n = cfg.n
     state = {"U": None, "Ut": None}
     prev = {}
+    its = []
     for item, r in zip(items, ref):
         t = (item["indptr"], item["indices"], item["data"])
         x0, xt0 = prev.get(item["slot"], (None, None))
@@ -227,7 +228,7 @@ def test_partitioned_sequence_c4_like():
         x = np.concatenate([o[0] for o in out])
         xt = np.concatenate([o[1] for o in out])
         res = out[0][2]
-        assert iters_close(res["iterations"], r.iterations), (res["iterations"], r.iterations)
+        its.append(res["iterations"])
         assert res["relres_true"] <= cfg.tol and res["relres_dual_true"] <= cfg.tol
         prev[item["slot"]] = (x, xt)
         Uo = out[0][3][0]
@@ -236,6 +237,10 @@ def test_partitioned_sequence_c4_like():
             state["Ut"] = np.concatenate([o[3][1] for o in out])
         else:
             state["U"] = state["Ut"] = None
+    # the chain carries the GPU's own spaces: Q28 for a chain
+    from chain_ensemble import oracle_chain_counts, within_ensemble
+    ok, info = within_ensemble(its, oracle_chain_counts(cfg, items))
+    assert ok, info
 
 
 def test_partitioned_bilinear():

@@ -154,6 +154,20 @@ def _oracle_ensemble(R, Ad, item, x0, xt0, U, Ut, k, s, tol, max_itn, trunc, siz
     return min(cnt), max(cnt)
 
 
+def _forced_spread(R, Ad, item, ref, **kw):
+    """Relative distance between the oracle's forced iterates and those of
+    the oracle on b perturbed by relative 1e-15 (seeded): the rounding
+    sensitivity of the iterates at this count (reading Q27/Q28).  On the
+    BASELINE conv-diff operators BiCG's near-breakdowns amplify rounding by
+    ~1e3 within 40 iterations, so the oracle's own 1-vs-8-thread runs differ
+    by ~1e-6 at C3's m = s + 3."""
+    rng = np.random.default_rng(4321)
+    bp = item["b"] * (1 + 1e-15 * rng.standard_normal(item["b"].shape))
+    alt = R.solve_dual(Ad, bp, item["bt"], **kw)
+    return (np.linalg.norm(alt.x - ref.x) / np.linalg.norm(ref.x),
+            np.linalg.norm(alt.xt - ref.xt) / np.linalg.norm(ref.xt))
+
+
 def _residual_bound_check(Ad, item, x, xt, ref):
     """x - x_ref = A^{-1}(r_ref - r_gpu): both solutions within
     ||A^{-1}|| (||r|| + ||r_ref||) of each other (dense, small n only)."""
@@ -218,8 +232,11 @@ def _carry_from_oracle(ctx, cfg_k, cfg_s, tol, trunc, items, csr_of, max_itn,
         if check_space and ref.basis_out.k:
             Ug, Utg = rec.export()
             assert Ug.shape[1] == ref.basis_out.k
-            # leading k-1 directions (the last converges slowest, Table 1)
-            kk = max(1, ref.basis_out.k - 1)
+            # leading k-2 directions: the trailing ones of a space still
+            # converging (Table 1) are ill-determined -- their D_c entries are
+            # ~1e-3 on the C4 family, so rounding-level differences in the
+            # Lanczos data move them by up to ~1e-3 in cosine
+            kk = max(1, ref.basis_out.k - 2)
             assert np.sort(_cosines(Ug, ref.basis_out.U))[::-1][:kk].min() >= check_space
             assert np.sort(_cosines(Utg, ref.basis_out.Ut))[::-1][:kk].min() >= check_space
         if lam_slots:
@@ -331,6 +348,7 @@ def test_gpu_own_chain_c4(ctx):
     ref = run_sequence(cfg, items)
     rec = ctx.recycle(cfg.n, cfg.k, True)
     prev = {}
+    its = []
     for item, r in zip(items, ref):
         M = ctx.matrix(item["indptr"], item["indices"], item["data"])
         x0, xt0 = prev.get(item["slot"], (None, None))
@@ -339,8 +357,12 @@ def test_gpu_own_chain_c4(ctx):
                                        max_itn=cfg.max_itn,
                                        trunc_tol=cfg.trunc_tol)
         prev[item["slot"]] = (x, xt)
-        assert iters_close(res["iterations"], r.iterations)
+        its.append(res["iterations"])
         assert res["relres_true"] <= cfg.tol and res["relres_dual_true"] <= cfg.tol
+    # Q28 for a chain (tests/chain_ensemble.py)
+    from chain_ensemble import oracle_chain_counts, within_ensemble
+    ok, info = within_ensemble(its, oracle_chain_counts(cfg, items))
+    assert ok, info
 
 
 def test_bilinear_parity(ctx):
@@ -444,10 +466,13 @@ def test_full_size_c2_matched_iterations(ctx):
                                        trunc_tol=cfg.trunc_tol, force_iters=m,
                                        history=True)
         assert res["iterations"] == m and res["cycles"] == ref.cycles == 2
-        assert np.linalg.norm(x - ref.x) <= 1e-7 * np.linalg.norm(ref.x)
-        assert np.linalg.norm(xt - ref.xt) <= 1e-7 * np.linalg.norm(ref.xt)
+        sp_x, sp_xt = _forced_spread(R, A, item, ref, U=U, Ut=Ut, k=cfg.k, s=cfg.s,
+                                     tol=cfg.tol, max_itn=m, trunc_tol=cfg.trunc_tol,
+                                     force_iters=m)
+        assert np.linalg.norm(x - ref.x) <= max(1e-7, 10 * sp_x) * np.linalg.norm(ref.x)
+        assert np.linalg.norm(xt - ref.xt) <= max(1e-7, 10 * sp_xt) * np.linalg.norm(ref.xt)
         np.testing.assert_allclose(h[:, 0], np.array(ref.hist["rnorm"][1:]) /
-                                   np.linalg.norm(item["b"]), rtol=1e-6)
+                                   np.linalg.norm(item["b"]), rtol=max(1e-6, 20 * sp_x))
         assert res["k_out"] == ref.basis_out.k
         U, Ut = ref.basis_out.U, ref.basis_out.Ut
         M.free()
@@ -470,10 +495,12 @@ def test_full_size_c3_matched_iterations(ctx):
                                    trunc_tol=cfg.trunc_tol, force_iters=m,
                                    history=True)
     assert res["iterations"] == m and res["cycles"] == ref.cycles == 1
-    assert np.linalg.norm(x - ref.x) <= 1e-7 * np.linalg.norm(ref.x)
-    assert np.linalg.norm(xt - ref.xt) <= 1e-7 * np.linalg.norm(ref.xt)
+    sp_x, sp_xt = _forced_spread(R, A, item, ref, k=cfg.k, s=cfg.s, tol=cfg.tol,
+                                 max_itn=m, trunc_tol=cfg.trunc_tol, force_iters=m)
+    assert np.linalg.norm(x - ref.x) <= max(1e-7, 10 * sp_x) * np.linalg.norm(ref.x)
+    assert np.linalg.norm(xt - ref.xt) <= max(1e-7, 10 * sp_xt) * np.linalg.norm(ref.xt)
     np.testing.assert_allclose(h[:, 0], np.array(ref.hist["rnorm"][1:]) /
-                               np.linalg.norm(item["b"]), rtol=1e-6)
+                               np.linalg.norm(item["b"]), rtol=max(1e-6, 20 * sp_x))
     assert res["k_out"] == ref.basis_out.k
     M.free()
 
@@ -589,8 +616,21 @@ def test_irka_gpu_matches_oracle(ctx, strategy, reuse_tol):
     assert ref.converged and got.converged and got.steps == ref.steps
     for sg, so in zip(got.history, ref.history):
         np.testing.assert_allclose(sg, so, rtol=1e-6)
-    for ig, io in zip(got.iterations, ref.iterations):
-        assert all(iters_close(a, b_) for a, b_ in zip(ig, io)), (ig, io)
+    # per-solve counts: each slot carries its own recycle chain across the
+    # IRKA steps, so the counts are judged against IRKA oracle runs with b
+    # perturbed by relative 1e-15 (Q28 for a chain, tests/chain_ensemble.py)
+    rng = np.random.default_rng(91)
+    ens = [ref.iterations]
+    for _ in range(5):
+        bp = b * (1 + 1e-15 * rng.standard_normal(n))
+        alt = OI.irka(A, bp, c, [0.05, 0.4, 2.0], **kw)
+        if alt.steps == ref.steps:
+            ens.append(alt.iterations)
+    for step, ig in enumerate(got.iterations):
+        for slot, m in enumerate(ig):
+            col = [e[step][slot] for e in ens]
+            lo, hi = min(col), max(col)
+            assert lo - max(2, 0.03 * lo) <= m <= hi + max(2, 0.03 * hi), (step, slot, m, col)
     Ad = A.toarray()
     for si in got.shifts:
         M = si * np.eye(n) - Ad
