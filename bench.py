@@ -1,9 +1,13 @@
 #!/usr/bin/env python
 """RBiCG iterations/s on B200 (BASELINE.json metric) -- one JSON line.
 
-Workload (N=1): BASELINE.json configs[1] = C2, the 2-D upwind conv-diff
-sequence on a 1024^2 grid (n = 1,048,576, fp64, k = 10, s = 40, tol 1e-8,
-10 dual pairs; synthetic, seeded per SURVEY.md §8(d)).
+Workload (N=1, default): BASELINE.json configs[2] = C3, the 3-D conv-diff
+sequence on a 192^3 grid (n = 7,077,888, nnz = 49.3 M, fp64, k = 10, s = 40,
+tol 1e-8, 8 dual pairs; synthetic, seeded per SURVEY.md §8(d)) -- a config of
+the metric's 1/2/4/8-GPU set.  Under the recycle rule (Q13 at the
+paper's 1e-6, Q32) every system after the first starts with a recycle space,
+so the timed systems run the augmented iteration with its projections.
+--config C2|C4|C5 selects another config.
 
 A *step* is one dual-pair solve of the sequence through the C ABI
 (rbicg_matrix_csr from device CSR -> SELL-32 + conj-transpose build,
@@ -12,8 +16,16 @@ recycle updates, step 7, true residuals), carrying the recycle space from
 system to system.  value = iterations / device time of the K timed steps.
 
 Timing: W warm-up steps, then K steps bracketed by barrier + synchronize and
-CUDA events; max over ranks.  Per-iteration traffic (637 MB at C2) is larger
-than the 126 MB L2, so no explicit flush is needed ("inputs larger than L2").
+CUDA events; max over ranks.  Per-iteration traffic (C3: 1.7 GB with k = 1,
+4.1 GB with k = 10; C2: 0.2 GB) is larger than the 126 MB L2 except C2's
+(L2 hits of the vectors written by the previous launch are counted by ncu's
+DRAM bytes in `roofline.traffic`), so no explicit flush is needed.
+
+roofline: the dominant hot-loop kernel of the last timed system's matrix and
+recycle space, each kernel timed alone as back-to-back launches in a CUDA
+graph on the library stream; `traffic` = ncu DRAM bytes per launch of the
+same kernel, captured in-run by a subprocess after the timed region
+(scripts/kernel_traffic.py, same config and recycle width).
 
 --impl reference runs the CPU oracle (the only other allowed use of oracle/)
 on a bounded sample of the same workload.
@@ -23,6 +35,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import re
 import statistics
 import subprocess
 import sys
@@ -35,6 +48,7 @@ sys.path.insert(0, ROOT)
 import numpy as np
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+DEFAULT_CONFIG = "C3"
 FALLBACK_HBM = 6650.0
 
 
@@ -145,6 +159,57 @@ def alg_bytes_fused(cfg_n, nnz, w=8, shared_cols=False, dcols=False):
     return mat + 12 * cfg_n * w
 
 
+NCU_KERNELS = {"pass1": "k_pass1", "pass2": "k_pass2", "fused": "k_fused"}
+
+
+def ncu_traffic(cfg, k, dom):
+    """ncu DRAM bytes (read + write) per launch of the dominant kernel, from a
+    subprocess run of scripts/kernel_traffic.py on the same config and
+    recycle width (after the timed region; its times are never reported)."""
+    import csv
+    import io
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found"
+    name = NCU_KERNELS[dom]
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum",
+           "--kernel-name", f"regex:^{name}", "--launch-skip", "2", "--launch-count", "3",
+           "--csv", "--clock-control", "none", sys.executable,
+           os.path.join(ROOT, "scripts", "kernel_traffic.py"), cfg.name, str(k)]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    except Exception as e:   # noqa: BLE001
+        return None, f"ncu failed: {e}"
+    rows = [r for r in csv.reader(io.StringIO(out.stdout)) if len(r) > 10]
+    start = [i for i, r in enumerate(rows) if "Kernel Name" in r and "Metric Value" in r]
+    if not start:
+        return None, "ncu produced no rows (rc %d): %s" % (out.returncode, out.stderr[-200:])
+    rows = rows[start[0]:]
+    hdr = rows[0]
+    ik, im, iv, iid = (hdr.index("Kernel Name"), hdr.index("Metric Name"),
+                       hdr.index("Metric Value"), hdr.index("ID"))
+    per = {}
+    for r in rows[1:]:
+        if not re.search(rf"(^|[\s:]){name}s?<", r[ik]):
+            continue
+        v = float(r[iv].replace(",", ""))
+        per.setdefault(r[iid], 0.0)
+        per[r[iid]] += v
+    if not per:
+        return None, "no %s launches in the capture" % name
+    unit = "byte"
+    for r in rows[1:]:
+        if re.search(rf"(^|[\s:]){name}s?<", r[ik]):
+            unit = r[hdr.index("Metric Unit")]
+            break
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+    vals = [v * scale for v in per.values()]
+    return sum(vals) / len(vals), (f"ncu dram__bytes_read.sum + dram__bytes_write.sum, "
+                                   f"{name} (k = {k}), mean of {len(vals)} launches, "
+                                   f"scripts/kernel_traffic.py {cfg.name} {k}")
+
+
 def run_gpu(args, rank, world):
     import torch
     from paper_1010_0762_b200 import api
@@ -188,9 +253,21 @@ def run_gpu(args, rank, world):
 
     prev = {}   # C4 (Q7): previous sweep's solution of the same shift slot
 
+    # the roofline times the hot-loop kernels with the largest input space a
+    # timed system started from (copied device to device before that step,
+    # outside its events) -- the iteration the timed region mostly ran
+    snap = {"R": None, "k": 0}
+
     def one(i, timed):
         d = dsys[i] if dsys[i] is not None else upload(systems[i])
         slot = systems[i].get("slot")
+        if timed and not part:
+            kin = R.k
+            if kin > snap["k"]:
+                if snap["R"] is None:
+                    snap["R"] = ctx.recycle(r1 - r0, cfg.k, cfg.complex)
+                snap["R"].copy_from(R)
+                snap["k"] = kin
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         eb = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -246,46 +323,16 @@ def run_gpu(args, rank, world):
         iters = int(tsum[1]) // world if part else int(tsum[1])
 
     # ---- roofline of the dominant kernel: per-kernel CUDA events on the
-    # library stream, resident state of the last system, its recycle space
+    # library stream, resident state of the last system and the recycle space
+    # the sequence carries (the timed systems' own k)
     last = dsys[-1]
-    kctx, kR = ctx, R
+    kctx, kR = ctx, (snap["R"] if snap["R"] is not None else R)
     if part:   # the partitioned context has no timing hook: the kernels on one GPU
         kctx = api.Context(dev)
         kR = kctx.recycle(cfg.n, cfg.k, cfg.complex)
     A = kctx.matrix(last["indptr"], last["indices"], last["data"])
     kt = kctx.time_kernels(A, kR, k=cfg.k, s=cfg.s, iters=args.kernel_iters,
                            trunc_tol=cfg.trunc_tol)
-    # the same kernels with the projections active (k = cfg.k): the timed
-    # sequence ends with an empty recycle space (DESIGN §3 Q13 / §9), so the
-    # C~^*v / U y terms are probed on a seeded random space of cfg.k columns
-    probe = None
-    if cfg.k > 0 and not args.no_k_probe:
-        rng = np.random.default_rng(cfg.seed + 777)
-        shp = (cfg.n, cfg.k)
-        if cfg.complex:
-            Uq = rng.standard_normal(shp) + 1j * rng.standard_normal(shp)
-            Utq = rng.standard_normal(shp) + 1j * rng.standard_normal(shp)
-        else:
-            Uq, Utq = rng.standard_normal(shp), rng.standard_normal(shp)
-        Rq = kctx.recycle(cfg.n, cfg.k, cfg.complex)
-        Rq.import_(Uq, Utq)
-        del Uq, Utq
-        kq = kctx.time_kernels(A, Rq, k=cfg.k, s=cfg.s, iters=args.kernel_iters,
-                               trunc_tol=1e-300)
-        wq = 16 if cfg.complex else 8
-        q1, q2 = alg_bytes(cfg.n, cfg.nnz, kq["k"], wq, kq["lazy_x"], kq["shared_cols"])
-        okq = kq["graph_each_done_flag"] == 0 and kq["pass1_graph_ms"] > 0
-        m1 = kq["pass1_graph_ms"] if okq else kq["pass1_ms"]
-        m2 = kq["pass2_graph_ms"] if okq else kq["pass2_ms"]
-        pk, _ = hbm_peak()
-        probe = {"k_active": kq["k"], "pass1_ms": m1, "pass2_ms": m2,
-                 "pass1_GBps": q1 / (m1 * 1e-3) / 1e9, "pass2_GBps": q2 / (m2 * 1e-3) / 1e9,
-                 "loop_graph_iter_ms": kq["graph_iter_ms"],
-                 "iter_GBps": (q1 + q2) / (kq["graph_iter_ms"] * 1e-3) / 1e9,
-                 "iter_frac": (q1 + q2) / (kq["graph_iter_ms"] * 1e-3) / 1e9 / pk,
-                 "alg_bytes_per_iter": q1 + q2,
-                 "fused_k_ms": kq["fused_ms"] if kq["fused_ms"] > 0 else None,
-                 "space": "seeded N(0,1) U, U~ (%d columns), truncation off" % cfg.k}
     A.free()
     w = 16 if cfg.complex else 8
     p1, p2 = alg_bytes(cfg.n, cfg.nnz, kt["k"], w, kt["lazy_x"], kt["shared_cols"])
@@ -298,21 +345,49 @@ def run_gpu(args, rank, world):
     k1 = kt["pass1_graph_ms"] if ok else kt["pass1_ms"]
     k2 = kt["pass2_graph_ms"] if ok else kt["pass2_ms"]
     dom_bytes, dom_ms, dom = (p1, k1, "pass1") if k1 >= k2 else (p2, k2, "pass2")
-    # the solver's loop runs the fused iteration kernel while no recycle space
-    # is active (every timed system of C2, C3, C5): that kernel is the dominant one
+    # without a recycle space the solver's loop runs the fused iteration
+    # kernel: that kernel is then the dominant one
     fused = kt["k"] == 0 and kt["fused_ms"] > 0 and kt["fused_done_flag"] == 0
     pf = alg_bytes_fused(cfg.n, cfg.nnz, w, kt["shared_cols"], kt["dcols"])
     if fused:
         dom_bytes, dom_ms, dom = pf, kt["fused_ms"], "fused"
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
-    traffic = None   # ncu DRAM bytes per launch, recorded for the config it was captured on
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tj = json.load(f)
-        if tj.get("config", "C2") == cfg.name:
-            traffic = tj.get(dom)
-    except Exception:
-        pass
+    traffic, traffic_info = None, "skipped (--no-traffic)"
+    if not args.no_traffic and rank == 0:
+        try:
+            traffic, traffic_info = ncu_traffic(cfg, kt["k"], dom)
+        except Exception as e:   # noqa: BLE001  (a profiler problem never fails the bench)
+            traffic, traffic_info = None, f"ncu capture failed: {e!r}"
+
+    # C2-type workloads end without a recycle space: probe the k = cfg.k
+    # iteration on a seeded random space so its kernels are measured too
+    probe = None
+    if kt["k"] == 0 and cfg.k > 0 and not args.no_k_probe:
+        A = kctx.matrix(last["indptr"], last["indices"], last["data"])
+        rng = np.random.default_rng(cfg.seed + 777)
+        shp = (cfg.n, cfg.k)
+        if cfg.complex:
+            Uq = rng.standard_normal(shp) + 1j * rng.standard_normal(shp)
+            Utq = rng.standard_normal(shp) + 1j * rng.standard_normal(shp)
+        else:
+            Uq, Utq = rng.standard_normal(shp), rng.standard_normal(shp)
+        Rq = kctx.recycle(cfg.n, cfg.k, cfg.complex)
+        Rq.import_(Uq, Utq)
+        del Uq, Utq
+        kq = kctx.time_kernels(A, Rq, k=cfg.k, s=cfg.s, iters=args.kernel_iters,
+                               trunc_tol=1e-300)
+        q1, q2 = alg_bytes(cfg.n, cfg.nnz, kq["k"], w, kq["lazy_x"], kq["shared_cols"])
+        okq = kq["graph_each_done_flag"] == 0 and kq["pass1_graph_ms"] > 0
+        m1 = kq["pass1_graph_ms"] if okq else kq["pass1_ms"]
+        m2 = kq["pass2_graph_ms"] if okq else kq["pass2_ms"]
+        probe = {"k_active": kq["k"], "pass1_ms": m1, "pass2_ms": m2,
+                 "pass1_GBps": q1 / (m1 * 1e-3) / 1e9, "pass2_GBps": q2 / (m2 * 1e-3) / 1e9,
+                 "loop_graph_iter_ms": kq["graph_iter_ms"],
+                 "iter_GBps": (q1 + q2) / (kq["graph_iter_ms"] * 1e-3) / 1e9,
+                 "iter_frac": (q1 + q2) / (kq["graph_iter_ms"] * 1e-3) / 1e9 / peak,
+                 "alg_bytes_per_iter": q1 + q2,
+                 "space": "seeded N(0,1) U, U~ (%d columns), truncation off" % cfg.k}
+        A.free()
 
     # ---- e2e through the public API with HOST buffers (H2D/D2H in the call)
     e2e = None
@@ -401,7 +476,10 @@ def run_gpu(args, rank, world):
                      "k_active": kt["k"], "lazy_x": kt["lazy_x"], "shared_cols": kt["shared_cols"],
                      "int16_col_deltas": kt["dcols"],
                      "tma_pass1": kt["tma_pass1"],
+                     "traffic_source": traffic_info,
+                     "pass1_alg_bytes": p1, "pass2_alg_bytes": p2,
                      "iter_GBps": (p1 + p2) / (kt["graph_iter_ms"] * 1e-3) / 1e9,
+                     "iter_frac": (p1 + p2) / (kt["graph_iter_ms"] * 1e-3) / 1e9 / peak,
                      "fused_ms": kt["fused_ms"] if kt["fused_ms"] > 0 else None,
                      "fused_alg_bytes": pf,
                      "k_probe": probe},
@@ -412,30 +490,82 @@ def run_gpu(args, rank, world):
     return out
 
 
-def cpu_baseline(args, cfg, sample_iters):
-    """The oracle as it stands, on a bounded sample: the first `sample_iters`
-    iterations of system 0 (stop test off, Q27 force_iters), host cores."""
+def host_info():
+    """CPU model, usable cores and a single-thread STREAM triad (a = b + s c,
+    NumPy, 2^25 doubles per array, best of 5) measured in this run."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    nel = 1 << 25
+    bb = np.random.default_rng(1).random(nel)
+    cc = np.random.default_rng(2).random(nel)
+    aa = np.empty(nel)
+    best = float("inf")
+    for _ in range(5):
+        t0 = time.perf_counter()
+        np.multiply(cc, 3.0, out=aa)
+        np.add(aa, bb, out=aa)
+        best = min(best, time.perf_counter() - t0)
+    # the two NumPy passes move 5 arrays' worth (read c, write a; read a, b,
+    # write a); STREAM's triad counts 3
+    return {"cpu_model": model, "host_cores_available": len(os.sched_getaffinity(0)),
+            "stream_triad_gbs_1thread": 3 * 8 * nel / best / 1e9,
+            "stream_note": "NumPy a = 3c; a += b on 2^25 doubles, best of 5, counted as "
+                           "STREAM triad bytes (3 arrays)"}
+
+
+def _oracle_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
+    except Exception:   # noqa: BLE001
+        return 1
+
+
+def _seeded_space(cfg, k):
+    """A seeded N(0,1) k-column input space (the oracle's timing sample needs
+    the projections active without running the whole first system)."""
+    rng = np.random.default_rng(cfg.seed + 777)
+    shp = (cfg.n, k)
+    if cfg.complex:
+        return (rng.standard_normal(shp) + 1j * rng.standard_normal(shp),
+                rng.standard_normal(shp) + 1j * rng.standard_normal(shp))
+    return rng.standard_normal(shp), rng.standard_normal(shp)
+
+
+def cpu_baseline(args, cfg, sample_iters, k_active):
+    """The oracle as it stands, on a bounded sample: `sample_iters` forced
+    iterations (stop test off, Q27) of system 1 of the sequence, from a
+    seeded k_active-column input space when the timed systems ran with one
+    (so the sample runs the same augmented iteration), host cores (the
+    oracle's BLAS is limited to one thread, reading Q26; SciPy's SpMV is
+    single-threaded)."""
     import scipy.sparse as sp
     from oracle import rbicg as R
     from synth import system_sequence
-    try:
-        from threadpoolctl import threadpool_info
-        blas_threads = max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
-    except Exception:
-        blas_threads = 1
-    it = next(system_sequence(cfg, systems=[0]))
+    it = next(system_sequence(cfg, systems=[1], **({"lam_r": 0.0} if cfg.kind == "irka" else {})))
     A = sp.csr_matrix((it["data"], it["indices"], it["indptr"]), shape=(cfg.n, cfg.n))
+    U = Ut = None
+    if k_active > 0:
+        U, Ut = _seeded_space(cfg, k_active)
     t0 = time.perf_counter()
-    res = R.solve_dual(A, it["b"], it["bt"], k=cfg.k, s=cfg.s, tol=cfg.tol,
+    res = R.solve_dual(A, it["b"], it["bt"], U=U, Ut=Ut, k=cfg.k, s=cfg.s, tol=cfg.tol,
                        max_itn=sample_iters, trunc_tol=cfg.trunc_tol,
                        force_iters=sample_iters)
     el = time.perf_counter() - t0
-    return {"value": res.iterations / el, "unit": "iterations/s",
-            "cores": int(blas_threads), "kind": "oracle",
-            "host_cores_available": len(os.sched_getaffinity(0)),
-            "sample": f"{cfg.name} system 0, first {sample_iters} iterations "
-                      f"(force_iters, incl. {sample_iters // cfg.s} cycle ends), "
-                      f"{el:.1f} s"}
+    out = {"value": res.iterations / el, "unit": "iterations/s",
+           "cores": int(_oracle_threads()), "kind": "oracle",
+           "sample": f"{cfg.name} system 1, first {sample_iters} iterations (force_iters, incl. "
+                     f"{sample_iters // cfg.s} cycle ends, refresh of a seeded "
+                     f"{k_active}-column input space -> k_in = {res.basis_in.k}), {el:.1f} s"}
+    out.update(host_info())
+    return out
 
 
 def run_reference(args):
@@ -460,11 +590,7 @@ def run_reference(args):
         if i >= args.warmup:
             tot_it += res.iterations
             tot_t += el
-    try:
-        from threadpoolctl import threadpool_info
-        blas_threads = max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
-    except Exception:
-        blas_threads = 1
+    blas_threads = _oracle_threads()
     v = tot_it / tot_t
     sample = f"{cfg.name}: per step one cycle ({cfg.s} iterations, stop test off) of system j"
     return {"impl": "reference", "metric": "RBiCG iterations/sec (dual pair) and achieved HBM GB/s",
@@ -487,7 +613,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--kernel-iters", type=int, default=20)
     ap.add_argument("--cpu-sample-iters", type=int, default=0,
                     help="oracle sample length (0: 80 iterations at n ~ 1M, scaled "
@@ -496,13 +622,26 @@ def main():
     ap.add_argument("--no-k-probe", action="store_true",
                     help="skip the k = cfg.k kernel probe in the roofline block")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true",
+                    help="skip the in-run ncu capture of the dominant kernel's DRAM bytes")
     ap.add_argument("--no-update", action="store_true",
                     help="diagnostic only: no recycle-space updates (not the method's workload)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent copies instead of the row partition")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this command under torchrun
+        port = os.environ.get("MASTER_PORT", "29517")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", port, os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        if rank == 0:
+            print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+        sys.exit(2)
     if args.impl == "reference":
         if rank == 0:   # the other ranks exit without work
             print(json.dumps(run_reference(args)), flush=True)
@@ -516,7 +655,7 @@ def main():
             from synth import CONFIGS
             cfg = CONFIGS[args.config]
             m = args.cpu_sample_iters or max(8, min(80, int(80 * 3.2e6 / cfg.n)))
-            out["cpu_baseline"] = cpu_baseline(args, cfg, m)
+            out["cpu_baseline"] = cpu_baseline(args, cfg, m, out["roofline"]["k_active"])
         elif not args.no_cpu:
             out["cpu_baseline"] = None
         print(json.dumps(out), flush=True)

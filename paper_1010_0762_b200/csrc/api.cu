@@ -506,7 +506,10 @@ struct Solver {
       // decision is kept per (ctx, n, k, s) so a sequence does not query the
       // allocator every system (cudaMemGetInfo measured up to 20 ms)
       const size_t extra = (size_t)2 * ring * n * sizeof(T);
-      const int nblk = (k_basis == 0 ? 2 : 6) * kmax + 4 * std::max(k_basis, 0);   // (lazy U_j, candidate blocks)
+      // worst case of the n x k blocks: candidate U, Ũ and the cycle-end
+      // temporaries U_j, Ũ_j, C_j, C~_j (6 kmax; some allocated on first use)
+      // plus the refreshed input U, Ũ, C, C~ (4 k_basis)
+      const int nblk = 6 * kmax + 4 * std::max(k_basis, 0);
       const size_t need = extra + (size_t)(nblk + 2 * ring + 24) * n * sizeof(T);
       const uint64_t key = ((uint64_t)n << 20) ^ ((uint64_t)kmax << 10) ^ ((uint64_t)k_basis << 40) ^
                            (uint64_t)o.s ^ (sizeof(T) << 60);

@@ -260,7 +260,7 @@ __global__ void k_gram_reduce(const T *__restrict__ part, int nchunks, int mXY, 
 }
 
 template <typename T>
-void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
+static void gram_v1(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
           std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t strm) {
   const int mX = (int)X.size(), mY = (int)Y.size();
   G.assign((size_t)mX * mY, cplx(0, 0));
@@ -297,6 +297,168 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   const size_t gsm = sizeof(T) * 2 * 2 * GramRows<T>::v * (GT + 2);
   k_gram<T><<<grid, 256, gsm, strm>>>(dX, mX, dX + mX, mY, n, chunk, flags(X), flags(Y), dpart);
   k_gram_reduce<T><<<(mX * mY * 32 + 255) / 256, 256, 0, strm>>>(dpart, 4 * nchunks, mX * mY, dG);
+  count_launch(2);
+  std::vector<T> h((size_t)mX * mY);
+  RB_CUDA(cudaMemcpyAsync(h.data(), dG, g_bytes, cudaMemcpyDeviceToHost, strm));
+  RB_CUDA(cudaStreamSynchronize(strm));
+  ws_free(buf);
+  for (size_t i = 0; i < h.size(); ++i) G[i] = cplx(re(h[i]), im(h[i]));
+}
+
+// Register-tiled Gram (the pencil Grams of a cycle end: X = Ψ~ with 42..92
+// columns, Y = [Ψ, X0]): each thread owns an MX x MY micro-tile of the
+// block's output tile (up to 256 micro-tiles; the rest of the threads form
+// further row groups over the same tile); the tile's X and Y rows pass
+// through shared memory in double-buffered stages of G2R rows (cp.async, row
+// index fastest so a warp reads 32 consecutive rows of a column).  Every
+// column is read once per output tile -- one tile whenever the micro-tiles
+// fit (every cycle end of the BASELINE configs) -- and the inner loop does
+// MX*MY FMAs per MX + MY shared loads (fp64: 8 x 8, 64 FMAs per 16 loads).
+constexpr int G2R = 32;   // rows per stage
+template <typename T> struct Gram2Tile { static constexpr int mx = 8, my = 8; };
+template <> struct Gram2Tile<zc> { static constexpr int mx = 4, my = 4; };
+
+template <typename T, int MX, int MY>
+__global__ void __launch_bounds__(256, (MX * MY > 32 ? 1 : 2)) k_gram2(const ColDesc *__restrict__ X, int mX,
+                                                  const ColDesc *__restrict__ Y, int mY, int tX,
+                                                  int tY, int64_t n, int64_t chunk,
+                                                  T *__restrict__ part) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  const int tXp = (tX + MX - 1) / MX * MX, tYp = (tY + MY - 1) / MY * MY;
+  const int ntx = tXp / MX, nty = tYp / MY, nmt = ntx * nty;
+  const int ng = max(1, 256 / nmt);
+  const int ncol = tXp + tYp;
+  ColDesc *sd = reinterpret_cast<ColDesc *>(sm_raw);
+  T *sbase = reinterpret_cast<T *>(sm_raw + ((sizeof(ColDesc) * ncol + 15) / 16) * 16);
+  // [row][col]: X columns then Y columns; an odd row stride keeps the
+  // row-fast cp.async stores of a warp (32 rows of one column) on distinct banks
+  const int lds = ncol | 1;
+  const int stage = G2R * lds;
+  const int tilesY = (mY + tY - 1) / tY;
+  const int bx = blockIdx.x / tilesY, by = blockIdx.x % tilesY;
+  const int x0 = bx * tX, y0 = by * tY;
+  const int tid = threadIdx.x;
+  for (int c = tid; c < ncol; c += 256) {
+    ColDesc d{nullptr, 0};
+    if (c < tXp) {
+      if (c < tX && x0 + c < mX) d = X[x0 + c];
+    } else if (c - tXp < tY && y0 + c - tXp < mY) {
+      d = Y[y0 + c - tXp];
+    }
+    sd[c] = d;
+  }
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.y * chunk, r1 = min(n, r0 + chunk);
+  const int mt = tid % nmt, g = tid / nmt;
+  const bool active = g < ng;
+  const int ix = mt / nty, iy = mt % nty;
+  T acc[MX][MY];
+#pragma unroll
+  for (int u = 0; u < MX; ++u)
+#pragma unroll
+    for (int v = 0; v < MY; ++v) acc[u][v] = zero<T>();
+  const int nel = G2R * ncol;
+  auto load = [&](int64_t rb, int buf) {
+    T *st = sbase + buf * stage;
+    for (int e = tid; e < nel; e += 256) {
+      const int c = e / G2R, r = e % G2R;
+      const ColDesc d = sd[c];
+      const int64_t row = rb + r;
+      const bool ok = d.p != nullptr && row < r1;
+      const T *src = reinterpret_cast<const T *>(ok ? d.p : (const void *)part);
+      cp_async_el(st + r * lds + c, ok ? src + row * d.stride : src, ok);
+    }
+    cp_async_commit();
+  };
+  if (r0 < r1) load(r0, 0);
+  int buf = 0;
+  for (int64_t rb = r0; rb < r1; rb += G2R, buf ^= 1) {
+    if (rb + G2R < r1) load(rb + G2R, buf ^ 1);
+    else cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (active) {
+      const T *st = sbase + buf * stage;
+      for (int r = g; r < G2R; r += ng) {
+        const T *row = st + r * lds;
+        T xv[MX], yv[MY];
+        // micro-tile columns strided by the tile's micro-tile counts: the
+        // threads of a warp (consecutive iy) read consecutive words, no bank
+        // conflicts (contiguous 8-column micro-tiles put 9 threads on 2 banks)
+#pragma unroll
+        for (int u = 0; u < MX; ++u) xv[u] = conj(row[u * ntx + ix]);
+#pragma unroll
+        for (int v = 0; v < MY; ++v) yv[v] = row[tXp + v * nty + iy];
+#pragma unroll
+        for (int u = 0; u < MX; ++u)
+#pragma unroll
+          for (int v = 0; v < MY; ++v) acc[u][v] = mad(xv[u], yv[v], acc[u][v]);
+      }
+    }
+    __syncthreads();
+  }
+  if (!active) return;
+  // partial (chunk, row group) -> part[((chunk * ng + g) * mX + a) * mY + b]
+  const int64_t pc = (int64_t)blockIdx.y * ng + g;
+#pragma unroll
+  for (int u = 0; u < MX; ++u)
+#pragma unroll
+    for (int v = 0; v < MY; ++v) {
+      const int a = u * ntx + ix, bb = v * nty + iy;
+      if (a < tX && bb < tY && x0 + a < mX && y0 + bb < mY)
+        part[(pc * mX + x0 + a) * mY + y0 + bb] = acc[u][v];
+    }
+}
+
+template <typename T>
+void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
+          std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t strm) {
+  const int mX = (int)X.size(), mY = (int)Y.size();
+  G.assign((size_t)mX * mY, cplx(0, 0));
+  if (mX == 0 || mY == 0) return;
+  if (getenv("RBICG_GRAM_V1")) return gram_v1<T>(X, Y, n, G, ctx, strm);
+  constexpr int MX = Gram2Tile<T>::mx, MY = Gram2Tile<T>::my;
+  // output tile: all of X x Y when its micro-tiles fit 256 threads, else
+  // split Y (then X) into tiles that do
+  int ntxA = (mX + MX - 1) / MX, ntyA = (mY + MY - 1) / MY;
+  int ntx = std::min(ntxA, 16), nty = std::max(1, std::min(ntyA, 256 / ntx));
+  if (ntxA * ntyA <= 256) {
+    ntx = ntxA;
+    nty = ntyA;
+  }
+  const int tX = std::min(mX, ntx * MX), tY = std::min(mY, nty * MY);
+  const int tiles = ((mX + tX - 1) / tX) * ((mY + tY - 1) / tY);
+  const int nmt = ((tX + MX - 1) / MX) * ((tY + MY - 1) / MY);
+  const int ng = std::max(1, 256 / nmt);
+  const int ncol = (tX + MX - 1) / MX * MX + (tY + MY - 1) / MY * MY;
+  const size_t smem = ((sizeof(ColDesc) * ncol + 15) / 16) * 16 + sizeof(T) * 2 * G2R * (ncol | 1);
+  static bool attr = false;
+  if (!attr) {
+    RB_CUDA(cudaFuncSetAttribute((const void *)k_gram2<T, MX, MY>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  RB_CHECK(smem <= 200 * 1024, RBICG_EINVAL);
+  // resident blocks per SM (1 for the 8 x 8 fp64 micro-tiles: 64 accumulators
+  // per thread), whole waves of (tile, chunk) blocks
+  const int64_t slots = (int64_t)(MX * MY > 32 ? 2 : 4) * sm_budget(ctx->nsm);
+  int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4 * G2R - 1) / (4 * G2R),
+                                                            (slots + tiles - 1) / tiles));
+  const int64_t chunk = ((n + nchunks - 1) / nchunks + G2R - 1) / G2R * G2R;
+  nchunks = (int)((n + chunk - 1) / chunk);
+  const size_t desc_bytes = sizeof(ColDesc) * (mX + mY);
+  const size_t part_bytes = sizeof(T) * (size_t)nchunks * ng * mX * mY;
+  const size_t g_bytes = sizeof(T) * (size_t)mX * mY;
+  char *buf = (char *)ws_alloc(desc_bytes + part_bytes + g_bytes + 64);
+  ColDesc *dX = (ColDesc *)buf;
+  T *dpart = (T *)(buf + ((desc_bytes + 15) / 16) * 16);
+  T *dG = dpart + (size_t)nchunks * ng * mX * mY;
+  std::vector<ColDesc> both(X);
+  both.insert(both.end(), Y.begin(), Y.end());
+  RB_CUDA(cudaMemcpyAsync(dX, both.data(), desc_bytes, cudaMemcpyHostToDevice, strm));
+  dim3 grid(tiles, nchunks);
+  k_gram2<T, MX, MY><<<grid, 256, smem, strm>>>(dX, mX, dX + mX, mY, tX, tY, n, chunk, dpart);
+  k_gram_reduce<T><<<(mX * mY * 32 + 255) / 256, 256, 0, strm>>>(dpart, ng * nchunks, mX * mY, dG);
   count_launch(2);
   std::vector<T> h((size_t)mX * mY);
   RB_CUDA(cudaMemcpyAsync(h.data(), dG, g_bytes, cudaMemcpyDeviceToHost, strm));

@@ -46,6 +46,7 @@ static struct {
   zggev_t zggev = nullptr;
   dgesvd_t dgesvd = nullptr;
   zgesvd_t zgesvd = nullptr;
+  int (*set_threads_local)(int) = nullptr;   // OpenBLAS >= 0.3.27, per calling thread
 } L;
 
 static void *sym(const char *name) {
@@ -68,8 +69,13 @@ static void load() {
     L.zggev = (zggev_t)sym("zggev_");
     L.dgesvd = (dgesvd_t)sym("dgesvd_");
     L.zgesvd = (zgesvd_t)sym("zgesvd_");
+    L.set_threads_local = (int (*)(int))dlsym(L.h, "openblas_set_num_threads_local");
   });
   RB_CHECK(L.dggev && L.zggev && L.dgesvd && L.zgesvd && L.dgeev && L.zgeev, RBICG_ELAPACK);
+  // The pencils are of order <= k + s (<= 70): OpenBLAS's thread pool costs
+  // more than it saves there (C3 general-case cycle end: ~10 ms of host eig
+  // per cycle with the default pool) -- one thread for this calling thread
+  if (L.set_threads_local) L.set_threads_local(1);
 }
 
 // Standard eigenproblem P w = λ w with left and right vectors (the Q = I

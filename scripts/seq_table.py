@@ -20,6 +20,7 @@ cfg = CONFIGS[name]
 if nsys:
     cfg = cfg.scaled(cfg.N, systems=nsys)
 do_bicg = "--no-bicg" not in sys.argv
+pencil = "fast" if "--fast" in sys.argv else "plain"
 ctx = api.Context(0)
 R = ctx.recycle(cfg.n, cfg.k, complex_=cfg.complex)
 rows = []
@@ -44,7 +45,7 @@ for item in system_sequence(cfg):
     t = time.time()
     x, xt, res, _ = ctx.solve_dual(A, d["b"], d["bt"], x0, xt0, R, k=cfg.k, s=cfg.s,
                                    tol=cfg.tol, max_itn=cfg.max_itn,
-                                   trunc_tol=cfg.trunc_tol)
+                                   trunc_tol=cfg.trunc_tol, pencil=pencil)
     torch.cuda.synchronize()
     if cfg.kind == "irka":
         prev[item["slot"]] = (x, xt)
