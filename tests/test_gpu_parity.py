@@ -218,7 +218,8 @@ def _carry_from_oracle(ctx, cfg_k, cfg_s, tol, trunc, items, csr_of, max_itn,
                                       max_itn, trunc)
             assert hi - lo > max(2, 0.03 * hi), (its, lo, hi)   # really chaotic
             assert lo - 2 <= m <= hi + 2, (its, lo, hi)
-            _residual_bound_check(Ad, item, x, xt, ref)
+            if Ad.shape[0] <= 5000:   # dense ||A^{-1}|| only at small n
+                _residual_bound_check(Ad, item, x, xt, ref)
         elif m != ref.iterations:
             ref_m = R.solve_dual(Ad, item["b"], item["bt"], x0, xt0, U=U, Ut=Ut,
                                  k=cfg_k, s=cfg_s, tol=tol, max_itn=max_itn,
@@ -741,3 +742,156 @@ def test_fused_and_two_kernel_forms_agree(ctx, monkeypatch):
     assert res["iterations"] == m and res["cycles"] == ref.cycles == 2
     assert np.linalg.norm(x - ref.x) <= 1e-9 * np.linalg.norm(ref.x)
     assert res["k_out"] == ref.basis_out.k
+
+
+# ------------------------------------------------------------------ full size, k > 0
+def _seeded_space(cfg, k, seed_off=777):
+    rng = np.random.default_rng(cfg.seed + seed_off)
+    shp = (cfg.n, k)
+    if cfg.complex:
+        return (rng.standard_normal(shp) + 1j * rng.standard_normal(shp),
+                rng.standard_normal(shp) + 1j * rng.standard_normal(shp))
+    return rng.standard_normal(shp), rng.standard_normal(shp)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_full_size_projection_parity(ctx, name):
+    """Per-call projection parity at BASELINE size with a live recycle space
+    (Q25, 1e-12): the device refresh of a seeded k-column space for system 1
+    (C = AU, C~ = A^*Ũ, unit columns, SVD, truncation at the paper's 1e-6,
+    P:690-705) and ζ = D_c^{-1}C~^*z, ζ~ = D_c^{-1}C^*z~ against the oracle
+    on the gauge-invariant C ζ; D_c to 1e-12; the device basis bi-orthogonal."""
+    from oracle import rbicg as R
+    cfg = CONFIGS[name]
+    item = next(system_sequence(cfg, systems=[1]))
+    A = _csr((item["indptr"], item["indices"], item["data"]))
+    U, Ut = _seeded_space(cfg, cfg.k)
+    B = R.biorthogonalize(A, R.adjoint(A), U, Ut, cfg.trunc_tol)
+    assert B.k > 0
+    M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+    rec = ctx.recycle(cfg.n, cfg.k)
+    rec.import_(U, Ut)
+    z, zt = item["b"], item["bt"]
+    out = ctx.project(M, rec, z, zt, cfg.trunc_tol)
+    assert out["k"] == B.k
+    np.testing.assert_allclose(out["d"], B.d, rtol=1e-12)
+    ref = B.C @ ((B.Ct / B.d).conj().T @ z)
+    got = out["C"] @ out["zeta"]
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(z) * \
+        np.linalg.norm(B.C) / B.d.min()
+    reft = B.Ct @ ((B.C / B.d).conj().T @ zt)
+    gott = out["Ct"] @ out["zetat"]
+    assert np.linalg.norm(gott - reft) <= 1e-12 * np.linalg.norm(zt) * \
+        np.linalg.norm(B.Ct) / B.d.min()
+    G = out["Ct"].conj().T @ out["C"]
+    np.testing.assert_allclose(G, np.diag(out["d"]), atol=1e-10 * out["d"].max())
+    M.free()
+
+
+def _robust_prefix(ref_hist, alt_hist, rel=1e-8):
+    """Length of the leading stretch where the oracle and the oracle on
+    1e-15-perturbed b agree to `rel` (before BiCG's rounding amplification,
+    Q27/Q28, makes the histories differ)."""
+    a, b = np.abs(np.asarray(ref_hist)), np.asarray(alt_hist)
+    dev = np.abs(np.asarray(ref_hist) - b) > rel * np.maximum(a, 1e-300)
+    return int(np.argmax(dev)) if dev.any() else len(a)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_full_size_k_matched_iterations(ctx, name):
+    """Algorithm 2 with the projections active at BASELINE size:
+    system 1 from a recycle space -- C3: the oracle's own, built by its cycle
+    end after s + 3 iterations of system 0 (harmonic Ritz vectors of T_1,
+    P:614-628); C2: a seeded k-column space (C2's own spaces are truncated to
+    p = 0) -- both sides forced to m = s + 3 iterations (Q27)
+    across one cycle end of the "later system, cycle 1" case.
+    The α and ‖r‖ histories agree to 1e-6 over the stretch where the oracle
+    agrees with itself under a 1e-15 perturbation of b (BiCG's rounding
+    amplification, Q28) and that stretch is >= 3 iterations; x, x~ agree to
+    1e-7 or 10x the oracle's own spread; k_in equal, k_out within one
+    (borderline σ at the 1e-6 cut); leading output directions agree."""
+    from oracle import rbicg as R
+    cfg = CONFIGS[name]
+    items = list(system_sequence(cfg, systems=[0, 1]))
+    m = cfg.s + 3
+    if name == "C3":
+        A0 = _csr((items[0]["indptr"], items[0]["indices"], items[0]["data"]))
+        first = R.solve_dual(A0, items[0]["b"], items[0]["bt"], k=cfg.k, s=cfg.s, tol=cfg.tol,
+                             max_itn=m, trunc_tol=cfg.trunc_tol, force_iters=m)
+        U, Ut = first.basis_out.U, first.basis_out.Ut
+        del A0, first
+    else:
+        U, Ut = _seeded_space(cfg, cfg.k)
+    item = items[1]
+    A = _csr((item["indptr"], item["indices"], item["data"]))
+    kw = dict(U=U, Ut=Ut, k=cfg.k, s=cfg.s, tol=cfg.tol, max_itn=m,
+              trunc_tol=cfg.trunc_tol, force_iters=m)
+    ref = R.solve_dual(A, item["b"], item["bt"], **kw)
+    assert ref.basis_in.k > 0 and ref.cycles == 1
+    rng = np.random.default_rng(4321)
+    alt = R.solve_dual(A, item["b"] * (1 + 1e-15 * rng.standard_normal(cfg.n)), item["bt"], **kw)
+    sp_x = np.linalg.norm(alt.x - ref.x) / np.linalg.norm(ref.x)
+    sp_xt = np.linalg.norm(alt.xt - ref.xt) / np.linalg.norm(ref.xt)
+    M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+    rec = ctx.recycle(cfg.n, cfg.k)
+    rec.import_(U, Ut)
+    x, xt, res, h = ctx.solve_dual(M, item["b"], item["bt"], R=rec, k=cfg.k, s=cfg.s,
+                                   tol=cfg.tol, max_itn=m, trunc_tol=cfg.trunc_tol,
+                                   force_iters=m, history=True)
+    assert res["iterations"] == m and res["cycles"] == 1
+    assert res["k_in"] == ref.basis_in.k and abs(res["k_out"] - ref.basis_out.k) <= 1
+    assert np.linalg.norm(x - ref.x) <= max(1e-7, 10 * sp_x) * np.linalg.norm(ref.x)
+    assert np.linalg.norm(xt - ref.xt) <= max(1e-7, 10 * sp_xt) * np.linalg.norm(ref.xt)
+    # the stretch where a 1e-15 perturbation moves the oracle's α by < 1e-10:
+    # beyond it the ~1e-16 differences of the device's reduction order, which
+    # the near-singular projections (D_c down to 1e-6) amplify more than a
+    # perturbation of b, have grown past 1e-6
+    na = _robust_prefix(np.real(ref.hist["alpha"]), np.real(alt.hist["alpha"]), rel=1e-10)
+    assert na >= 3, na
+    np.testing.assert_allclose(h[:na, 2], np.real(ref.hist["alpha"])[:na], rtol=1e-6)
+    rn = np.array(ref.hist["rnorm"][1:]) / np.linalg.norm(item["b"])
+    np.testing.assert_allclose(h[:na, 0], rn[:na], rtol=1e-6)
+    kk = min(res["k_out"], ref.basis_out.k) - 2
+    if kk > 0:
+        Ug, Utg = rec.export()
+        assert np.sort(_cosines(Ug, ref.basis_out.U))[::-1][:kk].min() >= 0.99
+        assert np.sort(_cosines(Utg, ref.basis_out.Ut))[::-1][:kk].min() >= 0.99
+    M.free()
+
+
+def test_full_size_c4_sweep(ctx):
+    """One full IRKA-like sweep of C4 at BASELINE size (n = 10^6 complex,
+    k = 8, s = 40, the paper's truncation 1e-6): six shifted dual systems,
+    each solved by both sides from the oracle's input recycle space (Q27
+    protocol: iterations max(2, 3 %) or the Q28 ensemble, solutions 1e-7 at
+    matched counts, true residuals <= tol, same k_in).  Shifts placed right of
+    0 (lam_r = 0) instead of the ARPACK estimate of max Re λ(K) (~50 s of
+    host time), the same on both sides."""
+    cfg = CONFIGS["C4"].scaled(100, systems=6)
+    items = list(system_sequence(cfg, lam_r=0.0))
+    its = _carry_from_oracle(ctx, cfg.k, cfg.s, cfg.tol, cfg.trunc_tol, items,
+                             lambda it: _csr((it["indptr"], it["indices"], it["data"])),
+                             cfg.max_itn, lam_slots=True)
+    assert len(its) == 6
+
+
+def test_full_size_c2_fused_count_vs_algorithm2(ctx):
+    """The default k = 0 iteration (one kernel per iteration, β from the
+    one-step expansion of ρ) against Algorithm 2 AS WRITTEN
+    (oracle variant="standard") on C2 system 0 at full size
+    (n = 1,048,576, ~3,300 iterations): iteration counts within BASELINE's
+    max(2, 3 %), both converged, true residuals <= tol.  (Measured here:
+    oracle 3,352; look-ahead oracle 3,339; GPU 3,313.)"""
+    from oracle import rbicg as R
+    cfg = CONFIGS["C2"]
+    item = next(system_sequence(cfg, systems=[0]))
+    A = _csr((item["indptr"], item["indices"], item["data"]))
+    ref = R.solve_dual(A, item["b"], item["bt"], k=0, s=cfg.s, tol=cfg.tol,
+                       max_itn=cfg.max_itn, variant="standard")
+    M = ctx.matrix(item["indptr"], item["indices"], item["data"])
+    x, xt, res, _ = ctx.solve_dual(M, item["b"], item["bt"], k=0, s=cfg.s, tol=cfg.tol,
+                                   max_itn=cfg.max_itn)
+    assert ref.status == 0 and res["status"] == 0
+    assert iters_close(res["iterations"], ref.iterations), (res["iterations"], ref.iterations)
+    assert res["relres_true"] <= cfg.tol and res["relres_dual_true"] <= cfg.tol
+    M.free()
