@@ -234,9 +234,17 @@ def run_gpu(args, rank, world):
     systems = build_systems(cfg, list(range(steps)))
     # inputs resident in HBM before the timed region (the matrix is passed
     # whole; vectors are this rank's rows)
+    def local_csr(it):
+        """This rank's rows of A: local rowptr, GLOBAL columns (§8(b))."""
+        ip = it["indptr"]
+        a, b = int(ip[r0]), int(ip[r1])
+        return {"indptr": np.ascontiguousarray(ip[r0:r1 + 1] - ip[r0], dtype=np.int32),
+                "indices": np.ascontiguousarray(it["indices"][a:b]),
+                "data": np.ascontiguousarray(it["data"][a:b])}
+
     def upload(it):
-        d = {k: torch.from_numpy(np.ascontiguousarray(it[k])).to(f"cuda:{dev}")
-             for k in ("indptr", "indices", "data")}
+        loc = local_csr(it)
+        d = {k: torch.from_numpy(loc[k]).to(f"cuda:{dev}") for k in ("indptr", "indices", "data")}
         for k in ("b", "bt"):
             d[k] = torch.from_numpy(np.ascontiguousarray(it[k][r0:r1])).to(f"cuda:{dev}")
         return d
@@ -330,7 +338,11 @@ def run_gpu(args, rank, world):
     if part:   # the partitioned context has no timing hook: the kernels on one GPU
         kctx = api.Context(dev)
         kR = kctx.recycle(cfg.n, cfg.k, cfg.complex)
-    A = kctx.matrix(last["indptr"], last["indices"], last["data"])
+    if part:
+        g = systems[-1]
+        A = kctx.matrix(g["indptr"], g["indices"], g["data"])
+    else:
+        A = kctx.matrix(last["indptr"], last["indices"], last["data"])
     kt = kctx.time_kernels(A, kR, k=cfg.k, s=cfg.s, iters=args.kernel_iters,
                            trunc_tol=cfg.trunc_tol)
     A.free()
@@ -363,7 +375,8 @@ def run_gpu(args, rank, world):
     # iteration on a seeded random space so its kernels are measured too
     probe = None
     if kt["k"] == 0 and cfg.k > 0 and not args.no_k_probe:
-        A = kctx.matrix(last["indptr"], last["indices"], last["data"])
+        g = systems[-1] if part else last
+        A = kctx.matrix(g["indptr"], g["indices"], g["data"])
         rng = np.random.default_rng(cfg.seed + 777)
         shp = (cfg.n, cfg.k)
         if cfg.complex:
@@ -401,7 +414,8 @@ def run_gpu(args, rank, world):
             return out
         h_sys = []
         for it in systems[args.warmup:steps]:
-            hs = {k: pinned(np.ascontiguousarray(it[k])) for k in ("indptr", "indices", "data")}
+            loc = local_csr(it)
+            hs = {k: pinned(loc[k]) for k in ("indptr", "indices", "data")}
             for k in ("b", "bt"):
                 hs[k] = pinned(np.ascontiguousarray(it[k][r0:r1]))
             hs["x"] = pinned(np.zeros_like(hs["b"]))

@@ -76,12 +76,16 @@ typedef struct rbicg_rec rbicg_rec;
  *           partitioned path where fewer GPUs than ranks exist.
  * Rows are split evenly: rank q owns [floor(q n/P), floor((q+1) n/P)).
  * Partitioned calls are collective: every rank makes the same calls in the
- * same order.  rbicg_matrix_csr takes the GLOBAL CSR on every rank (each rank
- * keeps its rows of A and A^* and derives its halo plan without
- * communication); vectors (b, x, u, w, ...) and recycle blocks are the rank's
- * own rows; scalar results are replicated.  The dbg_project and
- * dbg_time_kernels hooks are single-GPU only (RBICG_EINVAL).
- * row_begin/row_end are informative (see rbicg_plan_partition). */
+ * same order.  rbicg_matrix_csr takes ONLY the rank's block of rows (local
+ * rowptr, GLOBAL column indices, local values; blocks are contiguous and in
+ * rank order, of any sizes -- the library gathers the sizes): the rows of A^*
+ * in the block are assembled on the device from the rank's entries plus the
+ * entries of A in its columns held by other ranks, exchanged over the
+ * communicator; the ghost/send plan is cached per context while the block's
+ * sparsity pattern (hashed on the device) repeats.  Vectors (b, x, u, w, ...)
+ * and recycle blocks are the rank's own rows; scalar results are replicated.
+ * The dbg_project and dbg_time_kernels hooks are single-GPU only
+ * (RBICG_EINVAL).  row_begin/row_end are informative. */
 typedef struct {
   int32_t rank, nranks;
   uint8_t nccl_id[128];
@@ -133,7 +137,10 @@ int rbicg_finalize(rbicg_ctx *ctx);
  * P:44-52) and its explicit conjugate transpose A^* (BASELINE.json (1)).
  * rowptr[n+1], colind[nnz] are int32 CSR (columns need not be sorted; n and
  * nnz < 2^31), val[nnz] of `dtype`.  on_device selects where the three
- * arrays live.  The matrix is immutable once built. */
+ * arrays live.  The matrix is immutable once built.  On a partitioned
+ * context n and nnz count the rank's block of rows only and colind holds
+ * global column indices (see rbicg_dist); the global order is the sum of the
+ * blocks (< 2^31).  Collective there. */
 int rbicg_matrix_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz,
                      const int32_t *rowptr, const int32_t *colind,
                      const void *val, rbicg_dtype dtype, int on_device,

@@ -1643,71 +1643,6 @@ int64_t rbicg_launch_count(void) { return g_launches.load(); }
 // indices (own rows first, then the ghost columns sorted by global index,
 // grouped by owner) and the send lists of its own rows (dist.cpp).  No
 // communication is needed: each rank derives its plan from the same matrix.
-static void build_partitioned(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rp_d,
-                              const int32_t *ci_d, const void *vv_d, rbicg_dtype dt, rbicg_mat *M) {
-  const size_t w = wbytes(dt);
-  std::vector<int32_t> rp(n + 1), ci(std::max<int64_t>(nnz, 1));
-  std::vector<unsigned char> vv(w * std::max<int64_t>(nnz, 1));
-  RB_CUDA(cudaMemcpyAsync(rp.data(), rp_d, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, ctx->stream));
-  if (nnz) {
-    RB_CUDA(cudaMemcpyAsync(ci.data(), ci_d, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, ctx->stream));
-    RB_CUDA(cudaMemcpyAsync(vv.data(), vv_d, w * nnz, cudaMemcpyDeviceToHost, ctx->stream));
-  }
-  RB_CUDA(cudaStreamSynchronize(ctx->stream));
-  // the plan depends only on the pattern, which a sequence keeps:
-  // reuse the last one when the pattern is unchanged
-  static std::mutex mu;
-  static std::map<const rbicg_ctx *, std::tuple<std::vector<int32_t>, std::vector<int32_t>, Plan>> cache;
-  Plan pl;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(ctx);
-    if (it != cache.end() && std::get<2>(it->second).P == ctx->nranks &&
-        std::get<2>(it->second).q == ctx->rank && std::get<0>(it->second) == rp &&
-        std::get<1>(it->second) == ci) {
-      pl = std::get<2>(it->second);
-    } else {
-      pl = make_plan(n, rp.data(), ci.data(), ctx->nranks, ctx->rank);
-      cache[ctx] = std::make_tuple(rp, ci, pl);
-    }
-  }
-  std::vector<int32_t> rpA, ciA, rpH, ciH;
-  std::vector<unsigned char> vA, vH;
-  local_csr(pl, n, rp.data(), ci.data(), vv.data(), w, dt == RBICG_C128, false, rpA, ciA, vA);
-  local_csr(pl, n, rp.data(), ci.data(), vv.data(), w, dt == RBICG_C128, true, rpH, ciH, vH);
-  std::vector<void *> tmp;
-  auto up = [&](const void *src, size_t bytes) {
-    void *d = ws_alloc(std::max<size_t>(bytes, 16));
-    tmp.push_back(d);
-    if (bytes) RB_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    return d;
-  };
-  const int32_t *drpA = (const int32_t *)up(rpA.data(), 4 * rpA.size());
-  const int32_t *dciA = (const int32_t *)up(ciA.data(), 4 * ciA.size());
-  const void *dvA = up(vA.data(), vA.size());
-  const int32_t *drpH = (const int32_t *)up(rpH.data(), 4 * rpH.size());
-  const int32_t *dciH = (const int32_t *)up(ciH.data(), 4 * ciH.size());
-  const void *dvH = up(vH.data(), vH.size());
-  build_matrix_local(ctx, pl.nloc, drpA, dciA, dvA, drpH, dciH, dvH, dt, M);
-  for (void *d : tmp) ws_free(d);
-  M->nnz = (int64_t)ciA.size();
-  M->row_begin = pl.r0;
-  HaloPlan &h = M->halo;
-  h.nloc = pl.nloc;
-  h.nghost = (int64_t)pl.ghost.size();
-  h.nsend = (int64_t)pl.send_idx.size();
-  h.send_nbr = pl.send_nbr;
-  h.recv_nbr = pl.recv_nbr;
-  h.send_off = pl.send_off;
-  h.send_cnt = pl.send_cnt;
-  h.recv_off = pl.recv_off;
-  h.recv_cnt = pl.recv_cnt;
-  h.send_idx = (int32_t *)ws_alloc(4 * std::max<int64_t>(h.nsend, 1));
-  if (h.nsend)
-    RB_CUDA(cudaMemcpyAsync(h.send_idx, pl.send_idx.data(), 4 * h.nsend, cudaMemcpyHostToDevice, ctx->stream));
-  RB_CUDA(cudaStreamSynchronize(ctx->stream));
-}
-
 int rbicg_init(rbicg_ctx **out, int device, void *stream, const rbicg_dist *dist) {
   if (!out) return RBICG_EINVAL;
   if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks ||
@@ -1781,6 +1716,7 @@ int rbicg_finalize(rbicg_ctx *ctx) {
     g_ctxs.erase(ctx);
   }
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  forget_partition_plan(ctx);
   ws_release_all();
   cudaEventDestroy(ctx->order_ev);
   cudaStreamDestroy(ctx->stream);
@@ -1807,7 +1743,7 @@ int rbicg_matrix_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowp
     }
     auto *M = new rbicg_mat();
     M->ctx = ctx;
-    M->n_global = n;
+    M->n_global = n;   // partitioned: n is the block's row count (build_partitioned sets the total)
     try {
       if (ctx->dist()) build_partitioned(ctx, n, nnz, rp, ci, vv, dtype, M);
       else build_matrix(ctx, n, nnz, rp, ci, vv, dtype, M);

@@ -168,6 +168,12 @@ void build_matrix_local(rbicg_ctx *ctx, int64_t nloc, const int32_t *rpA, const 
                         const void *vA, const int32_t *rpH, const int32_t *ciH, const void *vH,
                         rbicg_dtype dt, rbicg_mat *M);
 
+// ---- partition.cu: the row-block store of a partitioned context (the block's
+// rows of A with GLOBAL columns in; A^* rows by the value halo; halo plan)
+void build_partitioned(rbicg_ctx *ctx, int64_t nloc, int64_t nnz, const int32_t *rowptr_d,
+                       const int32_t *colind_global_d, const void *val_d, rbicg_dtype dt, rbicg_mat *M);
+void forget_partition_plan(const rbicg_ctx *ctx);
+
 // ---- kernels.cu (launch wrappers; all on ctx->stream)
 void prepare_kernels();        // one-time function attributes (not capturable)
 void prepare_block_kernels();

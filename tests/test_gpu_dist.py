@@ -38,6 +38,16 @@ def _rows(n, P, q):
     return (n * q) // P, (n * (q + 1)) // P
 
 
+def _local(t, r0, r1):
+    """The row block [r0, r1) of a CSR triple: local rowptr, GLOBAL column
+    indices, local values -- what a partitioned rbicg_matrix_csr takes
+    (§8(b): every rank passes only its own rows)."""
+    indptr, indices, data = t[:3]
+    a, b = int(indptr[r0]), int(indptr[r1])
+    return (np.ascontiguousarray(indptr[r0:r1 + 1] - indptr[r0], dtype=np.int32),
+            np.ascontiguousarray(indices[a:b], dtype=np.int32), np.ascontiguousarray(data[a:b]))
+
+
 def run_group(P, fn):
     """fn(ctx, rank, r0, r1) on P virtual ranks (threads); results by rank."""
     import torch
@@ -75,7 +85,7 @@ def test_partitioned_spmv_pair(P, cplx):
 
     def fn(ctx, q):
         r0, r1 = _rows(n, P, q)
-        M = ctx.matrix(*t)
+        M = ctx.matrix(*_local(t, r0, r1))
         return ctx.spmv_pair(M, p[r0:r1].copy(), pt[r0:r1].copy())
 
     res = run_group(P, fn)
@@ -85,13 +95,51 @@ def test_partitioned_spmv_pair(P, cplx):
     assert np.linalg.norm(zt - zt_ref) <= 1e-12 * np.linalg.norm(zt_ref)
 
 
+@pytest.mark.parametrize("blocks", [(100, 500, 400), (640, 1, 359)])
+def test_partitioned_uneven_blocks_spmv_and_solve(blocks):
+    """Blocks of any sizes in rank order (the library gathers the block sizes):
+    the SpMV pair on a nonsymmetric pattern to 1e-12 and a BiCG solve equal
+    to the even partition's iterations; the second matrix of the same pattern
+    reuses the cached halo plan (same results)."""
+    n = sum(blocks)
+    P = len(blocks)
+    beg = np.concatenate([[0], np.cumsum(blocks)])
+    t = random_sparse(n, 0.01, seed=77, complex_=False)
+    A = _csr(t)
+    p, pt = vec(n, 3, False), vec(n, 4, False)
+    z_ref, zt_ref = A @ p, A.conj().T @ pt
+    b, bt = vec(n, 5, False), vec(n, 6, False)
+
+    def fn(ctx, q):
+        r0, r1 = int(beg[q]), int(beg[q + 1])
+        outs = []
+        for _ in range(2):   # same pattern twice: cached plan
+            M = ctx.matrix(*_local(t, r0, r1))
+            z, zt = ctx.spmv_pair(M, p[r0:r1].copy(), pt[r0:r1].copy())
+            x, xt, res, _ = ctx.solve_dual(M, b[r0:r1].copy(), bt[r0:r1].copy(), k=0, s=10,
+                                           tol=1e-10, max_itn=2000)
+            outs.append((z, zt, x, res["iterations"]))
+            M.free()
+        return outs
+
+    res = run_group(P, fn)
+    for rep in range(2):
+        z = np.concatenate([r[rep][0] for r in res])
+        zt = np.concatenate([r[rep][1] for r in res])
+        assert np.linalg.norm(z - z_ref) <= 1e-12 * np.linalg.norm(z_ref)
+        assert np.linalg.norm(zt - zt_ref) <= 1e-12 * np.linalg.norm(zt_ref)
+        x = np.concatenate([r[rep][2] for r in res])
+        assert np.linalg.norm(b - A @ x) <= 1e-9 * np.linalg.norm(b)
+    assert len({r[0][3] for r in res} | {r[1][3] for r in res}) == 1
+
+
 def _solve_group(P, t, b, bt, k, s, tol, max_itn, trunc, U=None, Ut=None, force=0,
                  history=False, pencil="plain"):
     n = len(b)
 
     def fn(ctx, q):
         r0, r1 = _rows(n, P, q)
-        M = ctx.matrix(*t)
+        M = ctx.matrix(*_local(t, r0, r1))
         rec = ctx.recycle(r1 - r0, max(k, 1), np.iscomplexobj(b))
         if U is not None and U.shape[1]:
             rec.import_(U[r0:r1].copy(), Ut[r0:r1].copy())
@@ -214,7 +262,7 @@ def test_partitioned_sequence_c4_like():
 
         def fn(ctx, q, item=item, x0=x0, xt0=xt0, U=U, Ut=Ut):
             r0, r1 = _rows(n, P, q)
-            M = ctx.matrix(*t)
+            M = ctx.matrix(*_local(t, r0, r1))
             rec = ctx.recycle(r1 - r0, cfg.k, True)
             if U is not None and U.shape[1]:
                 rec.import_(U[r0:r1].copy(), Ut[r0:r1].copy())
@@ -253,7 +301,7 @@ def test_partitioned_bilinear():
 
     def fn(ctx, q):
         r0, r1 = _rows(n, P, q)
-        M = ctx.matrix(*t)
+        M = ctx.matrix(*_local(t, r0, r1))
         return ctx.bilinear(M, u[r0:r1].copy(), w[r0:r1].copy(), k=4, s=10, tol=1e-10,
                             max_itn=1000)[0]
 
@@ -300,6 +348,7 @@ def test_nccl_one_rank_partitioned_path_matches_plain(monkeypatch, fused):
         rec = ctx.recycle(cfg.n, cfg.k)
         runs = []
         for item in items:
+            # one rank: its block is every row (global == local)
             M = ctx.matrix(item["indptr"], item["indices"], item["data"])
             x, xt, res, h = ctx.solve_dual(M, item["b"], item["bt"], R=rec, k=cfg.k, s=cfg.s,
                                            tol=cfg.tol, max_itn=cfg.max_itn,
