@@ -493,3 +493,59 @@ def test_next1_single_reduction_matches_algorithm2(cplx, variant):
     np.testing.assert_allclose(got.x, ref.x, rtol=1e-8)
     xd = np.linalg.solve(As.toarray(), b2)
     assert np.linalg.norm(got.x - xd) <= 1e-9 * np.linalg.norm(xd)
+
+
+# ------------------------------------------------------------------ Q3 / Q11 pins
+def test_q3_serious_breakdown_at_start_and_redraw():
+    """(r~_0, r_0) = 0 exactly (b = e_1, b~ = e_2, x_{-1} = 0): Algorithm 1/2
+    step 3 -- without a re-draw vector the solve reports a
+    serious breakdown at iteration 0 (Q3, Q4); with one (used once) it runs
+    and converges to the dense solution."""
+    from oracle import rbicg as R
+    n = 6
+    A = sp.csr_matrix(np.diag(np.arange(1.0, n + 1)) + np.diag(np.full(n - 1, 0.3), 1)
+                      + np.diag(np.full(n - 1, -0.2), -1))
+    b, bt = np.eye(n)[0], np.eye(n)[1]
+    res = R.solve_dual(A, b, bt, k=0, s=5, tol=1e-12, max_itn=50)
+    assert res.status == R.BREAKDOWN_SERIOUS and res.iterations == 0
+    res2 = R.solve_dual(A, b, bt, k=0, s=5, tol=1e-12, max_itn=50,
+                        xt_redraw=np.linspace(-1, 1, n))
+    assert res2.status == R.OK
+    np.testing.assert_allclose(res2.x, np.linalg.solve(A.toarray(), b), rtol=1e-10, atol=1e-12)
+
+
+def test_q3_second_kind_breakdown():
+    """σ_1 = (p~_1, A p_1) = 0 with ρ_0 ≠ 0: A = [[0, 1], [1, 0]], b = b~ = e_1
+    (p_1 = e_1, A p_1 = e_2 ⊥ e_1) -- the textbook zero-curvature failure of
+    CG on an indefinite matrix; BiCG reports a breakdown of the second kind
+    before its first update (Q3)."""
+    from oracle import rbicg as R
+    from oracle.bicg import bicg, BREAKDOWN_SECOND
+    A = sp.csr_matrix(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    e1 = np.array([1.0, 0.0])
+    res = R.solve_dual(A, e1, e1, k=0, s=5, tol=1e-12, max_itn=10)
+    assert res.status == R.BREAKDOWN_SECOND and res.iterations == 0
+    out = bicg(A, e1, e1, np.zeros(2), np.zeros(2), 1e-12, 10)
+    assert out["status"] == BREAKDOWN_SECOND
+
+
+def test_q3_breakdown_predicate():
+    from oracle.bicg import breakdown
+    assert breakdown(0.0, 1.0, 1.0, 0.0)              # exact zero (the paper's "= 0")
+    assert breakdown(float("nan"), 1.0, 1.0, 0.0)     # non-finite
+    assert breakdown(float("inf"), 1.0, 1.0, 0.0)
+    assert not breakdown(1e-300, 1.0, 1.0, 0.0)       # tiny but nonzero passes at eps = 0
+    assert breakdown(1e-15, 1.0, 1.0, 1e-14) and not breakdown(1e-13, 1.0, 1.0, 1e-14)
+
+
+def test_q11_infinite_eigenvalues_excluded():
+    """Q11: the pencil's infinite eigenvalues (β_QZ = 0, a singular Q) are not
+    'nearest the origin' candidates: P = diag(1, 2, 3, 4), Q = diag(1, 0, 1, 1)
+    has eigenvalues {1, ∞, 3, 4}; the two nearest the origin are 1 and 3."""
+    from oracle import rbicg as R
+    P = np.diag([1.0, 2.0, 3.0, 4.0])
+    Q = np.diag([1.0, 0.0, 1.0, 1.0])
+    W, Wt, lam = R.solve_pencil(P, Q, 2, real=True)
+    np.testing.assert_allclose(np.sort(lam.real), [1.0, 3.0], rtol=1e-12)
+    # the selected right vectors span e_1, e_3
+    assert np.abs(W[[1, 3], :]).max() < 1e-12
