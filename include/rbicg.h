@@ -173,6 +173,36 @@ int rbicg_solve_dual(rbicg_ctx *ctx, const rbicg_mat *A, const void *b,
                      rbicg_rec *R, const rbicg_opts *opts, int on_device,
                      rbicg_result *res, double *hist);
 
+/* Split preconditioning (the paper's experiments,
+ * PAPER.md:1330-1333, :1406-1409).  rbicg_prec_ilut factors the n x n CSR
+ * (host or device arrays; same conventions as rbicg_matrix_csr) by Crout ILU
+ * with threshold droptol (ILUC, no pivoting; drop rule of the paper's Matlab:
+ * off-diagonal U(k, j) kept if |u| >= droptol ||A(:, j)||, L(i, k) kept if
+ * |l| >= droptol ||A(:, k)|| before the division by the pivot; droptol = 0 is
+ * the exact LU).  Host factorisation (per-system setup), device factors L, U
+ * and their conjugate transposes.  RBICG_EINVAL on a zero pivot or on a
+ * partitioned context.  rbicg_prec_export copies L (which = 0: strictly lower
+ * part, unit diagonal implied) or U (which = 1) to host CSR; two-call (NULL
+ * arrays: *nnz only).
+ * rbicg_solve_dual_pc runs Algorithm 2 on the split-preconditioned pair
+ *   (L^{-1} A U^{-1}) x̂ = L^{-1} b,   (L^{-1} A U^{-1})^* x̂~ = U^{-*} b~,
+ * x_{-1}, x~_{-1} mapped to x̂ = U x, x̂~ = L^* x~ and back after step 7; the
+ * recycle space in R, the stop test and the true residuals belong to the
+ * preconditioned pair (readings Q33, Q34).  Same arguments as
+ * rbicg_solve_dual; P = NULL is rbicg_solve_dual.  One GPU only. */
+typedef struct rbicg_prec rbicg_prec;
+int rbicg_prec_ilut(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr,
+                    const int32_t *colind, const void *val, rbicg_dtype dtype,
+                    double droptol, int on_device, rbicg_prec **P);
+int rbicg_prec_free(rbicg_prec *P);
+int rbicg_prec_export(const rbicg_prec *P, int which, int32_t *rowptr,
+                      int32_t *colind, void *val, int64_t *nnz);
+int rbicg_solve_dual_pc(rbicg_ctx *ctx, const rbicg_mat *A, const rbicg_prec *P,
+                        const void *b, const void *bt, void *x, void *xt,
+                        const void *xt_redraw, rbicg_rec *R,
+                        const rbicg_opts *opts, int on_device,
+                        rbicg_result *res, double *hist);
+
 /* u^* A^{-1} w from the dual pair A x = w, A^* x~ = u, estimator
  * u^*x + x~^*(w - Ax) (reading Q19).  value: one scalar of A's dtype (host).
  * x, xt: nullable outputs (initial guesses are zero). */

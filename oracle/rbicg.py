@@ -55,7 +55,10 @@ def empty_basis(n, dtype):
 
 
 def adjoint(A):
-    """Explicit conjugate transpose A^* (BASELINE.json (1))."""
+    """Explicit conjugate transpose A^* (BASELINE.json (1)); an operator
+    (oracle.precond.SplitOperator, NEXT-4) supplies its own adjoint."""
+    if hasattr(A, "adjoint_op"):
+        return A.adjoint_op()
     return A.conj().T.tocsr()
 
 

@@ -107,6 +107,12 @@ _sig = {
     "rbicg_solve_dual": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp,
                                    C.POINTER(Opts), C.c_int, C.POINTER(Result),
                                    vp]),
+    "rbicg_prec_ilut": (C.c_int, [vp, C.c_int64, C.c_int64, vp, vp, vp, C.c_int, C.c_double,
+                                  C.c_int, C.POINTER(vp)]),
+    "rbicg_prec_free": (C.c_int, [vp]),
+    "rbicg_prec_export": (C.c_int, [vp, C.c_int, vp, vp, vp, C.POINTER(C.c_int64)]),
+    "rbicg_solve_dual_pc": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                      C.POINTER(Opts), C.c_int, C.POINTER(Result), vp]),
     "rbicg_bilinear": (C.c_int, [vp, vp, vp, vp, vp, C.POINTER(Opts), C.c_int,
                                  vp, C.POINTER(Result)]),
     "rbicg_dbg_spmv_pair": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int]),

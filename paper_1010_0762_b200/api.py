@@ -103,14 +103,20 @@ class Context:
         return Recycle(self, n, k_max, complex_)
 
     # ------------------------------------------------------------ solve
+    def precond_ilut(self, indptr, indices, data, droptol=0.05):
+        """Crout ILUT split preconditioner M = L U ≈ A (rbicg_prec_ilut,
+        SURVEY §8(f) NEXT-4)."""
+        return Precond(self, indptr, indices, data, droptol)
+
     def solve_dual(self, A, b, bt, x=None, xt=None, R=None, *, k=10, s=40,
                    tol=1e-8, max_itn=20000, trunc_tol=1e-6, update_recycle=True,
                    force_iters=0, xt_redraw=None, history=False, inplace=False,
-                   pencil="plain"):
+                   pencil="plain", M=None):
         """inplace=True: x, xt (given, contiguous, b's dtype) are the in/out
         buffers themselves (e.g. page-locked host arrays); otherwise copies.
         pencil: "plain" (explicit Grams) or "fast" (§4.4 recurrences,
-        rbicg_opts.pencil = 1)."""
+        rbicg_opts.pencil = 1).  M: a Precond -- split-preconditioned solve
+        (rbicg_solve_dual_pc; the recycle space belongs to L^{-1}AU^{-1})."""
         if pencil not in ("plain", "fast"):
             raise ValueError(pencil)
         dev = _is_torch(b)
@@ -140,11 +146,18 @@ class Context:
                                    dtype=torch.float64, device=b.device)
             else:
                 hist = np.zeros((max(max_itn, force_iters), 6))
-        code = lib.rbicg_solve_dual(self._h, A._h, _ptr(b), _ptr(bt), _ptr(x),
-                                    _ptr(xt), _ptr(xt_redraw),
-                                    R._h if R is not None else None,
-                                    C.byref(o), 1 if dev else 0, C.byref(res),
-                                    _ptr(hist))
+        if M is not None:
+            code = lib.rbicg_solve_dual_pc(self._h, A._h, M._h, _ptr(b), _ptr(bt), _ptr(x),
+                                           _ptr(xt), _ptr(xt_redraw),
+                                           R._h if R is not None else None,
+                                           C.byref(o), 1 if dev else 0, C.byref(res),
+                                           _ptr(hist))
+        else:
+            code = lib.rbicg_solve_dual(self._h, A._h, _ptr(b), _ptr(bt), _ptr(x),
+                                        _ptr(xt), _ptr(xt_redraw),
+                                        R._h if R is not None else None,
+                                        C.byref(o), 1 if dev else 0, C.byref(res),
+                                        _ptr(hist))
         check(code)
         r = res.as_dict()
         if hist is not None:
@@ -232,6 +245,54 @@ class Matrix:
     def free(self):
         if self._h:
             lib.rbicg_matrix_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Precond:
+    """Split preconditioner M = L U ≈ A by Crout ILUT (rbicg_prec_ilut)."""
+
+    def __init__(self, ctx, indptr, indices, data, droptol):
+        self.ctx = ctx
+        dev = _is_torch(data)
+        if not dev:
+            indptr = np.ascontiguousarray(indptr, dtype=np.int32)
+            indices = np.ascontiguousarray(indices, dtype=np.int32)
+            data = np.ascontiguousarray(data)
+            if data.dtype not in (np.float64, np.complex128):
+                data = data.astype(np.float64)
+        self.n = int(len(indptr) - 1)
+        self.complex_ = _dtype_code(data) == C128
+        self._h = C.c_void_p()
+        ctx._children.append(weakref.ref(self))
+        check(lib.rbicg_prec_ilut(ctx._h, self.n, int(len(indices)), _ptr(indptr), _ptr(indices),
+                                  _ptr(data), C128 if self.complex_ else F64, float(droptol),
+                                  1 if dev else 0, C.byref(self._h)))
+
+    def factor(self, which):
+        """scipy CSR of L (which="L", unit diagonal included) or U."""
+        import scipy.sparse as sp
+        w = 0 if which == "L" else 1
+        nnz = C.c_int64()
+        check(lib.rbicg_prec_export(self._h, w, None, None, None, C.byref(nnz)))
+        rp = np.zeros(self.n + 1, np.int32)
+        ci = np.zeros(max(nnz.value, 1), np.int32)
+        v = np.zeros(max(nnz.value, 1), np.complex128 if self.complex_ else np.float64)
+        check(lib.rbicg_prec_export(self._h, w, _ptr(rp), _ptr(ci), _ptr(v), C.byref(nnz)))
+        F = sp.csr_matrix((v[:nnz.value], ci[:nnz.value], rp), shape=(self.n, self.n))
+        if which == "L":
+            F = (F + sp.identity(self.n, dtype=v.dtype, format="csr")).tocsr()
+        F.sort_indices()
+        return F
+
+    def free(self):
+        if self._h:
+            lib.rbicg_prec_free(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):

@@ -371,6 +371,16 @@ struct Solver {
     v.resize(sz);
     if (sz) cm->bcast_host(v.data(), sizeof(V) * sz, 0);
   }
+  // split preconditioner (NEXT-4, precond.cu): the loop runs on Â = L^{-1}AU^{-1}
+  const rbicg_prec *pc = nullptr;
+  PcWork pcw_main, pcw_side;   // scratch per stream (loop / cycle-end worker)
+  rbicg_mat eye;               // identity store: residual r = b - I (Â x) by k_resid
+  T *pfix = nullptr, *ptfix = nullptr;   // p_i, p~_i at fixed addresses for the captured Â launches
+  // C = A X on the loop's or the worker's stream (Â X with a preconditioner)
+  void spmm_op(bool adj, const T *X, T *Y, int k, cudaStream_t s) {
+    if (pc) pc_apply_block<T>(pc, M, adj, X, Y, k, s == ctx->stream ? pcw_main : pcw_side, s);
+    else launch_spmm<T>(adj ? M->AH : M->A, X, Y, k, s);
+  }
   std::vector<void *> owned;
   T *rring = nullptr, *rtring = nullptr, *p[2] = {}, *pt[2] = {}, *z = nullptr, *zt = nullptr;
   T *zp[2] = {}, *ztp[2] = {};   // fused iteration: (z_i, p_i) pairs by parity
@@ -471,6 +481,12 @@ struct Solver {
       for (void *q : owned) ws_free(q);
     }
     pinned_free(hst, sizeof(DevState<T>));
+    if (pc) {
+      pc_work_free(pcw_main);
+      pc_work_free(pcw_side);
+      free_devmat(eye.A);
+      free_devmat(eye.AH);
+    }
     if (tm)
       fprintf(stderr, "rbicg ~Solver join %.2f stream %.2f graph %.2f free %.2f ms\n", t1 - t0, t2 - t1,
               t3 - t2, now_ms() - t3);
@@ -599,6 +615,25 @@ struct Solver {
     const int nout = 3 * KMAX + 8 + 2 * KMAX;
     part = alloc((size_t)nout * ctx->grid_stream);
     memset(hst, 0, sizeof(DevState<T>));
+    if (pc) {
+      pc_work_alloc(pc, pcw_main);
+      pc_work_alloc(pc, pcw_side);
+      pfix = alloc(n);
+      ptfix = alloc(n);
+      std::vector<int32_t> rp(n + 1), ci(n);
+      std::vector<T> v(n, mk_re<T>(1.0));
+      for (int64_t i = 0; i <= n; ++i) rp[i] = (int32_t)i;
+      for (int64_t i = 0; i < n; ++i) ci[i] = (int32_t)i;
+      int32_t *drp = (int32_t *)ws_alloc(4 * (n + 1)), *dci = (int32_t *)ws_alloc(4 * n);
+      T *dv = (T *)ws_alloc(sizeof(T) * n);
+      RB_CUDA(cudaMemcpyAsync(drp, rp.data(), 4 * (n + 1), cudaMemcpyHostToDevice, ctx->stream));
+      RB_CUDA(cudaMemcpyAsync(dci, ci.data(), 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+      RB_CUDA(cudaMemcpyAsync(dv, v.data(), sizeof(T) * n, cudaMemcpyHostToDevice, ctx->stream));
+      build_matrix_local(ctx, n, drp, dci, dv, drp, dci, dv, m->dtype, &eye);
+      ws_free(drp);
+      ws_free(dci);
+      ws_free(dv);
+    }
     launches0 = g_launches.load();
     tmark("state+hist");
   }
@@ -660,7 +695,7 @@ struct Solver {
     // 1/σ_min and the ring-column form of Σ α_i p_i loses digits to
     // cancellation (C1 system 3: true residual 2.4e-10 against 8e-11 eager,
     // tol 1e-10), so x is updated every iteration as in Algorithm 2
-    lazy_x = getenv("RBICG_EAGER_X") == nullptr && cur.k == 0;
+    lazy_x = getenv("RBICG_EAGER_X") == nullptr && cur.k == 0 && !pc;
     la.lazy_x = lazy_x ? 1 : 0;
     la.pseg[0] = psegs[0];
     la.pseg[1] = psegs[1];
@@ -816,8 +851,8 @@ struct Solver {
         Uh = tmp.U;
         Uth = tmp.Ut;
       }
-      launch_spmm<T>(M->A, Uh, tmp.C, kin, ctx->stream);
-      launch_spmm<T>(M->AH, Uth, tmp.Ct, kin, ctx->stream);
+      spmm_op(false, Uh, tmp.C, kin, ctx->stream);
+      spmm_op(true, Uth, tmp.Ct, kin, ctx->stream);
       biorth(U, Ut, tmp.C, tmp.Ct, kin, cur, ctx->stream, ctx->comm.get());
     }
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -841,6 +876,15 @@ struct Solver {
   // C^*r~): the partitioned form exchanges the ghosts of x first and sums the
   // block results over the ranks before the scalar step.
   void residual(const T *xv, const T *xtv, T *r, T *rt, int coef) {
+    if (pc) {   // r = b - Â x: Â x by the operator, then k_resid against the identity
+      T *ax = (T *)pcw_main.u, *axt = (T *)pcw_main.v;
+      pc_apply_pair<T>(pc, M, xv, xtv, ax, axt, pcw_main, ctx->stream, nullptr);
+      LoopArgs<T> li = la;
+      li.A = eye.A;
+      li.AH = eye.AH;
+      launch_resid<T>(li, b, bt, ax, axt, r, rt, coef, ctx->stream);
+      return;
+    }
     if (dist) {
       halo_rows(const_cast<T *>(xv), 1, ctx->comm.get(), hsend, ctx->stream);
       halo_rows(const_cast<T *>(xtv), 1, ctx->comm.get(), hsend, ctx->stream);
@@ -950,7 +994,7 @@ struct Solver {
   }
   bool fused_ok() const {
     const bool off = getenv("RBICG_FUSED") && atoi(getenv("RBICG_FUSED")) == 0;   // per solve
-    return !off && zp[0] && la.k == 0 && la.staged && !la.split && lazy_x;
+    return !off && !pc && zp[0] && la.k == 0 && la.staged && !la.split && lazy_x;
   }
   void capture_graph() {
     if (dist && !ctx->comm->capturable()) {
@@ -973,6 +1017,11 @@ struct Solver {
       if (dist) {
         if (fused) dist_iteration_fused(ctx->stream);
         else dist_iteration(ctx->stream);
+      } else if (pc) {   // NEXT-4: p update, z = Â p (solves + SpMV pair), reductions, pass 2
+        launch_pc_pupdate<T>(la, pfix, ptfix, ctx->stream);
+        pc_apply_pair<T>(pc, M, pfix, ptfix, z, zt, pcw_main, ctx->stream, &st->done);
+        launch_pc_proj<T>(la, ctx->stream);
+        launch_pass2<T>(la, ctx->stream);
       } else if (fused) {
         launch_fused<T>(la, ctx->stream);
       } else {
@@ -1263,8 +1312,8 @@ struct Solver {
         // until the new U_j, C_j are formed, after this Gram)
         halo_rows(prev->U, kp, cms_pre, hsend_side, cs);
         halo_rows(prev->Ut, kp, cms_pre, hsend_side, cs);
-        launch_spmm<T>(M->A, prev->U, tmp.C, kp, cs);
-        launch_spmm<T>(M->AH, prev->Ut, tmp.Ct, kp, cs);
+        spmm_op(false, prev->U, tmp.C, kp, cs);
+        spmm_op(true, prev->Ut, tmp.Ct, kp, cs);
         for (int c = 0; c < kp; ++c) {
           X.push_back(col(tmp.Ct, c, kp));
           Y.push_back(col(tmp.C, c, kp));
@@ -1542,8 +1591,8 @@ struct Solver {
         Phase ph("cycle.spmm", cs);
         halo_rows(tmp.U, ksel, cms, hsend_side, cs);
         halo_rows(tmp.Ut, ksel, cms, hsend_side, cs);
-        launch_spmm<T>(M->A, tmp.U, tmp.C, ksel, cs);
-        launch_spmm<T>(M->AH, tmp.Ut, tmp.Ct, ksel, cs);
+        spmm_op(false, tmp.U, tmp.C, ksel, cs);
+        spmm_op(true, tmp.Ut, tmp.Ct, ksel, cs);
       }
       biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false, nullptr, nullptr,
              nullptr, &Fk, &Ftk);
@@ -1855,7 +1904,7 @@ int rbicg_recycle_export(const rbicg_rec *R, int32_t *k, void *U, void *Ut, int 
 template <typename T>
 static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void *bt, void *x,
                    void *xt, const void *xt_redraw, rbicg_rec *R, const rbicg_opts *opts,
-                   int on_device, rbicg_result *res, double *hist_out) {
+                   int on_device, rbicg_result *res, double *hist_out, const rbicg_prec *P = nullptr) {
   const double t_start = now_ms();
   static const bool timing = getenv("RBICG_TIMING") != nullptr;
   std::vector<std::pair<const char *, double>> marks;
@@ -1863,6 +1912,7 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
     if (timing) marks.emplace_back(nm, now_ms());
   };
   Solver<T> S;
+  S.pc = P;
   const int kin = R ? R->k : 0;
   S.setup(ctx, A, *opts, kin);
   mark("setup");
@@ -1873,6 +1923,20 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
   copy_in(S.bt, bt, vb, on_device, st);
   copy_in(S.x, x, vb, on_device, st);
   copy_in(S.xt, xt, vb, on_device, st);
+  // NEXT-4: the preconditioned pair -- b̂ = L^{-1}b, b̂~ = U^{-*}b~,
+  // x̂_{-1} = U x_{-1}, x̂~_{-1} = L^* x~_{-1} (precond.cu)
+  auto pc_map = [&](T *v, int which, bool solve) {
+    T *t = (T *)S.pcw_main.u;
+    if (solve) pc_solve_factor<T>(P, which, v, t, S.pcw_main, st);
+    else pc_mul_factor<T>(P, which, v, t, st);
+    RB_CUDA(cudaMemcpyAsync(v, t, vb, cudaMemcpyDeviceToDevice, st));
+  };
+  if (P) {
+    pc_map(S.b, 0, true);
+    pc_map(S.bt, 3, true);
+    pc_map(S.x, 1, false);
+    pc_map(S.xt, 2, false);
+  }
   S.zero_p0(st);
   // Step 1 + refresh
   S.refresh(R && kin > 0 ? (const T *)R->U : nullptr, R && kin > 0 ? (const T *)R->Ut : nullptr,
@@ -1885,6 +1949,7 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
   mark("init");
   if (S.hst->done == 1 && S.hst->status == RBICG_BREAKDOWN_SERIOUS && xt_redraw) {
     copy_in(S.xt, xt_redraw, vb, on_device, st);
+    if (P) pc_map(S.xt, 2, false);
     S.initial_projection();
   }
   const double t_loop0 = now_ms();
@@ -1969,6 +2034,10 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
   const DevState<T> fin = *S.hst;
   S.pull();
   const double tr = std::sqrt(S.hst->rn2 / S.hst->bn2), trt = std::sqrt(S.hst->rtn2 / S.hst->btn2);
+  if (P) {   // x = U^{-1} x̂, x~ = L^{-*} x̂~
+    pc_map(S.xo, 1, true);
+    pc_map(S.xto, 2, true);
+  }
   copy_out(x, S.xo, vb, on_device, st);
   copy_out(xt, S.xto, vb, on_device, st);
   // recycle space for the next system (Q18)
@@ -2059,6 +2128,77 @@ int rbicg_solve_dual(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const vo
       status = solve_t<double>(ctx, A, b, bt, x, xt, xt_redraw, R, o, on_device, res, hist);
     else
       status = solve_t<zc>(ctx, A, b, bt, x, xt, xt_redraw, R, o, on_device, res, hist);
+  });
+  return rc ? rc : status;
+}
+
+// ------------------------------------------------------------------ NEXT-4
+int rbicg_prec_ilut(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr, const int32_t *colind,
+                    const void *val, rbicg_dtype dtype, double droptol, int on_device, rbicg_prec **P) {
+  if (!ctx || !P || n <= 0 || nnz < 0 || n >= INT32_MAX || !(droptol >= 0)) return RBICG_EINVAL;
+  if (dtype != RBICG_F64 && dtype != RBICG_C128) return RBICG_EINVAL;
+  if (ctx->dist()) return RBICG_EINVAL;
+  return run_guarded([&] {
+    RB_CUDA(cudaSetDevice(ctx->device));
+    const size_t w = wbytes(dtype);
+    std::vector<int32_t> rp(n + 1), ci(std::max<int64_t>(nnz, 1));
+    std::vector<unsigned char> vv(w * std::max<int64_t>(nnz, 1));
+    auto get = [&](void *dst, const void *src, size_t bytes) {
+      if (!bytes) return;
+      if (on_device) RB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+      else memcpy(dst, src, bytes);
+    };
+    get(rp.data(), rowptr, 4 * (n + 1));
+    get(ci.data(), colind, 4 * nnz);
+    get(vv.data(), val, w * nnz);
+    auto *p = new rbicg_prec();
+    p->ctx = ctx;
+    p->n = n;
+    p->dtype = dtype;
+    p->droptol = droptol;
+    try {
+      pc_build(p, rp.data(), ci.data(), vv.data());
+    } catch (...) {
+      pc_free(p);
+      delete p;
+      throw;
+    }
+    *P = p;
+  });
+}
+
+int rbicg_prec_free(rbicg_prec *P) {
+  if (!P) return RBICG_EINVAL;
+  pc_free(P);
+  delete P;
+  return 0;
+}
+
+int rbicg_prec_export(const rbicg_prec *P, int which, int32_t *rowptr, int32_t *colind, void *val,
+                      int64_t *nnz) {
+  if (!P || !nnz || (which != 0 && which != 1)) return RBICG_EINVAL;
+  return run_guarded([&] {
+    RB_CUDA(cudaSetDevice(P->ctx->device));
+    pc_export(P, which, rowptr, colind, val, nnz);
+  });
+}
+
+int rbicg_solve_dual_pc(rbicg_ctx *ctx, const rbicg_mat *A, const rbicg_prec *P, const void *b, const void *bt,
+                        void *x, void *xt, const void *xt_redraw, rbicg_rec *R, const rbicg_opts *o,
+                        int on_device, rbicg_result *res, double *hist) {
+  if (!P) return rbicg_solve_dual(ctx, A, b, bt, x, xt, xt_redraw, R, o, on_device, res, hist);
+  if (!ctx || !A || !b || !bt || !x || !xt || !o || ctx->dist()) return RBICG_EINVAL;
+  if (P->n != A->n || P->dtype != A->dtype) return RBICG_EINVAL;
+  if (o->s < 2 || o->k < 0 || o->k > KMAX || o->max_itn < 0 || !(o->tol >= 0)) return RBICG_EINVAL;
+  if (R && (R->n != A->n || R->dtype != A->dtype || o->k > R->kmax)) return RBICG_EINVAL;
+  int status = 0;
+  int rc = run_guarded([&] {
+    RB_CUDA(cudaSetDevice(ctx->device));
+    order_after_user(ctx);
+    if (A->dtype == RBICG_F64)
+      status = solve_t<double>(ctx, A, b, bt, x, xt, xt_redraw, R, o, on_device, res, hist, P);
+    else
+      status = solve_t<zc>(ctx, A, b, bt, x, xt, xt_redraw, R, o, on_device, res, hist, P);
   });
   return rc ? rc : status;
 }

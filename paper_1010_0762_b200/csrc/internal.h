@@ -148,6 +148,34 @@ struct rbicg_mat {
   rbicg::HaloPlan halo;            // partitioned: ghost rows / send lists
 };
 
+namespace rbicg {
+// one triangular factor of the split preconditioner, device CSR (precond.cu)
+struct TriCSR {
+  int64_t n = 0, nnz = 0;
+  int32_t *rp = nullptr, *ci = nullptr;
+  void *v = nullptr;
+  int unit = 0;     // unit diagonal (not stored)
+  int upper = 0;    // solve backward (rows n-1 .. 0)
+  int32_t *order = nullptr;   // rows sorted by dependency level (the solve's claim order)
+  int levels = 0;
+};
+// scratch of the preconditioned operator (one per stream that applies it)
+struct PcWork {
+  int *flags = nullptr;
+  unsigned long long *counter = nullptr;
+  void *y = nullptr, *yt = nullptr, *q = nullptr, *qt = nullptr, *v = nullptr, *u = nullptr;
+};
+}  // namespace rbicg
+
+struct rbicg_prec {   // split preconditioner M = L U ≈ A (NEXT-4, precond.cu)
+  rbicg_ctx *ctx = nullptr;
+  int64_t n = 0;
+  rbicg_dtype dtype = RBICG_F64;
+  double droptol = 0;
+  rbicg::TriCSR L, U, LH, UH;   // L unit lower, U upper, L^* unit upper, U^* lower
+  int64_t nnzL = 0, nnzU = 0;
+};
+
 struct rbicg_rec {
   rbicg_ctx *ctx = nullptr;
   int64_t n = 0;
@@ -174,6 +202,25 @@ void build_partitioned(rbicg_ctx *ctx, int64_t nloc, int64_t nnz, const int32_t 
                        const int32_t *colind_global_d, const void *val_d, rbicg_dtype dt, rbicg_mat *M);
 void forget_partition_plan(const rbicg_ctx *ctx);
 
+// ---- precond.cu (split preconditioning, NEXT-4): Â = L^{-1} A U^{-1}
+void pc_build(rbicg_prec *P, const int32_t *rowptr_h, const int32_t *colind_h, const void *val_h);
+void pc_free(rbicg_prec *P);
+void pc_export(const rbicg_prec *P, int which, int32_t *rp, int32_t *ci, void *v, int64_t *nnz);
+void pc_work_alloc(const rbicg_prec *P, PcWork &w);
+void pc_work_free(PcWork &w);
+// z = Â p and z~ = Â^* p~ (either side may be null); `done`: skip when the
+// solver's loop state says finished/paused (nullable)
+template <typename T>
+void pc_apply_pair(const rbicg_prec *P, const rbicg_mat *M, const T *p, const T *pt, T *z, T *zt, PcWork &w,
+                   cudaStream_t s, const int *done);
+template <typename T>   // Y = Â X (adj: Â^* X), row-major n x k blocks
+void pc_apply_block(const rbicg_prec *P, const rbicg_mat *M, bool adj, const T *X, T *Y, int k, PcWork &w,
+                    cudaStream_t s);
+template <typename T>   // x = F^{-1} b, F = L, U, L^*, U^* for which = 0..3
+void pc_solve_factor(const rbicg_prec *P, int which, const T *b, T *x, PcWork &w, cudaStream_t s);
+template <typename T>   // y = F x
+void pc_mul_factor(const rbicg_prec *P, int which, const T *x, T *y, cudaStream_t s);
+
 // ---- kernels.cu (launch wrappers; all on ctx->stream)
 void prepare_kernels();        // one-time function attributes (not capturable)
 void prepare_block_kernels();
@@ -182,6 +229,8 @@ template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_pass2(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_fused(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_leader_fused(const LoopArgs<T> &a, cudaStream_t s);
+template <typename T> void launch_pc_pupdate(const LoopArgs<T> &a, T *pfix, T *ptfix, cudaStream_t s);
+template <typename T> void launch_pc_proj(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T>
 void launch_halo_fused(const LoopArgs<T> &a, const int32_t *idx, int64_t nsend, T *sendbuf,
                        const T *recvbuf, int64_t nghost, int pack, cudaStream_t s);

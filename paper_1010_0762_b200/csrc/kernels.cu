@@ -193,6 +193,94 @@ __global__ void __launch_bounds__(BS, MINB) k_pass2(LoopArgs<T> a, int staged) {
   p2_leader<T>(a, st, sn, sn.iter, s_fin);
 }
 
+// ============================================================== split-preconditioned form (NEXT-4)
+// Â = L^{-1} A U^{-1} is not a SELL matrix, so with a preconditioner the
+// iteration's first phase is split: k_pc_pupdate (p_i = r_{i-1} + β p_{i-1},
+// duals; also into fixed buffers for the captured operator launches), then
+// z_i = Â p_i, z~_i = Â^* p~_i (precond.cu: triangular solves and the SpMV
+// pair), then k_pc_proj (the pass-1 reduction without the SpMV: C~^*z, C^*z~,
+// C^*p~, p~^*z and the Q32 sums, the same leader), then pass 2 unchanged.
+template <typename T>
+__global__ void __launch_bounds__(BS) k_pc_pupdate(LoopArgs<T> a, T *pfix, T *ptfix) {
+  __shared__ Snap<T> sn;
+  snap_load(a.st, a.k, sn);
+  if (sn.done) return;
+  const int it = sn.iter;
+  const T beta = sn.beta, cb = conj(sn.beta);
+  const T *r = a.rring + (int64_t)(it % a.ring) * a.ldr;
+  const T *rt = a.rtring + (int64_t)(it % a.ring) * a.ldr;
+  const T *po = pcol(a, it), *pto = ptcol(a, it);
+  T *pn = pcol(a, it + 1), *ptn = ptcol(a, it + 1);
+  for (int64_t row = blockIdx.x * (int64_t)BS + threadIdx.x; row < a.n; row += (int64_t)gridDim.x * BS) {
+    const T v = mad(beta, po[row], r[row]);
+    const T vt = mad(cb, pto[row], rt[row]);
+    pn[row] = v;
+    ptn[row] = vt;
+    pfix[row] = v;
+    ptfix[row] = vt;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(BS) k_pc_proj(LoopArgs<T> a) {
+  __shared__ P1Scratch<T> sc;
+  __shared__ Snap<T> sn;
+  __shared__ T s_v[5 * BS];   // z, z~, p~, r, r~ rows of the tile
+  __shared__ T s_fin[5 * KMAX + 1];
+  __shared__ T s_w[BS / 32];
+  __shared__ T s_alpha;
+  __shared__ int s_last, s_ok;
+  DevState<T> *st = a.st;
+  snap_load(st, a.k, sn);
+  if (sn.done) return;
+  const int tid = threadIdx.x, k = a.k, it = sn.iter;
+  const int64_t n = a.n;
+  const T *r = a.rring + (int64_t)(it % a.ring) * a.ldr;
+  const T *rt = a.rtring + (int64_t)(it % a.ring) * a.ldr;
+  const T *ptn = ptcol(a, it + 1);
+  const int rstep = k > 0 ? BS / k : 0;
+  const int kt = rstep * k;
+  T a1 = zero<T>(), a2 = zero<T>(), a3 = zero<T>(), a4 = zero<T>(), a5 = zero<T>(), aptz = zero<T>();
+  const int64_t ntiles = (n + BS - 1) / BS;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * BS;
+    const int rows = (int)min((int64_t)BS, n - row0);
+    if (tid < rows) {
+      const int64_t row = row0 + tid;
+      const T z = a.z[row], zt = a.zt[row], pt = ptn[row];
+      s_v[tid] = z;
+      s_v[BS + tid] = zt;
+      s_v[2 * BS + tid] = pt;
+      s_v[3 * BS + tid] = r[row];
+      s_v[4 * BS + tid] = rt[row];
+      aptz = cmad(pt, z, aptz);   // (p~_i, z_i)
+    }
+    if (k > 0) {
+      __syncthreads();
+      if (tid < kt) {
+        const int nel = rows * k;
+        const T *__restrict__ Ct = a.Ct + row0 * k;
+        const T *__restrict__ C = a.C + row0 * k;
+        int lr = tid / k;
+        for (int e = tid; e < nel; e += kt, lr += rstep) {
+          const T ct = Ct[e], c = C[e];
+          a1 = cmad(ct, s_v[lr], a1);            // C~^* z
+          a2 = cmad(c, s_v[BS + lr], a2);        // C^* z~
+          a3 = cmad(c, s_v[2 * BS + lr], a3);    // C^* p~
+          a4 = cmad(ct, s_v[3 * BS + lr], a4);   // C~^* r   (Q32)
+          a5 = cmad(c, s_v[4 * BS + lr], a5);    // C^* r~
+        }
+      }
+      __syncthreads();
+    }
+  }
+  p1_partials<T>(a, sc, s_w, a1, a2, a3, a4, a5, aptz);
+  if (!last_block(&st->cnt[0], &s_last)) return;
+  final_reduce(a.part, p1_nsums(k), gridDim.x, s_fin);
+  if (tid == 0) st->cnt[0] = 0;
+  p1_leader<T>(a, st, sn, it, s_fin, &s_alpha, &s_ok);
+}
+
 // ============================================================== row-partitioned form
 // The scalar steps after the allreduce of the block sums (one block each);
 // every rank runs them on identical global sums, so the scalars stay
@@ -1105,6 +1193,14 @@ template <typename T> void launch_fused(const LoopArgs<T> &a0, cudaStream_t s) {
   count_launch();
 }
 
+template <typename T> void launch_pc_pupdate(const LoopArgs<T> &a, T *pfix, T *ptfix, cudaStream_t s) {
+  k_pc_pupdate<T><<<grid_for(a.n, a.G), BS, 0, s>>>(a, pfix, ptfix);
+  count_launch();
+}
+template <typename T> void launch_pc_proj(const LoopArgs<T> &a, cudaStream_t s) {
+  k_pc_proj<T><<<grid_for(a.n, a.G), BS, 0, s>>>(a);
+  count_launch();
+}
 template <typename T> void launch_leader_fused(const LoopArgs<T> &a, cudaStream_t s) {
   k_leader_fused<T><<<1, 32, 0, s>>>(a);
   count_launch();
@@ -1246,6 +1342,8 @@ void prepare_kernels() {
   template void launch_pass2<T>(const LoopArgs<T> &, cudaStream_t);                          \
   template void launch_fused<T>(const LoopArgs<T> &, cudaStream_t);                          \
   template void launch_leader_fused<T>(const LoopArgs<T> &, cudaStream_t);                   \
+  template void launch_pc_pupdate<T>(const LoopArgs<T> &, T *, T *, cudaStream_t);           \
+  template void launch_pc_proj<T>(const LoopArgs<T> &, cudaStream_t);                         \
   template void launch_halo_fused<T>(const LoopArgs<T> &, const int32_t *, int64_t, T *,      \
                                      const T *, int64_t, int, cudaStream_t);                 \
   template void launch_resid<T>(const LoopArgs<T> &, const T *, const T *, const T *,        \
