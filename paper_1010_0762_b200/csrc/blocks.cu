@@ -975,6 +975,17 @@ void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int 
   const int p = pin + (out_last ? 1 : 0);   // columns of M
   if (p <= 0) return;
   RB_CHECK(p <= KMAX, RBICG_EINVAL);
+  // the register-tiled multi-output GEMM (8 columns' loads in flight, two rows
+  // per thread): C3 cycle-end U_j = Φ_j W_j (41 -> 10 columns) 1.27 ms at
+  // 2.7 TB/s with the panel kernel below (RBICG_GEMM_PANELS_V1=1)
+  static const bool v1 = getenv("RBICG_GEMM_PANELS_V1") != nullptr;
+  if (!v1 && mX > 16) {   // (10 -> 10 columns: 0.33 ms here vs 0.41 ms multi-output)
+    std::vector<std::pair<T *, int>> outs{{out, pin}};
+    if (out_last) outs.emplace_back(out_last, 1);
+    gemm_multi<T>(X, M, outs, n, ctx, strm);
+    RB_CUDA(cudaStreamSynchronize(strm));
+    return;
+  }
   std::vector<T> hM((size_t)mX * p);
   for (size_t i = 0; i < hM.size(); ++i) {
     T v = zero<T>();
