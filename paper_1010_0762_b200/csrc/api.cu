@@ -396,7 +396,7 @@ struct Solver {
     T *U = nullptr, *Ut = nullptr, *C = nullptr, *Ct = nullptr;
     int k = 0;
     std::vector<double> d;
-  } cur, cand[1], tmp;   // cand keeps U, Ũ only (C, C~ are recomputed where needed)
+  } cur, cand[1], tmp;   // cand: U_j, Ũ_j and, when a cycle end formed them, C_j, C~_j
   int cand_cur = -1;
   // §4.4 (opts.pencil = 1): cycle j-1's small matrices for the recurrences of
   // cycle j -- G1 = Ψ~^*Ψ (m x m), G2 = Ψ~^*Φ (m x mphi), H, H~ (m x mphi)
@@ -461,6 +461,15 @@ struct Solver {
     if (B.U) return;
     B.U = alloc((size_t)nx * kmax);
     B.Ut = alloc((size_t)nx * kmax);
+  }
+  // the candidate's C_j = A U_j, C~_j (truncated like U_j): the next cycle
+  // end's C_{j-1} without an SpMM (allocated once a truncation keeps
+  // directions: never on C2/C5, whose spaces are truncated away)
+  bool cand_c_valid = false;
+  template <typename BB> void ensure_basis_c(BB &B) {
+    if (B.C) return;
+    B.C = alloc((size_t)n * kmax);
+    B.Ct = alloc((size_t)n * kmax);
   }
   ~Solver() {
     static const bool tm = getenv("RBICG_TIMING") != nullptr;
@@ -764,13 +773,11 @@ struct Solver {
     for (int a2 = 0; a2 < kin; ++a2)
       for (int b2 = 0; b2 < kin; ++b2) pairs.emplace_back(kin + a2, b2);
     std::vector<cplx> G((size_t)4 * kin * kin, 0.0), gv;
-    if (gv_in) {   // the Gram came out of the fused relation pass (k_relgram)
+    if (gv_in) {   // a Gram computed elsewhere
       gv = *gv_in;
     } else {
       Phase ph("biorth.gram", bs);
-      static const bool old_gram = getenv("RBICG_GRAM_PAIRS") != nullptr;
-      if (old_gram) gram_pairs<T>({C, Ct}, {kin, kin}, pairs, n, gv, ctx, bs);
-      else gram_cc<T>(C, Ct, kin, n, gv, ctx, bs);   // same outputs, register-tiled
+      gram_cc<T>(C, Ct, kin, n, gv, ctx, bs);   // register-tiled
     }
     sum_host(dist ? cm : nullptr, gv);   // partial Grams of the row blocks (C-4)
     {
@@ -835,6 +842,7 @@ struct Solver {
     gemm_panels<T>(cols_of(U), Fu, pk, n, out.U, ctx, bs);
     gemm_panels<T>(cols_of(Ut), Fut, pk, n, out.Ut, ctx, bs);
     if (with_c) {
+      ensure_basis_c(out);
       gemm_panels<T>(cols_of(C), Fu, pk, n, out.C, ctx, bs);
       gemm_panels<T>(cols_of(Ct), Fut, pk, n, out.Ct, ctx, bs);
     }
@@ -1171,9 +1179,6 @@ struct Solver {
       outs.push_back({x, 1});
       outst.push_back({xt, 1});
     }
-    if (gram_out && !with_u &&
-        relgram<T>(X, Xt, M, Mt, p, ksel, fl ? 1 : 0, n, x, xt, *gram_out, ctx, cs))
-      return;   // C_j, C~_j stayed on chip; the Gram is in *gram_out
     if (gram_out) gram_out->clear();
     gemm_multi<T>(X, M, outs, n, ctx, cs);
     gemm_multi<T>(Xt, Mt, outst, n, ctx, cs);
@@ -1312,15 +1317,22 @@ struct Solver {
           sy.push_back(1.0);
         }
       if (havePrev) {
-        // C_{j-1} = A U_{j-1}, C~_{j-1} = A^* Ũ_{j-1} into the temporaries (free
-        // until the new U_j, C_j are formed, after this Gram)
-        halo_rows(prev->U, kp, cms_pre, hsend_side, cs);
-        halo_rows(prev->Ut, kp, cms_pre, hsend_side, cs);
-        spmm_op(false, prev->U, tmp.C, kp, cs);
-        spmm_op(true, prev->Ut, tmp.Ct, kp, cs);
+        // C_{j-1} = A U_{j-1}, C~_{j-1} = A^* Ũ_{j-1}: kept from the last cycle
+        // end when it formed them, else into the temporaries (free until the
+        // new U_j, C_j are formed, after this Gram)
+        const T *Cp = tmp.C, *Ctp = tmp.Ct;
+        if (cand_c_valid && prev->C) {
+          Cp = prev->C;
+          Ctp = prev->Ct;
+        } else {
+          halo_rows(prev->U, kp, cms_pre, hsend_side, cs);
+          halo_rows(prev->Ut, kp, cms_pre, hsend_side, cs);
+          spmm_op(false, prev->U, tmp.C, kp, cs);
+          spmm_op(true, prev->Ut, tmp.Ct, kp, cs);
+        }
         for (int c = 0; c < kp; ++c) {
-          X.push_back(col(tmp.Ct, c, kp));
-          Y.push_back(col(tmp.C, c, kp));
+          X.push_back(col(Ctp, c, kp));
+          Y.push_back(col(Cp, c, kp));
           sx.push_back(1.0);
           sy.push_back(1.0);
         }
@@ -1528,13 +1540,9 @@ struct Solver {
         static const bool u_late = !getenv("RBICG_U_EARLY");
         const bool chk = getenv("RBICG_C_CHECK") && !dist;
         Phase ph("cycle.gemm_UCx", cs);
-        // (opt-in, RBICG_RELGRAM=1: the one-pass relation GEMM + Gram keeping C_j
-        // on chip measured slower -- C2 330 us vs 311 us for the two GEMMs and
-        // the Gram; C5 cycle ends 1.43 vs 1.00 s)
-        static const bool fuse_gram = getenv("RBICG_RELGRAM") != nullptr;
         std::vector<cplx> gvf;
         relation_gemm(rows, cols, top, Gam, Gamt, sel.W, sel.Wt, Wrow, Wtrow, ksel, sv, svt, fa, fb,
-                      lo, rec, cs, !u_late || chk, (u_late && !chk && !dist && fuse_gram) ? &gvf : nullptr);
+                      lo, rec, cs, !u_late || chk, nullptr);
         fa = fb = 0;
         if (getenv("RBICG_C_CHECK") && !dist) {   // debug: relation vs explicit SpMM
           RB_CUDA(cudaStreamSynchronize(cs));
@@ -1554,8 +1562,9 @@ struct Solver {
                   std::sqrt(dn / std::max(nn, 1e-300)));
         }
         if (!u_late || chk) {
-          biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false, nullptr, nullptr,
+          biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/!keep_fast, nullptr, nullptr,
                  nullptr, &Fk, &Ftk);
+          cand_c_valid = !keep_fast && out.k > 0;
         } else {
           std::vector<cplx> Fu, Fut;
           biorth(nullptr, nullptr, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false, &Fu, &Fut,
@@ -1577,7 +1586,18 @@ struct Solver {
             Phase phu("cycle.gemm_U", cs);
             gemm_multi<T>(Xv, Mu, {{out.U, pk}}, n, ctx, cs);
             gemm_multi<T>(Xvt, Mut, {{out.Ut, pk}}, n, ctx, cs);
+            if (!keep_fast) {   // C_j N_p for the next cycle end's C_{j-1}
+              ensure_basis_c(out);
+              std::vector<ColDesc> Xc, Xct;
+              for (int c = 0; c < ksel; ++c) {
+                Xc.push_back(col(tmp.C, c, ksel));
+                Xct.push_back(col(tmp.Ct, c, ksel));
+              }
+              gemm_panels<T>(Xc, Fu, pk, n, out.C, ctx, cs);
+              gemm_panels<T>(Xct, Fut, pk, n, out.Ct, ctx, cs);
+            }
           }
+          cand_c_valid = !keep_fast && out.k > 0;
         }
       } else {
       {
@@ -1598,8 +1618,9 @@ struct Solver {
         spmm_op(false, tmp.U, tmp.C, ksel, cs);
         spmm_op(true, tmp.Ut, tmp.Ct, ksel, cs);
       }
-      biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false, nullptr, nullptr,
+      biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/!keep_fast, nullptr, nullptr,
              nullptr, &Fk, &Ftk);
+      cand_c_valid = !keep_fast && out.k > 0;
       }
     }
     if (keep_fast) {   // U_j = Φ_j (W_j Fu): F = W Fu w.r.t. the normalised Φ_j

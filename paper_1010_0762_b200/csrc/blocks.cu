@@ -156,98 +156,6 @@ template <typename T> void launch_spmm(const DevMat &A, const T *X, T *Y, int k,
 }
 
 // ------------------------------------------------------------------ Gram
-constexpr int GT = 32;   // output tile edge
-template <typename T> struct GramRows { static constexpr int v = sizeof(T) == 8 ? 64 : 32; };
-
-template <typename T>
-__global__ void __launch_bounds__(256, 3) k_gram(const ColDesc *__restrict__ X, int mX,
-                                                 const ColDesc *__restrict__ Y, int mY, int64_t n,
-                                                 int64_t chunk, unsigned xrow_fast,
-                                                 unsigned yrow_fast, T *__restrict__ part) {
-  constexpr int GR = GramRows<T>::v;   // rows per smem sub-tile
-  constexpr int LD = GT + 2;           // padded row (keeps 16-byte alignment)
-  extern __shared__ __align__(16) unsigned char sm_raw[];
-  T *sbase = reinterpret_cast<T *>(sm_raw);   // 2 stages x (sx[GR][LD], sy[GR][LD])
-  constexpr int STAGE = 2 * GR * LD;
-  __shared__ ColDesc sdx[GT], sdy[GT];
-  const int tilesY = (mY + GT - 1) / GT;
-  const int txi = blockIdx.x / tilesY, tyi = blockIdx.x % tilesY;
-  const int tx0 = txi * GT, ty0 = tyi * GT;
-  const bool xr = (xrow_fast >> txi) & 1u, yr = (yrow_fast >> tyi) & 1u;
-  const int64_t r0 = (int64_t)blockIdx.y * chunk;
-  const int64_t r1 = min(n, r0 + chunk);
-  const int tid = threadIdx.x;
-  // 4 row groups x (8 x 8) threads, each thread a 4 x 4 register micro-tile
-  const int g = tid >> 6, t = tid & 63, ta = t >> 3, tb = t & 7;
-  T acc[4][4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) acc[u][v] = zero<T>();
-  constexpr int NQ = GR * GT / 256;
-  if (tid < GT) {
-    sdx[tid] = tx0 + tid < mX ? X[tx0 + tid] : ColDesc{nullptr, 0};
-    sdy[tid] = ty0 + tid < mY ? Y[ty0 + tid] : ColDesc{nullptr, 0};
-  }
-  __syncthreads();
-  auto load = [&](int64_t rb, int buf) {
-    T *sx = sbase + buf * STAGE, *sy = sx + GR * LD;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const int e = tid + 256 * q;
-      const int rr = xr ? e % GR : e / GT, cc = xr ? e / GR : e % GT;
-      const int64_t row = rb + rr;
-      const ColDesc d = sdx[cc];
-      const bool ok = d.p && row < r1;
-      const T *src = reinterpret_cast<const T *>(d.p ? d.p : (const void *)part);
-      cp_async_el(sx + rr * LD + cc, ok ? src + row * d.stride : src, ok);
-    }
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const int e = tid + 256 * q;
-      const int rr = yr ? e % GR : e / GT, cc = yr ? e / GR : e % GT;
-      const int64_t row = rb + rr;
-      const ColDesc d = sdy[cc];
-      const bool ok = d.p && row < r1;
-      const T *src = reinterpret_cast<const T *>(d.p ? d.p : (const void *)part);
-      cp_async_el(sy + rr * LD + cc, ok ? src + row * d.stride : src, ok);
-    }
-    cp_async_commit();
-  };
-  if (r0 < r1) load(r0, 0);
-  int buf = 0;
-  for (int64_t rb = r0; rb < r1; rb += GR, buf ^= 1) {
-    if (rb + GR < r1) load(rb + GR, buf ^ 1);
-    else cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const T *sx = sbase + buf * STAGE, *sy = sx + GR * LD;
-#pragma unroll 4
-    for (int rr = g; rr < GR; rr += 4) {
-      T xv[4], yv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        xv[u] = conj(sx[rr * LD + ta * 4 + u]);
-        yv[u] = sy[rr * LD + tb * 4 + u];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = mad(xv[u], yv[v], acc[u][v]);
-    }
-    __syncthreads();
-  }
-  // partial chunk index = 4 * chunk + group (fixed order in the reduction)
-  const int64_t pc = (int64_t)blockIdx.y * 4 + g;
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int a = tx0 + ta * 4 + u, bb = ty0 + tb * 4 + v;
-      if (a < mX && bb < mY) part[(pc * mX + a) * mY + bb] = acc[u][v];
-    }
-}
-
 // one warp per output entry: lanes sum chunks strided by 32, fixed shuffle tree
 template <typename T>
 __global__ void k_gram_reduce(const T *__restrict__ part, int nchunks, int mXY, T *__restrict__ G) {
@@ -257,52 +165,6 @@ __global__ void k_gram_reduce(const T *__restrict__ part, int nchunks, int mXY, 
   for (int c = l; c < nchunks; c += 32) s = add(s, part[(int64_t)c * mXY + w]);
   s = warp_sum(s);
   if (l == 0) G[w] = s;
-}
-
-template <typename T>
-static void gram_v1(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
-          std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t strm) {
-  const int mX = (int)X.size(), mY = (int)Y.size();
-  G.assign((size_t)mX * mY, cplx(0, 0));
-  if (mX == 0 || mY == 0) return;
-  const int tiles = ((mX + GT - 1) / GT) * ((mY + GT - 1) / GT);
-  // whole waves: tiles * nchunks a multiple of 3 resident blocks per SM
-  const int64_t slots = (int64_t)3 * sm_budget(ctx->nsm);
-  int64_t want = std::max<int64_t>(1, (n + 1023) / 1024);          // >= 1024 rows per chunk
-  int64_t waves = std::max<int64_t>(1, std::min<int64_t>(4, (want * tiles + slots - 1) / slots));
-  int nchunks = (int)std::max<int64_t>(1, (waves * slots) / tiles);
-  constexpr int GR = GramRows<T>::v;
-  const int64_t chunk = ((n + nchunks - 1) / nchunks + GR - 1) / GR * GR;
-  nchunks = (int)((n + chunk - 1) / chunk);
-  const size_t desc_bytes = sizeof(ColDesc) * (mX + mY);
-  const size_t part_bytes = sizeof(T) * (size_t)nchunks * 4 * mX * mY;
-  const size_t g_bytes = sizeof(T) * (size_t)mX * mY;
-  char *buf = (char *)ws_alloc(desc_bytes + part_bytes + g_bytes + 64);
-  ColDesc *dX = (ColDesc *)buf;
-  T *dpart = (T *)(buf + ((desc_bytes + 15) / 16) * 16);
-  T *dG = dpart + (size_t)nchunks * 4 * mX * mY;
-  std::vector<ColDesc> both(X);
-  both.insert(both.end(), Y.begin(), Y.end());
-  RB_CUDA(cudaMemcpyAsync(dX, both.data(), desc_bytes, cudaMemcpyHostToDevice, strm));
-  auto flags = [](const std::vector<ColDesc> &V) {
-    unsigned f = 0;
-    for (size_t g = 0; g * GT < V.size() && g < 32; ++g) {
-      bool vec = true;
-      for (size_t c = g * GT; c < std::min(V.size(), (g + 1) * GT); ++c) vec &= V[c].stride == 1;
-      if (vec) f |= 1u << g;
-    }
-    return f;
-  };
-  dim3 grid(tiles, nchunks);
-  const size_t gsm = sizeof(T) * 2 * 2 * GramRows<T>::v * (GT + 2);
-  k_gram<T><<<grid, 256, gsm, strm>>>(dX, mX, dX + mX, mY, n, chunk, flags(X), flags(Y), dpart);
-  k_gram_reduce<T><<<(mX * mY * 32 + 255) / 256, 256, 0, strm>>>(dpart, 4 * nchunks, mX * mY, dG);
-  count_launch(2);
-  std::vector<T> h((size_t)mX * mY);
-  RB_CUDA(cudaMemcpyAsync(h.data(), dG, g_bytes, cudaMemcpyDeviceToHost, strm));
-  RB_CUDA(cudaStreamSynchronize(strm));
-  ws_free(buf);
-  for (size_t i = 0; i < h.size(); ++i) G[i] = cplx(re(h[i]), im(h[i]));
 }
 
 // Register-tiled Gram (the pencil Grams of a cycle end: X = Ψ~ with 42..92
@@ -315,11 +177,9 @@ static void gram_v1(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y
 // fit (every cycle end of the BASELINE configs) -- and the inner loop does
 // MX*MY FMAs per MX + MY shared loads (fp64: 8 x 8, 64 FMAs per 16 loads).
 constexpr int G2R = 32;   // rows per stage
-template <typename T> struct Gram2Tile { static constexpr int mx = 8, my = 8; };
-template <> struct Gram2Tile<zc> { static constexpr int mx = 4, my = 4; };
 
 template <typename T, int MX, int MY>
-__global__ void __launch_bounds__(256, (MX * MY > 32 ? 1 : 2)) k_gram2(const ColDesc *__restrict__ X, int mX,
+__global__ void __launch_bounds__(256, (sizeof(T) * MX * MY > 256 ? 1 : 2)) k_gram2(const ColDesc *__restrict__ X, int mX,
                                                   const ColDesc *__restrict__ Y, int mY, int tX,
                                                   int tY, int64_t n, int64_t chunk,
                                                   T *__restrict__ part) {
@@ -410,14 +270,10 @@ __global__ void __launch_bounds__(256, (MX * MY > 32 ? 1 : 2)) k_gram2(const Col
     }
 }
 
-template <typename T>
-void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
-          std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t strm) {
+template <typename T, int MX, int MY>
+static void gram2_run(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
+                      std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t strm) {
   const int mX = (int)X.size(), mY = (int)Y.size();
-  G.assign((size_t)mX * mY, cplx(0, 0));
-  if (mX == 0 || mY == 0) return;
-  if (getenv("RBICG_GRAM_V1")) return gram_v1<T>(X, Y, n, G, ctx, strm);
-  constexpr int MX = Gram2Tile<T>::mx, MY = Gram2Tile<T>::my;
   // output tile: all of X x Y when its micro-tiles fit 256 threads, else
   // split Y (then X) into tiles that do
   int ntxA = (mX + MX - 1) / MX, ntyA = (mY + MY - 1) / MY;
@@ -441,7 +297,7 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   RB_CHECK(smem <= 200 * 1024, RBICG_EINVAL);
   // resident blocks per SM (1 for the 8 x 8 fp64 micro-tiles: 64 accumulators
   // per thread), whole waves of (tile, chunk) blocks
-  const int64_t slots = (int64_t)(MX * MY > 32 ? 2 : 4) * sm_budget(ctx->nsm);
+  const int64_t slots = (int64_t)(sizeof(T) * MX * MY > 256 ? 2 : 4) * sm_budget(ctx->nsm);
   int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4 * G2R - 1) / (4 * G2R),
                                                             (slots + tiles - 1) / tiles));
   const int64_t chunk = ((n + nchunks - 1) / nchunks + G2R - 1) / G2R * G2R;
@@ -467,131 +323,20 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   for (size_t i = 0; i < h.size(); ++i) G[i] = cplx(re(h[i]), im(h[i]));
 }
 
-// ------------------------------------------------------------------ sparse Gram
-// Selected entries G[a][b] = x_a^H x_b of the column concatenation of a few
-// compact row-major panels (column norms and C~^*C of the SVD step).  A row
-// sub-tile of every panel is one contiguous block: it is copied with 16-byte
-// cp.async (double-buffered) and each thread accumulates up to PPT pairs.
-constexpr int PPT = 6;
-constexpr int MAXP = 4;
-constexpr int GPR = 64;   // rows per double-buffered sub-tile of k_gram_pairs
-struct PanelSet {
-  const void *p[MAXP];
-  int nc[MAXP];     // columns (= leading dimension, compact panels)
-  int off[MAXP];    // smem offset (elements) of the panel's sub-tile in a stage
-  int np, width;    // panels, total columns
-};
 template <typename T>
-__global__ void __launch_bounds__(256) k_gram_pairs(PanelSet P, const int2 *__restrict__ pairs,
-                                                    int npairs, int64_t n, int64_t chunk,
-                                                    T *__restrict__ part) {
-  constexpr int GR = GPR;
-  extern __shared__ __align__(16) unsigned char sm_raw[];
-  T *sbase = reinterpret_cast<T *>(sm_raw);
-  const int stage = GR * P.width;
-  const int tid = threadIdx.x;
-  const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(n, r0 + chunk);
-  T acc[PPT];
-  int pa[PPT], pb[PPT], sa[PPT], sb[PPT];
-#pragma unroll
-  for (int q = 0; q < PPT; ++q) {
-    acc[q] = zero<T>();
-    const int pi = tid + 256 * q;
-    int a = pi < npairs ? pairs[pi].x : -1, b = pi < npairs ? pairs[pi].y : 0;
-    // map concatenated column -> (smem offset, row stride)
-    int oa = 0, ob = 0, wa = 1, wb = 1;
-    for (int p = 0, c0 = 0; p < P.np; c0 += P.nc[p], ++p) {
-      if (a >= c0 && a < c0 + P.nc[p]) { oa = P.off[p] + (a - c0); wa = P.nc[p]; }
-      if (b >= c0 && b < c0 + P.nc[p]) { ob = P.off[p] + (b - c0); wb = P.nc[p]; }
-    }
-    pa[q] = a < 0 ? -1 : oa;
-    pb[q] = ob;
-    sa[q] = wa;
-    sb[q] = wb;
+void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
+          std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t strm) {
+  const int mX = (int)X.size(), mY = (int)Y.size();
+  G.assign((size_t)mX * mY, cplx(0, 0));
+  if (mX == 0 || mY == 0) return;
+  static const int var = getenv("RBICG_GRAM2") ? atoi(getenv("RBICG_GRAM2")) : 0;
+  if constexpr (sizeof(T) == 16) {
+    gram2_run<T, 4, 4>(X, Y, n, G, ctx, strm);
+  } else {
+    if (var == 48) return gram2_run<T, 4, 8>(X, Y, n, G, ctx, strm);
+    if (var == 44) return gram2_run<T, 4, 4>(X, Y, n, G, ctx, strm);
+    gram2_run<T, 8, 8>(X, Y, n, G, ctx, strm);
   }
-  auto load = [&](int64_t rb, int buf) {
-    T *s = sbase + buf * stage;
-    const int rows = (int)min((int64_t)GR, r1 - rb);
-    for (int p = 0; p < P.np; ++p) {
-      const T *src = reinterpret_cast<const T *>(P.p[p]) + rb * P.nc[p];
-      T *dst = s + P.off[p];
-      const int ne = GR * P.nc[p], nv = rows * P.nc[p];
-      constexpr int PER = 16 / sizeof(T);   // elements per 16-byte copy
-      for (int e = tid * PER; e < ne; e += 256 * PER) {
-        // bytes actually read (the rest of the 16-byte chunk is zero filled)
-        const int valid = max(0, min(PER, nv - e)) * (int)sizeof(T);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst + e)),
-                     "l"(valid ? src + e : src), "r"(valid)
-                     : "memory");
-      }
-    }
-    cp_async_commit();
-  };
-  if (r0 < r1) load(r0, 0);
-  int buf = 0;
-  for (int64_t rb = r0; rb < r1; rb += GR, buf ^= 1) {
-    if (rb + GR < r1) load(rb + GR, buf ^ 1);
-    else cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const T *s = sbase + buf * stage;
-    const int rows = (int)min((int64_t)GR, r1 - rb);
-#pragma unroll
-    for (int q = 0; q < PPT; ++q) {
-      if (pa[q] < 0) continue;
-      T acc_q = acc[q];
-      for (int rr = 0; rr < rows; ++rr)
-        acc_q = mad(conj(s[pa[q] + rr * sa[q]]), s[pb[q] + rr * sb[q]], acc_q);
-      acc[q] = acc_q;
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int q = 0; q < PPT; ++q) {
-    const int pi = tid + 256 * q;
-    if (pi < npairs) part[(int64_t)blockIdx.x * npairs + pi] = acc[q];
-  }
-}
-
-template <typename T>
-void gram_pairs(const std::vector<const T *> &panels, const std::vector<int> &ncols,
-                const std::vector<std::pair<int, int>> &pairs, int64_t n, std::vector<cplx> &out,
-                rbicg_ctx *ctx, cudaStream_t strm) {
-  const int np = (int)pairs.size();
-  out.assign(np, cplx(0, 0));
-  if (!np) return;
-  RB_CHECK(np <= 256 * PPT && panels.size() <= (size_t)MAXP, RBICG_EINVAL);
-  PanelSet P{};
-  P.np = (int)panels.size();
-  int w = 0;
-  for (int p = 0; p < P.np; ++p) {
-    P.p[p] = panels[p];
-    P.nc[p] = ncols[p];
-    P.off[p] = GPR * w;
-    w += ncols[p];
-  }
-  P.width = w;
-  const size_t sm = 2 * sizeof(T) * GPR * (size_t)w;
-  RB_CHECK(sm <= 160 * 1024, RBICG_EINVAL);
-  const int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, 4 * sm_budget(ctx->nsm)));
-  const int64_t chunk = ((n + nchunks - 1) / nchunks + GPR - 1) / GPR * GPR;
-  const int nb = (int)((n + chunk - 1) / chunk);
-  std::vector<int2> hp(np);
-  for (int i = 0; i < np; ++i) hp[i] = make_int2(pairs[i].first, pairs[i].second);
-  const size_t pb = sizeof(int2) * np, off2 = (pb + 15) / 16 * 16;
-  char *buf = (char *)ws_alloc(off2 + sizeof(T) * ((size_t)nb * np + np) + 64);
-  int2 *dp = (int2 *)buf;
-  T *dpart = (T *)(buf + off2);
-  T *dG = dpart + (size_t)nb * np;
-  RB_CUDA(cudaMemcpyAsync(dp, hp.data(), pb, cudaMemcpyHostToDevice, strm));
-  k_gram_pairs<T><<<nb, 256, sm, strm>>>(P, dp, np, n, chunk, dpart);
-  k_gram_reduce<T><<<(np * 32 + 255) / 256, 256, 0, strm>>>(dpart, nb, np, dG);
-  count_launch(2);
-  std::vector<T> h(np);
-  RB_CUDA(cudaMemcpyAsync(h.data(), dG, sizeof(T) * np, cudaMemcpyDeviceToHost, strm));
-  RB_CUDA(cudaStreamSynchronize(strm));
-  ws_free(buf);
-  for (int i = 0; i < np; ++i) out[i] = cplx(re(h[i]), im(h[i]));
 }
 
 // ------------------------------------------------------------------ C~^*C Gram
@@ -732,191 +477,6 @@ void gram_cc(const T *C, const T *Ct, int k, int64_t n, std::vector<cplx> &out, 
   RB_CUDA(cudaStreamSynchronize(strm));
   ws_free(buf);
   for (int i = 0; i < np; ++i) out[i] = cplx(re(h[i]), im(h[i]));
-}
-
-// ------------------------------------------------------------------ relation GEMM + Gram
-// The T_j-pencil cycle end without storing C_j: one pass over the Υ_j, Ῡ_j
-// ring columns forms, per 256-row tile, the rows of C_j = Υ_j M and
-// C~_j = Ῡ_j M~ (and the lazy-x flush column, written to x, x~), keeps them in
-// shared memory only, and accumulates the bi-orthogonality Gram (|c_j|^2,
-// |c~_j|^2, c~_a^* c_b) with 4 x 4 register tiles as k_gram_cc does.  C_j is
-// never written: with p = 0 after the truncation (every C2/C3/C5 cycle) it is
-// not needed, and with p > 0 U_j N_p is formed from the V_j columns and the
-// next system's refresh computes C = A U.
-template <typename T, int PB>
-__global__ void __launch_bounds__(256, 2) k_relgram(const ColDesc *__restrict__ X, const ColDesc *__restrict__ Xt,
-                                                    int mX, const T *__restrict__ M, const T *__restrict__ Mt,
-                                                    int p, int k, int fl, int64_t n, T *__restrict__ xo,
-                                                    T *__restrict__ xto, T *__restrict__ part) {
-  constexpr int AU = PB <= 12 ? 8 : 4;
-  extern __shared__ __align__(16) unsigned char sm_raw[];
-  T *sM = reinterpret_cast<T *>(sm_raw);   // [2][mX][PB]
-  T *sG = sM + (size_t)2 * mX * PB;        // [16][256]: each thread's Gram tile (kept out of registers)
-  T *sC = sG + (size_t)16 * 256;           // [256][k + 1], then C~ [256][k + 1]
-  const int ld = k + 1;
-  T *sCt = sC + (size_t)256 * ld;
-  ColDesc *sX = reinterpret_cast<ColDesc *>(sCt + (size_t)256 * ld);   // [2][mX]
-  const int tid = threadIdx.x;
-  for (int e = tid; e < 2 * mX * PB; e += 256) {
-    const int side = e / (mX * PB), r = e % (mX * PB), a = r / PB, c = r % PB;
-    sM[e] = c < p ? (side ? Mt : M)[a * p + c] : zero<T>();
-  }
-  for (int e = tid; e < 2 * mX; e += 256) sX[e] = e < mX ? X[e] : Xt[e - mX];
-  const int kb = (k + 3) / 4, W = kb * kb + 2 * kb, R = max(1, 256 / W);
-  const int item = tid % W, grp = tid / W;
-  const bool act = grp < R;
-  const bool tile = item < kb * kb;
-  const int A = tile ? item / kb : 0, B = tile ? item % kb : (item - kb * kb) % kb;
-  const int nside = tile ? 0 : (item - kb * kb) / kb;
-  for (int e = 0; e < 16; ++e) sG[e * 256 + tid] = zero<T>();
-  __syncthreads();
-  const int64_t ntiles = (n + 255) / 256;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t row = t * 256 + tid;
-    const bool ok = row < n;
-    const int rows = (int)min((int64_t)256, n - t * 256);
-    for (int side = 0; side < 2; ++side) {
-      const ColDesc *cx = sX + side * mX;
-      const T *mm = sM + (size_t)side * mX * PB;
-      T acc[PB];
-#pragma unroll
-      for (int c = 0; c < PB; ++c) acc[c] = zero<T>();
-      int a = 0;
-      for (; a + AU <= mX; a += AU) {
-        T xv[AU];
-#pragma unroll
-        for (int u = 0; u < AU; ++u)
-          xv[u] = ok ? reinterpret_cast<const T *>(cx[a + u].p)[row * cx[a + u].stride] : zero<T>();
-#pragma unroll
-        for (int u = 0; u < AU; ++u)
-#pragma unroll
-          for (int c = 0; c < PB; ++c) acc[c] = mad(xv[u], mm[(a + u) * PB + c], acc[c]);
-      }
-      for (; a < mX; ++a) {
-        const T xv = ok ? reinterpret_cast<const T *>(cx[a].p)[row * cx[a].stride] : zero<T>();
-#pragma unroll
-        for (int c = 0; c < PB; ++c) acc[c] = mad(xv, mm[a * PB + c], acc[c]);
-      }
-      T *dst = side ? sCt : sC;
-#pragma unroll
-      for (int c = 0; c < PB; ++c)
-        if (c < k) dst[tid * ld + c] = ok ? acc[c] : zero<T>();
-      if (fl && ok) {
-        T fx = zero<T>();
-#pragma unroll
-        for (int c = 0; c < PB; ++c)
-          if (c == k) fx = acc[c];
-        (side ? xto : xo)[row] = fx;
-      }
-    }
-    __syncthreads();
-    if (act) {
-      T g[4][4];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) g[e / 4][e % 4] = sG[e * 256 + tid];
-      if (tile) {
-        for (int rr = grp; rr < rows; rr += R) {
-          T av[4], bv[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int ca = 4 * A + i, cb = 4 * B + i;
-            av[i] = ca < k ? sCt[rr * ld + ca] : zero<T>();
-            bv[i] = cb < k ? sC[rr * ld + cb] : zero<T>();
-          }
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) g[i][j] = cmad(av[i], bv[j], g[i][j]);
-        }
-      } else {
-        const T *sx = nside ? sCt : sC;
-        for (int rr = grp; rr < rows; rr += R) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int cj = 4 * B + j;
-            const T v = cj < k ? sx[rr * ld + cj] : zero<T>();
-            g[0][j] = cmad(v, v, g[0][j]);
-          }
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < 16; ++e) sG[e * 256 + tid] = g[e / 4][e % 4];
-    }
-    __syncthreads();
-  }
-  T *red = sC;   // >= R * W * 16 elements (checked by the host)
-  if (act)
-#pragma unroll
-    for (int e = 0; e < 16; ++e) red[((size_t)grp * W + item) * 16 + e] = sG[e * 256 + tid];
-  __syncthreads();
-  const int np = 2 * k + k * k;
-  for (int o = tid; o < np; o += 256) {
-    int it, e;
-    if (o < k) {
-      it = kb * kb + o / 4;
-      e = o % 4;
-    } else if (o < 2 * k) {
-      it = kb * kb + kb + (o - k) / 4;
-      e = (o - k) % 4;
-    } else {
-      const int a2 = (o - 2 * k) / k, b2 = (o - 2 * k) % k;
-      it = (a2 / 4) * kb + b2 / 4;
-      e = (a2 % 4) * 4 + b2 % 4;
-    }
-    T sum = zero<T>();
-    for (int gg = 0; gg < R; ++gg) sum = add(sum, red[((size_t)gg * W + it) * 16 + e]);
-    part[(int64_t)blockIdx.x * np + o] = sum;
-  }
-}
-
-template <typename T>
-bool relgram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Xt, const std::vector<cplx> &M,
-             const std::vector<cplx> &Mt, int p, int k, int fl, int64_t n, T *x, T *xt,
-             std::vector<cplx> &gv, rbicg_ctx *ctx, cudaStream_t strm) {
-  const int mX = (int)X.size();
-  const int PB = p <= 12 ? 12 : (p <= 24 && sizeof(T) == 8 ? 24 : 0);
-  if (!PB || (int)Xt.size() != mX || k < 1) return false;   // caller: GEMM + Gram
-  const int kb = (k + 3) / 4, W = kb * kb + 2 * kb, R = std::max(1, 256 / W);
-  const size_t ctile = (size_t)2 * 256 * (k + 1);
-  const size_t sm = sizeof(T) * ((size_t)2 * mX * PB + 16 * 256 + std::max(ctile, (size_t)16 * W * R)) +
-                    sizeof(ColDesc) * 2 * mX + 16;
-  if (sm > 200 * 1024) return false;
-  const int np = 2 * k + k * k;
-  std::vector<T> hM((size_t)2 * mX * p);
-  for (size_t i = 0; i < (size_t)mX * p; ++i) {
-    for (int side = 0; side < 2; ++side) {
-      T v = zero<T>();
-      const cplx c = side ? Mt[i] : M[i];
-      reinterpret_cast<double *>(&v)[0] = c.real();
-      if (sizeof(T) == 16) reinterpret_cast<double *>(&v)[1] = c.imag();
-      hM[side * (size_t)mX * p + i] = v;
-    }
-  }
-  auto kern = PB == 12 ? k_relgram<T, 12> : k_relgram<T, 24>;
-  int per = 1;
-  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, sm));
-  const int64_t tiles = (n + 255) / 256;
-  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)std::max(1, per) * sm_budget(ctx->nsm)));
-  const size_t db = sizeof(ColDesc) * 2 * mX, mb = sizeof(T) * hM.size();
-  char *buf = (char *)ws_alloc(db + 16 + mb + 16 + sizeof(T) * ((size_t)nb * np + np) + 64);
-  ColDesc *dX = (ColDesc *)buf;
-  T *dM = (T *)(buf + (db + 15) / 16 * 16);
-  T *dpart = (T *)((char *)dM + (mb + 15) / 16 * 16);
-  T *dG = dpart + (size_t)nb * np;
-  std::vector<ColDesc> XX(X);
-  XX.insert(XX.end(), Xt.begin(), Xt.end());
-  RB_CUDA(cudaMemcpyAsync(dX, XX.data(), db, cudaMemcpyHostToDevice, strm));
-  RB_CUDA(cudaMemcpyAsync(dM, hM.data(), mb, cudaMemcpyHostToDevice, strm));
-  kern<<<nb, 256, sm, strm>>>(dX, dX + mX, mX, dM, dM + (size_t)mX * p, p, k, fl, n, x, xt, dpart);
-  k_gram_reduce<T><<<(np * 32 + 255) / 256, 256, 0, strm>>>(dpart, nb, np, dG);
-  count_launch(2);
-  std::vector<T> h(np);
-  RB_CUDA(cudaMemcpyAsync(h.data(), dG, sizeof(T) * np, cudaMemcpyDeviceToHost, strm));
-  RB_CUDA(cudaStreamSynchronize(strm));
-  ws_free(buf);
-  gv.resize(np);
-  for (int i = 0; i < np; ++i) gv[i] = cplx(re(h[i]), im(h[i]));
-  return true;
 }
 
 // ------------------------------------------------------------------ panels x M
@@ -1128,147 +688,6 @@ __global__ void __launch_bounds__(256, (gm_minb<T, PB, RX>())) k_gemm_multi(cons
 // memory by 1-D bulk copies (cp.async.bulk + mbarrier), double buffered, so
 // HBM requests stay in flight while the FMAs of the previous tile run.  The
 // ragged last tile is filled by ordinary loads.
-template <typename T> constexpr int gm_rows() { return sizeof(T) == 8 ? 256 : 128; }
-template <typename T>
-__host__ __device__ inline size_t gm_stage_bytes(int mX) {
-  return (size_t)mX * gm_rows<T>() * sizeof(T);
-}
-template <typename T, int PB, int RPT>
-__global__ void __launch_bounds__(gm_rows<T>() / RPT, 1) k_gemm_multi_tma(const ColDesc *__restrict__ X, int mX,
-                                                                  const T *__restrict__ M, int p,
-                                                                  int64_t n, OutSegs O, int nst,
-                                                                  int own_stg) {
-  constexpr int TR = gm_rows<T>();
-  constexpr int GM_THREADS = TR / RPT;
-  extern __shared__ __align__(16) unsigned char sm_raw[];
-  __shared__ __align__(8) uint64_t bars[2];
-  __shared__ int s_cb[PB], s_cs[PB], s_off[4];   // output column -> staging offset, row stride
-  T *stage0 = reinterpret_cast<T *>(sm_raw);   // nst x [mX][TR]
-  T *sM = stage0 + (size_t)nst * mX * TR;      // [mX][PB]
-  ColDesc *sX = reinterpret_cast<ColDesc *>(sM + (size_t)mX * PB);
-  // output staging: the consumed input stage when it is large enough, else
-  // its own region; segment sg is a row-major TR x nc block (one bulk store)
-  T *sO = reinterpret_cast<T *>(reinterpret_cast<unsigned char *>(sX) +
-                                ((sizeof(ColDesc) * mX + 15) / 16) * 16);
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    int off = 0, c0 = 0;
-    for (int sg = 0; sg < O.ns; ++sg) {
-      s_off[sg] = off;
-      for (int c = 0; c < O.nc[sg]; ++c) {
-        s_cb[c0 + c] = off + c;
-        s_cs[c0 + c] = O.nc[sg];
-      }
-      off += TR * O.nc[sg];
-      c0 += O.nc[sg];
-    }
-    for (int c = c0; c < PB; ++c) s_cb[c] = s_cs[c] = 0;
-  }
-  for (int e = tid; e < mX * PB; e += GM_THREADS) {
-    const int a = e / PB, c = e % PB;
-    sM[e] = c < p ? M[a * p + c] : zero<T>();
-  }
-  for (int e = tid; e < mX; e += GM_THREADS) sX[e] = X[e];
-  if (tid == 0) {
-    for (int q = 0; q < nst; ++q) mbar_init(&bars[q], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const int64_t ntiles = (n + TR - 1) / TR;
-  const int64_t nfull = n / TR;   // tiles [0, nfull) are whole
-  auto issue = [&](int64_t t, int q) {
-    if (t >= nfull) return;   // ragged tail: ordinary loads at use
-    T *dst = stage0 + (size_t)q * mX * TR;
-    mbar_expect_tx(&bars[q], (uint32_t)(mX * TR * sizeof(T)));
-    for (int a = 0; a < mX; ++a)
-      tma_load_1d(dst + (size_t)a * TR, reinterpret_cast<const T *>(sX[a].p) + t * TR,
-                  (uint32_t)(TR * sizeof(T)), &bars[q]);
-  };
-  if (tid == 0)
-    for (int q = 0; q < nst; ++q) issue(blockIdx.x + (int64_t)q * gridDim.x, q);
-  uint32_t phases = 0;   // bit q: parity of stage q
-  int q = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    T *sx = stage0 + (size_t)q * mX * TR;
-    if (t < nfull) {
-      mbar_wait(&bars[q], (phases >> q) & 1u);
-      phases ^= 1u << q;
-    } else {
-      const int64_t r0 = t * TR;
-      for (int e = tid; e < mX * TR; e += GM_THREADS) {
-        const int a = e / TR, rr = e % TR;
-        sx[e] = r0 + rr < n ? reinterpret_cast<const T *>(sX[a].p)[r0 + rr] : zero<T>();
-      }
-      __syncthreads();
-    }
-    T acc[RPT][PB];
-#pragma unroll
-    for (int r = 0; r < RPT; ++r)
-#pragma unroll
-      for (int c = 0; c < PB; ++c) acc[r][c] = zero<T>();
-#pragma unroll 2
-    for (int a = 0; a < mX; ++a) {
-      T xv[RPT];
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) xv[r] = sx[(size_t)a * TR + r * GM_THREADS + tid];
-      const MPair<T> *mp = reinterpret_cast<const MPair<T> *>(sM + a * PB);
-#pragma unroll
-      for (int c2 = 0; c2 < PB / 2; ++c2) {
-        const MPair<T> m = mp[c2];
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          acc[r][2 * c2] = mad(xv[r], m.a, acc[r][2 * c2]);
-          acc[r][2 * c2 + 1] = mad(xv[r], m.b, acc[r][2 * c2 + 1]);
-        }
-      }
-    }
-    __syncthreads();   // stage q fully read
-    if (t < nfull) {
-      // stage the tile's outputs in shared memory, one bulk store per
-      // segment, then refill stage q once the stores have read it
-      T *stg = own_stg ? sO : sx;
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        const int lr = r * GM_THREADS + tid;
-#pragma unroll
-        for (int c = 0; c < PB; ++c)
-          if (c < p) stg[s_cb[c] + lr * s_cs[c]] = acc[r][c];
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
-      if (tid == 0) {
-        for (int sg = 0; sg < O.ns; ++sg) {
-          T *dst = reinterpret_cast<T *>(O.p[sg]) + t * TR * O.nc[sg];
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                       "r"(smem_u32(stg + s_off[sg])), "r"((uint32_t)(TR * O.nc[sg] * sizeof(T)))
-                       : "memory");
-        }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        issue(t + (int64_t)nst * gridDim.x, q);
-      }
-      q = (q + 1 == nst) ? 0 : q + 1;
-      continue;
-    }
-    q = (q + 1 == nst) ? 0 : q + 1;
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      const int64_t row = t * TR + r * GM_THREADS + tid;
-      if (row >= n) continue;
-      int c0 = 0;
-      for (int sg = 0; sg < O.ns; ++sg) {
-        T *out = reinterpret_cast<T *>(O.p[sg]);
-        const int nc = O.nc[sg];
-#pragma unroll
-        for (int c = 0; c < PB; ++c)
-          if (c >= c0 && c < c0 + nc) out[row * nc + (c - c0)] = acc[r][c];
-        c0 += nc;
-      }
-    }
-  }
-  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
 template <typename T>
 void gemm_multi(const std::vector<ColDesc> &X, const std::vector<cplx> &M,
                 const std::vector<std::pair<T *, int>> &outs, int64_t n, rbicg_ctx *ctx,
@@ -1318,42 +737,6 @@ void gemm_multi(const std::vector<ColDesc> &X, const std::vector<cplx> &M,
   T *dM = (T *)(buf + ((desc_bytes + 15) / 16) * 16);
   RB_CUDA(cudaMemcpyAsync(dX, X.data(), desc_bytes, cudaMemcpyHostToDevice, strm));
   RB_CUDA(cudaMemcpyAsync(dM, hM.data(), sizeof(T) * hM.size(), cudaMemcpyHostToDevice, strm));
-  // staged form: every column unit-stride and 16-byte aligned, two stages fit
-  // (opt-in, RBICG_GEMM_TMA=1: measured 232 us vs 209 us for the register
-  // form on the C2 relation GEMM -- shared-memory bound at 8 warps/SM)
-  bool tma = getenv("RBICG_GEMM_TMA") != nullptr;
-  for (int a = 0; a < mX && tma; ++a)
-    tma = X[a].stride == 1 && ((uintptr_t)X[a].p & 15) == 0;
-  static const int g_rpt = getenv("RBICG_GEMM_RPT") ? atoi(getenv("RBICG_GEMM_RPT")) : 1;
-  // output staging in the consumed stage when it holds the tile's p columns
-  const int own_stg = mX < p ? 1 : 0;
-  const size_t stg_bytes = own_stg ? (size_t)gm_rows<T>() * p * sizeof(T) : 0;
-  auto go_tma = [&](auto kern, int PB, int rpt) {
-    const size_t fixed = sizeof(T) * (size_t)mX * PB + ((sizeof(ColDesc) * mX + 15) / 16) * 16 + stg_bytes;
-    const int nst = fixed + 2 * gm_stage_bytes<T>(mX) <= 220 * 1024 ? 2 : 1;
-    const size_t sm = fixed + nst * gm_stage_bytes<T>(mX);
-    const int64_t tiles = (n + gm_rows<T>() - 1) / gm_rows<T>();
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, sm_budget(ctx->nsm)));
-    kern<<<grid, gm_rows<T>() / rpt, sm, strm>>>(dX, mX, dM, p, n, O, nst, own_stg);
-  };
-  bool seg_ok = true;   // bulk stores: 16-byte aligned segment bases
-  for (size_t q2 = 0; q2 < outs.size(); ++q2) seg_ok = seg_ok && ((uintptr_t)outs[q2].first & 15) == 0;
-  if (tma && seg_ok &&
-      sizeof(ColDesc) * mX + 16 + sizeof(T) * (size_t)mX * 32 + stg_bytes + gm_stage_bytes<T>(mX) <= 220 * 1024) {
-    if (g_rpt == 2 && sizeof(T) == 8) {
-      if (p <= 12) go_tma(k_gemm_multi_tma<T, 12, 2>, 12, 2);
-      else if (p <= 24) go_tma(k_gemm_multi_tma<T, 24, 2>, 24, 2);
-      else go_tma(k_gemm_multi_tma<T, 32, 2>, 32, 2);
-    } else {
-      if (p <= 12) go_tma(k_gemm_multi_tma<T, 12, 1>, 12, 1);
-      else if (p <= 24) go_tma(k_gemm_multi_tma<T, 24, 1>, 24, 1);
-      else go_tma(k_gemm_multi_tma<T, 32, 1>, 32, 1);
-    }
-    count_launch();
-    RB_CUDA(cudaStreamSynchronize(strm));
-    ws_free(buf);
-    return;
-  }
   auto go = [&](auto kern, int PB, int rpt) {
     const size_t sm = sizeof(T) * (size_t)mX * PB + sizeof(ColDesc) * mX;
     RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
@@ -1380,16 +763,8 @@ void gemm_multi(const std::vector<ColDesc> &X, const std::vector<cplx> &M,
 }
 
 void prepare_block_kernels() {
-  RB_CUDA(cudaFuncSetAttribute(k_gram<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-  RB_CUDA(cudaFuncSetAttribute(k_gram<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-  RB_CUDA(cudaFuncSetAttribute(k_gram_pairs<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-  RB_CUDA(cudaFuncSetAttribute(k_gram_pairs<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_gram_cc<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_gram_cc<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-  RB_CUDA(cudaFuncSetAttribute(k_relgram<double, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  RB_CUDA(cudaFuncSetAttribute(k_relgram<double, 24>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  RB_CUDA(cudaFuncSetAttribute(k_relgram<zc, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  RB_CUDA(cudaFuncSetAttribute(k_relgram<zc, 24>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_spmm<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_spmm<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 #define RB_GATTR(T, PB)                                                                      \
@@ -1405,24 +780,11 @@ void prepare_block_kernels() {
                  (const void *)k_gemm_multi<zc, 24>, (const void *)k_gemm_multi<zc, 32>,
                  (const void *)k_gemm_multi<double, 12, 1>, (const void *)k_gemm_multi<zc, 12, 1>})
     RB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  for (auto f : {(const void *)k_gemm_multi_tma<double, 12, 1>, (const void *)k_gemm_multi_tma<double, 24, 1>,
-                 (const void *)k_gemm_multi_tma<double, 32, 1>, (const void *)k_gemm_multi_tma<zc, 12, 1>,
-                 (const void *)k_gemm_multi_tma<zc, 24, 1>, (const void *)k_gemm_multi_tma<zc, 32, 1>,
-                 (const void *)k_gemm_multi_tma<double, 12, 2>, (const void *)k_gemm_multi_tma<double, 24, 2>,
-                 (const void *)k_gemm_multi_tma<double, 32, 2>, (const void *)k_gemm_multi_tma<zc, 12, 2>,
-                 (const void *)k_gemm_multi_tma<zc, 24, 2>, (const void *)k_gemm_multi_tma<zc, 32, 2>})
-    allow_max_dyn_smem(f);
 }
 
 #define RB_BINST(T)                                                                        \
-  template bool relgram<T>(const std::vector<ColDesc> &, const std::vector<ColDesc> &,            \
-                           const std::vector<cplx> &, const std::vector<cplx> &, int, int, int,    \
-                           int64_t, T *, T *, std::vector<cplx> &, rbicg_ctx *, cudaStream_t);    \
   template void gram_cc<T>(const T *, const T *, int, int64_t, std::vector<cplx> &, rbicg_ctx *, \
                            cudaStream_t);                                                     \
-  template void gram_pairs<T>(const std::vector<const T *> &, const std::vector<int> &,        \
-                              const std::vector<std::pair<int, int>> &, int64_t,              \
-                              std::vector<cplx> &, rbicg_ctx *, cudaStream_t);               \
   template void launch_spmm<T>(const DevMat &, const T *, T *, int, cudaStream_t);         \
   template void gram<T>(const std::vector<ColDesc> &, const std::vector<ColDesc> &, int64_t, \
                         std::vector<cplx> &, rbicg_ctx *, cudaStream_t);                   \

@@ -271,16 +271,8 @@ template <typename T>
 void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
           std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t s);   // G = X^H Y (row-major mX x mY)
 template <typename T>
-bool relgram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Xt, const std::vector<cplx> &M,
-             const std::vector<cplx> &Mt, int p, int k, int fl, int64_t n, T *x, T *xt,
-             std::vector<cplx> &gv, rbicg_ctx *ctx, cudaStream_t strm);
-template <typename T>
 void gram_cc(const T *C, const T *Ct, int k, int64_t n, std::vector<cplx> &out, rbicg_ctx *ctx,
              cudaStream_t strm);
-template <typename T>
-void gram_pairs(const std::vector<const T *> &panels, const std::vector<int> &ncols,
-                const std::vector<std::pair<int, int>> &pairs, int64_t n, std::vector<cplx> &out,
-                rbicg_ctx *ctx, cudaStream_t s);   // out[i] = x_{a_i}^H x_{b_i}, compact panels
 template <typename T>
 void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int p, int64_t n,
                  T *out, rbicg_ctx *ctx, cudaStream_t s, bool sync = true,
