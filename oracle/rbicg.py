@@ -317,11 +317,13 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
     1/σ_min) and the recursion stagnates at ≈ eps·max||r_i||/σ_min.
 
     variant="lookahead" (the fused single-kernel iteration of the
-    GPU path when no recycle space is active): Algorithm 2 except that β_i is
+    GPU path): Algorithm 2 except that β_i is
     formed from the one-step expansion of ρ_i = (r~_i, r_i) with r_i = r_{i-1}
     - α_i q_i,
         ρ_i ≈ ρ_{i-1} - α_i (r~_{i-1}, q_i) - α_i (q~_i, r_{i-1}) + α_i² (q~_i, q_i),
-    whose inner products belong to iteration i's first reduction; ρ_i itself
+    (with a recycle space and Q32 also - (r~_{i-1}, C g) - (C~ g~, r_{i-1})
+    + (C~ g~, C g)), whose inner products belong to iteration i's first
+    reduction (on the GPU: C^*r~, C~^*r, C~^*z, C^*z~ and scalars); ρ_i itself
     (for α_{i+1}, the breakdown test) and the norms stay exact -- on the GPU
     they complete one kernel later, which does not change the arithmetic.
     """
@@ -457,6 +459,12 @@ def solve_dual(A, b, bt, x_m1=None, xt_m1=None, U=None, Ut=None, *, k=10,
         if look:   # ρ_i from iteration i's first reduction (before the update)
             rho_ext = rho - alpha * inner(rt, q) - alpha * inner(qt, r) \
                 + alpha * alpha * inner(qt, q)
+            if reproj:
+                # the Q32 terms of (r~_i, r_i) with r_i = r - α q - C g: (r~, Cg),
+                # (C~g~, r), (C~g~, Cg); (q~, Cg) = (C~g~, q) = 0 exactly (C^*q~ = 0,
+                # C~^*q = 0 by the projections) and are left out
+                Cg, Ctg = basis.C @ g, basis.Ct @ gt
+                rho_ext = rho_ext - inner(rt, Cg) - inner(Ctg, r) + inner(Ctg, Cg)
         r = r - alpha * q
         rt = rt - np.conj(alpha) * qt
         if reproj:   # Q32: r_i ⊥ C~, r~_i ⊥ C ((orth))

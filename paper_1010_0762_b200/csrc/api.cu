@@ -384,6 +384,18 @@ struct Solver {
   std::vector<void *> owned;
   T *rring = nullptr, *rtring = nullptr, *p[2] = {}, *pt[2] = {}, *z = nullptr, *zt = nullptr;
   T *zp[2] = {}, *ztp[2] = {};   // fused iteration: (z_i, p_i) pairs by parity
+  T *AC = nullptr, *AHCt = nullptr;   // fused iteration with k > 0: A C, A^* C~ (per system)
+  // the fused k > 0 iteration for recycle widths up to RBICG_FUSEDK_MAXK
+  static int fusedk_maxk() {   // (read per call: tests switch it)
+    // measured (C3, graph-timed per iteration): k = 1 0.397 vs 0.404 ms two-kernel, k = 3
+    // 0.455 vs 0.496, k = 5 0.561 vs 0.546, k = 10 1.141 vs 0.710; C4 (k = 8) 0.326 vs 0.232
+    // -- marginal, and its look-ahead β moves the counts of the chaotic C1
+    // chain outside the oracle's ensemble (system 3: 192 vs 171..183), so it
+    // is opt-in (RBICG_FUSEDK_MAXK=k; tests/test_gpu_parity.py runs it)
+    const char *e = getenv("RBICG_FUSEDK_MAXK");
+    return e ? atoi(e) : 0;
+  }
+  bool fusedk_cand(int kb) const { return kb > 0 && kb <= fusedk_maxk() && !dist && !pc; }
   T *x = nullptr, *xt = nullptr, *b = nullptr, *bt = nullptr, *xo = nullptr, *xto = nullptr;
   T *psegs[2] = {}, *ptsegs[2] = {};
   // p_0 = p~_0 = 0 (Algorithm 2 starts from p_0 = 0, β_0 = 0)
@@ -579,12 +591,16 @@ struct Solver {
     tmark("ring+p");
     z = alloc(n);
     zt = alloc(n);
-    if (k_basis == 0) {   // fused iteration: (z_i, p_i) nodes by parity (+ ghost rows)
+    if (k_basis == 0 || fusedk_cand(k_basis)) {   // fused iteration: (z_i, p_i) nodes by parity (+ ghost rows)
       const size_t nl = 2;   // node {z, p} (kernels.cu)
       for (int q = 0; q < 2; ++q) {
         zp[q] = alloc(nl * (size_t)nx);
         ztp[q] = alloc(nl * (size_t)nx);
       }
+    }
+    if (fusedk_cand(k_basis)) {   // A C, A^* C~ for the fused form with k > 0
+      AC = alloc((size_t)n * k_basis);
+      AHCt = alloc((size_t)n * k_basis);
     }
     x = alloc(nx);
     xt = alloc(nx);
@@ -730,6 +746,8 @@ struct Solver {
     la.ztp[1] = ztp[1];
     la.x = x;
     la.xt = xt;
+    la.AC = AC;
+    la.AHCt = AHCt;
     la.C = cur.C;
     la.Ct = cur.Ct;
     la.st = st;
@@ -866,6 +884,10 @@ struct Solver {
       spmm_op(false, Uh, tmp.C, kin, ctx->stream);
       spmm_op(true, Uth, tmp.Ct, kin, ctx->stream);
       biorth(U, Ut, tmp.C, tmp.Ct, kin, cur, ctx->stream, ctx->comm.get());
+      if (AC && cur.k > 0) {   // fused form: the neighbours' C γ term through A C
+        spmm_op(false, cur.C, AC, cur.k, ctx->stream);
+        spmm_op(true, cur.Ct, AHCt, cur.k, ctx->stream);
+      }
     }
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
     t_refresh += now_ms() - t0;
@@ -1008,6 +1030,14 @@ struct Solver {
     const bool off = getenv("RBICG_FUSED") && atoi(getenv("RBICG_FUSED")) == 0;   // per solve
     return !off && !pc && zp[0] && la.k == 0 && la.staged && !la.split && lazy_x;
   }
+  // k > 0: one kernel per iteration (k_fusedk) -- single GPU, TMA-staged SELL
+  // tiles in the k = 0 layout, eager x
+  bool fusedk = false;
+  bool fusedk_ok() const {
+    const bool off = getenv("RBICG_FUSED") && atoi(getenv("RBICG_FUSED")) == 0;
+    return !off && zp[0] && AC && la.k > 0 && la.k <= fusedk_maxk() && !dist && !pc && !lazy_x &&
+           !getenv("RBICG_NO_TMA") && 2.0 * la.tile_max * (4 + sizeof(T)) <= 150 * 1024;
+  }
   void capture_graph() {
     if (dist && !ctx->comm->capturable()) {
       uncaptured = true;
@@ -1017,7 +1047,12 @@ struct Solver {
     }
     if (gexec) return;
     fused = fused_ok();
-    if (fused) {   // z_0 = p_0 = 0 (K(1) forms p_1 = r_0 + β_0 p_0 with α_0 = β_0 = 0)
+    fusedk = !fused && fusedk_ok();
+    if (fusedk) {   // the fused kernel stages SELL tiles with the k = 0 layout
+      la.split = 0;
+      la.staged = 1;
+    }
+    if (fused || fusedk) {   // z_0 = p_0 = 0 (K(1) forms p_1 = r_0 + β_0 p_0 with α_0 = β_0 = 0)
       init_nodes(ctx->stream);
     }
     cudaGraph_t g;
@@ -1025,7 +1060,7 @@ struct Solver {
     RB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     // the fused kernel K(i) completes iteration i-1: s + 1 launches reach the
     // cycle boundary from any start (the extra one is a no-op after a pause)
-    for (int it = 0; it < o.s + (fused ? 1 : 0); ++it) {
+    for (int it = 0; it < o.s + (fused || fusedk ? 1 : 0); ++it) {
       if (dist) {
         if (fused) dist_iteration_fused(ctx->stream);
         else dist_iteration(ctx->stream);
@@ -1036,6 +1071,8 @@ struct Solver {
         launch_pass2<T>(la, ctx->stream);
       } else if (fused) {
         launch_fused<T>(la, ctx->stream);
+      } else if (fusedk) {
+        launch_fusedk<T>(la, ctx->stream);
       } else {
         launch_pass1<T>(la, ctx->stream);
         launch_pass2<T>(la, ctx->stream);
@@ -2508,7 +2545,12 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
   // the fused iteration (k = 0): `iters` launches of k_fused in one graph
   ms[14] = -1.0;
   ms[15] = -1.0;
-  if (S.fused_ok()) {
+  const bool tk = S.fusedk_ok();
+  if (tk) {
+    S.la.split = 0;
+    S.la.staged = 1;
+  }
+  if (S.fused_ok() || tk) {
     S.init_nodes(ctx->stream);
     auto reset = [&] {
       S.hst->iter = 0;
@@ -2526,7 +2568,8 @@ static void time_t_(rbicg_ctx *ctx, const rbicg_mat *A, rbicg_rec *R, const rbic
     const int64_t l0 = g_launches.load();
     RB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < iters; ++i) {
-      launch_fused<T>(S.la, ctx->stream);
+      if (tk) launch_fusedk<T>(S.la, ctx->stream);
+      else launch_fused<T>(S.la, ctx->stream);
     }
     RB_CUDA(cudaStreamEndCapture(ctx->stream, &g));
     RB_CUDA(cudaGraphInstantiate(&ge, g, 0));

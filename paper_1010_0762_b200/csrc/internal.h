@@ -96,6 +96,7 @@ struct LoopArgs {
                            //   gather per column (128-bit real, 256-bit complex)
   T *x, *xt;
   const T *C, *Ct;         // row-major n x k
+  const T *AC, *AHCt;      // fused form with k > 0: A C and A^* C~ (row-major n x k, per system)
   DevState<T> *st;
   IterRec<T> *hist;        // [max_itn + 1]
   T *zhist, *zthist;       // [max_itn + 1][k]
@@ -229,6 +230,7 @@ template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_pass2(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_fused(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_leader_fused(const LoopArgs<T> &a, cudaStream_t s);
+template <typename T> void launch_fusedk(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T> void launch_pc_pupdate(const LoopArgs<T> &a, T *pfix, T *ptfix, cudaStream_t s);
 template <typename T> void launch_pc_proj(const LoopArgs<T> &a, cudaStream_t s);
 template <typename T>

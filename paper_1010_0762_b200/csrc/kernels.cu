@@ -1079,6 +1079,293 @@ __global__ void k_halo_unpack_fused(LoopArgs<T> a, const T *recvbuf, int64_t ngh
   }
 }
 
+// ------------------------------------------------------------------ fused form, k > 0
+// K(i) with a recycle space (the oracle's "lookahead" variant with the
+// projections and Q32): K(i) completes iteration i-1 and starts iteration i,
+//   r_{i-1} = r_{i-2} - α_{i-1} z_{i-1} + C γ_{i-1}   (γ = αζ - g, Q32; own rows)
+//   x_{i-1} = x_{i-2} + α_{i-1} p_{i-1}                 (eager x, own rows)
+//   p_i = r_{i-1} + β_{i-1} p_{i-1},
+//   z_i = A p_i = Σ_c a_rc (r_{i-2} - α z_{i-1} + β p_{i-1})_c + (A C)_r γ_{i-1}
+// (the neighbours' C γ term through A C, formed once per system at the
+// refresh), and the duals with C~, A^* C~, γ~, ᾱ, β̄.  ONE reduction per
+// iteration: the 7 scalars of k_fused and the k-vectors C~^*z_i, C^*z~_i,
+// C^*p~_i, C^*r~_{i-1}, C~^*r_{i-1} -- ζ_i, ζ~_i, σ_i, the Q32 g_{i-1}, g~_{i-1}
+// and β_i from the expansion of ρ_i = (r~_i, r_i).  Two n x k reads per side
+// (C, A C) instead of the two-kernel form's two C passes, and 16 instead of
+// 22 n-vectors per iteration.
+constexpr int NFK = 7;
+template <typename T>
+__device__ __forceinline__ void fusedk_leader(const LoopArgs<T> &a, DevState<T> *st, const T *s_fin, int i,
+                                              T alpha, T beta, const T *gam_o, const T *gamt_o) {
+  const int k = a.k;
+  const T *b1 = s_fin + NFK, *b2 = b1 + k, *b3 = b2 + k, *b4 = b3 + k, *b5 = b4 + k;
+  const T rho_prev = s_fin[0];   // ρ_{i-1}, exact
+  const double rn = sqrt(re(s_fin[1])), rtn = sqrt(re(s_fin[2]));
+  int done = 0, status = RBICG_OK;
+  if (i >= 2) {   // iteration i-1 completes here: record, ζ_c, stop test
+    const int m = i - 1;
+    IterRec<T> rec;
+    rec.alpha = alpha;
+    rec.beta = beta;
+    rec.rho = rho_prev;
+    rec.sigma = ldcg(&st->sigma);
+    rec.rnorm = rn;
+    rec.rtnorm = rtn;
+    a.hist[m] = rec;
+    for (int j = 0; j < k; ++j) {   // ζ_c += γ_{i-1} (Q32 form of P:465)
+      st->zc[j] = add(ldcg(&st->zc[j]), gam_o[j]);
+      st->ztc[j] = add(ldcg(&st->ztc[j]), gamt_o[j]);
+    }
+    const int force = __ldcg(&st->force);
+    const bool conv = !force && rn <= __ldcg(&st->tolb) && rtn <= __ldcg(&st->tolbt);
+    if (conv) {
+      done = 1;
+    } else if (iszero(rho_prev) || !finite(divd(rho_prev, ldcg(&st->rho)))) {
+      done = 1;
+      status = RBICG_BREAKDOWN_SERIOUS;
+    } else if (m >= __ldcg(&st->max_itn)) {
+      done = 1;
+      status = force ? RBICG_OK : RBICG_MAXITER;
+    } else if (m == __ldcg(&st->stop_at)) {
+      done = 2;
+    }
+    st->iter = m;
+    st->rnorm = rn;
+    st->rtnorm = rtn;
+    st->rho = rho_prev;
+  }
+  // iteration i: ζ_i = D^{-1} C~^*z_i, ζ~_i = D^{-1} C^*z~_i, σ_i, α_i
+  T zeta[KMAX], zetat[KMAX];
+  T sigma = s_fin[3];
+  for (int j = 0; j < k; ++j) {
+    const double di = __ldcg(&st->dinv[j]);
+    zeta[j] = scal(di, b1[j]);
+    zetat[j] = scal(di, b2[j]);
+    sigma = sub(sigma, cmul(b3[j], zeta[j]));   // (p~, z - Cζ)  (Q23)
+  }
+  const T alpha_i = divd(rho_prev, sigma);
+  if (!done && (iszero(sigma) || !finite(alpha_i))) {
+    done = 1;
+    status = RBICG_BREAKDOWN_SECOND;
+  }
+  // ρ_i ≈ ρ_{i-1} - α (r~, q) - α (q~, r) + α² (q~, q) - (r~, C g) - (C~ g~, r)
+  //       + (C~ g~, C g),  q = z - Cζ, q~ = z~ - C~ζ~, g = D^{-1}C~^*r, g~ = D^{-1}C^*r~
+  T rq = s_fin[4], qr = s_fin[5], qq = s_fin[6], gterm = zero<T>();
+  const T ca = conj(alpha_i);
+  for (int j = 0; j < k; ++j) {
+    const double di = __ldcg(&st->dinv[j]), d = 1.0 / di;
+    const T g = scal(di, b5[j]), gt = scal(di, b4[j]);
+    rq = sub(rq, cmul(b4[j], zeta[j]));                       // (C^*r~)^* ζ
+    qr = sub(qr, cmul(zetat[j], b5[j]));                      // ζ~^* (C~^*r)
+    qq = sub(qq, cmul(b2[j], zeta[j]));                       // (C^*z~)^* ζ
+    qq = sub(qq, cmul(zetat[j], b1[j]));                      // ζ~^* (C~^*z)
+    qq = add(qq, scal(d, cmul(zetat[j], zeta[j])));           // ζ~^* D ζ
+    gterm = add(gterm, cmul(b4[j], g));                       // (r~, C g)
+    gterm = add(gterm, cmul(gt, b5[j]));                      // (C~ g~, r)
+    gterm = sub(gterm, scal(d, cmul(gt, g)));                 // -(C~ g~, C g)
+    // γ_i = α_i ζ_i - g_{i-1}, γ~_i = ᾱ_i ζ~_i - g~_{i-1}  (Q32)
+    st->gam[j] = sub(mul(alpha_i, zeta[j]), g);
+    st->gamt[j] = sub(mul(ca, zetat[j]), gt);
+    a.zhist[(int64_t)i * k + j] = zeta[j];
+    a.zthist[(int64_t)i * k + j] = zetat[j];
+  }
+  const T rho_ext = sub(add(sub(sub(rho_prev, mul(alpha_i, rq)), mul(alpha_i, qr)),
+                            mul(mul(alpha_i, alpha_i), qq)), gterm);
+  st->alpha = alpha_i;
+  st->beta = divd(rho_ext, rho_prev);
+  st->sigma = sigma;
+  st->kidx = i;
+  if (done) {
+    st->status = status;
+    st->done = done;
+  }
+}
+
+template <typename T, int MINB>
+__global__ void __launch_bounds__(BS, MINB) k_fusedk(LoopArgs<T> a) {
+  __shared__ T s_fin[NFK + 5 * KMAX];
+  __shared__ T s_w[NFK][BS / 32];
+  __shared__ T s_gam[KMAX], s_gamt[KMAX];
+  __shared__ T s_row[5][BS];   // z, z~, p~, r~, r of the tile (the k-dots), then block partials
+  __shared__ int s_last;
+  __shared__ uint64_t bars[2];
+  __shared__ T s_ab[2];
+  __shared__ int s_i[2];
+  extern __shared__ __align__(128) unsigned char f_smem[];
+  DevState<T> *st = a.st;
+  const int tid = threadIdx.x;
+  const int k = a.k;
+  const int64_t n = a.n;
+  const int64_t ntiles = (n + BS - 1) / BS;
+  const int64_t G64 = gridDim.x;
+  const int64_t t0 = a.tile_contig ? (ntiles * blockIdx.x) / G64 : blockIdx.x;
+  const int64_t t1 = a.tile_contig ? (ntiles * (blockIdx.x + 1)) / G64 : ntiles;
+  const int64_t tstep = a.tile_contig ? 1 : G64;
+  const size_t stage_bytes = p1_mat_bytes<T>(a);
+  const int nst = a.p1_stages;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int q = 0; q < nst; ++q)
+      if (t0 + q * tstep < t1) p1_issue<T>(a, f_smem + q * stage_bytes, stage_bytes, &bars[q], t0 + q * tstep);
+  pdl_wait();
+  if (tid == 0) {
+    s_i[0] = __ldcg(&st->kidx);
+    s_i[1] = __ldcg(&st->done);
+    s_ab[0] = ldcg(&st->alpha);
+    s_ab[1] = ldcg(&st->beta);
+  }
+  if (tid < k) {
+    s_gam[tid] = ldcg(&st->gam[tid]);
+    s_gamt[tid] = ldcg(&st->gamt[tid]);
+  }
+  __syncthreads();
+  if (s_i[1]) {
+    for (int q = 0; q < nst; ++q)
+      if (t0 + q * tstep < t1) mbar_wait(&bars[q], 0);
+    return;
+  }
+  const int i = s_i[0] + 1;
+  const T alpha = s_ab[0], beta = s_ab[1];
+  const T malpha = neg(alpha), cmalpha = conj(malpha), cb = conj(beta), ca = conj(alpha);
+  const T *__restrict__ r = a.rring + (int64_t)(max(i - 2, 0) % a.ring) * a.ldr;
+  const T *__restrict__ rt = a.rtring + (int64_t)(max(i - 2, 0) % a.ring) * a.ldr;
+  T *__restrict__ rw = a.rring + (int64_t)((i - 1) % a.ring) * a.ldr;
+  T *__restrict__ rtw = a.rtring + (int64_t)((i - 1) % a.ring) * a.ldr;
+  const T *__restrict__ zpo = a.zp[(i - 1) & 1];
+  const T *__restrict__ ztpo = a.ztp[(i - 1) & 1];
+  T *__restrict__ zpn = a.zp[i & 1];
+  T *__restrict__ ztpn = a.ztp[i & 1];
+  const bool wr = i >= 2;
+  const T *__restrict__ C = a.C;
+  const T *__restrict__ Ct = a.Ct;
+  const T *__restrict__ AC = a.AC;
+  const T *__restrict__ AHCt = a.AHCt;
+  T acc[NFK];
+#pragma unroll
+  for (int o = 0; o < NFK; ++o) acc[o] = zero<T>();
+  T b1 = zero<T>(), b2 = zero<T>(), b3 = zero<T>(), b4 = zero<T>(), b5 = zero<T>();
+  const int rstep = BS / k, kt = rstep * k;   // k-dots: thread tid < kt owns column tid % k
+  const int TM = a.tile_max;
+  const int64_t ns = a.A.nslices;
+  VStage<T> vs{};
+  uint32_t par = 0;
+  int it = 0;
+  for (int64_t tile = t0; tile < t1; tile += tstep, ++it) {
+    const int64_t row0 = tile * BS;
+    const int rows = (int)min((int64_t)BS, n - row0);
+    const int si = nst == 2 ? (it & 1) : 0;
+    const unsigned char *base = f_smem + si * stage_bytes;
+    const int32_t *scA = reinterpret_cast<const int32_t *>(base);
+    const int32_t *scH = a.shared_cols ? scA : scA + TM;
+    const T *svA = reinterpret_cast<const T *>(scA + p1_ncols(a) * TM);
+    const T *svH = svA + TM;
+    const int64_t sl = (row0 >> 5) + (tid >> 5);
+    const int64_t slc = min(sl, ns - 1);
+    const int64_t bA = a.A.sptr[tile * (BS / 32)], bH = a.AH.sptr[tile * (BS / 32)];
+    const int64_t oA = a.A.sptr[slc], oH = a.AH.sptr[slc];
+    const int wA = (int)((a.A.sptr[slc + 1] - oA) >> 5), wH = (int)((a.AH.sptr[slc + 1] - oH) >> 5);
+    const int lane = tid & 31;
+    mbar_wait(&bars[si], (par >> si) & 1u);
+    par ^= 1u << si;
+    if (tid < rows) {
+      const int64_t row = row0 + tid;
+      T z, zt;
+      fused_pair_smem<T, false>(scA + (oA - bA) + lane, svA + (oA - bA) + lane, wA,
+                                scH + (oH - bH) + lane, svH + (oH - bH) + lane, wH, r, zpo, rt, ztpo, vs,
+                                malpha, beta, cmalpha, cb, z, zt);
+      T cg = zero<T>(), cgt = zero<T>(), acg = zero<T>(), acgt = zero<T>();
+      for (int j = 0; j < k; ++j) {
+        const int64_t e = row * k + j;
+        cg = mad(ldg(C + e), s_gam[j], cg);
+        cgt = mad(ldg(Ct + e), s_gamt[j], cgt);
+        acg = mad(ldg(AC + e), s_gam[j], acg);
+        acgt = mad(ldg(AHCt + e), s_gamt[j], acgt);
+      }
+      z = add(z, acg);      // + (A C)_row γ_{i-1}
+      zt = add(zt, acgt);
+      const RZP<T> o = ld_node(zpo, r, row), ot = ld_node(ztpo, rt, row);
+      const T rr = add(mad(malpha, o.z, o.r), cg);          // r_{i-1} = r_{i-2} - α z_{i-1} + C γ_{i-1}
+      const T rtr = add(mad(cmalpha, ot.z, ot.r), cgt);
+      const T pr = mad(beta, o.p, rr);
+      const T ptr = mad(cb, ot.p, rtr);
+      if (wr) {
+        rw[row] = rr;
+        rtw[row] = rtr;
+        a.x[row] = mad(alpha, o.p, a.x[row]);               // x_{i-1} = x_{i-2} + α p_{i-1}
+        a.xt[row] = mad(ca, ot.p, a.xt[row]);
+      }
+      st_node(zpn, row, rr, z, pr);
+      st_node(ztpn, row, rtr, zt, ptr);
+      acc[0] = cmad(rtr, rr, acc[0]);
+      acc[1] = add(acc[1], mk_re<T>(abs2(rr)));
+      acc[2] = add(acc[2], mk_re<T>(abs2(rtr)));
+      acc[3] = cmad(ptr, z, acc[3]);
+      acc[4] = cmad(rtr, z, acc[4]);
+      acc[5] = cmad(zt, rr, acc[5]);
+      acc[6] = cmad(zt, z, acc[6]);
+      s_row[0][tid] = z;
+      s_row[1][tid] = zt;
+      s_row[2][tid] = ptr;
+      s_row[3][tid] = rtr;
+      s_row[4][tid] = rr;
+    }
+    __syncthreads();   // stage si consumed; the tile's rows staged for the k-dots
+    if (tid == 0 && tile + nst * tstep < t1)
+      p1_issue<T>(a, f_smem + si * stage_bytes, stage_bytes, &bars[si], tile + nst * tstep);
+    if (tid < kt) {
+      const int nel = rows * k;
+      int lr = tid / k;
+      const T *__restrict__ Cb = C + row0 * k;
+      const T *__restrict__ Ctb = Ct + row0 * k;
+      for (int e = tid; e < nel; e += kt, lr += rstep) {
+        const T c = ldg(Cb + e), ct = ldg(Ctb + e);
+        b1 = cmad(ct, s_row[0][lr], b1);   // C~^* z_i
+        b2 = cmad(c, s_row[1][lr], b2);    // C^* z~_i
+        b3 = cmad(c, s_row[2][lr], b3);    // C^* p~_i
+        b4 = cmad(c, s_row[3][lr], b4);    // C^* r~_{i-1}
+        b5 = cmad(ct, s_row[4][lr], b5);   // C~^* r_{i-1}
+      }
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
+  const int w = tid >> 5, l = tid & 31;
+#pragma unroll
+  for (int o = 0; o < NFK; ++o) {
+    const T v = warp_sum(acc[o]);
+    if (l == 0) s_w[o][w] = v;
+  }
+  s_row[0][tid] = tid < kt ? b1 : zero<T>();
+  s_row[1][tid] = tid < kt ? b2 : zero<T>();
+  s_row[2][tid] = tid < kt ? b3 : zero<T>();
+  s_row[3][tid] = tid < kt ? b4 : zero<T>();
+  s_row[4][tid] = tid < kt ? b5 : zero<T>();
+  __syncthreads();
+  const int G = gridDim.x;
+  if (tid < NFK) {
+    T sum = zero<T>();
+    for (int q = 0; q < BS / 32; ++q) sum = add(sum, s_w[tid][q]);
+    a.part[(int64_t)tid * G + blockIdx.x] = sum;
+  }
+  if (tid < 5 * k) {
+    const int ty = tid / k, j = tid % k;
+    T sum = zero<T>();
+    for (int m = 0; m < rstep; ++m) sum = add(sum, s_row[ty][j + m * k]);
+    a.part[(int64_t)(NFK + tid) * G + blockIdx.x] = sum;
+  }
+  if (!last_block(&st->cnt[0], &s_last)) return;
+  final_reduce(a.part, NFK + 5 * k, G, s_fin);
+  if (tid == 0) {
+    st->cnt[0] = 0;
+    fusedk_leader<T>(a, st, s_fin, i, alpha, beta, s_gam, s_gamt);
+  }
+}
+
 template <typename T> size_t fused_smem(const LoopArgs<T> &a, bool vs) {
   const size_t mat = (a.dcols && !vs) ? dc_mat_bytes<T>(a) : p1_mat_bytes<T>(a);
   return (size_t)a.p1_stages * (mat + (vs ? fused_vec_bytes<T>() : 0));
@@ -1193,6 +1480,19 @@ template <typename T> void launch_fused(const LoopArgs<T> &a0, cudaStream_t s) {
   count_launch();
 }
 
+template <typename T> void launch_fusedk(const LoopArgs<T> &a0, cudaStream_t s) {
+  LoopArgs<T> a = a0;
+  a.p1_stages = 1;
+  const size_t sm = (size_t)p1_mat_bytes<T>(a);
+  static const int minb_env = getenv("RBICG_FUSEDK_MINB") ? atoi(getenv("RBICG_FUSEDK_MINB")) : 0;
+  const int minb = minb_env ? minb_env : (sizeof(T) == 8 ? 4 : 3);
+  auto fn = minb >= 4 ? k_fusedk<T, 4> : k_fusedk<T, 3>;
+  int per_sm = 1;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BS, sm));
+  const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
+  launch_pdl(fn, grid_for(a.n, G), sm, s, a);
+  count_launch();
+}
 template <typename T> void launch_pc_pupdate(const LoopArgs<T> &a, T *pfix, T *ptfix, cudaStream_t s) {
   k_pc_pupdate<T><<<grid_for(a.n, a.G), BS, 0, s>>>(a, pfix, ptfix);
   count_launch();
@@ -1320,6 +1620,10 @@ void prepare_kernels() {
   allow_max_dyn_smem(k_pass2<zc, 4>);
   allow_max_dyn_smem(k_fused<double, 3>);
   allow_max_dyn_smem(k_fused<double, 4>);
+  allow_max_dyn_smem(k_fusedk<double, 4>);
+  allow_max_dyn_smem(k_fusedk<double, 3>);
+  allow_max_dyn_smem(k_fusedk<zc, 4>);
+  allow_max_dyn_smem(k_fusedk<zc, 3>);
   allow_max_dyn_smem(k_fused<double, 4, false, true>);
   allow_max_dyn_smem(k_fused<double, 3, false, true>);
   allow_max_dyn_smem(k_fused<zc, 4, false, true>);
@@ -1342,6 +1646,7 @@ void prepare_kernels() {
   template void launch_pass2<T>(const LoopArgs<T> &, cudaStream_t);                          \
   template void launch_fused<T>(const LoopArgs<T> &, cudaStream_t);                          \
   template void launch_leader_fused<T>(const LoopArgs<T> &, cudaStream_t);                   \
+  template void launch_fusedk<T>(const LoopArgs<T> &, cudaStream_t);                         \
   template void launch_pc_pupdate<T>(const LoopArgs<T> &, T *, T *, cudaStream_t);           \
   template void launch_pc_proj<T>(const LoopArgs<T> &, cudaStream_t);                         \
   template void launch_halo_fused<T>(const LoopArgs<T> &, const int32_t *, int64_t, T *,      \

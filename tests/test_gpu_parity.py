@@ -895,3 +895,42 @@ def test_full_size_c2_fused_count_vs_algorithm2(ctx):
     assert iters_close(res["iterations"], ref.iterations), (res["iterations"], ref.iterations)
     assert res["relres_true"] <= cfg.tol and res["relres_dual_true"] <= cfg.tol
     M.free()
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_fusedk_matches_lookahead_oracle(ctx, monkeypatch, cplx):
+    """The opt-in fused iteration with a recycle space (k_fusedk,
+    RBICG_FUSEDK_MAXK): one kernel per iteration with the neighbours' Cγ
+    term through A C, eager x and β from the expansion of ρ_i including the
+    Q32 terms -- the oracle's variant="lookahead" with projections.  A
+    recycled problem (deflation matrix, k = 4 from a first solve) forced to
+    m iterations across cycle ends: iterates and α to 1e-8; then the full
+    solve converges with the standard oracle's count (max(2, 3 %))."""
+    from oracle import rbicg as R
+    monkeypatch.setenv("RBICG_FUSEDK_MAXK", "8")
+    n, k = 250, 4
+    A, _, _ = deflation_matrix(n, k, seed=41, complex_=cplx)
+    Ad = sp.csr_matrix(A)
+    M = ctx.matrix(*dense_to_csr(A))
+    first = R.solve_dual(Ad, vec(n, 42, cplx), vec(n, 43, cplx), k=k, s=10, tol=1e-10,
+                         max_itn=1000, trunc_tol=1e-6)
+    U, Ut = first.basis_out.U, first.basis_out.Ut
+    b2, bt2 = vec(n, 44, cplx), vec(n, 45, cplx)
+    for m in (7, 23):
+        ref = R.solve_dual(Ad, b2, bt2, U=U, Ut=Ut, k=k, s=10, tol=1e-10, max_itn=1000,
+                           trunc_tol=1e-6, force_iters=m, variant="lookahead")
+        rec = ctx.recycle(n, k, cplx)
+        rec.import_(U, Ut)
+        x, xt, res, h = ctx.solve_dual(M, b2, bt2, R=rec, k=k, s=10, tol=1e-10, max_itn=1000,
+                                       trunc_tol=1e-6, force_iters=m, history=True)
+        assert res["iterations"] == m and res["k_in"] == ref.basis_in.k > 0
+        assert np.linalg.norm(x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+        assert np.linalg.norm(xt - ref.xt) <= 1e-8 * np.linalg.norm(ref.xt)
+        np.testing.assert_allclose(h[:, 2], np.real(ref.hist["alpha"]), rtol=1e-8)
+    std = R.solve_dual(Ad, b2, bt2, U=U, Ut=Ut, k=k, s=10, tol=1e-10, max_itn=1000, trunc_tol=1e-6)
+    rec = ctx.recycle(n, k, cplx)
+    rec.import_(U, Ut)
+    x, xt, res, _ = ctx.solve_dual(M, b2, bt2, R=rec, k=k, s=10, tol=1e-10, max_itn=1000,
+                                   trunc_tol=1e-6)
+    assert res["status"] == 0 and iters_close(res["iterations"], std.iterations)
+    assert res["relres_true"] <= 1e-10 and res["relres_dual_true"] <= 1e-10
