@@ -123,7 +123,9 @@ typedef struct {
   double t_loop_ms, t_cycle_dev_ms, t_host_eig_ms, t_refresh_ms, t_total_ms;
   double alg_bytes;                       /* algorithmic HBM bytes of the loop */
   int32_t kernel_launches;                /* kernels launched by this call     */
-  int32_t reserved;
+  int32_t lookahead_cancellations;        /* fused iteration: iterations whose look-ahead
+                                             ρ_i expansion cancelled to < 1e3 eps of its
+                                             terms (β_i inexact)    */
 } rbicg_result;
 
 /* Create a context on `device`, adopting `cuda_stream` (a cudaStream_t, NULL

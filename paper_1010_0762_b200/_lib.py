@@ -84,10 +84,10 @@ class Result(C.Structure):
                 ("t_loop_ms", C.c_double), ("t_cycle_dev_ms", C.c_double),
                 ("t_host_eig_ms", C.c_double), ("t_refresh_ms", C.c_double),
                 ("t_total_ms", C.c_double), ("alg_bytes", C.c_double),
-                ("kernel_launches", C.c_int32), ("reserved", C.c_int32)]
+                ("kernel_launches", C.c_int32), ("lookahead_cancellations", C.c_int32)]
 
     def as_dict(self):
-        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
+        d = {f: getattr(self, f) for f, _ in self._fields_}
         d["status_name"] = STATUS.get(self.status, str(self.status))
         return d
 

@@ -2171,6 +2171,7 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
                        (S.fused && S.la.dcols ? 2.0 * A->nnz : 0.0);
     res->alg_bytes = fin.iter * (mat + 4.0 * kk * n * w + 20.0 * n * w);
     res->kernel_launches = (int32_t)(g_launches.load() - S.launches0);
+    res->lookahead_cancellations = fin.la_cancel;
   }
   return status;
 }

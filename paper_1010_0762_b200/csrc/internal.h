@@ -42,6 +42,8 @@ template <typename T>
 struct DevState {
   int iter;      // completed iterations i
   int kidx;      // fused form: k_fused launches that did work (K(i), i = kidx + 1 next)
+  int la_cancel; // fused form: iterations whose look-ahead ρ_i expansion cancelled (|ρ_ext| <
+                 //   1e3 eps (|ρ_{i-1}| + |α||(r~,z)| + |α||(z~,r)| + |α|²|(z~,z)|)): β_i inexact
   int done;      // 0 running, 1 finished, 2 paused at a cycle boundary
   int status;    // RBICG_* of the finished iteration
   int max_itn;

@@ -757,6 +757,12 @@ __device__ __forceinline__ void fused_leader(const LoopArgs<T> &a, DevState<T> *
   // ρ_i ≈ ρ_{i-1} - α_i (r~, z) - α_i (z~, r) + α_i² (z~, z)
   const T rho_ext = add(sub(sub(rho_prev, mul(alpha_i, s_fin[4])), mul(alpha_i, s_fin[5])),
                         mul(mul(alpha_i, alpha_i), s_fin[6]));
+  {   // flag a cancelling expansion (near-breakdown regime): β_i is then inexact
+    const double aa = sqrt(abs2(alpha_i));
+    const double mag = sqrt(abs2(rho_prev)) + aa * (sqrt(abs2(s_fin[4])) + sqrt(abs2(s_fin[5]))) +
+                       aa * aa * sqrt(abs2(s_fin[6]));
+    if (sqrt(abs2(rho_ext)) < 1e3 * 2.220446049250313e-16 * mag) st->la_cancel += 1;
+  }
   st->alpha = alpha_i;
   st->beta = divd(rho_ext, rho_prev);
   st->sigma = sigma;
@@ -1171,6 +1177,11 @@ __device__ __forceinline__ void fusedk_leader(const LoopArgs<T> &a, DevState<T> 
   }
   const T rho_ext = sub(add(sub(sub(rho_prev, mul(alpha_i, rq)), mul(alpha_i, qr)),
                             mul(mul(alpha_i, alpha_i), qq)), gterm);
+  {   // flag a cancelling expansion (β_i inexact)
+    const double aa = sqrt(abs2(alpha_i));
+    const double mag = sqrt(abs2(rho_prev)) + aa * (sqrt(abs2(rq)) + sqrt(abs2(qr))) + aa * aa * sqrt(abs2(qq));
+    if (sqrt(abs2(rho_ext)) < 1e3 * 2.220446049250313e-16 * mag) st->la_cancel += 1;
+  }
   st->alpha = alpha_i;
   st->beta = divd(rho_ext, rho_prev);
   st->sigma = sigma;
