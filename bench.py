@@ -374,7 +374,7 @@ def run_gpu(args, rank, world):
     # C2-type workloads end without a recycle space: probe the k = cfg.k
     # iteration on a seeded random space so its kernels are measured too
     probe = None
-    if kt["k"] == 0 and cfg.k > 0 and not args.no_k_probe:
+    if kt["k"] == 0 and cfg.k > 0 and not args.no_k_probe and cfg.n <= 16_000_000:
         g = systems[-1] if part else last
         A = kctx.matrix(g["indptr"], g["indices"], g["data"])
         rng = np.random.default_rng(cfg.seed + 777)

@@ -26,6 +26,12 @@ Parity unpinned: nothing in this package is unpinned except the paper's
 figure/table values that need unavailable data.
 """
 
-from threadpoolctl import threadpool_limits as _threadpool_limits
+# load every BLAS the oracle uses (NumPy's and SciPy's bundled OpenBLAS)
+# before limiting them, so the limit reaches both
+import numpy as _np  # noqa: E402
+import scipy.linalg as _sla  # noqa: E402,F401
+import scipy.sparse.linalg as _spla  # noqa: E402,F401
+from threadpoolctl import threadpool_limits as _threadpool_limits  # noqa: E402
 
+_np.dot(_np.ones(2), _np.ones(2))   # (OpenBLAS initialises its pool on first use)
 _threadpool_limits(1)   # Q26: one fixed reduction order (see above)
