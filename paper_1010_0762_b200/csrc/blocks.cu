@@ -336,7 +336,7 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   } else {
     if (var == 48) return gram2_run<T, 4, 8>(X, Y, n, G, ctx, strm);
     if (var == 44) return gram2_run<T, 4, 4>(X, Y, n, G, ctx, strm);
-    gram2_run<T, 8, 8>(X, Y, n, G, ctx, strm);
+    gram2_run<T, 8, 8>(X, Y, n, G, ctx, strm);   // RBICG_GRAM2=88
   }
 }
 
