@@ -212,6 +212,32 @@ int rbicg_bilinear(rbicg_ctx *ctx, const rbicg_mat *A, const void *u,
                    const void *w, rbicg_rec *R, const rbicg_opts *opts,
                    int on_device, void *value, rbicg_result *res);
 
+/* IRKA support (Algorithm 3; the model
+ * G(s) = c^*(sI - A)^{-1} b with E = I).
+ * rbicg_matrix_shifted_csr builds the store of sigma I - A directly from the
+ * CSR of A (the shifted system of one IRKA shift): the same
+ * arguments as rbicg_matrix_csr plus sigma = (sigma_re, sigma_im); every
+ * entry is negated and sigma added on the diagonal, on the device, before the
+ * SELL build.  Every row must hold its diagonal entry once (RBICG_EINVAL
+ * otherwise); sigma_im must be 0 for RBICG_F64.  One GPU only.
+ * rbicg_reduced_model forms the projected model of step 2d:
+ *   Ar = W^* A V,  Er = W^* V (E = I, reading Q20),  br = W^* b,  cr = V^* c
+ * with V = [v_1 .. v_r], W = [w_1 .. w_r] the primal and dual solutions of
+ * the r shifted pairs (each column contiguous: column i at V + i n), b, c of
+ * length n, all of A's dtype on the device (on_device = 1) or host.  A v_i
+ * runs the library's SpMV, the products its Gram kernel.  Outputs are host
+ * arrays of A's dtype: Ar, Er row-major r x r, br, cr of length r.
+ * 1 <= r <= 32.  One GPU only (RBICG_EINVAL on a partitioned context). */
+int rbicg_matrix_shifted_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz,
+                             const int32_t *rowptr, const int32_t *colind,
+                             const void *val, rbicg_dtype dtype,
+                             double sigma_re, double sigma_im, int on_device,
+                             rbicg_mat **A);
+int rbicg_reduced_model(rbicg_ctx *ctx, const rbicg_mat *A, int32_t r,
+                        const void *V, const void *W, const void *b,
+                        const void *c, int on_device, void *Ar, void *Er,
+                        void *br, void *cr);
+
 /* Parity hooks (per-call checks, BASELINE.json: 1e-12 relative).
  * spmv_pair: z = A p, zt = A^* pt.
  * project: given R's refreshed basis for A, zeta = D_c^{-1} C~^* z and

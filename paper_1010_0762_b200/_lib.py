@@ -98,6 +98,10 @@ _sig = {
     "rbicg_finalize": (C.c_int, [vp]),
     "rbicg_matrix_csr": (C.c_int, [vp, C.c_int64, C.c_int64, vp, vp, vp, C.c_int,
                                    C.c_int, C.POINTER(vp)]),
+    "rbicg_matrix_shifted_csr": (C.c_int, [vp, C.c_int64, C.c_int64, vp, vp, vp, C.c_int,
+                                           C.c_double, C.c_double, C.c_int, C.POINTER(vp)]),
+    "rbicg_reduced_model": (C.c_int, [vp, vp, C.c_int32, vp, vp, vp, vp, C.c_int,
+                                      vp, vp, vp, vp]),
     "rbicg_matrix_free": (C.c_int, [vp]),
     "rbicg_recycle_new": (C.c_int, [vp, C.c_int64, C.c_int32, C.c_int,
                                     C.POINTER(vp)]),

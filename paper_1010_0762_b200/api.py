@@ -96,8 +96,29 @@ class Context:
             pass
 
     # ------------------------------------------------------------ matrices
-    def matrix(self, indptr, indices, data):
-        return Matrix(self, indptr, indices, data)
+    def matrix(self, indptr, indices, data, shift=None):
+        """Store of A; with shift=sigma the store of sigma I - A, formed on the
+        device (rbicg_matrix_shifted_csr, IRKA's shifted systems)."""
+        return Matrix(self, indptr, indices, data, shift=shift)
+
+    def reduced_model(self, A, V, W, b, c):
+        """(W^*AV, W^*V, W^*b, V^*c) of IRKA step 2d (rbicg_reduced_model):
+        V, W of shape (r, n) (one solution per row, contiguous), b, c of
+        length n, all numpy or all CUDA tensors of A's dtype.  Returns numpy
+        arrays (r x r, r x r, r, r)."""
+        r = int(V.shape[0])
+        dev = _is_torch(V)
+        if not dev:
+            dt = np.complex128 if A.complex_ else np.float64
+            V, W, b, c = (np.ascontiguousarray(a, dtype=dt) for a in (V, W, b, c))
+        else:
+            V, W, b, c = (a.contiguous() for a in (V, W, b, c))
+        dt = np.complex128 if A.complex_ else np.float64
+        Ar, Er = np.zeros((r, r), dt), np.zeros((r, r), dt)
+        br, cr = np.zeros(r, dt), np.zeros(r, dt)
+        check(lib.rbicg_reduced_model(self._h, A._h, r, _ptr(V), _ptr(W), _ptr(b), _ptr(c),
+                                      1 if dev else 0, _ptr(Ar), _ptr(Er), _ptr(br), _ptr(cr)))
+        return Ar, Er, br, cr
 
     def recycle(self, n, k_max, complex_=False):
         return Recycle(self, n, k_max, complex_)
@@ -223,7 +244,7 @@ class Context:
 class Matrix:
     """Device SELL-32 store of A and A^* (rbicg_matrix_csr)."""
 
-    def __init__(self, ctx, indptr, indices, data):
+    def __init__(self, ctx, indptr, indices, data, shift=None):
         self.ctx = ctx
         dev = _is_torch(data)
         if not dev:
@@ -237,10 +258,18 @@ class Matrix:
         self.complex_ = _dtype_code(data) == C128
         self._h = C.c_void_p()
         ctx._children.append(weakref.ref(self))
-        check(lib.rbicg_matrix_csr(ctx._h, self.n, self.nnz, _ptr(indptr),
-                                   _ptr(indices), _ptr(data),
-                                   C128 if self.complex_ else F64,
-                                   1 if dev else 0, C.byref(self._h)))
+        if shift is None:
+            check(lib.rbicg_matrix_csr(ctx._h, self.n, self.nnz, _ptr(indptr),
+                                       _ptr(indices), _ptr(data),
+                                       C128 if self.complex_ else F64,
+                                       1 if dev else 0, C.byref(self._h)))
+        else:
+            sg = complex(shift)
+            check(lib.rbicg_matrix_shifted_csr(ctx._h, self.n, self.nnz, _ptr(indptr),
+                                               _ptr(indices), _ptr(data),
+                                               C128 if self.complex_ else F64,
+                                               sg.real, sg.imag, 1 if dev else 0,
+                                               C.byref(self._h)))
 
     def free(self):
         if self._h:

@@ -1835,11 +1835,12 @@ int rbicg_finalize(rbicg_ctx *ctx) {
   return 0;
 }
 
-int rbicg_matrix_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr,
-                     const int32_t *colind, const void *val, rbicg_dtype dtype, int on_device,
-                     rbicg_mat **A) {
+static int matrix_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr,
+                      const int32_t *colind, const void *val, rbicg_dtype dtype, int on_device,
+                      rbicg_mat **A, const cplx *shift) {
   if (!ctx || !A || n <= 0 || nnz < 0 || n >= INT32_MAX || nnz >= INT32_MAX) return RBICG_EINVAL;
   if (dtype != RBICG_F64 && dtype != RBICG_C128) return RBICG_EINVAL;
+  if (shift && (ctx->dist() || (dtype == RBICG_F64 && shift->imag() != 0))) return RBICG_EINVAL;
   return run_guarded([&] {
     RB_CUDA(cudaSetDevice(ctx->device));
     order_after_user(ctx);
@@ -1851,6 +1852,16 @@ int rbicg_matrix_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowp
     if (nnz) {
       copy_in(ci, colind, sizeof(int32_t) * nnz, on_device, ctx->stream);
       copy_in(vv, val, w * nnz, on_device, ctx->stream);
+    }
+    if (shift) {   // sigma I - A on the staged copy (the caller's arrays untouched)
+      try {
+        shift_csr_values(ctx, n, rp, ci, vv, dtype, shift->real(), shift->imag());
+      } catch (...) {
+        ws_free(rp);
+        ws_free(ci);
+        ws_free(vv);
+        throw;
+      }
     }
     auto *M = new rbicg_mat();
     M->ctx = ctx;
@@ -1873,6 +1884,19 @@ int rbicg_matrix_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowp
     ws_free(vv);
     *A = M;
   });
+}
+
+int rbicg_matrix_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr,
+                     const int32_t *colind, const void *val, rbicg_dtype dtype, int on_device,
+                     rbicg_mat **A) {
+  return matrix_csr(ctx, n, nnz, rowptr, colind, val, dtype, on_device, A, nullptr);
+}
+
+int rbicg_matrix_shifted_csr(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr,
+                             const int32_t *colind, const void *val, rbicg_dtype dtype,
+                             double sigma_re, double sigma_im, int on_device, rbicg_mat **A) {
+  const cplx sg(sigma_re, sigma_im);
+  return matrix_csr(ctx, n, nnz, rowptr, colind, val, dtype, on_device, A, &sg);
 }
 
 int rbicg_matrix_free(rbicg_mat *A) {
@@ -2310,6 +2334,73 @@ int rbicg_bilinear(rbicg_ctx *ctx, const rbicg_mat *A, const void *u, const void
   });
   for (void *q : {dx, dxt, du, dw, dr}) ws_free(q);
   return rc ? rc : status;
+}
+
+int rbicg_reduced_model(rbicg_ctx *ctx, const rbicg_mat *A, int32_t r, const void *V, const void *W,
+                        const void *b, const void *c, int on_device, void *Ar, void *Er, void *br,
+                        void *cr) {
+  if (!ctx || !A || !V || !W || !b || !c || !Ar || !Er || !br || !cr) return RBICG_EINVAL;
+  if (r < 1 || r > 32 || ctx->dist()) return RBICG_EINVAL;
+  const size_t wb = wbytes(A->dtype);
+  const int64_t n = A->n;
+  void *dV = nullptr, *dW = nullptr, *dAV = nullptr, *db = nullptr, *dc = nullptr;
+  const int rc = run_guarded([&] {
+    RB_CUDA(cudaSetDevice(ctx->device));
+    order_after_user(ctx);
+    dV = ws_alloc(wb * n * r);
+    dW = ws_alloc(wb * n * r);
+    dAV = ws_alloc(wb * n * r);
+    db = ws_alloc(wb * n);
+    dc = ws_alloc(wb * n);
+    copy_in(dV, V, wb * n * r, on_device, ctx->stream);
+    copy_in(dW, W, wb * n * r, on_device, ctx->stream);
+    copy_in(db, b, wb * n, on_device, ctx->stream);
+    copy_in(dc, c, wb * n, on_device, ctx->stream);
+    // A v_i (one column = an n x 1 row-major block for the SpMM kernel)
+    for (int i = 0; i < r; ++i) {
+      if (A->dtype == RBICG_F64)
+        launch_spmm<double>(A->A, (const double *)dV + (size_t)i * n, (double *)dAV + (size_t)i * n, 1,
+                            ctx->stream);
+      else
+        launch_spmm<zc>(A->A, (const zc *)dV + (size_t)i * n, (zc *)dAV + (size_t)i * n, 1, ctx->stream);
+    }
+    // [W^*AV | W^*V | W^*b] and V^*c through the Gram kernel
+    std::vector<ColDesc> X, Y, Xv, Yc{{dc, 1}};
+    for (int i = 0; i < r; ++i) {
+      X.push_back({(const char *)dW + wb * n * i, 1});
+      Xv.push_back({(const char *)dV + wb * n * i, 1});
+    }
+    for (int i = 0; i < r; ++i) Y.push_back({(const char *)dAV + wb * n * i, 1});
+    for (int i = 0; i < r; ++i) Y.push_back({(const char *)dV + wb * n * i, 1});
+    Y.push_back({db, 1});
+    std::vector<cplx> G, Gc;
+    if (A->dtype == RBICG_F64) {
+      gram<double>(X, Y, n, G, ctx, ctx->stream);
+      gram<double>(Xv, Yc, n, Gc, ctx, ctx->stream);
+    } else {
+      gram<zc>(X, Y, n, G, ctx, ctx->stream);
+      gram<zc>(Xv, Yc, n, Gc, ctx, ctx->stream);
+    }
+    const int m = 2 * r + 1;
+    auto put = [&](void *dst, int64_t idx, cplx v) {
+      if (A->dtype == RBICG_F64) ((double *)dst)[idx] = v.real();
+      else {
+        ((double *)dst)[2 * idx] = v.real();
+        ((double *)dst)[2 * idx + 1] = v.imag();
+      }
+    };
+    for (int i = 0; i < r; ++i) {
+      for (int j = 0; j < r; ++j) {
+        put(Ar, (int64_t)i * r + j, G[(size_t)i * m + j]);
+        put(Er, (int64_t)i * r + j, G[(size_t)i * m + r + j]);
+      }
+      put(br, i, G[(size_t)i * m + 2 * r]);
+      put(cr, i, Gc[i]);
+    }
+  });
+  for (void *q : {dV, dW, dAV, db, dc})
+    if (q) ws_free(q);
+  return rc;
 }
 
 int rbicg_dbg_spmv_pair(rbicg_ctx *ctx, const rbicg_mat *A, const void *p, const void *pt, void *z,

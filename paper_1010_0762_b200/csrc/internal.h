@@ -193,6 +193,9 @@ namespace rbicg {
 void build_matrix(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr_d,
                   const int32_t *col_d, const void *val_d, rbicg_dtype dt, rbicg_mat *M);
 void free_devmat(DevMat &m);
+// val <- sigma I - A on a device CSR (every row holds its diagonal once, else EINVAL)
+void shift_csr_values(rbicg_ctx *ctx, int64_t n, const int32_t *rowptr_d, const int32_t *col_d,
+                      void *val_d, rbicg_dtype dt, double sigma_re, double sigma_im);
 // partitioned store: local rows of A and of A^* given as CSR (device arrays,
 // local column indices in [0, nloc + nghost))
 void build_matrix_local(rbicg_ctx *ctx, int64_t nloc, const int32_t *rpA, const int32_t *ciA,

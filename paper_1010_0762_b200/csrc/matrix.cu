@@ -309,6 +309,43 @@ void build_matrix_local(rbicg_ctx *ctx, int64_t nloc, const int32_t *rpA, const 
   RB_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+// sigma I - A in place on a device CSR value array (IRKA's shifted systems,
+// P:1100-1101): one thread per row negates its entries and adds sigma to the
+// diagonal; a row without exactly one diagonal entry sets *bad.
+template <typename T>
+__global__ void k_shift_rows(const int32_t *rowptr, const int32_t *col, T *val, int64_t n, T sigma,
+                             int *bad) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int diag = 0;
+    for (int32_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+      T v = neg(val[e]);
+      if (col[e] == r) {
+        v = add(v, sigma);
+        ++diag;
+      }
+      val[e] = v;
+    }
+    if (diag != 1) atomicOr(bad, 1);
+  }
+}
+
+void shift_csr_values(rbicg_ctx *ctx, int64_t n, const int32_t *rowptr_d, const int32_t *col_d,
+                      void *val_d, rbicg_dtype dt, double sre, double sim) {
+  int *bad = (int *)ws_alloc(sizeof(int));
+  RB_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+  if (dt == RBICG_F64)
+    k_shift_rows<double><<<grid1d(n), 256, 0, ctx->stream>>>(rowptr_d, col_d, (double *)val_d, n, sre, bad);
+  else
+    k_shift_rows<zc><<<grid1d(n), 256, 0, ctx->stream>>>(rowptr_d, col_d, (zc *)val_d, n, mk(sre, sim), bad);
+  count_launch();
+  int h = 0;
+  RB_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  ws_free(bad);
+  RB_CHECK(h == 0, RBICG_EINVAL);
+}
+
 void free_devmat(DevMat &m) {
   // pooled device memory (reused by the next system's store); no device sync
   ws_free(m.sptr);

@@ -4,10 +4,13 @@ The model is G(s) = c^*(sE - A)^{-1} b with E = I (PAPER.md:963-977,
 :1186-1194).  Every dual pair (σ_i I - A) v_i = b, (σ_i I - A)^* w_i = c runs
 through ``Context.solve_dual`` (the sm_100a hot path) with recycling strategy
 1: shift slot i keeps its recycle handle and its previous
-solutions from one IRKA step to the next.  The products A v_i use the
-library's SpMV kernels; the reduced model A_r = W_r^*AV_r, E_r = W_r^*V_r
-(reading Q20: E_r = W_r^*EV_r), its r x r eigenproblem and the shift update
-σ_i ← -λ_i(A_r, E_r) are host control work of r x r size (as the cycle-end
+solutions from one IRKA step to the next.  Everything of size n stays on
+the device: the CSR of A, b, c and the solutions V, W (torch CUDA tensors);
+each shifted store σ_i I - A is formed by the library from A's CSR
+(rbicg_matrix_shifted_csr) and the reduced model A_r = W_r^*AV_r,
+E_r = W_r^*V_r (reading Q20: E_r = W_r^*EV_r), W_r^*b, V_r^*c by its SpMV
+and Gram kernels (rbicg_reduced_model).  Only the r x r eigenproblem and the
+shift update σ_i ← -λ_i(A_r, E_r) are host control work (as the cycle-end
 pencil is for the solver).  Readings (Q29): convergence on the
 relative shift change, slots paired by sorting shifts by (|σ|, arg σ).
 """
@@ -60,12 +63,23 @@ def irka(ctx, indptr, indices, data, b, c, shifts0, *, k=8, s=40, tol=1e-10,
     strategy 1/2/3: the recycling strategies of PAPER.md:1196-1235 (see
     oracle/irka.py for the readings); strategies 2 and 3 copy the chosen
     space into the solve's own handle on the device (Recycle.copy_from)."""
+    import torch
     A = sp.csr_matrix((np.asarray(data, np.complex128), indices, indptr))
     n = A.shape[0]
-    I = sp.identity(n, dtype=np.complex128, format="csr")
-    MA = ctx.matrix(A.indptr, A.indices, A.data)          # for the products A v_i
-    b = np.asarray(b, np.complex128)
-    c = np.asarray(c, np.complex128)
+    if np.any(A.diagonal() == 0) or not A.has_sorted_indices:   # setup only: every row
+        Ac = A.tocoo()                                          # holds its diagonal once
+        ii = np.arange(n)
+        A = sp.csr_matrix((np.concatenate([Ac.data, np.zeros(n, np.complex128)]),
+                           (np.concatenate([Ac.row, ii]), np.concatenate([Ac.col, ii]))),
+                          shape=(n, n))
+        A.sum_duplicates()
+        A.sort_indices()
+    dev = torch.device("cuda", ctx.device)
+    Ad = [torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+          for a in (A.indptr.astype(np.int32), A.indices.astype(np.int32), A.data)]
+    MA = ctx.matrix(*Ad)                                   # for the products A v_i
+    b = torch.from_numpy(np.asarray(b, np.complex128).copy()).to(dev)
+    c = torch.from_numpy(np.asarray(c, np.complex128).copy()).to(dev)
     sig = order_shifts(shifts0)
     r = len(sig)
     slots = [dict(R=ctx.recycle(n, max(k, 1), True), x=None, xt=None) for _ in range(r)]
@@ -75,8 +89,8 @@ def irka(ctx, indptr, indices, data, b, c, shifts0, *, k=8, s=40, tol=1e-10,
     spare = []           # handles of the pool two steps back, reused
 
     def solve_all(sig):
-        V = np.zeros((n, r), np.complex128)
-        W = np.zeros((n, r), np.complex128)
+        V = torch.zeros((r, n), dtype=torch.complex128, device=dev)
+        W = torch.zeros((r, n), dtype=torch.complex128, device=dev)
         its = []
         cur_pool = []
         for i, si in enumerate(sig):
@@ -91,15 +105,13 @@ def irka(ctx, indptr, indices, data, b, c, shifts0, *, k=8, s=40, tol=1e-10,
                     Rh.copy_from(src)
                 else:
                     Rh.clear()
-            As = (si * I - A).tocsr()
-            As.sort_indices()
-            M = ctx.matrix(As.indptr, As.indices, As.data)
+            M = ctx.matrix(*Ad, shift=si)                  # σ_i I - A on the device
             x, xt, res, _ = ctx.solve_dual(M, b, c, st["x"], st["xt"],
                                            R=Rh if recycle else None,
                                            k=k if recycle else 0, s=s, tol=tol,
                                            max_itn=max_itn, trunc_tol=trunc_tol)
             M.free()
-            V[:, i], W[:, i] = x, xt
+            V[i], W[i] = x, xt
             st["x"], st["xt"] = x, xt                     # previous solution
             if strategy == 2 and chain[0] is not None:
                 spare.append(chain[0])
@@ -112,9 +124,7 @@ def irka(ctx, indptr, indices, data, b, c, shifts0, *, k=8, s=40, tol=1e-10,
         return V, W, its
 
     def reduced(V, W):
-        AV = np.column_stack([ctx.spmv_pair(MA, V[:, i].copy(), V[:, i].copy())[0]
-                              for i in range(r)])
-        return W.conj().T @ AV, W.conj().T @ V, W.conj().T @ b, V.conj().T @ c
+        return ctx.reduced_model(MA, V, W, b, c)
 
     V, W, its = solve_all(sig)
     run.history.append(sig.copy())
