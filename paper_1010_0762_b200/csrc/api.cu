@@ -679,14 +679,17 @@ struct Solver {
     // per row and matrix, 128-row tiles) leaves room to stage the C, C~ rows.
     auto envi = [](const char *nm, int dflt) { const char *e = getenv(nm); return e ? atoi(e) : dflt; };
     const char *sc = getenv("RBICG_P1_STAGEC");
-    const double cap = (sc ? atof(sc) : 110.0) * 1024;
+    const double cap = (sc ? atof(sc) : (sizeof(T) == 16 ? 0.0 : 110.0)) * 1024;
     // measured (C3, graph-timed pass 1): one thread per row over 256-row tiles
     // wins while the C, C~ tile is small (k = 1: 0.279 vs 0.322 ms, k = 3: 0.316
     // vs 0.336), the split form from k = 5 on (0.352 vs 0.378; k = 10: 0.441 vs
     // 0.539) and for complex data (C4, k = 8: 0.145 vs 0.172)
     la.split = envi("RBICG_SPLIT", (cur.k > 3 || (cur.k > 0 && sizeof(T) == 16)) ? 1 : 0);
     la.p1_stages = std::min(2, std::max(1, envi("RBICG_P1_STAGES", 1)));
-    la.stage_v = envi("RBICG_STAGEV", la.split ? 1 : 0);
+    // complex split form: neither the vector rows nor the C, C~ tile staged, so
+    // 4 CTAs/SM fit (2 with both staged, 92 KB each): C4 k = 8 pass 1 0.1435 ->
+    // 0.1363 ms (graph-timed); real data keeps both (4 CTAs/SM with them)
+    la.stage_v = envi("RBICG_STAGEV", la.split && sizeof(T) == 8 ? 1 : 0);
     la.l2ef = envi("RBICG_L2EF", 1);
     la.pf = envi("RBICG_PF", 0);
     la.abl = 0;
