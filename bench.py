@@ -265,11 +265,14 @@ def run_gpu(args, rank, world):
     # timed system started from (copied device to device before that step,
     # outside its events) -- the iteration the timed region mostly ran
     snap = {"R": None, "k": 0}
+    # (not for spaces over 8 GB -- C5 with k = 20 on one GPU needs the memory;
+    # the roofline then times the space the sequence ends with)
+    snap_ok = 2 * cfg.n * cfg.k * (16 if cfg.complex else 8) <= 8 << 30
 
     def one(i, timed):
         d = dsys[i] if dsys[i] is not None else upload(systems[i])
         slot = systems[i].get("slot")
-        if timed and not part:
+        if timed and not part and snap_ok:
             kin = R.k
             if kin > snap["k"]:
                 if snap["R"] is None:

@@ -477,12 +477,38 @@ struct Solver {
   // the candidate's C_j = A U_j, C~_j (truncated like U_j): the next cycle
   // end's C_{j-1} without an SpMM (allocated once a truncation keeps
   // directions: never on C2/C5, whose spaces are truncated away)
+  // Kept only while memory allows (C5 with k = 20 on one GPU: 18 GB); else the
+  // next cycle end forms C_{j-1} by the SpMM.  Returns whether B.C exists.
   bool cand_c_valid = false;
-  template <typename BB> void ensure_basis_c(BB &B) {
-    if (B.C) return;
+  bool cand_c_off = false;
+  template <typename BB> bool ensure_basis_c(BB &B) {
+    if (B.C) return true;
+    if (cand_c_off) return false;
+    const size_t blk = sizeof(T) * (size_t)n * kmax;
+    size_t avail = 0, tot = 0;
+    if (cudaMemGetInfo(&avail, &tot) != cudaSuccess) {
+      cudaGetLastError();
+      avail = 0;
+    }
+    {   // free blocks of the previous solve's arena count as available
+      std::lock_guard<std::mutex> la(g_arena_mu);
+      for (size_t i = arena_pos; i < ctx->arena.size(); ++i)
+        if (ctx->arena[i].second) avail += ctx->arena[i].first;
+    }
+    // the lazily allocated U_j, Ũ_j temporaries may still come, + 2 GB margin
+    const size_t reserve = (tmp.U ? 0 : 2 * sizeof(T) * (size_t)nx * kmax) + ((size_t)2 << 30);
+    if (avail < 2 * blk + reserve) {
+      cand_c_off = true;
+      return false;
+    }
     B.C = alloc((size_t)n * kmax);
     B.Ct = alloc((size_t)n * kmax);
+    return true;
   }
+  // one GPU: the cycle-end candidate's U, Ũ live in the recycle handle's own
+  // buffers (its input space is consumed by the refresh; the handle is
+  // emptied until the solve returns its new space) -- 2 n x k_max blocks
+  void *borrow_u = nullptr, *borrow_ut = nullptr;
   ~Solver() {
     static const bool tm = getenv("RBICG_TIMING") != nullptr;
     const double t0 = tm ? now_ms() : 0;
@@ -623,8 +649,13 @@ struct Solver {
       // use when the system starts without a space (C5 fits the overlapped
       // cycle end on one GPU thanks to the 2 n x k blocks saved)
       const bool lazy_u = (B == &tmp || B == &cand[0]) && tmp_u_lazy();
-      B->U = kb && !lazy_u ? alloc((size_t)nx * kb) : nullptr;
-      B->Ut = kb && !lazy_u ? alloc((size_t)nx * kb) : nullptr;
+      if (B == &cand[0] && borrow_u) {
+        B->U = (T *)borrow_u;
+        B->Ut = (T *)borrow_ut;
+      } else {
+        B->U = kb && !lazy_u ? alloc((size_t)nx * kb) : nullptr;
+        B->Ut = kb && !lazy_u ? alloc((size_t)nx * kb) : nullptr;
+      }
       B->k = 0;
       if (B == &cand[0]) continue;
       B->C = kb ? alloc((size_t)n * kb) : nullptr;
@@ -638,7 +669,7 @@ struct Solver {
     zhist = alloc((size_t)H * kmax);
     zthist = alloc((size_t)H * kmax);
     const int nout = 3 * KMAX + 8 + 2 * KMAX;
-    part = alloc((size_t)nout * ctx->grid_stream);
+    part = alloc((size_t)nout * ctx->grid_stream * (dist ? 2 : 1));   // 2: halo-overlap launches
     memset(hst, 0, sizeof(DevState<T>));
     if (pc) {
       pc_work_alloc(pc, pcw_main);
@@ -862,8 +893,7 @@ struct Solver {
     ensure_basis_u(out);
     gemm_panels<T>(cols_of(U), Fu, pk, n, out.U, ctx, bs);
     gemm_panels<T>(cols_of(Ut), Fut, pk, n, out.Ut, ctx, bs);
-    if (with_c) {
-      ensure_basis_c(out);
+    if (with_c && ensure_basis_c(out)) {
       gemm_panels<T>(cols_of(C), Fu, pk, n, out.C, ctx, bs);
       gemm_panels<T>(cols_of(Ct), Fut, pk, n, out.Ct, ctx, bs);
     }
@@ -950,19 +980,67 @@ struct Solver {
   // (C-3), β step and stop test.
   // fused form over the row partition: ONE allreduce per iteration (the
   // halo carries r, z, p and the duals of the iteration's gathered state)
+  // Halo overlap: the exchange + unpack go to the halo stream
+  // while the iteration's SpMV kernel visits its interior tiles (no ghost
+  // column, matrix.cu build_matrix_local); the boundary tiles follow the join.
+  // One reduction spans both launches (LoopArgs::phase).  Without boundary
+  // (one rank) or interior tiles it is one launch after the halo.
+  bool overlap_ok() const {
+    return dist && M->ord && M->nint > 0 && M->nint < M->ntl && M->nint_h > 0 && M->nint_h < M->ntl_h &&
+           !getenv("RBICG_NO_HALO_OVERLAP");
+  }
+  template <typename Exch, typename Launch>
+  void overlapped(cudaStream_t s, Exch exch, Launch launch) {
+    if (!overlap_ok()) {
+      exch(s);
+      launch(la);
+      return;
+    }
+    RB_CUDA(cudaEventRecord(ctx->ev_fork, s));
+    RB_CUDA(cudaStreamWaitEvent(ctx->halo_stream, ctx->ev_fork, 0));
+    exch(ctx->halo_stream);
+    RB_CUDA(cudaEventRecord(ctx->ev_join, ctx->halo_stream));
+    LoopArgs<T> a = la;
+    a.ordered = 1;
+    a.torder = M->ord;
+    a.torder_h = M->ord_h;
+    a.tile_contig = 0;
+    a.pstride = 2 * ctx->grid_stream;
+    const bool h = la.split != 0;   // the split pass 1 visits 128-row tiles
+    const int64_t ni = h ? M->nint_h : M->nint, nt = h ? M->ntl_h : M->ntl;
+    a.phase = 1;
+    a.tbase = 0;
+    a.tcount = ni;
+    launch(a);
+    RB_CUDA(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    a.phase = 2;
+    a.tbase = ni;
+    a.tcount = nt - ni;
+    g_pdl_off = true;
+    launch(a);
+    g_pdl_off = false;
+  }
   void dist_iteration_fused(cudaStream_t s) {
     launch_halo_fused<T>(la, M->halo.send_idx, M->halo.nsend, hsend, nullptr, 0, 1, s);
-    ctx->comm->exchange(M->halo, hsend, hrecv, (int64_t)M->halo.nghost * sizeof(T), sizeof(T), 6, s);
-    launch_halo_fused<T>(la, nullptr, 0, nullptr, hrecv, M->halo.nghost, 0, s);
-    launch_fused<T>(la, s);
+    overlapped(
+        s,
+        [&](cudaStream_t hs) {
+          ctx->comm->exchange(M->halo, hsend, hrecv, (int64_t)M->halo.nghost * sizeof(T), sizeof(T), 6, hs);
+          launch_halo_fused<T>(la, nullptr, 0, nullptr, hrecv, M->halo.nghost, 0, hs);
+        },
+        [&](const LoopArgs<T> &a) { launch_fused<T>(a, s); });
     allreduce_red(7, s);
     launch_leader_fused<T>(la, s);
   }
   void dist_iteration(cudaStream_t s) {
     launch_halo_pack_loop<T>(la, M->halo.send_idx, M->halo.nsend, hsend, s);
-    ctx->comm->exchange(M->halo, hsend, hrecv, (int64_t)M->halo.nghost * sizeof(T), sizeof(T), 4, s);
-    launch_halo_unpack_loop<T>(la, hrecv, M->halo.nghost, s);
-    launch_pass1<T>(la, s);
+    overlapped(
+        s,
+        [&](cudaStream_t hs) {
+          ctx->comm->exchange(M->halo, hsend, hrecv, (int64_t)M->halo.nghost * sizeof(T), sizeof(T), 4, hs);
+          launch_halo_unpack_loop<T>(la, hrecv, M->halo.nghost, hs);
+        },
+        [&](const LoopArgs<T> &a) { launch_pass1<T>(a, s); });
     allreduce_red(p1_nsums(la.k), s);
     launch_leader1<T>(la, s);
     launch_pass2<T>(la, s);
@@ -1604,7 +1682,7 @@ struct Solver {
         if (!u_late || chk) {
           biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/!keep_fast, nullptr, nullptr,
                  nullptr, &Fk, &Ftk);
-          cand_c_valid = !keep_fast && out.k > 0;
+          cand_c_valid = !keep_fast && out.k > 0 && out.C;
         } else {
           std::vector<cplx> Fu, Fut;
           biorth(nullptr, nullptr, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/false, &Fu, &Fut,
@@ -1626,8 +1704,7 @@ struct Solver {
             Phase phu("cycle.gemm_U", cs);
             gemm_multi<T>(Xv, Mu, {{out.U, pk}}, n, ctx, cs);
             gemm_multi<T>(Xvt, Mut, {{out.Ut, pk}}, n, ctx, cs);
-            if (!keep_fast) {   // C_j N_p for the next cycle end's C_{j-1}
-              ensure_basis_c(out);
+            if (!keep_fast && ensure_basis_c(out)) {   // C_j N_p for the next cycle end's C_{j-1}
               std::vector<ColDesc> Xc, Xct;
               for (int c = 0; c < ksel; ++c) {
                 Xc.push_back(col(tmp.C, c, ksel));
@@ -1637,7 +1714,7 @@ struct Solver {
               gemm_panels<T>(Xct, Fut, pk, n, out.Ct, ctx, cs);
             }
           }
-          cand_c_valid = !keep_fast && out.k > 0;
+          cand_c_valid = !keep_fast && out.k > 0 && out.C;
         }
       } else {
       {
@@ -1660,7 +1737,7 @@ struct Solver {
       }
       biorth(tmp.U, tmp.Ut, tmp.C, tmp.Ct, ksel, out, cs, cms, /*with_c=*/!keep_fast, nullptr, nullptr,
              nullptr, &Fk, &Ftk);
-      cand_c_valid = !keep_fast && out.k > 0;
+      cand_c_valid = !keep_fast && out.k > 0 && out.C;
       }
     }
     if (keep_fast) {   // U_j = Φ_j (W_j Fu): F = W Fu w.r.t. the normalised Φ_j
@@ -1799,6 +1876,10 @@ int rbicg_init(rbicg_ctx **out, int device, void *stream, const rbicg_dist *dist
           c->comm = make_comm_threads(dist->rank, dist->nranks, dist->nccl_id, 0);
           c->comm_side = make_comm_threads(dist->rank, dist->nranks, dist->nccl_id, 1);
         }
+        // the halo stream runs at the loop's (high) priority
+        RB_CUDA(cudaStreamCreateWithPriority(&c->halo_stream, cudaStreamNonBlocking, c->prio_hi));
+        RB_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        RB_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
       } catch (...) {
         cudaEventDestroy(c->order_ev);
         cudaStreamDestroy(c->stream);
@@ -1830,6 +1911,9 @@ int rbicg_finalize(rbicg_ctx *ctx) {
     g_ctxs.erase(ctx);
   }
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->halo_stream) cudaStreamDestroy(ctx->halo_stream);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   forget_partition_plan(ctx);
   ws_release_all();
   cudaEventDestroy(ctx->order_ev);
@@ -1906,6 +1990,8 @@ int rbicg_matrix_free(rbicg_mat *A) {
   if (!A) return RBICG_EINVAL;
   // no ctx dereference: the ctx may already be finalized (cudaFree syncs)
   if (A->halo.send_idx) ws_free(A->halo.send_idx);
+  if (A->ord) ws_free(A->ord);
+  if (A->ord_h) ws_free(A->ord_h);
   free_devmat(A->A);
   free_devmat(A->AH);
   delete A;
@@ -2003,6 +2089,11 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
   Solver<T> S;
   S.pc = P;
   const int kin = R ? R->k : 0;
+  const bool borrow = R && !ctx->dist() && opts->k > 0 && opts->update_recycle;
+  if (borrow) {
+    S.borrow_u = R->U;
+    S.borrow_ut = R->Ut;
+  }
   S.setup(ctx, A, *opts, kin);
   mark("setup");
   const int64_t n = A->n;
@@ -2030,6 +2121,7 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
   // Step 1 + refresh
   S.refresh(R && kin > 0 ? (const T *)R->U : nullptr, R && kin > 0 ? (const T *)R->Ut : nullptr,
             opts->k > 0 ? kin : 0);
+  if (borrow) R->k = 0;   // its buffers now hold the cycle-end candidate (empty on error)
   mark("refresh");
   S.make_args();
   S.init_state();
@@ -2135,7 +2227,7 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
     const typename Solver<T>::Basis *src = &S.cur;
     if (update && S.cand_cur >= 0) src = &S.cand[S.cand_cur];
     k_out = std::min(src->k, R->kmax);
-    if (k_out > 0) {
+    if (k_out > 0 && src->U != R->U) {   // (the candidate already lives there when borrowed)
       RB_CUDA(cudaMemcpyAsync(R->U, src->U, sizeof(T) * n * k_out, cudaMemcpyDeviceToDevice, st));
       RB_CUDA(cudaMemcpyAsync(R->Ut, src->Ut, sizeof(T) * n * k_out, cudaMemcpyDeviceToDevice, st));
     }

@@ -98,6 +98,7 @@ inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_
 // (0: all SMs).  The overlapped cycle end runs its kernels under a cap so the
 // loop's kernels keep SMs to dispatch onto (RBICG_SIDE_SMS).
 extern thread_local int g_sm_cap;
+extern thread_local bool g_pdl_off;   // launch without programmatic dependent launch
 inline int sm_budget(int nsm) { return g_sm_cap > 0 && g_sm_cap < nsm ? g_sm_cap : nsm; }
 
 // ---------------------------------------------------------------- errors

@@ -222,15 +222,43 @@ __device__ __forceinline__ bool last_block(unsigned *cnt, int *s_flag) {
   return *s_flag != 0;
 }
 
+// Tile visiting order of the SpMV kernels (LoopArgs::torder): the number of
+// tiles this launch visits, the tile of visit index ix, and the reduction's
+// block count / this block's slot.
+template <typename T> __device__ __forceinline__ int64_t launch_tiles(const LoopArgs<T> &a, int64_t ntiles) {
+  return a.ordered ? a.tcount : ntiles;
+}
+template <typename T>
+__device__ __forceinline__ int64_t tile_at(const LoopArgs<T> &a, const int32_t *ord, int64_t ix) {
+  return a.ordered ? (int64_t)ord[a.tbase + ix] : ix;
+}
+// the reduction of one iteration's SpMV kernel: stride of the partials,
+// this block's slot, and (phase 2 / single launch) the number of partials
+template <typename T> __device__ __forceinline__ int red_stride(const LoopArgs<T> &a) {
+  return a.phase ? a.pstride : (int)gridDim.x;
+}
+template <typename T> __device__ __forceinline__ int red_slot(const LoopArgs<T> &a) {
+  return (a.phase == 2 ? __ldcg(&a.st->g1) : 0) + (int)blockIdx.x;
+}
+template <typename T> __device__ __forceinline__ int red_count(const LoopArgs<T> &a) {
+  return (a.phase == 2 ? __ldcg(&a.st->g1) : 0) + (int)gridDim.x;
+}
+// phase 1: record the grid and stop after the partials (true = return)
+template <typename T> __device__ __forceinline__ bool interior_done(const LoopArgs<T> &a) {
+  if (a.phase != 1) return false;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.st->g1 = (int)gridDim.x;
+  return true;
+}
+
 // Final fixed-order reduction of `nout` outputs stored as part[o*G + b].
 // All partial loads of a lane are issued before any add (they are L2 hits;
 // a dependent chain of G/32 loads would cost microseconds at the kernel tail).
 constexpr int RED_PER_LANE = 20;   // one round of loads for G <= 640 blocks
 template <typename T>
-__device__ __forceinline__ void final_reduce(const T *part, int nout, int G, T *s_fin) {
+__device__ __forceinline__ void final_reduce(const T *part, int nout, int G, T *s_fin, int stride = 0) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   for (int o = w; o < nout; o += BS / 32) {
-    const T *src = part + (int64_t)o * G;
+    const T *src = part + (int64_t)o * (stride ? stride : G);
     T acc = zero<T>();
     for (int q0 = 0; q0 < G; q0 += 32 * RED_PER_LANE) {
       T v[RED_PER_LANE];
@@ -497,8 +525,10 @@ __device__ __forceinline__ void p1_tiles(const LoopArgs<T> &a, unsigned char *ds
   T *__restrict__ ptnew = ptcol(a, it + 1);
   const int rstep = k > 0 ? BS / k : 0;
   const int kt = rstep * k;
+  const int64_t nvis = launch_tiles(a, ntiles);
   int i = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += G64, ++i) {
+  for (int64_t ix = blockIdx.x; ix < nvis; ix += G64, ++i) {
+    const int64_t tile = tile_at(a, a.torder, ix);
     const int64_t row0 = tile * BS;
     const int rows = (int)min((int64_t)BS, n - row0);
     const bool cst = stage_c && rows == BS;
@@ -508,10 +538,10 @@ __device__ __forceinline__ void p1_tiles(const LoopArgs<T> &a, unsigned char *ds
       tma_load_1d(sC, a.C + tile * BS * k, cbytes, &bars[2]);
       tma_load_1d(sC + BS * k, a.Ct + tile * BS * k, cbytes, &bars[2]);
     }
-    if (a.pf && tid == 32 && tile + G64 < ntiles && (tile + G64 + 1) * BS <= n) {
+    if (a.pf && tid == 32 && ix + G64 < nvis && (tile_at(a, a.torder, ix + G64) + 1) * BS <= n) {
       // the vector rows of this block's next tile: first touched by the
       // gathers of nearby tiles, so pull them into L2 ahead of the wave
-      const int64_t r1 = (tile + G64) * BS;
+      const int64_t r1 = tile_at(a, a.torder, ix + G64) * BS;
       const uint32_t vb = BS * (uint32_t)sizeof(T);
       prefetch_l2(r + r1, vb);
       prefetch_l2(rt + r1, vb);
@@ -578,10 +608,11 @@ __device__ __forceinline__ void p1_tiles(const LoopArgs<T> &a, unsigned char *ds
                      ldv<COH>(ptold + row));
         }
       }
-      __syncthreads();   // stage si consumed -> refill with tile + nst G
-      if (tid == 0 && tile + nst * G64 < ntiles) {
-        p1_issue<T>(a, dsm + si * stage_bytes, stage_bytes, &bars[si], tile + nst * G64);
-        if (stage_v) p1_issue_vec<T>(a, dsm + si * stage_bytes, &bars[si], tile + nst * G64, it);
+      __syncthreads();   // stage si consumed -> refill with visit ix + nst G
+      if (tid == 0 && ix + nst * G64 < nvis) {
+        const int64_t tn = tile_at(a, a.torder, ix + nst * G64);
+        p1_issue<T>(a, dsm + si * stage_bytes, stage_bytes, &bars[si], tn);
+        if (stage_v) p1_issue_vec<T>(a, dsm + si * stage_bytes, &bars[si], tn, it);
       }
     } else if (tid < rows) {
       const int64_t row = row0 + tid;
@@ -745,8 +776,10 @@ __device__ __forceinline__ void p1_tiles_split(const LoopArgs<T> &a, unsigned ch
   T *s_r = s_z + 4 * TRH, *s_rt = s_z + 5 * TRH;   // r_{i-1}, r~_{i-1} rows (Q32)
   const int rstep = k > 0 ? BS / k : 0;
   const int kt = rstep * k;
+  const int64_t nvis = launch_tiles(a, ntiles);
   int i = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += G64, ++i) {
+  for (int64_t ix = blockIdx.x; ix < nvis; ix += G64, ++i) {
+    const int64_t tile = tile_at(a, a.torder_h, ix);
     const int64_t row0 = tile * TRH;
     const int rows = (int)min((int64_t)TRH, n - row0);
     const bool cst = stage_c && rows == TRH;
@@ -794,9 +827,10 @@ __device__ __forceinline__ void p1_tiles_split(const LoopArgs<T> &a, unsigned ch
       }
     }
     __syncthreads();   // stage si consumed -> refill with tile + nst G
-    if (tid == 0 && tile + nst * G64 < ntiles) {
-      p1s_issue<T>(a, dsm + si * stage_bytes, &bars[si], tile + nst * G64);
-      if (stage_v) p1s_issue_vec<T>(a, dsm + si * stage_bytes, &bars[si], tile + nst * G64, it);
+    if (tid == 0 && ix + nst * G64 < nvis) {
+      const int64_t tn = tile_at(a, a.torder_h, ix + nst * G64);
+      p1s_issue<T>(a, dsm + si * stage_bytes, &bars[si], tn);
+      if (stage_v) p1s_issue_vec<T>(a, dsm + si * stage_bytes, &bars[si], tn, it);
     }
     if (!side && lr < rows) aptz = cmad(s_pt[lr], s_z[lr], aptz);   // p~^* z
     if (k > 0) {
@@ -844,7 +878,7 @@ __device__ __forceinline__ void p1_partials(const LoopArgs<T> &a, P1Scratch<T> &
                                             T a2, T a3, T a4, T a5, T aptz) {
   const int tid = threadIdx.x;
   const int k = a.k;
-  const int G = gridDim.x;
+  const int G = red_stride(a), b = red_slot(a);
   const int rstep = k > 0 ? BS / k : 0;
   const int kt = rstep * k;
   if (k > 0) {
@@ -857,9 +891,9 @@ __device__ __forceinline__ void p1_partials(const LoopArgs<T> &a, P1Scratch<T> &
     const int ty = tid / k, j = tid % k;
     T s = zero<T>();
     for (int m = 0; m < rstep; ++m) s = add(s, sc.s_red()[ty * BS + j + m * k]);
-    a.part[(int64_t)tid * G + blockIdx.x] = s;
+    a.part[(int64_t)tid * G + b] = s;
   }
-  if (tid == 0) a.part[(int64_t)(3 * k) * G + blockIdx.x] = bptz;
+  if (tid == 0) a.part[(int64_t)(3 * k) * G + b] = bptz;
   if (k > 0) {   // second round through the same scratch
     __syncthreads();
     sc.s_red()[tid] = tid < kt ? a4 : zero<T>();
@@ -869,7 +903,7 @@ __device__ __forceinline__ void p1_partials(const LoopArgs<T> &a, P1Scratch<T> &
       const int ty = tid / k, j = tid % k;
       T s = zero<T>();
       for (int m = 0; m < rstep; ++m) s = add(s, sc.s_red()[ty * BS + j + m * k]);
-      a.part[(int64_t)(3 * k + 1 + tid) * G + blockIdx.x] = s;
+      a.part[(int64_t)(3 * k + 1 + tid) * G + b] = s;
     }
   }
 }

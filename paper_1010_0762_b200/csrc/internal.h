@@ -52,6 +52,7 @@ struct DevState {
   int k;
   int seg_start;   // lazy x: first iteration index of the open segment
   unsigned cnt[4];
+  int g1;        // halo overlap: blocks of the interior launch (LoopArgs::phase)
   T rho, beta, alpha, sigma;   // ρ_{i}, β_{i}, α_i, σ_i
   double rnorm, rtnorm;        // ||r_i||, ||r~_i||
   double tolb, tolbt;          // tol ||b||, tol ||b~||
@@ -105,6 +106,18 @@ struct LoopArgs {
   T *part;                 // block partials [outputs][G]
   int dist;                // row-partitioned: reduction tails write local sums to red
   T *red;                  //   (allreduced, then a one-block leader kernel runs the scalar step)
+  // halo overlap (row partition): the tiles of the SpMV kernels are visited in
+  // torder (256-row tiles) / torder_h (128-row tiles, split pass 1) -- interior
+  // tiles (no ghost column) first -- and one iteration's kernel runs as two
+  // launches: [0, nint) while the halo is in flight, [nint, ntiles) after it.
+  // ordered = 0: every tile in natural order (one GPU).  phase 1 (interior
+  // launch) writes its block partials at part[o * pstride + b] and records its
+  // grid size in st->g1; phase 2 (boundary launch, issued after phase 1 has
+  // completed) writes at slots g1 + b and its last block reduces all g1 + G2.
+  int ordered;
+  const int32_t *torder, *torder_h;
+  int64_t tbase, tcount;
+  int phase, pstride;
 };
 
 struct ColDesc {           // one column of an n-row panel: p[row * stride]
@@ -138,6 +151,10 @@ struct rbicg_ctx {
   // device buffers of the last solve (bytes, pointer), reused by the next
   std::vector<std::pair<size_t, void *>> arena;
   cudaStream_t side = nullptr;   // cycle-end stream (low priority), kept across solves
+  // row partition: the halo exchange runs on halo_stream (fork / join events)
+  // while the interior tiles of the iteration's SpMV kernel run
+  cudaStream_t halo_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   uint64_t async_key = 0;        // (n, k, s, dtype) of the last doubled-ring decision
   bool async_ok = false;
 };
@@ -149,6 +166,11 @@ struct rbicg_mat {
   rbicg_dtype dtype = RBICG_F64;
   rbicg::DevMat A, AH;             // partitioned: columns local (own, then ghosts)
   rbicg::HaloPlan halo;            // partitioned: ghost rows / send lists
+  // partitioned: tile visiting orders for the halo overlap (LoopArgs::torder):
+  // 256-row (ord) and 128-row (ord_h) tiles, interior tiles (no ghost column
+  // in A or A^*) first; nint / nint_h interior tiles of ntl / ntl_h
+  int32_t *ord = nullptr, *ord_h = nullptr;
+  int64_t nint = 0, ntl = 0, nint_h = 0, ntl_h = 0;
 };
 
 namespace rbicg {

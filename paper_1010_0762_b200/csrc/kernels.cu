@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(BS, MINB) k_pass1(LoopArgs<T> a) {
   extern __shared__ __align__(128) unsigned char p1_smem[];
   DevState<T> *st = a.st;
   const int tid = threadIdx.x;
-  const int64_t ntiles = (a.n + BS - 1) / BS;
+  const int64_t nvis = launch_tiles(a, (a.n + BS - 1) / BS);
   const int64_t G64 = gridDim.x;
   const size_t stage_bytes = p1_stage_bytes<T>(a);
   const int nst = a.p1_stages;
@@ -47,21 +47,23 @@ __global__ void __launch_bounds__(BS, MINB) k_pass1(LoopArgs<T> a) {
     __syncthreads();
     if (tid == 0)
       for (int q = 0; q < nst; ++q)
-        if ((int64_t)blockIdx.x + q * G64 < ntiles)
-          p1_issue<T>(a, p1_smem + q * stage_bytes, stage_bytes, &bars[q], blockIdx.x + q * G64);
+        if ((int64_t)blockIdx.x + q * G64 < nvis)
+          p1_issue<T>(a, p1_smem + q * stage_bytes, stage_bytes, &bars[q],
+                      tile_at(a, a.torder, blockIdx.x + q * G64));
   }
   pdl_wait();
   snap_load(st, a.k, sn);
   if (tid == 0 && stage_v)   // the vector rows depend on the previous kernel
     for (int q = 0; q < nst; ++q)
-      if ((int64_t)blockIdx.x + q * G64 < ntiles) {
+      if ((int64_t)blockIdx.x + q * G64 < nvis) {
         if (sn.done) mbar_arrive(&bars[q]);
-        else p1_issue_vec<T>(a, p1_smem + q * stage_bytes, &bars[q], blockIdx.x + q * G64, sn.iter);
+        else p1_issue_vec<T>(a, p1_smem + q * stage_bytes, &bars[q], tile_at(a, a.torder, blockIdx.x + q * G64),
+                             sn.iter);
       }
   if (sn.done) {
     if (a.staged)   // drain the copies in flight
       for (int q = 0; q < nst; ++q)
-        if ((int64_t)blockIdx.x + q * G64 < ntiles) mbar_wait(&bars[q], 0);
+        if ((int64_t)blockIdx.x + q * G64 < nvis) mbar_wait(&bars[q], 0);
     return;
   }
   uint32_t par = 0;
@@ -70,8 +72,8 @@ __global__ void __launch_bounds__(BS, MINB) k_pass1(LoopArgs<T> a) {
                      a.lazy_x && sn.iter == sn.seg_start, a1, a2, a3, a4, a5, aptz);
   pdl_trigger();
   p1_partials<T>(a, sc, s_w, a1, a2, a3, a4, a5, aptz);
-  if (!last_block(&st->cnt[0], &s_last)) return;
-  final_reduce(a.part, p1_nsums(a.k), gridDim.x, s_fin);
+  if (interior_done(a) || !last_block(&st->cnt[0], &s_last)) return;
+  final_reduce(a.part, p1_nsums(a.k), red_count(a), s_fin, red_stride(a));
   if (tid == 0) st->cnt[0] = 0;
   if (a.dist) {   // local sums -> allreduce -> k_leader1
     for (int o = tid; o < p1_nsums(a.k); o += BS) a.red[o] = s_fin[o];
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(BS, 4) k_pass1s(LoopArgs<T> a) {
   extern __shared__ __align__(128) unsigned char p1_smem[];
   DevState<T> *st = a.st;
   const int tid = threadIdx.x;
-  const int64_t ntiles = (a.n + TRH - 1) / TRH;
+  const int64_t nvis = launch_tiles(a, (a.n + TRH - 1) / TRH);
   const int64_t G64 = gridDim.x;
   const size_t stage_bytes = p1s_stage_bytes<T>(a);
   const int nst = a.p1_stages;
@@ -107,19 +109,20 @@ __global__ void __launch_bounds__(BS, 4) k_pass1s(LoopArgs<T> a) {
   __syncthreads();
   if (tid == 0)   // prologue independent of the previous kernel: first matrix tiles
     for (int q = 0; q < nst; ++q)
-      if ((int64_t)blockIdx.x + q * G64 < ntiles)
-        p1s_issue<T>(a, p1_smem + q * stage_bytes, &bars[q], blockIdx.x + q * G64);
+      if ((int64_t)blockIdx.x + q * G64 < nvis)
+        p1s_issue<T>(a, p1_smem + q * stage_bytes, &bars[q], tile_at(a, a.torder_h, blockIdx.x + q * G64));
   pdl_wait();
   snap_load(st, a.k, sn);
   if (tid == 0 && stage_v)   // the vector rows depend on the previous kernel
     for (int q = 0; q < nst; ++q)
-      if ((int64_t)blockIdx.x + q * G64 < ntiles) {
+      if ((int64_t)blockIdx.x + q * G64 < nvis) {
         if (sn.done) mbar_arrive(&bars[q]);
-        else p1s_issue_vec<T>(a, p1_smem + q * stage_bytes, &bars[q], blockIdx.x + q * G64, sn.iter);
+        else p1s_issue_vec<T>(a, p1_smem + q * stage_bytes, &bars[q], tile_at(a, a.torder_h, blockIdx.x + q * G64),
+                              sn.iter);
       }
   if (sn.done) {
     for (int q = 0; q < nst; ++q)
-      if ((int64_t)blockIdx.x + q * G64 < ntiles) mbar_wait(&bars[q], 0);
+      if ((int64_t)blockIdx.x + q * G64 < nvis) mbar_wait(&bars[q], 0);
     return;
   }
   uint32_t par = 0;
@@ -128,8 +131,8 @@ __global__ void __launch_bounds__(BS, 4) k_pass1s(LoopArgs<T> a) {
                                a.lazy_x && sn.iter == sn.seg_start, a1, a2, a3, a4, a5, aptz);
   pdl_trigger();
   p1_partials<T>(a, sc, s_w, a1, a2, a3, a4, a5, aptz);
-  if (!last_block(&st->cnt[0], &s_last)) return;
-  final_reduce(a.part, p1_nsums(a.k), gridDim.x, s_fin);
+  if (interior_done(a) || !last_block(&st->cnt[0], &s_last)) return;
+  final_reduce(a.part, p1_nsums(a.k), red_count(a), s_fin, red_stride(a));
   if (tid == 0) st->cnt[0] = 0;
   if (a.dist) {   // local sums -> allreduce -> k_leader1
     for (int o = tid; o < p1_nsums(a.k); o += BS) a.red[o] = s_fin[o];
@@ -869,10 +872,11 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   DevState<T> *st = a.st;
   const int tid = threadIdx.x;
   const int64_t n = a.n;
-  const int64_t ntiles = (n + BS - 1) / BS;
+  const int64_t ntiles = launch_tiles(a, (n + BS - 1) / BS);   // visits of this launch
   const int64_t G64 = gridDim.x;
-  // this CTA's tiles: grid-strided (b, b + G, ...) or one contiguous run
-  // (a.tile_contig: neighbouring tiles' vector rows stay in this SM's L1)
+  // this CTA's visits: grid-strided (b, b + G, ...) or one contiguous run
+  // (a.tile_contig: neighbouring tiles' vector rows stay in this SM's L1);
+  // visit ix is tile tile_at(ix) (natural order on one GPU)
   const int64_t t0 = a.tile_contig ? (ntiles * blockIdx.x) / G64 : blockIdx.x;
   const int64_t t1 = a.tile_contig ? (ntiles * (blockIdx.x + 1)) / G64 : ntiles;
   const int64_t tstep = a.tile_contig ? 1 : G64;
@@ -888,8 +892,9 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   if (tid == 0)
     for (int q = 0; q < nst; ++q)
       if (t0 + q * tstep < t1) {
-        if (DC) fused_issue_dc<T>(a, f_smem + q * stage_bytes, &bars[q], t0 + q * tstep);
-        else p1_issue<T>(a, f_smem + q * stage_bytes, stage_bytes, &bars[q], t0 + q * tstep);
+        const int64_t tq = tile_at(a, a.torder, t0 + q * tstep);
+        if (DC) fused_issue_dc<T>(a, f_smem + q * stage_bytes, &bars[q], tq);
+        else p1_issue<T>(a, f_smem + q * stage_bytes, stage_bytes, &bars[q], tq);
       }
   pdl_wait();
   if (tid == 0) {
@@ -927,8 +932,8 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   if (VS && tid == 0)   // the vector parts of the first tiles (written by the previous kernel)
     for (int q = 0; q < nst; ++q)
       if (t0 + q * tstep < t1)
-        fused_issue_vec<T>(f_smem + q * stage_bytes + mat_bytes, &bars[q], t0 + q * tstep, n, r,
-                           zpo, rt, ztpo);
+        fused_issue_vec<T>(f_smem + q * stage_bytes + mat_bytes, &bars[q], tile_at(a, a.torder, t0 + q * tstep),
+                           n, r, zpo, rt, ztpo);
   T acc[NFUSED];
 #pragma unroll
   for (int o = 0; o < NFUSED; ++o) acc[o] = zero<T>();
@@ -936,7 +941,8 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   const int64_t ns = a.A.nslices;
   uint32_t par = 0;
   int it = 0;
-  for (int64_t tile = t0; tile < t1; tile += tstep, ++it) {
+  for (int64_t ix = t0; ix < t1; ix += tstep, ++it) {
+    const int64_t tile = tile_at(a, a.torder, ix);
     const int64_t row0 = tile * BS;
     const int rows = (int)min((int64_t)BS, n - row0);
     const int si = nst == 2 ? (it & 1) : 0;
@@ -1002,12 +1008,11 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
       acc[6] = cmad(zt, z, acc[6]);        // (z~_i, z_i)
     }
     __syncthreads();   // stage si consumed
-    if (tid == 0 && tile + nst * tstep < t1) {
-      if (DC) fused_issue_dc<T>(a, f_smem + si * stage_bytes, &bars[si], tile + nst * tstep);
-      else p1_issue<T>(a, f_smem + si * stage_bytes, stage_bytes, &bars[si], tile + nst * tstep);
-      if (VS)
-        fused_issue_vec<T>(f_smem + si * stage_bytes + mat_bytes, &bars[si], tile + nst * tstep, n, r, zpo,
-                           rt, ztpo);
+    if (tid == 0 && ix + nst * tstep < t1) {
+      const int64_t tn = tile_at(a, a.torder, ix + nst * tstep);
+      if (DC) fused_issue_dc<T>(a, f_smem + si * stage_bytes, &bars[si], tn);
+      else p1_issue<T>(a, f_smem + si * stage_bytes, stage_bytes, &bars[si], tn);
+      if (VS) fused_issue_vec<T>(f_smem + si * stage_bytes + mat_bytes, &bars[si], tn, n, r, zpo, rt, ztpo);
     }
   }
   pdl_trigger();
@@ -1022,10 +1027,10 @@ __global__ void __launch_bounds__(BS, MINB) k_fused(LoopArgs<T> a) {
   if (tid < NFUSED) {
     T sum = zero<T>();
     for (int q = 0; q < BS / 32; ++q) sum = add(sum, s_w[tid][q]);
-    a.part[(int64_t)tid * gridDim.x + blockIdx.x] = sum;
+    a.part[(int64_t)tid * red_stride(a) + red_slot(a)] = sum;
   }
-  if (!last_block(&st->cnt[0], &s_last)) return;
-  final_reduce(a.part, NFUSED, gridDim.x, s_fin);
+  if (interior_done(a) || !last_block(&st->cnt[0], &s_last)) return;
+  final_reduce(a.part, NFUSED, red_count(a), s_fin, red_stride(a));
   if (tid == 0) st->cnt[0] = 0;
   if (a.dist) {   // local sums -> allreduce -> k_leader_fused
     if (tid < NFUSED) a.red[tid] = s_fin[tid];
@@ -1387,6 +1392,12 @@ static int grid_for(int64_t n, int G) {
   const int64_t tiles = (n + BS - 1) / BS;
   return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, G));
 }
+// grid of an SpMV-kernel launch: its visits (halo-overlap ranges) or all tiles
+template <typename T> static int grid_visits(const LoopArgs<T> &a, int G) {
+  return a.ordered ? (int)std::max<int64_t>(1, std::min<int64_t>(a.tcount, G)) : grid_for(a.n, G);
+}
+// the boundary launch of the halo overlap follows an event join: plain launch
+thread_local bool g_pdl_off = false;
 
 template <typename T> size_t pass1_smem(const LoopArgs<T> &a) {
   return (size_t)a.p1_stages * p1_stage_bytes<T>(a) +
@@ -1401,7 +1412,7 @@ static void launch_pdl(void (*kern)(KArgs...), int grid, size_t sm, cudaStream_t
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl && !g_pdl_off ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   RB_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
@@ -1429,7 +1440,7 @@ template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s) {
     int per_sm = 1;
     RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass1s_fn<T>(), BS, sm));
     const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
-    const int64_t tiles = (a.n + TRH - 1) / TRH;
+    const int64_t tiles = a.ordered ? a.tcount : (a.n + TRH - 1) / TRH;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, G)));
     cfg.blockDim = dim3(BS);
@@ -1437,7 +1448,7 @@ template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s) {
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl && !g_pdl_off ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     void *args[] = {(void *)&a};
@@ -1452,7 +1463,7 @@ template <typename T> void launch_pass1(const LoopArgs<T> &a, cudaStream_t s) {
   auto fn = minb >= 6 ? k_pass1<T, 6> : (minb == 5 ? k_pass1<T, 5> : k_pass1<T, 4>);
   RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BS, sm));
   const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
-  launch_pdl(fn, grid_for(a.n, G), sm, s, a);
+  launch_pdl(fn, grid_visits(a, G), sm, s, a);
   count_launch();
 }
 
@@ -1487,7 +1498,7 @@ template <typename T> void launch_fused(const LoopArgs<T> &a0, cudaStream_t s) {
   int per_sm = 1;
   RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BS, sm));
   const int G = std::min(a.G, std::max(1, per_sm) * a.nsm);
-  launch_pdl(fn, grid_for(a.n, G), sm, s, a);
+  launch_pdl(fn, grid_visits(a, G), sm, s, a);
   count_launch();
 }
 

@@ -293,11 +293,55 @@ void build_matrix(rbicg_ctx *ctx, int64_t n, int64_t nnz, const int32_t *rowptr_
     build_t<zc>(ctx, n, nnz, rowptr_d, col_d, (const zc *)val_d, M);
 }
 
+// rows that reference a ghost column (>= nloc) in A or A^*: flag their
+// 256-row and 128-row tiles
+__global__ void k_ghost_tiles(const int32_t *rpA, const int32_t *ciA, const int32_t *rpH,
+                              const int32_t *ciH, int64_t nloc, int *f256, int *f128) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nloc;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    bool g = false;
+    for (int32_t e = rpA[r]; e < rpA[r + 1] && !g; ++e) g = ciA[e] >= nloc;
+    for (int32_t e = rpH[r]; e < rpH[r + 1] && !g; ++e) g = ciH[e] >= nloc;
+    if (g) {
+      f256[r / BS] = 1;
+      f128[r / TRH] = 1;
+    }
+  }
+}
+
+static int32_t *tile_order(const std::vector<int> &flag, int64_t &nint) {
+  std::vector<int32_t> ord;
+  ord.reserve(flag.size());
+  for (size_t t = 0; t < flag.size(); ++t)
+    if (!flag[t]) ord.push_back((int32_t)t);
+  nint = (int64_t)ord.size();
+  for (size_t t = 0; t < flag.size(); ++t)
+    if (flag[t]) ord.push_back((int32_t)t);
+  int32_t *d = (int32_t *)ws_alloc(sizeof(int32_t) * std::max<size_t>(ord.size(), 1));
+  RB_CUDA(cudaMemcpy(d, ord.data(), sizeof(int32_t) * ord.size(), cudaMemcpyHostToDevice));
+  return d;
+}
+
 void build_matrix_local(rbicg_ctx *ctx, int64_t nloc, const int32_t *rpA, const int32_t *ciA,
                         const void *vA, const int32_t *rpH, const int32_t *ciH, const void *vH,
                         rbicg_dtype dt, rbicg_mat *M) {
   M->n = nloc;
   M->dtype = dt;
+  {   // halo-overlap tile orders (interior tiles first)
+    const int64_t t256 = (nloc + BS - 1) / BS, t128 = (nloc + TRH - 1) / TRH;
+    int *f = (int *)ws_alloc(sizeof(int) * (t256 + t128));
+    RB_CUDA(cudaMemsetAsync(f, 0, sizeof(int) * (t256 + t128), ctx->stream));
+    k_ghost_tiles<<<grid1d(nloc), 256, 0, ctx->stream>>>(rpA, ciA, rpH, ciH, nloc, f, f + t256);
+    count_launch();
+    std::vector<int> h(t256 + t128);
+    RB_CUDA(cudaMemcpyAsync(h.data(), f, sizeof(int) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    ws_free(f);
+    M->ord = tile_order(std::vector<int>(h.begin(), h.begin() + t256), M->nint);
+    M->ord_h = tile_order(std::vector<int>(h.begin() + t256, h.end()), M->nint_h);
+    M->ntl = t256;
+    M->ntl_h = t128;
+  }
   if (dt == RBICG_F64) {
     csr_to_sell<double>(ctx, nloc, rpA, ciA, (const double *)vA, M->A);
     csr_to_sell<double>(ctx, nloc, rpH, ciH, (const double *)vH, M->AH);
