@@ -20,6 +20,8 @@
 #include <thread>
 #include <tuple>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3 (no link dependency)
+
 #include "internal.h"
 #include "dist_plan.h"
 
@@ -165,11 +167,14 @@ static bool trace_on() {
   return on;
 }
 static std::map<std::string, std::pair<double, int>> g_trace;
+// Every Phase is also an NVTX range (per-phase ranges for nsys /
+// ncu --nvtx); the solve's top-level stages are NvtxSeq ranges below.
 struct Phase {
   const char *nm;
   cudaStream_t s;
   double t0;
   Phase(const char *n, cudaStream_t st) : nm(n), s(st), t0(0) {
+    nvtxRangePushA(n);
     if (trace_on()) {
       cudaStreamSynchronize(s);
       t0 = std::chrono::duration<double, std::milli>(
@@ -185,7 +190,17 @@ struct Phase {
       e.first += t1 - t0;
       e.second += 1;
     }
+    nvtxRangePop();
   }
+};
+// consecutive NVTX ranges of one host thread: next() closes the open one
+struct NvtxSeq {
+  explicit NvtxSeq(const char *first) { nvtxRangePushA(first); }
+  void next(const char *nm) {
+    nvtxRangePop();
+    nvtxRangePushA(nm);
+  }
+  ~NvtxSeq() { nvtxRangePop(); }
 };
 static void trace_dump() {
   if (!trace_on()) return;
@@ -2083,8 +2098,16 @@ static int solve_t(rbicg_ctx *ctx, const rbicg_mat *A, const void *b, const void
   const double t_start = now_ms();
   static const bool timing = getenv("RBICG_TIMING") != nullptr;
   std::vector<std::pair<const char *, double>> marks;
+  // NVTX: rbicg.setup, .refresh, .init, .capture, .loop, .join, .step7, .output
+  NvtxSeq nv("rbicg.setup");
   auto mark = [&](const char *nm) {
     if (timing) marks.emplace_back(nm, now_ms());
+    static const std::map<std::string, const char *> nxt = {
+        {"setup", "rbicg.refresh"}, {"refresh", "rbicg.init"}, {"init", "rbicg.capture"},
+        {"capture", "rbicg.loop"},  {"loop", "rbicg.join"},    {"join", "rbicg.step7"},
+        {"finish", "rbicg.output"}};
+    auto it = nxt.find(nm);
+    if (it != nxt.end()) nv.next(it->second);
   };
   Solver<T> S;
   S.pc = P;
