@@ -337,6 +337,13 @@ void build_matrix_local(rbicg_ctx *ctx, int64_t nloc, const int32_t *rpA, const 
     RB_CUDA(cudaMemcpyAsync(h.data(), f, sizeof(int) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
     ws_free(f);
+    // RBICG_FORCE_HALO_SPLIT=1 (tests): the last eighth of the tiles counts as
+    // boundary even without ghosts, so a one-rank NCCL context runs the overlap
+    // (fork/join + two launches) inside its captured graph
+    if (getenv("RBICG_FORCE_HALO_SPLIT")) {
+      for (int64_t t = t256 - std::max<int64_t>(1, t256 / 8); t < t256; ++t) h[t] = 1;
+      for (int64_t t = t128 - std::max<int64_t>(1, t128 / 8); t < t128; ++t) h[t256 + t] = 1;
+    }
     M->ord = tile_order(std::vector<int>(h.begin(), h.begin() + t256), M->nint);
     M->ord_h = tile_order(std::vector<int>(h.begin() + t256, h.end()), M->nint_h);
     M->ntl = t256;
