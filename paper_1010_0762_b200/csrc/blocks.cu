@@ -90,11 +90,15 @@ __global__ void __launch_bounds__(256) k_spmm_wide(DevMat A, const T *__restrict
 
 // One thread per row computing all k outputs (KB >= k accumulators): the
 // row's SELL entries are read once (coalesced across the warp) and each
-// nonzero gathers one contiguous k-row of X; the output row is k contiguous
-// values.  A persistent grid of whole waves.
+// nonzero gathers one contiguous k-row of X.  k_spmm_rows0 (round 1, one
+// nonzero at a time, RBICG_SPMM_V=0) was latency-bound (C3 cycle end 0.65 ms
+// per SpMM, 2.9 TB/s); k_spmm_rows hoists a chunk of the row's SELL entries
+// and keeps that chunk's X rows in flight (16-byte loads and stores for even
+// k): 0.50 ms.  (Staging the output tile in shared memory for coalesced
+// stores measured 0.66 ms.)
 template <typename T, int KB>
-__global__ void __launch_bounds__(256) k_spmm_rows(DevMat A, const T *__restrict__ X,
-                                                   T *__restrict__ Y, int k) {
+__global__ void __launch_bounds__(256) k_spmm_rows0(DevMat A, const T *__restrict__ X,
+                                                    T *__restrict__ Y, int k) {
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < A.n;
        row += (int64_t)gridDim.x * blockDim.x) {
     const int64_t sl = row >> 5;
@@ -118,14 +122,82 @@ __global__ void __launch_bounds__(256) k_spmm_rows(DevMat A, const T *__restrict
       if (j < k) yr[j] = acc[j];
   }
 }
+template <typename T, int KB>
+__global__ void __launch_bounds__(256) k_spmm_rows(DevMat A, const T *__restrict__ X,
+                                                    T *__restrict__ Y, int k) {
+  constexpr int NQ = (192 / (KB * (int)sizeof(T))) < 1 ? 1 : ((192 / (KB * (int)sizeof(T))) > 4 ? 4 : (192 / (KB * (int)sizeof(T))));
+  const bool vec = sizeof(T) == 8 && (k % 2) == 0 && ((uintptr_t)X % 16) == 0 && ((uintptr_t)Y % 16) == 0;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < A.n;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sl = row >> 5;
+    const int lane = (int)(row & 31);
+    const int64_t off = A.sptr[sl];
+    const int w = (int)((A.sptr[sl + 1] - off) >> 5);
+    T acc[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) acc[j] = zero<T>();
+    for (int j0 = 0; j0 < w; j0 += NQ) {
+      int c[NQ];
+      T v[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const bool in = j0 + q < w;
+        c[q] = in ? __ldcs(A.cols + off + (j0 + q) * 32 + lane) : (int)row;
+        v[q] = in ? reinterpret_cast<const T *>(A.vals)[off + (j0 + q) * 32 + lane] : zero<T>();
+      }
+      T xv[NQ][KB];
+      if constexpr (sizeof(T) == 8 && KB % 2 == 0) {
+        if (vec) {
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+#pragma unroll
+            for (int j = 0; j < KB; j += 2) {
+              double2 t = j < k ? reinterpret_cast<const double2 *>(X + (int64_t)c[q] * k)[j / 2]
+                                : make_double2(0.0, 0.0);
+              xv[q][j] = t.x;
+              xv[q][j + 1] = t.y;
+            }
+        } else {
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+#pragma unroll
+            for (int j = 0; j < KB; ++j) xv[q][j] = j < k ? X[(int64_t)c[q] * k + j] : zero<T>();
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+          for (int j = 0; j < KB; ++j) xv[q][j] = j < k ? X[(int64_t)c[q] * k + j] : zero<T>();
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int j = 0; j < KB; ++j) acc[j] = mad(v[q], xv[q][j], acc[j]);
+    }
+    T *yr = Y + row * k;
+    if constexpr (sizeof(T) == 8 && KB % 2 == 0) {
+      if (vec) {
+#pragma unroll
+        for (int j = 0; j < KB; j += 2)
+          if (j < k) reinterpret_cast<double2 *>(yr)[j / 2] = make_double2(acc[j], acc[j + 1]);
+        continue;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < k) yr[j] = acc[j];
+  }
+}
 
 template <typename T, int KB>
 static void spmm_rows_launch(const DevMat &A, const T *X, T *Y, int k, cudaStream_t s, int nsm) {
+  static const bool v0 = getenv("RBICG_SPMM_V") && atoi(getenv("RBICG_SPMM_V")) == 0;
+  auto fn = v0 ? k_spmm_rows0<T, KB> : k_spmm_rows<T, KB>;
   int per = 1;
-  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_spmm_rows<T, KB>, 256, 0));
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, 0));
   const int64_t blocks = (A.n + 255) / 256;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)std::max(1, per) * nsm));
-  k_spmm_rows<T, KB><<<grid, 256, 0, s>>>(A, X, Y, k);
+  fn<<<grid, 256, 0, s>>>(A, X, Y, k);
 }
 
 template <typename T> void launch_spmm(const DevMat &A, const T *X, T *Y, int k, cudaStream_t s) {
@@ -271,6 +343,159 @@ __global__ void __launch_bounds__(256, (sizeof(T) * MX * MY > 256 ? 1 : 2)) k_gr
     }
 }
 
+// fp64 tensor-core Gram (real data): the same stages as k_gram2, stored
+// column-major ([col][row], column stride GMS = 36 doubles, so the fragment
+// loads of a half-warp -- 4 rows x 4 columns -- hit distinct banks), and each
+// warp of a 2 x 4 warp grid owns up to RTM x RTN 8 x 8 output tiles computed
+// by mma.sync m8n8k4 f64 (DMMA): per 4-row k-step RTM + RTN fragment loads
+// feed RTM * RTN MMAs (0.5-0.75 bytes of shared memory per FMA against 2 for
+// the 8 x 8 FFMA micro-tile, which is shared-memory bound).  One output tile
+// covers mX <= 8 * 2 * RTM, mY <= 8 * 4 * RTN; partials per chunk as k_gram2
+// (ng = 1).
+template <int RTM, int RTN, int GR, int NST>
+__global__ void __launch_bounds__(256) k_gram_mma(const ColDesc *__restrict__ X, int mX,
+                                                  const ColDesc *__restrict__ Y, int mY, int64_t n,
+                                                  int64_t chunk, double *__restrict__ part) {
+  constexpr int GMS = GR + 4;   // column stride (= 4 mod 16 doubles)
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  const int tXp = (mX + 7) / 8 * 8, tYp = (mY + 7) / 8 * 8;
+  const int ncol = tXp + tYp;
+  ColDesc *sd = reinterpret_cast<ColDesc *>(sm_raw);
+  double *sbase = reinterpret_cast<double *>(sm_raw + ((sizeof(ColDesc) * ncol + 15) / 16) * 16);
+  const int stage = ncol * GMS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int c = tid; c < ncol; c += 256) {
+    ColDesc d{nullptr, 0};
+    if (c < tXp) {
+      if (c < mX) d = X[c];
+    } else if (c - tXp < mY) {
+      d = Y[c - tXp];
+    }
+    sd[c] = d;
+  }
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(n, r0 + chunk);
+  // thread -> (row lr = tid % GR of the stage, columns tid / GR + i 256 / GR):
+  // no per-element index arithmetic (the loader dominated the instruction count)
+  const int lr = tid % GR, cstep = 256 / GR;
+  auto load = [&](int64_t rb, int buf) {
+    double *st = sbase + buf * stage + lr;
+    const int64_t row = rb + lr;
+    const bool rok = row < r1;
+    for (int c = tid / GR; c < ncol; c += cstep) {
+      const ColDesc d = sd[c];
+      const bool ok = rok && d.p != nullptr;
+      const double *src = reinterpret_cast<const double *>(ok ? d.p : (const void *)part);
+      cp_async_el(st + c * GMS, ok ? src + row * d.stride : src, ok);
+    }
+    cp_async_commit();
+  };
+  // warp w owns the output column tiles w, w + 8, ... (RTN of them) with
+  // every row tile (RTM >= TM): balanced for TN = 8 (C2/C3: 7 MMAs per warp
+  // and k-step), one B fragment reused by all RTM A fragments
+  const int TM = tXp / 8, TN = tYp / 8;
+  double acc[RTM][RTN][2];
+#pragma unroll
+  for (int i = 0; i < RTM; ++i)
+#pragma unroll
+    for (int j = 0; j < RTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int fr = lane & 3, fc = lane >> 2;   // fragment row (k) and column (m or n)
+  // NST-stage ring: NST - 1 stages in flight while one is consumed
+#pragma unroll
+  for (int q = 0; q < NST - 1; ++q) {
+    if (r0 + q * GR < r1) load(r0 + q * GR, q);
+    else cp_async_commit();
+  }
+  int buf = 0;
+  for (int64_t rb = r0; rb < r1; rb += GR, buf = (buf + 1) % NST) {
+    {
+      const int64_t rn = rb + (int64_t)(NST - 1) * GR;
+      if (rn < r1) load(rn, (buf + NST - 1) % NST);
+      else cp_async_commit();
+    }
+    cp_async_wait<NST - 1>();
+    __syncthreads();
+    const double *st = sbase + buf * stage;
+#pragma unroll 2
+    for (int k0 = 0; k0 < GR; k0 += 4) {
+      double a[RTM];
+#pragma unroll
+      for (int i = 0; i < RTM; ++i) a[i] = (i < TM) ? st[(i * 8 + fc) * GMS + k0 + fr] : 0.0;
+#pragma unroll
+      for (int j = 0; j < RTN; ++j) {
+        const int tn = warp + 8 * j;
+        if (tn >= TN) break;
+        const double b = st[(tXp + tn * 8 + fc) * GMS + k0 + fr];
+#pragma unroll
+        for (int i = 0; i < RTM; ++i)
+          if (i < TM)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                         : "d"(a[i]), "d"(b));
+      }
+    }
+    __syncthreads();
+  }
+  // D fragment: row fc (of the 8 x 8 tile), columns 2 fr, 2 fr + 1
+#pragma unroll
+  for (int i = 0; i < RTM; ++i)
+#pragma unroll
+    for (int j = 0; j < RTN; ++j) {
+      const int a = i * 8 + fc, tn = warp + 8 * j;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int bb = tn * 8 + 2 * fr + q;
+        if (i < TM && tn < TN && a < mX && bb < mY)
+          part[((int64_t)blockIdx.x * mX + a) * mY + bb] = acc[i][j][q];
+      }
+    }
+}
+
+// RTM = 10 row tiles, RTN = 2 column tiles per warp: X up to 80 columns, Y up
+// to 128 (every BASELINE pencil: C2/C3 51 x 61, C5 71 x 91); false when it
+// does not apply
+template <int GR, int NST>
+static bool gram_mma_run(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
+                         std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t strm) {
+  constexpr int RTM = 10, RTN = 2, GMS = GR + 4;
+  const int mX = (int)X.size(), mY = (int)Y.size();
+  if (mX > 8 * RTM || mY > 8 * 8 * RTN) return false;
+  const int ncol = (mX + 7) / 8 * 8 + (mY + 7) / 8 * 8;
+  const size_t smem = ((sizeof(ColDesc) * ncol + 15) / 16) * 16 + sizeof(double) * NST * (size_t)ncol * GMS;
+  static bool attr = false;
+  if (!attr) {
+    RB_CUDA(cudaFuncSetAttribute((const void *)k_gram_mma<RTM, RTN, GR, NST>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  if (smem > 200 * 1024) return false;
+  int per = 1;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gram_mma<RTM, RTN, GR, NST>, 256, smem));
+  const int64_t slots = (int64_t)std::max(1, per) * sm_budget(ctx->nsm);
+  int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4 * GR - 1) / (4 * GR), slots));
+  const int64_t chunk = ((n + nchunks - 1) / nchunks + GR - 1) / GR * GR;
+  nchunks = (int)((n + chunk - 1) / chunk);
+  const size_t desc_bytes = sizeof(ColDesc) * (mX + mY);
+  const size_t part_bytes = sizeof(double) * (size_t)nchunks * mX * mY;
+  const size_t g_bytes = sizeof(double) * (size_t)mX * mY;
+  char *buf = (char *)ws_alloc(desc_bytes + part_bytes + g_bytes + 64);
+  ColDesc *dX = (ColDesc *)buf;
+  double *dpart = (double *)(buf + ((desc_bytes + 15) / 16) * 16);
+  double *dG = dpart + (size_t)nchunks * mX * mY;
+  std::vector<ColDesc> both(X);
+  both.insert(both.end(), Y.begin(), Y.end());
+  RB_CUDA(cudaMemcpyAsync(dX, both.data(), desc_bytes, cudaMemcpyHostToDevice, strm));
+  k_gram_mma<RTM, RTN, GR, NST><<<nchunks, 256, smem, strm>>>(dX, mX, dX + mX, mY, n, chunk, dpart);
+  k_gram_reduce<double><<<(mX * mY * 32 + 255) / 256, 256, 0, strm>>>(dpart, nchunks, mX * mY, dG);
+  count_launch(2);
+  std::vector<double> h((size_t)mX * mY);
+  RB_CUDA(cudaMemcpyAsync(h.data(), dG, g_bytes, cudaMemcpyDeviceToHost, strm));
+  RB_CUDA(cudaStreamSynchronize(strm));
+  ws_free(buf);
+  for (size_t i = 0; i < h.size(); ++i) G[i] = cplx(h[i], 0.0);
+  return true;
+}
+
 template <typename T, int MX, int MY>
 static void gram2_run(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
                       std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t strm) {
@@ -334,6 +559,10 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   if constexpr (sizeof(T) == 16) {
     gram2_run<T, 4, 4>(X, Y, n, G, ctx, strm);
   } else {
+    // fp64 tensor cores (RBICG_GRAM2=88 / 48 / 44: the FFMA micro-tile forms)
+    // (16-row stages, 3-4 stages, TMA bulk staging per column segment and a
+    // 2 x 4 warp grid measured slower: 3.4-5.4 ms)
+    if (var == 0 && gram_mma_run<32, 2>(X, Y, n, G, ctx, strm)) return;
     if (var == 48) return gram2_run<T, 4, 8>(X, Y, n, G, ctx, strm);
     if (var == 44) return gram2_run<T, 4, 4>(X, Y, n, G, ctx, strm);
     gram2_run<T, 8, 8>(X, Y, n, G, ctx, strm);   // RBICG_GRAM2=88
@@ -349,7 +578,10 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
 // contiguous ranges).  Output order: |c_j|^2, |c~_j|^2, then c~_a^* c_b (a-major).
 // GCR rows per sub-tile (64; 288-row sub-tiles measured no faster at k = 10:
 // 93 vs 87 us on C2)
-static int gcr_rows(int) { return 64; }
+static int gcr_rows(int) {
+  static const int r = getenv("RBICG_GCR_ROWS") ? atoi(getenv("RBICG_GCR_ROWS")) : 128;
+  return r;
+}
 template <typename T>
 __global__ void __launch_bounds__(256) k_gram_cc(const T *__restrict__ C, const T *__restrict__ Ct, int k,
                                                  int64_t n, int64_t chunk, int GCR, T *__restrict__ part) {
@@ -464,7 +696,12 @@ void gram_cc(const T *C, const T *Ct, int k, int64_t n, std::vector<cplx> &out, 
   const size_t sm = std::max(sizeof(T) * 2 * 2 * GCR * (size_t)k,
                              sizeof(T) * 16 * (size_t)W * std::max(1, 256 / W));
   RB_CHECK(sm <= 160 * 1024, RBICG_EINVAL);
-  const int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, 4 * sm_budget(ctx->nsm)));
+  // one full wave of resident blocks (a partial second wave left SMs idle)
+  int per = 1;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gram_cc<T>, 256, sm));
+  static const int cps = getenv("RBICG_GCR_CPS") ? atoi(getenv("RBICG_GCR_CPS")) : 0;
+  const int nchunks = (int)std::max<int64_t>(
+      1, std::min<int64_t>((n + 1023) / 1024, (cps ? cps : std::max(1, per)) * sm_budget(ctx->nsm)));
   const int64_t chunk = ((n + nchunks - 1) / nchunks + GCR - 1) / GCR * GCR;
   const int nb = (int)((n + chunk - 1) / chunk);
   char *buf = (char *)ws_alloc(sizeof(T) * ((size_t)nb * np + np) + 64);
@@ -519,6 +756,89 @@ __global__ void __launch_bounds__(256) k_gemm_panels(const ColDesc *__restrict__
   }
 }
 
+// out (row-major n x p) = X (row-major n x m, ONE contiguous block) M: the
+// biorthogonalisation's U F, C F and the candidate's C_j N_p.
+// 256-row tiles of X (contiguous 256 m values) stream into shared memory by
+// cp.async, double buffered; thread = row (PB accumulators, M broadcast from
+// shared memory); the tile's output (contiguous 256 p values) is staged and
+// stored with 16-byte coalesced stores.  The strided-column form
+// (k_gemm_panels) ran these at 3.3 TB/s (C3, 0.33 ms per 10 -> 10 GEMM).
+template <typename T, int PB>
+__global__ void __launch_bounds__(256) k_gemm_rm(const T *__restrict__ X, int m, const T *__restrict__ M,
+                                                 int p, int64_t n, T *__restrict__ out) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  T *sM = reinterpret_cast<T *>(sm_raw);     // [m][PB]
+  T *sX = sM + (size_t)m * PB;               // 2 x [256 m]
+  T *sO = sX + (size_t)2 * 256 * m;          // [256 p]
+  const int tid = threadIdx.x;
+  for (int e = tid; e < m * PB; e += 256) {
+    const int a = e / PB, c = e % PB;
+    sM[e] = c < p ? M[a * p + c] : zero<T>();
+  }
+  const int64_t ntiles = (n + 255) / 256;
+  constexpr int PER = 16 / sizeof(T);
+  auto load = [&](int64_t tile, int buf) {
+    const int64_t base = tile * 256 * m;
+    const int ne = (int)min((int64_t)256, n - tile * 256) * m;
+    T *dst = sX + (size_t)buf * 256 * m;
+    for (int e = tid * PER; e < ne; e += 256 * PER) {
+      const int valid = max(0, min(PER, ne - e)) * (int)sizeof(T);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst + e)),
+                   "l"(X + base + e), "r"(valid)
+                   : "memory");
+    }
+    cp_async_commit();
+  };
+  int buf = 0;
+  if ((int64_t)blockIdx.x < ntiles) load(blockIdx.x, 0);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
+    if (tile + gridDim.x < ntiles) load(tile + gridDim.x, buf ^ 1);
+    else cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const int rows = (int)min((int64_t)256, n - tile * 256);
+    if (tid < rows) {
+      const T *xr = sX + (size_t)buf * 256 * m + (size_t)tid * m;
+      T acc[PB];
+#pragma unroll
+      for (int c = 0; c < PB; ++c) acc[c] = zero<T>();
+      for (int a = 0; a < m; ++a) {
+        const T xv = xr[a];
+#pragma unroll
+        for (int c = 0; c < PB; ++c) acc[c] = mad(xv, sM[a * PB + c], acc[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < PB; ++c)
+        if (c < p) sO[tid * p + c] = acc[c];
+    }
+    __syncthreads();
+    const int64_t ob = tile * 256 * p;
+    const int ne = rows * p;
+    if ((ob % PER) == 0) {
+      const int nv = ne / PER;
+      for (int e = tid; e < nv; e += 256)
+        reinterpret_cast<double2 *>(out + ob)[e] = reinterpret_cast<const double2 *>(sO)[e];
+      for (int e = nv * PER + tid; e < ne; e += 256) out[ob + e] = sO[e];
+    } else {
+      for (int e = tid; e < ne; e += 256) out[ob + e] = sO[e];
+    }
+    // (the next iteration's __syncthreads orders these sO reads before its writes)
+  }
+}
+
+template <typename T, int PB>
+static void gemm_rm_launch(const T *X, int m, const T *dM, int p, int64_t n, T *out, rbicg_ctx *ctx,
+                           cudaStream_t strm) {
+  const size_t sm = sizeof(T) * ((size_t)m * PB + (size_t)2 * 256 * m + (size_t)256 * p);
+  RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
+  int per = 1;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gemm_rm<T, PB>, 256, sm));
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((n + 255) / 256, (int64_t)std::max(1, per) * sm_budget(ctx->nsm)));
+  k_gemm_rm<T, PB><<<grid, 256, sm, strm>>>(X, m, dM, p, n, out);
+  count_launch();
+}
+
 template <typename T, int PB>
 static void gemm_launch(const ColDesc *dX, int mX, const T *dM, int p, int64_t n, T *out,
                         T *out_last, rbicg_ctx *ctx, cudaStream_t strm) {
@@ -563,7 +883,20 @@ void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int 
     RB_CUDA(cudaMemcpyAsync(dX, X.data(), sizeof(ColDesc) * mX, cudaMemcpyHostToDevice, strm));
     RB_CUDA(cudaMemcpyAsync(dM, hM.data(), sizeof(T) * hM.size(), cudaMemcpyHostToDevice, strm));
   }
-  if (p <= 4) gemm_launch<T, 4>(dX, mX, dM, p, n, out, out_last, ctx, strm);
+  // the columns of ONE row-major n x mX block (U, C of a basis): staged tiles
+  bool rm = !out_last && mX > 0 && X[0].stride == mX && ((uintptr_t)X[0].p % 16) == 0 && !v1;
+  for (int a = 1; rm && a < mX; ++a)
+    rm = X[a].stride == mX && (const char *)X[a].p == (const char *)X[0].p + (size_t)a * sizeof(T);
+  static const bool rm_off = getenv("RBICG_GEMM_RM") && atoi(getenv("RBICG_GEMM_RM")) == 0;
+  if (rm && !rm_off) {
+    const T *X0 = reinterpret_cast<const T *>(X[0].p);
+    if (p <= 4) gemm_rm_launch<T, 4>(X0, mX, dM, p, n, out, ctx, strm);
+    else if (p <= 8) gemm_rm_launch<T, 8>(X0, mX, dM, p, n, out, ctx, strm);
+    else if (p <= 12) gemm_rm_launch<T, 12>(X0, mX, dM, p, n, out, ctx, strm);
+    else if (p <= 16) gemm_rm_launch<T, 16>(X0, mX, dM, p, n, out, ctx, strm);
+    else if (p <= 24) gemm_rm_launch<T, 24>(X0, mX, dM, p, n, out, ctx, strm);
+    else gemm_rm_launch<T, 32>(X0, mX, dM, p, n, out, ctx, strm);
+  } else if (p <= 4) gemm_launch<T, 4>(dX, mX, dM, p, n, out, out_last, ctx, strm);
   else if (p <= 8) gemm_launch<T, 8>(dX, mX, dM, p, n, out, out_last, ctx, strm);
   else if (p <= 12) gemm_launch<T, 12>(dX, mX, dM, p, n, out, out_last, ctx, strm);
   else if (p <= 16) gemm_launch<T, 16>(dX, mX, dM, p, n, out, out_last, ctx, strm);
@@ -768,6 +1101,14 @@ void prepare_block_kernels() {
   RB_CUDA(cudaFuncSetAttribute(k_gram_cc<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_spmm<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   RB_CUDA(cudaFuncSetAttribute(k_spmm<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+#define RB_SATTR(T, KB)                                                                      \
+  RB_CUDA(cudaFuncSetAttribute(k_gemm_rm<T, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                               200 * 1024));
+  RB_SATTR(double, 4) RB_SATTR(double, 8) RB_SATTR(double, 12) RB_SATTR(double, 16)
+  RB_SATTR(double, 24) RB_SATTR(double, 32)
+  RB_SATTR(zc, 4) RB_SATTR(zc, 8) RB_SATTR(zc, 12) RB_SATTR(zc, 16) RB_SATTR(zc, 24)
+  RB_SATTR(zc, 32)
+#undef RB_SATTR
 #define RB_GATTR(T, PB)                                                                      \
   RB_CUDA(cudaFuncSetAttribute(k_gemm_panels<T, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                200 * 1024));

@@ -40,7 +40,8 @@ SWITCHES = [
     ("RBICG_SPMM_SLICE", "1"), ("RBICG_SYNC_CYCLE", "1"), ("RBICG_SIDE_SMS", "0"),
     ("RBICG_SIDE_PRIO", "h"), ("RBICG_U_EARLY", "1"), ("RBICG_C_SPMM", "1"),
     ("RBICG_GEMM_RPT", "1"), ("RBICG_GEMM_PANELS_V1", "1"), ("RBICG_GRAM2", "48"),
-    ("RBICG_GRAM2", "44"), ("RBICG_TMP_U_EAGER", "1"), ("RBICG_C_CHECK", "1"),
+    ("RBICG_GRAM2", "44"), ("RBICG_GRAM2", "88"), ("RBICG_SPMM_V", "0"), ("RBICG_GEMM_RM", "0"),
+    ("RBICG_GCR_ROWS", "64"), ("RBICG_TMP_U_EAGER", "1"), ("RBICG_C_CHECK", "1"),
     ("RBICG_TRACE", "1"), ("RBICG_TIMING", "1"), ("RBICG_TRSV_BLOCKS", "8"),
 ]
 
