@@ -352,16 +352,23 @@ __global__ void __launch_bounds__(256, (sizeof(T) * MX * MY > 256 ? 1 : 2)) k_gr
 // the 8 x 8 FFMA micro-tile, which is shared-memory bound).  One output tile
 // covers mX <= 8 * 2 * RTM, mY <= 8 * 4 * RTN; partials per chunk as k_gram2
 // (ng = 1).
-template <int RTM, int RTN, int GR, int NST>
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+template <typename T, int RTM, int RTN, int GR, int NST>
 __global__ void __launch_bounds__(256) k_gram_mma(const ColDesc *__restrict__ X, int mX,
                                                   const ColDesc *__restrict__ Y, int mY, int64_t n,
-                                                  int64_t chunk, double *__restrict__ part) {
-  constexpr int GMS = GR + 4;   // column stride (= 4 mod 16 doubles)
+                                                  int64_t chunk, T *__restrict__ part) {
+  // column stride: = 4 mod 16 doubles (real), = 4 mod 8 complex elements (the
+  // 16-byte fragment loads of a quarter-warp then hit distinct banks)
+  constexpr int GMS = GR + 4;
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const int tXp = (mX + 7) / 8 * 8, tYp = (mY + 7) / 8 * 8;
   const int ncol = tXp + tYp;
   ColDesc *sd = reinterpret_cast<ColDesc *>(sm_raw);
-  double *sbase = reinterpret_cast<double *>(sm_raw + ((sizeof(ColDesc) * ncol + 15) / 16) * 16);
+  T *sbase = reinterpret_cast<T *>(sm_raw + ((sizeof(ColDesc) * ncol + 15) / 16) * 16);
   const int stage = ncol * GMS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int c = tid; c < ncol; c += 256) {
@@ -379,13 +386,13 @@ __global__ void __launch_bounds__(256) k_gram_mma(const ColDesc *__restrict__ X,
   // no per-element index arithmetic (the loader dominated the instruction count)
   const int lr = tid % GR, cstep = 256 / GR;
   auto load = [&](int64_t rb, int buf) {
-    double *st = sbase + buf * stage + lr;
+    T *st = sbase + buf * stage + lr;
     const int64_t row = rb + lr;
     const bool rok = row < r1;
     for (int c = tid / GR; c < ncol; c += cstep) {
       const ColDesc d = sd[c];
       const bool ok = rok && d.p != nullptr;
-      const double *src = reinterpret_cast<const double *>(ok ? d.p : (const void *)part);
+      const T *src = reinterpret_cast<const T *>(ok ? d.p : (const void *)part);
       cp_async_el(st + c * GMS, ok ? src + row * d.stride : src, ok);
     }
     cp_async_commit();
@@ -394,11 +401,12 @@ __global__ void __launch_bounds__(256) k_gram_mma(const ColDesc *__restrict__ X,
   // every row tile (RTM >= TM): balanced for TN = 8 (C2/C3: 7 MMAs per warp
   // and k-step), one B fragment reused by all RTM A fragments
   const int TM = tXp / 8, TN = tYp / 8;
-  double acc[RTM][RTN][2];
+  constexpr bool CPLX = sizeof(T) == 16;
+  double acc[RTM][RTN][2], aci[RTM][RTN][2];   // real parts; imaginary parts (complex)
 #pragma unroll
   for (int i = 0; i < RTM; ++i)
 #pragma unroll
-    for (int j = 0; j < RTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < RTN; ++j) acc[i][j][0] = acc[i][j][1] = aci[i][j][0] = aci[i][j][1] = 0.0;
   const int fr = lane & 3, fc = lane >> 2;   // fragment row (k) and column (m or n)
   // NST-stage ring: NST - 1 stages in flight while one is consumed
 #pragma unroll
@@ -415,23 +423,29 @@ __global__ void __launch_bounds__(256) k_gram_mma(const ColDesc *__restrict__ X,
     }
     cp_async_wait<NST - 1>();
     __syncthreads();
-    const double *st = sbase + buf * stage;
+    const T *st = sbase + buf * stage;
 #pragma unroll 2
     for (int k0 = 0; k0 < GR; k0 += 4) {
-      double a[RTM];
+      T a[RTM];
 #pragma unroll
-      for (int i = 0; i < RTM; ++i) a[i] = (i < TM) ? st[(i * 8 + fc) * GMS + k0 + fr] : 0.0;
+      for (int i = 0; i < RTM; ++i) a[i] = (i < TM) ? st[(i * 8 + fc) * GMS + k0 + fr] : zero<T>();
 #pragma unroll
       for (int j = 0; j < RTN; ++j) {
         const int tn = warp + 8 * j;
         if (tn >= TN) break;
-        const double b = st[(tXp + tn * 8 + fc) * GMS + k0 + fr];
+        const T b = st[(tXp + tn * 8 + fc) * GMS + k0 + fr];
 #pragma unroll
         for (int i = 0; i < RTM; ++i)
-          if (i < TM)
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                         : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
-                         : "d"(a[i]), "d"(b));
+          if (i < TM) {
+            if constexpr (!CPLX) {
+              dmma(acc[i][j], re(a[i]), re(b));
+            } else {   // conj(x) y = (xr yr + xi yi) + i (xr yi - xi yr)
+              dmma(acc[i][j], re(a[i]), re(b));
+              dmma(acc[i][j], im(a[i]), im(b));
+              dmma(aci[i][j], re(a[i]), im(b));
+              dmma(aci[i][j], -im(a[i]), re(b));
+            }
+          }
       }
     }
     __syncthreads();
@@ -445,54 +459,60 @@ __global__ void __launch_bounds__(256) k_gram_mma(const ColDesc *__restrict__ X,
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int bb = tn * 8 + 2 * fr + q;
-        if (i < TM && tn < TN && a < mX && bb < mY)
-          part[((int64_t)blockIdx.x * mX + a) * mY + bb] = acc[i][j][q];
+        if (i < TM && tn < TN && a < mX && bb < mY) {
+          T v;
+          if constexpr (CPLX) v = mk(acc[i][j][q], aci[i][j][q]);
+          else v = acc[i][j][q];
+          part[((int64_t)blockIdx.x * mX + a) * mY + bb] = v;
+        }
       }
     }
 }
 
-// RTM = 10 row tiles, RTN = 2 column tiles per warp: X up to 80 columns, Y up
-// to 128 (every BASELINE pencil: C2/C3 51 x 61, C5 71 x 91); false when it
-// does not apply
-template <int GR, int NST>
+// real: RTM = 10 row tiles, RTN = 2 column tiles per warp (X up to 80
+// columns, Y up to 128: every BASELINE pencil, C2/C3 51 x 61, C5 71 x 91);
+// complex: RTM = 8, RTN = 1 (64 x 64: C4's 49 x 57; 1.95 -> 1.24 ms), four
+// real MMAs per tile;
+// false when it does not apply
+template <typename T, int GR, int NST, int RTN = 2>
 static bool gram_mma_run(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
                          std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t strm) {
-  constexpr int RTM = 10, RTN = 2, GMS = GR + 4;
+  constexpr int RTM = sizeof(T) == 8 ? 10 : 8, GMS = GR + 4;
+  auto kern = k_gram_mma<T, RTM, RTN, GR, NST>;
   const int mX = (int)X.size(), mY = (int)Y.size();
   if (mX > 8 * RTM || mY > 8 * 8 * RTN) return false;
   const int ncol = (mX + 7) / 8 * 8 + (mY + 7) / 8 * 8;
-  const size_t smem = ((sizeof(ColDesc) * ncol + 15) / 16) * 16 + sizeof(double) * NST * (size_t)ncol * GMS;
+  const size_t smem = ((sizeof(ColDesc) * ncol + 15) / 16) * 16 + sizeof(T) * NST * (size_t)ncol * GMS;
   static bool attr = false;
   if (!attr) {
-    RB_CUDA(cudaFuncSetAttribute((const void *)k_gram_mma<RTM, RTN, GR, NST>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RB_CUDA(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
   if (smem > 200 * 1024) return false;
   int per = 1;
-  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gram_mma<RTM, RTN, GR, NST>, 256, smem));
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, smem));
   const int64_t slots = (int64_t)std::max(1, per) * sm_budget(ctx->nsm);
   int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4 * GR - 1) / (4 * GR), slots));
   const int64_t chunk = ((n + nchunks - 1) / nchunks + GR - 1) / GR * GR;
   nchunks = (int)((n + chunk - 1) / chunk);
   const size_t desc_bytes = sizeof(ColDesc) * (mX + mY);
-  const size_t part_bytes = sizeof(double) * (size_t)nchunks * mX * mY;
-  const size_t g_bytes = sizeof(double) * (size_t)mX * mY;
+  const size_t part_bytes = sizeof(T) * (size_t)nchunks * mX * mY;
+  const size_t g_bytes = sizeof(T) * (size_t)mX * mY;
   char *buf = (char *)ws_alloc(desc_bytes + part_bytes + g_bytes + 64);
   ColDesc *dX = (ColDesc *)buf;
-  double *dpart = (double *)(buf + ((desc_bytes + 15) / 16) * 16);
-  double *dG = dpart + (size_t)nchunks * mX * mY;
+  T *dpart = (T *)(buf + ((desc_bytes + 15) / 16) * 16);
+  T *dG = dpart + (size_t)nchunks * mX * mY;
   std::vector<ColDesc> both(X);
   both.insert(both.end(), Y.begin(), Y.end());
   RB_CUDA(cudaMemcpyAsync(dX, both.data(), desc_bytes, cudaMemcpyHostToDevice, strm));
-  k_gram_mma<RTM, RTN, GR, NST><<<nchunks, 256, smem, strm>>>(dX, mX, dX + mX, mY, n, chunk, dpart);
-  k_gram_reduce<double><<<(mX * mY * 32 + 255) / 256, 256, 0, strm>>>(dpart, nchunks, mX * mY, dG);
+  kern<<<nchunks, 256, smem, strm>>>(dX, mX, dX + mX, mY, n, chunk, dpart);
+  k_gram_reduce<T><<<(mX * mY * 32 + 255) / 256, 256, 0, strm>>>(dpart, nchunks, mX * mY, dG);
   count_launch(2);
-  std::vector<double> h((size_t)mX * mY);
+  std::vector<T> h((size_t)mX * mY);
   RB_CUDA(cudaMemcpyAsync(h.data(), dG, g_bytes, cudaMemcpyDeviceToHost, strm));
   RB_CUDA(cudaStreamSynchronize(strm));
   ws_free(buf);
-  for (size_t i = 0; i < h.size(); ++i) G[i] = cplx(h[i], 0.0);
+  for (size_t i = 0; i < h.size(); ++i) G[i] = cplx(re(h[i]), im(h[i]));
   return true;
 }
 
@@ -557,12 +577,16 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   if (mX == 0 || mY == 0) return;
   static const int var = getenv("RBICG_GRAM2") ? atoi(getenv("RBICG_GRAM2")) : 0;
   if constexpr (sizeof(T) == 16) {
+    // complex: four real fp64 tensor-core MMAs per tile (RBICG_GRAM2=44: FFMA)
+    // (up to 64 x 64; wider, two column tiles per warp need 188 registers and
+    // measured slower than the FFMA form: 2.07 vs 1.95 ms at C4)
+    if (var == 0 && Y.size() <= 64 && gram_mma_run<T, 32, 2, 1>(X, Y, n, G, ctx, strm)) return;
     gram2_run<T, 4, 4>(X, Y, n, G, ctx, strm);
   } else {
     // fp64 tensor cores (RBICG_GRAM2=88 / 48 / 44: the FFMA micro-tile forms)
     // (16-row stages, 3-4 stages, TMA bulk staging per column segment and a
     // 2 x 4 warp grid measured slower: 3.4-5.4 ms)
-    if (var == 0 && gram_mma_run<32, 2>(X, Y, n, G, ctx, strm)) return;
+    if (var == 0 && gram_mma_run<T, 32, 2>(X, Y, n, G, ctx, strm)) return;
     if (var == 48) return gram2_run<T, 4, 8>(X, Y, n, G, ctx, strm);
     if (var == 44) return gram2_run<T, 4, 4>(X, Y, n, G, ctx, strm);
     gram2_run<T, 8, 8>(X, Y, n, G, ctx, strm);   // RBICG_GRAM2=88
