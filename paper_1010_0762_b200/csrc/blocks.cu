@@ -203,8 +203,11 @@ static void spmm_rows_launch(const DevMat &A, const T *X, T *Y, int k, cudaStrea
 template <typename T> void launch_spmm(const DevMat &A, const T *X, T *Y, int k, cudaStream_t s) {
   if (k <= 0) return;
   RB_CHECK(k <= KMAX, RBICG_EINVAL);
+  // real data: the row form (C3 cycle end 0.50 vs 0.65 ms for the slice form);
+  // complex: the slice form (thread per (row, column): a warp's gathers cover
+  // 32 / k whole 16k-byte X rows) -- C4 0.104 vs 0.25 ms
   static const bool rows_form = !getenv("RBICG_SPMM_SLICE");
-  if (rows_form && A.max_w <= 64) {
+  if (rows_form && sizeof(T) == 8 && A.max_w <= 64) {
     int dev = 0, nsm = 148;
     RB_CUDA(cudaGetDevice(&dev));
     RB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -578,9 +581,24 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
   static const int var = getenv("RBICG_GRAM2") ? atoi(getenv("RBICG_GRAM2")) : 0;
   if constexpr (sizeof(T) == 16) {
     // complex: four real fp64 tensor-core MMAs per tile (RBICG_GRAM2=44: FFMA)
-    // (up to 64 x 64; wider, two column tiles per warp need 188 registers and
-    // measured slower than the FFMA form: 2.07 vs 1.95 ms at C4)
-    if (var == 0 && Y.size() <= 64 && gram_mma_run<T, 32, 2, 1>(X, Y, n, G, ctx, strm)) return;
+    // (up to 64 x 64 per launch; a wider Y is split into 64-column pieces --
+    // two column tiles per warp need 188 registers and measured slower than the
+    // FFMA form, 2.07 vs 1.95 ms at C4)
+    if (var == 0 && X.size() <= 64) {
+      const int mX = (int)X.size(), mY = (int)Y.size();
+      bool ok = true;
+      for (int y0 = 0; y0 < mY && ok; y0 += 64) {
+        const int w = std::min(64, mY - y0);
+        std::vector<ColDesc> Yp(Y.begin() + y0, Y.begin() + y0 + w);
+        std::vector<cplx> Gp;
+        Gp.assign((size_t)mX * w, cplx(0, 0));
+        ok = gram_mma_run<T, 32, 2, 1>(X, Yp, n, Gp, ctx, strm);
+        if (ok)
+          for (int a = 0; a < mX; ++a)
+            for (int b = 0; b < w; ++b) G[(size_t)a * mY + y0 + b] = Gp[(size_t)a * w + b];
+      }
+      if (ok) return;
+    }
     gram2_run<T, 4, 4>(X, Y, n, G, ctx, strm);
   } else {
     // fp64 tensor cores (RBICG_GRAM2=88 / 48 / 44: the FFMA micro-tile forms)
