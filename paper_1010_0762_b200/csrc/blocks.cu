@@ -122,10 +122,11 @@ __global__ void __launch_bounds__(256) k_spmm_rows0(DevMat A, const T *__restric
       if (j < k) yr[j] = acc[j];
   }
 }
-template <typename T, int KB>
-__global__ void __launch_bounds__(256) k_spmm_rows(DevMat A, const T *__restrict__ X,
+template <typename T, int KB, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_spmm_rows(DevMat A, const T *__restrict__ X,
                                                     T *__restrict__ Y, int k) {
-  constexpr int NQ = (192 / (KB * (int)sizeof(T))) < 1 ? 1 : ((192 / (KB * (int)sizeof(T))) > 4 ? 4 : (192 / (KB * (int)sizeof(T))));
+  constexpr int NQ0 = (192 / (KB * (int)sizeof(T))) < 1 ? 1 : ((192 / (KB * (int)sizeof(T))) > 4 ? 4 : (192 / (KB * (int)sizeof(T))));
+  constexpr int NQ = MINB >= 3 && KB >= 8 ? 1 : NQ0;
   const bool vec = sizeof(T) == 8 && (k % 2) == 0 && ((uintptr_t)X % 16) == 0 && ((uintptr_t)Y % 16) == 0;
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < A.n;
        row += (int64_t)gridDim.x * blockDim.x) {
@@ -192,7 +193,15 @@ __global__ void __launch_bounds__(256) k_spmm_rows(DevMat A, const T *__restrict
 template <typename T, int KB>
 static void spmm_rows_launch(const DevMat &A, const T *X, T *Y, int k, cudaStream_t s, int nsm) {
   static const bool v0 = getenv("RBICG_SPMM_V") && atoi(getenv("RBICG_SPMM_V")) == 0;
-  auto fn = v0 ? k_spmm_rows0<T, KB> : k_spmm_rows<T, KB>;
+  // resident blocks per SM the kernel is compiled for (register cap; the
+  // gathers are latency-bound: ncu long-scoreboard stalls dominate at 2 blocks
+  // of 94 registers).  3 (64 registers, one nonzero's X row per step for
+  // k >= 8): C3 k = 10 SpMM 503 -> 435 us (profiles/r02_spmm_minb.txt);
+  // RBICG_SPMM_MINB=1 restores the uncapped form (same FMA order, same bits)
+  static const int minb = getenv("RBICG_SPMM_MINB") ? atoi(getenv("RBICG_SPMM_MINB")) : 3;
+  auto fn = v0 ? k_spmm_rows0<T, KB>
+               : (minb >= 4 ? k_spmm_rows<T, KB, 4>
+                            : (minb == 3 ? k_spmm_rows<T, KB, 3> : (minb == 2 ? k_spmm_rows<T, KB, 2> : k_spmm_rows<T, KB>)));
   int per = 1;
   RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, 0));
   const int64_t blocks = (A.n + 255) / 256;
@@ -346,21 +355,25 @@ __global__ void __launch_bounds__(256, (sizeof(T) * MX * MY > 256 ? 1 : 2)) k_gr
     }
 }
 
-// fp64 tensor-core Gram (real data): the same stages as k_gram2, stored
-// column-major ([col][row], column stride GMS = 36 doubles, so the fragment
-// loads of a half-warp -- 4 rows x 4 columns -- hit distinct banks), and each
-// warp of a 2 x 4 warp grid owns up to RTM x RTN 8 x 8 output tiles computed
-// by mma.sync m8n8k4 f64 (DMMA): per 4-row k-step RTM + RTN fragment loads
-// feed RTM * RTN MMAs (0.5-0.75 bytes of shared memory per FMA against 2 for
-// the 8 x 8 FFMA micro-tile, which is shared-memory bound).  One output tile
-// covers mX <= 8 * 2 * RTM, mY <= 8 * 4 * RTN; partials per chunk as k_gram2
-// (ng = 1).
+// fp64 tensor-core Gram: the same stages as k_gram2, stored column-major
+// ([col][row], column stride GMS = GR + 4 doubles, so the fragment loads of a
+// half-warp -- 4 rows x 4 columns -- hit distinct banks); the TM x TN grid of
+// 8 x 8 output tiles is computed by mma.sync m8n8k4 f64 (DMMA, the only fp64
+// tensor-core form on sm_100a).  Work split: the tiles in column-major order
+// (tm fastest) are cut into 8 contiguous ranges of ceil(TM*TN / 8) tiles, one
+// per warp, so every SM sub-partition (warps w, w + 4) gets the same number of
+// DMMAs.  (Round 2's first form gave warp w whole column tiles w, w + 8, ...:
+// with TN = 9 (C3: 61 x 71) warp 0 did twice the work and its sub-partition's
+// DMMA pipe bounded the kernel -- ncu: tensor pipe 62 % active, 3.19 ms.)
+// Within a range the B fragment of a column is reused by its consecutive row
+// tiles.  Partials per chunk as k_gram2 (ng = 1).  Complex: four real MMAs per
+// tile (conj(x) y).
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
-template <typename T, int RTM, int RTN, int GR, int NST>
+template <typename T, int NTW, int GR, int NST>
 __global__ void __launch_bounds__(256) k_gram_mma(const ColDesc *__restrict__ X, int mX,
                                                   const ColDesc *__restrict__ Y, int mY, int64_t n,
                                                   int64_t chunk, T *__restrict__ part) {
@@ -400,16 +413,34 @@ __global__ void __launch_bounds__(256) k_gram_mma(const ColDesc *__restrict__ X,
     }
     cp_async_commit();
   };
-  // warp w owns the output column tiles w, w + 8, ... (RTN of them) with
-  // every row tile (RTM >= TM): balanced for TN = 8 (C2/C3: 7 MMAs per warp
-  // and k-step), one B fragment reused by all RTM A fragments
-  const int TM = tXp / 8, TN = tYp / 8;
+  // this warp's tiles: linear indices [t0, t0 + nt) of the column-major grid
+  const int TM = tXp / 8, TN = tYp / 8, NT = TM * TN;
+  const int per = (NT + 7) / 8;
+  const int t0 = min(NT, warp * per), nt = min(NT, t0 + per) - t0;
+  const int tm0 = t0 % TM, tn0 = t0 / TM;
   constexpr bool CPLX = sizeof(T) == 16;
-  double acc[RTM][RTN][2], aci[RTM][RTN][2];   // real parts; imaginary parts (complex)
+  double acc[NTW][2], aci[NTW][2];   // real parts; imaginary parts (complex)
 #pragma unroll
-  for (int i = 0; i < RTM; ++i)
+  for (int t = 0; t < NTW; ++t) acc[t][0] = acc[t][1] = aci[t][0] = aci[t][1] = 0.0;
+  // fragment offsets of the warp's tiles, fixed for the whole kernel (slots
+  // t >= nt repeat the last tile: their loads stay in the stage, their MMAs
+  // are skipped); with them the inner loop has no index arithmetic and its
+  // loads can all be issued ahead of the MMAs
+  int oa[NTW], ob[NTW];
+  {
+    int tm = tm0, tn = min(tn0, TN - 1);
 #pragma unroll
-    for (int j = 0; j < RTN; ++j) acc[i][j][0] = acc[i][j][1] = aci[i][j][0] = aci[i][j][1] = 0.0;
+    for (int t = 0; t < NTW; ++t) {
+      oa[t] = tm * 8 * GMS;
+      ob[t] = tn * 8 * GMS;
+      if (t + 1 < nt) {
+        if (++tm == TM) {
+          tm = 0;
+          ++tn;
+        }
+      }
+    }
+  }
   const int fr = lane & 3, fc = lane >> 2;   // fragment row (k) and column (m or n)
   // NST-stage ring: NST - 1 stages in flight while one is consumed
 #pragma unroll
@@ -427,74 +458,93 @@ __global__ void __launch_bounds__(256) k_gram_mma(const ColDesc *__restrict__ X,
     cp_async_wait<NST - 1>();
     __syncthreads();
     const T *st = sbase + buf * stage;
+    const T *sa = st + fc * GMS + fr;                 // A fragments: X column tm * 8 + fc
+    const T *sb = st + (tXp + fc) * GMS + fr;         // B fragments: Y column tn * 8 + fc
 #pragma unroll 2
     for (int k0 = 0; k0 < GR; k0 += 4) {
-      T a[RTM];
+      T b = sb[ob[0] + k0];
 #pragma unroll
-      for (int i = 0; i < RTM; ++i) a[i] = (i < TM) ? st[(i * 8 + fc) * GMS + k0 + fr] : zero<T>();
-#pragma unroll
-      for (int j = 0; j < RTN; ++j) {
-        const int tn = warp + 8 * j;
-        if (tn >= TN) break;
-        const T b = st[(tXp + tn * 8 + fc) * GMS + k0 + fr];
-#pragma unroll
-        for (int i = 0; i < RTM; ++i)
-          if (i < TM) {
-            if constexpr (!CPLX) {
-              dmma(acc[i][j], re(a[i]), re(b));
-            } else {   // conj(x) y = (xr yr + xi yi) + i (xr yi - xi yr)
-              dmma(acc[i][j], re(a[i]), re(b));
-              dmma(acc[i][j], im(a[i]), im(b));
-              dmma(aci[i][j], re(a[i]), im(b));
-              dmma(aci[i][j], -im(a[i]), re(b));
-            }
+      for (int t = 0; t < NTW; ++t) {
+        if (t > 0 && ob[t] != ob[t - 1]) b = sb[ob[t] + k0];   // a new column tile
+        const T a = sa[oa[t] + k0];
+        if (t < nt) {
+          if constexpr (!CPLX) {
+            dmma(acc[t], re(a), re(b));
+          } else {   // conj(x) y = (xr yr + xi yi) + i (xr yi - xi yr)
+            dmma(acc[t], re(a), re(b));
+            dmma(acc[t], im(a), im(b));
+            dmma(aci[t], re(a), im(b));
+            dmma(aci[t], -im(a), re(b));
           }
+        }
       }
     }
     __syncthreads();
   }
   // D fragment: row fc (of the 8 x 8 tile), columns 2 fr, 2 fr + 1
+  int tm = tm0, tn = tn0;
 #pragma unroll
-  for (int i = 0; i < RTM; ++i)
-#pragma unroll
-    for (int j = 0; j < RTN; ++j) {
-      const int a = i * 8 + fc, tn = warp + 8 * j;
+  for (int t = 0; t < NTW; ++t) {
+    if (t < nt) {
+      const int a = tm * 8 + fc;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int bb = tn * 8 + 2 * fr + q;
-        if (i < TM && tn < TN && a < mX && bb < mY) {
+        if (a < mX && bb < mY) {
           T v;
-          if constexpr (CPLX) v = mk(acc[i][j][q], aci[i][j][q]);
-          else v = acc[i][j][q];
+          if constexpr (CPLX) v = mk(acc[t][q], aci[t][q]);
+          else v = acc[t][q];
           part[((int64_t)blockIdx.x * mX + a) * mY + bb] = v;
         }
       }
+      if (++tm == TM) {
+        tm = 0;
+        ++tn;
+      }
     }
+  }
 }
 
-// real: RTM = 10 row tiles, RTN = 2 column tiles per warp (X up to 80
-// columns, Y up to 128: every BASELINE pencil, C2/C3 51 x 61, C5 71 x 91);
-// complex: RTM = 8, RTN = 1 (64 x 64: C4's 49 x 57; 1.95 -> 1.24 ms), four
-// real MMAs per tile;
-// false when it does not apply
-template <typename T, int GR, int NST, int RTN = 2>
+// real: up to 10 x 16 tiles (X up to 80 columns, Y up to 128: every BASELINE
+// pencil, C2/C3 51..61 x 61..71, C5 71 x 91), NTW = 20 tiles per warp;
+// complex: up to 8 x 8 tiles (64 x 64 per launch: C4's 49 x 57), four real
+// MMAs per tile; false when it does not apply
+template <typename T, int GR, int NST>
 static bool gram_mma_run(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t n,
                          std::vector<cplx> &G, rbicg_ctx *ctx, cudaStream_t strm) {
-  constexpr int RTM = sizeof(T) == 8 ? 10 : 8, GMS = GR + 4;
-  auto kern = k_gram_mma<T, RTM, RTN, GR, NST>;
+  constexpr bool CPLX = sizeof(T) == 16;
+  constexpr int MAXM = CPLX ? 64 : 80, MAXN = CPLX ? 64 : 128;
+  constexpr int GMS = GR + 4;
   const int mX = (int)X.size(), mY = (int)Y.size();
-  if (mX > 8 * RTM || mY > 8 * 8 * RTN) return false;
+  if (mX > MAXM || mY > MAXN) return false;
+  // tiles per warp: the smallest instantiated NTW >= ceil(TM TN / 8)
+  const int per = ((mX + 7) / 8 * ((mY + 7) / 8) + 7) / 8;
+  void (*kern)(const ColDesc *, int, const ColDesc *, int, int64_t, int64_t, T *) = nullptr;
+  if constexpr (CPLX) {
+    if (per <= 2) kern = k_gram_mma<T, 2, GR, NST>;
+    else if (per <= 4) kern = k_gram_mma<T, 4, GR, NST>;
+    else if (per <= 6) kern = k_gram_mma<T, 6, GR, NST>;
+    else kern = k_gram_mma<T, 8, GR, NST>;
+  } else {
+    if (per <= 2) kern = k_gram_mma<T, 2, GR, NST>;
+    else if (per <= 4) kern = k_gram_mma<T, 4, GR, NST>;
+    else if (per <= 6) kern = k_gram_mma<T, 6, GR, NST>;
+    else if (per <= 7) kern = k_gram_mma<T, 7, GR, NST>;
+    else if (per <= 8) kern = k_gram_mma<T, 8, GR, NST>;
+    else if (per <= 9) kern = k_gram_mma<T, 9, GR, NST>;
+    else if (per <= 10) kern = k_gram_mma<T, 10, GR, NST>;
+    else if (per <= 12) kern = k_gram_mma<T, 12, GR, NST>;
+    else if (per <= 14) kern = k_gram_mma<T, 14, GR, NST>;
+    else if (per <= 16) kern = k_gram_mma<T, 16, GR, NST>;
+    else kern = k_gram_mma<T, 20, GR, NST>;
+  }
   const int ncol = (mX + 7) / 8 * 8 + (mY + 7) / 8 * 8;
   const size_t smem = ((sizeof(ColDesc) * ncol + 15) / 16) * 16 + sizeof(T) * NST * (size_t)ncol * GMS;
-  static bool attr = false;
-  if (!attr) {
-    RB_CUDA(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  RB_CUDA(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   if (smem > 200 * 1024) return false;
-  int per = 1;
-  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, smem));
-  const int64_t slots = (int64_t)std::max(1, per) * sm_budget(ctx->nsm);
+  int occ = 1;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+  const int64_t slots = (int64_t)std::max(1, occ) * sm_budget(ctx->nsm);
   int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4 * GR - 1) / (4 * GR), slots));
   const int64_t chunk = ((n + nchunks - 1) / nchunks + GR - 1) / GR * GR;
   nchunks = (int)((n + chunk - 1) / chunk);
@@ -592,7 +642,7 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
         std::vector<ColDesc> Yp(Y.begin() + y0, Y.begin() + y0 + w);
         std::vector<cplx> Gp;
         Gp.assign((size_t)mX * w, cplx(0, 0));
-        ok = gram_mma_run<T, 32, 2, 1>(X, Yp, n, Gp, ctx, strm);
+        ok = gram_mma_run<T, 32, 2>(X, Yp, n, Gp, ctx, strm);
         if (ok)
           for (int a = 0; a < mX; ++a)
             for (int b = 0; b < w; ++b) G[(size_t)a * mY + y0 + b] = Gp[(size_t)a * w + b];
@@ -726,6 +776,156 @@ __global__ void __launch_bounds__(256) k_gram_cc(const T *__restrict__ C, const 
   }
 }
 
+// fp64 tensor-core form (real data, the default): the register-tiled FFMA
+// kernel above is shared-memory bound (ncu, C3 k = 10: smem wavefronts 80 %
+// of peak, 0.50 ms for 1.13 GB, 0.35 of the HBM peak) -- every 4 x 4 tile
+// re-reads its operands.  Here each warp takes 4-row k-steps of the staged
+// rows and one fragment load per 8-column tile of C~ and of C feeds all
+// KT^2 tiles of C~^*C (mma.sync m8n8k4 f64); the column norms are plain FMAs
+// on the fragment registers (lane = (row k0 + (lane & 3), column lane >> 2)
+// of the tile), summed over the 4 row lanes at the end -- as diagonal MMA
+// tiles they doubled the MMA count (ncu: 0.29 ms, MMA-bound).
+// Stages: 128 rows of C and of C~ (contiguous), 3-deep cp.async ring.  Same
+// partial layout as k_gram_cc (|c_j|^2, |c~_j|^2, c~_a^*c_b).
+template <int KT>
+__global__ void __launch_bounds__(256) k_gram_cc_mma(const double *__restrict__ C,
+                                                     const double *__restrict__ Ct, int k, int64_t n,
+                                                     int64_t chunk, double *__restrict__ part) {
+  constexpr int GCR = 128, NST = 3, NTL = KT * KT + 2 * KT;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  double *sbase = reinterpret_cast<double *>(sm_raw);   // NST x [C rows | C~ rows]
+  double nt_[KT], nc_[KT];                              // per-lane column-norm partials
+  const int stage = 2 * GCR * k;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fr = lane & 3, fc = lane >> 2;
+  const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(n, r0 + chunk);
+  auto load = [&](int64_t rb, int buf) {
+    double *st = sbase + buf * stage;
+    const int rows = (int)min((int64_t)GCR, r1 - rb);
+    const int ne = GCR * k, nv = rows * k;
+    for (int q = 0; q < 2; ++q) {
+      const double *src = (q ? Ct : C) + rb * k;
+      double *dst = st + q * GCR * k;
+      for (int e = tid * 2; e < ne; e += 256 * 2) {
+        const int valid = max(0, min(2, nv - e)) * 8;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst + e)),
+                     "l"(valid ? src + e : src), "r"(valid)
+                     : "memory");
+      }
+    }
+    cp_async_commit();
+  };
+  double acc[KT * KT][2];   // C~^*C tiles (i-major)
+#pragma unroll
+  for (int t = 0; t < KT * KT; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < KT; ++i) nt_[i] = nc_[i] = 0.0;
+#pragma unroll
+  for (int q = 0; q < NST - 1; ++q) {
+    if (r0 + q * GCR < r1) load(r0 + q * GCR, q);
+    else cp_async_commit();
+  }
+  int buf = 0;
+  for (int64_t rb = r0; rb < r1; rb += GCR, buf = (buf + 1) % NST) {
+    {
+      const int64_t rn = rb + (int64_t)(NST - 1) * GCR;
+      if (rn < r1) load(rn, (buf + NST - 1) % NST);
+      else cp_async_commit();
+    }
+    cp_async_wait<NST - 1>();
+    __syncthreads();
+    const double *sc = sbase + buf * stage, *sct = sc + GCR * k;
+#pragma unroll 2
+    for (int ks = warp; ks < GCR / 4; ks += 8) {
+      const int ro = (ks * 4 + fr) * k;
+      double at[KT], bc[KT];
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+        const int col = i * 8 + fc;
+        at[i] = col < k ? sct[ro + col] : 0.0;
+        bc[i] = col < k ? sc[ro + col] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < KT; ++i)
+#pragma unroll
+        for (int j = 0; j < KT; ++j) dmma(acc[i * KT + j], at[i], bc[j]);
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+        nt_[i] = fma(at[i], at[i], nt_[i]);
+        nc_[i] = fma(bc[i], bc[i], nc_[i]);
+      }
+    }
+    __syncthreads();
+  }
+  // warp partials -> shared memory (reusing the stages), summed in warp order
+  double *red = sbase;   // [warp][tile][64]
+#pragma unroll
+  for (int t = 0; t < KT * KT; ++t) {
+    red[((size_t)warp * NTL + t) * 64 + fc * 8 + 2 * fr] = acc[t][0];
+    red[((size_t)warp * NTL + t) * 64 + fc * 8 + 2 * fr + 1] = acc[t][1];
+  }
+  // norms: sum the 4 row lanes (fr) of each column, store on the diagonal
+  // slots of the norm "tiles" (the layout the output loop reads)
+#pragma unroll
+  for (int i = 0; i < KT; ++i) {
+    double a = nt_[i], c = nc_[i];
+    a += __shfl_xor_sync(0xffffffffu, a, 1);
+    a += __shfl_xor_sync(0xffffffffu, a, 2);
+    c += __shfl_xor_sync(0xffffffffu, c, 1);
+    c += __shfl_xor_sync(0xffffffffu, c, 2);
+    if (fr == 0) {
+      red[((size_t)warp * NTL + KT * KT + i) * 64 + fc * 9] = a;
+      red[((size_t)warp * NTL + KT * KT + KT + i) * 64 + fc * 9] = c;
+    }
+  }
+  __syncthreads();
+  const int np = 2 * k + k * k;
+  for (int o = tid; o < np; o += 256) {
+    int t, e;
+    if (o < k) {   // |c_o|^2
+      t = KT * KT + KT + o / 8;
+      e = (o % 8) * 9;
+    } else if (o < 2 * k) {   // |c~_o|^2
+      t = KT * KT + (o - k) / 8;
+      e = ((o - k) % 8) * 9;
+    } else {   // c~_a^* c_b
+      const int a2 = (o - 2 * k) / k, b2 = (o - 2 * k) % k;
+      t = (a2 / 8) * KT + b2 / 8;
+      e = (a2 % 8) * 8 + b2 % 8;
+    }
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) sum += red[((size_t)w * NTL + t) * 64 + e];
+    part[(int64_t)blockIdx.x * np + o] = sum;
+  }
+}
+
+template <int KT>
+static void gram_cc_mma_launch(const double *C, const double *Ct, int k, int64_t n, double *dpart_out,
+                               int &nb_out, rbicg_ctx *ctx, cudaStream_t strm, double **buf_out) {
+  constexpr int GCR = 128, NST = 3, NTL = KT * KT + 2 * KT;
+  const size_t sm = std::max(sizeof(double) * NST * 2 * GCR * (size_t)k, sizeof(double) * 8 * NTL * 64);
+  static bool attr = false;
+  if (!attr) {
+    RB_CUDA(cudaFuncSetAttribute((const void *)k_gram_cc_mma<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024));
+    attr = true;
+  }
+  RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
+  int per = 1;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gram_cc_mma<KT>, 256, sm));
+  const int np = 2 * k + k * k;
+  int nchunks = (int)std::max<int64_t>(
+      1, std::min<int64_t>((n + 4 * GCR - 1) / (4 * GCR), (int64_t)std::max(1, per) * sm_budget(ctx->nsm)));
+  const int64_t chunk = ((n + nchunks - 1) / nchunks + GCR - 1) / GCR * GCR;
+  const int nb = (int)((n + chunk - 1) / chunk);
+  double *buf = (double *)ws_alloc(sizeof(double) * ((size_t)nb * np + np) + 64);
+  k_gram_cc_mma<KT><<<nb, 256, sm, strm>>>(C, Ct, k, n, chunk, buf);
+  (void)dpart_out;
+  nb_out = nb;
+  *buf_out = buf;
+}
+
 template <typename T>
 void gram_cc(const T *C, const T *Ct, int k, int64_t n, std::vector<cplx> &out, rbicg_ctx *ctx,
              cudaStream_t strm) {
@@ -734,6 +934,27 @@ void gram_cc(const T *C, const T *Ct, int k, int64_t n, std::vector<cplx> &out, 
   if (k == 0) return;
   const int kb = (k + 3) / 4, W = kb * kb + 2 * kb;
   RB_CHECK(W <= 256, RBICG_EINVAL);
+  static const bool ffma = getenv("RBICG_GRAM_CC_FFMA") != nullptr;
+  if constexpr (sizeof(T) == 8) {
+    // fp64 tensor cores (rows 16-byte aligned: C, C~ of the recycle blocks)
+    if (!ffma && ((uintptr_t)C % 16) == 0 && ((uintptr_t)Ct % 16) == 0) {
+      int nb = 0;
+      double *buf = nullptr;
+      if (k <= 8) gram_cc_mma_launch<1>(C, Ct, k, n, nullptr, nb, ctx, strm, &buf);
+      else if (k <= 16) gram_cc_mma_launch<2>(C, Ct, k, n, nullptr, nb, ctx, strm, &buf);
+      else if (k <= 24) gram_cc_mma_launch<3>(C, Ct, k, n, nullptr, nb, ctx, strm, &buf);
+      else gram_cc_mma_launch<4>(C, Ct, k, n, nullptr, nb, ctx, strm, &buf);
+      double *dG = buf + (size_t)nb * np;
+      k_gram_reduce<double><<<(np * 32 + 255) / 256, 256, 0, strm>>>(buf, nb, np, dG);
+      count_launch(2);
+      std::vector<double> h(np);
+      RB_CUDA(cudaMemcpyAsync(h.data(), dG, sizeof(double) * np, cudaMemcpyDeviceToHost, strm));
+      RB_CUDA(cudaStreamSynchronize(strm));
+      ws_free(buf);
+      for (int i = 0; i < np; ++i) out[i] = cplx(h[i], 0.0);
+      return;
+    }
+  }
   const int GCR = gcr_rows(k);
   const size_t sm = std::max(sizeof(T) * 2 * 2 * GCR * (size_t)k,
                              sizeof(T) * 16 * (size_t)W * std::max(1, 256 / W));
