@@ -505,6 +505,138 @@ __global__ void __launch_bounds__(256) k_gram_mma(const ColDesc *__restrict__ X,
   }
 }
 
+// Real data, the default: the same stages with a 2-D warp grid (WR x WC = 8
+// warps, warp w = (w / WC, w % WC)), each warp owning an RM x RN rectangle of
+// output tiles whose RM A fragments and RN B fragments it loads once per
+// k-step: RM + RN fragment loads feed RM * RN MMAs.  The flat per-warp tile
+// ranges above re-load an A fragment per tile and were bound by shared-memory
+// wavefronts (ncu, C3 7 x 8 tiles: 76 % of the smem peak, DMMA pipe 57 %);
+// the host picks (WR, RM, RN) for the shape by a cost model of the busiest
+// SM sub-partition's MMAs against the stage's shared-memory wavefronts.
+template <typename T, int RMX, int RNX, int GR, int NST>
+__global__ void __launch_bounds__(256) k_gram_mma2(const ColDesc *__restrict__ X, int mX,
+                                                   const ColDesc *__restrict__ Y, int mY, int64_t n,
+                                                   int64_t chunk, T *__restrict__ part, int WC, int RM,
+                                                   int RN) {
+  constexpr int GMS = GR + 4;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  const int tXp = (mX + 7) / 8 * 8, tYp = (mY + 7) / 8 * 8;
+  const int ncol = tXp + tYp;
+  ColDesc *sd = reinterpret_cast<ColDesc *>(sm_raw);
+  T *sbase = reinterpret_cast<T *>(sm_raw + ((sizeof(ColDesc) * ncol + 15) / 16) * 16);
+  const int stage = ncol * GMS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int c = tid; c < ncol; c += 256) {
+    ColDesc d{nullptr, 0};
+    if (c < tXp) {
+      if (c < mX) d = X[c];
+    } else if (c - tXp < mY) {
+      d = Y[c - tXp];
+    }
+    sd[c] = d;
+  }
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(n, r0 + chunk);
+  const int lr = tid % GR, cstep = 256 / GR;
+  auto load = [&](int64_t rb, int buf) {
+    T *st = sbase + buf * stage + lr;
+    const int64_t row = rb + lr;
+    const bool rok = row < r1;
+    for (int c = tid / GR; c < ncol; c += cstep) {
+      const ColDesc d = sd[c];
+      const bool ok = rok && d.p != nullptr;
+      const T *src = reinterpret_cast<const T *>(ok ? d.p : (const void *)part);
+      cp_async_el(st + c * GMS, ok ? src + row * d.stride : src, ok);
+    }
+    cp_async_commit();
+  };
+  const int TM = tXp / 8, TN = tYp / 8;
+  const int tm0 = (warp / WC) * RM, tn0 = (warp % WC) * RN;
+  const int rm = max(0, min(RM, TM - tm0)), rn = max(0, min(RN, TN - tn0));
+  double acc[RMX][RNX][2];
+#pragma unroll
+  for (int i = 0; i < RMX; ++i)
+#pragma unroll
+    for (int j = 0; j < RNX; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int fr = lane & 3, fc = lane >> 2;
+#pragma unroll
+  for (int q = 0; q < NST - 1; ++q) {
+    if (r0 + q * GR < r1) load(r0 + q * GR, q);
+    else cp_async_commit();
+  }
+  int buf = 0;
+  for (int64_t rb = r0; rb < r1; rb += GR, buf = (buf + 1) % NST) {
+    {
+      const int64_t rn_ = rb + (int64_t)(NST - 1) * GR;
+      if (rn_ < r1) load(rn_, (buf + NST - 1) % NST);
+      else cp_async_commit();
+    }
+    cp_async_wait<NST - 1>();
+    __syncthreads();
+    if (rm > 0 && rn > 0) {
+      const T *st = sbase + buf * stage;
+      const T *sa = st + (tm0 * 8 + fc) * GMS + fr;
+      const T *sb = st + (tXp + tn0 * 8 + fc) * GMS + fr;
+#pragma unroll 2
+      for (int k0 = 0; k0 < GR; k0 += 4) {
+        double a[RMX], b[RNX];
+#pragma unroll
+        for (int i = 0; i < RMX; ++i) a[i] = i < rm ? re(sa[i * 8 * GMS + k0]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < RNX; ++j) b[j] = j < rn ? re(sb[j * 8 * GMS + k0]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < RNX; ++j)
+          if (j < rn)
+#pragma unroll
+            for (int i = 0; i < RMX; ++i)
+              if (i < rm) dmma(acc[i][j], a[i], b[j]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < RMX; ++i)
+#pragma unroll
+    for (int j = 0; j < RNX; ++j)
+      if (i < rm && j < rn) {
+        const int a = (tm0 + i) * 8 + fc;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int bb = (tn0 + j) * 8 + 2 * fr + q;
+          if (a < mX && bb < mY) part[((int64_t)blockIdx.x * mX + a) * mY + bb] = T(acc[i][j][q]);
+        }
+      }
+}
+
+// warp-grid choice for k_gram_mma2: (WR, RM, RN) minimising
+// max(16 x MMAs of the busiest sub-partition, 2 x fragment loads + stage
+// writes) per k-step -- cycles of the DMMA pipe (16 per m8n8k4 f64, measured
+// 37 TFLOP/s) against shared-memory wavefronts (256-byte fragment loads)
+struct WarpGrid {
+  int WR, WC, RM, RN, cost;
+};
+static WarpGrid pick_warp_grid(int TM, int TN, int ncol, const int (*shapes)[2], int nshapes) {
+  WarpGrid best{0, 0, 0, 0, 1 << 30};
+  for (int WR : {1, 2, 4, 8}) {
+    const int WC = 8 / WR, RM = (TM + WR - 1) / WR, RN = (TN + WC - 1) / WC;
+    bool fits = false;
+    for (int q = 0; q < nshapes; ++q) fits |= RM <= shapes[q][0] && RN <= shapes[q][1];
+    if (!fits) continue;
+    int D[4] = {0, 0, 0, 0}, L = 0;
+    for (int w = 0; w < 8; ++w) {
+      const int r = std::max(0, std::min(RM, TM - (w / WC) * RM));
+      const int c = std::max(0, std::min(RN, TN - (w % WC) * RN));
+      D[w % 4] += r * c;
+      if (r > 0 && c > 0) L += r + c;
+    }
+    const int maxD = std::max(std::max(D[0], D[1]), std::max(D[2], D[3]));
+    // primary: the bound; ties (common: equal MMA balance) to fewer loads
+    const int cost = 4 * std::max(16 * maxD, 2 * L + ncol / 3) + (2 * L + ncol / 3) / 8;
+    if (cost < best.cost) best = WarpGrid{WR, WC, RM, RN, cost};
+  }
+  return best;
+}
+
 // real: up to 10 x 16 tiles (X up to 80 columns, Y up to 128: every BASELINE
 // pencil, C2/C3 51..61 x 61..71, C5 71 x 91), NTW = 20 tiles per warp;
 // complex: up to 8 x 8 tiles (64 x 64 per launch: C4's 49 x 57), four real
@@ -540,10 +672,54 @@ static bool gram_mma_run(const std::vector<ColDesc> &X, const std::vector<ColDes
   }
   const int ncol = (mX + 7) / 8 * 8 + (mY + 7) / 8 * 8;
   const size_t smem = ((sizeof(ColDesc) * ncol + 15) / 16) * 16 + sizeof(T) * NST * (size_t)ncol * GMS;
-  RB_CUDA(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  // real data: the 2-D warp grid (RBICG_GRAM_FLAT=1: the flat tile ranges)
+  static const bool flat = getenv("RBICG_GRAM_FLAT") != nullptr;
+  void (*kern2)(const ColDesc *, int, const ColDesc *, int, int64_t, int64_t, T *, int, int, int) = nullptr;
+  WarpGrid wg{};
+  if constexpr (!CPLX) {
+    if (!flat) {
+      // instantiated rectangles (RMX, RNX)
+      static const int shapes[][2] = {{2, 1}, {4, 1}, {7, 1}, {8, 1}, {10, 2}, {2, 2}, {3, 2}, {4, 2}, {4, 3},
+                                      {5, 2}, {5, 3}, {5, 4}, {2, 3}, {2, 4}, {2, 5}, {3, 4}, {3, 6}, {3, 8}};
+      const int nsh = (int)(sizeof(shapes) / sizeof(shapes[0]));
+      const int TM = (mX + 7) / 8, TN = (mY + 7) / 8;
+      wg = pick_warp_grid(TM, TN, 8 * (TM + TN), shapes, nsh);
+      // the smallest instantiated rectangle holding (RM, RN).  Measured on the
+      // C3 probe's two pencils (profiles/r02_gram_forms.txt): 7 x 8 tiles
+      // 2.49 ms (flat 2.45), 8 x 9 tiles 2.86 ms (flat 3.66) -- the grid is the
+      // default wherever it fits (the cost model picks its shape only)
+      int bq = -1;
+      for (int q = 0; q < nsh; ++q)
+        if (wg.RM <= shapes[q][0] && wg.RN <= shapes[q][1] &&
+            (bq < 0 || shapes[q][0] * shapes[q][1] < shapes[bq][0] * shapes[bq][1]))
+          bq = q;
+      switch (bq) {
+        case 0: kern2 = k_gram_mma2<T, 2, 1, GR, NST>; break;
+        case 1: kern2 = k_gram_mma2<T, 4, 1, GR, NST>; break;
+        case 2: kern2 = k_gram_mma2<T, 7, 1, GR, NST>; break;
+        case 3: kern2 = k_gram_mma2<T, 8, 1, GR, NST>; break;
+        case 4: kern2 = k_gram_mma2<T, 10, 2, GR, NST>; break;
+        case 5: kern2 = k_gram_mma2<T, 2, 2, GR, NST>; break;
+        case 6: kern2 = k_gram_mma2<T, 3, 2, GR, NST>; break;
+        case 7: kern2 = k_gram_mma2<T, 4, 2, GR, NST>; break;
+        case 8: kern2 = k_gram_mma2<T, 4, 3, GR, NST>; break;
+        case 9: kern2 = k_gram_mma2<T, 5, 2, GR, NST>; break;
+        case 10: kern2 = k_gram_mma2<T, 5, 3, GR, NST>; break;
+        case 11: kern2 = k_gram_mma2<T, 5, 4, GR, NST>; break;
+        case 12: kern2 = k_gram_mma2<T, 2, 3, GR, NST>; break;
+        case 13: kern2 = k_gram_mma2<T, 2, 4, GR, NST>; break;
+        case 14: kern2 = k_gram_mma2<T, 2, 5, GR, NST>; break;
+        case 15: kern2 = k_gram_mma2<T, 3, 4, GR, NST>; break;
+        case 16: kern2 = k_gram_mma2<T, 3, 6, GR, NST>; break;
+        case 17: kern2 = k_gram_mma2<T, 3, 8, GR, NST>; break;
+        default: break;
+      }
+    }
+  }
+  const void *kv = kern2 ? (const void *)kern2 : (const void *)kern;   // (attributes: prepare_block_kernels)
   if (smem > 200 * 1024) return false;
   int occ = 1;
-  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kv, 256, smem));
   const int64_t slots = (int64_t)std::max(1, occ) * sm_budget(ctx->nsm);
   int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4 * GR - 1) / (4 * GR), slots));
   const int64_t chunk = ((n + nchunks - 1) / nchunks + GR - 1) / GR * GR;
@@ -558,7 +734,8 @@ static bool gram_mma_run(const std::vector<ColDesc> &X, const std::vector<ColDes
   std::vector<ColDesc> both(X);
   both.insert(both.end(), Y.begin(), Y.end());
   RB_CUDA(cudaMemcpyAsync(dX, both.data(), desc_bytes, cudaMemcpyHostToDevice, strm));
-  kern<<<nchunks, 256, smem, strm>>>(dX, mX, dX + mX, mY, n, chunk, dpart);
+  if (kern2) kern2<<<nchunks, 256, smem, strm>>>(dX, mX, dX + mX, mY, n, chunk, dpart, wg.WC, wg.RM, wg.RN);
+  else kern<<<nchunks, 256, smem, strm>>>(dX, mX, dX + mX, mY, n, chunk, dpart);
   k_gram_reduce<T><<<(mX * mY * 32 + 255) / 256, 256, 0, strm>>>(dpart, nchunks, mX * mY, dG);
   count_launch(2);
   std::vector<T> h((size_t)mX * mY);
@@ -905,13 +1082,7 @@ static void gram_cc_mma_launch(const double *C, const double *Ct, int k, int64_t
                                int &nb_out, rbicg_ctx *ctx, cudaStream_t strm, double **buf_out) {
   constexpr int GCR = 128, NST = 3, NTL = KT * KT + 2 * KT;
   const size_t sm = std::max(sizeof(double) * NST * 2 * GCR * (size_t)k, sizeof(double) * 8 * NTL * 64);
-  static bool attr = false;
-  if (!attr) {
-    RB_CUDA(cudaFuncSetAttribute((const void *)k_gram_cc_mma<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024));
-    attr = true;
-  }
-  RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
+  RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);   // (attributes: prepare_block_kernels)
   int per = 1;
   RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gram_cc_mma<KT>, 256, sm));
   const int np = 2 * k + k * k;
@@ -1380,6 +1551,34 @@ void prepare_block_kernels() {
   RB_GATTR(zc, 4) RB_GATTR(zc, 8) RB_GATTR(zc, 12) RB_GATTR(zc, 16) RB_GATTR(zc, 24)
   RB_GATTR(zc, 32)
 #undef RB_GATTR
+  // every Gram / SpMM instantiation the cycle end can pick, loaded and given
+  // its shared-memory limit here: under lazy module loading a first launch in
+  // the middle of a sequence loads the kernel then (measured: C4 systems that
+  // met a new pencil shape took 37-110 ms instead of 11-21 ms)
+#define RB_G2(R, C) (const void *)k_gram_mma2<double, R, C, 32, 2>,
+  for (auto f : {RB_G2(2, 1) RB_G2(4, 1) RB_G2(7, 1) RB_G2(8, 1) RB_G2(10, 2) RB_G2(2, 2) RB_G2(3, 2)
+                     RB_G2(4, 2) RB_G2(4, 3) RB_G2(5, 2) RB_G2(5, 3) RB_G2(5, 4) RB_G2(2, 3) RB_G2(2, 4)
+                         RB_G2(2, 5) RB_G2(3, 4) RB_G2(3, 6) RB_G2(3, 8)(const void *)k_gram_mma<double, 2, 32, 2>,
+                 (const void *)k_gram_mma<double, 4, 32, 2>, (const void *)k_gram_mma<double, 6, 32, 2>,
+                 (const void *)k_gram_mma<double, 7, 32, 2>, (const void *)k_gram_mma<double, 8, 32, 2>,
+                 (const void *)k_gram_mma<double, 9, 32, 2>, (const void *)k_gram_mma<double, 10, 32, 2>,
+                 (const void *)k_gram_mma<double, 12, 32, 2>, (const void *)k_gram_mma<double, 14, 32, 2>,
+                 (const void *)k_gram_mma<double, 16, 32, 2>, (const void *)k_gram_mma<double, 20, 32, 2>,
+                 (const void *)k_gram_mma<zc, 2, 32, 2>, (const void *)k_gram_mma<zc, 4, 32, 2>,
+                 (const void *)k_gram_mma<zc, 6, 32, 2>, (const void *)k_gram_mma<zc, 8, 32, 2>,
+                 (const void *)k_gram_cc_mma<1>, (const void *)k_gram_cc_mma<2>, (const void *)k_gram_cc_mma<3>,
+                 (const void *)k_gram_cc_mma<4>, (const void *)k_gram2<double, 8, 8>,
+                 (const void *)k_gram2<double, 4, 8>, (const void *)k_gram2<double, 4, 4>,
+                 (const void *)k_gram2<zc, 4, 4>})
+    RB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+#undef RB_G2
+#define RB_SP(T, KB)                                                                                   (const void *)k_spmm_rows<T, KB>, (const void *)k_spmm_rows<T, KB, 2>, (const void *)k_spmm_rows<T, KB, 3>,       (const void *)k_spmm_rows<T, KB, 4>, (const void *)k_spmm_rows0<T, KB>,
+  for (auto f : {RB_SP(double, 4) RB_SP(double, 8) RB_SP(double, 12) RB_SP(double, 16) RB_SP(double, 24)
+                     RB_SP(double, 32)(const void *)k_spmm_wide<double>, (const void *)k_spmm_wide<zc>}) {
+    cudaFuncAttributes fa;
+    RB_CUDA(cudaFuncGetAttributes(&fa, f));
+  }
+#undef RB_SP
   for (auto f : {(const void *)k_gemm_multi<double, 12>, (const void *)k_gemm_multi<double, 24>,
                  (const void *)k_gemm_multi<double, 32>, (const void *)k_gemm_multi<zc, 12>,
                  (const void *)k_gemm_multi<zc, 24>, (const void *)k_gemm_multi<zc, 32>,

@@ -43,6 +43,7 @@ SWITCHES = [
     ("RBICG_GRAM2", "44"), ("RBICG_GRAM2", "88"), ("RBICG_SPMM_V", "0"), ("RBICG_GEMM_RM", "0"),
     ("RBICG_GCR_ROWS", "64"), ("RBICG_TMP_U_EAGER", "1"), ("RBICG_C_CHECK", "1"),
     ("RBICG_TRACE", "1"), ("RBICG_TIMING", "1"), ("RBICG_TRSV_BLOCKS", "8"),
+    ("RBICG_GRAM_FLAT", "1"), ("RBICG_GRAM_CC_FFMA", "1"), ("RBICG_SPMM_MINB", "1"),
 ]
 
 
