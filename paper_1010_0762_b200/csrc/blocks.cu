@@ -1200,10 +1200,16 @@ __global__ void __launch_bounds__(256) k_gemm_panels(const ColDesc *__restrict__
 template <typename T, int PB>
 __global__ void __launch_bounds__(256) k_gemm_rm(const T *__restrict__ X, int m, const T *__restrict__ M,
                                                  int p, int64_t n, T *__restrict__ out) {
+  // complex: the tile is staged TRANSPOSED ([a][row], row stride 257): the
+  // row-major form put a thread's 16-byte elements 16 m bytes apart, an 8-way
+  // bank conflict for m = 8 on every read (ncu: C4 8 -> 8 GEMM 96 us, 0.41 of
+  // the HBM peak); the output tile likewise ([c][row])
+  constexpr bool TR = sizeof(T) == 16;
+  constexpr int LD = TR ? 257 : 256;
   extern __shared__ __align__(16) unsigned char sm_raw[];
   T *sM = reinterpret_cast<T *>(sm_raw);     // [m][PB]
-  T *sX = sM + (size_t)m * PB;               // 2 x [256 m]
-  T *sO = sX + (size_t)2 * 256 * m;          // [256 p]
+  T *sX = sM + (size_t)m * PB;               // 2 x [256 m] (complex: 2 x [m][257])
+  T *sO = sX + (size_t)2 * LD * m;           // [256 p] (complex: [p][257])
   const int tid = threadIdx.x;
   for (int e = tid; e < m * PB; e += 256) {
     const int a = e / PB, c = e % PB;
@@ -1214,10 +1220,12 @@ __global__ void __launch_bounds__(256) k_gemm_rm(const T *__restrict__ X, int m,
   auto load = [&](int64_t tile, int buf) {
     const int64_t base = tile * 256 * m;
     const int ne = (int)min((int64_t)256, n - tile * 256) * m;
-    T *dst = sX + (size_t)buf * 256 * m;
+    T *dst = sX + (size_t)buf * LD * m;
     for (int e = tid * PER; e < ne; e += 256 * PER) {
       const int valid = max(0, min(PER, ne - e)) * (int)sizeof(T);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst + e)),
+      T *d = dst + e;
+      if constexpr (TR) d = dst + (e % m) * LD + e / m;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(d)),
                    "l"(X + base + e), "r"(valid)
                    : "memory");
     }
@@ -1232,23 +1240,25 @@ __global__ void __launch_bounds__(256) k_gemm_rm(const T *__restrict__ X, int m,
     __syncthreads();
     const int rows = (int)min((int64_t)256, n - tile * 256);
     if (tid < rows) {
-      const T *xr = sX + (size_t)buf * 256 * m + (size_t)tid * m;
+      const T *xr = sX + (size_t)buf * LD * m + (TR ? (size_t)tid : (size_t)tid * m);
       T acc[PB];
 #pragma unroll
       for (int c = 0; c < PB; ++c) acc[c] = zero<T>();
       for (int a = 0; a < m; ++a) {
-        const T xv = xr[a];
+        const T xv = xr[TR ? a * LD : a];
 #pragma unroll
         for (int c = 0; c < PB; ++c) acc[c] = mad(xv, sM[a * PB + c], acc[c]);
       }
 #pragma unroll
       for (int c = 0; c < PB; ++c)
-        if (c < p) sO[tid * p + c] = acc[c];
+        if (c < p) sO[TR ? c * LD + tid : tid * p + c] = acc[c];
     }
     __syncthreads();
     const int64_t ob = tile * 256 * p;
     const int ne = rows * p;
-    if ((ob % PER) == 0) {
+    if constexpr (TR) {
+      for (int e = tid; e < ne; e += 256) out[ob + e] = sO[(e % p) * LD + e / p];
+    } else if ((ob % PER) == 0) {
       const int nv = ne / PER;
       for (int e = tid; e < nv; e += 256)
         reinterpret_cast<double2 *>(out + ob)[e] = reinterpret_cast<const double2 *>(sO)[e];
@@ -1263,7 +1273,8 @@ __global__ void __launch_bounds__(256) k_gemm_rm(const T *__restrict__ X, int m,
 template <typename T, int PB>
 static void gemm_rm_launch(const T *X, int m, const T *dM, int p, int64_t n, T *out, rbicg_ctx *ctx,
                            cudaStream_t strm) {
-  const size_t sm = sizeof(T) * ((size_t)m * PB + (size_t)2 * 256 * m + (size_t)256 * p);
+  const size_t LD = sizeof(T) == 16 ? 257 : 256;   // (complex: transposed tiles, k_gemm_rm)
+  const size_t sm = sizeof(T) * ((size_t)m * PB + 2 * LD * m + LD * p);
   RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
   int per = 1;
   RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gemm_rm<T, PB>, 256, sm));
