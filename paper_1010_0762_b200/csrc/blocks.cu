@@ -831,10 +831,6 @@ void gram(const std::vector<ColDesc> &X, const std::vector<ColDesc> &Y, int64_t 
     // fp64 tensor cores (RBICG_GRAM2=88 / 48 / 44: the FFMA micro-tile forms)
     // (16-row stages, 3-4 stages, TMA bulk staging per column segment and a
     // 2 x 4 warp grid measured slower: 3.4-5.4 ms)
-    // stage shape (rows per stage, ring depth): RBICG_GRAM_STAGE=1 (16, 4), 2 (64, 2)
-    static const int stg = getenv("RBICG_GRAM_STAGE") ? atoi(getenv("RBICG_GRAM_STAGE")) : 0;
-    if (var == 0 && stg == 1 && gram_mma_run<T, 16, 4>(X, Y, n, G, ctx, strm)) return;
-    if (var == 0 && stg == 2 && gram_mma_run<T, 64, 2>(X, Y, n, G, ctx, strm)) return;
     if (var == 0 && gram_mma_run<T, 32, 2>(X, Y, n, G, ctx, strm)) return;
     if (var == 48) return gram2_run<T, 4, 8>(X, Y, n, G, ctx, strm);
     if (var == 44) return gram2_run<T, 4, 4>(X, Y, n, G, ctx, strm);

@@ -1,11 +1,10 @@
 # pencil-Gram forms on one C3 general-case cycle-end probe: the default (2-D
 # warp grid, k_gram_mma2) and the flat tile ranges (RBICG_GRAM_FLAT=1,
-# k_gram_mma) and the stage shapes (RBICG_GRAM_STAGE=1: 16 rows x 4, =2: 64 x 2);
-# ncu launch lists.  bash scripts/gram_forms.sh TAG
+# k_gram_mma); ncu launch lists.  bash scripts/gram_forms.sh TAG
 TAG=${1:-gf}
 mkdir -p gpurun_out
-for v in default RBICG_GRAM_FLAT RBICG_GRAM_STAGE1 RBICG_GRAM_STAGE2; do
-  case $v in default) e="";; RBICG_GRAM_STAGE1) e="RBICG_GRAM_STAGE=1";; RBICG_GRAM_STAGE2) e="RBICG_GRAM_STAGE=2";; *) e="$v=1";; esac
+for v in default RBICG_GRAM_FLAT; do
+  case $v in default) e="";; *) e="$v=1";; esac
   env $e RBICG_SYNC_CYCLE=1 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none --kernel-name regex:"k_gram|k_spmm" --csv \
     --log-file gpurun_out/${TAG}_$v.csv python scripts/cycle_end_probe.py C3 > gpurun_out/${TAG}_$v.log 2>&1
