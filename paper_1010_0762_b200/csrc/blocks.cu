@@ -1126,7 +1126,11 @@ void gram_cc(const T *C, const T *Ct, int k, int64_t n, std::vector<cplx> &out, 
       return;
     }
   }
-  const int GCR = gcr_rows(k);
+  // rows per stage: halved until two stages of both blocks fit (complex k > 19
+  // overflowed the 160 KB stage budget at 128 rows: EINVAL, caught by
+  // test_projection_parity_widths)
+  int GCR = gcr_rows(k);
+  while (GCR > 16 && sizeof(T) * 2 * 2 * GCR * (size_t)k > 160 * 1024) GCR /= 2;
   const size_t sm = std::max(sizeof(T) * 2 * 2 * GCR * (size_t)k,
                              sizeof(T) * 16 * (size_t)W * std::max(1, 256 / W));
   RB_CHECK(sm <= 160 * 1024, RBICG_EINVAL);
@@ -1333,6 +1337,11 @@ void gemm_panels(const std::vector<ColDesc> &X, const std::vector<cplx> &M, int 
   for (int a = 1; rm && a < mX; ++a)
     rm = X[a].stride == mX && (const char *)X[a].p == (const char *)X[0].p + (size_t)a * sizeof(T);
   static const bool rm_off = getenv("RBICG_GEMM_RM") && atoi(getenv("RBICG_GEMM_RM")) == 0;
+  {   // the staged form only when its tiles fit (complex k > 16: the panel kernel)
+    const int PB = p <= 4 ? 4 : p <= 8 ? 8 : p <= 12 ? 12 : p <= 16 ? 16 : p <= 24 ? 24 : 32;
+    const size_t LD = sizeof(T) == 16 ? 257 : 256;
+    if (sizeof(T) * ((size_t)mX * PB + 2 * LD * mX + LD * p) > 200 * 1024) rm = false;
+  }
   if (rm && !rm_off) {
     const T *X0 = reinterpret_cast<const T *>(X[0].p);
     if (p <= 4) gemm_rm_launch<T, 4>(X0, mX, dM, p, n, out, ctx, strm);

@@ -104,6 +104,35 @@ def test_projection_parity(ctx, cplx):
     np.testing.assert_allclose(G, np.diag(out["d"]), atol=1e-10 * out["d"].max())
 
 
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("n,k", [(1000, 1), (1000, 3), (4099, 8), (4099, 9), (1000, 16), (4099, 17),
+                                 (1000, 25), (4099, 32)])
+def test_projection_parity_widths(ctx, cplx, n, k):
+    """The refresh's bi-orthogonalisation Gram (norms of C, C~ and C~^*C) at every
+    tile width of the fp64 tensor-core form (k_gram_cc_mma, 8-column tiles: KT = 1..4,
+    k odd and even) and row counts that end in a partial 128-row stage; complex data
+    runs the FFMA form.  Against the oracle's biorthogonalize:
+    the singular values D_c to 1e-12 and the gauge-invariant projection C D^{-1} C~^*z."""
+    from oracle import rbicg as R
+    t = random_sparse(n, 6.0 / n, seed=100 + k, complex_=cplx)
+    A = _csr(t)
+    AH = A.conj().T.tocsr()
+    U = vec(n * k, 200 + k, cplx).reshape(n, k)
+    Ut = vec(n * k, 300 + k, cplx).reshape(n, k)
+    B = R.biorthogonalize(A, AH, U, Ut, 1e-6)
+    M = ctx.matrix(*t)
+    rec = ctx.recycle(n, k, cplx)
+    rec.import_(U, Ut)
+    z, zt = vec(n, 14, cplx), vec(n, 15, cplx)
+    out = ctx.project(M, rec, z, zt, 1e-6)
+    assert out["k"] == B.k
+    np.testing.assert_allclose(out["d"], B.d, rtol=1e-12)
+    ref = B.C @ ((B.Ct / B.d).conj().T @ z)
+    got = out["C"] @ out["zeta"]
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(z) * \
+        np.linalg.norm(B.C) / B.d.min()
+
+
 # ------------------------------------------------------------------ solves
 def _solve_both(ctx, A, Ad, b, bt, U=None, Ut=None, **kw):
     from oracle import rbicg as R
