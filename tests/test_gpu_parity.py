@@ -335,6 +335,18 @@ def test_c4_small_complex_sequence(ctx, pencil):
                        cfg.max_itn, lam_slots=True, check_space=0.9999, pencil=pencil)
 
 
+def test_c4_small_complex_sequence_wide_k(ctx):
+    """A complex sequence with a wide recycle space (k = 24 > 16: the complex
+    pencil's X side exceeds 64 columns -> the FFMA Gram, the U F GEMM falls back
+    to the panel kernel, the C~^*C Gram runs 64-row stages) against the oracle
+    under the Q27 protocol."""
+    cfg = CONFIGS["C4"].scaled(10, systems=4, s=24, k=24)
+    items = list(system_sequence(cfg, lam_r=0.0))
+    _carry_from_oracle(ctx, cfg.k, cfg.s, cfg.tol, cfg.trunc_tol, items,
+                       lambda it: _csr((it["indptr"], it["indices"], it["data"])),
+                       cfg.max_itn, lam_slots=True, check_space=0.99)
+
+
 @pytest.mark.parametrize("cplx", [False, True])
 def test_fast_pencil_output_space(ctx, cplx):
     """§4.4 assembly (rbicg_opts.pencil = 1): the
