@@ -1078,8 +1078,8 @@ __global__ void __launch_bounds__(256) k_gram_cc_mma(const double *__restrict__ 
 }
 
 template <int KT>
-static void gram_cc_mma_launch(const double *C, const double *Ct, int k, int64_t n, double *dpart_out,
-                               int &nb_out, rbicg_ctx *ctx, cudaStream_t strm, double **buf_out) {
+static void gram_cc_mma_launch(const double *C, const double *Ct, int k, int64_t n, int &nb_out,
+                               rbicg_ctx *ctx, cudaStream_t strm, double **buf_out) {
   constexpr int GCR = 128, NST = 3, NTL = KT * KT + 2 * KT;
   const size_t sm = std::max(sizeof(double) * NST * 2 * GCR * (size_t)k, sizeof(double) * 8 * NTL * 64);
   RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);   // (attributes: prepare_block_kernels)
@@ -1092,7 +1092,6 @@ static void gram_cc_mma_launch(const double *C, const double *Ct, int k, int64_t
   const int nb = (int)((n + chunk - 1) / chunk);
   double *buf = (double *)ws_alloc(sizeof(double) * ((size_t)nb * np + np) + 64);
   k_gram_cc_mma<KT><<<nb, 256, sm, strm>>>(C, Ct, k, n, chunk, buf);
-  (void)dpart_out;
   nb_out = nb;
   *buf_out = buf;
 }
@@ -1111,10 +1110,10 @@ void gram_cc(const T *C, const T *Ct, int k, int64_t n, std::vector<cplx> &out, 
     if (!ffma && ((uintptr_t)C % 16) == 0 && ((uintptr_t)Ct % 16) == 0) {
       int nb = 0;
       double *buf = nullptr;
-      if (k <= 8) gram_cc_mma_launch<1>(C, Ct, k, n, nullptr, nb, ctx, strm, &buf);
-      else if (k <= 16) gram_cc_mma_launch<2>(C, Ct, k, n, nullptr, nb, ctx, strm, &buf);
-      else if (k <= 24) gram_cc_mma_launch<3>(C, Ct, k, n, nullptr, nb, ctx, strm, &buf);
-      else gram_cc_mma_launch<4>(C, Ct, k, n, nullptr, nb, ctx, strm, &buf);
+      if (k <= 8) gram_cc_mma_launch<1>(C, Ct, k, n, nb, ctx, strm, &buf);
+      else if (k <= 16) gram_cc_mma_launch<2>(C, Ct, k, n, nb, ctx, strm, &buf);
+      else if (k <= 24) gram_cc_mma_launch<3>(C, Ct, k, n, nb, ctx, strm, &buf);
+      else gram_cc_mma_launch<4>(C, Ct, k, n, nb, ctx, strm, &buf);
       double *dG = buf + (size_t)nb * np;
       k_gram_reduce<double><<<(np * 32 + 255) / 256, 256, 0, strm>>>(buf, nb, np, dG);
       count_launch(2);
