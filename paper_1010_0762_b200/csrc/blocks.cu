@@ -207,6 +207,7 @@ static void spmm_rows_launch(const DevMat &A, const T *X, T *Y, int k, cudaStrea
   const int64_t blocks = (A.n + 255) / 256;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)std::max(1, per) * nsm));
   fn<<<grid, 256, 0, s>>>(A, X, Y, k);
+  RB_CUDA(cudaGetLastError());   // a launch that could not start (config) fails here
 }
 
 template <typename T> void launch_spmm(const DevMat &A, const T *X, T *Y, int k, cudaStream_t s) {
@@ -232,9 +233,11 @@ template <typename T> void launch_spmm(const DevMat &A, const T *X, T *Y, int k,
   const size_t sm = (size_t)32 * std::max(1, A.max_w) * (sizeof(T) + 4);
   if (sm <= 48 * 1024) {
     k_spmm<T><<<(int)A.nslices, 32 * k, sm, s>>>(A, X, Y, k);
+    RB_CUDA(cudaGetLastError());   // a launch that could not start (config) fails here
   } else {
     const int grid = (int)std::min<int64_t>((A.n * k + 255) / 256, 148 * 16);
     k_spmm_wide<T><<<grid, 256, 0, s>>>(A, X, Y, k);
+    RB_CUDA(cudaGetLastError());   // a launch that could not start (config) fails here
   }
   count_launch();
 }
@@ -737,6 +740,7 @@ static bool gram_mma_run(const std::vector<ColDesc> &X, const std::vector<ColDes
   if (kern2) kern2<<<nchunks, 256, smem, strm>>>(dX, mX, dX + mX, mY, n, chunk, dpart, wg.WC, wg.RM, wg.RN);
   else kern<<<nchunks, 256, smem, strm>>>(dX, mX, dX + mX, mY, n, chunk, dpart);
   k_gram_reduce<T><<<(mX * mY * 32 + 255) / 256, 256, 0, strm>>>(dpart, nchunks, mX * mY, dG);
+  RB_CUDA(cudaGetLastError());   // a launch that could not start (config) fails here
   count_launch(2);
   std::vector<T> h((size_t)mX * mY);
   RB_CUDA(cudaMemcpyAsync(h.data(), dG, g_bytes, cudaMemcpyDeviceToHost, strm));
@@ -791,6 +795,7 @@ static void gram2_run(const std::vector<ColDesc> &X, const std::vector<ColDesc> 
   dim3 grid(tiles, nchunks);
   k_gram2<T, MX, MY><<<grid, 256, smem, strm>>>(dX, mX, dX + mX, mY, tX, tY, n, chunk, dpart);
   k_gram_reduce<T><<<(mX * mY * 32 + 255) / 256, 256, 0, strm>>>(dpart, ng * nchunks, mX * mY, dG);
+  RB_CUDA(cudaGetLastError());   // a launch that could not start (config) fails here
   count_launch(2);
   std::vector<T> h((size_t)mX * mY);
   RB_CUDA(cudaMemcpyAsync(h.data(), dG, g_bytes, cudaMemcpyDeviceToHost, strm));
@@ -1092,6 +1097,7 @@ static void gram_cc_mma_launch(const double *C, const double *Ct, int k, int64_t
   const int nb = (int)((n + chunk - 1) / chunk);
   double *buf = (double *)ws_alloc(sizeof(double) * ((size_t)nb * np + np) + 64);
   k_gram_cc_mma<KT><<<nb, 256, sm, strm>>>(C, Ct, k, n, chunk, buf);
+  RB_CUDA(cudaGetLastError());   // a launch that could not start (config) fails here
   nb_out = nb;
   *buf_out = buf;
 }
@@ -1116,6 +1122,7 @@ void gram_cc(const T *C, const T *Ct, int k, int64_t n, std::vector<cplx> &out, 
       else gram_cc_mma_launch<4>(C, Ct, k, n, nb, ctx, strm, &buf);
       double *dG = buf + (size_t)nb * np;
       k_gram_reduce<double><<<(np * 32 + 255) / 256, 256, 0, strm>>>(buf, nb, np, dG);
+      RB_CUDA(cudaGetLastError());   // a launch that could not start (config) fails here
       count_launch(2);
       std::vector<double> h(np);
       RB_CUDA(cudaMemcpyAsync(h.data(), dG, sizeof(double) * np, cudaMemcpyDeviceToHost, strm));
@@ -1146,6 +1153,7 @@ void gram_cc(const T *C, const T *Ct, int k, int64_t n, std::vector<cplx> &out, 
   T *dG = dpart + (size_t)nb * np;
   k_gram_cc<T><<<nb, 256, sm, strm>>>(C, Ct, k, n, chunk, GCR, dpart);
   k_gram_reduce<T><<<(np * 32 + 255) / 256, 256, 0, strm>>>(dpart, nb, np, dG);
+  RB_CUDA(cudaGetLastError());   // a launch that could not start (config) fails here
   count_launch(2);
   std::vector<T> h(np);
   RB_CUDA(cudaMemcpyAsync(h.data(), dG, sizeof(T) * np, cudaMemcpyDeviceToHost, strm));
@@ -1284,6 +1292,7 @@ static void gemm_rm_launch(const T *X, int m, const T *dM, int p, int64_t n, T *
   const int grid = (int)std::max<int64_t>(
       1, std::min<int64_t>((n + 255) / 256, (int64_t)std::max(1, per) * sm_budget(ctx->nsm)));
   k_gemm_rm<T, PB><<<grid, 256, sm, strm>>>(X, m, dM, p, n, out);
+  RB_CUDA(cudaGetLastError());   // a launch that could not start (config) fails here
   count_launch();
 }
 
@@ -1294,6 +1303,7 @@ static void gemm_launch(const ColDesc *dX, int mX, const T *dM, int p, int64_t n
   RB_CHECK(sm <= 200 * 1024, RBICG_EINVAL);
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_budget(ctx->nsm) * 8);
   k_gemm_panels<T, PB><<<grid, 256, sm, strm>>>(dX, mX, dM, p, n, out, out_last);
+  RB_CUDA(cudaGetLastError());   // a launch that could not start (config) fails here
   count_launch();
 }
 
@@ -1533,6 +1543,7 @@ void gemm_multi(const std::vector<ColDesc> &X, const std::vector<cplx> &M,
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((n + rows_per_block - 1) / rows_per_block, (int64_t)std::max(1, per) * sm_budget(ctx->nsm)));
     kern<<<grid, 256, sm, strm>>>(dX, mX, dM, p, n, O);
+    RB_CUDA(cudaGetLastError());   // a launch that could not start (config) fails here
   };
   static const int rx = getenv("RBICG_GEMM_RPT") ? atoi(getenv("RBICG_GEMM_RPT")) : 0;
   const int r2 = sizeof(T) == 8 ? 2 : 1;
