@@ -155,8 +155,8 @@ struct rbicg_ctx {
   // while the interior tiles of the iteration's SpMV kernel run
   cudaStream_t halo_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  uint64_t async_key = 0;        // (n, k, s, dtype) of the last doubled-ring decision
-  bool async_ok = false;
+  uint64_t async_key = 0;        // (n, k, s, dtype) of the last device-memory query
+  size_t async_avail = 0;        // free + this ctx's idle arena bytes at that query
 };
 
 struct rbicg_mat {
