@@ -5,8 +5,11 @@ Workload (N=1, default): BASELINE.json configs[2] = C3, the 3-D conv-diff
 sequence on a 192^3 grid (n = 7,077,888, nnz = 49.3 M, fp64, k = 10, s = 40,
 tol 1e-8, 8 dual pairs; synthetic, seeded per SURVEY.md §8(d)) -- a config of
 the metric's 1/2/4/8-GPU set.  Under the recycle rule (Q13 at the
-paper's 1e-6, Q32) every system after the first starts with a recycle space,
-so the timed systems run the augmented iteration with its projections.
+paper's 1e-6, Q32) a system starts with the recycle space the previous one
+left after truncation: `config.k_in_per_system` records its width (C3 chain:
+4, 0, 5, 0, 0 on the timed systems), systems with k_in > 0 run the augmented
+iteration with its projections, the others plain BiCG steps plus the
+cycle-end recycle updates (DESIGN §3 table).
 --config C2|C4|C5 selects another config.
 
 A *step* is one dual-pair solve of the sequence through the C ABI
